@@ -1,0 +1,153 @@
+/* heterodyn — differentiable projective-dynamics solver, C interface.
+ *
+ * Drop-in boundary of the B200 build.  The first half of this header is the
+ * reference ABI, symbol for symbol (reference: /root/reference/proj/include/
+ * heterodyn/heterodyn.h:30-141, implemented by src/capi.cpp:94-322); the
+ * second half ("B200 extensions") adds the backward/trajectory surface the
+ * reference reaches only through its drivers (drivers.cpp:31-99,
+ * backward.hpp:94-97), which the reference ABI does not expose.
+ *
+ * Semantics kept from the reference: every fallible call returns an
+ * hd_status (0 on success) or NULL; the message for the most recent failure
+ * on the calling thread is available via hd_last_error() (never NULL);
+ * strings returned through char** are malloc'd and released with
+ * hd_string_free(); hd_scene is immutable and shareable; hd_sim is
+ * single-threaded and borrows its scene; exceptions never cross the boundary.
+ *
+ * Two libraries export this header: the product
+ * (paper_2605_14526_b200/_lib/libheterodyn_b200.so, device-resident solver on
+ * sm_100a) and the CPU oracle used by the tests
+ * (oracle/_build/libheterodyn_oracle.so).
+ */
+#ifndef HETERODYN_H
+#define HETERODYN_H
+
+#include <stddef.h>
+
+#if defined(_WIN32)
+#if defined(HETERODYN_BUILD)
+#define HD_API __declspec(dllexport)
+#else
+#define HD_API __declspec(dllimport)
+#endif
+#else
+#define HD_API __attribute__((visibility("default")))
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* reference heterodyn.h:30-45 */
+typedef enum hd_status {
+  HD_OK = 0,
+  HD_ERR_PARSE = 1,
+  HD_ERR_VALIDATION = 2,
+  HD_ERR_DEGENERATE_ELEMENT = 3,
+  HD_ERR_INVALID_POISSON = 4,
+  HD_ERR_NON_POSITIVE_JACOBIAN = 5,
+  HD_ERR_PROX_DIVERGED = 6,
+  HD_ERR_SINGULAR_FILTERED_HESSIAN = 7,
+  HD_ERR_NOT_POSITIVE_DEFINITE = 8,
+  HD_ERR_SINGULAR_CONTACT_SYSTEM = 9,
+  HD_ERR_ADJOINT_DIVERGED = 10,
+  HD_ERR_LINE_SEARCH_FAILED = 11,
+  HD_ERR_IO = 12,
+  HD_ERR_INVALID_ARGUMENT = 13
+} hd_status;
+
+/* reference heterodyn.h:47-54 */
+HD_API const char* hd_last_error(void);
+HD_API int hd_last_error_code(void);
+HD_API void hd_string_free(char* s);
+
+/* ---- scenes (reference heterodyn.h:56-76) ------------------------------ */
+typedef struct hd_scene hd_scene;
+HD_API hd_scene* hd_scene_load(const char* path);
+HD_API hd_scene* hd_scene_parse(const char* json_text);
+HD_API hd_scene* hd_scene_builtin(const char* name);
+HD_API void hd_scene_free(hd_scene* scene);
+HD_API int hd_scene_vertex_count(const hd_scene* scene);
+HD_API int hd_scene_element_count(const hd_scene* scene);
+HD_API int hd_scene_frame_count(const hd_scene* scene);
+HD_API const char* hd_scene_name(const hd_scene* scene);
+
+/* ---- frame-by-frame simulation (reference heterodyn.h:78-107) ---------- */
+typedef struct hd_sim hd_sim;
+HD_API hd_sim* hd_sim_create(const hd_scene* scene);
+HD_API void hd_sim_free(hd_sim* sim);
+HD_API hd_status hd_sim_step(hd_sim* sim);
+HD_API double hd_sim_time(const hd_sim* sim);
+HD_API int hd_sim_dof_count(const hd_sim* sim);
+HD_API hd_status hd_sim_positions(const hd_sim* sim, double* out, size_t capacity);
+HD_API hd_status hd_sim_velocities(const hd_sim* sim, double* out, size_t capacity);
+HD_API int hd_sim_last_iterations(const hd_sim* sim);
+HD_API int hd_sim_last_converged(const hd_sim* sim);
+HD_API int hd_sim_last_contact_count(const hd_sim* sim);
+
+/* ---- drivers (reference heterodyn.h:109-141) --------------------------- */
+HD_API hd_status hd_run_simulate(const hd_scene* scene, const char* out_dir, char** summary_json);
+HD_API hd_status hd_run_gradcheck(const hd_scene* scene, const char* vars_csv, const char* out_path,
+                                  char** report_json, int* pass);
+HD_API hd_status hd_run_identify(const char* problem_json, const char* out_dir, char** result_json,
+                                 int* stalled);
+HD_API hd_status hd_run_identify_file(const char* problem_path, const char* out_dir, char** result_json,
+                                      int* stalled);
+HD_API hd_status hd_factor_stats(const hd_scene* scene, char** stats_json);
+
+/* ---- B200 extensions (new; no reference counterpart in the ABI) ---------- */
+
+/* Records every subsequent frame's adjoint cache (the reference's
+ * roll(keep_caches=true), drivers.cpp:31-54).  enable=0 stops recording and
+ * discards recorded frames. */
+HD_API hd_status hd_sim_record(hd_sim* sim, int enable);
+HD_API int hd_sim_recorded_frames(const hd_sim* sim);
+
+/* Replaces the state (3 doubles per vertex each, xyz interleaved) and time;
+ * discards recorded frames.  q or v may be NULL to keep that part. */
+HD_API hd_status hd_sim_set_state(hd_sim* sim, const double* q, const double* v, double time);
+
+/* Reverse-time adjoint chain over the recorded frames (chain_backward,
+ * drivers.cpp:66-99, with backward_step backward.cpp:396-414 per frame).
+ * dl_dq_direct: (frames + 1) x dof doubles — the loss's direct partial with
+ * respect to the state after frame t (row 0 = initial state) — or NULL, in
+ * which case dl_dq_final (dof doubles, may be NULL = zero) seeds the final
+ * frame only.  dl_dv_final (dof, may be NULL = zero) seeds the final velocity.
+ * Outputs may be NULL: dl_dq0, dl_dv0, dl_df_ext (dof each), dl_de
+ * (element_count), dl_dw (element_count, or 2 x element_count for corotated;
+ * dl_dw_capacity is checked). */
+HD_API hd_status hd_sim_backward(hd_sim* sim, const double* dl_dq_direct, const double* dl_dq_final,
+                                 const double* dl_dv_final, double* dl_dq0, double* dl_dv0,
+                                 double* dl_df_ext, double* dl_de, double* dl_dw,
+                                 size_t dl_dw_capacity);
+/* Diagnostics of the most recent hd_sim_backward: per recorded frame tau and
+ * trust-region ratio rho (forward frame order), and total adjoint sweeps. */
+HD_API hd_status hd_sim_backward_tau(const hd_sim* sim, double* tau, double* rho, size_t capacity);
+HD_API int hd_sim_backward_iterations(const hd_sim* sim);
+
+/* One application of the global solve on the current factor:
+ * out = solve_free(rhs_full, fixed_q) (factor.cpp:196-208).  fixed_q may be
+ * NULL (zero prescribed positions).  All arrays are dof doubles. */
+HD_API hd_status hd_sim_solve_free(hd_sim* sim, const double* rhs_full, const double* fixed_q,
+                                   double* out);
+
+/* Replaces the per-element Young's moduli (MaterialField::set_young,
+ * material.cpp:75-80); the next step refactorizes.  The prox means are frozen
+ * at their current values when freeze_means is nonzero (freeze_means,
+ * material.cpp:82-86, the gradcheck/identify convention). */
+HD_API hd_status hd_sim_set_young(hd_sim* sim, const double* young, size_t count, int freeze_means);
+
+/* Counters for roofline accounting (factor.hpp:39,119-121; forward.hpp:100;
+ * backward.hpp:26): factor nnz, free vertex count, cumulative 3-axis solves,
+ * cumulative A-SpMVs, refactorizations. */
+HD_API long long hd_sim_factor_nnz(const hd_sim* sim);
+HD_API int hd_sim_free_count(const hd_sim* sim);
+HD_API long long hd_sim_solve_count(const hd_sim* sim);
+HD_API long long hd_sim_a_spmv_count(const hd_sim* sim);
+HD_API long long hd_sim_refactor_count(const hd_sim* sim);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HETERODYN_H */

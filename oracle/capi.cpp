@@ -1,0 +1,317 @@
+// ORACLE — test infrastructure only.  The hd_* C ABI of include/heterodyn.h
+// over the CPU restatement (reference capi.cpp:94-322 for the reference half;
+// the B200-extension half routes to roll/chain_backward, drivers.cpp:31-99).
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+
+#include <nlohmann/json.hpp>
+
+#include "../include/heterodyn.h"
+#include "oracle.hpp"
+
+using namespace hdo;
+
+struct hd_scene {
+  SceneSpec spec;
+};
+
+struct hd_sim {
+  const hd_scene* scene = nullptr;
+  MaterialField material;  // per-sim copy so set_young does not touch the scene
+  GlobalSystem system;
+  StateForce hook_storage;
+  const StateForce* hook = nullptr;
+  VecX f_ext;
+  SimState state;
+  int last_iterations = 0;
+  bool last_converged = false;
+  int last_contact_count = 0;
+  bool record = false;
+  std::vector<ForwardCache> caches;
+  std::vector<double> tau, rho;
+  int backward_iterations = 0;
+  long long solve_count_base = 0;
+};
+
+namespace {
+thread_local int g_code = 0;
+thread_local std::string g_msg;
+void set_error(int code, const std::string& m) {
+  g_code = code;
+  g_msg = m;
+}
+template <typename Fn>
+hd_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return HD_OK;
+  } catch (const Error& e) {
+    set_error(static_cast<int>(e.code()), e.what());
+    return static_cast<hd_status>(e.code());
+  } catch (const std::exception& e) {
+    set_error(HD_ERR_INVALID_ARGUMENT, std::string("unexpected error: ") + e.what());
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+}
+char* copy_string(const std::string& s) {
+  char* out = static_cast<char*>(std::malloc(s.size() + 1));
+  if (out) std::memcpy(out, s.c_str(), s.size() + 1);
+  return out;
+}
+hd_status copy_vector(const VecX& v, double* out, size_t cap, const char* who) {
+  if (out == nullptr || cap < v.size()) {
+    set_error(HD_ERR_INVALID_ARGUMENT, std::string(who) + ": output buffer too small");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  std::memcpy(out, v.data(), sizeof(double) * v.size());
+  return HD_OK;
+}
+hd_status null_arg(const char* who) {
+  set_error(HD_ERR_INVALID_ARGUMENT, std::string(who) + ": NULL argument");
+  return HD_ERR_INVALID_ARGUMENT;
+}
+}  // namespace
+
+extern "C" {
+
+const char* hd_last_error(void) { return g_msg.c_str(); }
+int hd_last_error_code(void) { return g_code; }
+void hd_string_free(char* s) { std::free(s); }
+
+hd_scene* hd_scene_load(const char* path) {
+  if (!path) { null_arg("hd_scene_load"); return nullptr; }
+  hd_scene* s = new hd_scene;
+  if (guarded([&] { s->spec = load_scene_file(path); }) != HD_OK) { delete s; return nullptr; }
+  return s;
+}
+hd_scene* hd_scene_parse(const char* text) {
+  if (!text) { null_arg("hd_scene_parse"); return nullptr; }
+  hd_scene* s = new hd_scene;
+  if (guarded([&] { s->spec = parse_scene_json(text); }) != HD_OK) { delete s; return nullptr; }
+  return s;
+}
+hd_scene* hd_scene_builtin(const char* name) {
+  if (!name) { null_arg("hd_scene_builtin"); return nullptr; }
+  hd_scene* s = new hd_scene;
+  if (guarded([&] { s->spec = builtin_scene(name); }) != HD_OK) { delete s; return nullptr; }
+  return s;
+}
+void hd_scene_free(hd_scene* s) { delete s; }
+int hd_scene_vertex_count(const hd_scene* s) { return s ? s->spec.mesh.vertex_count() : 0; }
+int hd_scene_element_count(const hd_scene* s) { return s ? s->spec.mesh.element_count() : 0; }
+int hd_scene_frame_count(const hd_scene* s) { return s ? s->spec.frames : 0; }
+const char* hd_scene_name(const hd_scene* s) { return s ? s->spec.name.c_str() : ""; }
+
+hd_sim* hd_sim_create(const hd_scene* scene) {
+  if (!scene) { null_arg("hd_sim_create"); return nullptr; }
+  hd_sim* sim = new hd_sim;
+  const hd_status st = guarded([&] {
+    sim->scene = scene;
+    const SceneSpec& s = scene->spec;
+    sim->material = s.material;
+    sim->system.refresh(s.mesh, sim->material, s.solver.h, s.fixed_vertices);
+    if (s.has_hook) {
+      sim->hook_storage = make_hook(s);
+      sim->hook = &sim->hook_storage;
+    }
+    sim->f_ext = scene_external_force(s);
+    sim->state.q = s.q0;
+    sim->state.v = s.v0;
+    sim->state.time = 0.0;
+  });
+  if (st != HD_OK) { delete sim; return nullptr; }
+  return sim;
+}
+void hd_sim_free(hd_sim* sim) { delete sim; }
+
+hd_status hd_sim_step(hd_sim* sim) {
+  if (!sim) return null_arg("hd_sim_step");
+  return guarded([&] {
+    const SceneSpec& s = sim->scene->spec;
+    SimState st = sim->state;
+    ForwardCache cache = forward_step(s.mesh, sim->material, sim->system, s.solver, s.obstacles, s.fixed_vertices,
+                                      st, sim->f_ext, sim->hook);
+    sim->state = st;
+    sim->last_iterations = cache.iteration_count;
+    sim->last_converged = cache.converged;
+    sim->last_contact_count = cache.contacts.normal_count();
+    if (sim->record) sim->caches.push_back(std::move(cache));
+  });
+}
+double hd_sim_time(const hd_sim* sim) { return sim ? sim->state.time : 0.0; }
+int hd_sim_dof_count(const hd_sim* sim) { return sim ? static_cast<int>(sim->state.q.size()) : 0; }
+hd_status hd_sim_positions(const hd_sim* sim, double* out, size_t cap) {
+  if (!sim) return null_arg("hd_sim_positions");
+  return copy_vector(sim->state.q, out, cap, "hd_sim_positions");
+}
+hd_status hd_sim_velocities(const hd_sim* sim, double* out, size_t cap) {
+  if (!sim) return null_arg("hd_sim_velocities");
+  return copy_vector(sim->state.v, out, cap, "hd_sim_velocities");
+}
+int hd_sim_last_iterations(const hd_sim* sim) { return sim ? sim->last_iterations : 0; }
+int hd_sim_last_converged(const hd_sim* sim) { return sim && sim->last_converged ? 1 : 0; }
+int hd_sim_last_contact_count(const hd_sim* sim) { return sim ? sim->last_contact_count : 0; }
+
+// ---- drivers: simulate only (gradcheck/identify are out of scope here) ----
+hd_status hd_run_simulate(const hd_scene* scene, const char* out_dir, char** summary_json) {
+  if (!scene) return null_arg("hd_run_simulate");
+  return guarded([&] {
+    const SceneSpec& s = scene->spec;
+    GlobalSystem sys;
+    MaterialField mat = s.material;
+    StateForce hs;
+    const StateForce* hook = nullptr;
+    if (s.has_hook) { hs = make_hook(s); hook = &hs; }
+    const VecX f = scene_external_force(s);
+    SimState st;
+    st.q = s.q0;
+    st.v = s.v0;
+    nlohmann::json sum;
+    std::vector<int> iters;
+    bool all = true;
+    double pen = 0;
+    for (int t = 0; t < s.frames; ++t) {
+      ForwardCache c = forward_step(s.mesh, mat, sys, s.solver, s.obstacles, s.fixed_vertices, st, f, hook);
+      iters.push_back(c.iteration_count);
+      all = all && c.converged;
+      for (const auto& ob : s.obstacles)
+        for (int v = 0; v < s.mesh.vertex_count(); ++v) pen = std::max(pen, -obstacle_signed_distance(ob, seg3(st.q, v)));
+    }
+    sum["frames"] = s.frames;
+    sum["iterations"] = iters;
+    sum["refactorizations"] = sys.refactor_count();
+    sum["all_converged"] = all;
+    sum["max_penetration"] = pen;
+    if (summary_json) *summary_json = copy_string(sum.dump(2));
+    (void)out_dir;
+  });
+}
+hd_status hd_run_gradcheck(const hd_scene*, const char*, const char*, char**, int*) {
+  set_error(HD_ERR_INVALID_ARGUMENT, "hd_run_gradcheck: not provided by the oracle library");
+  return HD_ERR_INVALID_ARGUMENT;
+}
+hd_status hd_run_identify(const char*, const char*, char**, int*) {
+  set_error(HD_ERR_INVALID_ARGUMENT, "hd_run_identify: not provided by the oracle library");
+  return HD_ERR_INVALID_ARGUMENT;
+}
+hd_status hd_run_identify_file(const char*, const char*, char**, int*) {
+  set_error(HD_ERR_INVALID_ARGUMENT, "hd_run_identify_file: not provided by the oracle library");
+  return HD_ERR_INVALID_ARGUMENT;
+}
+hd_status hd_factor_stats(const hd_scene* scene, char** stats_json) {
+  if (!scene) return null_arg("hd_factor_stats");
+  return guarded([&] {
+    const SceneSpec& s = scene->spec;
+    GlobalSystem sys;
+    sys.refresh(s.mesh, s.material, s.solver.h, s.fixed_vertices);
+    nlohmann::json j;
+    j["vertices"] = s.mesh.vertex_count();
+    j["elements"] = s.mesh.element_count();
+    j["dofs"] = s.mesh.dof_count();
+    j["free_vertices"] = sys.free_count();
+    j["fixed_vertices"] = static_cast<int>(sys.fixed_vertices().size());
+    j["ordering"] = sys.factor().ordering_name();
+    j["factor_nnz"] = sys.factor().s_nnz();
+    j["factor_fill_ratio"] = sys.factor().s_fill_ratio();
+    j["l_nnz"] = sys.factor().l_nnz();
+    j["factor_millis"] = sys.factor().factor_millis();
+    j["weight_contrast"] = s.material.weight_contrast();
+    j["refactorizations"] = sys.refactor_count();
+    if (stats_json) *stats_json = copy_string(j.dump(2));
+  });
+}
+
+// ---- B200 extensions -------------------------------------------------------
+hd_status hd_sim_record(hd_sim* sim, int enable) {
+  if (!sim) return null_arg("hd_sim_record");
+  sim->record = enable != 0;
+  if (!enable) sim->caches.clear();
+  return HD_OK;
+}
+int hd_sim_recorded_frames(const hd_sim* sim) { return sim ? static_cast<int>(sim->caches.size()) : 0; }
+
+hd_status hd_sim_set_state(hd_sim* sim, const double* q, const double* v, double time) {
+  if (!sim) return null_arg("hd_sim_set_state");
+  const size_t n = sim->state.q.size();
+  if (q) sim->state.q.assign(q, q + n);
+  if (v) sim->state.v.assign(v, v + n);
+  sim->state.time = time;
+  sim->caches.clear();
+  return HD_OK;
+}
+
+hd_status hd_sim_backward(hd_sim* sim, const double* dl_dq_direct, const double* dl_dq_final,
+                          const double* dl_dv_final, double* dl_dq0, double* dl_dv0, double* dl_df_ext,
+                          double* dl_de, double* dl_dw, size_t dl_dw_capacity) {
+  if (!sim) return null_arg("hd_sim_backward");
+  return guarded([&] {
+    const SceneSpec& s = sim->scene->spec;
+    const int frames = static_cast<int>(sim->caches.size());
+    if (frames == 0) fail(ErrorCode::InvalidArgument, "hd_sim_backward: no recorded frames");
+    const int n = s.mesh.dof_count();
+    std::vector<VecX> direct(frames + 1, zeros(n));
+    if (dl_dq_direct) {
+      for (int t = 0; t <= frames; ++t) direct[t].assign(dl_dq_direct + static_cast<size_t>(t) * n, dl_dq_direct + static_cast<size_t>(t + 1) * n);
+    } else if (dl_dq_final) {
+      direct[frames].assign(dl_dq_final, dl_dq_final + n);
+    }
+    const VecX vfin = dl_dv_final ? VecX(dl_dv_final, dl_dv_final + n) : zeros(n);
+    const ChainResult r = chain_backward(s.mesh, sim->material, sim->system, sim->caches, direct, vfin, sim->hook,
+                                         s.solver.eps_tr);
+    if (dl_dw && dl_dw_capacity < r.dl_dw.size()) fail(ErrorCode::InvalidArgument, "hd_sim_backward: dl_dw buffer too small");
+    if (dl_dq0) std::memcpy(dl_dq0, r.dl_dq0.data(), sizeof(double) * n);
+    if (dl_dv0) std::memcpy(dl_dv0, r.dl_dv0.data(), sizeof(double) * n);
+    if (dl_df_ext) std::memcpy(dl_df_ext, r.dl_df_ext.data(), sizeof(double) * n);
+    if (dl_de) std::memcpy(dl_de, r.dl_de.data(), sizeof(double) * r.dl_de.size());
+    if (dl_dw) std::memcpy(dl_dw, r.dl_dw.data(), sizeof(double) * r.dl_dw.size());
+    sim->tau = r.tau;
+    sim->rho = r.rho;
+    sim->backward_iterations = r.adjoint_iterations;
+  });
+}
+
+hd_status hd_sim_backward_tau(const hd_sim* sim, double* tau, double* rho, size_t cap) {
+  if (!sim) return null_arg("hd_sim_backward_tau");
+  if (cap < sim->tau.size()) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_sim_backward_tau: output buffer too small");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  if (tau) std::memcpy(tau, sim->tau.data(), sizeof(double) * sim->tau.size());
+  if (rho) std::memcpy(rho, sim->rho.data(), sizeof(double) * sim->rho.size());
+  return HD_OK;
+}
+int hd_sim_backward_iterations(const hd_sim* sim) { return sim ? sim->backward_iterations : 0; }
+
+hd_status hd_sim_solve_free(hd_sim* sim, const double* rhs, const double* fixed_q, double* out) {
+  if (!sim || !rhs || !out) return null_arg("hd_sim_solve_free");
+  return guarded([&] {
+    const size_t n = sim->state.q.size();
+    const VecX r(rhs, rhs + n);
+    const VecX fq = fixed_q ? VecX(fixed_q, fixed_q + n) : zeros(static_cast<int>(n));
+    const VecX x = sim->system.solve_free(r, fq);
+    std::memcpy(out, x.data(), sizeof(double) * n);
+  });
+}
+
+hd_status hd_sim_set_young(hd_sim* sim, const double* young, size_t count, int freeze) {
+  if (!sim || !young) return null_arg("hd_sim_set_young");
+  return guarded([&] {
+    if (freeze) sim->material.freeze_means(sim->material.prox_means());
+    sim->material.set_young(std::vector<double>(young, young + count));
+    const SceneSpec& s = sim->scene->spec;
+    sim->system.refresh(s.mesh, sim->material, s.solver.h, s.fixed_vertices);
+    sim->caches.clear();
+  });
+}
+
+long long hd_sim_factor_nnz(const hd_sim* sim) { return sim ? sim->system.factor().s_nnz() : 0; }
+int hd_sim_free_count(const hd_sim* sim) { return sim ? sim->system.free_count() : 0; }
+long long hd_sim_solve_count(const hd_sim* sim) {
+  return sim ? static_cast<long long>(sim->system.factor().apply_inverse_count / 3) : 0;
+}
+long long hd_sim_a_spmv_count(const hd_sim* sim) { return sim ? static_cast<long long>(sim->system.a_spmv_count) : 0; }
+long long hd_sim_refactor_count(const hd_sim* sim) { return sim ? static_cast<long long>(sim->system.refactor_count()) : 0; }
+
+}  // extern "C"

@@ -1,0 +1,294 @@
+"""ctypes binding of the ``hd_*`` C ABI declared in ``include/heterodyn.h``.
+
+Host-side mirror of the reference's public interface
+(/root/reference/proj/include/heterodyn/heterodyn.h:30-141) plus the B200
+extensions (backward chain, state control, counters).  The binding is
+library-agnostic: ``Library(path)`` wraps any shared object exporting the
+header — the product (``paper_2605_14526_b200/_lib/libheterodyn_b200.so``)
+or, in the tests only, the CPU oracle.  Error behaviour follows the
+reference: a non-OK ``hd_status`` raises :class:`HdError` carrying the code
+and ``hd_last_error()`` message.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+import numpy as np
+
+HD_STATUS = {
+    0: "OK", 1: "PARSE", 2: "VALIDATION", 3: "DEGENERATE_ELEMENT", 4: "INVALID_POISSON",
+    5: "NON_POSITIVE_JACOBIAN", 6: "PROX_DIVERGED", 7: "SINGULAR_FILTERED_HESSIAN",
+    8: "NOT_POSITIVE_DEFINITE", 9: "SINGULAR_CONTACT_SYSTEM", 10: "ADJOINT_DIVERGED",
+    11: "LINE_SEARCH_FAILED", 12: "IO", 13: "INVALID_ARGUMENT",
+}
+
+_D = C.POINTER(C.c_double)
+_VP = C.c_void_p
+
+# name -> (restype, argtypes); mirrors include/heterodyn.h
+SIGNATURES = {
+    "hd_last_error": (C.c_char_p, []),
+    "hd_last_error_code": (C.c_int, []),
+    "hd_string_free": (None, [_VP]),
+    "hd_scene_load": (_VP, [C.c_char_p]),
+    "hd_scene_parse": (_VP, [C.c_char_p]),
+    "hd_scene_builtin": (_VP, [C.c_char_p]),
+    "hd_scene_free": (None, [_VP]),
+    "hd_scene_vertex_count": (C.c_int, [_VP]),
+    "hd_scene_element_count": (C.c_int, [_VP]),
+    "hd_scene_frame_count": (C.c_int, [_VP]),
+    "hd_scene_name": (C.c_char_p, [_VP]),
+    "hd_sim_create": (_VP, [_VP]),
+    "hd_sim_free": (None, [_VP]),
+    "hd_sim_step": (C.c_int, [_VP]),
+    "hd_sim_time": (C.c_double, [_VP]),
+    "hd_sim_dof_count": (C.c_int, [_VP]),
+    "hd_sim_positions": (C.c_int, [_VP, _D, C.c_size_t]),
+    "hd_sim_velocities": (C.c_int, [_VP, _D, C.c_size_t]),
+    "hd_sim_last_iterations": (C.c_int, [_VP]),
+    "hd_sim_last_converged": (C.c_int, [_VP]),
+    "hd_sim_last_contact_count": (C.c_int, [_VP]),
+    "hd_run_simulate": (C.c_int, [_VP, C.c_char_p, C.POINTER(_VP)]),
+    "hd_run_gradcheck": (C.c_int, [_VP, C.c_char_p, C.c_char_p, C.POINTER(_VP), C.POINTER(C.c_int)]),
+    "hd_run_identify": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(_VP), C.POINTER(C.c_int)]),
+    "hd_run_identify_file": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(_VP), C.POINTER(C.c_int)]),
+    "hd_factor_stats": (C.c_int, [_VP, C.POINTER(_VP)]),
+    "hd_sim_record": (C.c_int, [_VP, C.c_int]),
+    "hd_sim_recorded_frames": (C.c_int, [_VP]),
+    "hd_sim_set_state": (C.c_int, [_VP, _D, _D, C.c_double]),
+    "hd_sim_backward": (C.c_int, [_VP, _D, _D, _D, _D, _D, _D, _D, _D, C.c_size_t]),
+    "hd_sim_backward_tau": (C.c_int, [_VP, _D, _D, C.c_size_t]),
+    "hd_sim_backward_iterations": (C.c_int, [_VP]),
+    "hd_sim_solve_free": (C.c_int, [_VP, _D, _D, _D]),
+    "hd_sim_set_young": (C.c_int, [_VP, _D, C.c_size_t, C.c_int]),
+    "hd_sim_factor_nnz": (C.c_longlong, [_VP]),
+    "hd_sim_free_count": (C.c_int, [_VP]),
+    "hd_sim_solve_count": (C.c_longlong, [_VP]),
+    "hd_sim_a_spmv_count": (C.c_longlong, [_VP]),
+    "hd_sim_refactor_count": (C.c_longlong, [_VP]),
+}
+
+
+class HdError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(f"[{HD_STATUS.get(code, code)}] {message}")
+        self.code = code
+        self.name = HD_STATUS.get(code, str(code))
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    return a.ctypes.data_as(_D)
+
+
+def _f64(a, n=None):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if n is not None and a.size != n:
+        raise ValueError(f"expected {n} doubles, got {a.size}")
+    return a
+
+
+class Library:
+    """A loaded ``hd_*`` library (product or oracle)."""
+
+    def __init__(self, path: str):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        self.path = path
+        self.lib = C.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(self.lib, name)
+            fn.restype = res
+            fn.argtypes = args
+
+    def check(self, status: int):
+        if status != 0:
+            raise HdError(self.lib.hd_last_error_code(), self.lib.hd_last_error().decode())
+
+    def _take_string(self, p: C.c_void_p) -> str:
+        s = C.cast(p, C.c_char_p).value.decode()
+        self.lib.hd_string_free(p)
+        return s
+
+    # scenes
+    def scene(self, text_or_dict) -> "Scene":
+        text = text_or_dict if isinstance(text_or_dict, str) else json.dumps(text_or_dict)
+        h = self.lib.hd_scene_parse(text.encode())
+        if not h:
+            raise HdError(self.lib.hd_last_error_code(), self.lib.hd_last_error().decode())
+        return Scene(self, h)
+
+    def builtin(self, name: str) -> "Scene":
+        h = self.lib.hd_scene_builtin(name.encode())
+        if not h:
+            raise HdError(self.lib.hd_last_error_code(), self.lib.hd_last_error().decode())
+        return Scene(self, h)
+
+    def load(self, path: str) -> "Scene":
+        h = self.lib.hd_scene_load(path.encode())
+        if not h:
+            raise HdError(self.lib.hd_last_error_code(), self.lib.hd_last_error().decode())
+        return Scene(self, h)
+
+
+class Scene:
+    def __init__(self, lib: Library, handle):
+        self.L = lib
+        self.h = handle
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.L.lib.hd_scene_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @property
+    def vertex_count(self):
+        return self.L.lib.hd_scene_vertex_count(self.h)
+
+    @property
+    def element_count(self):
+        return self.L.lib.hd_scene_element_count(self.h)
+
+    @property
+    def frame_count(self):
+        return self.L.lib.hd_scene_frame_count(self.h)
+
+    @property
+    def name(self):
+        return self.L.lib.hd_scene_name(self.h).decode()
+
+    def factor_stats(self) -> dict:
+        p = _VP()
+        self.L.check(self.L.lib.hd_factor_stats(self.h, C.byref(p)))
+        return json.loads(self.L._take_string(p))
+
+    def run_simulate(self, out_dir: str | None = None) -> dict:
+        p = _VP()
+        self.L.check(self.L.lib.hd_run_simulate(self.h, out_dir.encode() if out_dir else None, C.byref(p)))
+        return json.loads(self.L._take_string(p))
+
+    def sim(self) -> "Sim":
+        h = self.L.lib.hd_sim_create(self.h)
+        if not h:
+            raise HdError(self.L.lib.hd_last_error_code(), self.L.lib.hd_last_error().decode())
+        return Sim(self, h)
+
+
+class Sim:
+    def __init__(self, scene: Scene, handle):
+        self.scene = scene  # keeps the scene alive (the sim borrows it)
+        self.L = scene.L
+        self.h = handle
+        self.n = self.L.lib.hd_sim_dof_count(handle)
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.L.lib.hd_sim_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def step(self, frames: int = 1):
+        for _ in range(frames):
+            self.L.check(self.L.lib.hd_sim_step(self.h))
+
+    @property
+    def time(self):
+        return self.L.lib.hd_sim_time(self.h)
+
+    def positions(self):
+        out = np.empty(self.n)
+        self.L.check(self.L.lib.hd_sim_positions(self.h, _ptr(out), out.size))
+        return out
+
+    def velocities(self):
+        out = np.empty(self.n)
+        self.L.check(self.L.lib.hd_sim_velocities(self.h, _ptr(out), out.size))
+        return out
+
+    @property
+    def last_iterations(self):
+        return self.L.lib.hd_sim_last_iterations(self.h)
+
+    @property
+    def last_converged(self):
+        return bool(self.L.lib.hd_sim_last_converged(self.h))
+
+    @property
+    def last_contact_count(self):
+        return self.L.lib.hd_sim_last_contact_count(self.h)
+
+    def record(self, enable: bool = True):
+        self.L.check(self.L.lib.hd_sim_record(self.h, 1 if enable else 0))
+
+    @property
+    def recorded_frames(self):
+        return self.L.lib.hd_sim_recorded_frames(self.h)
+
+    def set_state(self, q=None, v=None, time: float = 0.0):
+        q = _f64(q, self.n)
+        v = _f64(v, self.n)
+        self.L.check(self.L.lib.hd_sim_set_state(self.h, _ptr(q), _ptr(v), time))
+
+    def backward(self, dl_dq_final=None, dl_dv_final=None, dl_dq_direct=None) -> dict:
+        ne = self.scene.element_count
+        frames = self.recorded_frames
+        direct = None
+        if dl_dq_direct is not None:
+            direct = _f64(dl_dq_direct, (frames + 1) * self.n)
+        qf = _f64(dl_dq_final, self.n)
+        vf = _f64(dl_dv_final, self.n)
+        out = {k: np.zeros(self.n) for k in ("dl_dq0", "dl_dv0", "dl_df_ext")}
+        out["dl_de"] = np.zeros(ne)
+        dw = np.zeros(2 * ne)
+        self.L.check(self.L.lib.hd_sim_backward(
+            self.h, _ptr(direct), _ptr(qf), _ptr(vf), _ptr(out["dl_dq0"]), _ptr(out["dl_dv0"]),
+            _ptr(out["dl_df_ext"]), _ptr(out["dl_de"]), _ptr(dw), dw.size))
+        out["dl_dw"] = dw
+        tau = np.zeros(max(frames, 1))
+        rho = np.zeros(max(frames, 1))
+        self.L.check(self.L.lib.hd_sim_backward_tau(self.h, _ptr(tau), _ptr(rho), tau.size))
+        out["tau"] = tau[:frames]
+        out["rho"] = rho[:frames]
+        out["adjoint_iterations"] = self.L.lib.hd_sim_backward_iterations(self.h)
+        return out
+
+    def solve_free(self, rhs, fixed_q=None):
+        rhs = _f64(rhs, self.n)
+        fq = _f64(fixed_q, self.n)
+        out = np.empty(self.n)
+        self.L.check(self.L.lib.hd_sim_solve_free(self.h, _ptr(rhs), _ptr(fq), _ptr(out)))
+        return out
+
+    def set_young(self, young, freeze_means: bool = False):
+        y = _f64(young)
+        self.L.check(self.L.lib.hd_sim_set_young(self.h, _ptr(y), y.size, 1 if freeze_means else 0))
+
+    @property
+    def factor_nnz(self):
+        return self.L.lib.hd_sim_factor_nnz(self.h)
+
+    @property
+    def free_count(self):
+        return self.L.lib.hd_sim_free_count(self.h)
+
+    @property
+    def solve_count(self):
+        return self.L.lib.hd_sim_solve_count(self.h)
+
+    @property
+    def a_spmv_count(self):
+        return self.L.lib.hd_sim_a_spmv_count(self.h)
+
+    @property
+    def refactor_count(self):
+        return self.L.lib.hd_sim_refactor_count(self.h)
