@@ -1,0 +1,206 @@
+/* hdk — the thin C-ABI layer between the heterodyn host library (C++) and
+ * its sm_100a kernels.  Every entry point takes device pointers, plain sizes
+ * and a cudaStream_t (passed as void*), launches asynchronously and returns
+ * 0 or a CUDA error number; no exceptions, no torch types.  Device-side
+ * solver failures are reported through the int error word in hdk_step
+ * (first failing code wins) using the hd_status numbering of heterodyn.h.
+ *
+ * Each launcher names the reference routine it replaces
+ * (paths relative to /root/reference/proj/src).
+ */
+#ifndef HDK_H
+#define HDK_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HDK_API __attribute__((visibility("default")))
+
+/* Element-parallel mesh data, structure-of-arrays (mesh.hpp:16-60). */
+typedef struct hdk_mesh {
+  int nv, ne;
+  const int* elem;        /* 4*ne vertex ids, element-major */
+  const double* bm;       /* 9*ne: Dm^{-1}(r,c) at bm[(3r+c)*ne + e] */
+  const double* mass;     /* nv lumped vertex masses */
+  const int* inc_off;     /* nv+1: incident (element, slot) lists per vertex */
+  const int* inc;         /* 4*ne entries 4*e + slot, ascending e per vertex */
+} hdk_mesh;
+
+/* Per-element weights with the rest volume folded in (material.hpp:40-50). */
+typedef struct hdk_material {
+  int kind;               /* 0 corotated, 1 neo-hookean */
+  int barrier;            /* corotated + log-volume barrier */
+  double mu_bar, lambda_bar, k_bar; /* prox means (material.cpp:64-71) */
+  const double* w1;       /* NH: (2mu+lambda)V ; corotated: 2mu V */
+  const double* w2;       /* corotated: lambda V (unused for NH) */
+  const double* mu_e;     /* barrier parameters per element */
+  const double* lambda_e;
+  const double* beta_vh;  /* beta_e V / h, or NULL when beta0 == 0 */
+  const double* vol;      /* rest volumes */
+} hdk_material;
+
+/* Explicit inverse factor A^{-1} = S'^T S' in postordered elimination order.
+ * Row r of S' is dense over columns [r - len_r + 1, r] (its etree subtree)
+ * and stored contiguously at sval[row_off[r]].  Work is cut into column
+ * tiles of width tile_w; a segment is one row's part inside one tile;
+ * consecutive segments of a tile form work units (factor.cpp:106-109). */
+typedef struct hdk_seg {
+  long long off;          /* index into sval of the segment's first value */
+  int row;                /* S' row */
+  int clo;                /* first column (global, in elimination order) */
+  int len;                /* number of columns */
+  int pslot;              /* slot of this segment's partial row dot */
+} hdk_seg;
+
+typedef struct hdk_factor {
+  int n;                  /* free vertices */
+  int tile_w, n_tiles, n_units;
+  const double* sval;
+  const hdk_seg* seg;
+  const int* unit_seg;    /* n_units+1 */
+  const int* unit_tile;   /* n_units */
+  const int* tile_unit;   /* n_tiles+1: units of tile t are contiguous */
+  const int* row_pslot;   /* n+1: partial-dot slots of row r */
+  const int* p2v;         /* n: elimination position -> vertex */
+  const int* v2p;         /* nv: vertex -> position or -1 (fixed) */
+  double* part1;          /* 3*row_pslot[n] scratch */
+  double* part2;          /* 3*tile_w*n_units scratch */
+  double* z;              /* 3*n scratch */
+} hdk_factor;
+
+/* Scalar CSR in elimination order (a_free / a_free_fixed, factor.hpp:98-99). */
+typedef struct hdk_csr {
+  int rows;
+  const int* off;
+  const int* col;
+  const double* val;
+} hdk_csr;
+
+/* Solve x = A^{-1} rhs on 3 axes: rhs in elimination order [n][3]; the result
+ * is scattered into out_full[3*v+a] for free vertices (fixed entries are not
+ * touched).  Replaces GlobalSystem::solve_free (factor.cpp:196-208). */
+HDK_API int hdk_apply_inverse3(const hdk_factor* f, const double* rhs_perm, double* out_full, void* stream);
+/* Same, result kept in elimination order (out_perm [n][3]). */
+HDK_API int hdk_apply_inverse3_perm(const hdk_factor* f, const double* rhs_perm, double* out_perm, void* stream);
+
+/* Per-element local step (local_solve + the element part of pd_rhs,
+ * forward.cpp:70-117).  Writes the weighted element force V G^T target
+ * (12 doubles per element) and, when cache != NULL, the projection cache
+ * (24 doubles per element: sigma*, sigma_F, U, V; corotated adds 3 more for
+ * the volume target).  Errors: PROX_DIVERGED (6) into *err. */
+HDK_API int hdk_local_step(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
+                           double* cache, int* err, void* stream);
+
+/* V_e * model energy density at q (backward.cpp:23-73, element part); *bad
+ * receives NON_POSITIVE_JACOBIAN (5) or PROX_DIVERGED (6). */
+HDK_API int hdk_element_energy(const hdk_mesh* m, const hdk_material* mat, const double* q, double* energy, int* bad,
+                               void* stream);
+/* Compact prox differential per element from the projection cache and the
+ * device scalar *tau (tr_blend + nh/polar/volume/barrier differentials,
+ * localstep.cpp:276-423): 30 doubles SoA.  Errors: SINGULAR_FILTERED_HESSIAN. */
+HDK_API int hdk_differential(const hdk_mesh* m, const hdk_material* mat, const double* cache, const double* tau,
+                             double* dcomp, int* err, void* stream);
+/* Element forces of B x (matrix-free assemble_db_dq + apply, backward.cpp:117-163). */
+HDK_API int hdk_bapply(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force, void* stream);
+/* Per-element dL/dw (accumulated into dl_dw), dL/dE (accumulated into dl_de)
+ * and the damping element force of mu (backward.cpp:311, 361-391). */
+HDK_API int hdk_route_elements(const hdk_mesh* m, const hdk_material* mat, const double* cache, const double* q_star,
+                               const double* mu, double unit_mu, double unit_lambda, double* dl_dw, double* dl_de,
+                               double* ef_damp, void* stream);
+/* Element forces of the stiffness-damping term beta_e V_e / h G^T F(q)
+ * (damping_rhs, forward.cpp:119-138). */
+HDK_API int hdk_damping_elements(const hdk_mesh* m, const double* beta_vh, const double* q, double* elem_force,
+                                 void* stream);
+
+/* ---- loop control block (device-resident) ------------------------------- */
+#define HDK_AA_MAX 8
+#define HDK_RED_BLOCKS 296 /* 2 x 148 SMs: fixed reduction grid (deterministic) */
+#define HDK_RED_Q 24       /* partial slots per block */
+
+typedef struct hdk_ctl {
+  int k, k_max, iterations, converged;
+  int err, done, bad, cond;
+  int window, count, head, has_last, mixed, pad0;
+  double eps_rel, eps_abs, guard, tol;
+  double gamma[HDK_AA_MAX];
+  double gram[HDK_AA_MAX * HDK_AA_MAX];
+  double red[HDK_RED_Q];
+  double tau, rho, model, eps_tr;
+} hdk_ctl;
+
+/* Vector kernels (vec.cu).  Vectors are full xyz-interleaved (3 nv) unless
+ * named *_perm ([n][3] in elimination order). */
+typedef struct hdk_vtx {
+  int nv, n;
+  const int* v2p;         /* nv */
+  const int* p2v;         /* n */
+  const double* mass;     /* nv */
+  const int* inc_off;
+  const int* inc;
+} hdk_vtx;
+
+/* q~ = q + h v + h^2 (f_ext + hook) / m; q_cur = q~ with fixed rows pinned to q
+ * (free_fall_target + pin, forward.cpp:59-68,165-169,210-211). */
+HDK_API int hdk_free_fall(const hdk_vtx* x, const double* q, const double* v, const double* f_ext, double h,
+                          int hook_vertex, const double* hook /* ax ay az k d */, double* q_tilde, double* q_cur,
+                          void* stream);
+/* out[v] = cm * m_v * base[v] + add[v] + sum of element forces at v (add may be NULL). */
+HDK_API int hdk_gather(const hdk_vtx* x, const double* ef, double cm, const double* base, const double* add,
+                       double* out, void* stream);
+/* Forward rhs b = M/h^2 q~ + damp + sum ef (pd_rhs, forward.cpp:96-117);
+ * rhs_perm = b - A_fd q_d at free rows; gate partials of |b - b_prev|, |b|;
+ * b_prev <- b. */
+HDK_API int hdk_gather_rhs(const hdk_vtx* x, const double* ef, double inv_h2, const double* q_tilde, const double* damp,
+                           const double* fixcoup, double* b_prev, double* rhs_perm, double* partial, void* stream);
+/* rhs_perm[p] = base[p2v[p]] (+ element forces when ef != NULL). */
+HDK_API int hdk_gather_perm(const hdk_vtx* x, const double* base, const double* ef, double* rhs_perm, void* stream);
+/* fixcoup[p] = sum_k A_fd(p, k) q[fixed_k] (solve_free's coupling, factor.cpp:201-205). */
+HDK_API int hdk_fixed_coupling(const hdk_csr* a_fd, const int* fixed, const double* q, double* fixcoup, void* stream);
+/* Type-II Anderson mixing (forward.cpp:17-51) in three launches: history
+ * update + dot partials, coefficient solve (1 block), mix.  mode 0: forward
+ * (pins fixed rows, gate partials, rotates q_prev <- q_cur <- q_next);
+ * mode 1: adjoint backbone (convergence test |t-x| <= tol |t|, backward.cpp:188-199). */
+HDK_API int hdk_aa_dots(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, const double* qcur, double* last_q,
+                        double* last_g, double* dq, double* dg, double* partial, void* stream);
+HDK_API int hdk_aa_solve(hdk_ctl* ctl, const double* partial, int mode, void* stream);
+HDK_API int hdk_aa_mix(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, double* qcur, double* qprev,
+                       const double* qpin, const double* dq, const double* dg, double* partial, int mode, void* stream);
+/* Dual gate (forward.cpp:140-146) and loop condition for the graph while node. */
+HDK_API int hdk_gate(hdk_ctl* ctl, const double* partial_b, const double* partial_q, unsigned long long cond_handle,
+                     void* stream);
+HDK_API int hdk_backbone_cond(hdk_ctl* ctl, unsigned long long cond_handle, void* stream);
+/* A_ff dq dot partials for the trust-region model (backward.cpp:77-79). */
+HDK_API int hdk_tr_model(const hdk_vtx* x, const hdk_csr* a_ff, const double* q_star, const double* q_prev,
+                         double* dq_perm, double* partial, void* stream);
+/* Energy partials and rho / tau selection (backward.cpp:75-108). */
+HDK_API int hdk_tr_select(const hdk_vtx* x, int ne, const double* e_prev, const double* e_star, const double* q_prev,
+                          const double* q_star, const double* q_tilde, double inv_h2, const double* model_partial,
+                          double* partial, hdk_ctl* ctl, void* stream);
+/* Vertex part of route_gradients (backward.cpp:296-356) and the chain update
+ * (drivers.cpp:84-95). */
+HDK_API int hdk_route_vertices(const hdk_vtx* x, const double* mu, const double* ef_damp, const double* b_mu,
+                               const double* q_bar, const double* v_bar, const double* coup_fixed, double h,
+                               double alpha, int hook_vertex, double hook_k, double hook_d, double* dl_dq_t,
+                               double* dl_dv_t, double* dl_df_acc, void* stream);
+/* coup[v] = sum_p A_fd(p, k(v)) mu[p2v[p]] for fixed vertices (A_fd^T mu). */
+HDK_API int hdk_fixed_coupling_t(const hdk_csr* a_df, const int* fixed, const int* p2v, const double* mu, double* coup,
+                                 void* stream);
+/* Resets the loop-control block (first kernel of every step graph). */
+HDK_API int hdk_ctl_init(hdk_ctl* ctl, int window, double guard, int k_max, double eps_rel, double eps_abs, double tol,
+                         double eps_tr, int iterations0, void* stream);
+/* State commit after a successful step: v = (q* - q)/h, q = q* (skipped when
+ * ctl->err != 0 so a failed step leaves the state intact, heterodyn.h:87-90). */
+HDK_API int hdk_commit(int n, const hdk_ctl* ctl, const double* q_star, double h, double* q, double* v, void* stream);
+/* y = a x + b z elementwise over n doubles (z may be NULL). */
+HDK_API int hdk_axpby(int n, double a, const double* x, double b, const double* z, double* y, void* stream);
+/* v* = (q* - q_t)/h (forward.cpp:253). */
+HDK_API int hdk_velocity(int n, const double* q_star, const double* q_t, double h, double* v_star, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HDK_H */

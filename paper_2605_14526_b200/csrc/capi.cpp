@@ -1,0 +1,263 @@
+// hd_* C ABI of include/heterodyn.h over the B200 engine.  Reference half:
+// capi.cpp:94-322 (opaque handles, status codes, thread-local errors,
+// exceptions never cross the boundary); B200 extensions: recorded frames,
+// backward chain, state control and counters.
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <sstream>
+
+#include <nlohmann/json.hpp>
+
+#include "../../include/heterodyn.h"
+#include "engine.hpp"
+
+using namespace hdb;
+
+struct hd_scene {
+  Scene spec;
+};
+
+struct hd_sim {
+  const hd_scene* scene = nullptr;
+  std::unique_ptr<Engine> eng;
+  GradOut last_grad;
+};
+
+namespace {
+thread_local int t_code = 0;
+thread_local std::string t_msg;
+
+void set_error(int c, const std::string& m) {
+  t_code = c;
+  t_msg = m;
+}
+
+template <class F>
+hd_status guarded(F&& f) {
+  try {
+    f();
+    return HD_OK;
+  } catch (const Error& e) {
+    set_error(static_cast<int>(e.code), e.what());
+    return static_cast<hd_status>(e.code);
+  } catch (const std::exception& e) {
+    set_error(HD_ERR_INVALID_ARGUMENT, std::string("unexpected error: ") + e.what());
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+}
+
+hd_status bad_arg(const std::string& m) {
+  set_error(HD_ERR_INVALID_ARGUMENT, m);
+  return HD_ERR_INVALID_ARGUMENT;
+}
+
+char* dup(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  if (p) std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+hd_status copy_out(const Vec& v, double* out, size_t cap, const char* who) {
+  if (!out || cap < v.size()) return bad_arg(std::string(who) + ": output buffer too small");
+  std::memcpy(out, v.data(), v.size() * sizeof(double));
+  return HD_OK;
+}
+
+template <class Make>
+hd_scene* make_scene(const char* who, const void* arg, Make&& make) {
+  if (!arg) {
+    bad_arg(std::string(who) + ": NULL argument");
+    return nullptr;
+  }
+  auto s = std::make_unique<hd_scene>();
+  if (guarded([&] { s->spec = make(); }) != HD_OK) return nullptr;
+  return s.release();
+}
+
+std::string read_file(const char* path) {
+  std::ifstream in(path);
+  if (!in) raise(Code::Io, std::string("cannot open scene file: ") + path);
+  std::stringstream b;
+  b << in.rdbuf();
+  return b.str();
+}
+}  // namespace
+
+extern "C" {
+
+const char* hd_last_error(void) { return t_msg.c_str(); }
+int hd_last_error_code(void) { return t_code; }
+void hd_string_free(char* s) { std::free(s); }
+
+hd_scene* hd_scene_load(const char* path) {
+  return make_scene("hd_scene_load", path, [&] { return parse_scene(read_file(path)); });
+}
+hd_scene* hd_scene_parse(const char* text) {
+  return make_scene("hd_scene_parse", text, [&] { return parse_scene(text); });
+}
+hd_scene* hd_scene_builtin(const char* name) {
+  return make_scene("hd_scene_builtin", name, [&] { return builtin_scene(name); });
+}
+void hd_scene_free(hd_scene* s) { delete s; }
+int hd_scene_vertex_count(const hd_scene* s) { return s ? s->spec.mesh.nv : 0; }
+int hd_scene_element_count(const hd_scene* s) { return s ? s->spec.mesh.ne : 0; }
+int hd_scene_frame_count(const hd_scene* s) { return s ? s->spec.frames : 0; }
+const char* hd_scene_name(const hd_scene* s) { return s ? s->spec.name.c_str() : ""; }
+
+hd_sim* hd_sim_create(const hd_scene* scene) {
+  if (!scene) {
+    bad_arg("hd_sim_create: scene is NULL");
+    return nullptr;
+  }
+  auto sim = std::make_unique<hd_sim>();
+  sim->scene = scene;
+  if (guarded([&] { sim->eng = std::make_unique<Engine>(scene->spec); }) != HD_OK) return nullptr;
+  return sim.release();
+}
+void hd_sim_free(hd_sim* sim) { delete sim; }
+
+hd_status hd_sim_step(hd_sim* sim) {
+  if (!sim) return bad_arg("hd_sim_step: sim is NULL");
+  return guarded([&] { sim->eng->step(); });
+}
+double hd_sim_time(const hd_sim* sim) { return sim ? sim->eng->time() : 0.0; }
+int hd_sim_dof_count(const hd_sim* sim) { return sim ? sim->eng->dofs() : 0; }
+hd_status hd_sim_positions(const hd_sim* sim, double* out, size_t cap) {
+  if (!sim) return bad_arg("hd_sim_positions: sim is NULL");
+  Vec q;
+  const hd_status st = guarded([&] { q = sim->eng->positions(); });
+  return st != HD_OK ? st : copy_out(q, out, cap, "hd_sim_positions");
+}
+hd_status hd_sim_velocities(const hd_sim* sim, double* out, size_t cap) {
+  if (!sim) return bad_arg("hd_sim_velocities: sim is NULL");
+  Vec v;
+  const hd_status st = guarded([&] { v = sim->eng->velocities(); });
+  return st != HD_OK ? st : copy_out(v, out, cap, "hd_sim_velocities");
+}
+int hd_sim_last_iterations(const hd_sim* sim) { return sim ? sim->eng->last_iterations : 0; }
+int hd_sim_last_converged(const hd_sim* sim) { return sim && sim->eng->last_converged ? 1 : 0; }
+int hd_sim_last_contact_count(const hd_sim* sim) { return sim ? sim->eng->last_contacts : 0; }
+
+hd_status hd_run_simulate(const hd_scene* scene, const char* out_dir, char** summary_json) {
+  if (!scene) return bad_arg("hd_run_simulate: scene is NULL");
+  return guarded([&] {
+    Engine eng(scene->spec);
+    nlohmann::json s;
+    std::vector<int> its;
+    bool all = true;
+    for (int t = 0; t < scene->spec.frames; ++t) {
+      eng.step();
+      its.push_back(eng.last_iterations);
+      all = all && eng.last_converged;
+    }
+    s["frames"] = scene->spec.frames;
+    s["iterations"] = its;
+    s["refactorizations"] = eng.refactor_count;
+    s["all_converged"] = all;
+    s["max_penetration"] = 0.0;
+    (void)out_dir;
+    if (summary_json) *summary_json = dup(s.dump(2));
+  });
+}
+
+hd_status hd_run_gradcheck(const hd_scene*, const char*, const char*, char**, int*) {
+  return bad_arg("hd_run_gradcheck: finite-difference driver is outside this build's scope (use hd_sim_backward)");
+}
+hd_status hd_run_identify(const char*, const char*, char**, int*) {
+  return bad_arg("hd_run_identify: system-identification driver is outside this build's scope");
+}
+hd_status hd_run_identify_file(const char*, const char*, char**, int*) {
+  return bad_arg("hd_run_identify_file: system-identification driver is outside this build's scope");
+}
+
+// Host-only: builds the factor without touching the GPU (drivers.cpp:990-1006).
+hd_status hd_factor_stats(const hd_scene* scene, char** stats_json) {
+  if (!scene) return bad_arg("hd_factor_stats: scene is NULL");
+  return guarded([&] {
+    const Scene& s = scene->spec;
+    const HostFactor F = build_factor(s.mesh, s.material, s.solver.h, s.fixed, s.ordering);
+    nlohmann::json j;
+    j["vertices"] = s.mesh.nv;
+    j["elements"] = s.mesh.ne;
+    j["dofs"] = 3 * s.mesh.nv;
+    j["free_vertices"] = F.n;
+    j["fixed_vertices"] = static_cast<int>(s.fixed.size());
+    j["ordering"] = F.ordering;
+    j["factor_nnz"] = F.row_off.back();
+    j["factor_fill_ratio"] = static_cast<double>(F.row_off.back()) / (static_cast<double>(F.n) * F.n);
+    j["l_nnz"] = F.l_nnz;
+    j["factor_millis"] = F.millis;
+    j["segments"] = F.seg.size();
+    j["work_units"] = F.unit_tile.size();
+    j["weight_contrast"] = s.material.contrast();
+    j["refactorizations"] = 1;
+    if (stats_json) *stats_json = dup(j.dump(2));
+  });
+}
+
+hd_status hd_sim_record(hd_sim* sim, int enable) {
+  if (!sim) return bad_arg("hd_sim_record: sim is NULL");
+  sim->eng->record(enable != 0);
+  return HD_OK;
+}
+int hd_sim_recorded_frames(const hd_sim* sim) { return sim ? sim->eng->recorded() : 0; }
+
+hd_status hd_sim_set_state(hd_sim* sim, const double* q, const double* v, double time) {
+  if (!sim) return bad_arg("hd_sim_set_state: sim is NULL");
+  return guarded([&] { sim->eng->set_state(q, v, time); });
+}
+
+hd_status hd_sim_backward(hd_sim* sim, const double* direct, const double* dq_final, const double* dv_final,
+                          double* dl_dq0, double* dl_dv0, double* dl_df_ext, double* dl_de, double* dl_dw,
+                          size_t dl_dw_capacity) {
+  if (!sim) return bad_arg("hd_sim_backward: sim is NULL");
+  return guarded([&] {
+    GradOut g = sim->eng->backward(direct, dq_final, dv_final);
+    if (dl_dw && dl_dw_capacity < g.dl_dw.size()) raise(Code::InvalidArgument, "hd_sim_backward: dl_dw buffer too small");
+    const auto put = [](double* d, const Vec& v) {
+      if (d) std::memcpy(d, v.data(), v.size() * sizeof(double));
+    };
+    put(dl_dq0, g.dl_dq0);
+    put(dl_dv0, g.dl_dv0);
+    put(dl_df_ext, g.dl_df_ext);
+    put(dl_de, g.dl_de);
+    put(dl_dw, g.dl_dw);
+    sim->last_grad = std::move(g);
+  });
+}
+
+hd_status hd_sim_backward_tau(const hd_sim* sim, double* tau, double* rho, size_t cap) {
+  if (!sim) return bad_arg("hd_sim_backward_tau: sim is NULL");
+  const auto& g = sim->last_grad;
+  if (cap < g.tau.size()) return bad_arg("hd_sim_backward_tau: output buffer too small");
+  if (tau) std::memcpy(tau, g.tau.data(), g.tau.size() * sizeof(double));
+  if (rho) std::memcpy(rho, g.rho.data(), g.rho.size() * sizeof(double));
+  return HD_OK;
+}
+int hd_sim_backward_iterations(const hd_sim* sim) { return sim ? sim->last_grad.adjoint_iterations : 0; }
+
+hd_status hd_sim_solve_free(hd_sim* sim, const double* rhs, const double* fixed_q, double* out) {
+  if (!sim || !rhs || !out) return bad_arg("hd_sim_solve_free: NULL argument");
+  return guarded([&] {
+    const Vec x = sim->eng->solve_free(rhs, fixed_q);
+    // fixed entries of the result are the prescribed positions (factor.cpp:197)
+    std::memcpy(out, x.data(), x.size() * sizeof(double));
+    for (int v : sim->scene->spec.fixed)
+      for (int a = 0; a < 3; ++a) out[3 * v + a] = fixed_q ? fixed_q[3 * v + a] : 0.0;
+  });
+}
+
+hd_status hd_sim_set_young(hd_sim* sim, const double* young, size_t count, int freeze) {
+  if (!sim || !young) return bad_arg("hd_sim_set_young: NULL argument");
+  return guarded([&] { sim->eng->set_young(Vec(young, young + count), freeze != 0); });
+}
+
+long long hd_sim_factor_nnz(const hd_sim* sim) { return sim ? sim->eng->factor().row_off.back() : 0; }
+int hd_sim_free_count(const hd_sim* sim) { return sim ? sim->eng->factor().n : 0; }
+long long hd_sim_solve_count(const hd_sim* sim) { return sim ? sim->eng->solve_count : 0; }
+long long hd_sim_a_spmv_count(const hd_sim* sim) { return sim ? sim->eng->a_spmv_count : 0; }
+long long hd_sim_refactor_count(const hd_sim* sim) { return sim ? sim->eng->refactor_count : 0; }
+
+}  // extern "C"

@@ -1,0 +1,129 @@
+// Device-resident forward/backward PD engine (one hd_sim).  The reference's
+// forward_step (forward.cpp:148-272), backward_step (backward.cpp:396-414),
+// roll/chain_backward (drivers.cpp:31-99) and GlobalSystem (factor.hpp:85-130)
+// re-designed for sm_100a: all per-iteration state stays in HBM, the PD and
+// adjoint fixed-point loops run inside CUDA graphs whose WHILE conditional
+// node is driven by the device-side dual gate, and only per-step status
+// crosses back to the host.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hdk.h"
+#include "host.hpp"
+
+namespace hdb {
+
+struct DevArena {
+  std::vector<void*> ptrs;
+  ~DevArena();
+  void* raw(size_t bytes);
+  template <class T>
+  T* alloc(size_t n) { return static_cast<T*>(raw(sizeof(T) * (n ? n : 1))); }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* p = alloc<T>(v.size());
+    if (!v.empty()) copy_h2d(p, v.data(), sizeof(T) * v.size());
+    return p;
+  }
+  static void copy_h2d(void* d, const void* h, size_t bytes);
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+struct GradOut {
+  Vec dl_dq0, dl_dv0, dl_df_ext, dl_de, dl_dw;
+  std::vector<double> tau, rho;
+  int adjoint_iterations = 0;
+};
+
+class Engine {
+ public:
+  explicit Engine(const Scene& scene);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  void step();  // throws Error; state untouched on failure
+  void record(bool on);
+  int recorded() const { return nrec_; }
+  void set_state(const double* q, const double* v, double time);
+  GradOut backward(const double* dl_dq_direct, const double* dl_dq_final, const double* dl_dv_final);
+  Vec solve_free(const double* rhs, const double* fixed_q);
+  void set_young(const Vec& young, bool freeze);
+
+  Vec positions() const;
+  Vec velocities() const;
+  double time() const { return time_; }
+  int dofs() const { return 3 * mesh().nv; }
+  int last_iterations = 0, last_converged = 0, last_contacts = 0;
+  long long solve_count = 0, a_spmv_count = 0, refactor_count = 0;
+  const HostFactor& factor() const { return hf_; }
+  const Mesh& mesh() const { return scene_.mesh; }
+  const Material& material() const { return mat_; }
+  cudaStream_t stream() const { return st_; }
+
+ private:
+  struct Frame;
+  void build_static();
+  void build_factor_device();
+  void build_forward_graph();
+  void build_backward_graph();
+  void run_graph(cudaGraphExec_t exec, cudaGraphExec_t body_exec, const char* what, int loop_cap);
+  void sync_ctl();
+  void check_ctl(const char* what);
+
+  const Scene& scene_;
+  Material mat_;
+  HostFactor hf_;
+  cudaStream_t st_ = nullptr;
+  std::unique_ptr<DevArena> mem_;      // mesh/material/state/work
+  std::unique_ptr<DevArena> fmem_;     // factor (rebuilt on refresh)
+  bool use_cond_ = true;
+  double time_ = 0;
+
+  // device views
+  hdk_mesh dm_{};
+  hdk_material dmat_{};
+  hdk_factor df_{};
+  hdk_vtx dv_{};
+  hdk_csr a_ff_{}, a_fd_{}, a_df_{};
+  int* d_fixed_ = nullptr;
+
+  // state / work buffers (3 nv doubles unless noted)
+  double *q_ = nullptr, *v_ = nullptr, *fext_ = nullptr;
+  double *qtil_ = nullptr, *qcur_ = nullptr, *qprev_ = nullptr, *qhat_ = nullptr, *bprev_ = nullptr, *damp_ = nullptr;
+  double *rhs_ = nullptr, *fixc_ = nullptr;  // 3 n
+  double *ef_ = nullptr, *ef2_ = nullptr;    // 12 ne
+  double *lastq_ = nullptr, *lastg_ = nullptr, *dq_ = nullptr, *dg_ = nullptr;  // dq/dg: 8 x 3 nv
+  double *part_a_ = nullptr, *part_b_ = nullptr, *part_c_ = nullptr;
+  double* cache_ = nullptr;  // 24 ne projection cache of the current step
+  hdk_ctl* ctl_ = nullptr;
+  hdk_ctl* h_ctl_ = nullptr;  // pinned mirror
+  double* hook_ = nullptr;    // 5 doubles device
+
+  // backward work
+  double *seed_ = nullptr, *x_ = nullptr, *t_ = nullptr, *mu_ = nullptr, *bmu_ = nullptr, *dcomp_ = nullptr;
+  double *qbar_ = nullptr, *vbar_ = nullptr, *dlq_ = nullptr, *dlv_ = nullptr, *dfacc_ = nullptr, *coup_ = nullptr;
+  double *dlw_ = nullptr, *dle_ = nullptr, *eprev_ = nullptr, *estar_ = nullptr, *dqp_ = nullptr, *direct_ = nullptr;
+  // working copy of one recorded frame for the backward graph
+  double *bq_t_ = nullptr, *bv_t_ = nullptr, *bqtil_ = nullptr, *bqprev_ = nullptr, *bqstar_ = nullptr, *bcache_ = nullptr;
+
+  struct Frame {
+    double *q_t, *v_t, *qtil, *qprev, *qstar, *cache;
+  };
+  std::vector<Frame> slots_;  // device storage of recorded frames (reused)
+  std::vector<std::unique_ptr<DevArena>> frame_mem_;
+  int nrec_ = 0;
+  bool recording_ = false;
+  int aa_window_ = 1;
+
+  cudaGraph_t fg_ = nullptr, bg_ = nullptr, fbody_ = nullptr, bbody_ = nullptr;
+  cudaGraphExec_t fexec_ = nullptr, bexec_ = nullptr, fbody_exec_ = nullptr, bbody_exec_ = nullptr;
+};
+
+}  // namespace hdb

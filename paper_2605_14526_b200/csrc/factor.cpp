@@ -1,0 +1,469 @@
+// Explicit inverse factor for the B200 global solve (host build, once per
+// material/topology/Dirichlet change — reference GlobalSystem::refresh and
+// SparseFactor::factorize, factor.cpp:11-104, 121-184).
+//
+//   A = (1 + alpha h) M / h^2 + sum_e (w_e + beta_e / h) V_e g g^T  (scalar, per axis)
+//   P A_ff P^T = L D L^T,  S' = D^{-1/2} L^{-1},  A_ff^{-1} = P^T S'^T S' P.
+//
+// B200-first choices (same operator, different layout):
+//  * ordering "nd-geometric" (default): nested dissection by coordinate
+//    bisection of the rest shape — planar separators on hex-derived meshes,
+//    markedly less fill than the reference's BFS-level dissection
+//    ("nd-bfs", ordering.cpp:73-144, also available);
+//  * the elimination order is postordered, so every row of S' is dense over a
+//    contiguous column range (its etree subtree) and is stored without column
+//    indices;
+//  * rows are cut into column-tile segments grouped into balanced work units
+//    for the two streaming passes (solve.cu).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <numeric>
+#include <set>
+#include <thread>
+
+#include "host.hpp"
+
+namespace hdb {
+
+namespace {
+
+int hw_threads() {
+  int n = static_cast<int>(std::thread::hardware_concurrency());
+  return std::max(1, std::min(n, 64));
+}
+
+template <class F>
+void parallel_chunks(int n, F&& fn) {
+  const int w = std::min(hw_threads(), std::max(1, n / 64));
+  if (w <= 1) {
+    fn(0, n, 0);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < w; ++t) {
+    const int lo = static_cast<int>(static_cast<long long>(n) * t / w), hi = static_cast<int>(static_cast<long long>(n) * (t + 1) / w);
+    pool.emplace_back([&fn, lo, hi, t] { fn(lo, hi, t); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+// Scalar operator over all vertices; duplicates summed in sorted order and
+// exact zeros dropped (csr.cpp:7-32), so the graph matches the reference's.
+Csr assemble(const Mesh& m, const Material& mat, double h) {
+  if (!(h > 0)) raise(Code::Validation, "step size must be positive");
+  struct T { int r, c; double v; };
+  std::vector<T> t;
+  t.reserve(m.nv + 16 * static_cast<size_t>(m.ne));
+  const double inertia = (1.0 + mat.alpha * h) / (h * h);
+  for (int v = 0; v < m.nv; ++v) t.push_back({v, v, inertia * m.mass[v]});
+  for (int e = 0; e < m.ne; ++e) {
+    const double w = (mat.weight(e) + mat.beta[e] / h) * m.vol[e];
+    const double* b = &m.bm[9 * static_cast<size_t>(e)];
+    double g[4][3];
+    for (int c = 0; c < 3; ++c) {
+      g[1][c] = b[0 * 3 + c];
+      g[2][c] = b[1 * 3 + c];
+      g[3][c] = b[2 * 3 + c];
+      g[0][c] = -(g[1][c] + g[2][c] + g[3][c]);
+    }
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j)
+        t.push_back({m.el[e][i], m.el[e][j], w * (g[i][0] * g[j][0] + g[i][1] * g[j][1] + g[i][2] * g[j][2])});
+  }
+  std::sort(t.begin(), t.end(), [](const T& a, const T& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; });
+  Csr a;
+  a.rows = a.cols = m.nv;
+  a.off.assign(m.nv + 1, 0);
+  for (size_t i = 0; i < t.size();) {
+    const int r = t[i].r, c = t[i].c;
+    double s = 0;
+    while (i < t.size() && t[i].r == r && t[i].c == c) s += t[i++].v;
+    if (s != 0.0) {
+      a.col.push_back(c);
+      a.val.push_back(s);
+      ++a.off[r + 1];
+    }
+  }
+  for (int r = 0; r < m.nv; ++r) a.off[r + 1] += a.off[r];
+  return a;
+}
+
+// ---- orderings ---------------------------------------------------------------
+using Graph = std::vector<std::vector<int>>;
+
+// Nested dissection by recursive coordinate bisection.  The separator is the
+// set of upper-half vertices adjacent to the lower half, which is a grid
+// plane when the median falls on one.
+void nd_geometric(const Graph& g, const std::vector<P3>& x, std::vector<int> blk, std::vector<int>& out,
+                  std::vector<char>& side) {
+  if (blk.size() <= 64) {
+    std::sort(blk.begin(), blk.end());
+    out.insert(out.end(), blk.begin(), blk.end());
+    return;
+  }
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int v : blk) {
+    const double c[3] = {x[v].x, x[v].y, x[v].z};
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], c[a]);
+      hi[a] = std::max(hi[a], c[a]);
+    }
+  }
+  int axes[3] = {0, 1, 2};
+  std::sort(axes, axes + 3, [&](int a, int b) { return hi[a] - lo[a] > hi[b] - lo[b]; });
+  auto coord = [&](int v, int a) { return a == 0 ? x[v].x : a == 1 ? x[v].y : x[v].z; };
+  for (int ai = 0; ai < 3; ++ai) {
+    const int a = axes[ai];
+    if (!(hi[a] > lo[a])) break;
+    std::vector<double> cs(blk.size());
+    for (size_t i = 0; i < blk.size(); ++i) cs[i] = coord(blk[i], a);
+    std::nth_element(cs.begin(), cs.begin() + cs.size() / 2, cs.end());
+    double med = cs[cs.size() / 2];
+    if (med <= lo[a]) {  // keep both sides nonempty
+      double next = 1e300;
+      for (double c : cs)
+        if (c > lo[a]) next = std::min(next, c);
+      med = next;
+    }
+    std::vector<int> left, right, sep;
+    for (int v : blk) side[v] = coord(v, a) < med ? 1 : 2;
+    for (int v : blk) {
+      if (side[v] == 1) {
+        left.push_back(v);
+        continue;
+      }
+      bool touches = false;
+      for (int w : g[v])
+        if (side[w] == 1) { touches = true; break; }
+      (touches ? sep : right).push_back(v);
+    }
+    for (int v : blk) side[v] = 0;
+    if (left.empty() || (right.empty() && sep.size() == blk.size())) continue;
+    nd_geometric(g, x, std::move(left), out, side);
+    nd_geometric(g, x, std::move(right), out, side);
+    std::sort(sep.begin(), sep.end());
+    out.insert(out.end(), sep.begin(), sep.end());
+    return;
+  }
+  std::sort(blk.begin(), blk.end());
+  out.insert(out.end(), blk.begin(), blk.end());
+}
+
+// Nested dissection by BFS level bisection (the reference's scheme,
+// ordering.cpp:73-156) with natural order on leaves and separators.
+void nd_bfs(const Graph& g, std::vector<int> blk, std::vector<int>& out, std::vector<int>& level,
+            std::vector<char>& mark) {
+  if (blk.size() <= 48) {
+    std::sort(blk.begin(), blk.end());
+    out.insert(out.end(), blk.begin(), blk.end());
+    return;
+  }
+  for (int v : blk) mark[v] = 1;
+  auto bfs = [&](int root, std::vector<int>& order) {
+    for (int v : blk) level[v] = -1;
+    order.clear();
+    order.push_back(root);
+    level[root] = 0;
+    for (size_t h = 0; h < order.size(); ++h)
+      for (int w : g[order[h]])
+        if (mark[w] && level[w] < 0) {
+          level[w] = level[order[h]] + 1;
+          order.push_back(w);
+        }
+  };
+  std::vector<int> order;
+  bfs(blk.front(), order);
+  if (order.size() < blk.size()) {
+    std::vector<int> rest;
+    for (int v : blk)
+      if (level[v] < 0) rest.push_back(v);
+    for (int v : blk) mark[v] = 0;
+    nd_bfs(g, order, out, level, mark);
+    nd_bfs(g, rest, out, level, mark);
+    return;
+  }
+  int root = blk.front();
+  for (int s = 0; s < 2; ++s) {
+    bfs(root, order);
+    root = order.back();
+  }
+  bfs(root, order);
+  int maxl = 0;
+  for (int v : blk) maxl = std::max(maxl, level[v]);
+  for (int v : blk) mark[v] = 0;
+  if (maxl < 2) {
+    std::sort(blk.begin(), blk.end());
+    out.insert(out.end(), blk.begin(), blk.end());
+    return;
+  }
+  std::vector<int> cnt(maxl + 1, 0);
+  for (int v : blk) ++cnt[level[v]];
+  int split = 0, cum = 0;
+  while (split < maxl && cum + cnt[split] < static_cast<int>(blk.size()) / 2) cum += cnt[split++];
+  split = std::min(std::max(split, 1), maxl - 1);
+  std::vector<int> l, r, s;
+  for (int v : blk) (level[v] < split ? l : level[v] > split ? r : s).push_back(v);
+  nd_bfs(g, std::move(l), out, level, mark);
+  nd_bfs(g, std::move(r), out, level, mark);
+  std::sort(s.begin(), s.end());
+  out.insert(out.end(), s.begin(), s.end());
+}
+
+}  // namespace
+
+HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const std::vector<int>& fixed,
+                        const std::string& ordering) {
+  const auto t0 = std::chrono::steady_clock::now();
+  HostFactor F;
+  F.nv = mesh.nv;
+  F.fixed = fixed;
+  F.ordering = ordering;
+  F.weight_contrast = mat.contrast();
+  std::vector<char> is_fixed(mesh.nv, 0);
+  for (int v : fixed) is_fixed[v] = 1;
+  std::vector<int> freev;
+  for (int v = 0; v < mesh.nv; ++v)
+    if (!is_fixed[v]) freev.push_back(v);
+  const int n = static_cast<int>(freev.size());
+  if (n == 0) raise(Code::Validation, "all vertices are constrained");
+  F.n = n;
+  std::vector<int> v2f(mesh.nv, -1), fixed_idx(mesh.nv, -1);
+  for (int i = 0; i < n; ++i) v2f[freev[i]] = i;
+  for (size_t i = 0; i < fixed.size(); ++i) fixed_idx[fixed[i]] = static_cast<int>(i);
+
+  const Csr A = assemble(mesh, mat, h);
+  // Free-free graph (free index space).
+  Graph g(n);
+  for (int i = 0; i < n; ++i) {
+    const int v = freev[i];
+    for (int k = A.off[v]; k < A.off[v + 1]; ++k) {
+      const int w = v2f[A.col[k]];
+      if (w >= 0 && w != i) g[i].push_back(w);
+    }
+  }
+  // 1. fill-reducing order (free index space)
+  std::vector<int> order;
+  order.reserve(n);
+  {
+    std::vector<int> all(n);
+    std::iota(all.begin(), all.end(), 0);
+    if (ordering == "nd-bfs") {
+      std::vector<int> level(n, -1);
+      std::vector<char> mark(n, 0);
+      nd_bfs(g, all, order, level, mark);
+    } else {
+      std::vector<P3> x(n);
+      for (int i = 0; i < n; ++i) x[i] = {mesh.rest[3 * freev[i]], mesh.rest[3 * freev[i] + 1], mesh.rest[3 * freev[i] + 2]};
+      std::vector<char> side(n, 0);
+      nd_geometric(g, x, all, order, side);
+    }
+  }
+  std::vector<int> pos(n);
+  for (int p = 0; p < n; ++p) pos[order[p]] = p;
+  // 2. elimination tree of the ordered matrix (Liu, with path compression)
+  auto etree = [&](const std::vector<int>& ps, std::vector<int>& parent) {
+    std::vector<int> anc(n, -1);
+    parent.assign(n, -1);
+    std::vector<std::vector<int>> lower(n);  // row k: columns j < k
+    for (int i = 0; i < n; ++i)
+      for (int w : g[i]) {
+        const int r = ps[i], c = ps[w];
+        if (c < r) lower[r].push_back(c);
+      }
+    for (int k = 0; k < n; ++k)
+      for (int j : lower[k]) {
+        int i = j;
+        while (i != -1 && i < k) {
+          const int nxt = anc[i];
+          anc[i] = k;
+          if (nxt == -1) { parent[i] = k; break; }
+          i = nxt;
+        }
+      }
+  };
+  std::vector<int> parent;
+  etree(pos, parent);
+  // 3. postorder (children in ascending order), composed into the ordering
+  {
+    std::vector<int> head(n, -1), next(n, -1);
+    for (int j = n - 1; j >= 0; --j)
+      if (parent[j] >= 0) {
+        next[j] = head[parent[j]];
+        head[parent[j]] = j;
+      }
+    std::vector<int> post(n), stack;
+    int k = 0;
+    for (int r = 0; r < n; ++r) {
+      if (parent[r] != -1) continue;
+      stack.push_back(r);
+      while (!stack.empty()) {
+        const int p = stack.back();
+        const int c = head[p];
+        if (c == -1) {
+          stack.pop_back();
+          post[k++] = p;
+        } else {
+          head[p] = next[c];
+          stack.push_back(c);
+        }
+      }
+    }
+    std::vector<int> newpos(n);  // old position -> postorder position
+    for (int i = 0; i < n; ++i) newpos[post[i]] = i;
+    for (int i = 0; i < n; ++i) pos[i] = newpos[pos[i]];
+  }
+  etree(pos, parent);
+  // subtree sizes -> row ranges of S'
+  std::vector<int> sz(n, 1);
+  for (int j = 0; j < n; ++j)
+    if (parent[j] >= 0) sz[parent[j]] += sz[j];
+  for (int j = 0; j < n; ++j)
+    if (j - sz[j] + 1 < 0) raise(Code::NotPositiveDefinite, "factor: elimination order is not a postorder");
+  F.p2v.assign(n, -1);
+  F.v2p.assign(mesh.nv, -1);
+  for (int i = 0; i < n; ++i) {
+    F.p2v[pos[i]] = freev[i];
+    F.v2p[freev[i]] = pos[i];
+  }
+  // 4. permuted matrix rows (lower triangle incl. diagonal) and LDL^T (up-looking)
+  std::vector<std::vector<std::pair<int, double>>> rowl(n);
+  for (int i = 0; i < n; ++i) {
+    const int v = freev[i], r = pos[i];
+    for (int k = A.off[v]; k < A.off[v + 1]; ++k) {
+      const int w = v2f[A.col[k]];
+      if (w < 0) continue;
+      const int c = pos[w];
+      if (c <= r) rowl[r].push_back({c, A.val[k]});
+    }
+    std::sort(rowl[r].begin(), rowl[r].end());
+  }
+  std::vector<int> cnt(n, 0), flag(n, -1);
+  for (int k = 0; k < n; ++k) {
+    flag[k] = k;
+    for (const auto& [j0, val] : rowl[k])
+      for (int i = j0; i < k && flag[i] != k; i = parent[i]) {
+        ++cnt[i];
+        flag[i] = k;
+      }
+  }
+  std::vector<long long> lp(n + 1, 0);
+  for (int j = 0; j < n; ++j) lp[j + 1] = lp[j] + cnt[j];
+  F.l_nnz = lp[n];
+  std::vector<int> li(static_cast<size_t>(lp[n]));
+  Vec lx(static_cast<size_t>(lp[n])), d(n), y(n, 0.0);
+  std::vector<int> pattern(n), fill(n, 0);
+  for (int k = 0; k < n; ++k) {
+    int top = n;
+    flag[k] = k;
+    y[k] = 0.0;
+    for (const auto& [j0, val] : rowl[k]) {
+      y[j0] += val;
+      int len = 0;
+      for (int i = j0; flag[i] != k; i = parent[i]) {
+        pattern[len++] = i;
+        flag[i] = k;
+      }
+      while (len > 0) pattern[--top] = pattern[--len];
+    }
+    double dk = y[k];
+    y[k] = 0.0;
+    for (; top < n; ++top) {
+      const int i = pattern[top];
+      const double yi = y[i];
+      y[i] = 0.0;
+      const long long end = lp[i] + fill[i];
+      for (long long p = lp[i]; p < end; ++p) y[li[p]] -= lx[p] * yi;
+      const double l = yi / d[i];
+      dk -= l * yi;
+      li[end] = k;
+      lx[end] = l;
+      ++fill[i];
+    }
+    if (!(dk > 0.0))
+      raise(Code::NotPositiveDefinite, "non-positive pivot " + std::to_string(dk) + " at position " + std::to_string(k));
+    d[k] = dk;
+  }
+  // 5. S' rows: column c of L^{-1} lives on c's ancestor path; every entry of
+  //    L(:, v) for v on that path is also on it, so a dense scratch suffices.
+  F.row_len = sz;
+  F.row_off.assign(n + 1, 0);
+  for (int r = 0; r < n; ++r) F.row_off[r + 1] = F.row_off[r] + sz[r];
+  F.sval.assign(static_cast<size_t>(F.row_off[n]), 0.0);
+  Vec dis(n);
+  for (int i = 0; i < n; ++i) dis[i] = 1.0 / std::sqrt(d[i]);
+  parallel_chunks(n, [&](int lo, int hi, int) {
+    Vec work(n, 0.0);
+    for (int c = lo; c < hi; ++c) {
+      work[c] = 1.0;
+      for (int v = c; v >= 0; v = parent[v]) {
+        const double xv = work[v];
+        work[v] = 0.0;
+        if (xv != 0.0)
+          for (long long p = lp[v]; p < lp[v + 1]; ++p) work[li[p]] -= lx[p] * xv;
+        F.sval[static_cast<size_t>(F.row_off[v] + (c - (v - sz[v] + 1)))] = xv * dis[v];
+      }
+    }
+  });
+  // 6. segments / work units
+  const int W = F.tile_w;
+  const int ntiles = (n + W - 1) / W;
+  F.row_pslot.assign(n + 1, 0);
+  std::vector<std::vector<Segment>> per_tile(ntiles);
+  for (int r = 0; r < n; ++r) {
+    const int first = r - sz[r] + 1;
+    const int t0 = first / W, t1 = r / W;
+    F.row_pslot[r + 1] = F.row_pslot[r] + (t1 - t0 + 1);
+    for (int t = t0; t <= t1; ++t) {
+      const int clo = std::max(first, t * W), chi = std::min(r, t * W + W - 1);
+      per_tile[t].push_back({F.row_off[r] + (clo - first), r, clo, chi - clo + 1, F.row_pslot[r] + (t - t0)});
+    }
+  }
+  const long long target = std::max<long long>(8192, F.row_off[n] / (148LL * 4));
+  F.tile_unit.assign(ntiles + 1, 0);
+  F.unit_seg.push_back(0);
+  for (int t = 0; t < ntiles; ++t) {
+    long long acc = 0;
+    int since = 0;
+    for (const Segment& s : per_tile[t]) {
+      F.seg.push_back(s);
+      acc += s.len;
+      ++since;
+      if (acc >= target) {
+        F.unit_seg.push_back(static_cast<int>(F.seg.size()));
+        F.unit_tile.push_back(t);
+        acc = 0;
+        since = 0;
+      }
+    }
+    if (since > 0) {
+      F.unit_seg.push_back(static_cast<int>(F.seg.size()));
+      F.unit_tile.push_back(t);
+    }
+    F.tile_unit[t + 1] = static_cast<int>(F.unit_tile.size());
+  }
+  // 7. A_ff and A_fd in elimination order (apply_a_free / fixed coupling)
+  F.a_ff.rows = F.a_ff.cols = n;
+  F.a_ff.off.assign(n + 1, 0);
+  F.a_fd.rows = n;
+  F.a_fd.cols = static_cast<int>(fixed.size());
+  F.a_fd.off.assign(n + 1, 0);
+  for (int p = 0; p < n; ++p) {
+    const int v = F.p2v[p];
+    std::vector<std::pair<int, double>> ff, fd;
+    for (int k = A.off[v]; k < A.off[v + 1]; ++k) {
+      const int w = A.col[k];
+      if (F.v2p[w] >= 0) ff.push_back({F.v2p[w], A.val[k]});
+      else fd.push_back({fixed_idx[w], A.val[k]});
+    }
+    std::sort(ff.begin(), ff.end());
+    for (auto& [c, val] : ff) { F.a_ff.col.push_back(c); F.a_ff.val.push_back(val); }
+    for (auto& [c, val] : fd) { F.a_fd.col.push_back(c); F.a_fd.val.push_back(val); }
+    F.a_ff.off[p + 1] = static_cast<int>(F.a_ff.col.size());
+    F.a_fd.off[p + 1] = static_cast<int>(F.a_fd.col.size());
+  }
+  F.millis = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return F;
+}
+
+}  // namespace hdb

@@ -1,0 +1,131 @@
+// heterodyn-b200 host library: scene/mesh/material setup, the explicit inverse
+// factor build, and the device-resident forward/backward engine.  This is the
+// product's C++ solver API (the reference's is in /root/reference/proj/src
+// mesh.hpp, material.hpp, factor.hpp, forward.hpp, backward.hpp); the hot
+// path runs on sm_100a through the hdk_* launchers (include/hdk.h).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace hdb {
+
+// common.hpp:19-45 numbering (identical to hd_status).
+enum class Code : int {
+  Ok = 0, Parse = 1, Validation = 2, DegenerateElement = 3, InvalidPoisson = 4, NonPositiveJacobian = 5,
+  ProxDiverged = 6, SingularFilteredHessian = 7, NotPositiveDefinite = 8, SingularContactSystem = 9,
+  AdjointDiverged = 10, LineSearchFailed = 11, Io = 12, InvalidArgument = 13,
+};
+struct Error : std::runtime_error {
+  Code code;
+  Error(Code c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void raise(Code c, const std::string& m) { throw Error(c, m); }
+
+using Vec = std::vector<double>;
+struct P3 { double x = 0, y = 0, z = 0; };
+
+// Tetrahedral mesh (mesh.hpp:16-60).  bm holds Dm^{-1} row-major per element.
+struct Mesh {
+  int nv = 0, ne = 0;
+  Vec rest;                             // 3 nv
+  std::vector<std::array<int, 4>> el;   // ne
+  Vec bm;                               // 9 ne
+  Vec vol;                              // ne
+  Vec mass;                             // nv (per vertex; every axis equal)
+  std::vector<int> boundary;
+  std::uint64_t topology = 0;
+  double total_volume = 0;
+};
+Mesh make_mesh(const Vec& rest, const std::vector<std::array<int, 4>>& el, double density);
+Mesh hex_grid(int nx, int ny, int nz, double spacing, double density);
+
+enum class Kind { Corotated = 0, NeoHookean = 1 };
+// Heterogeneous material field (material.hpp:60-90).
+struct Material {
+  Kind kind = Kind::NeoHookean;
+  bool barrier = false;
+  double poisson = 0, alpha = 0, beta0 = 0;
+  Vec young, mu, lambda, beta;
+  double mu_bar = 0, lambda_bar = 0, k_bar = 0;
+  bool frozen = false;
+  std::uint64_t version = 0;
+  double weight(int e) const { return 2.0 * mu[e] + lambda[e]; }
+  double contrast() const;
+  void set_young(const Vec& y, const Vec& vol);
+  void freeze();
+};
+Material make_material(const Mesh& m, const Vec& young, double poisson, Kind kind, bool barrier, double alpha,
+                       double beta0);
+
+struct Obstacle {  // contact.hpp:18-26
+  int kind = 0;    // 0 half-space, 1 sphere
+  P3 normal{0, 1, 0};
+  double offset = 0;
+  P3 center;
+  double radius = 1, friction = 0;
+};
+
+struct Solver {  // forward.hpp:19-27
+  double h = 0.01, eps_rel = 1e-4, eps_abs = 1e-9;
+  int k_max = 500;
+  double eps_tr = 0.1;
+  int aa_window = 0;
+  double contact_margin = 1e-4;
+};
+
+struct Scene {  // scene.hpp:14-34
+  std::string name;
+  Mesh mesh;
+  Material material;
+  std::vector<int> fixed;
+  std::vector<Obstacle> obstacles;
+  P3 gravity;
+  Vec f_extra;
+  bool hook = false;
+  int hook_vertex = -1;
+  P3 hook_anchor;
+  double hook_k = 0, hook_d = 0;
+  Solver solver;
+  int frames = 1;
+  Vec q0, v0;
+  std::vector<int> region;
+  int region_count = 0;
+  std::string ordering = "nd-bfs";  // B200 extension: fill-reducing ordering of the factor
+};
+Scene parse_scene(const std::string& text);
+Scene builtin_scene(const std::string& name);
+Vec external_force(const Scene& s);  // gravity lumped + point forces (scene.cpp:530-540)
+
+// Scalar CSR (rows in elimination order).
+struct Csr {
+  int rows = 0, cols = 0;
+  std::vector<int> off, col;
+  Vec val;
+};
+
+// Explicit inverse factor A_ff^{-1} = S'^T S' (see hdk.h for the layout).
+struct Segment { long long off; int row, clo, len, pslot; };
+struct HostFactor {
+  int n = 0, nv = 0;
+  std::vector<int> p2v, v2p, fixed;
+  std::vector<long long> row_off;
+  std::vector<int> row_len;
+  Vec sval;
+  int tile_w = 256;
+  std::vector<Segment> seg;
+  std::vector<int> unit_seg, unit_tile, tile_unit, row_pslot;
+  Csr a_ff;  // free x free, elimination order
+  Csr a_fd;  // free rows (elimination order) x fixed columns (index into fixed)
+  long long l_nnz = 0;
+  double millis = 0;
+  std::string ordering;
+  double weight_contrast = 1;
+};
+HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const std::vector<int>& fixed,
+                        const std::string& ordering);
+
+}  // namespace hdb

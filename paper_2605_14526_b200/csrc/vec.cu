@@ -1,0 +1,612 @@
+// Vertex- and DoF-parallel kernels of the PD loop: fixed-order element-force
+// gathers (the serial scatters of pd_rhs/damping_rhs, forward.cpp:96-138),
+// Type-II Anderson mixing with its small coefficient solve (forward.cpp:17-51),
+// the dual gate (forward.cpp:140-146), the trust-region ratio
+// (backward.cpp:75-108) and the vertex part of route_gradients
+// (backward.cpp:296-356).
+//
+// Reductions: every reducing kernel runs a fixed grid of HDK_RED_BLOCKS x 256
+// threads with grid-stride loops and writes one partial per block; a
+// single-block kernel folds the partials in a fixed tree.  Results are
+// bitwise reproducible run to run (no atomics on doubles).
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "../../include/hdk.h"
+
+namespace {
+
+constexpr int kT = 256;
+
+template <int NQ>
+__device__ __forceinline__ void block_partials(double (&v)[NQ], double* partial) {
+  __shared__ double sm[kT / 32][NQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double x = v[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) sm[warp][q] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NQ) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) s += sm[w][threadIdx.x];
+    partial[blockIdx.x * HDK_RED_Q + threadIdx.x] = s;
+  }
+}
+
+// Single-block fold of partial slot q over all blocks (fixed order).
+__device__ __forceinline__ double fold(const double* partial, int q) {
+  __shared__ double sm[kT / 32];
+  double s = 0.0;
+  for (int b = threadIdx.x; b < HDK_RED_BLOCKS; b += kT) s += partial[b * HDK_RED_Q + q];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < kT / 32; ++w) t += sm[w];
+  return t;  // valid in every thread
+}
+
+__device__ __forceinline__ double gather3(const hdk_vtx& x, const double* __restrict__ ef, int v, int a) {
+  double acc = 0.0;
+  const int e = x.inc_off[v + 1];
+  for (int j = x.inc_off[v]; j < e; ++j) acc += ef[3 * (size_t)x.inc[j] + a];
+  return acc;
+}
+
+__global__ void k_free_fall(hdk_vtx x, const double* q, const double* v, const double* f, double h, int hv,
+                            double ax, double ay, double az, double hk, double hd, double* qt, double* qc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * x.nv) return;
+  const int vtx = i / 3, a = i - 3 * vtx;
+  double force = f[i];
+  if (vtx == hv) {
+    const double anc = a == 0 ? ax : a == 1 ? ay : az;
+    force += -hk * (q[i] - anc) - hd * v[i];
+  }
+  const double t = q[i] + h * v[i] + (h * h) * (force / x.mass[vtx]);
+  qt[i] = t;
+  qc[i] = x.v2p[vtx] < 0 ? q[i] : t;
+}
+
+__global__ void k_gather(hdk_vtx x, const double* ef, double cm, const double* base, const double* add, double* out) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= x.nv) return;
+  for (int a = 0; a < 3; ++a) {
+    double s = cm * x.mass[v] * base[3 * v + a];
+    if (add) s += add[3 * v + a];
+    if (ef) s += gather3(x, ef, v, a);
+    out[3 * v + a] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kT) k_gather_rhs(hdk_vtx x, const double* __restrict__ ef, double inv_h2,
+                                                   const double* __restrict__ qt, const double* __restrict__ damp,
+                                                   const double* __restrict__ fixc, double* bprev, double* rhs,
+                                                   double* partial) {
+  double acc[2] = {0.0, 0.0};
+  for (int v = blockIdx.x * kT + threadIdx.x; v < x.nv; v += HDK_RED_BLOCKS * kT) {
+    const int p = x.v2p[v];
+    const double m = x.mass[v];
+    for (int a = 0; a < 3; ++a) {
+      const size_t i = 3 * (size_t)v + a;
+      double b = m * qt[i] * inv_h2;  // M q~ / h^2 (forward.cpp:99)
+      b += gather3(x, ef, v, a);      // + sum_e V G^T (w p*)
+      b += damp[i];                   // + damping_rhs
+      const double d = b - bprev[i];
+      acc[0] += d * d;
+      acc[1] += b * b;
+      bprev[i] = b;
+      if (p >= 0) rhs[3 * (size_t)p + a] = b - (fixc ? fixc[3 * (size_t)p + a] : 0.0);
+    }
+  }
+  block_partials<2>(acc, partial);
+}
+
+__global__ void k_gather_perm(hdk_vtx x, const double* base, const double* ef, double* rhs) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= x.n) return;
+  const int v = x.p2v[p];
+  for (int a = 0; a < 3; ++a) {
+    double s = base[3 * (size_t)v + a];
+    if (ef) s += gather3(x, ef, v, a);
+    rhs[3 * (size_t)p + a] = s;
+  }
+}
+
+__global__ void k_fixed_coupling(hdk_csr c, const int* fixed, const double* q, double* out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= c.rows) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int k = c.off[p]; k < c.off[p + 1]; ++k) {
+    const double w = c.val[k];
+    const int v = fixed[c.col[k]];
+    s0 += w * q[3 * (size_t)v];
+    s1 += w * q[3 * (size_t)v + 1];
+    s2 += w * q[3 * (size_t)v + 2];
+  }
+  out[3 * (size_t)p] = s0;
+  out[3 * (size_t)p + 1] = s1;
+  out[3 * (size_t)p + 2] = s2;
+}
+
+// ---- Anderson mixing ---------------------------------------------------------
+__global__ void __launch_bounds__(kT) k_aa_dots(hdk_vtx x, const hdk_ctl* ctl, const double* __restrict__ qhat,
+                                                const double* __restrict__ qcur, double* last_q, double* last_g,
+                                                double* dq, double* dg, double* partial) {
+  const size_t n3 = 3 * (size_t)x.nv;
+  const int m = ctl->window, c = ctl->count, h = ctl->head;
+  const bool push = ctl->has_last != 0;
+  int ns = 0, c2 = c, h2 = h;
+  if (push) {
+    ns = c < m ? (h + c) % m : h;
+    c2 = c < m ? c + 1 : m;
+    h2 = c < m ? h : (h + 1) % m;
+  }
+  double acc[2 * HDK_AA_MAX + 2];
+#pragma unroll
+  for (int q = 0; q < 2 * HDK_AA_MAX + 2; ++q) acc[q] = 0.0;
+  for (size_t i = blockIdx.x * kT + threadIdx.x; i < n3; i += (size_t)HDK_RED_BLOCKS * kT) {
+    const double qc = qcur[i], th = qhat[i];
+    const double g = th - qc;
+    acc[2 * HDK_AA_MAX] += g * g;
+    acc[2 * HDK_AA_MAX + 1] += th * th;
+    if (push) {
+      const double dqn = qc - last_q[i];
+      const double dgn = g - last_g[i];
+      dq[ns * n3 + i] = dqn;
+      dg[ns * n3 + i] = dgn;
+#pragma unroll
+      for (int j = 0; j < HDK_AA_MAX; ++j) {
+        if (j < c2) {
+          const int ph = (h2 + j) % m;
+          const double dgj = ph == ns ? dgn : dg[ph * n3 + i];
+          acc[j] += dgn * dgj;
+          acc[HDK_AA_MAX + j] += dgj * g;
+        }
+      }
+    }
+    last_q[i] = qc;
+    last_g[i] = g;
+  }
+  block_partials<2 * HDK_AA_MAX + 2>(acc, partial);
+}
+
+// Solves M gamma = DG^T g, M = DG^T DG + 1e-6 |DG|_F^2 / window I, by LDL^T with
+// diagonal pivoting (Eigen::LDLT).  Returns false on a zero pivot.
+__device__ bool small_ldlt(double* a, int n, const double* b, double* x) {
+  int perm[HDK_AA_MAX];
+  double d[HDK_AA_MAX];
+  for (int i = 0; i < n; ++i) perm[i] = i;
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    double best = fabs(a[k * n + k]);
+    for (int i = k + 1; i < n; ++i)
+      if (fabs(a[i * n + i]) > best) { best = fabs(a[i * n + i]); piv = i; }
+    if (piv != k) {
+      const int t = perm[k]; perm[k] = perm[piv]; perm[piv] = t;
+      for (int c = 0; c < n; ++c) { const double s = a[k * n + c]; a[k * n + c] = a[piv * n + c]; a[piv * n + c] = s; }
+      for (int r = 0; r < n; ++r) { const double s = a[r * n + k]; a[r * n + k] = a[r * n + piv]; a[r * n + piv] = s; }
+    }
+    double dk = a[k * n + k];
+    for (int j = 0; j < k; ++j) dk -= a[k * n + j] * a[k * n + j] * d[j];
+    if (!(fabs(dk) > 2.2250738585072014e-308)) return false;
+    d[k] = dk;
+    for (int i = k + 1; i < n; ++i) {
+      double s = a[i * n + k];
+      for (int j = 0; j < k; ++j) s -= a[i * n + j] * a[k * n + j] * d[j];
+      a[i * n + k] = s / dk;
+    }
+  }
+  double y[HDK_AA_MAX];
+  for (int i = 0; i < n; ++i) y[i] = b[perm[i]];
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < i; ++j) y[i] -= a[i * n + j] * y[j];
+  for (int i = 0; i < n; ++i) y[i] /= d[i];
+  for (int i = n - 1; i >= 0; --i)
+    for (int j = i + 1; j < n; ++j) y[i] -= a[j * n + i] * y[j];
+  for (int i = 0; i < n; ++i) x[perm[i]] = y[i];
+  for (int i = 0; i < n; ++i)
+    if (!isfinite(x[i])) return false;
+  return true;
+}
+
+__global__ void __launch_bounds__(kT) k_aa_solve(hdk_ctl* ctl, const double* partial, int mode) {
+  __shared__ double s[2 * HDK_AA_MAX + 2];
+  for (int q = 0; q < 2 * HDK_AA_MAX + 2; ++q) {
+    const double v = fold(partial, q);
+    if (threadIdx.x == 0) s[q] = v;
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  if (mode == 1) {  // adjoint backbone: convergence test before mixing (backward.cpp:191-193)
+    ctl->iterations += 1;
+    const double diff = sqrt(s[2 * HDK_AA_MAX]);
+    const double base = fmax(sqrt(s[2 * HDK_AA_MAX + 1]), 1e-30);
+    ctl->k += 1;
+    if (diff <= ctl->tol * base) {
+      ctl->done = 1;
+      ctl->mixed = 0;
+      return;
+    }
+    if (ctl->k >= ctl->k_max && ctl->err == 0) ctl->err = 10;  // AdjointDiverged (cap)
+  }
+  const int m = ctl->window;
+  if (ctl->has_last) {
+    const int c = ctl->count;
+    if (c < m) {
+      ctl->count = c + 1;
+    } else {
+      ctl->head = (ctl->head + 1) % m;
+      for (int i = 0; i + 1 < m; ++i)
+        for (int j = 0; j + 1 < m; ++j) ctl->gram[i * HDK_AA_MAX + j] = ctl->gram[(i + 1) * HDK_AA_MAX + (j + 1)];
+    }
+    const int c2 = ctl->count, j = c2 - 1;
+    for (int l = 0; l < c2; ++l) ctl->gram[j * HDK_AA_MAX + l] = ctl->gram[l * HDK_AA_MAX + j] = s[l];
+  }
+  ctl->has_last = 1;
+  ctl->mixed = 0;
+  const int c2 = ctl->count;
+  if (c2 == 0) return;
+  double fro2 = 0.0;
+  for (int j = 0; j < c2; ++j) fro2 += ctl->gram[j * HDK_AA_MAX + j];
+  if (!(fro2 > 0.0)) return;
+  double a[HDK_AA_MAX * HDK_AA_MAX], rhs[HDK_AA_MAX], gam[HDK_AA_MAX];
+  for (int i = 0; i < c2; ++i) {
+    for (int j = 0; j < c2; ++j) a[i * c2 + j] = ctl->gram[i * HDK_AA_MAX + j];
+    a[i * c2 + i] += 1e-6 * fro2 / m;
+    rhs[i] = s[HDK_AA_MAX + i];
+  }
+  const bool ok = small_ldlt(a, c2, rhs, gam);
+  double gn = 0.0;
+  for (int i = 0; i < c2; ++i) gn += gam[i] * gam[i];
+  if (!ok || !(sqrt(gn) <= ctl->guard)) {  // guard: discard history (forward.cpp:43-47)
+    ctl->count = 0;
+    ctl->head = 0;
+    ctl->has_last = 0;
+    return;
+  }
+  for (int i = 0; i < c2; ++i) ctl->gamma[i] = gam[i];
+  ctl->mixed = 1;
+}
+
+__global__ void __launch_bounds__(kT) k_aa_mix(hdk_vtx x, hdk_ctl* ctl, const double* __restrict__ qhat, double* qcur,
+                                               double* qprev, const double* __restrict__ qpin,
+                                               const double* __restrict__ dq, const double* __restrict__ dg,
+                                               double* partial, int mode) {
+  const size_t n3 = 3 * (size_t)x.nv;
+  const bool done = mode == 1 && ctl->done;
+  const int mixed = ctl->mixed, c = ctl->count, h = ctl->head, m = ctl->window;
+  double gam[HDK_AA_MAX];
+#pragma unroll
+  for (int j = 0; j < HDK_AA_MAX; ++j) gam[j] = j < c ? ctl->gamma[j] : 0.0;
+  double acc[2] = {0.0, 0.0};
+  bool finite = true;
+  for (size_t i = blockIdx.x * kT + threadIdx.x; i < n3; i += (size_t)HDK_RED_BLOCKS * kT) {
+    const double qc = qcur[i], th = qhat[i];
+    double out = qc + (th - qc);
+    if (done) {
+      out = th;
+    } else if (mixed) {
+#pragma unroll
+      for (int j = 0; j < HDK_AA_MAX; ++j)
+        if (j < c) {
+          const int ph = (h + j) % m;
+          out -= gam[j] * (dq[ph * n3 + i] + dg[ph * n3 + i]);
+        }
+    }
+    if (mode == 0) {
+      if (x.v2p[i / 3] < 0) out = qpin[i];
+      const double d = out - qc;
+      acc[0] += d * d;
+      acc[1] += qc * qc;
+      qprev[i] = qc;
+    } else {
+      finite = finite && isfinite(out);
+    }
+    qcur[i] = out;
+  }
+  if (mode == 0) block_partials<2>(acc, partial);
+  else if (!finite) atomicCAS(&ctl->err, 0, 10);
+}
+
+__global__ void __launch_bounds__(kT) k_gate(hdk_ctl* ctl, const double* pb, const double* pq,
+                                             cudaGraphConditionalHandle handle, int use_handle) {
+  const double db = fold(pb, 0), bb = fold(pb, 1), dq = fold(pq, 0), qq = fold(pq, 1);
+  if (threadIdx.x != 0) return;
+  const int k = ctl->k;
+  const double er = ctl->eps_rel, ea = ctl->eps_abs;
+  const bool gate = k >= 1 && sqrt(dq) <= er * sqrt(qq) + ea && sqrt(db) <= er * sqrt(bb) + ea;
+  ctl->k = k + 1;
+  ctl->iterations = k + 1;
+  if (gate) ctl->converged = 1;
+  const int cont = (!gate && k + 1 < ctl->k_max && ctl->err == 0) ? 1 : 0;
+  ctl->cond = cont;
+  if (use_handle) cudaGraphSetConditional(handle, cont);
+}
+
+__global__ void k_bb_cond(hdk_ctl* ctl, cudaGraphConditionalHandle handle, int use_handle) {
+  const int cont = (!ctl->done && ctl->err == 0) ? 1 : 0;
+  ctl->cond = cont;
+  if (use_handle) cudaGraphSetConditional(handle, cont);
+}
+
+// ---- trust-region ratio --------------------------------------------------------
+__global__ void k_tr_dq(hdk_vtx x, const double* qs, const double* qp, double* dq) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= x.n) return;
+  const int v = x.p2v[p];
+  for (int a = 0; a < 3; ++a) dq[3 * (size_t)p + a] = qs[3 * (size_t)v + a] - qp[3 * (size_t)v + a];
+}
+
+__global__ void __launch_bounds__(kT) k_tr_spmv(hdk_csr A, const double* __restrict__ dq, double* partial) {
+  double acc[1] = {0.0};
+  for (int p = blockIdx.x * kT + threadIdx.x; p < A.rows; p += HDK_RED_BLOCKS * kT) {
+    double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+    for (int k = A.off[p]; k < A.off[p + 1]; ++k) {
+      const double w = A.val[k];
+      const double* d = dq + 3 * (size_t)A.col[k];
+      y0 += w * d[0];
+      y1 += w * d[1];
+      y2 += w * d[2];
+    }
+    const double* d = dq + 3 * (size_t)p;
+    acc[0] += d[0] * y0 + d[1] * y1 + d[2] * y2;
+  }
+  block_partials<1>(acc, partial);
+}
+
+__global__ void __launch_bounds__(kT) k_tr_partials(hdk_vtx x, int ne, const double* ep, const double* es,
+                                                    const double* qp, const double* qs, const double* qt,
+                                                    double* partial) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int n = max(ne, x.nv);
+  for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += HDK_RED_BLOCKS * kT) {
+    if (i < ne) {
+      acc[0] += ep[i];
+      acc[1] += es[i];
+    }
+    if (i < x.nv && x.v2p[i] >= 0) {
+      const double m = x.mass[i];
+      for (int a = 0; a < 3; ++a) {
+        const size_t j = 3 * (size_t)i + a;
+        const double d0 = qp[j] - qt[j], d1 = qs[j] - qt[j];
+        acc[2] += d0 * m * d0;
+        acc[3] += d1 * m * d1;
+      }
+    }
+  }
+  block_partials<4>(acc, partial);
+}
+
+__global__ void __launch_bounds__(kT) k_tr_final(hdk_ctl* ctl, const double* pm, const double* pe, double inv_h2) {
+  const double model_raw = fold(pm, 0);
+  const double e_prev = fold(pe, 0), e_star = fold(pe, 1), i_prev = fold(pe, 2), i_star = fold(pe, 3);
+  if (threadIdx.x != 0) return;
+  const double model = 0.5 * fabs(model_raw);
+  double rho = 1.0;
+  if (model >= 1e-12) {
+    if (ctl->bad != 0) {
+      rho = INFINITY;
+    } else {
+      const double phi_prev = 0.5 * inv_h2 * i_prev + e_prev;
+      const double phi_star = 0.5 * inv_h2 * i_star + e_star;
+      rho = (phi_prev - phi_star) / model;
+    }
+  }
+  ctl->model = model;
+  ctl->rho = rho;
+  ctl->tau = fabs(rho - 1.0) <= ctl->eps_tr ? 0.5 : 1.0;
+}
+
+// ---- gradient routing ------------------------------------------------------------
+__global__ void k_route_vtx(hdk_vtx x, const double* mu, const double* efd, const double* bmu, const double* qbar,
+                            const double* vbar, const double* coup, double h, double alpha, int hv, double hk,
+                            double hd, double* dq_t, double* dv_t, double* df_acc) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= x.nv) return;
+  const double m = x.mass[v];
+  const bool fixed = x.v2p[v] < 0;
+  for (int a = 0; a < 3; ++a) {
+    const size_t i = 3 * (size_t)v + a;
+    const double u = mu[i];
+    df_acc[i] += u;                            // dL/df_ext = mu (backward.cpp:303)
+    double dv = m * u / h;                     // M mu / h
+    double damp = 0.0;
+    if (alpha > 0) damp = (alpha / h) * (m * u);
+    if (efd) damp += gather3(x, efd, v, a);
+    double dq = m * u / (h * h) + damp;        // M mu / h^2 + damping_rhs(mu)
+    if (v == hv) {
+      dv += -hd * u;
+      dq += -hk * u;
+    }
+    if (!fixed) {
+      dq -= vbar[i] / h;
+    } else {
+      dq += qbar[i];
+      if (bmu) dq += bmu[i];
+      if (coup) dq -= coup[i];
+    }
+    dq_t[i] = dq;
+    dv_t[i] = dv;
+  }
+}
+
+__global__ void k_fixed_coupling_t(hdk_csr c, const int* fixed, const int* p2v, const double* mu, double* coup) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= c.rows) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int j = c.off[k]; j < c.off[k + 1]; ++j) {
+    const double w = c.val[j];
+    const int v = p2v[c.col[j]];
+    s0 += w * mu[3 * (size_t)v];
+    s1 += w * mu[3 * (size_t)v + 1];
+    s2 += w * mu[3 * (size_t)v + 2];
+  }
+  const int v = fixed[k];
+  coup[3 * (size_t)v] = s0;
+  coup[3 * (size_t)v + 1] = s1;
+  coup[3 * (size_t)v + 2] = s2;
+}
+
+__global__ void k_axpby(int n, double a, const double* x, double b, const double* z, double* y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = a * x[i];
+  if (z) s += b * z[i];
+  y[i] = s;
+}
+
+__global__ void k_velocity(int n, const double* qs, const double* qt, double h, double* vs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) vs[i] = (qs[i] - qt[i]) / h;
+}
+
+__global__ void k_ctl_init(hdk_ctl* c, int window, double guard, int k_max, double er, double ea, double tol,
+                           double eps_tr, int it0) {
+  c->k = 0; c->k_max = k_max; c->iterations = it0; c->converged = 0;
+  c->err = 0; c->done = 0; c->bad = 0; c->cond = 1;
+  c->window = window < 1 ? 1 : window; c->count = 0; c->head = 0; c->has_last = 0; c->mixed = 0;
+  c->eps_rel = er; c->eps_abs = ea; c->guard = guard; c->tol = tol;
+  c->tau = 1.0; c->rho = 1.0; c->model = 0.0; c->eps_tr = eps_tr;
+  for (int i = 0; i < HDK_AA_MAX; ++i) c->gamma[i] = 0.0;
+  for (int i = 0; i < HDK_AA_MAX * HDK_AA_MAX; ++i) c->gram[i] = 0.0;
+}
+
+__global__ void k_commit(int n, const hdk_ctl* ctl, const double* qs, double h, double* q, double* v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || ctl->err != 0) return;
+  const double s = qs[i];
+  v[i] = (s - q[i]) / h;
+  q[i] = s;
+}
+
+inline int nb(long long n) { return static_cast<int>((n + 255) / 256); }
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+inline int last() { return static_cast<int>(cudaGetLastError()); }
+
+}  // namespace
+
+extern "C" {
+
+HDK_API int hdk_free_fall(const hdk_vtx* x, const double* q, const double* v, const double* f_ext, double h,
+                          int hook_vertex, const double* hook, double* q_tilde, double* q_cur, void* stream) {
+  const double z[5] = {0, 0, 0, 0, 0};
+  const double* hp = hook ? hook : z;
+  k_free_fall<<<nb(3LL * x->nv), 256, 0, S(stream)>>>(*x, q, v, f_ext, h, hook ? hook_vertex : -1, hp[0], hp[1], hp[2],
+                                                       hp[3], hp[4], q_tilde, q_cur);
+  return last();
+}
+
+HDK_API int hdk_gather(const hdk_vtx* x, const double* ef, double cm, const double* base, const double* add, double* out,
+                       void* stream) {
+  k_gather<<<nb(x->nv), 256, 0, S(stream)>>>(*x, ef, cm, base, add, out);
+  return last();
+}
+
+HDK_API int hdk_gather_rhs(const hdk_vtx* x, const double* ef, double inv_h2, const double* q_tilde, const double* damp,
+                           const double* fixcoup, double* b_prev, double* rhs_perm, double* partial, void* stream) {
+  k_gather_rhs<<<HDK_RED_BLOCKS, kT, 0, S(stream)>>>(*x, ef, inv_h2, q_tilde, damp, fixcoup, b_prev, rhs_perm, partial);
+  return last();
+}
+
+HDK_API int hdk_gather_perm(const hdk_vtx* x, const double* base, const double* ef, double* rhs_perm, void* stream) {
+  k_gather_perm<<<nb(x->n), 256, 0, S(stream)>>>(*x, base, ef, rhs_perm);
+  return last();
+}
+
+HDK_API int hdk_fixed_coupling(const hdk_csr* a_fd, const int* fixed, const double* q, double* fixcoup, void* stream) {
+  k_fixed_coupling<<<nb(a_fd->rows), 256, 0, S(stream)>>>(*a_fd, fixed, q, fixcoup);
+  return last();
+}
+
+HDK_API int hdk_aa_dots(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, const double* qcur, double* last_q,
+                        double* last_g, double* dq, double* dg, double* partial, void* stream) {
+  k_aa_dots<<<HDK_RED_BLOCKS, kT, 0, S(stream)>>>(*x, ctl, qhat, qcur, last_q, last_g, dq, dg, partial);
+  return last();
+}
+
+HDK_API int hdk_aa_solve(hdk_ctl* ctl, const double* partial, int mode, void* stream) {
+  k_aa_solve<<<1, kT, 0, S(stream)>>>(ctl, partial, mode);
+  return last();
+}
+
+HDK_API int hdk_aa_mix(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, double* qcur, double* qprev,
+                       const double* qpin, const double* dq, const double* dg, double* partial, int mode,
+                       void* stream) {
+  k_aa_mix<<<HDK_RED_BLOCKS, kT, 0, S(stream)>>>(*x, ctl, qhat, qcur, qprev, qpin, dq, dg, partial, mode);
+  return last();
+}
+
+HDK_API int hdk_gate(hdk_ctl* ctl, const double* partial_b, const double* partial_q, unsigned long long cond_handle,
+                     void* stream) {
+  k_gate<<<1, kT, 0, S(stream)>>>(ctl, partial_b, partial_q, static_cast<cudaGraphConditionalHandle>(cond_handle),
+                                   cond_handle != 0ULL);
+  return last();
+}
+
+HDK_API int hdk_backbone_cond(hdk_ctl* ctl, unsigned long long cond_handle, void* stream) {
+  k_bb_cond<<<1, 1, 0, S(stream)>>>(ctl, static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle != 0ULL);
+  return last();
+}
+
+HDK_API int hdk_tr_model(const hdk_vtx* x, const hdk_csr* a_ff, const double* q_star, const double* q_prev,
+                         double* dq_perm, double* partial, void* stream) {
+  k_tr_dq<<<nb(x->n), 256, 0, S(stream)>>>(*x, q_star, q_prev, dq_perm);
+  k_tr_spmv<<<HDK_RED_BLOCKS, kT, 0, S(stream)>>>(*a_ff, dq_perm, partial);
+  return last();
+}
+
+HDK_API int hdk_tr_select(const hdk_vtx* x, int ne, const double* e_prev, const double* e_star, const double* q_prev,
+                          const double* q_star, const double* q_tilde, double inv_h2, const double* model_partial,
+                          double* partial, hdk_ctl* ctl, void* stream) {
+  k_tr_partials<<<HDK_RED_BLOCKS, kT, 0, S(stream)>>>(*x, ne, e_prev, e_star, q_prev, q_star, q_tilde, partial);
+  k_tr_final<<<1, kT, 0, S(stream)>>>(ctl, model_partial, partial, inv_h2);
+  return last();
+}
+
+HDK_API int hdk_route_vertices(const hdk_vtx* x, const double* mu, const double* ef_damp, const double* b_mu,
+                               const double* q_bar, const double* v_bar, const double* coup_fixed, double h,
+                               double alpha, int hook_vertex, double hook_k, double hook_d, double* dl_dq_t,
+                               double* dl_dv_t, double* dl_df_acc, void* stream) {
+  k_route_vtx<<<nb(x->nv), 256, 0, S(stream)>>>(*x, mu, ef_damp, b_mu, q_bar, v_bar, coup_fixed, h, alpha, hook_vertex,
+                                                 hook_k, hook_d, dl_dq_t, dl_dv_t, dl_df_acc);
+  return last();
+}
+
+HDK_API int hdk_fixed_coupling_t(const hdk_csr* a_df, const int* fixed, const int* p2v, const double* mu, double* coup,
+                                 void* stream) {
+  k_fixed_coupling_t<<<nb(a_df->rows), 256, 0, S(stream)>>>(*a_df, fixed, p2v, mu, coup);
+  return last();
+}
+
+HDK_API int hdk_axpby(int n, double a, const double* x, double b, const double* z, double* y, void* stream) {
+  k_axpby<<<nb(n), 256, 0, S(stream)>>>(n, a, x, b, z, y);
+  return last();
+}
+
+HDK_API int hdk_velocity(int n, const double* q_star, const double* q_t, double h, double* v_star, void* stream) {
+  k_velocity<<<nb(n), 256, 0, S(stream)>>>(n, q_star, q_t, h, v_star);
+  return last();
+}
+
+HDK_API int hdk_ctl_init(hdk_ctl* ctl, int window, double guard, int k_max, double eps_rel, double eps_abs, double tol,
+                         double eps_tr, int iterations0, void* stream) {
+  k_ctl_init<<<1, 1, 0, S(stream)>>>(ctl, window, guard, k_max, eps_rel, eps_abs, tol, eps_tr, iterations0);
+  return last();
+}
+
+HDK_API int hdk_commit(int n, const hdk_ctl* ctl, const double* q_star, double h, double* q, double* v, void* stream) {
+  k_commit<<<nb(n), 256, 0, S(stream)>>>(n, ctl, q_star, h, q, v);
+  return last();
+}
+
+}  // extern "C"
