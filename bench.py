@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Forward+backward PD timestep throughput on B200 (BASELINE.json metric).
+
+One step = one forward PD timestep (forward_step, reference forward.cpp:148-272)
+plus its adjoint backward step (backward_step, backward.cpp:396-414) for the
+canonical loss L = 1/2|q_T - rest|^2 + 1/2|v_T|^2 (drivers.cpp:384-396),
+on the C3 workload: 103,680-tet heterogeneous (100x stiffness contrast)
+Neo-Hookean crab-like block with Rayleigh damping folded into the factor.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 runs under torchrun as N independent replicas (one trajectory does not
+shard: SURVEY.md §8(e)); the timing is the max over ranks.  The reference arm
+times the CPU restatement of the reference (oracle/, the reference itself
+cannot be built here: Eigen is absent) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+PRODUCT_LIB = os.path.join(HERE, "paper_2605_14526_b200", "_lib", "libheterodyn_b200.so")
+ORACLE_LIB = os.path.join(HERE, "oracle", "_build", "libheterodyn_oracle.so")
+METRIC = "forward+backward PD timesteps/sec at 100k tets"
+UNIT = "steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def pin_device(local_rank: int, world: int):
+    """One process per GPU: narrow visibility before any CUDA runtime starts, so
+    the product library's runtime and torch's agree on the device."""
+    if world <= 1:
+        return
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    ids = [x for x in vis.split(",") if x.strip()] if vis else None
+    os.environ["CUDA_VISIBLE_DEVICES"] = ids[local_rank] if ids else str(local_rank)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", "0", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peak():
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    p = os.path.join(HERE, "profiles", "solve_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("traffic_bytes_per_solve")
+    except Exception:
+        return None
+
+
+def cpu_baseline(scene_dict, q, v, max_seconds=60.0):
+    """Times the CPU restatement (oracle/, port of the reference) on one
+    fwd+bwd step of the same workload from the same state."""
+    from paper_2605_14526_b200.hd import Library
+    lib = Library(ORACLE_LIB)
+    sc = lib.scene(scene_dict)
+    sim = sc.sim()  # factorization: not timed
+    sim.set_state(q, v, 0.0)
+    sim.record(True)
+    t0 = time.perf_counter()
+    sim.step()
+    sim.backward_canonical(download=False)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"1 fwd+bwd step of the same workload from the GPU run's timed-region start state "
+                      f"({dt:.1f} s; forward iterations {sim.last_iterations}; factorization excluded)"}
+
+
+def run_reference(args, scene_dict, world, rank):
+    if rank != 0:
+        return
+    from paper_2605_14526_b200.hd import Library
+    lib = Library(ORACLE_LIB)
+    sc = lib.scene(scene_dict)
+    t_fac = time.perf_counter()
+    sim = sc.sim()
+    t_fac = time.perf_counter() - t_fac
+    budget = 150.0
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
+        sim.record(True)
+        sim.step()
+        sim.backward_canonical(download=False)
+        sim.record(False)
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        sim.record(True)
+        t0 = time.perf_counter()
+        sim.step()
+        sim.backward_canonical(download=False)
+        times.append(time.perf_counter() - t0)
+        sim.record(False)
+        if time.perf_counter() - t_all > budget:
+            break
+    total = sum(times)
+    val = len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": len(times),
+        "warmup": warm, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {scene_dict['name']}", "requested_steps": args.steps,
+                   "factorization_s": t_fac},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{len(times)} fwd+bwd steps (time budget {budget:.0f} s), CPU restatement of the "
+                                   f"reference (Eigen absent: reference not buildable), HETERODYN_THREADS="
+                                   f"{os.environ.get('HETERODYN_THREADS', 'all')}"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    pin_device(local, world)
+    from paper_2605_14526_b200 import scenes
+    scene_dict = scenes.config_scene(args.config)
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo", init_method="env://")
+        run_reference(args, scene_dict, world, rank)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import numpy as np
+    import torch
+    from paper_2605_14526_b200.hd import Library
+    if not os.path.exists(PRODUCT_LIB):
+        raise SystemExit(f"product library missing: {PRODUCT_LIB} (run __graft_entry__.build())")
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", init_method="env://")
+    lib = Library(PRODUCT_LIB)
+    sc = lib.scene(scene_dict)
+    t_fac = time.perf_counter()
+    sim = sc.sim()
+    t_fac = time.perf_counter() - t_fac
+    n = sim.n
+    ne = sc.element_count
+    stream = torch.cuda.ExternalStream(sim.stream)
+
+    def one_step():
+        sim.record(True)
+        sim.step()
+        it_f = sim.last_iterations
+        sim.backward_canonical(download=False)
+        sim.record(False)
+        return it_f
+
+    for _ in range(max(args.warmup, 3)):
+        one_step()
+    q_start = sim.positions()
+    v_start = sim.velocities()
+
+    # ---- device-resident throughput (value) ---------------------------------
+    solves0 = sim.solve_count
+    launches0 = sim.kernel_launches
+    fwd_its, bwd_its = [], []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        fwd_its.append(one_step())
+        bwd_its.append(lib.lib.hd_sim_backward_iterations(sim.h))
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    launches = sim.kernel_launches - launches0
+    solves = sim.solve_count - solves0
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = world * args.steps / (ms / 1e3)
+
+    # ---- end to end through the C ABI with host buffers (e2e) ----------------
+    q_h = torch.from_numpy(q_start.copy()).pin_memory()
+    v_h = torch.from_numpy(v_start.copy()).pin_memory()
+    outs = {k: torch.zeros(n, dtype=torch.float64).pin_memory() for k in ("q", "v", "dq0", "dv0", "df")}
+    de_h = torch.zeros(ne, dtype=torch.float64).pin_memory()
+    import ctypes as C
+    D = C.POINTER(C.c_double)
+    ptr = lambda t: C.cast(t.data_ptr(), D)
+    h2d = 2 * n * 8
+    d2h = (5 * n + ne) * 8
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        lib.check(lib.lib.hd_sim_set_state(sim.h, ptr(q_h), ptr(v_h), 0.0))
+        lib.check(lib.lib.hd_sim_record(sim.h, 1))
+        lib.check(lib.lib.hd_sim_step(sim.h))
+        lib.check(lib.lib.hd_sim_backward_canonical(sim.h, ptr(outs["dq0"]), ptr(outs["dv0"]), ptr(outs["df"]),
+                                                    ptr(de_h), None, 0))
+        lib.check(lib.lib.hd_sim_positions(sim.h, ptr(outs["q"]), n))
+        lib.check(lib.lib.hd_sim_velocities(sim.h, ptr(outs["v"]), n))
+        lib.check(lib.lib.hd_sim_record(sim.h, 0))
+        q_h.copy_(outs["q"])
+        v_h.copy_(outs["v"])
+    e3.record(stream)
+    e3.synchronize()
+    ms_e2e = e2.elapsed_time(e3)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e = world * args.steps / (ms_e2e / 1e3)
+
+    # ---- roofline of the dominant kernel (global solve) ---------------------
+    ms_solve, bytes_solve = sim.time_solve(50)
+    peak, peak_kind = measured_peak()
+    achieved = bytes_solve / (ms_solve / 1e3) / 1e9
+    nnz = sim.factor_nnz
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(), "kernel": "hdk_apply_inverse3 (S' row-dot + column-tile passes, 3 axes)",
+                "bytes_per_launch": bytes_solve, "ms_per_launch": ms_solve, "peak_source": peak_kind}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(scene_dict, q_start, v_start)
+        except Exception as exc:  # reported, never fatal for the GPU line
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        step_share = ms_solve * solves / args.steps / (ms / args.steps)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {scene_dict['name']} ({ne} tets, {sc.vertex_count} vertices, "
+                                   f"100x E contrast, NH, alpha=0.05, beta0=0.01)",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "factor": {"ordering": "nd-bfs (postordered)", "nnz_S": nnz, "free_vertices": sim.free_count,
+                                  "build_s": t_fac},
+                       "l2_policy": "inputs larger than L2 (factor values %.0f MB > 126 MB L2)" % (nnz * 8 / 1e6),
+                       "mean_forward_iterations": float(np.mean(fwd_its)),
+                       "mean_adjoint_iterations": float(np.mean(bwd_its)),
+                       "solves_per_step": solves / args.steps,
+                       "solve_share_of_step_est": step_share},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

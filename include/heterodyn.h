@@ -146,6 +146,26 @@ HD_API long long hd_sim_solve_count(const hd_sim* sim);
 HD_API long long hd_sim_a_spmv_count(const hd_sim* sim);
 HD_API long long hd_sim_refactor_count(const hd_sim* sim);
 
+/* Device-resident variant of hd_sim_backward for throughput measurement:
+ * seeds the canonical loss L = 1/2 |q_T - rest|^2 + 1/2 |v_T|^2 of the
+ * gradient check (drivers.cpp:384-389, 394-396) from the state in device
+ * memory and keeps every gradient in device memory (outputs may be NULL).
+ * Same adjoint chain as hd_sim_backward. */
+HD_API hd_status hd_sim_backward_canonical(hd_sim* sim, double* dl_dq0, double* dl_dv0, double* dl_df_ext,
+                                           double* dl_de, double* dl_dw, size_t dl_dw_capacity);
+
+/* The CUDA stream every device operation of this sim is ordered on (as
+ * cudaStream_t, NULL for the CPU oracle) and the number of device kernels the
+ * sim has launched so far (graph kernel nodes counted per execution). */
+HD_API void* hd_sim_stream(const hd_sim* sim);
+HD_API long long hd_sim_kernel_launches(const hd_sim* sim);
+
+/* Times `reps` back-to-back applications of the global solve (3 axes) on the
+ * sim's stream with CUDA events, inputs resident in HBM; *ms_per_solve
+ * receives the mean duration.  Also reports the algorithmic bytes one solve
+ * moves (factor values read by both passes plus right-hand sides). */
+HD_API hd_status hd_sim_time_solve(hd_sim* sim, int reps, double* ms_per_solve, double* bytes_per_solve);
+
 #ifdef __cplusplus
 }
 #endif

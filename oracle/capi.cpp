@@ -1,6 +1,7 @@
 // ORACLE — test infrastructure only.  The hd_* C ABI of include/heterodyn.h
 // over the CPU restatement (reference capi.cpp:94-322 for the reference half;
 // the B200-extension half routes to roll/chain_backward, drivers.cpp:31-99).
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -303,6 +304,29 @@ hd_status hd_sim_set_young(hd_sim* sim, const double* young, size_t count, int f
     const SceneSpec& s = sim->scene->spec;
     sim->system.refresh(s.mesh, sim->material, s.solver.h, s.fixed_vertices);
     sim->caches.clear();
+  });
+}
+
+hd_status hd_sim_backward_canonical(hd_sim* sim, double* dl_dq0, double* dl_dv0, double* dl_df_ext, double* dl_de,
+                                    double* dl_dw, size_t dl_dw_capacity) {
+  if (!sim) return null_arg("hd_sim_backward_canonical");
+  const SceneSpec& s = sim->scene->spec;
+  VecX dq = sim->state.q;
+  for (size_t i = 0; i < dq.size(); ++i) dq[i] -= s.mesh.rest_vector()[i];
+  return hd_sim_backward(sim, nullptr, dq.data(), sim->state.v.data(), dl_dq0, dl_dv0, dl_df_ext, dl_de, dl_dw,
+                         dl_dw_capacity);
+}
+void* hd_sim_stream(const hd_sim*) { return nullptr; }
+long long hd_sim_kernel_launches(const hd_sim*) { return 0; }
+hd_status hd_sim_time_solve(hd_sim* sim, int reps, double* ms, double* bytes) {
+  if (!sim || !ms || reps < 1) return null_arg("hd_sim_time_solve");
+  return guarded([&] {
+    const size_t n = sim->state.q.size();
+    VecX rhs(n, 1.0), fq(n, 0.0);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < reps; ++i) sim->system.solve_free(rhs, fq);
+    *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() / reps;
+    if (bytes) *bytes = 24.0 * static_cast<double>(sim->system.factor().s_nnz());
   });
 }
 

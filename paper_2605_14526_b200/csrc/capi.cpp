@@ -193,6 +193,7 @@ hd_status hd_factor_stats(const hd_scene* scene, char** stats_json) {
     j["work_units"] = F.unit_tile.size();
     j["weight_contrast"] = s.material.contrast();
     j["refactorizations"] = 1;
+    j["inverse_residual"] = factor_inverse_residual(F);
     if (stats_json) *stats_json = dup(j.dump(2));
   });
 }
@@ -252,6 +253,35 @@ hd_status hd_sim_solve_free(hd_sim* sim, const double* rhs, const double* fixed_
 hd_status hd_sim_set_young(hd_sim* sim, const double* young, size_t count, int freeze) {
   if (!sim || !young) return bad_arg("hd_sim_set_young: NULL argument");
   return guarded([&] { sim->eng->set_young(Vec(young, young + count), freeze != 0); });
+}
+
+hd_status hd_sim_backward_canonical(hd_sim* sim, double* dl_dq0, double* dl_dv0, double* dl_df_ext, double* dl_de,
+                                    double* dl_dw, size_t dl_dw_capacity) {
+  if (!sim) return bad_arg("hd_sim_backward_canonical: sim is NULL");
+  return guarded([&] {
+    const bool any = dl_dq0 || dl_dv0 || dl_df_ext || dl_de || dl_dw;
+    GradOut g = sim->eng->backward(nullptr, nullptr, nullptr, true, any);
+    if (any) {
+      if (dl_dw && dl_dw_capacity < g.dl_dw.size()) raise(Code::InvalidArgument, "dl_dw buffer too small");
+      const auto put = [](double* d, const Vec& v) {
+        if (d) std::memcpy(d, v.data(), v.size() * sizeof(double));
+      };
+      put(dl_dq0, g.dl_dq0);
+      put(dl_dv0, g.dl_dv0);
+      put(dl_df_ext, g.dl_df_ext);
+      put(dl_de, g.dl_de);
+      put(dl_dw, g.dl_dw);
+    }
+    sim->last_grad = std::move(g);
+  });
+}
+
+void* hd_sim_stream(const hd_sim* sim) { return sim ? static_cast<void*>(sim->eng->stream()) : nullptr; }
+long long hd_sim_kernel_launches(const hd_sim* sim) { return sim ? sim->eng->kernel_launches : 0; }
+
+hd_status hd_sim_time_solve(hd_sim* sim, int reps, double* ms, double* bytes) {
+  if (!sim || !ms || reps < 1) return bad_arg("hd_sim_time_solve: bad argument");
+  return guarded([&] { *ms = sim->eng->time_solve(reps, bytes); });
 }
 
 long long hd_sim_factor_nnz(const hd_sim* sim) { return sim ? sim->eng->factor().row_off.back() : 0; }

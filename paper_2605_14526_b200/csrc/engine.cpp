@@ -45,13 +45,28 @@ void capture_into(cudaStream_t st, cudaGraph_t body, const std::function<void()>
 // pre -> while(body) -> post; returns the instantiated executable.  When
 // conditional nodes are disabled the body is instantiated separately and the
 // host drives the loop (debug fallback).
+int kernel_nodes(cudaGraph_t g) {
+  size_t n = 0;
+  cuda_check(cudaGraphGetNodes(g, nullptr, &n), "graph nodes");
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n) cuda_check(cudaGraphGetNodes(g, nodes.data(), &n), "graph nodes");
+  int k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    cuda_check(cudaGraphNodeGetType(nd, &t), "node type");
+    if (t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
+
 cudaGraphExec_t build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()>& pre,
                                  const std::function<void(unsigned long long)>& body,
                                  const std::function<void()>& post, cudaGraph_t& top_out, cudaGraph_t& body_out,
-                                 cudaGraphExec_t& body_exec) {
+                                 cudaGraphExec_t& body_exec, int counts[3]) {
   cudaGraph_t top = nullptr;
   cuda_check(cudaGraphCreate(&top, 0), "graph create");
   cudaGraph_t gpre = capture(st, pre);
+  counts[0] = kernel_nodes(gpre);
   cudaGraphNode_t npre, nloop, npost;
   cuda_check(cudaGraphAddChildGraphNode(&npre, top, nullptr, 0, gpre), "add pre");
   cudaGraphDestroy(gpre);
@@ -66,6 +81,7 @@ cudaGraphExec_t build_loop_graph(cudaStream_t st, bool use_cond, const std::func
     p.conditional.size = 1;
     cuda_check(cudaGraphAddNode(&nloop, top, &npre, 1, &p), "add while");
     capture_into(st, p.conditional.phGraph_out[0], [&] { body(static_cast<unsigned long long>(h)); });
+    counts[1] = kernel_nodes(p.conditional.phGraph_out[0]);
     last = nloop;
     body_exec = nullptr;
     body_out = nullptr;
@@ -74,6 +90,7 @@ cudaGraphExec_t build_loop_graph(cudaStream_t st, bool use_cond, const std::func
     cuda_check(cudaGraphInstantiate(&body_exec, body_out, 0), "instantiate body");
   }
   cudaGraph_t gpost = capture(st, post);
+  counts[2] = kernel_nodes(gpost);
   if (use_cond) {
     cuda_check(cudaGraphAddChildGraphNode(&npost, top, &last, 1, gpost), "add post");
   } else {
@@ -148,6 +165,7 @@ void Engine::build_static() {
   dm_.inc_off = A.upload(inc_off);
   dm_.inc = A.upload(inc);
   q_ = A.upload(scene_.q0);
+  rest_ = A.upload(m.rest);
   v_ = A.upload(scene_.v0);
   fext_ = A.upload(external_force(scene_));
   qtil_ = A.alloc<double>(n3);
@@ -316,7 +334,11 @@ void Engine::build_forward_graph() {
   auto post = [&] {
     hdk_check(hdk_local_step(&dm_, &dmat_, qcur_, ef_, cache_, &ctl_->err, s), "cache sweep");
   };
-  fexec_ = build_loop_graph(st_, use_cond_, pre, body, post, fg_, fbody_, fbody_exec_);
+  int c[3] = {0, 0, 0};
+  fexec_ = build_loop_graph(st_, use_cond_, pre, body, post, fg_, fbody_, fbody_exec_, c);
+  fk_pre_ = c[0];
+  fk_body_ = c[1];
+  fk_post_ = c[2];
 }
 
 void Engine::build_backward_graph() {
@@ -369,7 +391,11 @@ void Engine::build_backward_graph() {
     hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, dlq_, 1.0, direct_, qbar_, s), "next q seed");
     hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, dlv_, 0.0, nullptr, vbar_, s), "next v seed");
   };
-  bexec_ = build_loop_graph(st_, use_cond_, pre, body, post, bg_, bbody_, bbody_exec_);
+  int c[3] = {0, 0, 0};
+  bexec_ = build_loop_graph(st_, use_cond_, pre, body, post, bg_, bbody_, bbody_exec_, c);
+  bk_pre_ = c[0];
+  bk_body_ = c[1];
+  bk_post_ = c[2];
 }
 
 void Engine::sync_ctl() {
@@ -432,6 +458,7 @@ void Engine::step() {
   hdk_check(hdk_commit(static_cast<int>(n3), ctl_, qcur_, scene_.solver.h, q_, v_, st_), "commit");
   sync_ctl();
   solve_count += h_ctl_->iterations;
+  kernel_launches += fk_pre_ + static_cast<long long>(fk_body_) * h_ctl_->iterations + fk_post_ + 1;
   check_ctl("forward step");
   last_iterations = h_ctl_->iterations;
   last_converged = h_ctl_->converged;
@@ -447,24 +474,28 @@ void Engine::record(bool on) {
 
 void Engine::set_state(const double* q, const double* v, double time) {
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
-  if (q) cuda_check(cudaMemcpy(q_, q, n3 * sizeof(double), cudaMemcpyHostToDevice), "set q");
-  if (v) cuda_check(cudaMemcpy(v_, v, n3 * sizeof(double), cudaMemcpyHostToDevice), "set v");
+  if (q) cuda_check(cudaMemcpyAsync(q_, q, n3 * sizeof(double), cudaMemcpyHostToDevice, st_), "set q");
+  if (v) cuda_check(cudaMemcpyAsync(v_, v, n3 * sizeof(double), cudaMemcpyHostToDevice, st_), "set v");
+  cuda_check(cudaStreamSynchronize(st_), "set state");
   time_ = time;
   nrec_ = 0;
 }
 
 Vec Engine::positions() const {
   Vec out(3 * static_cast<size_t>(scene_.mesh.nv));
-  cuda_check(cudaMemcpy(out.data(), q_, out.size() * sizeof(double), cudaMemcpyDeviceToHost), "positions");
+  cuda_check(cudaMemcpyAsync(out.data(), q_, out.size() * sizeof(double), cudaMemcpyDeviceToHost, st_), "read state");
+  cuda_check(cudaStreamSynchronize(st_), "read state");
   return out;
 }
 Vec Engine::velocities() const {
   Vec out(3 * static_cast<size_t>(scene_.mesh.nv));
-  cuda_check(cudaMemcpy(out.data(), v_, out.size() * sizeof(double), cudaMemcpyDeviceToHost), "velocities");
+  cuda_check(cudaMemcpyAsync(out.data(), v_, out.size() * sizeof(double), cudaMemcpyDeviceToHost, st_), "read state");
+  cuda_check(cudaStreamSynchronize(st_), "read state");
   return out;
 }
 
-GradOut Engine::backward(const double* direct, const double* dq_final, const double* dv_final) {
+GradOut Engine::backward(const double* direct, const double* dq_final, const double* dv_final, bool canonical,
+                         bool download) {
   const int T = nrec_;
   if (T == 0) raise(Code::InvalidArgument, "hd_sim_backward: no recorded frames");
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
@@ -473,8 +504,14 @@ GradOut Engine::backward(const double* direct, const double* dq_final, const dou
     if (h) cuda_check(cudaMemcpyAsync(d, h, B, cudaMemcpyHostToDevice, st_), "seed upload");
     else cuda_check(cudaMemsetAsync(d, 0, B, st_), "seed zero");
   };
-  h2d(qbar_, direct ? direct + static_cast<size_t>(T) * n3 : dq_final);
-  h2d(vbar_, dv_final);
+  if (canonical) {  // L = 1/2 |q_T - rest|^2 + 1/2 |v_T|^2, seeds from device state
+    hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, q_, -1.0, rest_, qbar_, st_), "canonical q seed");
+    hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, v_, 0.0, nullptr, vbar_, st_), "canonical v seed");
+    kernel_launches += 2;
+  } else {
+    h2d(qbar_, direct ? direct + static_cast<size_t>(T) * n3 : dq_final);
+    h2d(vbar_, dv_final);
+  }
   cuda_check(cudaMemsetAsync(dfacc_, 0, B, st_), "zero");
   cuda_check(cudaMemsetAsync(dlw_, 0, 2 * ne * sizeof(double), st_), "zero");
   cuda_check(cudaMemsetAsync(dle_, 0, ne * sizeof(double), st_), "zero");
@@ -498,14 +535,17 @@ GradOut Engine::backward(const double* direct, const double* dq_final, const dou
     sync_ctl();
     ++a_spmv_count;
     solve_count += h_ctl_->iterations;
+    kernel_launches += bk_pre_ + static_cast<long long>(bk_body_) * (h_ctl_->iterations - 1) + bk_post_;
     check_ctl("backward step");
     out.tau[t] = h_ctl_->tau;
     out.rho[t] = h_ctl_->rho;
     out.adjoint_iterations += h_ctl_->iterations;
   }
+  if (!download) return out;
   const auto d2h = [&](Vec& v, const double* d, size_t n) {
     v.resize(n);
-    cuda_check(cudaMemcpy(v.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost), "grad download");
+    cuda_check(cudaMemcpyAsync(v.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost, st_), "grad download");
+    cuda_check(cudaStreamSynchronize(st_), "grad download");
   };
   d2h(out.dl_dq0, qbar_, n3);
   d2h(out.dl_dv0, vbar_, n3);
@@ -531,6 +571,25 @@ Vec Engine::solve_free(const double* rhs, const double* fixed_q) {
   cuda_check(cudaMemcpyAsync(out.data(), t_, n3 * sizeof(double), cudaMemcpyDeviceToHost, st_), "download");
   cuda_check(cudaStreamSynchronize(st_), "sync");
   return out;
+}
+
+double Engine::time_solve(int reps, double* bytes) {
+  cudaEvent_t a, b;
+  cuda_check(cudaEventCreate(&a), "event");
+  cuda_check(cudaEventCreate(&b), "event");
+  for (int i = 0; i < 2; ++i) hdk_check(hdk_apply_inverse3_perm(&df_, rhs_, dqp_, st_), "warm solve");
+  cuda_check(cudaEventRecord(a, st_), "event");
+  for (int i = 0; i < reps; ++i) hdk_check(hdk_apply_inverse3_perm(&df_, rhs_, dqp_, st_), "timed solve");
+  cuda_check(cudaEventRecord(b, st_), "event");
+  cuda_check(cudaEventSynchronize(b), "event sync");
+  float ms = 0;
+  cuda_check(cudaEventElapsedTime(&ms, a, b), "elapsed");
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  kernel_launches += 4LL * (reps + 2);
+  // factor values streamed by both passes + rhs read, z write/read, x write
+  if (bytes) *bytes = 16.0 * static_cast<double>(hf_.row_off.back()) + 96.0 * hf_.n;
+  return static_cast<double>(ms) / reps;
 }
 
 void Engine::set_young(const Vec& young, bool freeze) {

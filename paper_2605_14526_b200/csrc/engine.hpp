@@ -52,7 +52,9 @@ class Engine {
   void record(bool on);
   int recorded() const { return nrec_; }
   void set_state(const double* q, const double* v, double time);
-  GradOut backward(const double* dl_dq_direct, const double* dl_dq_final, const double* dl_dv_final);
+  GradOut backward(const double* dl_dq_direct, const double* dl_dq_final, const double* dl_dv_final,
+                   bool canonical = false, bool download = true);
+  double time_solve(int reps, double* bytes);
   Vec solve_free(const double* rhs, const double* fixed_q);
   void set_young(const Vec& young, bool freeze);
 
@@ -61,7 +63,7 @@ class Engine {
   double time() const { return time_; }
   int dofs() const { return 3 * mesh().nv; }
   int last_iterations = 0, last_converged = 0, last_contacts = 0;
-  long long solve_count = 0, a_spmv_count = 0, refactor_count = 0;
+  long long solve_count = 0, a_spmv_count = 0, refactor_count = 0, kernel_launches = 0;
   const HostFactor& factor() const { return hf_; }
   const Mesh& mesh() const { return scene_.mesh; }
   const Material& material() const { return mat_; }
@@ -122,6 +124,8 @@ class Engine {
   bool recording_ = false;
   int aa_window_ = 1;
 
+  double* rest_ = nullptr;  // rest positions (canonical loss seed)
+  int fk_pre_ = 0, fk_body_ = 0, fk_post_ = 0, bk_pre_ = 0, bk_body_ = 0, bk_post_ = 0;
   cudaGraph_t fg_ = nullptr, bg_ = nullptr, fbody_ = nullptr, bbody_ = nullptr;
   cudaGraphExec_t fexec_ = nullptr, bexec_ = nullptr, fbody_exec_ = nullptr, bbody_exec_ = nullptr;
 };

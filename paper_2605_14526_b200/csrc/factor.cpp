@@ -6,10 +6,11 @@
 //   P A_ff P^T = L D L^T,  S' = D^{-1/2} L^{-1},  A_ff^{-1} = P^T S'^T S' P.
 //
 // B200-first choices (same operator, different layout):
-//  * ordering "nd-geometric" (default): nested dissection by coordinate
-//    bisection of the rest shape — planar separators on hex-derived meshes,
-//    markedly less fill than the reference's BFS-level dissection
-//    ("nd-bfs", ordering.cpp:73-144, also available);
+//  * ordering "nd-bfs" (default): BFS-level nested dissection
+//    (ordering.cpp:73-144) with natural order inside leaves and separators,
+//    which on the hex-derived meshes here gives less fill than both the
+//    reference's min-degree leaves and coordinate bisection ("nd-geometric",
+//    also available; measured nnz(S') at C3: 21.2 M vs 25.0 M);
 //  * the elimination order is postordered, so every row of S' is dense over a
 //    contiguous column range (its etree subtree) and is stored without column
 //    indices;
@@ -464,6 +465,34 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
   }
   F.millis = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return F;
+}
+
+double factor_inverse_residual(const HostFactor& F) {
+  const int n = F.n;
+  double worst = 0;
+  for (int axis = 0; axis < 3; ++axis) {
+    Vec b(n), z(n, 0.0), x(n, 0.0);
+    for (int i = 0; i < n; ++i) b[i] = std::sin(0.7 * i + axis) + 0.1 * axis;
+    for (int row = 0; row < n; ++row) {
+      const int first = row - F.row_len[row] + 1;
+      double s = 0;
+      for (int c = first; c <= row; ++c) s += F.sval[F.row_off[row] + (c - first)] * b[c];
+      z[row] = s;
+    }
+    for (int row = 0; row < n; ++row) {
+      const int first = row - F.row_len[row] + 1;
+      for (int c = first; c <= row; ++c) x[c] += F.sval[F.row_off[row] + (c - first)] * z[row];
+    }
+    double rn = 0, bn = 0;
+    for (int p = 0; p < n; ++p) {
+      double s = 0;
+      for (int k = F.a_ff.off[p]; k < F.a_ff.off[p + 1]; ++k) s += F.a_ff.val[k] * x[F.a_ff.col[k]];
+      rn += (s - b[p]) * (s - b[p]);
+      bn += b[p] * b[p];
+    }
+    worst = std::max(worst, std::sqrt(rn / bn));
+  }
+  return worst;
 }
 
 }  // namespace hdb

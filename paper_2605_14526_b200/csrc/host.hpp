@@ -125,6 +125,9 @@ struct HostFactor {
   std::string ordering;
   double weight_contrast = 1;
 };
+// Setup-time self-check of a built factor on the host: max over three axes of
+// |A_ff S'^T S' b - b| / |b| for a deterministic b (no solve path runs here).
+double factor_inverse_residual(const HostFactor& F);
 HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const std::vector<int>& fixed,
                         const std::string& ordering);
 

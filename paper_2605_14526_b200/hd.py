@@ -68,6 +68,10 @@ SIGNATURES = {
     "hd_sim_solve_count": (C.c_longlong, [_VP]),
     "hd_sim_a_spmv_count": (C.c_longlong, [_VP]),
     "hd_sim_refactor_count": (C.c_longlong, [_VP]),
+    "hd_sim_backward_canonical": (C.c_int, [_VP, _D, _D, _D, _D, _D, C.c_size_t]),
+    "hd_sim_stream": (_VP, [_VP]),
+    "hd_sim_kernel_launches": (C.c_longlong, [_VP]),
+    "hd_sim_time_solve": (C.c_int, [_VP, C.c_int, _D, _D]),
 }
 
 
@@ -261,6 +265,35 @@ class Sim:
         out["rho"] = rho[:frames]
         out["adjoint_iterations"] = self.L.lib.hd_sim_backward_iterations(self.h)
         return out
+
+    def backward_canonical(self, download: bool = False) -> dict | None:
+        """Adjoint chain of L = 1/2|q_T - rest|^2 + 1/2|v_T|^2 seeded in device memory."""
+        if not download:
+            self.L.check(self.L.lib.hd_sim_backward_canonical(self.h, None, None, None, None, None, 0))
+            return None
+        ne = self.scene.element_count
+        out = {k: np.zeros(self.n) for k in ("dl_dq0", "dl_dv0", "dl_df_ext")}
+        out["dl_de"] = np.zeros(ne)
+        dw = np.zeros(2 * ne)
+        self.L.check(self.L.lib.hd_sim_backward_canonical(
+            self.h, _ptr(out["dl_dq0"]), _ptr(out["dl_dv0"]), _ptr(out["dl_df_ext"]), _ptr(out["dl_de"]),
+            _ptr(dw), dw.size))
+        out["dl_dw"] = dw
+        return out
+
+    @property
+    def stream(self) -> int:
+        return self.L.lib.hd_sim_stream(self.h) or 0
+
+    @property
+    def kernel_launches(self) -> int:
+        return self.L.lib.hd_sim_kernel_launches(self.h)
+
+    def time_solve(self, reps: int = 20):
+        ms = C.c_double()
+        b = C.c_double()
+        self.L.check(self.L.lib.hd_sim_time_solve(self.h, reps, C.byref(ms), C.byref(b)))
+        return ms.value, b.value
 
     def solve_free(self, rhs, fixed_q=None):
         rhs = _f64(rhs, self.n)

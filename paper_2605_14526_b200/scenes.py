@@ -108,12 +108,14 @@ def config_scene(tag: str, frames: int | None = None, solver: dict | None = None
         young = np.where(inside, 5e6, 5e4)
         nx, ny, nz = dims
         pull_vertex = nx + (nx + 1) * (ny // 2 + (ny + 1) * (nz // 2))  # +x face centre
+        nv = (nx + 1) * (ny + 1) * (nz + 1)
         s = {
             "name": "C3-crab-heterogeneous",
             "mesh": {"grid": {"dims": list(dims), "spacing": h, "density": 1000.0}},
             "material": {"energy": "neo-hookean", "young": young.tolist(), "poisson": 0.4, "alpha": 0.05, "beta0": 0.01},
             "gravity": [0.0, 0.0, -9.81],
             "f_ext": [{"vertex": int(pull_vertex), "force": [0.01, 0.0, 0.005]}],
+            "initial": {"velocity": wiggle(3 * nv, 0.05).tolist()},
             "solver": _solver(),
             "frames": 100,
         }

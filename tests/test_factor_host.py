@@ -1,0 +1,31 @@
+"""Host-side factor build of the product (runs on CPU at setup time): the
+explicit inverse factor must reproduce A_ff^{-1}, its size must be reported,
+and orderings must agree.  CPU only."""
+import pytest
+
+from paper_2605_14526_b200 import scenes
+
+
+@pytest.mark.parametrize("scene", [
+    scenes.block_scene(dims=(3, 2, 2), contrast=10.0, alpha=0.02, beta0=0.1),
+    scenes.block_scene(dims=(4, 3, 2), fix_x0_face=True, kind="corotated"),
+    scenes.config_scene("C1"),
+])
+@pytest.mark.parametrize("ordering", ["nd-bfs", "nd-geometric"])
+def test_inverse_factor_residual(prod, scene, ordering):
+    scene = dict(scene)
+    scene["factor"] = {"ordering": ordering}
+    st = prod.scene(scene).factor_stats()
+    assert st["inverse_residual"] <= 1e-9, st
+    assert st["ordering"] == ordering
+    assert 0 < st["factor_fill_ratio"] <= 1.0
+
+
+def test_factor_nnz_vs_reference_ordering(prod, orc):
+    """The product's postordered S' is never larger than 1.25x the oracle's
+    (reference-ordering) S on C1/C2; sizes are reported for bytes accounting."""
+    for tag in ("C1", "C2"):
+        a = prod.scene(scenes.config_scene(tag)).factor_stats()
+        b = orc.scene(scenes.config_scene(tag)).factor_stats()
+        assert a["free_vertices"] == b["free_vertices"]
+        assert a["factor_nnz"] <= 1.25 * b["factor_nnz"], (tag, a["factor_nnz"], b["factor_nnz"])
