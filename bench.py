@@ -255,12 +255,11 @@ def main():
     ms = e0.elapsed_time(e1)
     launches = sim.kernel_launches - launches0
     solves = sim.solve_count - solves0
+    from paper_2605_14526_b200.dist import max_over_ranks, replica_value
+    ms = max_over_ranks(ms)
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
         dist.barrier()
-    value = world * args.steps / (ms / 1e3)
+    value = replica_value(args.steps, ms, world)
 
     # ---- end to end through the C ABI with host buffers (e2e) ----------------
     q_h = torch.from_numpy(q_start.copy()).pin_memory()
@@ -292,11 +291,8 @@ def main():
     e3.record(stream)
     e3.synchronize()
     ms_e2e = e2.elapsed_time(e3)
-    if world > 1:
-        t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
-    e2e = world * args.steps / (ms_e2e / 1e3)
+    ms_e2e = max_over_ranks(ms_e2e)
+    e2e = replica_value(args.steps, ms_e2e, world)
 
     # ---- roofline of the dominant kernel (global solve) ---------------------
     ms_solve, bytes_solve = sim.time_solve(50)

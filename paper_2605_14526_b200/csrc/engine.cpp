@@ -59,49 +59,50 @@ int kernel_nodes(cudaGraph_t g) {
   return k;
 }
 
-cudaGraphExec_t build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()>& pre,
-                                 const std::function<void(unsigned long long)>& body,
-                                 const std::function<void()>& post, cudaGraph_t& top_out, cudaGraph_t& body_out,
-                                 cudaGraphExec_t& body_exec, int counts[3]) {
+// pre -> while(body) -> post as one executable graph with a device-driven
+// WHILE conditional node.  With conditional nodes disabled
+// (HETERODYN_NO_COND_GRAPH=1, used for per-kernel profiling) pre, body and
+// post are instantiated separately and the host drives the loop.
+cudaGraphExec_t instantiate(cudaGraph_t g) {
+  cudaGraphExec_t e = nullptr;
+  cuda_check(cudaGraphInstantiate(&e, g, 0), "instantiate");
+  return e;
+}
+
+void build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()>& pre,
+                      const std::function<void(unsigned long long)>& body, const std::function<void()>& post,
+                      LoopGraph& out) {
+  out.destroy();
+  cudaGraph_t gpre = capture(st, pre);
+  cudaGraph_t gpost = capture(st, post);
+  out.counts[0] = kernel_nodes(gpre);
+  out.counts[2] = kernel_nodes(gpost);
+  if (!use_cond) {
+    cudaGraph_t gbody = capture(st, [&] { body(0ULL); });
+    out.counts[1] = kernel_nodes(gbody);
+    out.pre = instantiate(gpre);
+    out.body = instantiate(gbody);
+    out.post = instantiate(gpost);
+    for (cudaGraph_t g : {gpre, gbody, gpost}) cudaGraphDestroy(g);
+    return;
+  }
   cudaGraph_t top = nullptr;
   cuda_check(cudaGraphCreate(&top, 0), "graph create");
-  cudaGraph_t gpre = capture(st, pre);
-  counts[0] = kernel_nodes(gpre);
   cudaGraphNode_t npre, nloop, npost;
   cuda_check(cudaGraphAddChildGraphNode(&npre, top, nullptr, 0, gpre), "add pre");
-  cudaGraphDestroy(gpre);
-  cudaGraphNode_t last = npre;
-  if (use_cond) {
-    cudaGraphConditionalHandle h;
-    cuda_check(cudaGraphConditionalHandleCreate(&h, top, 1, cudaGraphCondAssignDefault), "cond handle");
-    cudaGraphNodeParams p{};
-    p.type = cudaGraphNodeTypeConditional;
-    p.conditional.handle = h;
-    p.conditional.type = cudaGraphCondTypeWhile;
-    p.conditional.size = 1;
-    cuda_check(cudaGraphAddNode(&nloop, top, &npre, 1, &p), "add while");
-    capture_into(st, p.conditional.phGraph_out[0], [&] { body(static_cast<unsigned long long>(h)); });
-    counts[1] = kernel_nodes(p.conditional.phGraph_out[0]);
-    last = nloop;
-    body_exec = nullptr;
-    body_out = nullptr;
-  } else {
-    body_out = capture(st, [&] { body(0ULL); });
-    cuda_check(cudaGraphInstantiate(&body_exec, body_out, 0), "instantiate body");
-  }
-  cudaGraph_t gpost = capture(st, post);
-  counts[2] = kernel_nodes(gpost);
-  if (use_cond) {
-    cuda_check(cudaGraphAddChildGraphNode(&npost, top, &last, 1, gpost), "add post");
-  } else {
-    // fallback: post runs as its own graph after the host loop
-    cuda_check(cudaGraphAddChildGraphNode(&npost, top, &last, 1, gpost), "add post");
-  }
-  cudaGraphDestroy(gpost);
-  cudaGraphExec_t exec = nullptr;
-  cuda_check(cudaGraphInstantiate(&exec, top, 0), "instantiate");
-  top_out = top;
-  return exec;
+  cudaGraphConditionalHandle h;
+  cuda_check(cudaGraphConditionalHandleCreate(&h, top, 1, cudaGraphCondAssignDefault), "cond handle");
+  cudaGraphNodeParams p{};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cuda_check(cudaGraphAddNode(&nloop, top, &npre, 1, &p), "add while");
+  capture_into(st, p.conditional.phGraph_out[0], [&] { body(static_cast<unsigned long long>(h)); });
+  out.counts[1] = kernel_nodes(p.conditional.phGraph_out[0]);
+  cuda_check(cudaGraphAddChildGraphNode(&npost, top, &nloop, 1, gpost), "add post");
+  out.exec = instantiate(top);
+  for (cudaGraph_t g : {gpre, gpost, top}) cudaGraphDestroy(g);
 }
 }  // namespace
 
@@ -115,6 +116,8 @@ Engine::Engine(const Scene& scene) : scene_(scene), mat_(scene.material) {
     raise(Code::InvalidArgument, "no CUDA device: the B200 engine has no CPU fallback");
   cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
   cuda_check(cudaMallocHost(&h_ctl_, sizeof(hdk_ctl)), "pinned ctl");
+  fgraph_ = std::make_unique<LoopGraph>();
+  bgraph_ = std::make_unique<LoopGraph>();
   hf_ = build_factor(scene.mesh, mat_, scene.solver.h, scene.fixed, scene.ordering);
   refactor_count = 1;
   build_static();
@@ -125,10 +128,8 @@ Engine::Engine(const Scene& scene) : scene_(scene), mat_(scene.material) {
 }
 
 Engine::~Engine() {
-  for (cudaGraphExec_t e : {fexec_, bexec_, fbody_exec_, bbody_exec_})
-    if (e) cudaGraphExecDestroy(e);
-  for (cudaGraph_t g : {fg_, bg_, fbody_, bbody_})
-    if (g) cudaGraphDestroy(g);
+  if (fgraph_) fgraph_->destroy();
+  if (bgraph_) bgraph_->destroy();
   frame_mem_.clear();
   fmem_.reset();
   mem_.reset();
@@ -303,10 +304,6 @@ void Engine::build_factor_device() {
 }
 
 void Engine::build_forward_graph() {
-  if (fexec_) { cudaGraphExecDestroy(fexec_); fexec_ = nullptr; }
-  if (fbody_exec_) { cudaGraphExecDestroy(fbody_exec_); fbody_exec_ = nullptr; }
-  if (fg_) { cudaGraphDestroy(fg_); fg_ = nullptr; }
-  if (fbody_) { cudaGraphDestroy(fbody_); fbody_ = nullptr; }
   const Solver& so = scene_.solver;
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
   const double h = so.h;
@@ -334,18 +331,13 @@ void Engine::build_forward_graph() {
   auto post = [&] {
     hdk_check(hdk_local_step(&dm_, &dmat_, qcur_, ef_, cache_, &ctl_->err, s), "cache sweep");
   };
-  int c[3] = {0, 0, 0};
-  fexec_ = build_loop_graph(st_, use_cond_, pre, body, post, fg_, fbody_, fbody_exec_, c);
-  fk_pre_ = c[0];
-  fk_body_ = c[1];
-  fk_post_ = c[2];
+  build_loop_graph(st_, use_cond_, pre, body, post, *fgraph_);
+  fk_pre_ = fgraph_->counts[0];
+  fk_body_ = fgraph_->counts[1];
+  fk_post_ = fgraph_->counts[2];
 }
 
 void Engine::build_backward_graph() {
-  if (bexec_) { cudaGraphExecDestroy(bexec_); bexec_ = nullptr; }
-  if (bbody_exec_) { cudaGraphExecDestroy(bbody_exec_); bbody_exec_ = nullptr; }
-  if (bg_) { cudaGraphDestroy(bg_); bg_ = nullptr; }
-  if (bbody_) { cudaGraphDestroy(bbody_); bbody_ = nullptr; }
   const Solver& so = scene_.solver;
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
   const double h = so.h;
@@ -391,11 +383,10 @@ void Engine::build_backward_graph() {
     hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, dlq_, 1.0, direct_, qbar_, s), "next q seed");
     hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, dlv_, 0.0, nullptr, vbar_, s), "next v seed");
   };
-  int c[3] = {0, 0, 0};
-  bexec_ = build_loop_graph(st_, use_cond_, pre, body, post, bg_, bbody_, bbody_exec_, c);
-  bk_pre_ = c[0];
-  bk_body_ = c[1];
-  bk_post_ = c[2];
+  build_loop_graph(st_, use_cond_, pre, body, post, *bgraph_);
+  bk_pre_ = bgraph_->counts[0];
+  bk_body_ = bgraph_->counts[1];
+  bk_post_ = bgraph_->counts[2];
 }
 
 void Engine::sync_ctl() {
@@ -403,15 +394,19 @@ void Engine::sync_ctl() {
   cuda_check(cudaStreamSynchronize(st_), "stream sync");
 }
 
-void Engine::run_graph(cudaGraphExec_t exec, cudaGraphExec_t body_exec, const char* what, int loop_cap) {
-  if (use_cond_) {
-    cuda_check(cudaGraphLaunch(exec, st_), what);
+void Engine::run_graph(LoopGraph& g, const char* what) {
+  if (g.exec) {
+    cuda_check(cudaGraphLaunch(g.exec, st_), what);
     return;
   }
-  // Fallback: the top graph holds pre + post only; drive the body from the host.
-  (void)body_exec;
-  (void)loop_cap;
-  raise(Code::InvalidArgument, "host-driven loop fallback is not available in this build");
+  // host-driven loop (profiling fallback): one status read per iteration
+  cuda_check(cudaGraphLaunch(g.pre, st_), what);
+  for (;;) {
+    cuda_check(cudaGraphLaunch(g.body, st_), what);
+    sync_ctl();
+    if (!h_ctl_->cond) break;
+  }
+  cuda_check(cudaGraphLaunch(g.post, st_), what);
 }
 
 void Engine::check_ctl(const char* what) {
@@ -430,7 +425,7 @@ void Engine::check_ctl(const char* what) {
 
 void Engine::step() {
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
-  run_graph(fexec_, fbody_exec_, "forward graph", scene_.solver.k_max);
+  run_graph(*fgraph_, "forward graph");
   if (recording_) {
     if (static_cast<int>(slots_.size()) <= nrec_) {
       auto a = std::make_unique<DevArena>();
@@ -531,7 +526,7 @@ GradOut Engine::backward(const double* direct, const double* dq_final, const dou
     cp(bqstar_, f.qstar, n3);
     cp(bcache_, f.cache, 24 * ne);
     if (direct) cuda_check(cudaMemcpyAsync(direct_, direct + static_cast<size_t>(t) * n3, B, cudaMemcpyHostToDevice, st_), "direct");
-    run_graph(bexec_, bbody_exec_, "backward graph", 500);
+    run_graph(*bgraph_, "backward graph");
     sync_ctl();
     ++a_spmv_count;
     solve_count += h_ctl_->iterations;

@@ -35,6 +35,19 @@ struct DevArena {
 
 void cuda_check(cudaError_t e, const char* what);
 
+struct LoopGraph {
+  cudaGraphExec_t exec = nullptr, pre = nullptr, body = nullptr, post = nullptr;
+  int counts[3] = {0, 0, 0};
+  void destroy() {
+    for (cudaGraphExec_t* e : {&exec, &pre, &body, &post})
+      if (*e) {
+        cudaGraphExecDestroy(*e);
+        *e = nullptr;
+      }
+  }
+};
+
+
 struct GradOut {
   Vec dl_dq0, dl_dv0, dl_df_ext, dl_de, dl_dw;
   std::vector<double> tau, rho;
@@ -75,7 +88,7 @@ class Engine {
   void build_factor_device();
   void build_forward_graph();
   void build_backward_graph();
-  void run_graph(cudaGraphExec_t exec, cudaGraphExec_t body_exec, const char* what, int loop_cap);
+  void run_graph(LoopGraph& g, const char* what);
   void sync_ctl();
   void check_ctl(const char* what);
 
@@ -126,8 +139,7 @@ class Engine {
 
   double* rest_ = nullptr;  // rest positions (canonical loss seed)
   int fk_pre_ = 0, fk_body_ = 0, fk_post_ = 0, bk_pre_ = 0, bk_body_ = 0, bk_post_ = 0;
-  cudaGraph_t fg_ = nullptr, bg_ = nullptr, fbody_ = nullptr, bbody_ = nullptr;
-  cudaGraphExec_t fexec_ = nullptr, bexec_ = nullptr, fbody_exec_ = nullptr, bbody_exec_ = nullptr;
+  std::unique_ptr<LoopGraph> fgraph_, bgraph_;
 };
 
 }  // namespace hdb
