@@ -43,24 +43,38 @@ typedef struct hdk_material {
 } hdk_material;
 
 /* Explicit inverse factor A^{-1} = S'^T S' in postordered elimination order.
- * Row r of S' is dense over columns [r - len_r + 1, r] (its etree subtree)
- * and stored contiguously at sval[row_off[r]].  Work is cut into column
- * tiles of width tile_w; a segment is one row's part inside one tile;
- * consecutive segments of a tile form work units (factor.cpp:106-109). */
-typedef struct hdk_seg {
-  long long off;          /* index into sval of the segment's first value */
-  int row;                /* S' row */
-  int clo;                /* first column (global, in elimination order) */
-  int len;                /* number of columns */
-  int pslot;              /* slot of this segment's partial row dot */
+ * Row r of S' is dense over columns [r - len_r + 1, r] (its etree subtree),
+ * so no column indices are stored.  Columns are cut into tiles of tile_w;
+ * a segment is one row's part inside one tile.  The values are stored
+ * tile-major as one stream: each work unit (a run of segments of one tile)
+ * is a run of chunks, each chunk a 16-byte aligned contiguous block of at most
+ * HDK_CHUNK_VALS values holding whole segments, with its segment descriptors
+ * contiguous too — so both passes stream chunks into shared memory with bulk
+ * asynchronous copies (factor.cpp:106-109). */
+#define HDK_CHUNK_VALS 3072
+#define HDK_CHUNK_SEGS 256
+
+typedef struct hdk_seg {   /* 16 bytes */
+  int row;                 /* S' row */
+  int pslot;               /* slot of this segment's partial row dot */
+  int clo_len;             /* first column within the tile | (len << 16) */
+  int coff;                /* offset of the first value within the chunk */
 } hdk_seg;
+
+typedef struct hdk_chunk {  /* 24 bytes */
+  long long off;            /* stream offset (doubles, even) */
+  int len;                  /* values incl. padding (even) */
+  int seg0, nseg;           /* descriptors [seg0, seg0 + nseg) */
+  int unit;
+} hdk_chunk;
 
 typedef struct hdk_factor {
   int n;                  /* free vertices */
-  int tile_w, n_tiles, n_units;
-  const double* sval;
+  int tile_w, n_tiles, n_units, n_chunks, grid;
+  const double* sval;     /* tile-major value stream */
   const hdk_seg* seg;
-  const int* unit_seg;    /* n_units+1 */
+  const hdk_chunk* chunk;
+  const int* unit_chunk;  /* n_units+1 */
   const int* unit_tile;   /* n_units */
   const int* tile_unit;   /* n_tiles+1: units of tile t are contiguous */
   const int* row_pslot;   /* n+1: partial-dot slots of row r */

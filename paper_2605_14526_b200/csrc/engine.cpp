@@ -249,12 +249,18 @@ void Engine::build_factor_device() {
   df_.tile_w = F.tile_w;
   df_.n_tiles = static_cast<int>(F.tile_unit.size()) - 1;
   df_.n_units = static_cast<int>(F.unit_tile.size());
-  df_.sval = A.upload(F.sval);
-  static_assert(sizeof(hdk_seg) == sizeof(Segment), "segment layout");
-  hdk_seg* segs = A.alloc<hdk_seg>(F.seg.size());
-  DevArena::copy_h2d(segs, F.seg.data(), sizeof(Segment) * F.seg.size());
+  df_.n_chunks = static_cast<int>(F.chunks.size());
+  df_.grid = 0;
+  df_.sval = A.upload(F.stream);
+  static_assert(sizeof(hdk_seg) == sizeof(SegDesc), "segment descriptor layout");
+  static_assert(sizeof(hdk_chunk) == sizeof(ChunkDesc), "chunk descriptor layout");
+  hdk_seg* segs = A.alloc<hdk_seg>(F.sdesc.size());
+  DevArena::copy_h2d(segs, F.sdesc.data(), sizeof(SegDesc) * F.sdesc.size());
   df_.seg = segs;
-  df_.unit_seg = A.upload(F.unit_seg);
+  hdk_chunk* ch = A.alloc<hdk_chunk>(F.chunks.size());
+  DevArena::copy_h2d(ch, F.chunks.data(), sizeof(ChunkDesc) * F.chunks.size());
+  df_.chunk = ch;
+  df_.unit_chunk = A.upload(F.unit_chunk);
   df_.unit_tile = A.upload(F.unit_tile);
   df_.tile_unit = A.upload(F.tile_unit);
   df_.row_pslot = A.upload(F.row_pslot);

@@ -28,6 +28,8 @@
 namespace hdb {
 
 namespace {
+constexpr int HDK_VALS = 3072;  // == HDK_CHUNK_VALS (include/hdk.h)
+constexpr int HDK_SEGS = 256;   // == HDK_CHUNK_SEGS
 
 int hw_threads() {
   int n = static_cast<int>(std::thread::hardware_concurrency());
@@ -442,6 +444,37 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
       F.unit_tile.push_back(t);
     }
     F.tile_unit[t + 1] = static_cast<int>(F.unit_tile.size());
+  }
+  // 6b. tile-major value stream: units -> chunks of whole segments, every chunk
+  //     16-byte aligned, descriptors contiguous per chunk
+  {
+    const int nu = static_cast<int>(F.unit_tile.size());
+    F.unit_chunk.assign(nu + 1, 0);
+    F.stream.reserve(static_cast<size_t>(F.row_off[n] * 1.05) + 16);
+    for (int u = 0; u < nu; ++u) {
+      const int t = F.unit_tile[u];
+      int s = F.unit_seg[u];
+      const int se = F.unit_seg[u + 1];
+      while (s < se) {
+        ChunkDesc c{static_cast<long long>(F.stream.size()), 0, static_cast<int>(F.sdesc.size()), 0, u};
+        int vals = 0;
+        while (s < se && c.nseg < HDK_SEGS && vals + F.seg[s].len <= HDK_VALS) {
+          const Segment& g = F.seg[s];
+          F.sdesc.push_back({g.row, g.pslot, (g.clo - t * W) | (g.len << 16), vals});
+          F.stream.insert(F.stream.end(), F.sval.begin() + g.off, F.sval.begin() + g.off + g.len);
+          vals += g.len;
+          ++c.nseg;
+          ++s;
+        }
+        if (vals & 1) {
+          F.stream.push_back(0.0);
+          ++vals;
+        }
+        c.len = vals;
+        F.chunks.push_back(c);
+      }
+      F.unit_chunk[u + 1] = static_cast<int>(F.chunks.size());
+    }
   }
   // 7. A_ff and A_fd in elimination order (apply_a_free / fixed coupling)
   F.a_ff.rows = F.a_ff.cols = n;

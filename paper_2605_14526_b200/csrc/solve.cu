@@ -3,84 +3,159 @@
 // (reference factor.cpp:106-109, 196-208; csr.cpp:40-47 does each of the six
 // serial CSR passes there).
 //
-// Layout (see hdk.h): S' = D^{-1/2} L^{-1} in a postordered elimination order,
-// so row r is dense over its etree subtree [r-len_r+1, r] and needs no column
-// indices: 8 B per nonzero instead of the reference's 12 B, and both passes
-// stream the same value array once, coalesced, for all three axes.
-//
-// Work decomposition: columns are cut into tiles of 256; a segment is one
-// row's part inside one tile; a work unit (one CTA) is a run of segments of one
-// tile with ~nnz/592 values.  Inside a CTA, lane j of every warp owns the tile
-// columns j + 32 m (m = 0..7), so the right-hand side (pass 1) or the
-// accumulators (pass 2) of a whole tile live in 24 registers per lane, every
-// segment read is a coalesced 256-byte row slice, and the segment descriptors
-// are staged once in shared memory.
+// Layout (hdk.h): S' = D^{-1/2} L^{-1} in a postordered elimination order, so
+// row r is dense over its etree subtree and needs no column indices (8 B per
+// nonzero instead of the reference's 12 B).  Values are stored tile-major as
+// one stream of 16-byte aligned chunks (whole row segments of one 256-column
+// tile), so each pass is a pure stream: persistent CTAs walk their work units
+// and a single elected thread keeps a ring of kStages chunks in flight with
+// bulk asynchronous copies (cp.async.bulk, the TMA engine's 1-D mode) that
+// complete on mbarriers, while 8 warps consume the chunk in shared memory.
+// Lane j owns the tile columns j + 32 m (m = 0..7): the right-hand side
+// (pass 1) or the accumulators (pass 2) of a tile live in 24 registers.
 //
 //   pass 1  k_rowdot   partial z_{r,t} = S'(r, tile t) . b_t   (warp per segment)
 //   reduce  k_zreduce  z_r = sum_t z_{r,t}                     (warp per row, fixed order)
 //   pass 2  k_coltile  x_t += S'(r, tile t)^T z_r               (warp-private accumulators,
-//                                                               fixed-order CTA fold)
+//                                                               fixed-order CTA fold per unit)
 //   reduce  k_xreduce  x_c = sum over the tile's units; scatter to xyz-interleaved
-// Every sum has a fixed order, so results are bitwise reproducible.
+// Work assignment and every sum are fixed, so results are bitwise reproducible.
 #include <cuda_runtime.h>
+
+#include <cstdint>
 
 #include "../../include/hdk.h"
 
 namespace {
 
-constexpr int kW = 256;        // tile width (columns)
-constexpr int kM = kW / 32;    // columns per lane
-constexpr int kWarps = 8;      // warps per CTA
+constexpr int kW = 256;       // tile width (columns)
+constexpr int kM = kW / 32;   // columns per lane
+constexpr int kWarps = 8;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kSegSmem = 512;  // descriptors staged per chunk
+constexpr int kVals = HDK_CHUNK_VALS;
+constexpr int kSegs = HDK_CHUNK_SEGS;
+constexpr int kStages1 = 3;   // pass 1 ring depth (2 CTAs / SM)
+constexpr int kStages2 = 2;   // pass 2 ring depth (plus fold + z buffers; 2 CTAs / SM)
 
-struct SegS {
-  long long off;
-  int row, clo, len, pslot;
+static_assert(kW == 256, "tile width is fixed by the factor layout");
+
+// ---- bulk-copy / mbarrier primitives (PTX) ----------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Chunk sequence of one persistent CTA: its units u = blockIdx.x + k * gridDim.x
+// in order, each unit's chunks in order.
+struct ChunkIter {
+  int u, c, cend, nu;
+  __device__ __forceinline__ void start(const hdk_factor& f) {
+    nu = f.n_units;
+    u = blockIdx.x;
+    c = u < nu ? f.unit_chunk[u] : 0;
+    cend = u < nu ? f.unit_chunk[u + 1] : 0;
+    skip_empty(f);
+  }
+  __device__ __forceinline__ void skip_empty(const hdk_factor& f) {
+    while (u < nu && c >= cend) {
+      u += gridDim.x;
+      if (u < nu) {
+        c = f.unit_chunk[u];
+        cend = f.unit_chunk[u + 1];
+      }
+    }
+  }
+  __device__ __forceinline__ bool valid() const { return u < nu; }
+  __device__ __forceinline__ void next(const hdk_factor& f) {
+    ++c;
+    skip_empty(f);
+  }
 };
 
-__device__ __forceinline__ void stage_segments(const hdk_seg* __restrict__ g, int s0, int n, SegS* sm) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const hdk_seg s = g[s0 + i];
-    sm[i].off = s.off;
-    sm[i].row = s.row;
-    sm[i].clo = s.clo;
-    sm[i].len = s.len;
-    sm[i].pslot = s.pslot;
-  }
+template <int S>
+struct Ring {
+  double vals[S][kVals];
+  hdk_seg segs[S][kSegs];
+  uint64_t full[S];
+};
+
+template <int S>
+__device__ __forceinline__ void issue(const hdk_factor& f, Ring<S>& r, int stage, int chunk) {
+  const hdk_chunk ch = f.chunk[chunk];
+  const uint32_t vb = static_cast<uint32_t>(ch.len) * 8u, sb = static_cast<uint32_t>(ch.nseg) * 16u;
+  mbar_expect_tx(&r.full[stage], vb + sb);
+  if (vb) bulk_g2s(r.vals[stage], f.sval + ch.off, vb, &r.full[stage]);
+  bulk_g2s(r.segs[stage], f.seg + ch.seg0, sb, &r.full[stage]);
 }
 
+// ---- pass 1 ------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double* __restrict__ rhs) {
-  __shared__ SegS ss[kSegSmem];
-  const int u = blockIdx.x;
-  const int c0 = f.unit_tile[u] * kW;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Ring<kStages1>& ring = *reinterpret_cast<Ring<kStages1>*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // right-hand side of the tile in registers: lane owns columns c0 + lane + 32 m
-  double b0[kM], b1[kM], b2[kM];
-#pragma unroll
-  for (int m = 0; m < kM; ++m) {
-    const int c = c0 + lane + 32 * m;
-    const bool ok = c < f.n;
-    b0[m] = ok ? __ldg(rhs + 3 * (size_t)c) : 0.0;
-    b1[m] = ok ? __ldg(rhs + 3 * (size_t)c + 1) : 0.0;
-    b2[m] = ok ? __ldg(rhs + 3 * (size_t)c + 2) : 0.0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages1; ++s) mbar_init(&ring.full[s], 1);
+    mbar_fence_init();
   }
-  const int s_beg = f.unit_seg[u], s_end = f.unit_seg[u + 1];
-  for (int base = s_beg; base < s_end; base += kSegSmem) {
-    const int cnt = min(kSegSmem, s_end - base);
-    __syncthreads();
-    stage_segments(f.seg, base, cnt, ss);
-    __syncthreads();
-    for (int i = warp; i < cnt; i += kWarps) {
-      const SegS sg = ss[i];
-      const double* __restrict__ val = f.sval + sg.off - (sg.clo - c0);  // val[c - c0] = S'(row, c)
-      const int lo = sg.clo - c0, hi = lo + sg.len;
+  __syncthreads();
+  ChunkIter prod, cons;
+  prod.start(f);
+  cons = prod;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kStages1 && prod.valid(); ++s, prod.next(f)) issue(f, ring, s, prod.c);
+  double b0[kM], b1[kM], b2[kM];
+  int tile = -1;
+  for (int k = 0; cons.valid(); ++k, cons.next(f)) {
+    const int st = k % kStages1;
+    const int t = f.unit_tile[cons.u];
+    if (t != tile) {  // right-hand side of the tile into registers
+      tile = t;
+#pragma unroll
+      for (int m = 0; m < kM; ++m) {
+        const int c = t * kW + lane + 32 * m;
+        const bool ok = c < f.n;
+        b0[m] = ok ? __ldg(rhs + 3 * (size_t)c) : 0.0;
+        b1[m] = ok ? __ldg(rhs + 3 * (size_t)c + 1) : 0.0;
+        b2[m] = ok ? __ldg(rhs + 3 * (size_t)c + 2) : 0.0;
+      }
+    }
+    mbar_wait(&ring.full[st], (k / kStages1) & 1);
+    const int nseg = f.chunk[cons.c].nseg;
+    const double* vals = ring.vals[st];
+    for (int i = warp; i < nseg; i += kWarps) {
+      const hdk_seg sg = ring.segs[st][i];
+      const int lo = sg.clo_len & 0xffff, hi = lo + (sg.clo_len >> 16);
+      const double* v = vals + sg.coff - lo;  // v[cl] = S'(row, tile column cl)
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
         if (cl >= lo && cl < hi) {
-          const double w = __ldg(val + cl);
+          const double w = v[cl];
           a0 += w * b0[m];
           a1 += w * b1[m];
           a2 += w * b2[m];
@@ -98,6 +173,12 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
         p[1] = a1;
         p[2] = a2;
       }
+    }
+    __syncthreads();  // stage st fully consumed
+    if (threadIdx.x == 0 && prod.valid()) {
+      fence_proxy_async();
+      issue(f, ring, st, prod.c);
+      prod.next(f);
     }
   }
 }
@@ -129,77 +210,27 @@ __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
-  __shared__ SegS ss[kSegSmem];
-  __shared__ double fold[kWarps / 2][3][kW];  // cross-warp fold, two rounds
-  const int u = blockIdx.x;
-  const int c0 = f.unit_tile[u] * kW;
+// ---- pass 2 ------------------------------------------------------------------
+struct Pass2Smem {
+  Ring<kStages2> ring;
+  double fold[kWarps / 2][3][kW];
+  double zc[kSegs][3];
+};
+
+__device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& sm, int unit, double (&x0)[kM],
+                                               double (&x1)[kM], double (&x2)[kM]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double x0[kM], x1[kM], x2[kM];
-#pragma unroll
-  for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
-  const int s_beg = f.unit_seg[u], s_end = f.unit_seg[u + 1];
-  for (int base = s_beg; base < s_end; base += kSegSmem) {
-    const int cnt = min(kSegSmem, s_end - base);
-    __syncthreads();
-    stage_segments(f.seg, base, cnt, ss);
-    __syncthreads();
-    int i = warp;
-    // two segments per iteration for memory-level parallelism
-    for (; i + kWarps < cnt; i += 2 * kWarps) {
-      const SegS sa = ss[i], sb = ss[i + kWarps];
-      const double* __restrict__ va = f.sval + sa.off - (sa.clo - c0);
-      const double* __restrict__ vb = f.sval + sb.off - (sb.clo - c0);
-      const int la = sa.clo - c0, ha = la + sa.len, lb = sb.clo - c0, hb = lb + sb.len;
-      const double* za = f.z + 3 * (size_t)sa.row;
-      const double* zb = f.z + 3 * (size_t)sb.row;
-      double wa[kM], wb[kM];
-#pragma unroll
-      for (int m = 0; m < kM; ++m) {
-        const int cl = lane + 32 * m;
-        wa[m] = (cl >= la && cl < ha) ? __ldg(va + cl) : 0.0;
-        wb[m] = (cl >= lb && cl < hb) ? __ldg(vb + cl) : 0.0;
-      }
-      const double za0 = __ldg(za), za1 = __ldg(za + 1), za2 = __ldg(za + 2);
-      const double zb0 = __ldg(zb), zb1 = __ldg(zb + 1), zb2 = __ldg(zb + 2);
-#pragma unroll
-      for (int m = 0; m < kM; ++m) {
-        x0[m] += wa[m] * za0;
-        x1[m] += wa[m] * za1;
-        x2[m] += wa[m] * za2;
-        x0[m] += wb[m] * zb0;
-        x1[m] += wb[m] * zb1;
-        x2[m] += wb[m] * zb2;
-      }
-    }
-    for (; i < cnt; i += kWarps) {
-      const SegS sa = ss[i];
-      const double* __restrict__ va = f.sval + sa.off - (sa.clo - c0);
-      const int la = sa.clo - c0, ha = la + sa.len;
-      const double* za = f.z + 3 * (size_t)sa.row;
-      const double za0 = __ldg(za), za1 = __ldg(za + 1), za2 = __ldg(za + 2);
-#pragma unroll
-      for (int m = 0; m < kM; ++m) {
-        const int cl = lane + 32 * m;
-        const double w = (cl >= la && cl < ha) ? __ldg(va + cl) : 0.0;
-        x0[m] += w * za0;
-        x1[m] += w * za1;
-        x2[m] += w * za2;
-      }
-    }
-  }
-  // fixed-order fold of the 8 warp-private accumulators: warps 4..7 park,
-  // 0..3 add; then 2..3 park, 0..1 add; then 1 parks, 0 adds and writes.
-  __syncthreads();
+  // fixed-order fold: warps 4..7 into 0..3, 2..3 into 0..1, 1 into 0
 #pragma unroll
   for (int half = kWarps / 2; half >= 1; half >>= 1) {
+    __syncthreads();
     if (warp >= half && warp < 2 * half) {
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
-        fold[warp - half][0][cl] = x0[m];
-        fold[warp - half][1][cl] = x1[m];
-        fold[warp - half][2][cl] = x2[m];
+        sm.fold[warp - half][0][cl] = x0[m];
+        sm.fold[warp - half][1][cl] = x1[m];
+        sm.fold[warp - half][2][cl] = x2[m];
       }
     }
     __syncthreads();
@@ -207,22 +238,85 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
-        x0[m] += fold[warp][0][cl];
-        x1[m] += fold[warp][1][cl];
-        x2[m] += fold[warp][2][cl];
+        x0[m] += sm.fold[warp][0][cl];
+        x1[m] += sm.fold[warp][1][cl];
+        x2[m] += sm.fold[warp][2][cl];
       }
     }
-    __syncthreads();
   }
   if (warp == 0) {
 #pragma unroll
     for (int m = 0; m < kM; ++m) {
-      double* p = f.part2 + 3 * ((size_t)u * kW + lane + 32 * m);
+      double* p = f.part2 + 3 * ((size_t)unit * kW + lane + 32 * m);
       p[0] = x0[m];
       p[1] = x1[m];
       p[2] = x2[m];
     }
   }
+#pragma unroll
+  for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
+}
+
+__global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Pass2Smem& sm = *reinterpret_cast<Pass2Smem*>(smem_raw);
+  Ring<kStages2>& ring = sm.ring;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages2; ++s) mbar_init(&ring.full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  ChunkIter prod, cons;
+  prod.start(f);
+  cons = prod;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kStages2 && prod.valid(); ++s, prod.next(f)) issue(f, ring, s, prod.c);
+  double x0[kM], x1[kM], x2[kM];
+#pragma unroll
+  for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
+  int unit = -1;
+  for (int k = 0; cons.valid(); ++k, cons.next(f)) {
+    const int st = k % kStages2;
+    if (cons.u != unit) {
+      if (unit >= 0) fold_and_write(f, sm, unit, x0, x1, x2);
+      unit = cons.u;
+    }
+    mbar_wait(&ring.full[st], (k / kStages2) & 1);
+    const int nseg = f.chunk[cons.c].nseg;
+    // gather z of the chunk's rows once (one round trip for the whole chunk)
+    if (threadIdx.x < nseg) {
+      const double* z = f.z + 3 * (size_t)ring.segs[st][threadIdx.x].row;
+      sm.zc[threadIdx.x][0] = __ldg(z);
+      sm.zc[threadIdx.x][1] = __ldg(z + 1);
+      sm.zc[threadIdx.x][2] = __ldg(z + 2);
+    }
+    __syncthreads();
+    const double* vals = ring.vals[st];
+    for (int i = warp; i < nseg; i += kWarps) {
+      const hdk_seg sg = ring.segs[st][i];
+      const int lo = sg.clo_len & 0xffff, hi = lo + (sg.clo_len >> 16);
+      const double* v = vals + sg.coff - lo;
+      const double z0 = sm.zc[i][0], z1 = sm.zc[i][1], z2 = sm.zc[i][2];
+#pragma unroll
+      for (int m = 0; m < kM; ++m) {
+        const int cl = lane + 32 * m;
+        if (cl >= lo && cl < hi) {
+          const double w = v[cl];
+          x0[m] += w * z0;
+          x1[m] += w * z1;
+          x2[m] += w * z2;
+        }
+      }
+    }
+    __syncthreads();  // stage st and zc fully consumed
+    if (threadIdx.x == 0 && prod.valid()) {
+      fence_proxy_async();
+      issue(f, ring, st, prod.c);
+      prod.next(f);
+    }
+  }
+  if (unit >= 0) fold_and_write(f, sm, unit, x0, x1, x2);
 }
 
 template <bool kScatter>
@@ -244,12 +338,29 @@ __global__ void k_xreduce(hdk_factor f, double* __restrict__ out) {
   o[2] = a2;
 }
 
+int g_grid1 = 0, g_grid2 = 0;
+
 int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatter, cudaStream_t st) {
   if (f->n <= 0) return 0;
   if (f->tile_w != kW) return static_cast<int>(cudaErrorInvalidValue);
-  k_rowdot<<<f->n_units, kThreads, 0, st>>>(*f, rhs_perm);
+  static bool configured = false;
+  const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem);
+  if (!configured) {
+    cudaFuncSetAttribute(k_rowdot, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
+    cudaFuncSetAttribute(k_coltile, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s2));
+    int dev = 0, sms = 148, b1 = 1, b2 = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_rowdot, kThreads, s1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_coltile, kThreads, s2);
+    g_grid1 = sms * (b1 > 0 ? b1 : 1);  // persistent: one resident wave
+    g_grid2 = sms * (b2 > 0 ? b2 : 1);
+    configured = true;
+  }
+  const int g1 = f->grid > 0 ? f->grid : g_grid1, g2 = f->grid > 0 ? f->grid : g_grid2;
+  k_rowdot<<<g1 < f->n_units ? g1 : f->n_units, kThreads, s1, st>>>(*f, rhs_perm);
   k_zreduce<<<(f->n * 32 + 255) / 256, 256, 0, st>>>(*f);
-  k_coltile<<<f->n_units, kThreads, 0, st>>>(*f);
+  k_coltile<<<g2 < f->n_units ? g2 : f->n_units, kThreads, s2, st>>>(*f);
   if (scatter)
     k_xreduce<true><<<(f->n + 255) / 256, 256, 0, st>>>(*f, out);
   else
