@@ -46,11 +46,11 @@ typedef struct hdk_material {
  * Row r of S' is dense over columns [r - len_r + 1, r] (its etree subtree),
  * so no column indices are stored.  Columns are cut into tiles of tile_w;
  * a segment is one row's part inside one tile.  The values are stored
- * tile-major as one stream: each work unit (a run of segments of one tile)
- * is a run of chunks, each chunk a 16-byte aligned contiguous block of at most
- * HDK_CHUNK_VALS values holding whole segments, with its segment descriptors
- * contiguous too — so both passes stream chunks into shared memory with bulk
- * asynchronous copies (factor.cpp:106-109). */
+ * tile-major as one stream of chunks: a chunk is a 16-byte aligned contiguous
+ * block of at most HDK_CHUNK_VALS values holding whole segments of one tile,
+ * with its segment descriptors contiguous too.  Each pass hands every
+ * persistent CTA an equal contiguous range of chunks, streamed into shared
+ * memory with bulk asynchronous copies (factor.cpp:106-109). */
 #define HDK_CHUNK_VALS 3072
 #define HDK_CHUNK_SEGS 256
 
@@ -65,23 +65,22 @@ typedef struct hdk_chunk {  /* 24 bytes */
   long long off;            /* stream offset (doubles, even) */
   int len;                  /* values incl. padding (even) */
   int seg0, nseg;           /* descriptors [seg0, seg0 + nseg) */
-  int unit;
+  int tile;
 } hdk_chunk;
 
 typedef struct hdk_factor {
   int n;                  /* free vertices */
-  int tile_w, n_tiles, n_units, n_chunks, grid;
+  int tile_w, n_tiles, n_chunks;
+  int max_ctas;           /* part2 holds (n_tiles + max_ctas) tile partials */
   const double* sval;     /* tile-major value stream */
   const hdk_seg* seg;
   const hdk_chunk* chunk;
-  const int* unit_chunk;  /* n_units+1 */
-  const int* unit_tile;   /* n_units */
-  const int* tile_unit;   /* n_tiles+1: units of tile t are contiguous */
+  const int* tile_chunk;  /* n_tiles+1: first chunk of each tile */
   const int* row_pslot;   /* n+1: partial-dot slots of row r */
   const int* p2v;         /* n: elimination position -> vertex */
   const int* v2p;         /* nv: vertex -> position or -1 (fixed) */
   double* part1;          /* 3*row_pslot[n] scratch */
-  double* part2;          /* 3*tile_w*n_units scratch */
+  double* part2;          /* 3*tile_w*(n_tiles+max_ctas) scratch */
   double* z;              /* 3*n scratch */
 } hdk_factor;
 

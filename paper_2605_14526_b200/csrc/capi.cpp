@@ -190,7 +190,8 @@ hd_status hd_factor_stats(const hd_scene* scene, char** stats_json) {
     j["l_nnz"] = F.l_nnz;
     j["factor_millis"] = F.millis;
     j["segments"] = F.seg.size();
-    j["work_units"] = F.unit_tile.size();
+    j["chunks"] = F.chunks.size();
+    j["stream_values"] = F.stream.size();
     j["weight_contrast"] = s.material.contrast();
     j["refactorizations"] = 1;
     j["inverse_residual"] = factor_inverse_residual(F);

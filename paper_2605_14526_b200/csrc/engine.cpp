@@ -247,10 +247,9 @@ void Engine::build_factor_device() {
   const HostFactor& F = hf_;
   df_.n = F.n;
   df_.tile_w = F.tile_w;
-  df_.n_tiles = static_cast<int>(F.tile_unit.size()) - 1;
-  df_.n_units = static_cast<int>(F.unit_tile.size());
+  df_.n_tiles = static_cast<int>(F.tile_chunk.size()) - 1;
   df_.n_chunks = static_cast<int>(F.chunks.size());
-  df_.grid = 0;
+  df_.max_ctas = 148 * 8;
   df_.sval = A.upload(F.stream);
   static_assert(sizeof(hdk_seg) == sizeof(SegDesc), "segment descriptor layout");
   static_assert(sizeof(hdk_chunk) == sizeof(ChunkDesc), "chunk descriptor layout");
@@ -260,14 +259,12 @@ void Engine::build_factor_device() {
   hdk_chunk* ch = A.alloc<hdk_chunk>(F.chunks.size());
   DevArena::copy_h2d(ch, F.chunks.data(), sizeof(ChunkDesc) * F.chunks.size());
   df_.chunk = ch;
-  df_.unit_chunk = A.upload(F.unit_chunk);
-  df_.unit_tile = A.upload(F.unit_tile);
-  df_.tile_unit = A.upload(F.tile_unit);
+  df_.tile_chunk = A.upload(F.tile_chunk);
   df_.row_pslot = A.upload(F.row_pslot);
   df_.p2v = A.upload(F.p2v);
   df_.v2p = A.upload(F.v2p);
   df_.part1 = A.alloc<double>(3 * static_cast<size_t>(F.row_pslot.back()));
-  df_.part2 = A.alloc<double>(3 * static_cast<size_t>(F.tile_w) * df_.n_units);
+  df_.part2 = A.alloc<double>(3 * static_cast<size_t>(F.tile_w) * (df_.n_tiles + df_.max_ctas));
   df_.z = A.alloc<double>(3 * static_cast<size_t>(F.n));
   rhs_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
   fixc_ = A.alloc<double>(3 * static_cast<size_t>(F.n));

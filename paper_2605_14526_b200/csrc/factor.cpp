@@ -14,8 +14,9 @@
 //  * the elimination order is postordered, so every row of S' is dense over a
 //    contiguous column range (its etree subtree) and is stored without column
 //    indices;
-//  * rows are cut into column-tile segments grouped into balanced work units
-//    for the two streaming passes (solve.cu).
+//  * rows are cut into 256-column tile segments, packed tile-major into
+//    16-byte aligned chunks that the two streaming passes (solve.cu) split
+//    evenly over persistent CTAs.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -408,7 +409,7 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
       }
     }
   });
-  // 6. segments / work units
+  // 6. segments (row parts inside 256-column tiles)
   const int W = F.tile_w;
   const int ntiles = (n + W - 1) / W;
   F.row_pslot.assign(n + 1, 0);
@@ -422,44 +423,20 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
       per_tile[t].push_back({F.row_off[r] + (clo - first), r, clo, chi - clo + 1, F.row_pslot[r] + (t - t0)});
     }
   }
-  const long long target = std::max<long long>(8192, F.row_off[n] / (148LL * 4));
-  F.tile_unit.assign(ntiles + 1, 0);
-  F.unit_seg.push_back(0);
-  for (int t = 0; t < ntiles; ++t) {
-    long long acc = 0;
-    int since = 0;
-    for (const Segment& s : per_tile[t]) {
-      F.seg.push_back(s);
-      acc += s.len;
-      ++since;
-      if (acc >= target) {
-        F.unit_seg.push_back(static_cast<int>(F.seg.size()));
-        F.unit_tile.push_back(t);
-        acc = 0;
-        since = 0;
-      }
-    }
-    if (since > 0) {
-      F.unit_seg.push_back(static_cast<int>(F.seg.size()));
-      F.unit_tile.push_back(t);
-    }
-    F.tile_unit[t + 1] = static_cast<int>(F.unit_tile.size());
-  }
-  // 6b. tile-major value stream: units -> chunks of whole segments, every chunk
-  //     16-byte aligned, descriptors contiguous per chunk
+  for (int t = 0; t < ntiles; ++t) F.seg.insert(F.seg.end(), per_tile[t].begin(), per_tile[t].end());
+  // 6b. tile-major value stream: per tile, chunks of whole segments, every
+  //     chunk 16-byte aligned, descriptors contiguous per chunk
   {
-    const int nu = static_cast<int>(F.unit_tile.size());
-    F.unit_chunk.assign(nu + 1, 0);
-    F.stream.reserve(static_cast<size_t>(F.row_off[n] * 1.05) + 16);
-    for (int u = 0; u < nu; ++u) {
-      const int t = F.unit_tile[u];
-      int s = F.unit_seg[u];
-      const int se = F.unit_seg[u + 1];
-      while (s < se) {
-        ChunkDesc c{static_cast<long long>(F.stream.size()), 0, static_cast<int>(F.sdesc.size()), 0, u};
+    F.tile_chunk.assign(ntiles + 1, 0);
+    F.stream.reserve(static_cast<size_t>(F.row_off[n] * 1.02) + 16);
+    for (int t = 0; t < ntiles; ++t) {
+      const auto& list = per_tile[t];
+      size_t s = 0;
+      while (s < list.size()) {
+        ChunkDesc c{static_cast<long long>(F.stream.size()), 0, static_cast<int>(F.sdesc.size()), 0, t};
         int vals = 0;
-        while (s < se && c.nseg < HDK_SEGS && vals + F.seg[s].len <= HDK_VALS) {
-          const Segment& g = F.seg[s];
+        while (s < list.size() && c.nseg < HDK_SEGS && vals + list[s].len <= HDK_VALS) {
+          const Segment& g = list[s];
           F.sdesc.push_back({g.row, g.pslot, (g.clo - t * W) | (g.len << 16), vals});
           F.stream.insert(F.stream.end(), F.sval.begin() + g.off, F.sval.begin() + g.off + g.len);
           vals += g.len;
@@ -473,7 +450,7 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
         c.len = vals;
         F.chunks.push_back(c);
       }
-      F.unit_chunk[u + 1] = static_cast<int>(F.chunks.size());
+      F.tile_chunk[t + 1] = static_cast<int>(F.chunks.size());
     }
   }
   // 7. A_ff and A_fd in elimination order (apply_a_free / fixed coupling)

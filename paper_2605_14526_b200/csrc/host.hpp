@@ -110,7 +110,7 @@ struct Csr {
 // Explicit inverse factor A_ff^{-1} = S'^T S' (see hdk.h for the layout).
 struct Segment { long long off; int row, clo, len, pslot; };  // off: row-major sval
 struct SegDesc { int row, pslot, clo_len, coff; };              // device descriptor (hdk_seg)
-struct ChunkDesc { long long off; int len, seg0, nseg, unit; };  // device chunk (hdk_chunk)
+struct ChunkDesc { long long off; int len, seg0, nseg, tile; };  // device chunk (hdk_chunk)
 struct HostFactor {
   int n = 0, nv = 0;
   std::vector<int> p2v, v2p, fixed;
@@ -119,12 +119,12 @@ struct HostFactor {
   Vec sval;
   int tile_w = 256;
   std::vector<Segment> seg;
-  std::vector<int> unit_seg, unit_tile, tile_unit, row_pslot;
+  std::vector<int> row_pslot;
   // tile-major stream for the device passes
   Vec stream;
   std::vector<SegDesc> sdesc;
   std::vector<ChunkDesc> chunks;
-  std::vector<int> unit_chunk;
+  std::vector<int> tile_chunk;
   Csr a_ff;  // free x free, elimination order
   Csr a_fd;  // free rows (elimination order) x fixed columns (index into fixed)
   long long l_nnz = 0;

@@ -7,8 +7,9 @@
 // row r is dense over its etree subtree and needs no column indices (8 B per
 // nonzero instead of the reference's 12 B).  Values are stored tile-major as
 // one stream of 16-byte aligned chunks (whole row segments of one 256-column
-// tile), so each pass is a pure stream: persistent CTAs walk their work units
-// and a single elected thread keeps a ring of kStages chunks in flight with
+// tile), so each pass is a pure stream: persistent CTA b owns the contiguous
+// chunk range [b C / G, (b+1) C / G) and a single elected thread keeps a ring
+// of kStages chunks in flight with
 // bulk asynchronous copies (cp.async.bulk, the TMA engine's 1-D mode) that
 // complete on mbarriers, while 8 warps consume the chunk in shared memory.
 // Lane j owns the tile columns j + 32 m (m = 0..7): the right-hand side
@@ -17,8 +18,8 @@
 //   pass 1  k_rowdot   partial z_{r,t} = S'(r, tile t) . b_t   (warp per segment)
 //   reduce  k_zreduce  z_r = sum_t z_{r,t}                     (warp per row, fixed order)
 //   pass 2  k_coltile  x_t += S'(r, tile t)^T z_r               (warp-private accumulators,
-//                                                               fixed-order CTA fold per unit)
-//   reduce  k_xreduce  x_c = sum over the tile's units; scatter to xyz-interleaved
+//                                                               fixed-order CTA fold per tile)
+//   reduce  k_xreduce  x_c = sum over the CTAs that touched the tile; scatter
 // Work assignment and every sum are fixed, so results are bitwise reproducible.
 #include <cuda_runtime.h>
 
@@ -69,32 +70,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Chunk sequence of one persistent CTA: its units u = blockIdx.x + k * gridDim.x
-// in order, each unit's chunks in order.
-struct ChunkIter {
-  int u, c, cend, nu;
-  __device__ __forceinline__ void start(const hdk_factor& f) {
-    nu = f.n_units;
-    u = blockIdx.x;
-    c = u < nu ? f.unit_chunk[u] : 0;
-    cend = u < nu ? f.unit_chunk[u + 1] : 0;
-    skip_empty(f);
-  }
-  __device__ __forceinline__ void skip_empty(const hdk_factor& f) {
-    while (u < nu && c >= cend) {
-      u += gridDim.x;
-      if (u < nu) {
-        c = f.unit_chunk[u];
-        cend = f.unit_chunk[u + 1];
-      }
-    }
-  }
-  __device__ __forceinline__ bool valid() const { return u < nu; }
-  __device__ __forceinline__ void next(const hdk_factor& f) {
-    ++c;
-    skip_empty(f);
-  }
-};
+// Balanced contiguous chunk ranges: CTA b of G owns [first(b), first(b+1)).
+__device__ __forceinline__ int range_first(long long b, int G, int C) { return static_cast<int>(b * C / G); }
+// The CTA owning chunk c (G <= C, so no range is empty).
+__device__ __forceinline__ int cta_of(long long c, int G, int C) {
+  return static_cast<int>(((c + 1) * G + C - 1) / C) - 1;
+}
 
 template <int S>
 struct Ring {
@@ -122,29 +103,29 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
     mbar_fence_init();
   }
   __syncthreads();
-  ChunkIter prod, cons;
-  prod.start(f);
-  cons = prod;
+  const int c_beg = range_first(blockIdx.x, gridDim.x, f.n_chunks);
+  const int c_end = range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
+  int prod = c_beg;
   if (threadIdx.x == 0)
-    for (int s = 0; s < kStages1 && prod.valid(); ++s, prod.next(f)) issue(f, ring, s, prod.c);
+    for (int s = 0; s < kStages1 && prod < c_end; ++s, ++prod) issue(f, ring, s, prod);
   double b0[kM], b1[kM], b2[kM];
   int tile = -1;
-  for (int k = 0; cons.valid(); ++k, cons.next(f)) {
+  for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
     const int st = k % kStages1;
-    const int t = f.unit_tile[cons.u];
-    if (t != tile) {  // right-hand side of the tile into registers
-      tile = t;
+    const hdk_chunk ch = f.chunk[c];
+    if (ch.tile != tile) {  // right-hand side of the tile into registers
+      tile = ch.tile;
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
-        const int c = t * kW + lane + 32 * m;
-        const bool ok = c < f.n;
-        b0[m] = ok ? __ldg(rhs + 3 * (size_t)c) : 0.0;
-        b1[m] = ok ? __ldg(rhs + 3 * (size_t)c + 1) : 0.0;
-        b2[m] = ok ? __ldg(rhs + 3 * (size_t)c + 2) : 0.0;
+        const int col = tile * kW + lane + 32 * m;
+        const bool ok = col < f.n;
+        b0[m] = ok ? __ldg(rhs + 3 * (size_t)col) : 0.0;
+        b1[m] = ok ? __ldg(rhs + 3 * (size_t)col + 1) : 0.0;
+        b2[m] = ok ? __ldg(rhs + 3 * (size_t)col + 2) : 0.0;
       }
     }
     mbar_wait(&ring.full[st], (k / kStages1) & 1);
-    const int nseg = f.chunk[cons.c].nseg;
+    const int nseg = ch.nseg;
     const double* vals = ring.vals[st];
     for (int i = warp; i < nseg; i += kWarps) {
       const hdk_seg sg = ring.segs[st][i];
@@ -175,10 +156,10 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
       }
     }
     __syncthreads();  // stage st fully consumed
-    if (threadIdx.x == 0 && prod.valid()) {
+    if (threadIdx.x == 0 && prod < c_end) {
       fence_proxy_async();
-      issue(f, ring, st, prod.c);
-      prod.next(f);
+      issue(f, ring, st, prod);
+      ++prod;
     }
   }
 }
@@ -217,7 +198,7 @@ struct Pass2Smem {
   double zc[kSegs][3];
 };
 
-__device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& sm, int unit, double (&x0)[kM],
+__device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& sm, int slot, double (&x0)[kM],
                                                double (&x1)[kM], double (&x2)[kM]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // fixed-order fold: warps 4..7 into 0..3, 2..3 into 0..1, 1 into 0
@@ -247,7 +228,7 @@ __device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& s
   if (warp == 0) {
 #pragma unroll
     for (int m = 0; m < kM; ++m) {
-      double* p = f.part2 + 3 * ((size_t)unit * kW + lane + 32 * m);
+      double* p = f.part2 + 3 * ((size_t)slot * kW + lane + 32 * m);
       p[0] = x0[m];
       p[1] = x1[m];
       p[2] = x2[m];
@@ -267,23 +248,24 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
     mbar_fence_init();
   }
   __syncthreads();
-  ChunkIter prod, cons;
-  prod.start(f);
-  cons = prod;
+  const int c_beg = range_first(blockIdx.x, gridDim.x, f.n_chunks);
+  const int c_end = range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
+  int prod = c_beg;
   if (threadIdx.x == 0)
-    for (int s = 0; s < kStages2 && prod.valid(); ++s, prod.next(f)) issue(f, ring, s, prod.c);
+    for (int s = 0; s < kStages2 && prod < c_end; ++s, ++prod) issue(f, ring, s, prod);
   double x0[kM], x1[kM], x2[kM];
 #pragma unroll
   for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
-  int unit = -1;
-  for (int k = 0; cons.valid(); ++k, cons.next(f)) {
+  int tile = -1;
+  for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
     const int st = k % kStages2;
-    if (cons.u != unit) {
-      if (unit >= 0) fold_and_write(f, sm, unit, x0, x1, x2);
-      unit = cons.u;
+    const hdk_chunk ch = f.chunk[c];
+    if (ch.tile != tile) {  // partial of the previous tile: slot tile + b is unique
+      if (tile >= 0) fold_and_write(f, sm, tile + blockIdx.x, x0, x1, x2);
+      tile = ch.tile;
     }
     mbar_wait(&ring.full[st], (k / kStages2) & 1);
-    const int nseg = f.chunk[cons.c].nseg;
+    const int nseg = ch.nseg;
     // gather z of the chunk's rows once (one round trip for the whole chunk)
     if (threadIdx.x < nseg) {
       const double* z = f.z + 3 * (size_t)ring.segs[st][threadIdx.x].row;
@@ -310,24 +292,26 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
       }
     }
     __syncthreads();  // stage st and zc fully consumed
-    if (threadIdx.x == 0 && prod.valid()) {
+    if (threadIdx.x == 0 && prod < c_end) {
       fence_proxy_async();
-      issue(f, ring, st, prod.c);
-      prod.next(f);
+      issue(f, ring, st, prod);
+      ++prod;
     }
   }
-  if (unit >= 0) fold_and_write(f, sm, unit, x0, x1, x2);
+  if (tile >= 0) fold_and_write(f, sm, tile + blockIdx.x, x0, x1, x2);
 }
 
+// x_c = sum of the tile partials of the CTAs whose chunk ranges touch the
+// column's tile (CTA order), scattered to the full vector.
 template <bool kScatter>
-__global__ void k_xreduce(hdk_factor f, double* __restrict__ out) {
+__global__ void k_xreduce(hdk_factor f, int G, double* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= f.n) return;
   const int t = c / kW, cl = c - t * kW;
+  const int b0 = cta_of(f.tile_chunk[t], G, f.n_chunks), b1 = cta_of(f.tile_chunk[t + 1] - 1, G, f.n_chunks);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  const int ue = f.tile_unit[t + 1];
-  for (int u = f.tile_unit[t]; u < ue; ++u) {
-    const double* p = f.part2 + 3 * ((size_t)u * kW + cl);
+  for (int b = b0; b <= b1; ++b) {
+    const double* p = f.part2 + 3 * ((size_t)(t + b) * kW + cl);
     a0 += p[0];
     a1 += p[1];
     a2 += p[2];
@@ -357,14 +341,16 @@ int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatte
     g_grid2 = sms * (b2 > 0 ? b2 : 1);
     configured = true;
   }
-  const int g1 = f->grid > 0 ? f->grid : g_grid1, g2 = f->grid > 0 ? f->grid : g_grid2;
-  k_rowdot<<<g1 < f->n_units ? g1 : f->n_units, kThreads, s1, st>>>(*f, rhs_perm);
+  const int g1 = g_grid1 < f->n_chunks ? g_grid1 : f->n_chunks;
+  int g2 = g_grid2 < f->n_chunks ? g_grid2 : f->n_chunks;
+  if (g2 > f->max_ctas) g2 = f->max_ctas;
+  k_rowdot<<<g1, kThreads, s1, st>>>(*f, rhs_perm);
   k_zreduce<<<(f->n * 32 + 255) / 256, 256, 0, st>>>(*f);
-  k_coltile<<<g2 < f->n_units ? g2 : f->n_units, kThreads, s2, st>>>(*f);
+  k_coltile<<<g2, kThreads, s2, st>>>(*f);
   if (scatter)
-    k_xreduce<true><<<(f->n + 255) / 256, 256, 0, st>>>(*f, out);
+    k_xreduce<true><<<(f->n + 255) / 256, 256, 0, st>>>(*f, g2, out);
   else
-    k_xreduce<false><<<(f->n + 255) / 256, 256, 0, st>>>(*f, out);
+    k_xreduce<false><<<(f->n + 255) / 256, 256, 0, st>>>(*f, g2, out);
   return static_cast<int>(cudaGetLastError());
 }
 

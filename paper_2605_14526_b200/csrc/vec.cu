@@ -39,27 +39,32 @@ __device__ __forceinline__ void block_partials(double (&v)[NQ], double* partial)
   }
 }
 
-// Single-block fold of partial slot q over all blocks (fixed order).
-__device__ __forceinline__ double fold(const double* partial, int q) {
-  __shared__ double sm[kT / 32];
-  double s = 0.0;
-  for (int b = threadIdx.x; b < HDK_RED_BLOCKS; b += kT) s += partial[b * HDK_RED_Q + q];
+// Single-block fold of partial slots [0, nq) over all blocks (fixed order):
+// warp w folds slots w, w+8, ...; lanes stride over blocks, then a fixed
+// shuffle tree.  out must be shared memory; the caller syncs after.
+__device__ __forceinline__ void fold_all(const double* partial, int nq, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int q = warp; q < nq; q += kT / 32) {
+    double s = 0.0;
+    for (int b = lane; b < HDK_RED_BLOCKS; b += 32) s += partial[b * HDK_RED_Q + q];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
-  __syncthreads();
-  double t = 0.0;
-#pragma unroll
-  for (int w = 0; w < kT / 32; ++w) t += sm[w];
-  return t;  // valid in every thread
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[q] = s;
+  }
 }
 
-__device__ __forceinline__ double gather3(const hdk_vtx& x, const double* __restrict__ ef, int v, int a) {
-  double acc = 0.0;
+// Fixed-order sum of the element forces incident to vertex v (ascending
+// element order = the reference's serial scatter order).
+__device__ __forceinline__ void gather_vtx(const hdk_vtx& x, const double* __restrict__ ef, int v, double& s0,
+                                           double& s1, double& s2) {
+  s0 = s1 = s2 = 0.0;
   const int e = x.inc_off[v + 1];
-  for (int j = x.inc_off[v]; j < e; ++j) acc += ef[3 * (size_t)x.inc[j] + a];
-  return acc;
+  for (int j = x.inc_off[v]; j < e; ++j) {
+    const double* p = ef + 3 * (size_t)__ldg(x.inc + j);
+    s0 += __ldg(p);
+    s1 += __ldg(p + 1);
+    s2 += __ldg(p + 2);
+  }
 }
 
 __global__ void k_free_fall(hdk_vtx x, const double* q, const double* v, const double* f, double h, int hv,
@@ -80,10 +85,12 @@ __global__ void k_free_fall(hdk_vtx x, const double* q, const double* v, const d
 __global__ void k_gather(hdk_vtx x, const double* ef, double cm, const double* base, const double* add, double* out) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= x.nv) return;
+  double g[3] = {0.0, 0.0, 0.0};
+  if (ef) gather_vtx(x, ef, v, g[0], g[1], g[2]);
   for (int a = 0; a < 3; ++a) {
     double s = cm * x.mass[v] * base[3 * v + a];
     if (add) s += add[3 * v + a];
-    if (ef) s += gather3(x, ef, v, a);
+    s += g[a];
     out[3 * v + a] = s;
   }
 }
@@ -96,10 +103,12 @@ __global__ void __launch_bounds__(kT) k_gather_rhs(hdk_vtx x, const double* __re
   for (int v = blockIdx.x * kT + threadIdx.x; v < x.nv; v += HDK_RED_BLOCKS * kT) {
     const int p = x.v2p[v];
     const double m = x.mass[v];
+    double g[3];
+    gather_vtx(x, ef, v, g[0], g[1], g[2]);
     for (int a = 0; a < 3; ++a) {
       const size_t i = 3 * (size_t)v + a;
       double b = m * qt[i] * inv_h2;  // M q~ / h^2 (forward.cpp:99)
-      b += gather3(x, ef, v, a);      // + sum_e V G^T (w p*)
+      b += g[a];                      // + sum_e V G^T (w p*)
       b += damp[i];                   // + damping_rhs
       const double d = b - bprev[i];
       acc[0] += d * d;
@@ -115,11 +124,9 @@ __global__ void k_gather_perm(hdk_vtx x, const double* base, const double* ef, d
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= x.n) return;
   const int v = x.p2v[p];
-  for (int a = 0; a < 3; ++a) {
-    double s = base[3 * (size_t)v + a];
-    if (ef) s += gather3(x, ef, v, a);
-    rhs[3 * (size_t)p + a] = s;
-  }
+  double g[3] = {0.0, 0.0, 0.0};
+  if (ef) gather_vtx(x, ef, v, g[0], g[1], g[2]);
+  for (int a = 0; a < 3; ++a) rhs[3 * (size_t)p + a] = base[3 * (size_t)v + a] + g[a];
 }
 
 __global__ void k_fixed_coupling(hdk_csr c, const int* fixed, const double* q, double* out) {
@@ -221,11 +228,8 @@ __device__ bool small_ldlt(double* a, int n, const double* b, double* x) {
 
 __global__ void __launch_bounds__(kT) k_aa_solve(hdk_ctl* ctl, const double* partial, int mode) {
   __shared__ double s[2 * HDK_AA_MAX + 2];
-  for (int q = 0; q < 2 * HDK_AA_MAX + 2; ++q) {
-    const double v = fold(partial, q);
-    if (threadIdx.x == 0) s[q] = v;
-    __syncthreads();
-  }
+  fold_all(partial, 2 * HDK_AA_MAX + 2, s);
+  __syncthreads();
   if (threadIdx.x != 0) return;
   if (mode == 1) {  // adjoint backbone: convergence test before mixing (backward.cpp:191-193)
     ctl->iterations += 1;
@@ -320,8 +324,12 @@ __global__ void __launch_bounds__(kT) k_aa_mix(hdk_vtx x, hdk_ctl* ctl, const do
 
 __global__ void __launch_bounds__(kT) k_gate(hdk_ctl* ctl, const double* pb, const double* pq,
                                              cudaGraphConditionalHandle handle, int use_handle) {
-  const double db = fold(pb, 0), bb = fold(pb, 1), dq = fold(pq, 0), qq = fold(pq, 1);
+  __shared__ double sb[2], sq[2];
+  fold_all(pb, 2, sb);
+  fold_all(pq, 2, sq);
+  __syncthreads();
   if (threadIdx.x != 0) return;
+  const double db = sb[0], bb = sb[1], dq = sq[0], qq = sq[1];
   const int k = ctl->k;
   const double er = ctl->eps_rel, ea = ctl->eps_abs;
   const bool gate = k >= 1 && sqrt(dq) <= er * sqrt(qq) + ea && sqrt(db) <= er * sqrt(bb) + ea;
@@ -388,9 +396,12 @@ __global__ void __launch_bounds__(kT) k_tr_partials(hdk_vtx x, int ne, const dou
 }
 
 __global__ void __launch_bounds__(kT) k_tr_final(hdk_ctl* ctl, const double* pm, const double* pe, double inv_h2) {
-  const double model_raw = fold(pm, 0);
-  const double e_prev = fold(pe, 0), e_star = fold(pe, 1), i_prev = fold(pe, 2), i_star = fold(pe, 3);
+  __shared__ double sm_[1], se[4];
+  fold_all(pm, 1, sm_);
+  fold_all(pe, 4, se);
+  __syncthreads();
   if (threadIdx.x != 0) return;
+  const double model_raw = sm_[0], e_prev = se[0], e_star = se[1], i_prev = se[2], i_star = se[3];
   const double model = 0.5 * fabs(model_raw);
   double rho = 1.0;
   if (model >= 1e-12) {
@@ -415,6 +426,8 @@ __global__ void k_route_vtx(hdk_vtx x, const double* mu, const double* efd, cons
   if (v >= x.nv) return;
   const double m = x.mass[v];
   const bool fixed = x.v2p[v] < 0;
+  double g[3] = {0.0, 0.0, 0.0};
+  if (efd) gather_vtx(x, efd, v, g[0], g[1], g[2]);
   for (int a = 0; a < 3; ++a) {
     const size_t i = 3 * (size_t)v + a;
     const double u = mu[i];
@@ -422,7 +435,7 @@ __global__ void k_route_vtx(hdk_vtx x, const double* mu, const double* efd, cons
     double dv = m * u / h;                     // M mu / h
     double damp = 0.0;
     if (alpha > 0) damp = (alpha / h) * (m * u);
-    if (efd) damp += gather3(x, efd, v, a);
+    if (efd) damp += g[a];
     double dq = m * u / (h * h) + damp;        // M mu / h^2 + damping_rhs(mu)
     if (v == hv) {
       dv += -hd * u;
