@@ -31,12 +31,12 @@ namespace {
 
 constexpr int kW = 256;       // tile width (columns)
 constexpr int kM = kW / 32;   // columns per lane
-constexpr int kWarps = 8;
-constexpr int kThreads = 32 * kWarps;
+constexpr int kWarps = 8;     // consumer warps
+constexpr int kThreads = 32 * (kWarps + 1);  // + one producer warp
 constexpr int kVals = HDK_CHUNK_VALS;
 constexpr int kSegs = HDK_CHUNK_SEGS;
 constexpr int kStages1 = 3;   // pass 1 ring depth (2 CTAs / SM)
-constexpr int kStages2 = 2;   // pass 2 ring depth (plus fold + z buffers; 2 CTAs / SM)
+constexpr int kStages2 = 3;   // pass 2 ring depth (2 CTAs / SM)
 
 static_assert(kW == 256, "tile width is fixed by the factor layout");
 
@@ -50,6 +50,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -69,6 +72,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarps) : "memory"); }
 
 // Balanced contiguous chunk ranges: CTA b of G owns [first(b), first(b+1)).
 __device__ __forceinline__ int range_first(long long b, int G, int C) { return static_cast<int>(b * C / G); }
@@ -82,15 +86,36 @@ struct Ring {
   double vals[S][kVals];
   hdk_seg segs[S][kSegs];
   uint64_t full[S];
+  uint64_t empty[S];
 };
 
 template <int S>
-__device__ __forceinline__ void issue(const hdk_factor& f, Ring<S>& r, int stage, int chunk) {
-  const hdk_chunk ch = f.chunk[chunk];
-  const uint32_t vb = static_cast<uint32_t>(ch.len) * 8u, sb = static_cast<uint32_t>(ch.nseg) * 16u;
-  mbar_expect_tx(&r.full[stage], vb + sb);
-  if (vb) bulk_g2s(r.vals[stage], f.sval + ch.off, vb, &r.full[stage]);
-  bulk_g2s(r.segs[stage], f.seg + ch.seg0, sb, &r.full[stage]);
+__device__ __forceinline__ void ring_init(Ring<S>& r) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&r.full[s], 1);
+      mbar_init(&r.empty[s], kWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+}
+
+// Producer warp (one elected lane): keeps S chunks in flight; a stage is
+// refilled once all consumer warps have released it.
+template <int S>
+__device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_beg, int c_end) {
+  if ((threadIdx.x & 31) != 0) return;
+  for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
+    const int st = k % S;
+    if (k >= S) mbar_wait(&r.empty[st], ((k / S) - 1) & 1);
+    fence_proxy_async();
+    const hdk_chunk ch = f.chunk[c];
+    const uint32_t vb = static_cast<uint32_t>(ch.len) * 8u, sb = static_cast<uint32_t>(ch.nseg) * 16u;
+    mbar_expect_tx(&r.full[st], vb + sb);
+    if (vb) bulk_g2s(r.vals[st], f.sval + ch.off, vb, &r.full[st]);
+    bulk_g2s(r.segs[st], f.seg + ch.seg0, sb, &r.full[st]);
+  }
 }
 
 // ---- pass 1 ------------------------------------------------------------------
@@ -98,16 +123,13 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<kStages1>& ring = *reinterpret_cast<Ring<kStages1>*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages1; ++s) mbar_init(&ring.full[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
+  ring_init(ring);
   const int c_beg = range_first(blockIdx.x, gridDim.x, f.n_chunks);
   const int c_end = range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
-  int prod = c_beg;
-  if (threadIdx.x == 0)
-    for (int s = 0; s < kStages1 && prod < c_end; ++s, ++prod) issue(f, ring, s, prod);
+  if (warp == kWarps) {
+    produce(f, ring, c_beg, c_end);
+    return;
+  }
   double b0[kM], b1[kM], b2[kM];
   int tile = -1;
   for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
@@ -125,9 +147,9 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
       }
     }
     mbar_wait(&ring.full[st], (k / kStages1) & 1);
-    const int nseg = ch.nseg;
     const double* vals = ring.vals[st];
-    for (int i = warp; i < nseg; i += kWarps) {
+    // segment i of the chunk goes to warp (seg0 + i) mod 8: balanced over chunks
+    for (int i = (warp - ch.seg0) & (kWarps - 1); i < ch.nseg; i += kWarps) {
       const hdk_seg sg = ring.segs[st][i];
       const int lo = sg.clo_len & 0xffff, hi = lo + (sg.clo_len >> 16);
       const double* v = vals + sg.coff - lo;  // v[cl] = S'(row, tile column cl)
@@ -155,12 +177,8 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
         p[2] = a2;
       }
     }
-    __syncthreads();  // stage st fully consumed
-    if (threadIdx.x == 0 && prod < c_end) {
-      fence_proxy_async();
-      issue(f, ring, st, prod);
-      ++prod;
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[st]);
   }
 }
 
@@ -195,16 +213,16 @@ __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
 struct Pass2Smem {
   Ring<kStages2> ring;
   double fold[kWarps / 2][3][kW];
-  double zc[kSegs][3];
 };
 
+// Fixed-order fold of the consumer warps' accumulators (4..7 into 0..3, 2..3
+// into 0..1, 1 into 0) and write of the tile partial; consumer warps only.
 __device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& sm, int slot, double (&x0)[kM],
                                                double (&x1)[kM], double (&x2)[kM]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // fixed-order fold: warps 4..7 into 0..3, 2..3 into 0..1, 1 into 0
 #pragma unroll
   for (int half = kWarps / 2; half >= 1; half >>= 1) {
-    __syncthreads();
+    consumers_sync();
     if (warp >= half && warp < 2 * half) {
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
@@ -214,7 +232,7 @@ __device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& s
         sm.fold[warp - half][2][cl] = x2[m];
       }
     }
-    __syncthreads();
+    consumers_sync();
     if (warp < half) {
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
@@ -243,16 +261,13 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
   Pass2Smem& sm = *reinterpret_cast<Pass2Smem*>(smem_raw);
   Ring<kStages2>& ring = sm.ring;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages2; ++s) mbar_init(&ring.full[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
+  ring_init(ring);
   const int c_beg = range_first(blockIdx.x, gridDim.x, f.n_chunks);
   const int c_end = range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
-  int prod = c_beg;
-  if (threadIdx.x == 0)
-    for (int s = 0; s < kStages2 && prod < c_end; ++s, ++prod) issue(f, ring, s, prod);
+  if (warp == kWarps) {
+    produce(f, ring, c_beg, c_end);
+    return;
+  }
   double x0[kM], x1[kM], x2[kM];
 #pragma unroll
   for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
@@ -265,21 +280,25 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
       tile = ch.tile;
     }
     mbar_wait(&ring.full[st], (k / kStages2) & 1);
-    const int nseg = ch.nseg;
-    // gather z of the chunk's rows once (one round trip for the whole chunk)
-    if (threadIdx.x < nseg) {
-      const double* z = f.z + 3 * (size_t)ring.segs[st][threadIdx.x].row;
-      sm.zc[threadIdx.x][0] = __ldg(z);
-      sm.zc[threadIdx.x][1] = __ldg(z + 1);
-      sm.zc[threadIdx.x][2] = __ldg(z + 2);
-    }
-    __syncthreads();
     const double* vals = ring.vals[st];
-    for (int i = warp; i < nseg; i += kWarps) {
+    const int i0 = (warp - ch.seg0) & (kWarps - 1);
+    // z of this warp's segments: lane l holds the l-th one (<= 32 per chunk)
+    double zr0 = 0.0, zr1 = 0.0, zr2 = 0.0;
+    {
+      const int i = i0 + kWarps * lane;
+      if (i < ch.nseg) {
+        const double* z = f.z + 3 * (size_t)ring.segs[st][i].row;
+        zr0 = __ldg(z);
+        zr1 = __ldg(z + 1);
+        zr2 = __ldg(z + 2);
+      }
+    }
+    for (int i = i0, j = 0; i < ch.nseg; i += kWarps, ++j) {
       const hdk_seg sg = ring.segs[st][i];
       const int lo = sg.clo_len & 0xffff, hi = lo + (sg.clo_len >> 16);
       const double* v = vals + sg.coff - lo;
-      const double z0 = sm.zc[i][0], z1 = sm.zc[i][1], z2 = sm.zc[i][2];
+      const double z0 = __shfl_sync(0xffffffffu, zr0, j), z1 = __shfl_sync(0xffffffffu, zr1, j),
+                   z2 = __shfl_sync(0xffffffffu, zr2, j);
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
@@ -291,12 +310,8 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
         }
       }
     }
-    __syncthreads();  // stage st and zc fully consumed
-    if (threadIdx.x == 0 && prod < c_end) {
-      fence_proxy_async();
-      issue(f, ring, st, prod);
-      ++prod;
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[st]);
   }
   if (tile >= 0) fold_and_write(f, sm, tile + blockIdx.x, x0, x1, x2);
 }

@@ -226,60 +226,78 @@ __device__ bool small_ldlt(double* a, int n, const double* b, double* x) {
   return true;
 }
 
-__global__ void __launch_bounds__(kT) k_aa_solve(hdk_ctl* ctl, const double* partial, int mode) {
+__global__ void __launch_bounds__(kT) k_aa_solve(hdk_ctl* gctl, const double* partial, int mode) {
   __shared__ double s[2 * HDK_AA_MAX + 2];
+  __shared__ hdk_ctl c_sh;  // work on a shared-memory copy of the control block
+  {
+    const int* src = reinterpret_cast<const int*>(gctl);
+    int* dst = reinterpret_cast<int*>(&c_sh);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += kT) dst[i] = src[i];
+  }
   fold_all(partial, 2 * HDK_AA_MAX + 2, s);
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  if (mode == 1) {  // adjoint backbone: convergence test before mixing (backward.cpp:191-193)
-    ctl->iterations += 1;
-    const double diff = sqrt(s[2 * HDK_AA_MAX]);
-    const double base = fmax(sqrt(s[2 * HDK_AA_MAX + 1]), 1e-30);
-    ctl->k += 1;
-    if (diff <= ctl->tol * base) {
-      ctl->done = 1;
+  if (threadIdx.x == 0) {
+    hdk_ctl* ctl = &c_sh;
+    bool skip = false;
+    if (mode == 1) {  // adjoint backbone: convergence test before mixing (backward.cpp:191-193)
+      ctl->iterations += 1;
+      const double diff = sqrt(s[2 * HDK_AA_MAX]);
+      const double base = fmax(sqrt(s[2 * HDK_AA_MAX + 1]), 1e-30);
+      ctl->k += 1;
+      if (diff <= ctl->tol * base) {
+        ctl->done = 1;
+        ctl->mixed = 0;
+        skip = true;
+      } else if (ctl->k >= ctl->k_max && ctl->err == 0) {
+        ctl->err = 10;  // AdjointDiverged (cap)
+      }
+    }
+    if (!skip) {
+      const int m = ctl->window;
+      if (ctl->has_last) {
+        const int c = ctl->count;
+        if (c < m) {
+          ctl->count = c + 1;
+        } else {
+          ctl->head = (ctl->head + 1) % m;
+          for (int i = 0; i + 1 < m; ++i)
+            for (int j = 0; j + 1 < m; ++j) ctl->gram[i * HDK_AA_MAX + j] = ctl->gram[(i + 1) * HDK_AA_MAX + (j + 1)];
+        }
+        const int c2 = ctl->count, j = c2 - 1;
+        for (int l = 0; l < c2; ++l) ctl->gram[j * HDK_AA_MAX + l] = ctl->gram[l * HDK_AA_MAX + j] = s[l];
+      }
+      ctl->has_last = 1;
       ctl->mixed = 0;
-      return;
+      const int c2 = ctl->count;
+      double fro2 = 0.0;
+      for (int j = 0; j < c2; ++j) fro2 += ctl->gram[j * HDK_AA_MAX + j];
+      if (c2 > 0 && fro2 > 0.0) {
+        double a[HDK_AA_MAX * HDK_AA_MAX], rhs[HDK_AA_MAX], gam[HDK_AA_MAX];
+        for (int i = 0; i < c2; ++i) {
+          for (int j = 0; j < c2; ++j) a[i * c2 + j] = ctl->gram[i * HDK_AA_MAX + j];
+          a[i * c2 + i] += 1e-6 * fro2 / m;
+          rhs[i] = s[HDK_AA_MAX + i];
+        }
+        const bool ok = small_ldlt(a, c2, rhs, gam);
+        double gn = 0.0;
+        for (int i = 0; i < c2; ++i) gn += gam[i] * gam[i];
+        if (!ok || !(sqrt(gn) <= ctl->guard)) {  // guard: discard history (forward.cpp:43-47)
+          ctl->count = 0;
+          ctl->head = 0;
+          ctl->has_last = 0;
+        } else {
+          for (int i = 0; i < c2; ++i) ctl->gamma[i] = gam[i];
+          ctl->mixed = 1;
+        }
+      }
     }
-    if (ctl->k >= ctl->k_max && ctl->err == 0) ctl->err = 10;  // AdjointDiverged (cap)
   }
-  const int m = ctl->window;
-  if (ctl->has_last) {
-    const int c = ctl->count;
-    if (c < m) {
-      ctl->count = c + 1;
-    } else {
-      ctl->head = (ctl->head + 1) % m;
-      for (int i = 0; i + 1 < m; ++i)
-        for (int j = 0; j + 1 < m; ++j) ctl->gram[i * HDK_AA_MAX + j] = ctl->gram[(i + 1) * HDK_AA_MAX + (j + 1)];
-    }
-    const int c2 = ctl->count, j = c2 - 1;
-    for (int l = 0; l < c2; ++l) ctl->gram[j * HDK_AA_MAX + l] = ctl->gram[l * HDK_AA_MAX + j] = s[l];
+  __syncthreads();
+  {
+    const int* src = reinterpret_cast<const int*>(&c_sh);
+    int* dst = reinterpret_cast<int*>(gctl);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += kT) dst[i] = src[i];
   }
-  ctl->has_last = 1;
-  ctl->mixed = 0;
-  const int c2 = ctl->count;
-  if (c2 == 0) return;
-  double fro2 = 0.0;
-  for (int j = 0; j < c2; ++j) fro2 += ctl->gram[j * HDK_AA_MAX + j];
-  if (!(fro2 > 0.0)) return;
-  double a[HDK_AA_MAX * HDK_AA_MAX], rhs[HDK_AA_MAX], gam[HDK_AA_MAX];
-  for (int i = 0; i < c2; ++i) {
-    for (int j = 0; j < c2; ++j) a[i * c2 + j] = ctl->gram[i * HDK_AA_MAX + j];
-    a[i * c2 + i] += 1e-6 * fro2 / m;
-    rhs[i] = s[HDK_AA_MAX + i];
-  }
-  const bool ok = small_ldlt(a, c2, rhs, gam);
-  double gn = 0.0;
-  for (int i = 0; i < c2; ++i) gn += gam[i] * gam[i];
-  if (!ok || !(sqrt(gn) <= ctl->guard)) {  // guard: discard history (forward.cpp:43-47)
-    ctl->count = 0;
-    ctl->head = 0;
-    ctl->has_last = 0;
-    return;
-  }
-  for (int i = 0; i < c2; ++i) ctl->gamma[i] = gam[i];
-  ctl->mixed = 1;
 }
 
 __global__ void __launch_bounds__(kT) k_aa_mix(hdk_vtx x, hdk_ctl* ctl, const double* __restrict__ qhat, double* qcur,
