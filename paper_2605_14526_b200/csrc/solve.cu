@@ -182,26 +182,28 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
   }
 }
 
-// z_r = sum of the row's tile partials in tile order; one warp per row.
+// z_r = sum of the row's tile partials in tile order; four lanes per row.
 __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= f.n) return;
-  const int s0 = f.row_pslot[r], s1 = f.row_pslot[r + 1];
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = gid >> 2, sub = gid & 3;
+  const bool live = r < f.n;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  for (int s = s0 + lane; s < s1; s += 32) {
-    const double* p = f.part1 + 3 * (size_t)s;
-    a0 += p[0];
-    a1 += p[1];
-    a2 += p[2];
+  if (live) {
+    const int s1 = f.row_pslot[r + 1];
+    for (int s = f.row_pslot[r] + sub; s < s1; s += 4) {
+      const double* p = f.part1 + 3 * (size_t)s;
+      a0 += p[0];
+      a1 += p[1];
+      a2 += p[2];
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = 2; o > 0; o >>= 1) {
     a0 += __shfl_xor_sync(0xffffffffu, a0, o);
     a1 += __shfl_xor_sync(0xffffffffu, a1, o);
     a2 += __shfl_xor_sync(0xffffffffu, a2, o);
   }
-  if (lane == 0) {
+  if (live && sub == 0) {
     double* z = f.z + 3 * (size_t)r;
     z[0] = a0;
     z[1] = a1;
@@ -360,7 +362,7 @@ int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatte
   int g2 = g_grid2 < f->n_chunks ? g_grid2 : f->n_chunks;
   if (g2 > f->max_ctas) g2 = f->max_ctas;
   k_rowdot<<<g1, kThreads, s1, st>>>(*f, rhs_perm);
-  k_zreduce<<<(f->n * 32 + 255) / 256, 256, 0, st>>>(*f);
+  k_zreduce<<<(f->n * 4 + 255) / 256, 256, 0, st>>>(*f);
   k_coltile<<<g2, kThreads, s2, st>>>(*f);
   if (scatter)
     k_xreduce<true><<<(f->n + 255) / 256, 256, 0, st>>>(*f, g2, out);
