@@ -182,23 +182,25 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
   }
 }
 
-// z_r = sum of the row's tile partials in tile order; four lanes per row.
+// z_r = sum of the row's tile partials in tile order; eight lanes per row,
+// loads issued four at a time before adding.
 __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = gid >> 2, sub = gid & 3;
+  const int r = gid >> 3, sub = gid & 7;
   const bool live = r < f.n;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   if (live) {
     const int s1 = f.row_pslot[r + 1];
-    for (int s = f.row_pslot[r] + sub; s < s1; s += 4) {
+#pragma unroll 4
+    for (int s = f.row_pslot[r] + sub; s < s1; s += 8) {
       const double* p = f.part1 + 3 * (size_t)s;
-      a0 += p[0];
-      a1 += p[1];
-      a2 += p[2];
+      a0 += __ldcg(p);
+      a1 += __ldcg(p + 1);
+      a2 += __ldcg(p + 2);
     }
   }
 #pragma unroll
-  for (int o = 2; o > 0; o >>= 1) {
+  for (int o = 4; o > 0; o >>= 1) {
     a0 += __shfl_xor_sync(0xffffffffu, a0, o);
     a1 += __shfl_xor_sync(0xffffffffu, a1, o);
     a2 += __shfl_xor_sync(0xffffffffu, a2, o);
@@ -362,7 +364,7 @@ int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatte
   int g2 = g_grid2 < f->n_chunks ? g_grid2 : f->n_chunks;
   if (g2 > f->max_ctas) g2 = f->max_ctas;
   k_rowdot<<<g1, kThreads, s1, st>>>(*f, rhs_perm);
-  k_zreduce<<<(f->n * 4 + 255) / 256, 256, 0, st>>>(*f);
+  k_zreduce<<<(f->n * 8 + 255) / 256, 256, 0, st>>>(*f);
   k_coltile<<<g2, kThreads, s2, st>>>(*f);
   if (scatter)
     k_xreduce<true><<<(f->n + 255) / 256, 256, 0, st>>>(*f, g2, out);

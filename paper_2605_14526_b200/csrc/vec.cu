@@ -40,13 +40,22 @@ __device__ __forceinline__ void block_partials(double (&v)[NQ], double* partial)
 }
 
 // Single-block fold of partial slots [0, nq) over all blocks (fixed order):
-// warp w folds slots w, w+8, ...; lanes stride over blocks, then a fixed
-// shuffle tree.  out must be shared memory; the caller syncs after.
-__device__ __forceinline__ void fold_all(const double* partial, int nq, double* out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int q = warp; q < nq; q += kT / 32) {
+// warp w folds slots w, w + nwarps, ...; each lane issues all of its loads
+// before adding (no latency chain), then a fixed shuffle tree.  out must be
+// shared memory; the caller syncs after.
+constexpr int kFoldPerLane = (HDK_RED_BLOCKS + 31) / 32;
+__device__ __forceinline__ void fold_all(const double* __restrict__ partial, int nq, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int q = warp; q < nq; q += nw) {
+    double v[kFoldPerLane];
+#pragma unroll
+    for (int i = 0; i < kFoldPerLane; ++i) {
+      const int b = lane + 32 * i;
+      v[i] = b < HDK_RED_BLOCKS ? __ldcg(partial + b * HDK_RED_Q + q) : 0.0;
+    }
     double s = 0.0;
-    for (int b = lane; b < HDK_RED_BLOCKS; b += 32) s += partial[b * HDK_RED_Q + q];
+#pragma unroll
+    for (int i = 0; i < kFoldPerLane; ++i) s += v[i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) out[q] = s;
@@ -59,6 +68,7 @@ __device__ __forceinline__ void gather_vtx(const hdk_vtx& x, const double* __res
                                            double& s1, double& s2) {
   s0 = s1 = s2 = 0.0;
   const int e = x.inc_off[v + 1];
+#pragma unroll 4
   for (int j = x.inc_off[v]; j < e; ++j) {
     const double* p = ef + 3 * (size_t)__ldg(x.inc + j);
     s0 += __ldg(p);
@@ -134,6 +144,7 @@ __global__ void k_gather_perm(hdk_vtx x, const double* __restrict__ base, const 
     v = x.p2v[p];
     if (ef) {
       const int e = x.inc_off[v + 1];
+#pragma unroll 4
       for (int j = x.inc_off[v] + sub; j < e; j += 8) {
         const double* q = ef + 3 * (size_t)__ldg(x.inc + j);
         s0 += __ldg(q);
@@ -252,13 +263,14 @@ __device__ bool small_ldlt(double* a, int n, const double* b, double* x) {
   return true;
 }
 
-__global__ void __launch_bounds__(kT) k_aa_solve(hdk_ctl* gctl, const double* partial, int mode) {
+constexpr int kSolveT = 32 * (2 * HDK_AA_MAX + 2);  // one warp per folded quantity
+__global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const double* partial, int mode) {
   __shared__ double s[2 * HDK_AA_MAX + 2];
   __shared__ hdk_ctl c_sh;  // work on a shared-memory copy of the control block
   {
     const int* src = reinterpret_cast<const int*>(gctl);
     int* dst = reinterpret_cast<int*>(&c_sh);
-    for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += kT) dst[i] = src[i];
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += blockDim.x) dst[i] = src[i];
   }
   fold_all(partial, 2 * HDK_AA_MAX + 2, s);
   __syncthreads();
@@ -322,7 +334,7 @@ __global__ void __launch_bounds__(kT) k_aa_solve(hdk_ctl* gctl, const double* pa
   {
     const int* src = reinterpret_cast<const int*>(&c_sh);
     int* dst = reinterpret_cast<int*>(gctl);
-    for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += kT) dst[i] = src[i];
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += blockDim.x) dst[i] = src[i];
   }
 }
 
@@ -592,7 +604,7 @@ HDK_API int hdk_aa_dots(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, cons
 }
 
 HDK_API int hdk_aa_solve(hdk_ctl* ctl, const double* partial, int mode, void* stream) {
-  k_aa_solve<<<1, kT, 0, S(stream)>>>(ctl, partial, mode);
+  k_aa_solve<<<1, kSolveT, 0, S(stream)>>>(ctl, partial, mode);
   return last();
 }
 
