@@ -81,10 +81,15 @@ __device__ __forceinline__ int cta_of(long long c, int G, int C) {
   return static_cast<int>(((c + 1) * G + C - 1) / C) - 1;
 }
 
+struct ChunkInfo {
+  int nseg, tile, seg0, pad;
+};
+
 template <int S>
 struct Ring {
   double vals[S][kVals];
   hdk_seg segs[S][kSegs];
+  ChunkInfo info[S];  // written by the producer before its arrive (release)
   uint64_t full[S];
   uint64_t empty[S];
 };
@@ -106,11 +111,14 @@ __device__ __forceinline__ void ring_init(Ring<S>& r) {
 template <int S>
 __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_beg, int c_end) {
   if ((threadIdx.x & 31) != 0) return;
+  hdk_chunk nxt = c_beg < c_end ? f.chunk[c_beg] : hdk_chunk{};
   for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
     const int st = k % S;
+    const hdk_chunk ch = nxt;
+    if (c + 1 < c_end) nxt = f.chunk[c + 1];  // descriptor prefetch, off the critical path
     if (k >= S) mbar_wait(&r.empty[st], ((k / S) - 1) & 1);
     fence_proxy_async();
-    const hdk_chunk ch = f.chunk[c];
+    r.info[st] = ChunkInfo{ch.nseg, ch.tile, ch.seg0, 0};
     const uint32_t vb = static_cast<uint32_t>(ch.len) * 8u, sb = static_cast<uint32_t>(ch.nseg) * 16u;
     mbar_expect_tx(&r.full[st], vb + sb);
     if (vb) bulk_g2s(r.vals[st], f.sval + ch.off, vb, &r.full[st]);
@@ -134,7 +142,8 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
   int tile = -1;
   for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
     const int st = k % kStages1;
-    const hdk_chunk ch = f.chunk[c];
+    mbar_wait(&ring.full[st], (k / kStages1) & 1);
+    const ChunkInfo ch = ring.info[st];
     if (ch.tile != tile) {  // right-hand side of the tile into registers
       tile = ch.tile;
 #pragma unroll
@@ -146,7 +155,6 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
         b2[m] = ok ? __ldg(rhs + 3 * (size_t)col + 2) : 0.0;
       }
     }
-    mbar_wait(&ring.full[st], (k / kStages1) & 1);
     const double* vals = ring.vals[st];
     // segment i of the chunk goes to warp (seg0 + i) mod 8: balanced over chunks
     for (int i = (warp - ch.seg0) & (kWarps - 1); i < ch.nseg; i += kWarps) {
@@ -278,12 +286,12 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
   int tile = -1;
   for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
     const int st = k % kStages2;
-    const hdk_chunk ch = f.chunk[c];
+    mbar_wait(&ring.full[st], (k / kStages2) & 1);
+    const ChunkInfo ch = ring.info[st];
     if (ch.tile != tile) {  // partial of the previous tile: slot tile + b is unique
       if (tile >= 0) fold_and_write(f, sm, tile + blockIdx.x, x0, x1, x2);
       tile = ch.tile;
     }
-    mbar_wait(&ring.full[st], (k / kStages2) & 1);
     const double* vals = ring.vals[st];
     const int i0 = (warp - ch.seg0) & (kWarps - 1);
     // z of this warp's segments: lane l holds the l-th one (<= 32 per chunk)

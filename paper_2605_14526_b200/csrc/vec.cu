@@ -225,46 +225,94 @@ __global__ void __launch_bounds__(kT) k_aa_dots(hdk_vtx x, const hdk_ctl* ctl, c
 }
 
 // Solves M gamma = DG^T g, M = DG^T DG + 1e-6 |DG|_F^2 / window I, by LDL^T with
-// diagonal pivoting (Eigen::LDLT).  Returns false on a zero pivot.
-__device__ bool small_ldlt(double* a, int n, const double* b, double* x) {
-  int perm[HDK_AA_MAX];
-  double d[HDK_AA_MAX];
-  for (int i = 0; i < n; ++i) perm[i] = i;
-  for (int k = 0; k < n; ++k) {
+// diagonal pivoting (Eigen::LDLT).  N is a compile-time size so the whole
+// factorization lives in registers (pivot swaps are unrolled selects).
+template <int N>
+__device__ __forceinline__ bool ldlt_fixed(const double* m_in, int ld, const double* b, double* x) {
+  double a[N][N], d[N], y[N];
+  int perm[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    perm[i] = i;
+#pragma unroll
+    for (int j = 0; j < N; ++j) a[i][j] = m_in[i * ld + j];
+  }
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
     int piv = k;
-    double best = fabs(a[k * n + k]);
-    for (int i = k + 1; i < n; ++i)
-      if (fabs(a[i * n + i]) > best) { best = fabs(a[i * n + i]); piv = i; }
-    if (piv != k) {
-      const int t = perm[k]; perm[k] = perm[piv]; perm[piv] = t;
-      for (int c = 0; c < n; ++c) { const double s = a[k * n + c]; a[k * n + c] = a[piv * n + c]; a[piv * n + c] = s; }
-      for (int r = 0; r < n; ++r) { const double s = a[r * n + k]; a[r * n + k] = a[r * n + piv]; a[r * n + piv] = s; }
+    double best = fabs(a[k][k]);
+#pragma unroll
+    for (int i = k + 1; i < N; ++i)
+      if (fabs(a[i][i]) > best) { best = fabs(a[i][i]); piv = i; }
+#pragma unroll
+    for (int p = k + 1; p < N; ++p) {
+      if (p == piv) {
+        const int t = perm[k]; perm[k] = perm[p]; perm[p] = t;
+#pragma unroll
+        for (int c = 0; c < N; ++c) { const double t2 = a[k][c]; a[k][c] = a[p][c]; a[p][c] = t2; }
+#pragma unroll
+        for (int r = 0; r < N; ++r) { const double t2 = a[r][k]; a[r][k] = a[r][p]; a[r][p] = t2; }
+      }
     }
-    double dk = a[k * n + k];
-    for (int j = 0; j < k; ++j) dk -= a[k * n + j] * a[k * n + j] * d[j];
-    if (!(fabs(dk) > 2.2250738585072014e-308)) return false;
+    double dk = a[k][k];
+#pragma unroll
+    for (int j = 0; j < k; ++j) dk -= a[k][j] * a[k][j] * d[j];
+    if (!(fabs(dk) > 2.2250738585072014e-308)) ok = false;
     d[k] = dk;
-    for (int i = k + 1; i < n; ++i) {
-      double s = a[i * n + k];
-      for (int j = 0; j < k; ++j) s -= a[i * n + j] * a[k * n + j] * d[j];
-      a[i * n + k] = s / dk;
+#pragma unroll
+    for (int i = k + 1; i < N; ++i) {
+      double s = a[i][k];
+#pragma unroll
+      for (int j = 0; j < k; ++j) s -= a[i][j] * a[k][j] * d[j];
+      a[i][k] = s / dk;
     }
   }
-  double y[HDK_AA_MAX];
-  for (int i = 0; i < n; ++i) y[i] = b[perm[i]];
-  for (int i = 0; i < n; ++i)
-    for (int j = 0; j < i; ++j) y[i] -= a[i * n + j] * y[j];
-  for (int i = 0; i < n; ++i) y[i] /= d[i];
-  for (int i = n - 1; i >= 0; --i)
-    for (int j = i + 1; j < n; ++j) y[i] -= a[j * n + i] * y[j];
-  for (int i = 0; i < n; ++i) x[perm[i]] = y[i];
-  for (int i = 0; i < n; ++i)
-    if (!isfinite(x[i])) return false;
-  return true;
+  if (!ok) return false;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double bi = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (perm[i] == j) bi = b[j];
+    y[i] = bi;
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < i; ++j) y[i] -= a[i][j] * y[j];
+#pragma unroll
+  for (int i = 0; i < N; ++i) y[i] /= d[i];
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i)
+#pragma unroll
+    for (int j = i + 1; j < N; ++j) y[i] -= a[j][i] * y[j];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (perm[i] == j) x[j] = y[i];
+  bool fin = true;
+#pragma unroll
+  for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
+  return fin;
 }
 
-constexpr int kSolveT = 32 * (2 * HDK_AA_MAX + 2);  // one warp per folded quantity
-__global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const double* partial, int mode) {
+__device__ bool small_ldlt(const double* a, int ld, int n, const double* b, double* x) {
+  switch (n) {
+    case 1: return ldlt_fixed<1>(a, ld, b, x);
+    case 2: return ldlt_fixed<2>(a, ld, b, x);
+    case 3: return ldlt_fixed<3>(a, ld, b, x);
+    case 4: return ldlt_fixed<4>(a, ld, b, x);
+    case 5: return ldlt_fixed<5>(a, ld, b, x);
+    case 6: return ldlt_fixed<6>(a, ld, b, x);
+    case 7: return ldlt_fixed<7>(a, ld, b, x);
+    default: return ldlt_fixed<8>(a, ld, b, x);
+  }
+}
+
+constexpr int kSolveT = 256;  // 8 warps fold the 18 quantities; thread 0 keeps the solve in registers
+__global__ void __launch_bounds__(kSolveT, 1) k_aa_solve(hdk_ctl* gctl, const double* partial, int mode) {
   __shared__ double s[2 * HDK_AA_MAX + 2];
   __shared__ hdk_ctl c_sh;  // work on a shared-memory copy of the control block
   {
@@ -310,13 +358,13 @@ __global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const doubl
       double fro2 = 0.0;
       for (int j = 0; j < c2; ++j) fro2 += ctl->gram[j * HDK_AA_MAX + j];
       if (c2 > 0 && fro2 > 0.0) {
-        double a[HDK_AA_MAX * HDK_AA_MAX], rhs[HDK_AA_MAX], gam[HDK_AA_MAX];
+        __shared__ double a[HDK_AA_MAX * HDK_AA_MAX], rhs[HDK_AA_MAX], gam[HDK_AA_MAX];
         for (int i = 0; i < c2; ++i) {
-          for (int j = 0; j < c2; ++j) a[i * c2 + j] = ctl->gram[i * HDK_AA_MAX + j];
-          a[i * c2 + i] += 1e-6 * fro2 / m;
+          for (int j = 0; j < c2; ++j) a[i * HDK_AA_MAX + j] = ctl->gram[i * HDK_AA_MAX + j];
+          a[i * HDK_AA_MAX + i] += 1e-6 * fro2 / m;
           rhs[i] = s[HDK_AA_MAX + i];
         }
-        const bool ok = small_ldlt(a, c2, rhs, gam);
+        const bool ok = small_ldlt(a, HDK_AA_MAX, c2, rhs, gam);
         double gn = 0.0;
         for (int i = 0; i < c2; ++i) gn += gam[i] * gam[i];
         if (!ok || !(sqrt(gn) <= ctl->guard)) {  // guard: discard history (forward.cpp:43-47)
