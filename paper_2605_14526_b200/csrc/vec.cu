@@ -224,163 +224,142 @@ __global__ void __launch_bounds__(kT) k_aa_dots(hdk_vtx x, const hdk_ctl* ctl, c
   block_partials<2 * HDK_AA_MAX + 2>(acc, partial);
 }
 
-// Solves M gamma = DG^T g, M = DG^T DG + 1e-6 |DG|_F^2 / window I, by LDL^T with
-// diagonal pivoting (Eigen::LDLT).  N is a compile-time size so the whole
-// factorization lives in registers (pivot swaps are unrolled selects).
-template <int N>
-__device__ __forceinline__ bool ldlt_fixed(const double* m_in, int ld, const double* b, double* x) {
-  double a[N][N], d[N], y[N];
-  int perm[N];
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    perm[i] = i;
-#pragma unroll
-    for (int j = 0; j < N; ++j) a[i][j] = m_in[i * ld + j];
-  }
-  bool ok = true;
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    int piv = k;
-    double best = fabs(a[k][k]);
-#pragma unroll
-    for (int i = k + 1; i < N; ++i)
-      if (fabs(a[i][i]) > best) { best = fabs(a[i][i]); piv = i; }
-#pragma unroll
-    for (int p = k + 1; p < N; ++p) {
-      if (p == piv) {
-        const int t = perm[k]; perm[k] = perm[p]; perm[p] = t;
-#pragma unroll
-        for (int c = 0; c < N; ++c) { const double t2 = a[k][c]; a[k][c] = a[p][c]; a[p][c] = t2; }
-#pragma unroll
-        for (int r = 0; r < N; ++r) { const double t2 = a[r][k]; a[r][k] = a[r][p]; a[r][p] = t2; }
-      }
-    }
-    double dk = a[k][k];
-#pragma unroll
-    for (int j = 0; j < k; ++j) dk -= a[k][j] * a[k][j] * d[j];
-    if (!(fabs(dk) > 2.2250738585072014e-308)) ok = false;
-    d[k] = dk;
-#pragma unroll
-    for (int i = k + 1; i < N; ++i) {
-      double s = a[i][k];
-#pragma unroll
-      for (int j = 0; j < k; ++j) s -= a[i][j] * a[k][j] * d[j];
-      a[i][k] = s / dk;
-    }
-  }
-  if (!ok) return false;
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    double bi = 0.0;
-#pragma unroll
-    for (int j = 0; j < N; ++j)
-      if (perm[i] == j) bi = b[j];
-    y[i] = bi;
-  }
-#pragma unroll
-  for (int i = 0; i < N; ++i)
-#pragma unroll
-    for (int j = 0; j < i; ++j) y[i] -= a[i][j] * y[j];
-#pragma unroll
-  for (int i = 0; i < N; ++i) y[i] /= d[i];
-#pragma unroll
-  for (int i = N - 1; i >= 0; --i)
-#pragma unroll
-    for (int j = i + 1; j < N; ++j) y[i] -= a[j][i] * y[j];
-#pragma unroll
-  for (int i = 0; i < N; ++i)
-#pragma unroll
-    for (int j = 0; j < N; ++j)
-      if (perm[i] == j) x[j] = y[i];
-  bool fin = true;
-#pragma unroll
-  for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
-  return fin;
-}
-
-__device__ bool small_ldlt(const double* a, int ld, int n, const double* b, double* x) {
-  switch (n) {
-    case 1: return ldlt_fixed<1>(a, ld, b, x);
-    case 2: return ldlt_fixed<2>(a, ld, b, x);
-    case 3: return ldlt_fixed<3>(a, ld, b, x);
-    case 4: return ldlt_fixed<4>(a, ld, b, x);
-    case 5: return ldlt_fixed<5>(a, ld, b, x);
-    case 6: return ldlt_fixed<6>(a, ld, b, x);
-    case 7: return ldlt_fixed<7>(a, ld, b, x);
-    default: return ldlt_fixed<8>(a, ld, b, x);
-  }
-}
-
-constexpr int kSolveT = 256;  // 8 warps fold the 18 quantities; thread 0 keeps the solve in registers
-__global__ void __launch_bounds__(kSolveT, 1) k_aa_solve(hdk_ctl* gctl, const double* partial, int mode) {
+// Anderson coefficient solve (forward.cpp:31-47): M gamma = DG^T g with
+// M = DG^T DG + 1e-6 |DG|_F^2 / window I, by LDL^T with Eigen::LDLT's
+// diagonal pivoting (left-looking, pivots chosen on the untouched diagonal).
+// One warp: lane 0 does the short serial bookkeeping, the factorization runs
+// row-parallel over lanes; everything lives in shared memory.
+constexpr int kSolveT = 256;  // 8 warps fold the 18 partial sums
+__global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const double* partial, int mode) {
   __shared__ double s[2 * HDK_AA_MAX + 2];
-  __shared__ hdk_ctl c_sh;  // work on a shared-memory copy of the control block
+  __shared__ hdk_ctl c;  // shared-memory copy of the control block
+  __shared__ double A[HDK_AA_MAX][HDK_AA_MAX + 1], L[HDK_AA_MAX][HDK_AA_MAX + 1], d[HDK_AA_MAX], y[HDK_AA_MAX];
+  __shared__ int perm[HDK_AA_MAX], solve_n, ok;
   {
     const int* src = reinterpret_cast<const int*>(gctl);
-    int* dst = reinterpret_cast<int*>(&c_sh);
+    int* dst = reinterpret_cast<int*>(&c);
     for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += blockDim.x) dst[i] = src[i];
   }
   fold_all(partial, 2 * HDK_AA_MAX + 2, s);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    hdk_ctl* ctl = &c_sh;
-    bool skip = false;
-    if (mode == 1) {  // adjoint backbone: convergence test before mixing (backward.cpp:191-193)
-      ctl->iterations += 1;
-      const double diff = sqrt(s[2 * HDK_AA_MAX]);
-      const double base = fmax(sqrt(s[2 * HDK_AA_MAX + 1]), 1e-30);
-      ctl->k += 1;
-      if (diff <= ctl->tol * base) {
-        ctl->done = 1;
-        ctl->mixed = 0;
-        skip = true;
-      } else if (ctl->k >= ctl->k_max && ctl->err == 0) {
-        ctl->err = 10;  // AdjointDiverged (cap)
+  if (threadIdx.x >= 32) goto writeback;
+  {
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+      solve_n = 0;
+      bool skip = false;
+      if (mode == 1) {  // adjoint backbone: convergence test before mixing (backward.cpp:191-193)
+        c.iterations += 1;
+        const double diff = sqrt(s[2 * HDK_AA_MAX]);
+        const double base = fmax(sqrt(s[2 * HDK_AA_MAX + 1]), 1e-30);
+        c.k += 1;
+        if (diff <= c.tol * base) {
+          c.done = 1;
+          c.mixed = 0;
+          skip = true;
+        } else if (c.k >= c.k_max && c.err == 0) {
+          c.err = 10;  // AdjointDiverged (cap)
+        }
+      }
+      if (!skip) {
+        const int m = c.window;
+        if (c.has_last) {
+          const int n0 = c.count;
+          if (n0 < m) {
+            c.count = n0 + 1;
+          } else {
+            c.head = (c.head + 1) % m;
+            for (int i = 0; i + 1 < m; ++i)
+              for (int j = 0; j + 1 < m; ++j) c.gram[i * HDK_AA_MAX + j] = c.gram[(i + 1) * HDK_AA_MAX + (j + 1)];
+          }
+          const int n1 = c.count, j = n1 - 1;
+          for (int l = 0; l < n1; ++l) c.gram[j * HDK_AA_MAX + l] = c.gram[l * HDK_AA_MAX + j] = s[l];
+        }
+        c.has_last = 1;
+        c.mixed = 0;
+        const int n = c.count;
+        double fro2 = 0.0;
+        for (int j = 0; j < n; ++j) fro2 += c.gram[j * HDK_AA_MAX + j];
+        if (n > 0 && fro2 > 0.0) {
+          solve_n = n;
+          // pivot order: Eigen picks the largest |diagonal| among the remaining
+          // (untouched) diagonal entries, swapping it into place
+          double dg[HDK_AA_MAX];
+          for (int i = 0; i < n; ++i) {
+            perm[i] = i;
+            dg[i] = c.gram[i * HDK_AA_MAX + i] + 1e-6 * fro2 / m;
+          }
+          for (int k = 0; k < n; ++k) {
+            int piv = k;
+            double best = fabs(dg[k]);
+            for (int i = k + 1; i < n; ++i)
+              if (fabs(dg[i]) > best) { best = fabs(dg[i]); piv = i; }
+            const int tp = perm[k]; perm[k] = perm[piv]; perm[piv] = tp;
+            const double td = dg[k]; dg[k] = dg[piv]; dg[piv] = td;
+          }
+          y[0] = 1e-6 * fro2 / m;  // ridge, broadcast below
+        }
       }
     }
-    if (!skip) {
-      const int m = ctl->window;
-      if (ctl->has_last) {
-        const int c = ctl->count;
-        if (c < m) {
-          ctl->count = c + 1;
-        } else {
-          ctl->head = (ctl->head + 1) % m;
-          for (int i = 0; i + 1 < m; ++i)
-            for (int j = 0; j + 1 < m; ++j) ctl->gram[i * HDK_AA_MAX + j] = ctl->gram[(i + 1) * HDK_AA_MAX + (j + 1)];
-        }
-        const int c2 = ctl->count, j = c2 - 1;
-        for (int l = 0; l < c2; ++l) ctl->gram[j * HDK_AA_MAX + l] = ctl->gram[l * HDK_AA_MAX + j] = s[l];
+    __syncwarp();
+    const int n = solve_n;
+    if (n > 0) {
+      const double ridge = y[0];
+      __syncwarp();
+      // permuted matrix, rows over lanes
+      for (int e = lane; e < n * n; e += 32) {
+        const int i = e / n, j = e % n;
+        A[i][j] = c.gram[perm[i] * HDK_AA_MAX + perm[j]] + (perm[i] == perm[j] ? ridge : 0.0);
       }
-      ctl->has_last = 1;
-      ctl->mixed = 0;
-      const int c2 = ctl->count;
-      double fro2 = 0.0;
-      for (int j = 0; j < c2; ++j) fro2 += ctl->gram[j * HDK_AA_MAX + j];
-      if (c2 > 0 && fro2 > 0.0) {
-        __shared__ double a[HDK_AA_MAX * HDK_AA_MAX], rhs[HDK_AA_MAX], gam[HDK_AA_MAX];
-        for (int i = 0; i < c2; ++i) {
-          for (int j = 0; j < c2; ++j) a[i * HDK_AA_MAX + j] = ctl->gram[i * HDK_AA_MAX + j];
-          a[i * HDK_AA_MAX + i] += 1e-6 * fro2 / m;
-          rhs[i] = s[HDK_AA_MAX + i];
+      __syncwarp();
+      if (lane == 0) ok = 1;
+      __syncwarp();
+      for (int k = 0; k < n; ++k) {
+        if (lane == k) {
+          double dk = A[k][k];
+          for (int j = 0; j < k; ++j) dk -= L[k][j] * L[k][j] * d[j];
+          d[k] = dk;
+          if (!(fabs(dk) > 2.2250738585072014e-308)) ok = 0;
         }
-        const bool ok = small_ldlt(a, HDK_AA_MAX, c2, rhs, gam);
+        __syncwarp();
+        if (lane > k && lane < n) {
+          double v = A[lane][k];
+          for (int j = 0; j < k; ++j) v -= L[lane][j] * L[k][j] * d[j];
+          L[lane][k] = v / d[k];
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        double gam[HDK_AA_MAX];
+        bool good = ok != 0;
+        if (good) {
+          for (int i = 0; i < n; ++i) y[i] = s[HDK_AA_MAX + perm[i]];
+          for (int i = 0; i < n; ++i)
+            for (int j = 0; j < i; ++j) y[i] -= L[i][j] * y[j];
+          for (int i = 0; i < n; ++i) y[i] /= d[i];
+          for (int i = n - 1; i >= 0; --i)
+            for (int j = i + 1; j < n; ++j) y[i] -= L[j][i] * y[j];
+          for (int i = 0; i < n; ++i) gam[perm[i]] = y[i];
+          for (int i = 0; i < n; ++i) good = good && isfinite(gam[i]);
+        }
         double gn = 0.0;
-        for (int i = 0; i < c2; ++i) gn += gam[i] * gam[i];
-        if (!ok || !(sqrt(gn) <= ctl->guard)) {  // guard: discard history (forward.cpp:43-47)
-          ctl->count = 0;
-          ctl->head = 0;
-          ctl->has_last = 0;
+        if (good)
+          for (int i = 0; i < n; ++i) gn += gam[i] * gam[i];
+        if (!good || !(sqrt(gn) <= c.guard)) {  // guard: discard history (forward.cpp:43-47)
+          c.count = 0;
+          c.head = 0;
+          c.has_last = 0;
         } else {
-          for (int i = 0; i < c2; ++i) ctl->gamma[i] = gam[i];
-          ctl->mixed = 1;
+          for (int i = 0; i < n; ++i) c.gamma[i] = gam[i];
+          c.mixed = 1;
         }
       }
     }
   }
+writeback:
   __syncthreads();
   {
-    const int* src = reinterpret_cast<const int*>(&c_sh);
+    const int* src = reinterpret_cast<const int*>(&c);
     int* dst = reinterpret_cast<int*>(gctl);
     for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += blockDim.x) dst[i] = src[i];
   }
