@@ -46,6 +46,7 @@ __device__ __forceinline__ void block_partials(double (&v)[NQ], double* partial)
 constexpr int kFoldPerLane = (HDK_RED_BLOCKS + 31) / 32;
 __device__ __forceinline__ void fold_all(const double* __restrict__ partial, int nq, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll 1
   for (int q = warp; q < nq; q += nw) {
     double v[kFoldPerLane];
 #pragma unroll
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const doubl
   {
     const int* src = reinterpret_cast<const int*>(gctl);
     int* dst = reinterpret_cast<int*>(&c);
+    #pragma unroll 1
     for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += blockDim.x) dst[i] = src[i];
   }
   fold_all(partial, 2 * HDK_AA_MAX + 2, s);
@@ -269,29 +271,36 @@ __global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const doubl
             c.count = n0 + 1;
           } else {
             c.head = (c.head + 1) % m;
+            #pragma unroll 1
             for (int i = 0; i + 1 < m; ++i)
+              #pragma unroll 1
               for (int j = 0; j + 1 < m; ++j) c.gram[i * HDK_AA_MAX + j] = c.gram[(i + 1) * HDK_AA_MAX + (j + 1)];
           }
           const int n1 = c.count, j = n1 - 1;
+          #pragma unroll 1
           for (int l = 0; l < n1; ++l) c.gram[j * HDK_AA_MAX + l] = c.gram[l * HDK_AA_MAX + j] = s[l];
         }
         c.has_last = 1;
         c.mixed = 0;
         const int n = c.count;
         double fro2 = 0.0;
+        #pragma unroll 1
         for (int j = 0; j < n; ++j) fro2 += c.gram[j * HDK_AA_MAX + j];
         if (n > 0 && fro2 > 0.0) {
           solve_n = n;
           // pivot order: Eigen picks the largest |diagonal| among the remaining
           // (untouched) diagonal entries, swapping it into place
           double dg[HDK_AA_MAX];
+          #pragma unroll 1
           for (int i = 0; i < n; ++i) {
             perm[i] = i;
             dg[i] = c.gram[i * HDK_AA_MAX + i] + 1e-6 * fro2 / m;
           }
+          #pragma unroll 1
           for (int k = 0; k < n; ++k) {
             int piv = k;
             double best = fabs(dg[k]);
+            #pragma unroll 1
             for (int i = k + 1; i < n; ++i)
               if (fabs(dg[i]) > best) { best = fabs(dg[i]); piv = i; }
             const int tp = perm[k]; perm[k] = perm[piv]; perm[piv] = tp;
@@ -307,6 +316,7 @@ __global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const doubl
       const double ridge = y[0];
       __syncwarp();
       // permuted matrix, rows over lanes
+      #pragma unroll 1
       for (int e = lane; e < n * n; e += 32) {
         const int i = e / n, j = e % n;
         A[i][j] = c.gram[perm[i] * HDK_AA_MAX + perm[j]] + (perm[i] == perm[j] ? ridge : 0.0);
@@ -314,9 +324,11 @@ __global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const doubl
       __syncwarp();
       if (lane == 0) ok = 1;
       __syncwarp();
+      #pragma unroll 1
       for (int k = 0; k < n; ++k) {
         if (lane == k) {
           double dk = A[k][k];
+          #pragma unroll 1
           for (int j = 0; j < k; ++j) dk -= L[k][j] * L[k][j] * d[j];
           d[k] = dk;
           if (!(fabs(dk) > 2.2250738585072014e-308)) ok = 0;
@@ -324,6 +336,7 @@ __global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const doubl
         __syncwarp();
         if (lane > k && lane < n) {
           double v = A[lane][k];
+          #pragma unroll 1
           for (int j = 0; j < k; ++j) v -= L[lane][j] * L[k][j] * d[j];
           L[lane][k] = v / d[k];
         }
@@ -333,23 +346,33 @@ __global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const doubl
         double gam[HDK_AA_MAX];
         bool good = ok != 0;
         if (good) {
+          #pragma unroll 1
           for (int i = 0; i < n; ++i) y[i] = s[HDK_AA_MAX + perm[i]];
+          #pragma unroll 1
           for (int i = 0; i < n; ++i)
+            #pragma unroll 1
             for (int j = 0; j < i; ++j) y[i] -= L[i][j] * y[j];
+          #pragma unroll 1
           for (int i = 0; i < n; ++i) y[i] /= d[i];
+          #pragma unroll 1
           for (int i = n - 1; i >= 0; --i)
+            #pragma unroll 1
             for (int j = i + 1; j < n; ++j) y[i] -= L[j][i] * y[j];
+          #pragma unroll 1
           for (int i = 0; i < n; ++i) gam[perm[i]] = y[i];
+          #pragma unroll 1
           for (int i = 0; i < n; ++i) good = good && isfinite(gam[i]);
         }
         double gn = 0.0;
         if (good)
+          #pragma unroll 1
           for (int i = 0; i < n; ++i) gn += gam[i] * gam[i];
         if (!good || !(sqrt(gn) <= c.guard)) {  // guard: discard history (forward.cpp:43-47)
           c.count = 0;
           c.head = 0;
           c.has_last = 0;
         } else {
+          #pragma unroll 1
           for (int i = 0; i < n; ++i) c.gamma[i] = gam[i];
           c.mixed = 1;
         }
@@ -361,6 +384,7 @@ writeback:
   {
     const int* src = reinterpret_cast<const int*>(&c);
     int* dst = reinterpret_cast<int*>(gctl);
+    #pragma unroll 1
     for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += blockDim.x) dst[i] = src[i];
   }
 }
