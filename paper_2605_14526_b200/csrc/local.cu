@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/hdk.h"
+#include "launch.cuh"
 #include "dmath.cuh"
 
 using namespace hdk;
@@ -94,6 +95,8 @@ __device__ __forceinline__ bool project(const hdk_material& mat, int e, const V3
 
 __global__ void __launch_bounds__(128) k_local(hdk_mesh m, hdk_material mat, const double* __restrict__ q,
                                                 double* __restrict__ ef, double* __restrict__ cache, int* err) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m.ne) return;
   const ElemGeom g = load_geom(m, e);
@@ -131,6 +134,8 @@ __global__ void __launch_bounds__(128) k_local(hdk_mesh m, hdk_material mat, con
 // flags NonPositiveJacobian / ProxDiverged (tr_select_tau maps both to rho = inf).
 __global__ void __launch_bounds__(128) k_energy(hdk_mesh m, hdk_material mat, const double* __restrict__ q,
                                                  double* __restrict__ energy, int* bad) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m.ne) return;
   const ElemGeom g = load_geom(m, e);
@@ -186,6 +191,8 @@ __device__ __forceinline__ void load_cache(const double* __restrict__ c, int ne,
 // element weight and volume folded into J and the pair coefficients.
 __global__ void __launch_bounds__(128) k_differential(hdk_mesh m, hdk_material mat, const double* __restrict__ cache,
                                                        const double* tau_ptr, double* __restrict__ dcomp, int* err) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m.ne) return;
   const int ne = m.ne;
@@ -288,6 +295,8 @@ __global__ void __launch_bounds__(128) k_differential(hdk_mesh m, hdk_material m
 // Element force of B x: P = U (D o (U^T F(x) V)) V^T, f_i = P g_i.
 __global__ void __launch_bounds__(128) k_bapply(hdk_mesh m, const double* __restrict__ dcomp, const double* __restrict__ x,
                                                  double* __restrict__ ef) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m.ne) return;
   const size_t n = m.ne;
@@ -323,6 +332,8 @@ __global__ void __launch_bounds__(128) k_route_elem(hdk_mesh m, hdk_material mat
                                                      const double* __restrict__ q_star, const double* __restrict__ mu,
                                                      double unit_mu, double unit_lambda, double* __restrict__ dl_dw,
                                                      double* __restrict__ dl_de, double* __restrict__ ef_damp) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m.ne) return;
   const int ne = m.ne;
@@ -365,6 +376,8 @@ __global__ void __launch_bounds__(128) k_route_elem(hdk_mesh m, hdk_material mat
 
 __global__ void __launch_bounds__(128) k_damp_elem(hdk_mesh m, const double* __restrict__ beta_vh,
                                                     const double* __restrict__ q, double* __restrict__ ef) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m.ne) return;
   const ElemGeom g = load_geom(m, e);
@@ -384,38 +397,37 @@ extern "C" {
 
 HDK_API int hdk_local_step(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
                            double* cache, int* err, void* stream) {
-  k_local<<<blocks(m->ne, 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(*m, *mat, q, elem_force, cache, err);
+  hdk::launch(k_local, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q, elem_force, cache, err);
   return static_cast<int>(cudaGetLastError());
 }
 
 HDK_API int hdk_element_energy(const hdk_mesh* m, const hdk_material* mat, const double* q, double* energy, int* bad,
                                void* stream) {
-  k_energy<<<blocks(m->ne, 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(*m, *mat, q, energy, bad);
+  hdk::launch(k_energy, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q, energy, bad);
   return static_cast<int>(cudaGetLastError());
 }
 
 HDK_API int hdk_differential(const hdk_mesh* m, const hdk_material* mat, const double* cache, const double* tau,
                              double* dcomp, int* err, void* stream) {
-  k_differential<<<blocks(m->ne, 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(*m, *mat, cache, tau, dcomp, err);
+  hdk::launch(k_differential, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, cache, tau, dcomp, err);
   return static_cast<int>(cudaGetLastError());
 }
 
 HDK_API int hdk_bapply(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force, void* stream) {
-  k_bapply<<<blocks(m->ne, 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(*m, dcomp, x, elem_force);
+  hdk::launch(k_bapply, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, dcomp, x, elem_force);
   return static_cast<int>(cudaGetLastError());
 }
 
 HDK_API int hdk_route_elements(const hdk_mesh* m, const hdk_material* mat, const double* cache, const double* q_star,
                                const double* mu, double unit_mu, double unit_lambda, double* dl_dw, double* dl_de,
                                double* ef_damp, void* stream) {
-  k_route_elem<<<blocks(m->ne, 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
-      *m, *mat, cache, q_star, mu, unit_mu, unit_lambda, dl_dw, dl_de, ef_damp);
+  hdk::launch(k_route_elem, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, cache, q_star, mu, unit_mu, unit_lambda, dl_dw, dl_de, ef_damp);
   return static_cast<int>(cudaGetLastError());
 }
 
 HDK_API int hdk_damping_elements(const hdk_mesh* m, const double* beta_vh, const double* q, double* elem_force,
                                  void* stream) {
-  k_damp_elem<<<blocks(m->ne, 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(*m, beta_vh, q, elem_force);
+  hdk::launch(k_damp_elem, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, beta_vh, q, elem_force);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -26,6 +26,7 @@
 #include <cstdint>
 
 #include "../../include/hdk.h"
+#include "launch.cuh"
 
 namespace {
 
@@ -128,6 +129,8 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
 
 // ---- pass 1 ------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double* __restrict__ rhs) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<kStages1>& ring = *reinterpret_cast<Ring<kStages1>*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -193,6 +196,8 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
 // z_r = sum of the row's tile partials in tile order; eight lanes per row,
 // loads issued four at a time before adding.
 __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = gid >> 3, sub = gid & 7;
   const bool live = r < f.n;
@@ -269,6 +274,8 @@ __device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& s
 }
 
 __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Pass2Smem& sm = *reinterpret_cast<Pass2Smem*>(smem_raw);
   Ring<kStages2>& ring = sm.ring;
@@ -332,6 +339,8 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
 // column's tile (CTA order), scattered to the full vector.
 template <bool kScatter>
 __global__ void k_xreduce(hdk_factor f, int G, double* __restrict__ out) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= f.n) return;
   const int t = c / kW, cl = c - t * kW;
@@ -371,13 +380,13 @@ int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatte
   const int g1 = g_grid1 < f->n_chunks ? g_grid1 : f->n_chunks;
   int g2 = g_grid2 < f->n_chunks ? g_grid2 : f->n_chunks;
   if (g2 > f->max_ctas) g2 = f->max_ctas;
-  k_rowdot<<<g1, kThreads, s1, st>>>(*f, rhs_perm);
-  k_zreduce<<<(f->n * 8 + 255) / 256, 256, 0, st>>>(*f);
-  k_coltile<<<g2, kThreads, s2, st>>>(*f);
+  hdk::launch(k_rowdot, dim3(g1), dim3(kThreads), s1, st, *f, rhs_perm);
+  hdk::launch(k_zreduce, dim3((f->n * 8 + 255) / 256), dim3(256), 0, st, *f);
+  hdk::launch(k_coltile, dim3(g2), dim3(kThreads), s2, st, *f);
   if (scatter)
-    k_xreduce<true><<<(f->n + 255) / 256, 256, 0, st>>>(*f, g2, out);
+    hdk::launch(k_xreduce<true>, dim3((f->n + 255) / 256), dim3(256), 0, st, *f, g2, out);
   else
-    k_xreduce<false><<<(f->n + 255) / 256, 256, 0, st>>>(*f, g2, out);
+    hdk::launch(k_xreduce<false>, dim3((f->n + 255) / 256), dim3(256), 0, st, *f, g2, out);
   return static_cast<int>(cudaGetLastError());
 }
 

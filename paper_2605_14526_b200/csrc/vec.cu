@@ -14,6 +14,7 @@
 #include <cmath>
 
 #include "../../include/hdk.h"
+#include "launch.cuh"
 
 namespace {
 
@@ -80,6 +81,8 @@ __device__ __forceinline__ void gather_vtx(const hdk_vtx& x, const double* __res
 
 __global__ void k_free_fall(hdk_vtx x, const double* q, const double* v, const double* f, double h, int hv,
                             double ax, double ay, double az, double hk, double hd, double* qt, double* qc) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 3 * x.nv) return;
   const int vtx = i / 3, a = i - 3 * vtx;
@@ -94,6 +97,8 @@ __global__ void k_free_fall(hdk_vtx x, const double* q, const double* v, const d
 }
 
 __global__ void k_gather(hdk_vtx x, const double* ef, double cm, const double* base, const double* add, double* out) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= x.nv) return;
   double g[3] = {0.0, 0.0, 0.0};
@@ -110,6 +115,8 @@ __global__ void __launch_bounds__(kT) k_gather_rhs(hdk_vtx x, const double* __re
                                                    const double* __restrict__ qt, const double* __restrict__ damp,
                                                    const double* __restrict__ fixc, double* bprev, double* rhs,
                                                    double* partial) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   double acc[2] = {0.0, 0.0};
   for (int v = blockIdx.x * kT + threadIdx.x; v < x.nv; v += HDK_RED_BLOCKS * kT) {
     const int p = x.v2p[v];
@@ -136,6 +143,8 @@ __global__ void __launch_bounds__(kT) k_gather_rhs(hdk_vtx x, const double* __re
 // with a fixed shuffle tree.
 __global__ void k_gather_perm(hdk_vtx x, const double* __restrict__ base, const double* __restrict__ ef,
                               double* __restrict__ rhs) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int p = gid >> 3, sub = gid & 7;
   const bool live = p < x.n;
@@ -168,6 +177,8 @@ __global__ void k_gather_perm(hdk_vtx x, const double* __restrict__ base, const 
 }
 
 __global__ void k_fixed_coupling(hdk_csr c, const int* fixed, const double* q, double* out) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= c.rows) return;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -187,6 +198,8 @@ __global__ void k_fixed_coupling(hdk_csr c, const int* fixed, const double* q, d
 __global__ void __launch_bounds__(kT) k_aa_dots(hdk_vtx x, const hdk_ctl* ctl, const double* __restrict__ qhat,
                                                 const double* __restrict__ qcur, double* last_q, double* last_g,
                                                 double* dq, double* dg, double* partial) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const size_t n3 = 3 * (size_t)x.nv;
   const int m = ctl->window, c = ctl->count, h = ctl->head;
   const bool push = ctl->has_last != 0;
@@ -232,6 +245,8 @@ __global__ void __launch_bounds__(kT) k_aa_dots(hdk_vtx x, const hdk_ctl* ctl, c
 // row-parallel over lanes; everything lives in shared memory.
 constexpr int kSolveT = 256;  // 8 warps fold the 18 partial sums
 __global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const double* partial, int mode) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   __shared__ double s[2 * HDK_AA_MAX + 2];
   __shared__ hdk_ctl c;  // shared-memory copy of the control block
   __shared__ double A[HDK_AA_MAX][HDK_AA_MAX + 1], L[HDK_AA_MAX][HDK_AA_MAX + 1], d[HDK_AA_MAX], y[HDK_AA_MAX];
@@ -393,6 +408,8 @@ __global__ void __launch_bounds__(kT) k_aa_mix(hdk_vtx x, hdk_ctl* ctl, const do
                                                double* qprev, const double* __restrict__ qpin,
                                                const double* __restrict__ dq, const double* __restrict__ dg,
                                                double* partial, int mode) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const size_t n3 = 3 * (size_t)x.nv;
   const bool done = mode == 1 && ctl->done;
   const int mixed = ctl->mixed, c = ctl->count, h = ctl->head, m = ctl->window;
@@ -431,6 +448,8 @@ __global__ void __launch_bounds__(kT) k_aa_mix(hdk_vtx x, hdk_ctl* ctl, const do
 
 __global__ void __launch_bounds__(kT) k_gate(hdk_ctl* ctl, const double* pb, const double* pq,
                                              cudaGraphConditionalHandle handle, int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   __shared__ double sb[2], sq[2];
   fold_all(pb, 2, sb);
   fold_all(pq, 2, sq);
@@ -449,6 +468,8 @@ __global__ void __launch_bounds__(kT) k_gate(hdk_ctl* ctl, const double* pb, con
 }
 
 __global__ void k_bb_cond(hdk_ctl* ctl, cudaGraphConditionalHandle handle, int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int cont = (!ctl->done && ctl->err == 0) ? 1 : 0;
   ctl->cond = cont;
   if (use_handle) cudaGraphSetConditional(handle, cont);
@@ -456,6 +477,8 @@ __global__ void k_bb_cond(hdk_ctl* ctl, cudaGraphConditionalHandle handle, int u
 
 // ---- trust-region ratio --------------------------------------------------------
 __global__ void k_tr_dq(hdk_vtx x, const double* qs, const double* qp, double* dq) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= x.n) return;
   const int v = x.p2v[p];
@@ -463,6 +486,8 @@ __global__ void k_tr_dq(hdk_vtx x, const double* qs, const double* qp, double* d
 }
 
 __global__ void __launch_bounds__(kT) k_tr_spmv(hdk_csr A, const double* __restrict__ dq, double* partial) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   double acc[1] = {0.0};
   for (int p = blockIdx.x * kT + threadIdx.x; p < A.rows; p += HDK_RED_BLOCKS * kT) {
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
@@ -482,6 +507,8 @@ __global__ void __launch_bounds__(kT) k_tr_spmv(hdk_csr A, const double* __restr
 __global__ void __launch_bounds__(kT) k_tr_partials(hdk_vtx x, int ne, const double* ep, const double* es,
                                                     const double* qp, const double* qs, const double* qt,
                                                     double* partial) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const int n = max(ne, x.nv);
   for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += HDK_RED_BLOCKS * kT) {
@@ -503,6 +530,8 @@ __global__ void __launch_bounds__(kT) k_tr_partials(hdk_vtx x, int ne, const dou
 }
 
 __global__ void __launch_bounds__(kT) k_tr_final(hdk_ctl* ctl, const double* pm, const double* pe, double inv_h2) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   __shared__ double sm_[1], se[4];
   fold_all(pm, 1, sm_);
   fold_all(pe, 4, se);
@@ -529,6 +558,8 @@ __global__ void __launch_bounds__(kT) k_tr_final(hdk_ctl* ctl, const double* pm,
 __global__ void k_route_vtx(hdk_vtx x, const double* mu, const double* efd, const double* bmu, const double* qbar,
                             const double* vbar, const double* coup, double h, double alpha, int hv, double hk,
                             double hd, double* dq_t, double* dv_t, double* df_acc) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= x.nv) return;
   const double m = x.mass[v];
@@ -561,6 +592,8 @@ __global__ void k_route_vtx(hdk_vtx x, const double* mu, const double* efd, cons
 }
 
 __global__ void k_fixed_coupling_t(hdk_csr c, const int* fixed, const int* p2v, const double* mu, double* coup) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= c.rows) return;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -578,6 +611,8 @@ __global__ void k_fixed_coupling_t(hdk_csr c, const int* fixed, const int* p2v, 
 }
 
 __global__ void k_axpby(int n, double a, const double* x, double b, const double* z, double* y) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = a * x[i];
@@ -586,12 +621,16 @@ __global__ void k_axpby(int n, double a, const double* x, double b, const double
 }
 
 __global__ void k_velocity(int n, const double* qs, const double* qt, double h, double* vs) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) vs[i] = (qs[i] - qt[i]) / h;
 }
 
 __global__ void k_ctl_init(hdk_ctl* c, int window, double guard, int k_max, double er, double ea, double tol,
                            double eps_tr, int it0) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   c->k = 0; c->k_max = k_max; c->iterations = it0; c->converged = 0;
   c->err = 0; c->done = 0; c->bad = 0; c->cond = 1;
   c->window = window < 1 ? 1 : window; c->count = 0; c->head = 0; c->has_last = 0; c->mixed = 0;
@@ -602,6 +641,8 @@ __global__ void k_ctl_init(hdk_ctl* c, int window, double guard, int k_max, doub
 }
 
 __global__ void k_commit(int n, const hdk_ctl* ctl, const double* qs, double h, double* q, double* v) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || ctl->err != 0) return;
   const double s = qs[i];
@@ -621,75 +662,75 @@ HDK_API int hdk_free_fall(const hdk_vtx* x, const double* q, const double* v, co
                           int hook_vertex, const double* hook, double* q_tilde, double* q_cur, void* stream) {
   const double z[5] = {0, 0, 0, 0, 0};
   const double* hp = hook ? hook : z;
-  k_free_fall<<<nb(3LL * x->nv), 256, 0, S(stream)>>>(*x, q, v, f_ext, h, hook ? hook_vertex : -1, hp[0], hp[1], hp[2],
+  hdk::launch(k_free_fall, dim3(nb(3LL * x->nv)), dim3(256), 0, S(stream), *x, q, v, f_ext, h, hook ? hook_vertex : -1, hp[0], hp[1], hp[2],
                                                        hp[3], hp[4], q_tilde, q_cur);
   return last();
 }
 
 HDK_API int hdk_gather(const hdk_vtx* x, const double* ef, double cm, const double* base, const double* add, double* out,
                        void* stream) {
-  k_gather<<<nb(x->nv), 256, 0, S(stream)>>>(*x, ef, cm, base, add, out);
+  hdk::launch(k_gather, dim3(nb(x->nv)), dim3(256), 0, S(stream), *x, ef, cm, base, add, out);
   return last();
 }
 
 HDK_API int hdk_gather_rhs(const hdk_vtx* x, const double* ef, double inv_h2, const double* q_tilde, const double* damp,
                            const double* fixcoup, double* b_prev, double* rhs_perm, double* partial, void* stream) {
-  k_gather_rhs<<<HDK_RED_BLOCKS, kT, 0, S(stream)>>>(*x, ef, inv_h2, q_tilde, damp, fixcoup, b_prev, rhs_perm, partial);
+  hdk::launch(k_gather_rhs, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), *x, ef, inv_h2, q_tilde, damp, fixcoup, b_prev, rhs_perm, partial);
   return last();
 }
 
 HDK_API int hdk_gather_perm(const hdk_vtx* x, const double* base, const double* ef, double* rhs_perm, void* stream) {
-  k_gather_perm<<<nb(8LL * x->n), 256, 0, S(stream)>>>(*x, base, ef, rhs_perm);
+  hdk::launch(k_gather_perm, dim3(nb(8LL * x->n)), dim3(256), 0, S(stream), *x, base, ef, rhs_perm);
   return last();
 }
 
 HDK_API int hdk_fixed_coupling(const hdk_csr* a_fd, const int* fixed, const double* q, double* fixcoup, void* stream) {
-  k_fixed_coupling<<<nb(a_fd->rows), 256, 0, S(stream)>>>(*a_fd, fixed, q, fixcoup);
+  hdk::launch(k_fixed_coupling, dim3(nb(a_fd->rows)), dim3(256), 0, S(stream), *a_fd, fixed, q, fixcoup);
   return last();
 }
 
 HDK_API int hdk_aa_dots(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, const double* qcur, double* last_q,
                         double* last_g, double* dq, double* dg, double* partial, void* stream) {
-  k_aa_dots<<<HDK_RED_BLOCKS, kT, 0, S(stream)>>>(*x, ctl, qhat, qcur, last_q, last_g, dq, dg, partial);
+  hdk::launch(k_aa_dots, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), *x, ctl, qhat, qcur, last_q, last_g, dq, dg, partial);
   return last();
 }
 
 HDK_API int hdk_aa_solve(hdk_ctl* ctl, const double* partial, int mode, void* stream) {
-  k_aa_solve<<<1, kSolveT, 0, S(stream)>>>(ctl, partial, mode);
+  hdk::launch(k_aa_solve, dim3(1), dim3(kSolveT), 0, S(stream), ctl, partial, mode);
   return last();
 }
 
 HDK_API int hdk_aa_mix(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, double* qcur, double* qprev,
                        const double* qpin, const double* dq, const double* dg, double* partial, int mode,
                        void* stream) {
-  k_aa_mix<<<HDK_RED_BLOCKS, kT, 0, S(stream)>>>(*x, ctl, qhat, qcur, qprev, qpin, dq, dg, partial, mode);
+  hdk::launch(k_aa_mix, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), *x, ctl, qhat, qcur, qprev, qpin, dq, dg, partial, mode);
   return last();
 }
 
 HDK_API int hdk_gate(hdk_ctl* ctl, const double* partial_b, const double* partial_q, unsigned long long cond_handle,
                      void* stream) {
-  k_gate<<<1, kT, 0, S(stream)>>>(ctl, partial_b, partial_q, static_cast<cudaGraphConditionalHandle>(cond_handle),
+  hdk::launch(k_gate, dim3(1), dim3(kT), 0, S(stream), ctl, partial_b, partial_q, static_cast<cudaGraphConditionalHandle>(cond_handle),
                                    cond_handle != 0ULL);
   return last();
 }
 
 HDK_API int hdk_backbone_cond(hdk_ctl* ctl, unsigned long long cond_handle, void* stream) {
-  k_bb_cond<<<1, 1, 0, S(stream)>>>(ctl, static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle != 0ULL);
+  hdk::launch(k_bb_cond, dim3(1), dim3(1), 0, S(stream), ctl, static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle != 0ULL);
   return last();
 }
 
 HDK_API int hdk_tr_model(const hdk_vtx* x, const hdk_csr* a_ff, const double* q_star, const double* q_prev,
                          double* dq_perm, double* partial, void* stream) {
-  k_tr_dq<<<nb(x->n), 256, 0, S(stream)>>>(*x, q_star, q_prev, dq_perm);
-  k_tr_spmv<<<HDK_RED_BLOCKS, kT, 0, S(stream)>>>(*a_ff, dq_perm, partial);
+  hdk::launch(k_tr_dq, dim3(nb(x->n)), dim3(256), 0, S(stream), *x, q_star, q_prev, dq_perm);
+  hdk::launch(k_tr_spmv, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), *a_ff, dq_perm, partial);
   return last();
 }
 
 HDK_API int hdk_tr_select(const hdk_vtx* x, int ne, const double* e_prev, const double* e_star, const double* q_prev,
                           const double* q_star, const double* q_tilde, double inv_h2, const double* model_partial,
                           double* partial, hdk_ctl* ctl, void* stream) {
-  k_tr_partials<<<HDK_RED_BLOCKS, kT, 0, S(stream)>>>(*x, ne, e_prev, e_star, q_prev, q_star, q_tilde, partial);
-  k_tr_final<<<1, kT, 0, S(stream)>>>(ctl, model_partial, partial, inv_h2);
+  hdk::launch(k_tr_partials, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), *x, ne, e_prev, e_star, q_prev, q_star, q_tilde, partial);
+  hdk::launch(k_tr_final, dim3(1), dim3(kT), 0, S(stream), ctl, model_partial, partial, inv_h2);
   return last();
 }
 
@@ -697,35 +738,35 @@ HDK_API int hdk_route_vertices(const hdk_vtx* x, const double* mu, const double*
                                const double* q_bar, const double* v_bar, const double* coup_fixed, double h,
                                double alpha, int hook_vertex, double hook_k, double hook_d, double* dl_dq_t,
                                double* dl_dv_t, double* dl_df_acc, void* stream) {
-  k_route_vtx<<<nb(x->nv), 256, 0, S(stream)>>>(*x, mu, ef_damp, b_mu, q_bar, v_bar, coup_fixed, h, alpha, hook_vertex,
+  hdk::launch(k_route_vtx, dim3(nb(x->nv)), dim3(256), 0, S(stream), *x, mu, ef_damp, b_mu, q_bar, v_bar, coup_fixed, h, alpha, hook_vertex,
                                                  hook_k, hook_d, dl_dq_t, dl_dv_t, dl_df_acc);
   return last();
 }
 
 HDK_API int hdk_fixed_coupling_t(const hdk_csr* a_df, const int* fixed, const int* p2v, const double* mu, double* coup,
                                  void* stream) {
-  k_fixed_coupling_t<<<nb(a_df->rows), 256, 0, S(stream)>>>(*a_df, fixed, p2v, mu, coup);
+  hdk::launch(k_fixed_coupling_t, dim3(nb(a_df->rows)), dim3(256), 0, S(stream), *a_df, fixed, p2v, mu, coup);
   return last();
 }
 
 HDK_API int hdk_axpby(int n, double a, const double* x, double b, const double* z, double* y, void* stream) {
-  k_axpby<<<nb(n), 256, 0, S(stream)>>>(n, a, x, b, z, y);
+  hdk::launch(k_axpby, dim3(nb(n)), dim3(256), 0, S(stream), n, a, x, b, z, y);
   return last();
 }
 
 HDK_API int hdk_velocity(int n, const double* q_star, const double* q_t, double h, double* v_star, void* stream) {
-  k_velocity<<<nb(n), 256, 0, S(stream)>>>(n, q_star, q_t, h, v_star);
+  hdk::launch(k_velocity, dim3(nb(n)), dim3(256), 0, S(stream), n, q_star, q_t, h, v_star);
   return last();
 }
 
 HDK_API int hdk_ctl_init(hdk_ctl* ctl, int window, double guard, int k_max, double eps_rel, double eps_abs, double tol,
                          double eps_tr, int iterations0, void* stream) {
-  k_ctl_init<<<1, 1, 0, S(stream)>>>(ctl, window, guard, k_max, eps_rel, eps_abs, tol, eps_tr, iterations0);
+  hdk::launch(k_ctl_init, dim3(1), dim3(1), 0, S(stream), ctl, window, guard, k_max, eps_rel, eps_abs, tol, eps_tr, iterations0);
   return last();
 }
 
 HDK_API int hdk_commit(int n, const hdk_ctl* ctl, const double* q_star, double h, double* q, double* v, void* stream) {
-  k_commit<<<nb(n), 256, 0, S(stream)>>>(n, ctl, q_star, h, q, v);
+  hdk::launch(k_commit, dim3(nb(n)), dim3(256), 0, S(stream), n, ctl, q_star, h, q, v);
   return last();
 }
 
