@@ -110,13 +110,15 @@ __device__ __forceinline__ void ring_init(Ring<S>& r) {
 // Producer warp (one elected lane): keeps S chunks in flight; a stage is
 // refilled once all consumer warps have released it.
 template <int S>
-__device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_beg, int c_end) {
+__device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_beg, int c_end, bool reverse) {
   if ((threadIdx.x & 31) != 0) return;
-  hdk_chunk nxt = c_beg < c_end ? f.chunk[c_beg] : hdk_chunk{};
-  for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
+  const int n = c_end - c_beg;
+  auto chunk_at = [&](int k) { return reverse ? c_end - 1 - k : c_beg + k; };
+  hdk_chunk nxt = n > 0 ? f.chunk[chunk_at(0)] : hdk_chunk{};
+  for (int k = 0; k < n; ++k) {
     const int st = k % S;
     const hdk_chunk ch = nxt;
-    if (c + 1 < c_end) nxt = f.chunk[c + 1];  // descriptor prefetch, off the critical path
+    if (k + 1 < n) nxt = f.chunk[chunk_at(k + 1)];  // descriptor prefetch, off the critical path
     if (k >= S) mbar_wait(&r.empty[st], ((k / S) - 1) & 1);
     fence_proxy_async();
     r.info[st] = ChunkInfo{ch.nseg, ch.tile, ch.seg0, 0};
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
   const int c_beg = range_first(blockIdx.x, gridDim.x, f.n_chunks);
   const int c_end = range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
   if (warp == kWarps) {
-    produce(f, ring, c_beg, c_end);
+    produce(f, ring, c_beg, c_end, false);
     return;
   }
   double b0[kM], b1[kM], b2[kM];
@@ -283,15 +285,17 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
   ring_init(ring);
   const int c_beg = range_first(blockIdx.x, gridDim.x, f.n_chunks);
   const int c_end = range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
+  // Pass 2 walks its range backwards: the tail pass 1 just streamed is still
+  // in L2, and pass 2 ends where the next pass 1 begins.
   if (warp == kWarps) {
-    produce(f, ring, c_beg, c_end);
+    produce(f, ring, c_beg, c_end, true);
     return;
   }
   double x0[kM], x1[kM], x2[kM];
 #pragma unroll
   for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
   int tile = -1;
-  for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
+  for (int k = 0; k < c_end - c_beg; ++k) {
     const int st = k % kStages2;
     mbar_wait(&ring.full[st], (k / kStages2) & 1);
     const ChunkInfo ch = ring.info[st];
