@@ -130,6 +130,7 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
 }
 
 // ---- pass 1 ------------------------------------------------------------------
+template <bool kDry = false>  // kDry: stream only (microbenchmarks)
 __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double* __restrict__ rhs) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
@@ -161,33 +162,50 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
       }
     }
     const double* vals = ring.vals[st];
-    // segment i of the chunk goes to warp (seg0 + i) mod 8: balanced over chunks
-    for (int i = (warp - ch.seg0) & (kWarps - 1); i < ch.nseg; i += kWarps) {
-      const hdk_seg sg = ring.segs[st][i];
-      const int lo = sg.clo_len & 0xffff, hi = lo + (sg.clo_len >> 16);
-      const double* v = vals + sg.coff - lo;  // v[cl] = S'(row, tile column cl)
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    // segment pair p = {2p, 2p+1} of the chunk goes to warp (seg0/2 + p) mod 8
+    // (balanced over chunks); the two dot products share one shuffle tree.
+    const int npair = (ch.nseg + 1) >> 1;
+    for (int pi = (warp - (ch.seg0 >> 1)) & (kWarps - 1); pi < (kDry ? 0 : npair); pi += kWarps) {
+      const int ia = 2 * pi, ib = ia + 1;
+      const bool hasb = ib < ch.nseg;
+      const hdk_seg sa = ring.segs[st][ia];
+      const hdk_seg sb = hasb ? ring.segs[st][ib] : sa;
+      const int la = sa.clo_len & 0xffff, ha = hasb || true ? la + (sa.clo_len >> 16) : 0;
+      const int lb = sb.clo_len & 0xffff, hb = hasb ? lb + (sb.clo_len >> 16) : lb;
+      const double* va = vals + sa.coff - la;
+      const double* vb = vals + sb.coff - lb;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
-        if (cl >= lo && cl < hi) {
-          const double w = v[cl];
-          a0 += w * b0[m];
-          a1 += w * b1[m];
-          a2 += w * b2[m];
-        }
+        const double wa = (cl >= la && cl < ha) ? va[cl] : 0.0;
+        const double wb = (cl >= lb && cl < hb) ? vb[cl] : 0.0;
+        a0 += wa * b0[m];
+        a1 += wa * b1[m];
+        a2 += wa * b2[m];
+        c0 += wb * b0[m];
+        c1 += wb * b1[m];
+        c2 += wb * b2[m];
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         a0 += __shfl_xor_sync(0xffffffffu, a0, o);
         a1 += __shfl_xor_sync(0xffffffffu, a1, o);
         a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
       }
       if (lane == 0) {
-        double* p = f.part1 + 3 * (size_t)sg.pslot;
+        double* p = f.part1 + 3 * (size_t)sa.pslot;
         p[0] = a0;
         p[1] = a1;
         p[2] = a2;
+      } else if (lane == 1 && hasb) {
+        double* p = f.part1 + 3 * (size_t)sb.pslot;
+        p[0] = c0;
+        p[1] = c1;
+        p[2] = c2;
       }
     }
     __syncwarp();
@@ -231,50 +249,44 @@ __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
 // ---- pass 2 ------------------------------------------------------------------
 struct Pass2Smem {
   Ring<kStages2> ring;
-  double fold[kWarps / 2][3][kW];
+  double fold[3][kW];  // running sum of the fold (warps 7 -> 0)
 };
 
-// Fixed-order fold of the consumer warps' accumulators (4..7 into 0..3, 2..3
-// into 0..1, 1 into 0) and write of the tile partial; consumer warps only.
+// Fixed-order fold of the consumer warps' accumulators (7, 6, ..., 0 through
+// one tile-sized buffer) and write of the tile partial; consumer warps only.
 __device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& sm, int slot, double (&x0)[kM],
                                                double (&x1)[kM], double (&x2)[kM]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int half = kWarps / 2; half >= 1; half >>= 1) {
-    consumers_sync();
-    if (warp >= half && warp < 2 * half) {
-#pragma unroll
-      for (int m = 0; m < kM; ++m) {
-        const int cl = lane + 32 * m;
-        sm.fold[warp - half][0][cl] = x0[m];
-        sm.fold[warp - half][1][cl] = x1[m];
-        sm.fold[warp - half][2][cl] = x2[m];
-      }
-    }
-    consumers_sync();
-    if (warp < half) {
+  consumers_sync();
+#pragma unroll 1
+  for (int w = kWarps - 1; w >= 0; --w) {
+    if (warp == w) {
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
-        x0[m] += sm.fold[warp][0][cl];
-        x1[m] += sm.fold[warp][1][cl];
-        x2[m] += sm.fold[warp][2][cl];
+        const bool first = w == kWarps - 1;
+        const double s0 = first ? x0[m] : sm.fold[0][cl] + x0[m];
+        const double s1 = first ? x1[m] : sm.fold[1][cl] + x1[m];
+        const double s2 = first ? x2[m] : sm.fold[2][cl] + x2[m];
+        if (w == 0) {
+          double* p = f.part2 + 3 * ((size_t)slot * kW + cl);
+          p[0] = s0;
+          p[1] = s1;
+          p[2] = s2;
+        } else {
+          sm.fold[0][cl] = s0;
+          sm.fold[1][cl] = s1;
+          sm.fold[2][cl] = s2;
+        }
       }
     }
-  }
-  if (warp == 0) {
-#pragma unroll
-    for (int m = 0; m < kM; ++m) {
-      double* p = f.part2 + 3 * ((size_t)slot * kW + lane + 32 * m);
-      p[0] = x0[m];
-      p[1] = x1[m];
-      p[2] = x2[m];
-    }
+    consumers_sync();
   }
 #pragma unroll
   for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
 }
 
+template <bool kDry = false>
 __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
@@ -316,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
         zr2 = __ldg(z + 2);
       }
     }
-    for (int i = i0, j = 0; i < ch.nseg; i += kWarps, ++j) {
+    for (int i = i0, j = 0; i < (kDry ? 0 : ch.nseg); i += kWarps, ++j) {
       const hdk_seg sg = ring.segs[st][i];
       const int lo = sg.clo_len & 0xffff, hi = lo + (sg.clo_len >> 16);
       const double* v = vals + sg.coff - lo;
@@ -370,13 +382,13 @@ int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatte
   static bool configured = false;
   const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem);
   if (!configured) {
-    cudaFuncSetAttribute(k_rowdot, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
-    cudaFuncSetAttribute(k_coltile, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s2));
+    cudaFuncSetAttribute(k_rowdot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
+    cudaFuncSetAttribute(k_coltile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s2));
     int dev = 0, sms = 148, b1 = 1, b2 = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_rowdot, kThreads, s1);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_coltile, kThreads, s2);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_rowdot<false>, kThreads, s1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_coltile<false>, kThreads, s2);
     g_grid1 = sms * (b1 > 0 ? b1 : 1);  // persistent: one resident wave
     g_grid2 = sms * (b2 > 0 ? b2 : 1);
     configured = true;
@@ -384,9 +396,9 @@ int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatte
   const int g1 = g_grid1 < f->n_chunks ? g_grid1 : f->n_chunks;
   int g2 = g_grid2 < f->n_chunks ? g_grid2 : f->n_chunks;
   if (g2 > f->max_ctas) g2 = f->max_ctas;
-  hdk::launch(k_rowdot, dim3(g1), dim3(kThreads), s1, st, *f, rhs_perm);
+  hdk::launch(k_rowdot<false>, dim3(g1), dim3(kThreads), s1, st, *f, rhs_perm);
   hdk::launch(k_zreduce, dim3((f->n * 8 + 255) / 256), dim3(256), 0, st, *f);
-  hdk::launch(k_coltile, dim3(g2), dim3(kThreads), s2, st, *f);
+  hdk::launch(k_coltile<false>, dim3(g2), dim3(kThreads), s2, st, *f);
   if (scatter)
     hdk::launch(k_xreduce<true>, dim3((f->n + 255) / 256), dim3(256), 0, st, *f, g2, out);
   else
