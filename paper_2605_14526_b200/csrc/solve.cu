@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
       const bool hasb = ib < ch.nseg;
       const hdk_seg sa = ring.segs[st][ia];
       const hdk_seg sb = hasb ? ring.segs[st][ib] : sa;
-      const int la = sa.clo_len & 0xffff, ha = hasb || true ? la + (sa.clo_len >> 16) : 0;
+      const int la = sa.clo_len & 0xffff, ha = la + (sa.clo_len >> 16);
       const int lb = sb.clo_len & 0xffff, hb = hasb ? lb + (sb.clo_len >> 16) : lb;
       const double* va = vals + sa.coff - la;
       const double* vb = vals + sb.coff - lb;
@@ -249,38 +249,45 @@ __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
 // ---- pass 2 ------------------------------------------------------------------
 struct Pass2Smem {
   Ring<kStages2> ring;
-  double fold[3][kW];  // running sum of the fold (warps 7 -> 0)
+  double fold[kWarps / 2][3][kW];
 };
 
-// Fixed-order fold of the consumer warps' accumulators (7, 6, ..., 0 through
-// one tile-sized buffer) and write of the tile partial; consumer warps only.
+// Fixed-order fold of the consumer warps' accumulators (4..7 into 0..3, 2..3
+// into 0..1, 1 into 0) and write of the tile partial; consumer warps only.
 __device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& sm, int slot, double (&x0)[kM],
                                                double (&x1)[kM], double (&x2)[kM]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  consumers_sync();
-#pragma unroll 1
-  for (int w = kWarps - 1; w >= 0; --w) {
-    if (warp == w) {
+#pragma unroll
+  for (int half = kWarps / 2; half >= 1; half >>= 1) {
+    consumers_sync();
+    if (warp >= half && warp < 2 * half) {
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
-        const bool first = w == kWarps - 1;
-        const double s0 = first ? x0[m] : sm.fold[0][cl] + x0[m];
-        const double s1 = first ? x1[m] : sm.fold[1][cl] + x1[m];
-        const double s2 = first ? x2[m] : sm.fold[2][cl] + x2[m];
-        if (w == 0) {
-          double* p = f.part2 + 3 * ((size_t)slot * kW + cl);
-          p[0] = s0;
-          p[1] = s1;
-          p[2] = s2;
-        } else {
-          sm.fold[0][cl] = s0;
-          sm.fold[1][cl] = s1;
-          sm.fold[2][cl] = s2;
-        }
+        sm.fold[warp - half][0][cl] = x0[m];
+        sm.fold[warp - half][1][cl] = x1[m];
+        sm.fold[warp - half][2][cl] = x2[m];
       }
     }
     consumers_sync();
+    if (warp < half) {
+#pragma unroll
+      for (int m = 0; m < kM; ++m) {
+        const int cl = lane + 32 * m;
+        x0[m] += sm.fold[warp][0][cl];
+        x1[m] += sm.fold[warp][1][cl];
+        x2[m] += sm.fold[warp][2][cl];
+      }
+    }
+  }
+  if (warp == 0) {
+#pragma unroll
+    for (int m = 0; m < kM; ++m) {
+      double* p = f.part2 + 3 * ((size_t)slot * kW + lane + 32 * m);
+      p[0] = x0[m];
+      p[1] = x1[m];
+      p[2] = x2[m];
+    }
   }
 #pragma unroll
   for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
