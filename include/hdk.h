@@ -204,6 +204,8 @@ HDK_API int hdk_fixed_coupling_t(const hdk_csr* a_df, const int* fixed, const in
 /* Resets the loop-control block (first kernel of every step graph). */
 HDK_API int hdk_ctl_init(hdk_ctl* ctl, int window, double guard, int k_max, double eps_rel, double eps_abs, double tol,
                          double eps_tr, int iterations0, void* stream);
+/* Resets the loop counter and Anderson history only (tau/rho/err kept). */
+HDK_API int hdk_aa_reset(hdk_ctl* ctl, int window, double guard, int k_max, double tol, void* stream);
 /* State commit after a successful step: v = (q* - q)/h, q = q* (skipped when
  * ctl->err != 0 so a failed step leaves the state intact, heterodyn.h:87-90). */
 HDK_API int hdk_commit(int n, const hdk_ctl* ctl, const double* q_star, double h, double* q, double* v, void* stream);
@@ -211,6 +213,56 @@ HDK_API int hdk_commit(int n, const hdk_ctl* ctl, const double* q_star, double h
 HDK_API int hdk_axpby(int n, double a, const double* x, double b, const double* z, double* y, void* stream);
 /* v* = (q* - q_t)/h (forward.cpp:253). */
 HDK_API int hdk_velocity(int n, const double* q_star, const double* q_t, double h, double* v_star, void* stream);
+
+/* ---- contact (contact.cu) ------------------------------------------------ */
+/* Device view of one step's contact set in the reference's stacked row order:
+ * nc normal rows, then two tangent rows per frictional contact (contact.hpp:59-88). */
+typedef struct hdk_contacts {
+  int nc, nf, k, nu;          /* normal contacts, frictional contacts, rows, unique vertices */
+  const int* vertex;          /* nc */
+  const double* normal;       /* 3 nc */
+  const double* t1;           /* 3 nc */
+  const double* t2;           /* 3 nc */
+  const double* gap;          /* nc: gap offsets */
+  const double* mu;           /* nc: friction coefficients */
+  const double* r_n;          /* nc: h^2 W_nn */
+  const double* r_f;          /* nc: h^2 mean tangent W */
+  const int* fric;            /* nf: contact index of the f-th frictional contact */
+  const int* row_unique;      /* k: unique-vertex slot of each row */
+  const int* urow_off;        /* nu+1 */
+  const int* urow;            /* k: rows of each unique vertex, ascending */
+} hdk_contacts;
+
+/* flags[v * n_obstacles + o] = signed distance <= margin for free vertices
+ * (detect_contacts, contact.cpp:117-144); obstacles: 8 doubles each
+ * {kind(0 half-space, 1 sphere), nx, ny, nz, offset|radius, cx, cy, cz}. */
+HDK_API int hdk_contact_detect(int nv, const int* v2p, const double* q, int n_obstacles, const double* obstacles,
+                               double margin, unsigned char* flags, void* stream);
+HDK_API int hdk_contact_weights(const hdk_contacts* c, const double* q, const double* q_t, const double* lambda,
+                                double* omega, double* e_diag, void* stream);
+HDK_API int hdk_contact_jq(const hdk_contacts* c, const double* q, double* jq, void* stream);
+/* Lifted multiplier system of contact_iteration (column-major M). */
+HDK_API int hdk_contact_system(const hdk_contacts* c, const double* W, const double* omega, const double* e_diag,
+                               const double* lambda, const double* jq0, const double* q_t, double* M, double* rhs,
+                               void* stream);
+HDK_API int hdk_contact_project(const hdk_contacts* c, const double* step, double* lambda, int* err, void* stream);
+/* out = base + A^{-1} J^T (scale * omega o lambda) through the cached scalar
+ * columns U (n x nu, column-major); g is 3 nu scratch. */
+HDK_API int hdk_contact_correct(const hdk_contacts* c, int n, const int* p2v, const double* U, const double* omega,
+                                const double* lambda, double scale, double* g, const double* base, double* out,
+                                void* stream);
+HDK_API int hdk_contact_spikes(int n, const int* unique_pos, int u0, int count, double* rhs_perm, void* stream);
+HDK_API int hdk_contact_unspike(int n, const double* x_perm, int u0, int count, double* U, void* stream);
+HDK_API int hdk_contact_delassus(const hdk_contacts* c, const double* U, int n, const int* unique_pos, double* W,
+                                 void* stream);
+HDK_API int hdk_contact_reduced(const hdk_contacts* c, const double* X, size_t ldx, const double* omega,
+                                const double* e_diag, const double* z0, double* M, double* rhs, void* stream);
+HDK_API int hdk_contact_combine(int n3, const double* z0, const double* X, size_t ldx, int k, const double* omega,
+                                const double* y, double* mu, int* err, void* stream);
+HDK_API int hdk_contact_column_init(const hdk_contacts* c, int row, int nv, const int* v2p, const double* U, int n,
+                                    double* rhs, double* x0, void* stream);
+HDK_API int hdk_contact_friction_pushback(const hdk_contacts* c, const double* omega, const double* y, double* dl_dq,
+                                          void* stream);
 
 #ifdef __cplusplus
 }

@@ -7,6 +7,8 @@
 #include <cstring>
 #include <functional>
 
+#include <cusolverDn.h>
+
 namespace hdb {
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -77,19 +79,28 @@ void build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()
   cudaGraph_t gpost = capture(st, post);
   out.counts[0] = kernel_nodes(gpre);
   out.counts[2] = kernel_nodes(gpost);
+  size_t npre_nodes = 0, npost_nodes = 0;
+  cuda_check(cudaGraphGetNodes(gpre, nullptr, &npre_nodes), "graph nodes");
+  cuda_check(cudaGraphGetNodes(gpost, nullptr, &npost_nodes), "graph nodes");
   if (!use_cond) {
     cudaGraph_t gbody = capture(st, [&] { body(0ULL); });
     out.counts[1] = kernel_nodes(gbody);
-    out.pre = instantiate(gpre);
+    out.pre = npre_nodes ? instantiate(gpre) : nullptr;
     out.body = instantiate(gbody);
-    out.post = instantiate(gpost);
+    out.post = npost_nodes ? instantiate(gpost) : nullptr;
     for (cudaGraph_t g : {gpre, gbody, gpost}) cudaGraphDestroy(g);
     return;
   }
   cudaGraph_t top = nullptr;
   cuda_check(cudaGraphCreate(&top, 0), "graph create");
   cudaGraphNode_t npre, nloop, npost;
-  cuda_check(cudaGraphAddChildGraphNode(&npre, top, nullptr, 0, gpre), "add pre");
+  const cudaGraphNode_t* dep = nullptr;
+  size_t ndep = 0;
+  if (npre_nodes) {
+    cuda_check(cudaGraphAddChildGraphNode(&npre, top, nullptr, 0, gpre), "add pre");
+    dep = &npre;
+    ndep = 1;
+  }
   cudaGraphConditionalHandle h;
   cuda_check(cudaGraphConditionalHandleCreate(&h, top, 1, cudaGraphCondAssignDefault), "cond handle");
   cudaGraphNodeParams p{};
@@ -97,18 +108,24 @@ void build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()
   p.conditional.handle = h;
   p.conditional.type = cudaGraphCondTypeWhile;
   p.conditional.size = 1;
-  cuda_check(cudaGraphAddNode(&nloop, top, &npre, 1, &p), "add while");
+  cuda_check(cudaGraphAddNode(&nloop, top, dep, ndep, &p), "add while");
   capture_into(st, p.conditional.phGraph_out[0], [&] { body(static_cast<unsigned long long>(h)); });
   out.counts[1] = kernel_nodes(p.conditional.phGraph_out[0]);
-  cuda_check(cudaGraphAddChildGraphNode(&npost, top, &nloop, 1, gpost), "add post");
+  if (npost_nodes) cuda_check(cudaGraphAddChildGraphNode(&npost, top, &nloop, 1, gpost), "add post");
   out.exec = instantiate(top);
   for (cudaGraph_t g : {gpre, gpost, top}) cudaGraphDestroy(g);
+}
+
+cudaGraphExec_t capture_exec(cudaStream_t st, const std::function<void()>& fn, int* kernels) {
+  cudaGraph_t g = capture(st, fn);
+  if (kernels) *kernels = kernel_nodes(g);
+  cudaGraphExec_t e = instantiate(g);
+  cudaGraphDestroy(g);
+  return e;
 }
 }  // namespace
 
 Engine::Engine(const Scene& scene) : scene_(scene), mat_(scene.material) {
-  if (!scene.obstacles.empty())
-    raise(Code::InvalidArgument, "this build's device engine does not yet support obstacle contact scenes");
   const char* nc = std::getenv("HETERODYN_NO_COND_GRAPH");
   use_cond_ = !(nc && std::atoi(nc) != 0);
   int dev_count = 0;
@@ -130,6 +147,13 @@ Engine::Engine(const Scene& scene) : scene_(scene), mat_(scene.material) {
 Engine::~Engine() {
   if (fgraph_) fgraph_->destroy();
   if (bgraph_) bgraph_->destroy();
+  for (cudaGraphExec_t e : {bpre_, bpost_a_, bpost_b_, fpre_, fpost_})
+    if (e) cudaGraphExecDestroy(e);
+  for (void* p : {static_cast<void*>(cjq_), static_cast<void*>(cM_), static_cast<void*>(crhs_), static_cast<void*>(cg_),
+                  static_cast<void*>(cX_), static_cast<void*>(cz0_), static_cast<void*>(cwork_),
+                  static_cast<void*>(cinfo_)})
+    if (p) cudaFree(p);
+  if (cusolver_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(cusolver_));
   frame_mem_.clear();
   fmem_.reset();
   mem_.reset();
@@ -237,6 +261,16 @@ void Engine::build_static() {
   const double hk[5] = {scene_.hook_anchor.x, scene_.hook_anchor.y, scene_.hook_anchor.z, scene_.hook_k, scene_.hook_d};
   hook_ = A.alloc<double>(5);
   DevArena::copy_h2d(hook_, hk, sizeof(hk));
+  // obstacles: {kind, nx, ny, nz, offset|radius, cx, cy, cz}
+  Vec ob;
+  for (const Obstacle& o : scene_.obstacles) {
+    const double rec[8] = {static_cast<double>(o.kind), o.normal.x, o.normal.y, o.normal.z,
+                           o.kind == 0 ? o.offset : o.radius, o.center.x, o.center.y, o.center.z};
+    ob.insert(ob.end(), rec, rec + 8);
+  }
+  obst_ = A.upload(ob);
+  flags_ = A.alloc<unsigned char>(static_cast<size_t>(nv) * std::max<size_t>(1, scene_.obstacles.size()));
+  q0c_ = A.alloc<double>(n3);
   aa_window_ = scene_.solver.aa_window > 0 ? scene_.solver.aa_window : (mat_.contrast() > 10.0 ? 1 : 5);
   aa_window_ = std::min(aa_window_, HDK_AA_MAX);
 }
@@ -335,6 +369,15 @@ void Engine::build_forward_graph() {
     hdk_check(hdk_local_step(&dm_, &dmat_, qcur_, ef_, cache_, &ctl_->err, s), "cache sweep");
   };
   build_loop_graph(st_, use_cond_, pre, body, post, *fgraph_);
+  for (cudaGraphExec_t* e : {&fpre_, &fpost_})
+    if (*e) {
+      cudaGraphExecDestroy(*e);
+      *e = nullptr;
+    }
+  if (!scene_.obstacles.empty()) {
+    fpre_ = capture_exec(st_, pre, nullptr);
+    fpost_ = capture_exec(st_, post, nullptr);
+  }
   fk_pre_ = fgraph_->counts[0];
   fk_body_ = fgraph_->counts[1];
   fk_post_ = fgraph_->counts[2];
@@ -345,12 +388,17 @@ void Engine::build_backward_graph() {
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
   const double h = so.h;
   const bool has_fixed = !hf_.fixed.empty();
-  double umu = mat_.poisson, ula = 0;  // lame(1, nu)
-  umu = 1.0 / (2.0 * (1.0 + mat_.poisson));
-  ula = mat_.poisson / ((1.0 + mat_.poisson) * (1.0 - 2.0 * mat_.poisson));
+  const double umu = 1.0 / (2.0 * (1.0 + mat_.poisson));  // lame(1, nu) (backward.cpp:363)
+  const double ula = mat_.poisson / ((1.0 + mat_.poisson) * (1.0 - 2.0 * mat_.poisson));
   void* s = st_;
-  auto pre = [&] {
-    hdk_check(hdk_ctl_init(ctl_, HDK_AA_MAX, 1e8, 500, 0.0, 0.0, 1e-10, so.eps_tr, 1, s), "ctl init");
+  for (cudaGraphExec_t* e : {&bpre_, &bpost_a_, &bpost_b_})
+    if (*e) {
+      cudaGraphExecDestroy(*e);
+      *e = nullptr;
+    }
+  // tr_select_tau, differential, seed and the backbone's first solve
+  bpre_ = capture_exec(st_, [&] {
+    hdk_check(hdk_ctl_init(ctl_, HDK_AA_MAX, 1e8, 500, 0.0, 0.0, 1e-10, so.eps_tr, 0, s), "ctl init");
     hdk_check(hdk_tr_model(&dv_, &a_ff_, bqstar_, bqprev_, dqp_, part_a_, s), "tr model");
     hdk_check(hdk_element_energy(&dm_, &dmat_, bqprev_, eprev_, &ctl_->bad, s), "energy prev");
     hdk_check(hdk_element_energy(&dm_, &dmat_, bqstar_, estar_, &ctl_->bad, s), "energy star");
@@ -362,7 +410,9 @@ void Engine::build_backward_graph() {
     cuda_check(cudaMemsetAsync(t_, 0, n3 * sizeof(double), st_), "t zero");
     hdk_check(hdk_gather_perm(&dv_, seed_, nullptr, rhs_, s), "x0 rhs");
     hdk_check(hdk_apply_inverse3(&df_, rhs_, x_, s), "x0 solve");
-  };
+  }, &bk_pre_);
+  // backbone fixed point x <- A^{-1}(seed + B x) with AA(8) (backward.cpp:170-204)
+  auto pre = [&] { hdk_check(hdk_aa_reset(ctl_, HDK_AA_MAX, 1e8, 500, 1e-10, s), "aa reset"); };
   auto body = [&](unsigned long long handle) {
     hdk_check(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B x");
     hdk_check(hdk_gather_perm(&dv_, seed_, ef_, rhs_, s), "rhs");
@@ -372,7 +422,12 @@ void Engine::build_backward_graph() {
     hdk_check(hdk_aa_mix(&dv_, ctl_, t_, x_, nullptr, nullptr, dq_, dg_, part_c_, 1, s), "aa mix");
     hdk_check(hdk_backbone_cond(ctl_, handle, s), "cond");
   };
-  auto post = [&] {
+  build_loop_graph(st_, use_cond_, pre, body, [] {}, *bgraph_);
+  bk_body_ = bgraph_->counts[1];
+  bk_pre_ += bgraph_->counts[0];
+  // gradient routing (backward.cpp:286-394); the contact path adds the
+  // friction pushback between the two halves
+  bpost_a_ = capture_exec(st_, [&] {
     if (has_fixed) {
       hdk_check(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B mu");
       hdk_check(hdk_gather(&dv_, ef_, 0.0, x_, nullptr, bmu_, s), "B mu gather");
@@ -383,13 +438,13 @@ void Engine::build_backward_graph() {
     hdk_check(hdk_route_vertices(&dv_, x_, dmat_.beta_vh ? ef2_ : nullptr, has_fixed ? bmu_ : nullptr, qbar_, vbar_,
                                  has_fixed ? coup_ : nullptr, h, mat_.alpha, scene_.hook ? scene_.hook_vertex : -1,
                                  scene_.hook_k, scene_.hook_d, dlq_, dlv_, dfacc_, s), "route vertices");
+  }, &bk_post_);
+  int kb = 0;
+  bpost_b_ = capture_exec(st_, [&] {
     hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, dlq_, 1.0, direct_, qbar_, s), "next q seed");
     hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, dlv_, 0.0, nullptr, vbar_, s), "next v seed");
-  };
-  build_loop_graph(st_, use_cond_, pre, body, post, *bgraph_);
-  bk_pre_ = bgraph_->counts[0];
-  bk_body_ = bgraph_->counts[1];
-  bk_post_ = bgraph_->counts[2];
+  }, &kb);
+  bk_post_ += kb;
 }
 
 void Engine::sync_ctl() {
@@ -403,13 +458,13 @@ void Engine::run_graph(LoopGraph& g, const char* what) {
     return;
   }
   // host-driven loop (profiling fallback): one status read per iteration
-  cuda_check(cudaGraphLaunch(g.pre, st_), what);
+  if (g.pre) cuda_check(cudaGraphLaunch(g.pre, st_), what);
   for (;;) {
     cuda_check(cudaGraphLaunch(g.body, st_), what);
     sync_ctl();
     if (!h_ctl_->cond) break;
   }
-  cuda_check(cudaGraphLaunch(g.post, st_), what);
+  if (g.post) cuda_check(cudaGraphLaunch(g.post, st_), what);
 }
 
 void Engine::check_ctl(const char* what) {
@@ -428,7 +483,22 @@ void Engine::check_ctl(const char* what) {
 
 void Engine::step() {
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
-  run_graph(*fgraph_, "forward graph");
+  std::shared_ptr<ContactFrame> contacts;
+  if (!scene_.obstacles.empty()) {
+    cuda_check(cudaGraphLaunch(fpre_, st_), "forward pre");
+    kernel_launches += fk_pre_;
+    contacts = detect_and_setup();
+  }
+  if (contacts && contacts->k > 0) {
+    contact_loop(*contacts);
+    cuda_check(cudaGraphLaunch(fpost_, st_), "forward post");
+    // weights at the converged state (forward.cpp:258-262)
+    hdk_check(hdk_contact_weights(&contacts->view, qcur_, q_, contacts->lambda, contacts->omega, contacts->e_diag, st_),
+              "weights star");
+    kernel_launches += fk_post_ + 1;
+  } else {
+    run_graph(*fgraph_, "forward graph");
+  }
   if (recording_) {
     if (static_cast<int>(slots_.size()) <= nrec_) {
       auto a = std::make_unique<DevArena>();
@@ -455,12 +525,15 @@ void Engine::step() {
   }
   hdk_check(hdk_commit(static_cast<int>(n3), ctl_, qcur_, scene_.solver.h, q_, v_, st_), "commit");
   sync_ctl();
-  solve_count += h_ctl_->iterations;
-  kernel_launches += fk_pre_ + static_cast<long long>(fk_body_) * h_ctl_->iterations + fk_post_ + 1;
+  if (!(contacts && contacts->k > 0)) {
+    solve_count += h_ctl_->iterations;
+    kernel_launches += fk_pre_ + static_cast<long long>(fk_body_) * h_ctl_->iterations + fk_post_ + 1;
+  }
   check_ctl("forward step");
   last_iterations = h_ctl_->iterations;
   last_converged = h_ctl_->converged;
-  last_contacts = 0;
+  last_contacts = contacts ? contacts->nc : 0;
+  if (recording_) slots_[nrec_].contacts = contacts;
   time_ += scene_.solver.h;
   if (recording_) ++nrec_;
 }
@@ -529,15 +602,7 @@ GradOut Engine::backward(const double* direct, const double* dq_final, const dou
     cp(bqstar_, f.qstar, n3);
     cp(bcache_, f.cache, 24 * ne);
     if (direct) cuda_check(cudaMemcpyAsync(direct_, direct + static_cast<size_t>(t) * n3, B, cudaMemcpyHostToDevice, st_), "direct");
-    run_graph(*bgraph_, "backward graph");
-    sync_ctl();
-    ++a_spmv_count;
-    solve_count += h_ctl_->iterations;
-    kernel_launches += bk_pre_ + static_cast<long long>(bk_body_) * (h_ctl_->iterations - 1) + bk_post_;
-    check_ctl("backward step");
-    out.tau[t] = h_ctl_->tau;
-    out.rho[t] = h_ctl_->rho;
-    out.adjoint_iterations += h_ctl_->iterations;
+    backward_frame(t, out);
   }
   if (!download) return out;
   const auto d2h = [&](Vec& v, const double* d, size_t n) {

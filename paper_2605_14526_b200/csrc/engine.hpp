@@ -48,6 +48,23 @@ struct LoopGraph {
 };
 
 
+// One step's contact set: host copy (reference layout) + device view, the
+// cached scalar inverse columns U = A_s^{-1} E of its unique vertices, and the
+// converged multipliers / NCP weights consumed by the adjoint.
+struct ContactFrame {
+  int nc = 0, nf = 0, k = 0, nu = 0;
+  std::vector<int> vertex, fric, row_unique, urow_off, urow, unique_vertex, unique_pos;
+  Vec normal, t1, t2, gap, mu, r_n, r_f;
+  std::unique_ptr<DevArena> mem;
+  hdk_contacts view{};
+  double* U = nullptr;        // n x nu, column-major (elimination order rows)
+  int* unique_pos_d = nullptr;
+  double* W = nullptr;        // k x k
+  double* lambda = nullptr;   // k
+  double* omega = nullptr;    // k (weights_star after the step)
+  double* e_diag = nullptr;   // k
+};
+
 struct GradOut {
   Vec dl_dq0, dl_dv0, dl_df_ext, dl_de, dl_dw;
   std::vector<double> tau, rho;
@@ -89,6 +106,10 @@ class Engine {
   void build_forward_graph();
   void build_backward_graph();
   void run_graph(LoopGraph& g, const char* what);
+  void backward_frame(int t, GradOut& out);
+  std::shared_ptr<ContactFrame> detect_and_setup();
+  void contact_loop(ContactFrame& cf);
+  void ensure_solver_workspace(int k);
   void sync_ctl();
   void check_ctl(const char* what);
 
@@ -130,6 +151,7 @@ class Engine {
 
   struct Frame {
     double *q_t, *v_t, *qtil, *qprev, *qstar, *cache;
+    std::shared_ptr<ContactFrame> contacts;
   };
   std::vector<Frame> slots_;  // device storage of recorded frames (reused)
   std::vector<std::unique_ptr<DevArena>> frame_mem_;
@@ -140,6 +162,20 @@ class Engine {
   double* rest_ = nullptr;  // rest positions (canonical loss seed)
   int fk_pre_ = 0, fk_body_ = 0, fk_post_ = 0, bk_pre_ = 0, bk_body_ = 0, bk_post_ = 0;
   std::unique_ptr<LoopGraph> fgraph_, bgraph_;
+  cudaGraphExec_t bpre_ = nullptr, bpost_a_ = nullptr, bpost_b_ = nullptr;
+  cudaGraphExec_t fpre_ = nullptr, fpost_ = nullptr;  // pieces of the forward graph (contact path)
+  // contact
+  double* obst_ = nullptr;  // 8 doubles per obstacle
+  unsigned char* flags_ = nullptr;
+  double* q0c_ = nullptr;   // contact-free solve result of one iteration (full)
+  double *cjq_ = nullptr, *cM_ = nullptr, *crhs_ = nullptr, *cg_ = nullptr, *cX_ = nullptr, *cz0_ = nullptr;
+  size_t cX_cols_ = 0;
+  int c_cap_ = 0;
+  void* cusolver_ = nullptr;
+  double* cwork_ = nullptr;
+  int cwork_len_ = 0;
+  int* cinfo_ = nullptr;
+  std::shared_ptr<ContactFrame> cur_contacts_;
 };
 
 }  // namespace hdb

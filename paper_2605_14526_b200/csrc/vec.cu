@@ -640,6 +640,15 @@ __global__ void k_ctl_init(hdk_ctl* c, int window, double guard, int k_max, doub
   for (int i = 0; i < HDK_AA_MAX * HDK_AA_MAX; ++i) c->gram[i] = 0.0;
 }
 
+// Resets the loop / Anderson fields only (keeps tau, rho, bad, err).
+__global__ void k_aa_reset(hdk_ctl* c, int window, double guard, int k_max, double tol) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  c->k = 0; c->k_max = k_max; c->iterations = 0; c->converged = 0; c->done = 0; c->cond = 1;
+  c->window = window < 1 ? 1 : window; c->count = 0; c->head = 0; c->has_last = 0; c->mixed = 0;
+  c->guard = guard; c->tol = tol;
+}
+
 __global__ void k_commit(int n, const hdk_ctl* ctl, const double* qs, double h, double* q, double* v) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
@@ -762,6 +771,11 @@ HDK_API int hdk_velocity(int n, const double* q_star, const double* q_t, double 
 HDK_API int hdk_ctl_init(hdk_ctl* ctl, int window, double guard, int k_max, double eps_rel, double eps_abs, double tol,
                          double eps_tr, int iterations0, void* stream) {
   hdk::launch(k_ctl_init, dim3(1), dim3(1), 0, S(stream), ctl, window, guard, k_max, eps_rel, eps_abs, tol, eps_tr, iterations0);
+  return last();
+}
+
+HDK_API int hdk_aa_reset(hdk_ctl* ctl, int window, double guard, int k_max, double tol, void* stream) {
+  hdk::launch(k_aa_reset, dim3(1), dim3(1), 0, S(stream), ctl, window, guard, k_max, tol);
   return last();
 }
 

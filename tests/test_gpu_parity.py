@@ -28,7 +28,7 @@ def rest_of(scene):
     return None
 
 
-def run(lib, scene, frames, perturb=0.0):
+def run(lib, scene, frames, perturb=0.0, contacts=None):
     sc = lib.scene(scene)
     sim = sc.sim()
     if perturb:
@@ -39,6 +39,8 @@ def run(lib, scene, frames, perturb=0.0):
     for _ in range(frames):
         sim.step()
         traj.append((sim.positions(), sim.velocities(), sim.last_iterations, sim.last_converged))
+        if contacts is not None:
+            contacts.append(sim.last_contact_count)
     q, v = traj[-1][0], traj[-1][1]
     g = sim.backward(dl_dq_final=q, dl_dv_final=v)
     return traj, g
@@ -91,6 +93,42 @@ def test_trajectory_and_gradients(prod, orc, name):
             assert np.linalg.norm(gp[k]) == 0
             continue
         assert rel2(gp[k], go[k]) <= tol[k], (k, rel2(gp[k], go[k]), tol[k])
+
+
+CONTACT_CASES = {
+    "block-floor-friction": (scenes.block_scene(floor=True, friction=0.5, v0_amp=0.0, gravity_z=-2.0), 4),
+    "resting-box": ({"mesh": {"generator": "resting-box"}, "frames": 4,
+                     "solver": {"eps_rel": 1e-12, "eps_abs": 1e-14}}, 4),
+    "ball-drop": ({"mesh": {"generator": "ball-drop"}, "frames": 4, "initial": {"velocity": [0, 0, -20.0]},
+                   "solver": {"eps_rel": 1e-12, "eps_abs": 1e-14}}, 4),
+    "slab-on-sphere": ({"mesh": {"generator": "slab-on-sphere"}, "frames": 3, "gravity": [0, 0, -9.81],
+                        "initial": {"position_offset": [0, 0, -0.005]},
+                        "solver": {"eps_rel": 1e-12, "eps_abs": 1e-14}}, 3),
+}
+
+
+@pytest.mark.parametrize("name", list(CONTACT_CASES))
+def test_contact_trajectory_and_gradients(prod, orc, name):
+    """Contact sets per frame identical; state and chained gradients through the
+    frictional contact path (backward.cpp:227-283) within tolerance."""
+    scene, frames = CONTACT_CASES[name]
+    cp_, co_ = [], []
+    tp, gp = run(prod, scene, frames, contacts=cp_)
+    to, go = run(orc, scene, frames, contacts=co_)
+    assert cp_ == co_, (cp_, co_)
+    assert max(co_) > 0, "scene must exercise contact"
+    for f, ((qp, vp, ip, cpf), (qo, vo, io, cof)) in enumerate(zip(tp, to)):
+        assert cpf == cof
+        assert rel2(qp, qo) <= 1e-6, (f, rel2(qp, qo))
+        if np.linalg.norm(vo) > 1e-8:
+            assert rel2(vp, vo) <= 1e-6, (f, rel2(vp, vo))
+    np.testing.assert_array_equal(gp["tau"], go["tau"])
+    _, gs = run(orc, scene, frames, perturb=1e-15)
+    for k in GRADS:
+        if np.linalg.norm(go[k]) == 0:
+            continue
+        tol = max(1e-6, 10 * rel2(gs[k], go[k]))
+        assert rel2(gp[k], go[k]) <= tol, (k, rel2(gp[k], go[k]), tol)
 
 
 def test_solve_matches_oracle_and_inverts(prod, orc):
