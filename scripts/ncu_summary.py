@@ -20,7 +20,7 @@ def launches(path):
             v = float(r[vi].replace(",", ""))
         except ValueError:
             continue
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         name = r[ki].split("(")[0].replace("<unnamed>::", "")
         agg[name][0] += 1
         agg[name][1] += v
@@ -55,7 +55,32 @@ def report(path):
     return "\n".join(out)
 
 
+def traffic(path, kernels=("k_rowdot", "k_zreduce", "k_coltile", "k_xreduce")):
+    """DRAM bytes (read + write) of one 3-axis solve: the first capture of each
+    solve kernel in a --set full report, summed."""
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    h, units = rows[0], rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    seen = {}
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")].split("(")[0].replace("<unnamed>::", "").replace("void ", "")
+        base = name.split("<")[0]
+        if base in kernels and base not in seen:
+            b = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                b += float(r[h.index(k)].replace(",", "")) * scale[units[h.index(k)]]
+            seen[base] = b
+    return seen
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "--traffic":
+        import json
+        per = traffic(sys.argv[2])
+        print(json.dumps({"traffic_bytes_per_solve": sum(per.values()), "per_kernel_bytes": per,
+                          "source": sys.argv[2]}, indent=1))
+        sys.exit(0)
     for p in sys.argv[1:]:
         print(f"== {p}")
         print(launches(p) if p.endswith(".csv") else report(p))
