@@ -209,6 +209,14 @@ HDK_API int hdk_aa_reset(hdk_ctl* ctl, int window, double guard, int k_max, doub
 /* State commit after a successful step: v = (q* - q)/h, q = q* (skipped when
  * ctl->err != 0 so a failed step leaves the state intact, heterodyn.h:87-90). */
 HDK_API int hdk_commit(int n, const hdk_ctl* ctl, const double* q_star, double h, double* q, double* v, void* stream);
+
+/* ---- batched system-ID reductions (batch.cu) ---------------------------
+ * out = 1/2 |q - ref|^2 (n doubles, one deterministic block). */
+HDK_API int hdk_half_sqdist(int n, const double* q, const double* ref, double* out, void* stream);
+/* out[0] = sum_s loss[s], out[1 + i] = sum_s vec[s][i] in sample order; vec is
+ * a device array of `samples` device pointers to n doubles. */
+HDK_API int hdk_batch_sum(int samples, int n, const double* const* vec, const double* loss, double* out,
+                          void* stream);
 /* y = a x + b z elementwise over n doubles (z may be NULL). */
 HDK_API int hdk_axpby(int n, double a, const double* x, double b, const double* z, double* y, void* stream);
 /* v* = (q* - q_t)/h (forward.cpp:253). */

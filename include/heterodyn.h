@@ -166,6 +166,33 @@ HD_API long long hd_sim_kernel_launches(const hd_sim* sim);
  * moves (factor values read by both passes plus right-hand sides). */
 HD_API hd_status hd_sim_time_solve(hd_sim* sim, int reps, double* ms_per_solve, double* bytes_per_solve);
 
+/* ---- batched system-ID (config C5; new) --------------------------------
+ * One process's share of a batch of material-parameter samples.  Sample s
+ * simulates the scene with per-element Young's moduli young[s * ne .. +ne)
+ * (NULL = the scene's own for every sample) from the scene's initial state.
+ * One evaluation runs, for every sample, `frames` forward steps and the
+ * adjoint chain of L_s = 1/2 |q_T - q_target|^2 (roll + chain_backward,
+ * drivers.cpp:31-99, the objective of run_identify, drivers.cpp:848-851)
+ * and returns the per-sample losses and the sample-ordered sums
+ * sum_s L_s, sum_s dL_s/dE (element_count doubles).  The default target is
+ * the scene's initial positions.  threads = host threads driving samples
+ * concurrently (the product overlaps them on the device; the oracle runs
+ * them in order).  device_out, if not NULL, is a device pointer receiving
+ * [sum L, sum dL/dE] (1 + element_count doubles) — the buffer a caller hands
+ * to an NCCL all-reduce; it is complete when the call returns. */
+typedef struct hd_batch hd_batch;
+HD_API hd_batch* hd_batch_create(const hd_scene* scene, int samples, const double* young, size_t young_count,
+                                 int threads);
+HD_API void hd_batch_free(hd_batch* batch);
+HD_API int hd_batch_sample_count(const hd_batch* batch);
+HD_API hd_status hd_batch_set_target(hd_batch* batch, const double* q_target, size_t count);
+HD_API hd_status hd_batch_evaluate(hd_batch* batch, int frames, double* loss, size_t loss_capacity,
+                                   double* dl_de_sum, size_t dl_de_capacity, void* device_out);
+/* Device time of the last evaluation in milliseconds (CUDA events spanning
+ * every sample's stream; 0 for the oracle) and kernels launched so far. */
+HD_API double hd_batch_last_ms(const hd_batch* batch);
+HD_API long long hd_batch_kernel_launches(const hd_batch* batch);
+
 #ifdef __cplusplus
 }
 #endif

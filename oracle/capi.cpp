@@ -338,4 +338,74 @@ long long hd_sim_solve_count(const hd_sim* sim) {
 long long hd_sim_a_spmv_count(const hd_sim* sim) { return sim ? static_cast<long long>(sim->system.a_spmv_count) : 0; }
 long long hd_sim_refactor_count(const hd_sim* sim) { return sim ? static_cast<long long>(sim->system.refactor_count()) : 0; }
 
+
+// ---- batched system-ID (config C5): the checker runs the samples in order
+// with the single-trajectory API above (roll + chain_backward per sample,
+// drivers.cpp:31-99; objective of run_identify, drivers.cpp:848-851).
+struct hd_batch {
+  const hd_scene* scene = nullptr;
+  int samples = 0;
+  std::vector<double> young;  // samples x ne, empty = scene's
+  std::vector<double> target;
+};
+
+hd_batch* hd_batch_create(const hd_scene* scene, int samples, const double* young, size_t young_count, int) {
+  if (!scene) { null_arg("hd_batch_create"); return nullptr; }
+  const size_t ne = scene->spec.mesh.element_count();
+  if (samples < 1 || (young && young_count != ne * static_cast<size_t>(samples))) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_batch_create: bad sample count or young size");
+    return nullptr;
+  }
+  hd_batch* b = new hd_batch;
+  b->scene = scene;
+  b->samples = samples;
+  if (young) b->young.assign(young, young + young_count);
+  b->target = scene->spec.q0;
+  return b;
+}
+void hd_batch_free(hd_batch* b) { delete b; }
+int hd_batch_sample_count(const hd_batch* b) { return b ? b->samples : 0; }
+hd_status hd_batch_set_target(hd_batch* b, const double* q, size_t count) {
+  if (!b || !q) return null_arg("hd_batch_set_target");
+  if (count != b->target.size()) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_batch_set_target: count != dof");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  b->target.assign(q, q + count);
+  return HD_OK;
+}
+hd_status hd_batch_evaluate(hd_batch* b, int frames, double* loss, size_t loss_cap, double* grad, size_t grad_cap,
+                            void* device_out) {
+  if (!b) return null_arg("hd_batch_evaluate");
+  const size_t ne = b->scene->spec.mesh.element_count(), n = b->target.size();
+  if (device_out || frames < 1 || (loss && loss_cap < static_cast<size_t>(b->samples)) || (grad && grad_cap < ne)) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_batch_evaluate: bad argument (the CPU oracle has no device output)");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  std::vector<double> sum(ne, 0.0), dle(ne), q(n), dq(n);
+  for (int s = 0; s < b->samples; ++s) {
+    hd_sim* sim = hd_sim_create(b->scene);
+    if (!sim) return static_cast<hd_status>(hd_last_error_code());
+    hd_status st = HD_OK;
+    if (!b->young.empty()) st = hd_sim_set_young(sim, b->young.data() + s * ne, ne, 0);
+    if (st == HD_OK) st = hd_sim_record(sim, 1);
+    for (int f = 0; f < frames && st == HD_OK; ++f) st = hd_sim_step(sim);
+    if (st == HD_OK) st = hd_sim_positions(sim, q.data(), n);
+    double l = 0;
+    for (size_t i = 0; i < n; ++i) {
+      dq[i] = q[i] - b->target[i];
+      l += dq[i] * dq[i];
+    }
+    if (st == HD_OK) st = hd_sim_backward(sim, nullptr, dq.data(), nullptr, nullptr, nullptr, nullptr, dle.data(), nullptr, 0);
+    hd_sim_free(sim);
+    if (st != HD_OK) return st;
+    if (loss) loss[s] = 0.5 * l;
+    for (size_t e = 0; e < ne; ++e) sum[e] += dle[e];
+  }
+  if (grad) std::memcpy(grad, sum.data(), ne * sizeof(double));
+  return HD_OK;
+}
+double hd_batch_last_ms(const hd_batch*) { return 0.0; }
+long long hd_batch_kernel_launches(const hd_batch*) { return 0; }
+
 }  // extern "C"

@@ -1,0 +1,132 @@
+// Batched system-ID evaluation; see batch.hpp.
+#include "batch.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <exception>
+#include <mutex>
+#include <thread>
+
+namespace hdb {
+
+namespace {
+
+void hdk_check_b(int status, const char* what) {
+  if (status != 0) raise(Code::InvalidArgument, std::string("CUDA launch failed: ") + what);
+}
+
+// Runs body(i) for i in [0, count) on `threads` host threads (static
+// round-robin: sample i goes to thread i % threads, so a sample's work is
+// always issued from the same thread); the first exception is rethrown.
+template <class F>
+void parallel_samples(int count, int threads, int device, F&& body) {
+  std::exception_ptr err;
+  std::mutex m;
+  const auto run = [&](int t) {
+    try {
+      cuda_check(cudaSetDevice(device), "set device");
+      for (int i = t; i < count; i += threads) body(i);
+    } catch (...) {
+      std::lock_guard<std::mutex> g(m);
+      if (!err) err = std::current_exception();
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(run, t);
+  run(0);
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
+}
+
+}  // namespace
+
+Batch::Batch(const Scene& scene, int samples, const double* young, int threads) : scene_(scene) {
+  if (samples < 1) raise(Code::InvalidArgument, "hd_batch_create: at least one sample required");
+  if (!scene.obstacles.empty())
+    raise(Code::InvalidArgument, "hd_batch_create: batched system-ID runs contact-free scenes (config C5)");
+  cuda_check(cudaGetDevice(&device_), "get device");
+  threads_ = std::max(1, std::min(threads, samples));
+  const int ne = scene.mesh.ne;
+  eng_.resize(samples);
+  parallel_samples(samples, threads_, device_, [&](int s) {
+    if (young) {
+      Vec y(young + static_cast<size_t>(s) * ne, young + static_cast<size_t>(s + 1) * ne);
+      eng_[s] = std::make_unique<Engine>(scene, &y);
+    } else {
+      eng_[s] = std::make_unique<Engine>(scene);
+    }
+  });
+  cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "batch stream");
+  const size_t n3 = 3 * static_cast<size_t>(scene.mesh.nv);
+  cuda_check(cudaMalloc(&target_, n3 * sizeof(double)), "target");
+  cuda_check(cudaMemcpy(target_, scene.q0.data(), n3 * sizeof(double), cudaMemcpyHostToDevice), "target");
+  cuda_check(cudaMalloc(&loss_, samples * sizeof(double)), "loss");
+  cuda_check(cudaMalloc(&out_, (1 + static_cast<size_t>(ne)) * sizeof(double)), "out");
+  std::vector<const double*> g(samples);
+  for (int s = 0; s < samples; ++s) g[s] = eng_[s]->d_dl_de();
+  cuda_check(cudaMalloc(&grads_, samples * sizeof(double*)), "grad pointers");
+  cuda_check(cudaMemcpy(grads_, g.data(), samples * sizeof(double*), cudaMemcpyHostToDevice), "grad pointers");
+}
+
+Batch::~Batch() {
+  eng_.clear();
+  for (void* p : {static_cast<void*>(target_), static_cast<void*>(loss_), static_cast<void*>(out_),
+                  static_cast<void*>(grads_)})
+    if (p) cudaFree(p);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+void Batch::set_target(const double* q) {
+  const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
+  cuda_check(cudaMemcpy(target_, q, n3 * sizeof(double), cudaMemcpyHostToDevice), "target");
+}
+
+void Batch::evaluate(int frames, double* loss, double* grad_sum, double* device_out) {
+  if (frames < 1) raise(Code::InvalidArgument, "hd_batch_evaluate: frames must be >= 1");
+  const int S = samples(), ne = scene_.mesh.ne;
+  const int n3 = 3 * scene_.mesh.nv;
+  cudaEvent_t start, stop;
+  cuda_check(cudaEventCreate(&start), "event");
+  cuda_check(cudaEventCreate(&stop), "event");
+  std::vector<cudaEvent_t> done(S);
+  for (auto& e : done) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventRecord(start, st_), "event");
+  for (int s = 0; s < S; ++s) cuda_check(cudaStreamWaitEvent(eng_[s]->stream(), start, 0), "wait");
+  parallel_samples(S, threads_, device_, [&](int s) {
+    Engine& e = *eng_[s];
+    e.reset_state();
+    e.record(false);
+    e.record(true);
+    for (int f = 0; f < frames; ++f) e.step();
+    hdk_check_b(hdk_half_sqdist(n3, e.d_positions(), target_, loss_ + s, e.stream()), "loss");
+    e.backward(nullptr, nullptr, nullptr, true, false, target_);
+    e.record(false);
+    cuda_check(cudaEventRecord(done[s], e.stream()), "event");
+  });
+  for (int s = 0; s < S; ++s) cuda_check(cudaStreamWaitEvent(st_, done[s], 0), "wait");
+  hdk_check_b(hdk_batch_sum(S, ne, grads_, loss_, out_, st_), "batch sum");
+  own_launches_ += S + 1;
+  if (device_out)
+    cuda_check(cudaMemcpyAsync(device_out, out_, (1 + static_cast<size_t>(ne)) * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st_),
+               "device out");
+  cuda_check(cudaEventRecord(stop, st_), "event");
+  if (loss) cuda_check(cudaMemcpyAsync(loss, loss_, S * sizeof(double), cudaMemcpyDeviceToHost, st_), "loss out");
+  if (grad_sum)
+    cuda_check(cudaMemcpyAsync(grad_sum, out_ + 1, ne * sizeof(double), cudaMemcpyDeviceToHost, st_), "grad out");
+  cuda_check(cudaStreamSynchronize(st_), "batch sync");
+  float ms = 0;
+  cuda_check(cudaEventElapsedTime(&ms, start, stop), "elapsed");
+  last_ms = ms;
+  cudaEventDestroy(start);
+  cudaEventDestroy(stop);
+  for (auto& e : done) cudaEventDestroy(e);
+}
+
+long long Batch::kernel_launches() const {
+  long long k = own_launches_;
+  for (const auto& e : eng_) k += e->kernel_launches;
+  return k;
+}
+
+}  // namespace hdb

@@ -1,0 +1,49 @@
+// Batched system-ID evaluation: one GPU's
+// share of a batch of material-parameter samples.  Each sample owns a
+// device-resident engine (its own factor: a per-sample E is a per-sample A)
+// on its own CUDA stream; host worker threads drive the samples concurrently
+// so their latency-bound iterations overlap on the device.  One evaluation is
+// the reference's identify objective for every sample (run_identify,
+// drivers.cpp:848-851; roll + chain_backward, drivers.cpp:31-99):
+//   L_s = 1/2 |q_T(E_s) - q_target|^2,  dL_s/dE_s  (per element)
+// and the fixed-order sum over the local samples of [L_s, dL_s/dE] lands in
+// one device vector — the only data that crosses GPUs (NCCL all-reduce).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "engine.hpp"
+
+namespace hdb {
+
+class Batch {
+ public:
+  Batch(const Scene& scene, int samples, const double* young, int threads);
+  ~Batch();
+  Batch(const Batch&) = delete;
+  Batch& operator=(const Batch&) = delete;
+
+  int samples() const { return static_cast<int>(eng_.size()); }
+  void set_target(const double* q_target);
+  // Runs every sample's trajectory + adjoint; loss (samples) and grad_sum
+  // (element_count) are host outputs and may be null; device_out (1 +
+  // element_count doubles on this device) receives [sum L, sum dL/dE].
+  void evaluate(int frames, double* loss, double* grad_sum, double* device_out);
+  long long kernel_launches() const;
+  cudaStream_t stream() const { return st_; }
+  double last_ms = 0;  // device-side duration of the last evaluate (max over sample streams)
+
+ private:
+  const Scene& scene_;
+  std::vector<std::unique_ptr<Engine>> eng_;
+  int threads_ = 1, device_ = 0;
+  cudaStream_t st_ = nullptr;
+  double* target_ = nullptr;   // 3 nv
+  double* loss_ = nullptr;     // samples
+  double* out_ = nullptr;      // 1 + ne
+  const double** grads_ = nullptr;  // samples device pointers
+  long long own_launches_ = 0;
+};
+
+}  // namespace hdb

@@ -11,6 +11,7 @@
 #include <nlohmann/json.hpp>
 
 #include "../../include/heterodyn.h"
+#include "batch.hpp"
 #include "engine.hpp"
 
 using namespace hdb;
@@ -23,6 +24,11 @@ struct hd_sim {
   const hd_scene* scene = nullptr;
   std::unique_ptr<Engine> eng;
   GradOut last_grad;
+};
+
+struct hd_batch {
+  const hd_scene* scene = nullptr;
+  std::unique_ptr<Batch> b;
 };
 
 namespace {
@@ -292,3 +298,40 @@ long long hd_sim_a_spmv_count(const hd_sim* sim) { return sim ? sim->eng->a_spmv
 long long hd_sim_refactor_count(const hd_sim* sim) { return sim ? sim->eng->refactor_count : 0; }
 
 }  // extern "C"
+
+hd_batch* hd_batch_create(const hd_scene* scene, int samples, const double* young, size_t young_count, int threads) {
+  if (!scene) {
+    bad_arg("hd_batch_create: scene is NULL");
+    return nullptr;
+  }
+  auto b = std::make_unique<hd_batch>();
+  b->scene = scene;
+  const hd_status st = guarded([&] {
+    if (young && young_count != static_cast<size_t>(samples) * scene->spec.mesh.ne)
+      raise(Code::InvalidArgument, "hd_batch_create: young must hold samples x element_count values");
+    b->b = std::make_unique<Batch>(scene->spec, samples, young, threads);
+  });
+  return st == HD_OK ? b.release() : nullptr;
+}
+
+void hd_batch_free(hd_batch* batch) { delete batch; }
+int hd_batch_sample_count(const hd_batch* batch) { return batch ? batch->b->samples() : 0; }
+
+hd_status hd_batch_set_target(hd_batch* batch, const double* q, size_t count) {
+  if (!batch || !q) return bad_arg("hd_batch_set_target: NULL argument");
+  if (count != 3 * static_cast<size_t>(batch->scene->spec.mesh.nv)) return bad_arg("hd_batch_set_target: count != dof");
+  return guarded([&] { batch->b->set_target(q); });
+}
+
+hd_status hd_batch_evaluate(hd_batch* batch, int frames, double* loss, size_t loss_cap, double* grad, size_t grad_cap,
+                            void* device_out) {
+  if (!batch) return bad_arg("hd_batch_evaluate: batch is NULL");
+  if (loss && loss_cap < static_cast<size_t>(batch->b->samples()))
+    return bad_arg("hd_batch_evaluate: loss buffer too small");
+  if (grad && grad_cap < static_cast<size_t>(batch->scene->spec.mesh.ne))
+    return bad_arg("hd_batch_evaluate: gradient buffer too small");
+  return guarded([&] { batch->b->evaluate(frames, loss, grad, static_cast<double*>(device_out)); });
+}
+
+double hd_batch_last_ms(const hd_batch* batch) { return batch ? batch->b->last_ms : 0.0; }
+long long hd_batch_kernel_launches(const hd_batch* batch) { return batch ? batch->b->kernel_launches() : 0; }

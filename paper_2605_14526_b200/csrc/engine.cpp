@@ -125,7 +125,8 @@ cudaGraphExec_t capture_exec(cudaStream_t st, const std::function<void()>& fn, i
 }
 }  // namespace
 
-Engine::Engine(const Scene& scene) : scene_(scene), mat_(scene.material) {
+Engine::Engine(const Scene& scene, const Vec* young) : scene_(scene), mat_(scene.material) {
+  if (young) mat_.set_young(*young, scene.mesh.vol);
   const char* nc = std::getenv("HETERODYN_NO_COND_GRAPH");
   use_cond_ = !(nc && std::atoi(nc) != 0);
   int dev_count = 0;
@@ -552,6 +553,8 @@ void Engine::set_state(const double* q, const double* v, double time) {
   nrec_ = 0;
 }
 
+void Engine::reset_state() { set_state(scene_.q0.data(), scene_.v0.data(), 0.0); }
+
 Vec Engine::positions() const {
   Vec out(3 * static_cast<size_t>(scene_.mesh.nv));
   cuda_check(cudaMemcpyAsync(out.data(), q_, out.size() * sizeof(double), cudaMemcpyDeviceToHost, st_), "read state");
@@ -566,7 +569,7 @@ Vec Engine::velocities() const {
 }
 
 GradOut Engine::backward(const double* direct, const double* dq_final, const double* dv_final, bool canonical,
-                         bool download) {
+                         bool download, const double* d_target) {
   const int T = nrec_;
   if (T == 0) raise(Code::InvalidArgument, "hd_sim_backward: no recorded frames");
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
@@ -576,8 +579,10 @@ GradOut Engine::backward(const double* direct, const double* dq_final, const dou
     else cuda_check(cudaMemsetAsync(d, 0, B, st_), "seed zero");
   };
   if (canonical) {  // L = 1/2 |q_T - rest|^2 + 1/2 |v_T|^2, seeds from device state
-    hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, q_, -1.0, rest_, qbar_, st_), "canonical q seed");
-    hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, v_, 0.0, nullptr, vbar_, st_), "canonical v seed");
+    hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, q_, -1.0, d_target ? d_target : rest_, qbar_, st_),
+              "canonical q seed");
+    hdk_check(hdk_axpby(static_cast<int>(n3), d_target ? 0.0 : 1.0, v_, 0.0, nullptr, vbar_, st_),
+              "canonical v seed");
     kernel_launches += 2;
   } else {
     h2d(qbar_, direct ? direct + static_cast<size_t>(T) * n3 : dq_final);

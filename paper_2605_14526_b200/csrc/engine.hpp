@@ -73,7 +73,9 @@ struct GradOut {
 
 class Engine {
  public:
-  explicit Engine(const Scene& scene);
+  // young: optional per-element Young's moduli replacing the scene's (a
+  // parameter sample of a batch); the factor is built once for them.
+  explicit Engine(const Scene& scene, const Vec* young = nullptr);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -82,8 +84,11 @@ class Engine {
   void record(bool on);
   int recorded() const { return nrec_; }
   void set_state(const double* q, const double* v, double time);
+  // canonical: seed from device state, L = 1/2|q_T - ref|^2 (+ 1/2|v_T|^2 when
+  // d_target is null and ref is the rest shape); d_target is a device array.
   GradOut backward(const double* dl_dq_direct, const double* dl_dq_final, const double* dl_dv_final,
-                   bool canonical = false, bool download = true);
+                   bool canonical = false, bool download = true, const double* d_target = nullptr);
+  void reset_state();  // scene's initial state, time 0, recorded frames dropped
   double time_solve(int reps, double* bytes);
   Vec solve_free(const double* rhs, const double* fixed_q);
   void set_young(const Vec& young, bool freeze);
@@ -98,6 +103,8 @@ class Engine {
   const Mesh& mesh() const { return scene_.mesh; }
   const Material& material() const { return mat_; }
   cudaStream_t stream() const { return st_; }
+  const double* d_positions() const { return q_; }
+  const double* d_dl_de() const { return dle_; }
 
  private:
   struct Frame;

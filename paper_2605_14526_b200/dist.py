@@ -20,3 +20,24 @@ def max_over_ranks(ms: float) -> float:
 def replica_value(steps: int, ms: float, world: int) -> float:
     """Whole-job steps/s: every rank ran `steps` steps within the slowest rank's time."""
     return world * steps / (ms / 1e3)
+
+
+# ---- batched system-ID (C5): samples shard across ranks --------------------
+
+def shard(samples: int, rank: int, world: int) -> range:
+    """Contiguous block of sample indices owned by `rank` (sizes differ by at
+    most one; lower ranks take the remainder).  The global sample order is
+    rank-major, so the all-reduced sum is a fixed function of (samples, world)."""
+    base, rem = divmod(samples, world)
+    lo = rank * base + min(rank, rem)
+    return range(lo, lo + base + (1 if rank < rem else 0))
+
+
+def allreduce_loss_grad(buf: torch.Tensor) -> torch.Tensor:
+    """Sum [loss, dL/dtheta] over ranks in place — the only cross-GPU exchange of
+    the batched path.  `buf` lives on this rank's GPU for
+    NCCL (it is the device buffer hd_batch_evaluate filled) or on the CPU for
+    gloo."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+    return buf

@@ -72,6 +72,13 @@ SIGNATURES = {
     "hd_sim_stream": (_VP, [_VP]),
     "hd_sim_kernel_launches": (C.c_longlong, [_VP]),
     "hd_sim_time_solve": (C.c_int, [_VP, C.c_int, _D, _D]),
+    "hd_batch_create": (_VP, [_VP, C.c_int, _D, C.c_size_t, C.c_int]),
+    "hd_batch_free": (None, [_VP]),
+    "hd_batch_sample_count": (C.c_int, [_VP]),
+    "hd_batch_set_target": (C.c_int, [_VP, _D, C.c_size_t]),
+    "hd_batch_evaluate": (C.c_int, [_VP, C.c_int, _D, C.c_size_t, _D, C.c_size_t, _VP]),
+    "hd_batch_last_ms": (C.c_double, [_VP]),
+    "hd_batch_kernel_launches": (C.c_longlong, [_VP]),
 }
 
 
@@ -178,6 +185,19 @@ class Scene:
         p = _VP()
         self.L.check(self.L.lib.hd_run_simulate(self.h, out_dir.encode() if out_dir else None, C.byref(p)))
         return json.loads(self.L._take_string(p))
+
+    def batch(self, samples: int, young=None, threads: int = 8) -> "Batch":
+        """hd_batch_create: `samples` parameter samples of this scene; young is a
+        (samples, element_count) array of per-element Young's moduli or None."""
+        y = None
+        cnt = 0
+        if young is not None:
+            y = np.ascontiguousarray(young, dtype=np.float64).reshape(-1)
+            cnt = y.size
+        h = self.L.lib.hd_batch_create(self.h, samples, _ptr(y), cnt, threads)
+        if not h:
+            raise HdError(self.L.lib.hd_last_error_code(), self.L.lib.hd_last_error().decode())
+        return Batch(self, h, y)
 
     def sim(self) -> "Sim":
         h = self.L.lib.hd_sim_create(self.h)
@@ -325,3 +345,45 @@ class Sim:
     @property
     def refactor_count(self):
         return self.L.lib.hd_sim_refactor_count(self.h)
+
+
+class Batch:
+    """hd_batch_*: one process's share of a batched system-ID evaluation."""
+
+    def __init__(self, scene: Scene, handle, young):
+        self.scene = scene
+        self.L = scene.L
+        self.h = handle
+        self._young = young
+        self.samples = self.L.lib.hd_batch_sample_count(handle)
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.L.lib.hd_batch_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def set_target(self, q):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        self.L.check(self.L.lib.hd_batch_set_target(self.h, _ptr(q), q.size))
+
+    def evaluate(self, frames: int, device_out: int | None = None, want_host: bool = True) -> dict:
+        """Returns {"loss": per-sample losses, "dl_de": sum over samples} (host)
+        and/or writes [sum L, sum dL/dE] to the device pointer device_out."""
+        ne = self.scene.element_count
+        loss = np.zeros(self.samples) if want_host else None
+        grad = np.zeros(ne) if want_host else None
+        self.L.check(self.L.lib.hd_batch_evaluate(
+            self.h, frames, _ptr(loss), self.samples, _ptr(grad), ne,
+            C.c_void_p(device_out) if device_out else None))
+        return {"loss": loss, "dl_de": grad}
+
+    @property
+    def last_ms(self) -> float:
+        return self.L.lib.hd_batch_last_ms(self.h)
+
+    @property
+    def kernel_launches(self) -> int:
+        return self.L.lib.hd_batch_kernel_launches(self.h)

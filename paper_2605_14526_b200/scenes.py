@@ -11,6 +11,8 @@ Configurations (BASELINE.json ``configs``):
   C2  24x16x13 Neo-Hookean, nu=0.45, wiggle initial velocity    (29,952 tets)
   C3  40x24x18 crab-like Neo-Hookean, 100x stiffness contrast,
       Rayleigh damping, gravity + point pull                     (103,680 tets)
+  C5  batched system-ID: samples of C2 with E_s = 1e5 exp(0.5 z_s),
+      z_s ~ N(0, 1) from std::mt19937_64 seed 2605            (c5_young)
 """
 from __future__ import annotations
 
@@ -128,6 +130,58 @@ def config_scene(tag: str, frames: int | None = None, solver: dict | None = None
     if ordering:
         s["factor"] = {"ordering": ordering}
     return s
+
+
+class MT19937_64:
+    """std::mt19937_64 (the 64-bit Mersenne Twister of <random>), so the C5
+    sample parameters are reproducible from any language."""
+
+    def __init__(self, seed: int = 5489):
+        m = (1 << 64) - 1
+        self.mt = [0] * 312
+        self.mt[0] = seed & m
+        for i in range(1, 312):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & m
+        self.i = 312
+
+    def __call__(self) -> int:
+        m = (1 << 64) - 1
+        if self.i >= 312:
+            up, lo = 0xFFFFFFFF80000000, 0x7FFFFFFF
+            for k in range(312):
+                x = (self.mt[k] & up) | (self.mt[(k + 1) % 312] & lo)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= 0xB5026F5AA96619E9
+                self.mt[k] = self.mt[(k + 156) % 312] ^ xa
+            self.i = 0
+        x = self.mt[self.i]
+        self.i += 1
+        x ^= (x >> 29) & 0x5555555555555555
+        x ^= (x << 17) & 0x71D67FFFEDA60000
+        x ^= (x << 37) & 0xFFF7EEE000000000
+        x ^= x >> 43
+        return x & m
+
+
+def c5_normals(samples: int, seed: int = 2605) -> np.ndarray:
+    """z_s ~ N(0, 1): Box-Muller on pairs of 53-bit uniforms (u = (x >> 11) 2^-53)
+    drawn from std::mt19937_64(seed); the cosine branch, one z per pair."""
+    g = MT19937_64(seed)
+    z = np.empty(samples)
+    for s in range(samples):
+        u1 = (g() >> 11) * 2.0 ** -53
+        u2 = (g() >> 11) * 2.0 ** -53
+        z[s] = math.sqrt(-2.0 * math.log1p(-u1)) * math.cos(2.0 * math.pi * u2)
+    return z
+
+
+def c5_young(samples: int, element_count: int, base: float = 1e5, seed: int = 2605) -> np.ndarray:
+    """Per-sample Young's moduli of the batched system-ID configuration C5
+    (SURVEY.md §8(d)): sample s uses E_s = base exp(0.5 z_s) on every element.
+    Returns a (samples, element_count) array."""
+    z = c5_normals(samples, seed)
+    return np.repeat((base * np.exp(0.5 * z))[:, None], element_count, axis=1)
 
 
 def block_scene(dims=(2, 2, 2), spacing=0.1, kind="neo-hookean", young_base=5e4, contrast=1.0, poisson=0.4,

@@ -189,3 +189,35 @@ def test_c3_full_size_step(prod, orc):
     np.testing.assert_array_equal(gp["tau"], go["tau"])
     for k in GRADS:
         assert rel2(gp[k], go[k]) <= 1e-6, (k, rel2(gp[k], go[k]))
+
+
+@pytest.mark.gpu
+def test_batch_matches_oracle_and_is_deterministic(prod, orc):
+    """Batched system-ID (config C5 on a small mesh): per-sample losses and the
+    sample-ordered dL/dE sum match the oracle; the device output equals the host
+    output; results do not depend on the number of driving threads."""
+    import torch
+    scene = scenes.block_scene(dims=(3, 2, 2), frames=3, gravity_z=-9.81, alpha=0.02)
+    sp, so = prod.scene(scene), orc.scene(scene)
+    ne = sp.element_count
+    young = scenes.c5_young(6, ne, base=5e4)
+    target = np.asarray(so.sim().positions()) + 1e-3
+    bo = so.batch(6, young)
+    bo.set_target(target)
+    ro = bo.evaluate(3)
+    results = []
+    for threads in (1, 4):
+        bp = sp.batch(6, young, threads=threads)
+        bp.set_target(target)
+        dev = torch.zeros(1 + ne, dtype=torch.float64, device="cuda")
+        rp = bp.evaluate(3, device_out=dev.data_ptr())
+        assert rel2(rp["loss"], ro["loss"]) <= 1e-6
+        assert rel2(rp["dl_de"], ro["dl_de"]) <= 1e-6, rel2(rp["dl_de"], ro["dl_de"])
+        d = dev.cpu().numpy()
+        np.testing.assert_array_equal(d[1:], rp["dl_de"])
+        assert d[0] == pytest.approx(rp["loss"].sum(), rel=1e-14)
+        assert bp.last_ms > 0 and bp.kernel_launches > 0
+        results.append(rp)
+        rp2 = bp.evaluate(3)
+        np.testing.assert_array_equal(rp2["dl_de"], rp["dl_de"])
+    np.testing.assert_array_equal(results[0]["dl_de"], results[1]["dl_de"])
