@@ -40,6 +40,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
+    ap.add_argument("--workload", default="trajectory", choices=["trajectory", "batch"],
+                    help="trajectory: one C3 trajectory per GPU (replicas for N>1); "
+                         "batch: C5 batched system-ID, 64 C2 samples sharded over the GPUs + NCCL all-reduce")
+    ap.add_argument("--samples", type=int, default=64)
+    ap.add_argument("--frames", type=int, default=10, help="frames per sample trajectory (batch workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -186,11 +191,193 @@ def run_reference(args, scene_dict, world, rank):
     print(json.dumps(line), flush=True)
 
 
+BATCH_METRIC = "forward+backward PD timesteps/sec, batched system-ID (C5: 64 x 30k-tet samples)"
+
+
+def batch_setup(args):
+    from paper_2605_14526_b200 import scenes
+    scene_dict = scenes.config_scene("C2", frames=args.frames)
+    return scene_dict
+
+
+def run_batch_reference(args, world, rank):
+    """Reference arm of the batch workload: the CPU restatement evaluates a
+    bounded sample of the batch (one sample's trajectory) on the host cores."""
+    if rank != 0:
+        return
+    import numpy as np
+    from paper_2605_14526_b200 import scenes
+    from paper_2605_14526_b200.hd import Library
+    lib = Library(ORACLE_LIB)
+    scene_dict = batch_setup(args)
+    sc = lib.scene(scene_dict)
+    young = scenes.c5_young(args.samples, sc.element_count)
+    frames = min(args.frames, 2)
+    times = []
+    t_all = time.perf_counter()
+    for s in range(max(1, min(args.steps, 3))):
+        b = sc.batch(1, young[s:s + 1])
+        t0 = time.perf_counter()
+        b.evaluate(frames)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > 120:
+            break
+    val = frames * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": BATCH_METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": len(times), "warmup": 0, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C5: {args.samples} samples of {scene_dict['name']}, {args.frames} frames each"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{len(times)} samples x {frames} frames fwd+bwd (factorization included per "
+                                   f"sample, as the reference refactors per parameter sample)"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_batch(args, world, rank):
+    """C5: the batch's samples shard over the ranks (contiguous blocks); each
+    rank evaluates its samples concurrently on one GPU and the [sum L, sum
+    dL/dE] vectors are all-reduced over NCCL — the only cross-GPU traffic."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2605_14526_b200 import scenes
+    from paper_2605_14526_b200.dist import allreduce_loss_grad, max_over_ranks, shard
+    from paper_2605_14526_b200.hd import Library
+    torch.cuda.set_device(0)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    lib = Library(PRODUCT_LIB)
+    scene_dict = batch_setup(args)
+    sc = lib.scene(scene_dict)
+    ne, nv = sc.element_count, sc.vertex_count
+    young = scenes.c5_young(args.samples, ne)
+    mine = shard(args.samples, rank, world)
+    # target: the trajectory end state at the nominal modulus (the "measurement")
+    ref = sc.sim()
+    ref.step(args.frames)
+    target = ref.positions()
+    del ref
+    threads = max(1, min(len(mine), os.cpu_count() or 1))
+    t_build = time.perf_counter()
+    b = sc.batch(len(mine), young[mine.start:mine.stop], threads=threads)
+    t_build = time.perf_counter() - t_build
+    b.set_target(target)
+    buf = torch.zeros(1 + ne, dtype=torch.float64, device="cuda")
+    for _ in range(max(args.warmup, 3)):
+        b.evaluate(args.frames, device_out=buf.data_ptr(), want_host=False)
+        allreduce_loss_grad(buf)
+    launches0 = b.kernel_launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    dev_ms = 0.0
+    for _ in range(args.steps):
+        b.evaluate(args.frames, device_out=buf.data_ptr(), want_host=False)
+        dev_ms += b.last_ms
+        allreduce_loss_grad(buf)
+    e1.record()
+    e1.synchronize()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    launches = b.kernel_launches - launches0
+    units = args.samples * args.frames * args.steps  # sample-timesteps, all ranks
+    value = units / (ms / 1e3)
+    total = buf.cpu().numpy()
+
+    # e2e: target upload + evaluation + loss/gradient download through the C ABI
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_h = torch.from_numpy(np.ascontiguousarray(target)).pin_memory()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record()
+    for _ in range(args.steps):
+        b.set_target(t_h.numpy())
+        r = b.evaluate(args.frames, device_out=buf.data_ptr(), want_host=True)
+        allreduce_loss_grad(buf)
+        host_total = buf.cpu()
+    e3.record()
+    e3.synchronize()
+    ms_e2e = max_over_ranks(e2.elapsed_time(e3))
+    e2e = units / (ms_e2e / 1e3)
+
+    # roofline: the global solve of one C2 sample, timed alone
+    probe = sc.sim()
+    ms_solve, bytes_solve = probe.time_solve(50)
+    peak, peak_kind = measured_peak()
+    achieved = bytes_solve / (ms_solve / 1e3) / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from paper_2605_14526_b200.hd import Library as L2
+            o = L2(ORACLE_LIB).scene(scene_dict)
+            ob = o.batch(1, young[:1])
+            t0 = time.perf_counter()
+            ob.evaluate(2)
+            dt = time.perf_counter() - t0
+            cpu = {"value": 2 / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"1 sample x 2 frames fwd+bwd of the same batch ({dt:.1f} s, factorization included)"}
+        except Exception as exc:
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+    if rank == 0:
+        line = {
+            "metric": BATCH_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C5: {args.samples} samples of {scene_dict['name']} ({ne} tets, {nv} vertices, "
+                                   f"NH nu=0.45, beta0=0), E_s = 1e5 exp(0.5 z_s), mt19937_64 seed 2605, "
+                                   f"{args.frames} frames fwd+bwd per sample per step",
+                       "parallelism": f"samples sharded dp{world}, NCCL all-reduce of [loss, dL/dE] "
+                                      f"({(1 + ne) * 8} B) per step",
+                       "samples_per_rank": len(mine), "host_threads_per_rank": threads,
+                       "engine_build_s": t_build, "l2_policy": "per-sample factors 64 x ~%.0f MB exceed L2" %
+                                                               (probe.factor_nnz * 8 / 1e6),
+                       "device_busy_ms_per_step": dev_ms / args.steps,
+                       "loss_sum": float(total[0])},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 3 * nv * 8,
+                    "d2h_bytes_per_step": (len(mine) + ne) * 8 + (1 + ne) * 8},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "kernel": "hdk_apply_inverse3 on one C2 sample factor (timed alone)",
+                         "bytes_per_launch": bytes_solve, "ms_per_launch": ms_solve, "peak_source": peak_kind},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
     pin_device(local, world)
     from paper_2605_14526_b200 import scenes
+    if args.workload == "batch":
+        if args.impl == "reference":
+            if world > 1:
+                import torch.distributed as dist
+                dist.init_process_group("gloo", init_method="env://")
+            run_batch_reference(args, world, rank)
+            if world > 1:
+                dist.barrier()
+                dist.destroy_process_group()
+            return
+        if not os.path.exists(PRODUCT_LIB):
+            raise SystemExit(f"product library missing: {PRODUCT_LIB} (run __graft_entry__.build())")
+        run_batch(args, world, rank)
+        return
     scene_dict = scenes.config_scene(args.config)
     if args.impl == "reference":
         if world > 1:

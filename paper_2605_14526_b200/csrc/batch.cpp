@@ -23,9 +23,16 @@ void parallel_samples(int count, int threads, int device, F&& body) {
   std::exception_ptr err;
   std::mutex m;
   const auto run = [&](int t) {
+    int cur = -1;
     try {
       cuda_check(cudaSetDevice(device), "set device");
-      for (int i = t; i < count; i += threads) body(i);
+      for (int i = t; i < count; i += threads) {
+        cur = i;
+        body(i);
+      }
+    } catch (const Error& e) {
+      std::lock_guard<std::mutex> g(m);
+      if (!err) err = std::make_exception_ptr(Error(e.code, "sample " + std::to_string(cur) + ": " + e.what()));
     } catch (...) {
       std::lock_guard<std::mutex> g(m);
       if (!err) err = std::current_exception();
@@ -85,6 +92,8 @@ void Batch::evaluate(int frames, double* loss, double* grad_sum, double* device_
   if (frames < 1) raise(Code::InvalidArgument, "hd_batch_evaluate: frames must be >= 1");
   const int S = samples(), ne = scene_.mesh.ne;
   const int n3 = 3 * scene_.mesh.nv;
+  // frame slots are allocated up front, never while other samples' graphs run
+  parallel_samples(S, threads_, device_, [&](int s) { eng_[s]->reserve_frames(frames); });
   cudaEvent_t start, stop;
   cuda_check(cudaEventCreate(&start), "event");
   cuda_check(cudaEventCreate(&stop), "event");

@@ -501,18 +501,7 @@ void Engine::step() {
     run_graph(*fgraph_, "forward graph");
   }
   if (recording_) {
-    if (static_cast<int>(slots_.size()) <= nrec_) {
-      auto a = std::make_unique<DevArena>();
-      Frame f;
-      f.q_t = a->alloc<double>(n3);
-      f.v_t = a->alloc<double>(n3);
-      f.qtil = a->alloc<double>(n3);
-      f.qprev = a->alloc<double>(n3);
-      f.qstar = a->alloc<double>(n3);
-      f.cache = a->alloc<double>(24 * ne);
-      frame_mem_.push_back(std::move(a));
-      slots_.push_back(f);
-    }
+    if (static_cast<int>(slots_.size()) <= nrec_) add_slot();
     const Frame& fr = slots_[nrec_];
     const auto cp = [&](double* d, const double* src, size_t n) {
       cuda_check(cudaMemcpyAsync(d, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st_), "record");
@@ -537,6 +526,24 @@ void Engine::step() {
   if (recording_) slots_[nrec_].contacts = contacts;
   time_ += scene_.solver.h;
   if (recording_) ++nrec_;
+}
+
+void Engine::add_slot() {
+  const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
+  auto a = std::make_unique<DevArena>();
+  Frame f;
+  f.q_t = a->alloc<double>(n3);
+  f.v_t = a->alloc<double>(n3);
+  f.qtil = a->alloc<double>(n3);
+  f.qprev = a->alloc<double>(n3);
+  f.qstar = a->alloc<double>(n3);
+  f.cache = a->alloc<double>(24 * ne);
+  frame_mem_.push_back(std::move(a));
+  slots_.push_back(f);
+}
+
+void Engine::reserve_frames(int frames) {
+  while (static_cast<int>(slots_.size()) < frames) add_slot();
 }
 
 void Engine::record(bool on) {

@@ -82,6 +82,7 @@ class Engine {
 
   void step();  // throws Error; state untouched on failure
   void record(bool on);
+  void reserve_frames(int frames);  // allocate recorded-frame slots ahead of time
   int recorded() const { return nrec_; }
   void set_state(const double* q, const double* v, double time);
   // canonical: seed from device state, L = 1/2|q_T - ref|^2 (+ 1/2|v_T|^2 when
@@ -108,6 +109,7 @@ class Engine {
 
  private:
   struct Frame;
+  void add_slot();
   void build_static();
   void build_factor_device();
   void build_forward_graph();
