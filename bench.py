@@ -25,6 +25,9 @@ import threading
 import time
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+# the batch workload drives up to 32 sample streams concurrently; give each its
+# own hardware work queue (must be set before the CUDA runtime starts)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 sys.path.insert(0, HERE)
 
 PRODUCT_LIB = os.path.join(HERE, "paper_2605_14526_b200", "_lib", "libheterodyn_b200.so")
@@ -260,7 +263,7 @@ def run_batch(args, world, rank):
     ref.step(args.frames)
     target = ref.positions()
     del ref
-    threads = max(1, min(len(mine), os.cpu_count() or 1))
+    threads = max(1, min(len(mine), 32))
     t_build = time.perf_counter()
     b = sc.batch(len(mine), young[mine.start:mine.stop], threads=threads)
     t_build = time.perf_counter() - t_build

@@ -72,6 +72,8 @@ typedef struct hdk_factor {
   int n;                  /* free vertices */
   int tile_w, n_tiles, n_chunks;
   int max_ctas;           /* part2 holds (n_tiles + max_ctas) tile partials */
+  int grid_cap;           /* 0: one resident wave per pass; else at most this many CTAs per pass
+                             (lets concurrent samples of a batch share the SMs) */
   const double* sval;     /* tile-major value stream */
   const hdk_seg* seg;
   const hdk_chunk* chunk;

@@ -19,7 +19,7 @@ namespace hdb {
 
 class Batch {
  public:
-  Batch(const Scene& scene, int samples, const double* young, int threads);
+  Batch(const Scene& scene, int samples, const double* young, int threads, int solve_ctas = 0);
   ~Batch();
   Batch(const Batch&) = delete;
   Batch& operator=(const Batch&) = delete;

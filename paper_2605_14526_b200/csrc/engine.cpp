@@ -125,7 +125,9 @@ cudaGraphExec_t capture_exec(cudaStream_t st, const std::function<void()>& fn, i
 }
 }  // namespace
 
-Engine::Engine(const Scene& scene, const Vec* young) : scene_(scene), mat_(scene.material) {
+Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas)
+    : scene_(scene), mat_(scene.material), solve_ctas_(solve_ctas) {
+  if (const char* c = std::getenv("HETERODYN_SOLVE_CTAS")) solve_ctas_ = std::atoi(c);
   if (young) mat_.set_young(*young, scene.mesh.vol);
   const char* nc = std::getenv("HETERODYN_NO_COND_GRAPH");
   use_cond_ = !(nc && std::atoi(nc) != 0);
@@ -285,6 +287,7 @@ void Engine::build_factor_device() {
   df_.n_tiles = static_cast<int>(F.tile_chunk.size()) - 1;
   df_.n_chunks = static_cast<int>(F.chunks.size());
   df_.max_ctas = 148 * 8;
+  df_.grid_cap = solve_ctas_;
   df_.sval = A.upload(F.stream);
   static_assert(sizeof(hdk_seg) == sizeof(SegDesc), "segment descriptor layout");
   static_assert(sizeof(hdk_chunk) == sizeof(ChunkDesc), "chunk descriptor layout");

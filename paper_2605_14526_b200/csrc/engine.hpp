@@ -75,7 +75,8 @@ class Engine {
  public:
   // young: optional per-element Young's moduli replacing the scene's (a
   // parameter sample of a batch); the factor is built once for them.
-  explicit Engine(const Scene& scene, const Vec* young = nullptr);
+  // solve_ctas: cap on the CTAs of each solve pass (0 = one resident wave).
+  explicit Engine(const Scene& scene, const Vec* young = nullptr, int solve_ctas = 0);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -129,6 +130,7 @@ class Engine {
   std::unique_ptr<DevArena> mem_;      // mesh/material/state/work
   std::unique_ptr<DevArena> fmem_;     // factor (rebuilt on refresh)
   bool use_cond_ = true;
+  int solve_ctas_ = 0;
   double time_ = 0;
 
   // device views

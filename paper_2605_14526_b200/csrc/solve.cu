@@ -381,14 +381,14 @@ __global__ void k_xreduce(hdk_factor f, int G, double* __restrict__ out) {
   o[2] = a2;
 }
 
-int g_grid1 = 0, g_grid2 = 0;
+struct Grids {
+  int g1, g2;
+};
 
-int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatter, cudaStream_t st) {
-  if (f->n <= 0) return 0;
-  if (f->tile_w != kW) return static_cast<int>(cudaErrorInvalidValue);
-  static bool configured = false;
-  const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem);
-  if (!configured) {
+// One resident wave per pass, computed once per process (thread-safe static).
+const Grids& grids() {
+  static const Grids g = [] {
+    const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem);
     cudaFuncSetAttribute(k_rowdot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
     cudaFuncSetAttribute(k_coltile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s2));
     int dev = 0, sms = 148, b1 = 1, b2 = 1;
@@ -396,12 +396,20 @@ int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatte
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_rowdot<false>, kThreads, s1);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_coltile<false>, kThreads, s2);
-    g_grid1 = sms * (b1 > 0 ? b1 : 1);  // persistent: one resident wave
-    g_grid2 = sms * (b2 > 0 ? b2 : 1);
-    configured = true;
-  }
-  const int g1 = g_grid1 < f->n_chunks ? g_grid1 : f->n_chunks;
+    return Grids{sms * (b1 > 0 ? b1 : 1), sms * (b2 > 0 ? b2 : 1)};
+  }();
+  return g;
+}
+
+int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatter, cudaStream_t st) {
+  if (f->n <= 0) return 0;
+  if (f->tile_w != kW) return static_cast<int>(cudaErrorInvalidValue);
+  const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem);
+  const int g_grid1 = grids().g1, g_grid2 = grids().g2;
+  int g1 = g_grid1 < f->n_chunks ? g_grid1 : f->n_chunks;
   int g2 = g_grid2 < f->n_chunks ? g_grid2 : f->n_chunks;
+  if (f->grid_cap > 0 && g1 > f->grid_cap) g1 = f->grid_cap;
+  if (f->grid_cap > 0 && g2 > f->grid_cap) g2 = f->grid_cap;
   if (g2 > f->max_ctas) g2 = f->max_ctas;
   hdk::launch(k_rowdot<false>, dim3(g1), dim3(kThreads), s1, st, *f, rhs_perm);
   hdk::launch(k_zreduce, dim3((f->n * 8 + 255) / 256), dim3(256), 0, st, *f);

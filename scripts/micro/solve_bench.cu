@@ -23,7 +23,7 @@ int main(int argc, char** argv) {
   hdb::HostFactor F = hdb::build_factor(s.mesh, s.material, s.solver.h, s.fixed, s.ordering);
   printf("n %d nnz %lld chunks %zu stream %zu\n", F.n, F.row_off.back(), F.chunks.size(), F.stream.size());
   hdk_factor f{};
-  f.n = F.n; f.tile_w = F.tile_w; f.n_tiles = (int)F.tile_chunk.size() - 1; f.n_chunks = (int)F.chunks.size(); f.max_ctas = 148 * 8;
+  f.n = F.n; f.tile_w = F.tile_w; f.n_tiles = (int)F.tile_chunk.size() - 1; f.n_chunks = (int)F.chunks.size(); f.max_ctas = 148 * 8; f.grid_cap = 0;
   auto up = [](const void* h, size_t bytes) { void* d; cudaMalloc(&d, bytes); cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice); return d; };
   f.sval = (const double*)up(F.stream.data(), F.stream.size() * 8);
   f.seg = (const hdk_seg*)up(F.sdesc.data(), F.sdesc.size() * 16);
