@@ -11,6 +11,9 @@ Configurations (BASELINE.json ``configs``):
   C2  24x16x13 Neo-Hookean, nu=0.45, wiggle initial velocity    (29,952 tets)
   C3  40x24x18 crab-like Neo-Hookean, 100x stiffness contrast,
       Rayleigh damping, gravity + point pull                     (103,680 tets)
+  C4  soft gripper pad: C3-sized Neo-Hookean block (stiff core, soft pad,
+      100x contrast) pressed onto a rigid rounded cube edge (sphere
+      obstacle, friction 0.5)                                    (103,680 tets)
   C5  batched system-ID: samples of C2 with E_s = 1e5 exp(0.5 z_s),
       z_s ~ N(0, 1) from std::mt19937_64 seed 2605            (c5_young)
 """
@@ -73,8 +76,10 @@ def _solver(**kw):
     return base
 
 
-def config_scene(tag: str, frames: int | None = None, solver: dict | None = None, ordering: str | None = None) -> dict:
-    """Scene dict for configuration C1..C3 (SURVEY.md §8(d) synthetic inputs)."""
+def config_scene(tag: str, frames: int | None = None, solver: dict | None = None, ordering: str | None = None,
+                 dims: tuple | None = None) -> dict:
+    """Scene dict for configuration C1..C4 (SURVEY.md §8(d) synthetic inputs).
+    `dims` shrinks C4's grid for parity tests (same construction)."""
     tag = tag.upper()
     if tag == "C1":
         dims, h = (36, 6, 4), 0.05
@@ -118,6 +123,29 @@ def config_scene(tag: str, frames: int | None = None, solver: dict | None = None
             "gravity": [0.0, 0.0, -9.81],
             "f_ext": [{"vertex": int(pull_vertex), "force": [0.01, 0.0, 0.005]}],
             "initial": {"velocity": wiggle(3 * nv, 0.05).tolist()},
+            "solver": _solver(),
+            "frames": 100,
+        }
+    elif tag == "C4":
+        dims = tuple(dims) if dims else (40, 24, 18)
+        h = 0.01
+        nx, ny, nz = dims
+        c = element_centroids(dims, h)
+        ext = np.array(dims, dtype=float) * h
+        # stiff core (the gripper's skeleton) above a soft contact pad
+        core = (np.abs(c[:, 0] - 0.5 * ext[0]) <= 0.3 * ext[0]) & (np.abs(c[:, 1] - 0.5 * ext[1]) <= 0.3 * ext[1]) \
+            & (c[:, 2] >= 0.4 * ext[2])
+        young = np.where(core, 5e6, 5e4)
+        radius = 0.05
+        # rigid cube edge, rounded: its top touches the pad's bottom-face centre vertex
+        centre = [0.5 * ext[0], 0.5 * ext[1], -radius - 2e-4]
+        s = {
+            "name": "C4-gripper-pad",
+            "mesh": {"grid": {"dims": list(dims), "spacing": h, "density": 1000.0}},
+            "material": {"energy": "neo-hookean", "young": young.tolist(), "poisson": 0.4, "alpha": 0.05, "beta0": 0.01},
+            "gravity": [0.0, 0.0, -9.81],
+            "obstacles": [{"type": "sphere", "center": centre, "radius": radius, "friction": 0.5}],
+            "initial": {"velocity": [0.0, 0.0, -0.05]},
             "solver": _solver(),
             "frames": 100,
         }

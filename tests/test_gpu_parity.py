@@ -96,6 +96,8 @@ def test_trajectory_and_gradients(prod, orc, name):
 
 
 CONTACT_CASES = {
+    "C4-reduced": (scenes.config_scene("C4", dims=(10, 6, 6), frames=4,
+                                       solver={"eps_rel": 1e-12, "eps_abs": 1e-14}), 4),
     "block-floor-friction": (scenes.block_scene(floor=True, friction=0.5, v0_amp=0.0, gravity_z=-2.0), 4),
     "resting-box": ({"mesh": {"generator": "resting-box"}, "frames": 4,
                      "solver": {"eps_rel": 1e-12, "eps_abs": 1e-14}}, 4),
