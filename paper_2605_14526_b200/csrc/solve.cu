@@ -37,7 +37,8 @@ constexpr int kThreads = 32 * (kWarps + 1);  // + one producer warp
 constexpr int kVals = HDK_CHUNK_VALS;
 constexpr int kSegs = HDK_CHUNK_SEGS;
 constexpr int kStages1 = 3;   // pass 1 ring depth (2 CTAs / SM)
-constexpr int kStages2 = 3;   // pass 2 ring depth (2 CTAs / SM)
+constexpr int kStages2 = 5;   // pass 2 ring depth (1 CTA / SM)
+constexpr int kThreads2 = 32 * (kWarps + 2);  // pass 2: + copy warp + z-gather warp
 
 static_assert(kW == 256, "tile width is fixed by the factor layout");
 
@@ -71,6 +72,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
+}
+// 8-byte asynchronous global->shared copy (LDGSTS); completion is tracked by
+// cp_async_arrive on an mbarrier.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+// The mbarrier receives one arrival once all of this thread's prior cp.async
+// copies have landed (pending count not incremented: count them at init).
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarps) : "memory"); }
@@ -119,6 +130,74 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
     const int st = k % S;
     const hdk_chunk ch = nxt;
     if (k + 1 < n) nxt = f.chunk[chunk_at(k + 1)];  // descriptor prefetch, off the critical path
+    if (k >= S) mbar_wait(&r.empty[st], ((k / S) - 1) & 1);
+    fence_proxy_async();
+    r.info[st] = ChunkInfo{ch.nseg, ch.tile, ch.seg0, 0};
+    const uint32_t vb = static_cast<uint32_t>(ch.len) * 8u, sb = static_cast<uint32_t>(ch.nseg) * 16u;
+    mbar_expect_tx(&r.full[st], vb + sb);
+    if (vb) bulk_g2s(r.vals[st], f.sval + ch.off, vb, &r.full[st]);
+    bulk_g2s(r.segs[st], f.seg + ch.seg0, sb, &r.full[st]);
+  }
+}
+
+// Pass 2 ring: as Ring, plus the z rows of each staged chunk's segments,
+// gathered into shared memory by the producer warp (zfull) so the consumers
+// never wait on a global load.
+template <int S>
+struct Ring2 {
+  double vals[S][kVals];
+  hdk_seg segs[S][kSegs];
+  double zs[S][kSegs][3];
+  ChunkInfo info[S];
+  uint64_t full[S];
+  uint64_t zfull[S];
+  uint64_t empty[S];
+};
+
+template <int S>
+__device__ __forceinline__ void ring2_init(Ring2<S>& r) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&r.full[s], 1);
+      mbar_init(&r.zfull[s], 32);  // one cp.async arrival per producer lane
+      mbar_init(&r.empty[s], kWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+}
+
+// Pass 2 producer warps.  Warp kWarps (lane 0) streams chunks in reverse
+// order exactly as produce(); warp kWarps + 1 waits for each chunk to land and
+// gathers the z rows of its segments into zs with asynchronous 8-byte copies
+// that complete on zfull, so neither the stream nor the consumers wait on a
+// dependent global load.
+template <int S>
+__device__ __forceinline__ void gather_z(const hdk_factor& f, Ring2<S>& r, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < n; ++j) {
+    const int st = j % S;
+    mbar_wait(&r.full[st], (j / S) & 1);
+    const int nseg = r.info[st].nseg;
+    for (int i = lane; i < nseg; i += 32) {
+      const double* z = f.z + 3 * (size_t)r.segs[st][i].row;
+      cp_async8(&r.zs[st][i][0], z);
+      cp_async8(&r.zs[st][i][1], z + 1);
+      cp_async8(&r.zs[st][i][2], z + 2);
+    }
+    cp_async_arrive(&r.zfull[st]);
+  }
+}
+
+template <int S>
+__device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S>& r, int c_beg, int c_end) {
+  if ((threadIdx.x & 31) != 0) return;
+  const int n = c_end - c_beg;
+  hdk_chunk nxt = n > 0 ? f.chunk[c_end - 1] : hdk_chunk{};
+  for (int k = 0; k < n; ++k) {
+    const int st = k % S;
+    const hdk_chunk ch = nxt;
+    if (k + 1 < n) nxt = f.chunk[c_end - 2 - k];
     if (k >= S) mbar_wait(&r.empty[st], ((k / S) - 1) & 1);
     fence_proxy_async();
     r.info[st] = ChunkInfo{ch.nseg, ch.tile, ch.seg0, 0};
@@ -187,25 +266,24 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
         c1 += wb * b1[m];
         c2 += wb * b2[m];
       }
+      // reduce-scatter: lanes 0-15 keep segment a, lanes 16-31 segment b
+      // after the first exchange, so the pair costs 15 shuffles, not 30
+      const bool lo = lane < 16;
+      double k0 = lo ? a0 : c0, k1 = lo ? a1 : c1, k2 = lo ? a2 : c2;
+      k0 += __shfl_xor_sync(0xffffffffu, lo ? c0 : a0, 16);
+      k1 += __shfl_xor_sync(0xffffffffu, lo ? c1 : a1, 16);
+      k2 += __shfl_xor_sync(0xffffffffu, lo ? c2 : a2, 16);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-        a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+      for (int o = 8; o > 0; o >>= 1) {
+        k0 += __shfl_xor_sync(0xffffffffu, k0, o);
+        k1 += __shfl_xor_sync(0xffffffffu, k1, o);
+        k2 += __shfl_xor_sync(0xffffffffu, k2, o);
       }
-      if (lane == 0) {
-        double* p = f.part1 + 3 * (size_t)sa.pslot;
-        p[0] = a0;
-        p[1] = a1;
-        p[2] = a2;
-      } else if (lane == 1 && hasb) {
-        double* p = f.part1 + 3 * (size_t)sb.pslot;
-        p[0] = c0;
-        p[1] = c1;
-        p[2] = c2;
+      if (lane == 0 || (lane == 16 && hasb)) {
+        double* p = f.part1 + 3 * (size_t)(lane == 0 ? sa.pslot : sb.pslot);
+        p[0] = k0;
+        p[1] = k1;
+        p[2] = k2;
       }
     }
     __syncwarp();
@@ -248,7 +326,7 @@ __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
 
 // ---- pass 2 ------------------------------------------------------------------
 struct Pass2Smem {
-  Ring<kStages2> ring;
+  Ring2<kStages2> ring;
   double fold[kWarps / 2][3][kW];
 };
 
@@ -294,20 +372,24 @@ __device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& s
 }
 
 template <bool kDry = false>
-__global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
+__global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Pass2Smem& sm = *reinterpret_cast<Pass2Smem*>(smem_raw);
-  Ring<kStages2>& ring = sm.ring;
+  Ring2<kStages2>& ring = sm.ring;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  ring_init(ring);
+  ring2_init(ring);
   const int c_beg = range_first(blockIdx.x, gridDim.x, f.n_chunks);
   const int c_end = range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
   // Pass 2 walks its range backwards: the tail pass 1 just streamed is still
   // in L2, and pass 2 ends where the next pass 1 begins.
   if (warp == kWarps) {
-    produce(f, ring, c_beg, c_end, true);
+    stream2(f, ring, c_beg, c_end);
+    return;
+  }
+  if (warp == kWarps + 1) {
+    gather_z(f, ring, c_end - c_beg);
     return;
   }
   double x0[kM], x1[kM], x2[kM];
@@ -316,7 +398,7 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
   int tile = -1;
   for (int k = 0; k < c_end - c_beg; ++k) {
     const int st = k % kStages2;
-    mbar_wait(&ring.full[st], (k / kStages2) & 1);
+    mbar_wait(&ring.zfull[st], (k / kStages2) & 1);
     const ChunkInfo ch = ring.info[st];
     if (ch.tile != tile) {  // partial of the previous tile: slot tile + b is unique
       if (tile >= 0) fold_and_write(f, sm, tile + blockIdx.x, x0, x1, x2);
@@ -324,23 +406,11 @@ __global__ void __launch_bounds__(kThreads) k_coltile(hdk_factor f) {
     }
     const double* vals = ring.vals[st];
     const int i0 = (warp - ch.seg0) & (kWarps - 1);
-    // z of this warp's segments: lane l holds the l-th one (<= 32 per chunk)
-    double zr0 = 0.0, zr1 = 0.0, zr2 = 0.0;
-    {
-      const int i = i0 + kWarps * lane;
-      if (i < ch.nseg) {
-        const double* z = f.z + 3 * (size_t)ring.segs[st][i].row;
-        zr0 = __ldg(z);
-        zr1 = __ldg(z + 1);
-        zr2 = __ldg(z + 2);
-      }
-    }
-    for (int i = i0, j = 0; i < (kDry ? 0 : ch.nseg); i += kWarps, ++j) {
+    for (int i = i0; i < (kDry ? 0 : ch.nseg); i += kWarps) {
       const hdk_seg sg = ring.segs[st][i];
       const int lo = sg.clo_len & 0xffff, hi = lo + (sg.clo_len >> 16);
       const double* v = vals + sg.coff - lo;
-      const double z0 = __shfl_sync(0xffffffffu, zr0, j), z1 = __shfl_sync(0xffffffffu, zr1, j),
-                   z2 = __shfl_sync(0xffffffffu, zr2, j);
+      const double z0 = ring.zs[st][i][0], z1 = ring.zs[st][i][1], z2 = ring.zs[st][i][2];
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
@@ -395,7 +465,7 @@ const Grids& grids() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_rowdot<false>, kThreads, s1);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_coltile<false>, kThreads, s2);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_coltile<false>, kThreads2, s2);
     return Grids{sms * (b1 > 0 ? b1 : 1), sms * (b2 > 0 ? b2 : 1)};
   }();
   return g;
@@ -413,7 +483,7 @@ int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatte
   if (g2 > f->max_ctas) g2 = f->max_ctas;
   hdk::launch(k_rowdot<false>, dim3(g1), dim3(kThreads), s1, st, *f, rhs_perm);
   hdk::launch(k_zreduce, dim3((f->n * 8 + 255) / 256), dim3(256), 0, st, *f);
-  hdk::launch(k_coltile<false>, dim3(g2), dim3(kThreads), s2, st, *f);
+  hdk::launch(k_coltile<false>, dim3(g2), dim3(kThreads2), s2, st, *f);
   if (scatter)
     hdk::launch(k_xreduce<true>, dim3((f->n + 255) / 256), dim3(256), 0, st, *f, g2, out);
   else

@@ -44,7 +44,7 @@ int main(int argc, char** argv) {
   cudaFuncSetAttribute(k_coltile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
   cudaFuncSetAttribute(k_coltile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
   int o1, o2; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_rowdot<false>, kThreads, s1);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_coltile<false>, kThreads, s2);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_coltile<false>, kThreads2, s2);
   printf("smem1 %zu occ %d | smem2 %zu occ %d\n", s1, o1, s2, o2);
   const double gb = F.stream.size() * 8.0 / 1e9;
   for (int rep = 0; rep < 2; ++rep) {
@@ -53,9 +53,9 @@ int main(int argc, char** argv) {
     printf("rowdot wet  %7.2f us  %7.1f GB/s\n", t, gb / (t * 1e-6));
     t = time_kernel([](int g, size_t sm, const hdk_factor& f, const double* r) { k_rowdot<true><<<g, kThreads, sm>>>(f, r); }, 148 * o1, s1, f, drhs, 50);
     printf("rowdot dry  %7.2f us  %7.1f GB/s\n", t, gb / (t * 1e-6));
-    t = time_kernel([](int g, size_t sm, const hdk_factor& f, const double* r) { k_coltile<false><<<g, kThreads, sm>>>(f); }, 148 * o2, s2, f, drhs, 50);
+    t = time_kernel([](int g, size_t sm, const hdk_factor& f, const double* r) { k_coltile<false><<<g, kThreads2, sm>>>(f); }, 148 * o2, s2, f, drhs, 50);
     printf("coltile wet %7.2f us  %7.1f GB/s\n", t, gb / (t * 1e-6));
-    t = time_kernel([](int g, size_t sm, const hdk_factor& f, const double* r) { k_coltile<true><<<g, kThreads, sm>>>(f); }, 148 * o2, s2, f, drhs, 50);
+    t = time_kernel([](int g, size_t sm, const hdk_factor& f, const double* r) { k_coltile<true><<<g, kThreads2, sm>>>(f); }, 148 * o2, s2, f, drhs, 50);
     printf("coltile dry %7.2f us  %7.1f GB/s\n", t, gb / (t * 1e-6));
     t = time_kernel([](int g, size_t sm, const hdk_factor& f, const double* r) { k_zreduce<<<(f.n * 8 + 255) / 256, 256>>>(f); }, 0, 0, f, drhs, 50);
     printf("zreduce     %7.2f us\n", t);
