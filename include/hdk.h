@@ -84,6 +84,13 @@ typedef struct hdk_factor {
   double* part1;          /* 3*row_pslot[n] scratch */
   double* part2;          /* 3*tile_w*(n_tiles+max_ctas) scratch */
   double* z;              /* 3*n scratch */
+  /* Cost-balanced CTA ranges (chunk cost = values + alpha * segments), built
+   * on the host for the grids hdk_solve_grids reports; NULL = equal chunk
+   * counts per CTA. */
+  int grid1, grid2;
+  const int* first1;      /* grid1+1: first chunk of pass-1 CTA b */
+  const int* first2;      /* grid2+1: first chunk of pass-2 CTA b */
+  const int* tile_cta2;   /* 2*n_tiles: first and last pass-2 CTA touching tile t */
 } hdk_factor;
 
 /* Scalar CSR in elimination order (a_free / a_free_fixed, factor.hpp:98-99). */
@@ -98,6 +105,9 @@ typedef struct hdk_csr {
  * is scattered into out_full[3*v+a] for free vertices (fixed entries are not
  * touched).  Replaces GlobalSystem::solve_free (factor.cpp:196-208). */
 HDK_API int hdk_apply_inverse3(const hdk_factor* f, const double* rhs_perm, double* out_full, void* stream);
+/* Grid sizes (CTAs) of the two streaming passes hdk_apply_inverse3 launches
+ * for this factor (persistent: one resident wave, capped by grid_cap). */
+HDK_API int hdk_solve_grids(const hdk_factor* f, int* grid1, int* grid2);
 /* Same, result kept in elimination order (out_perm [n][3]). */
 HDK_API int hdk_apply_inverse3_perm(const hdk_factor* f, const double* rhs_perm, double* out_perm, void* stream);
 

@@ -304,6 +304,24 @@ void Engine::build_factor_device() {
   df_.part1 = A.alloc<double>(3 * static_cast<size_t>(F.row_pslot.back()));
   df_.part2 = A.alloc<double>(3 * static_cast<size_t>(F.tile_w) * (df_.n_tiles + df_.max_ctas));
   df_.z = A.alloc<double>(3 * static_cast<size_t>(F.n));
+  // cost-balanced CTA ranges for the grids the solve will launch: a segment
+  // costs about as much as 300 (pass 1) / 200 (pass 2) streamed values
+  // (per-CTA traces of the C3 factor, scripts/micro/solve_bench.cu)
+  {
+    int g1 = 0, g2 = 0;
+    hdk_check(hdk_solve_grids(&df_, &g1, &g2), "solve grids");
+    const auto env_cost = [](const char* name, double dflt) {
+      const char* v = std::getenv(name);
+      return v ? std::atof(v) : dflt;
+    };
+    const std::vector<int> f1 = balanced_ranges(F.chunks, g1, env_cost("HETERODYN_SEG_COST1", 300.0));
+    const std::vector<int> f2 = balanced_ranges(F.chunks, g2, env_cost("HETERODYN_SEG_COST2", 200.0));
+    df_.grid1 = g1;
+    df_.grid2 = g2;
+    df_.first1 = A.upload(f1);
+    df_.first2 = A.upload(f2);
+    df_.tile_cta2 = A.upload(tile_cta_ranges(F.tile_chunk, f2));
+  }
   rhs_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
   fixc_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
   dqp_ = A.alloc<double>(3 * static_cast<size_t>(F.n));

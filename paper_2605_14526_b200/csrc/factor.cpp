@@ -505,4 +505,38 @@ double factor_inverse_residual(const HostFactor& F) {
   return worst;
 }
 
+std::vector<int> balanced_ranges(const std::vector<ChunkDesc>& chunks, int G, double seg_cost) {
+  const int C = static_cast<int>(chunks.size());
+  std::vector<double> pre(C + 1, 0.0);
+  for (int c = 0; c < C; ++c) pre[c + 1] = pre[c] + chunks[c].len + seg_cost * chunks[c].nseg;
+  std::vector<int> first(G + 1, C);
+  first[0] = 0;
+  for (int b = 1; b < G; ++b) {
+    const double target = pre[C] * b / G;
+    int c = static_cast<int>(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+    // the chunk straddling the target goes to whichever side it mostly covers
+    if (c > 0 && c <= C && target - pre[c - 1] < pre[c] - target) --c;
+    if (C >= G) {  // keep every range non-empty
+      c = std::max(c, first[b - 1] + 1);
+      c = std::min(c, C - (G - b));
+    }
+    first[b] = std::max(c, first[b - 1]);
+  }
+  first[G] = C;
+  return first;
+}
+
+std::vector<int> tile_cta_ranges(const std::vector<int>& tile_chunk, const std::vector<int>& first) {
+  const int T = static_cast<int>(tile_chunk.size()) - 1;
+  const auto owner = [&](int c) {
+    return static_cast<int>(std::upper_bound(first.begin(), first.end() - 1, c) - first.begin()) - 1;
+  };
+  std::vector<int> out(2 * static_cast<size_t>(T));
+  for (int t = 0; t < T; ++t) {
+    out[2 * t] = owner(tile_chunk[t]);
+    out[2 * t + 1] = owner(tile_chunk[t + 1] - 1);
+  }
+  return out;
+}
+
 }  // namespace hdb

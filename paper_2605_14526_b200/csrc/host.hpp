@@ -132,6 +132,13 @@ struct HostFactor {
   std::string ordering;
   double weight_contrast = 1;
 };
+// Cost-balanced contiguous chunk ranges for G persistent CTAs: chunk cost =
+// values + seg_cost * segments; G + 1 boundaries, every range non-empty when
+// chunks >= G.
+std::vector<int> balanced_ranges(const std::vector<ChunkDesc>& chunks, int G, double seg_cost);
+// For each tile, the first and last CTA (of the ranges `first`) owning one of
+// its chunks (2 * n_tiles entries).
+std::vector<int> tile_cta_ranges(const std::vector<int>& tile_chunk, const std::vector<int>& first);
 // Setup-time self-check of a built factor on the host: max over three axes of
 // |A_ff S'^T S' b - b| / |b| for a deterministic b (no solve path runs here).
 double factor_inverse_residual(const HostFactor& F);

@@ -86,6 +86,20 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarps) : "memory"); }
 
+// Per-CTA timing trace, compiled only into microbenchmarks that define
+// HDK_SOLVE_TRACE: [2 b] = start, [2 b + 1] = end (globaltimer, ns) of CTA b.
+#ifdef HDK_SOLVE_TRACE
+__device__ unsigned long long* g_cta_trace = nullptr;
+#define HDK_TRACE_PTR g_cta_trace
+#else
+#define HDK_TRACE_PTR static_cast<unsigned long long*>(nullptr)
+#endif
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Balanced contiguous chunk ranges: CTA b of G owns [first(b), first(b+1)).
 __device__ __forceinline__ int range_first(long long b, int G, int C) { return static_cast<int>(b * C / G); }
 // The CTA owning chunk c (G <= C, so no range is empty).
@@ -210,15 +224,17 @@ __device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S>& r, int c_
 
 // ---- pass 1 ------------------------------------------------------------------
 template <bool kDry = false>  // kDry: stream only (microbenchmarks)
-__global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double* __restrict__ rhs) {
+__global__ void __launch_bounds__(kThreads, 2) k_rowdot(hdk_factor f, const double* __restrict__ rhs) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<kStages1>& ring = *reinterpret_cast<Ring<kStages1>*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long* trace = HDK_TRACE_PTR;
+  if (trace && threadIdx.x == 0) trace[2 * blockIdx.x] = globaltimer();
   ring_init(ring);
-  const int c_beg = range_first(blockIdx.x, gridDim.x, f.n_chunks);
-  const int c_end = range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
+  const int c_beg = f.first1 ? f.first1[blockIdx.x] : range_first(blockIdx.x, gridDim.x, f.n_chunks);
+  const int c_end = f.first1 ? f.first1[blockIdx.x + 1] : range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
   if (warp == kWarps) {
     produce(f, ring, c_beg, c_end, false);
     return;
@@ -243,7 +259,10 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
     const double* vals = ring.vals[st];
     // segment pair p = {2p, 2p+1} of the chunk goes to warp (seg0/2 + p) mod 8
     // (balanced over chunks); the two dot products share one shuffle tree.
+    // The stage is released as soon as the warp's last pair sits in
+    // registers, so the producer refills it while the arithmetic runs.
     const int npair = (ch.nseg + 1) >> 1;
+    bool released = false;
     for (int pi = (warp - (ch.seg0 >> 1)) & (kWarps - 1); pi < (kDry ? 0 : npair); pi += kWarps) {
       const int ia = 2 * pi, ib = ia + 1;
       const bool hasb = ib < ch.nseg;
@@ -253,18 +272,27 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
       const int lb = sb.clo_len & 0xffff, hb = hasb ? lb + (sb.clo_len >> 16) : lb;
       const double* va = vals + sa.coff - la;
       const double* vb = vals + sb.coff - lb;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+      double wa[kM], wb[kM];
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
-        const double wa = (cl >= la && cl < ha) ? va[cl] : 0.0;
-        const double wb = (cl >= lb && cl < hb) ? vb[cl] : 0.0;
-        a0 += wa * b0[m];
-        a1 += wa * b1[m];
-        a2 += wa * b2[m];
-        c0 += wb * b0[m];
-        c1 += wb * b1[m];
-        c2 += wb * b2[m];
+        wa[m] = (cl >= la && cl < ha) ? va[cl] : 0.0;
+        wb[m] = (cl >= lb && cl < hb) ? vb[cl] : 0.0;
+      }
+      if (pi + kWarps >= npair) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ring.empty[st]);
+        released = true;
+      }
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+#pragma unroll
+      for (int m = 0; m < kM; ++m) {
+        a0 += wa[m] * b0[m];
+        a1 += wa[m] * b1[m];
+        a2 += wa[m] * b2[m];
+        c0 += wb[m] * b0[m];
+        c1 += wb[m] * b1[m];
+        c2 += wb[m] * b2[m];
       }
       // reduce-scatter: lanes 0-15 keep segment a, lanes 16-31 segment b
       // after the first exchange, so the pair costs 15 shuffles, not 30
@@ -286,8 +314,14 @@ __global__ void __launch_bounds__(kThreads) k_rowdot(hdk_factor f, const double*
         p[2] = k2;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&ring.empty[st]);
+    if (!released) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ring.empty[st]);
+    }
+  }
+  if (trace) {
+    consumers_sync();
+    if (threadIdx.x == 0) trace[2 * blockIdx.x + 1] = globaltimer();
   }
 }
 
@@ -379,9 +413,11 @@ __global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
   Pass2Smem& sm = *reinterpret_cast<Pass2Smem*>(smem_raw);
   Ring2<kStages2>& ring = sm.ring;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long* trace = HDK_TRACE_PTR;
+  if (trace && threadIdx.x == 0) trace[2 * blockIdx.x] = globaltimer();
   ring2_init(ring);
-  const int c_beg = range_first(blockIdx.x, gridDim.x, f.n_chunks);
-  const int c_end = range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
+  const int c_beg = f.first2 ? f.first2[blockIdx.x] : range_first(blockIdx.x, gridDim.x, f.n_chunks);
+  const int c_end = f.first2 ? f.first2[blockIdx.x + 1] : range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
   // Pass 2 walks its range backwards: the tail pass 1 just streamed is still
   // in L2, and pass 2 ends where the next pass 1 begins.
   if (warp == kWarps) {
@@ -426,6 +462,10 @@ __global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
     if (lane == 0) mbar_arrive(&ring.empty[st]);
   }
   if (tile >= 0) fold_and_write(f, sm, tile + blockIdx.x, x0, x1, x2);
+  if (trace) {
+    consumers_sync();
+    if (threadIdx.x == 0) trace[2 * blockIdx.x + 1] = globaltimer();
+  }
 }
 
 // x_c = sum of the tile partials of the CTAs whose chunk ranges touch the
@@ -437,7 +477,8 @@ __global__ void k_xreduce(hdk_factor f, int G, double* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= f.n) return;
   const int t = c / kW, cl = c - t * kW;
-  const int b0 = cta_of(f.tile_chunk[t], G, f.n_chunks), b1 = cta_of(f.tile_chunk[t + 1] - 1, G, f.n_chunks);
+  const int b0 = f.tile_cta2 ? f.tile_cta2[2 * t] : cta_of(f.tile_chunk[t], G, f.n_chunks);
+  const int b1 = f.tile_cta2 ? f.tile_cta2[2 * t + 1] : cta_of(f.tile_chunk[t + 1] - 1, G, f.n_chunks);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (int b = b0; b <= b1; ++b) {
     const double* p = f.part2 + 3 * ((size_t)(t + b) * kW + cl);
@@ -471,23 +512,33 @@ const Grids& grids() {
   return g;
 }
 
+void pick_grids(const hdk_factor* f, int& g1, int& g2) {
+  g1 = grids().g1 < f->n_chunks ? grids().g1 : f->n_chunks;
+  g2 = grids().g2 < f->n_chunks ? grids().g2 : f->n_chunks;
+  if (f->grid_cap > 0 && g1 > f->grid_cap) g1 = f->grid_cap;
+  if (f->grid_cap > 0 && g2 > f->grid_cap) g2 = f->grid_cap;
+  if (g2 > f->max_ctas) g2 = f->max_ctas;
+}
+
 int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatter, cudaStream_t st) {
   if (f->n <= 0) return 0;
   if (f->tile_w != kW) return static_cast<int>(cudaErrorInvalidValue);
   const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem);
-  const int g_grid1 = grids().g1, g_grid2 = grids().g2;
-  int g1 = g_grid1 < f->n_chunks ? g_grid1 : f->n_chunks;
-  int g2 = g_grid2 < f->n_chunks ? g_grid2 : f->n_chunks;
-  if (f->grid_cap > 0 && g1 > f->grid_cap) g1 = f->grid_cap;
-  if (f->grid_cap > 0 && g2 > f->grid_cap) g2 = f->grid_cap;
-  if (g2 > f->max_ctas) g2 = f->max_ctas;
-  hdk::launch(k_rowdot<false>, dim3(g1), dim3(kThreads), s1, st, *f, rhs_perm);
-  hdk::launch(k_zreduce, dim3((f->n * 8 + 255) / 256), dim3(256), 0, st, *f);
-  hdk::launch(k_coltile<false>, dim3(g2), dim3(kThreads2), s2, st, *f);
+  int g1, g2;
+  pick_grids(f, g1, g2);
+  hdk_factor fl = *f;  // balanced ranges only if they were built for these grids
+  if (g1 != f->grid1) fl.first1 = nullptr;
+  if (g2 != f->grid2) {
+    fl.first2 = nullptr;
+    fl.tile_cta2 = nullptr;
+  }
+  hdk::launch(k_rowdot<false>, dim3(g1), dim3(kThreads), s1, st, fl, rhs_perm);
+  hdk::launch(k_zreduce, dim3((f->n * 8 + 255) / 256), dim3(256), 0, st, fl);
+  hdk::launch(k_coltile<false>, dim3(g2), dim3(kThreads2), s2, st, fl);
   if (scatter)
-    hdk::launch(k_xreduce<true>, dim3((f->n + 255) / 256), dim3(256), 0, st, *f, g2, out);
+    hdk::launch(k_xreduce<true>, dim3((f->n + 255) / 256), dim3(256), 0, st, fl, g2, out);
   else
-    hdk::launch(k_xreduce<false>, dim3((f->n + 255) / 256), dim3(256), 0, st, *f, g2, out);
+    hdk::launch(k_xreduce<false>, dim3((f->n + 255) / 256), dim3(256), 0, st, fl, g2, out);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -497,6 +548,14 @@ extern "C" {
 
 HDK_API int hdk_apply_inverse3(const hdk_factor* f, const double* rhs_perm, double* out_full, void* stream) {
   return launch(f, rhs_perm, out_full, true, static_cast<cudaStream_t>(stream));
+}
+
+HDK_API int hdk_solve_grids(const hdk_factor* f, int* grid1, int* grid2) {
+  int g1 = 0, g2 = 0;
+  pick_grids(f, g1, g2);
+  if (grid1) *grid1 = g1;
+  if (grid2) *grid2 = g2;
+  return static_cast<int>(cudaGetLastError());
 }
 
 HDK_API int hdk_apply_inverse3_perm(const hdk_factor* f, const double* rhs_perm, double* out_perm, void* stream) {

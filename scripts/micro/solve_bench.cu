@@ -1,7 +1,9 @@
 // Times the two streaming passes of the global solve on the real C3 factor
 // layout (dumped by the host library) — wet (real consumers) vs dry (stream only).
+#define HDK_SOLVE_TRACE 1
 #include "../../paper_2605_14526_b200/csrc/solve.cu"
 #include <cstdio>
+#include <algorithm>
 #include <vector>
 #include <fstream>
 #include "../../paper_2605_14526_b200/csrc/host.hpp"
@@ -62,6 +64,39 @@ int main(int argc, char** argv) {
     // full solve (alternating pass directions keep L2 warm)
     t = time_kernel([out](int g, size_t sm, const hdk_factor& f, const double* r) { hdk_apply_inverse3_perm(&f, r, out, 0); }, 0, 0, f, drhs, 50);
     printf("full solve  %7.2f us  (alg %7.1f GB/s)\n", t, 2 * gb / (t * 1e-6));
+  }
+  // cost-balanced CTA ranges: sweep the per-segment cost of both passes
+  {
+    const int G1 = 148 * o1, G2 = 148 * o2;
+    unsigned long long* tr; cudaMalloc(&tr, 16 * (size_t)std::max(G1, G2));
+    std::vector<unsigned long long> h(2 * std::max(G1, G2));
+    auto spread = [&](int G, const char* what) {
+      cudaMemcpy(h.data(), tr, 16 * (size_t)G, cudaMemcpyDeviceToHost);
+      unsigned long long t0 = ~0ull;
+      for (int b = 0; b < G; ++b) t0 = std::min(t0, h[2 * b]);
+      std::vector<double> d(G);
+      for (int b = 0; b < G; ++b) d[b] = (h[2 * b + 1] - t0) * 1e-3;
+      std::sort(d.begin(), d.end());
+      printf("    %s CTA ends: min %.2f p50 %.2f p90 %.2f max %.2f us\n", what, d[0], d[G / 2], d[G * 9 / 10], d[G - 1]);
+    };
+    for (double a : {0.0, 200.0, 300.0, 400.0, 600.0}) {
+      std::vector<int> f1 = hdb::balanced_ranges(F.chunks, G1, a), f2 = hdb::balanced_ranges(F.chunks, G2, a);
+      std::vector<int> tc = hdb::tile_cta_ranges(F.tile_chunk, f2);
+      hdk_factor fb = f;
+      fb.grid1 = G1; fb.grid2 = G2;
+      fb.first1 = (const int*)up(f1.data(), f1.size() * 4);
+      fb.first2 = (const int*)up(f2.data(), f2.size() * 4);
+      fb.tile_cta2 = (const int*)up(tc.data(), tc.size() * 4);
+      float t1 = time_kernel([](int g, size_t sm, const hdk_factor& f, const double* r) { k_rowdot<false><<<g, kThreads, sm>>>(f, r); }, G1, s1, fb, drhs, 50);
+      float t2 = time_kernel([](int g, size_t sm, const hdk_factor& f, const double* r) { k_coltile<false><<<g, kThreads2, sm>>>(f); }, G2, s2, fb, drhs, 50);
+      float t3 = time_kernel([out](int g, size_t sm, const hdk_factor& f, const double* r) { hdk_apply_inverse3_perm(&f, r, out, 0); }, 0, 0, fb, drhs, 50);
+      printf("seg cost %5.0f: rowdot %.2f us  coltile %.2f us  full %.2f us (alg %.1f GB/s)\n", a, t1, t2, t3, 2 * gb / (t3 * 1e-6));
+      cudaMemcpyToSymbol(g_cta_trace, &tr, sizeof(tr));
+      k_rowdot<false><<<G1, kThreads, s1>>>(fb, drhs); cudaDeviceSynchronize(); spread(G1, "rowdot ");
+      k_coltile<false><<<G2, kThreads2, s2>>>(fb); cudaDeviceSynchronize(); spread(G2, "coltile");
+      unsigned long long* nul = nullptr;
+      cudaMemcpyToSymbol(g_cta_trace, &nul, sizeof(nul));
+    }
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
 }
