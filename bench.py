@@ -48,6 +48,7 @@ def parse():
                          "batch: C5 batched system-ID, 64 C2 samples sharded over the GPUs + NCCL all-reduce")
     ap.add_argument("--samples", type=int, default=64)
     ap.add_argument("--frames", type=int, default=10, help="frames per sample trajectory (batch workload)")
+    ap.add_argument("--ordering", default=None, help="factor ordering: nd-bfs (default), nd-geometric or metis")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -418,7 +419,7 @@ def main():
             raise SystemExit(f"product library missing: {PRODUCT_LIB} (run __graft_entry__.build())")
         run_batch(args, world, rank)
         return
-    scene_dict = scenes.config_scene(args.config)
+    scene_dict = scenes.config_scene(args.config, ordering=args.ordering)
     if args.impl == "reference":
         if world > 1:
             import torch.distributed as dist
@@ -549,7 +550,7 @@ def main():
             "config": {"workload": f"{args.config}: {scene_dict['name']} ({ne} tets, {sc.vertex_count} vertices, "
                                    f"{WORKLOADS.get(args.config.upper(), '')})",
                        "parallelism": "replicas" if world > 1 else "single",
-                       "factor": {"ordering": "nd-bfs (postordered)", "nnz_S": nnz, "free_vertices": sim.free_count,
+                       "factor": {"ordering": f"{args.ordering or 'nd-bfs'} (postordered)", "nnz_S": nnz, "free_vertices": sim.free_count,
                                   "build_s": t_fac},
                        "l2_policy": "inputs larger than L2 (factor values %.0f MB > 126 MB L2)" % (nnz * 8 / 1e6),
                        "mean_forward_iterations": float(np.mean(fwd_its)),

@@ -24,6 +24,8 @@
 #include <set>
 #include <thread>
 
+#include <cusolverSp.h>
+
 #include "host.hpp"
 
 namespace hdb {
@@ -214,6 +216,31 @@ void nd_bfs(const Graph& g, std::vector<int> blk, std::vector<int>& out, std::ve
   out.insert(out.end(), s.begin(), s.end());
 }
 
+// METIS nested dissection through cuSOLVER's host entry point
+// (cusolverSpXcsrmetisndHost); the etree postorder below is applied on top.
+void metis_nd(const Graph& g, std::vector<int>& out) {
+  const int n = static_cast<int>(g.size());
+  std::vector<int> rp(n + 1, 0), ci;
+  for (int i = 0; i < n; ++i) {
+    std::vector<int> row = g[i];
+    row.push_back(i);
+    std::sort(row.begin(), row.end());
+    ci.insert(ci.end(), row.begin(), row.end());
+    rp[i + 1] = static_cast<int>(ci.size());
+  }
+  cusolverSpHandle_t h = nullptr;
+  if (cusolverSpCreate(&h) != CUSOLVER_STATUS_SUCCESS) raise(Code::InvalidArgument, "factor: cusolverSpCreate failed");
+  cusparseMatDescr_t d = nullptr;
+  cusparseCreateMatDescr(&d);
+  cusparseSetMatType(d, CUSPARSE_MATRIX_TYPE_GENERAL);
+  cusparseSetMatIndexBase(d, CUSPARSE_INDEX_BASE_ZERO);
+  out.assign(n, 0);
+  const cusolverStatus_t st = cusolverSpXcsrmetisndHost(h, n, rp[n], d, rp.data(), ci.data(), nullptr, out.data());
+  cusparseDestroyMatDescr(d);
+  cusolverSpDestroy(h);
+  if (st != CUSOLVER_STATUS_SUCCESS) raise(Code::InvalidArgument, "factor: METIS ordering failed");
+}
+
 }  // namespace
 
 HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const std::vector<int>& fixed,
@@ -256,6 +283,8 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
       std::vector<int> level(n, -1);
       std::vector<char> mark(n, 0);
       nd_bfs(g, all, order, level, mark);
+    } else if (ordering == "metis") {
+      metis_nd(g, order);
     } else {
       std::vector<P3> x(n);
       for (int i = 0; i < n; ++i) x[i] = {mesh.rest[3 * freev[i]], mesh.rest[3 * freev[i] + 1], mesh.rest[3 * freev[i] + 2]};
