@@ -72,6 +72,7 @@ typedef struct hdk_factor {
   int n;                  /* free vertices */
   int tile_w, n_tiles, n_chunks;
   int max_ctas;           /* part2 holds (n_tiles + max_ctas) tile partials */
+  int l2_hint;            /* 1: stream the values with an L2 evict_first policy */
   int grid_cap;           /* 0: one resident wave per pass; else at most this many CTAs per pass
                              (lets concurrent samples of a batch share the SMs) */
   const double* sval;     /* tile-major value stream */
@@ -109,6 +110,9 @@ HDK_API int hdk_apply_inverse3(const hdk_factor* f, const double* rhs_perm, doub
  * for this factor (persistent: one resident wave, capped by grid_cap). */
 HDK_API int hdk_solve_grids(const hdk_factor* f, int* grid1, int* grid2);
 /* Same, result kept in elimination order (out_perm [n][3]). */
+/* Solve passes without the final fold: the tile partials stay in f->part2
+ * for hdk_aa_dots_fused. */
+HDK_API int hdk_apply_inverse3_partial(const hdk_factor* f, const double* rhs_perm, void* stream);
 HDK_API int hdk_apply_inverse3_perm(const hdk_factor* f, const double* rhs_perm, double* out_perm, void* stream);
 
 /* Per-element local step (local_solve + the element part of pd_rhs,
@@ -191,6 +195,14 @@ HDK_API int hdk_fixed_coupling(const hdk_csr* a_fd, const int* fixed, const doub
 HDK_API int hdk_aa_dots(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, const double* qcur, double* last_q,
                         double* last_g, double* dq, double* dg, double* partial, void* stream);
 HDK_API int hdk_aa_solve(hdk_ctl* ctl, const double* partial, int mode, void* stream);
+/* Fused iteration tail after hdk_apply_inverse3_partial: folds the solve's
+ * pass-2 tile partials into qhat (free rows, full vertex order; fixed rows are
+ * read as they are), then hdk_aa_dots, then — in the block that finishes last —
+ * hdk_aa_solve; mode 1 also sets the WHILE condition (cond_handle != 0).
+ * ticket: one zero-initialised device counter per concurrent stream. */
+HDK_API int hdk_aa_dots_fused(const hdk_vtx* x, const hdk_factor* f, hdk_ctl* ctl, double* qhat, const double* qcur,
+                              double* last_q, double* last_g, double* dq, double* dg, double* partial,
+                              unsigned int* ticket, int mode, unsigned long long cond_handle, void* stream);
 HDK_API int hdk_aa_mix(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, double* qcur, double* qprev,
                        const double* qpin, const double* dq, const double* dg, double* partial, int mode, void* stream);
 /* Dual gate (forward.cpp:140-146) and loop condition for the graph while node. */

@@ -165,6 +165,12 @@ HD_API long long hd_sim_kernel_launches(const hd_sim* sim);
  * receives the mean duration.  Also reports the algorithmic bytes one solve
  * moves (factor values read by both passes plus right-hand sides). */
 HD_API hd_status hd_sim_time_solve(hd_sim* sim, int reps, double* ms_per_solve, double* bytes_per_solve);
+/* Profiling: times `reps` launches of the adjoint backbone iteration (one
+ * body of the backward WHILE loop, run on whatever the buffers hold after a
+ * backward step) with CUDA events.  skip_mask drops kernels for ablation:
+ * bit 0 B x, bit 1 rhs gather, bit 2 solve passes, bit 3 fused AA dots/solve,
+ * bit 4 AA mix.  Results of an ablated body are meaningless; only its time is. */
+HD_API hd_status hd_sim_time_backbone(hd_sim* sim, int reps, unsigned skip_mask, double* ms_per_iteration);
 
 /* ---- batched system-ID (config C5; new) --------------------------------
  * One process's share of a batch of material-parameter samples.  Sample s

@@ -291,6 +291,11 @@ hd_status hd_sim_time_solve(hd_sim* sim, int reps, double* ms, double* bytes) {
   return guarded([&] { *ms = sim->eng->time_solve(reps, bytes); });
 }
 
+hd_status hd_sim_time_backbone(hd_sim* sim, int reps, unsigned skip_mask, double* ms) {
+  if (!sim || !ms || reps < 1) return bad_arg("hd_sim_time_backbone: bad argument");
+  return guarded([&] { *ms = sim->eng->time_backbone(reps, skip_mask); });
+}
+
 long long hd_sim_factor_nnz(const hd_sim* sim) { return sim ? sim->eng->factor().row_off.back() : 0; }
 int hd_sim_free_count(const hd_sim* sim) { return sim ? sim->eng->factor().n : 0; }
 long long hd_sim_solve_count(const hd_sim* sim) { return sim ? sim->eng->solve_count : 0; }

@@ -213,6 +213,7 @@ void Engine::build_static() {
   part_c_ = A.alloc<double>(HDK_RED_BLOCKS * HDK_RED_Q);
   cache_ = A.alloc<double>(24 * ne);
   ctl_ = A.alloc<hdk_ctl>(1);
+  ticket_ = A.alloc<unsigned int>(1);
   seed_ = A.alloc<double>(n3);
   x_ = A.alloc<double>(n3);
   t_ = A.alloc<double>(n3);
@@ -288,6 +289,10 @@ void Engine::build_factor_device() {
   df_.n_chunks = static_cast<int>(F.chunks.size());
   df_.max_ctas = 148 * 8;
   df_.grid_cap = solve_ctas_;
+  {
+    const char* hint = std::getenv("HETERODYN_L2_HINT");
+    df_.l2_hint = hint ? std::atoi(hint) : 1;
+  }
   df_.sval = A.upload(F.stream);
   static_assert(sizeof(hdk_seg) == sizeof(SegDesc), "segment descriptor layout");
   static_assert(sizeof(hdk_chunk) == sizeof(ChunkDesc), "chunk descriptor layout");
@@ -381,9 +386,9 @@ void Engine::build_forward_graph() {
     hdk_check(hdk_local_step(&dm_, &dmat_, qcur_, ef_, nullptr, &ctl_->err, s), "local step");
     hdk_check(hdk_gather_rhs(&dv_, ef_, 1.0 / (h * h), qtil_, damp_, hf_.fixed.empty() ? nullptr : fixc_, bprev_, rhs_,
                              part_a_, s), "rhs");
-    hdk_check(hdk_apply_inverse3(&df_, rhs_, qhat_, s), "solve");
-    hdk_check(hdk_aa_dots(&dv_, ctl_, qhat_, qcur_, lastq_, lastg_, dq_, dg_, part_b_, s), "aa dots");
-    hdk_check(hdk_aa_solve(ctl_, part_b_, 0, s), "aa solve");
+    hdk_check(hdk_apply_inverse3_partial(&df_, rhs_, s), "solve");
+    hdk_check(hdk_aa_dots_fused(&dv_, &df_, ctl_, qhat_, qcur_, lastq_, lastg_, dq_, dg_, part_b_, ticket_, 0, 0ULL, s),
+              "aa dots + solve");
     hdk_check(hdk_aa_mix(&dv_, ctl_, qhat_, qcur_, qprev_, q_, dq_, dg_, part_c_, 0, s), "aa mix");
     hdk_check(hdk_gate(ctl_, part_a_, part_c_, handle, s), "gate");
   };
@@ -435,15 +440,7 @@ void Engine::build_backward_graph() {
   }, &bk_pre_);
   // backbone fixed point x <- A^{-1}(seed + B x) with AA(8) (backward.cpp:170-204)
   auto pre = [&] { hdk_check(hdk_aa_reset(ctl_, HDK_AA_MAX, 1e8, 500, 1e-10, s), "aa reset"); };
-  auto body = [&](unsigned long long handle) {
-    hdk_check(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B x");
-    hdk_check(hdk_gather_perm(&dv_, seed_, ef_, rhs_, s), "rhs");
-    hdk_check(hdk_apply_inverse3(&df_, rhs_, t_, s), "solve");
-    hdk_check(hdk_aa_dots(&dv_, ctl_, t_, x_, lastq_, lastg_, dq_, dg_, part_b_, s), "aa dots");
-    hdk_check(hdk_aa_solve(ctl_, part_b_, 1, s), "aa solve");
-    hdk_check(hdk_aa_mix(&dv_, ctl_, t_, x_, nullptr, nullptr, dq_, dg_, part_c_, 1, s), "aa mix");
-    hdk_check(hdk_backbone_cond(ctl_, handle, s), "cond");
-  };
+  auto body = [&](unsigned long long handle) { backbone_body(handle, 0u); };
   build_loop_graph(st_, use_cond_, pre, body, [] {}, *bgraph_);
   bk_body_ = bgraph_->counts[1];
   bk_pre_ += bgraph_->counts[0];
@@ -467,6 +464,37 @@ void Engine::build_backward_graph() {
     hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, dlv_, 0.0, nullptr, vbar_, s), "next v seed");
   }, &kb);
   bk_post_ += kb;
+}
+
+// One adjoint backbone iteration x <- A^{-1}(seed + B x) + AA(8)
+// (backward.cpp:170-204); skip bits drop kernels for timing ablations only.
+void Engine::backbone_body(unsigned long long handle, unsigned skip) {
+  void* s = st_;
+  if (!(skip & 1u)) hdk_check(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B x");
+  if (!(skip & 2u)) hdk_check(hdk_gather_perm(&dv_, seed_, ef_, rhs_, s), "rhs");
+  if (!(skip & 4u)) hdk_check(hdk_apply_inverse3_partial(&df_, rhs_, s), "solve");
+  if (!(skip & 8u))
+    hdk_check(hdk_aa_dots_fused(&dv_, &df_, ctl_, t_, x_, lastq_, lastg_, dq_, dg_, part_b_, ticket_, 1, handle, s),
+              "aa dots + solve + cond");
+  if (!(skip & 16u)) hdk_check(hdk_aa_mix(&dv_, ctl_, t_, x_, nullptr, nullptr, dq_, dg_, part_c_, 1, s), "aa mix");
+}
+
+double Engine::time_backbone(int reps, unsigned skip) {
+  cudaGraphExec_t g = capture_exec(st_, [&] { backbone_body(0ULL, skip); }, nullptr);
+  cudaEvent_t a, b;
+  cuda_check(cudaEventCreate(&a), "event");
+  cuda_check(cudaEventCreate(&b), "event");
+  for (int i = 0; i < 3; ++i) cuda_check(cudaGraphLaunch(g, st_), "warm body");
+  cuda_check(cudaEventRecord(a, st_), "event");
+  for (int i = 0; i < reps; ++i) cuda_check(cudaGraphLaunch(g, st_), "timed body");
+  cuda_check(cudaEventRecord(b, st_), "event");
+  cuda_check(cudaEventSynchronize(b), "event sync");
+  float ms = 0;
+  cuda_check(cudaEventElapsedTime(&ms, a, b), "elapsed");
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaGraphExecDestroy(g);
+  return static_cast<double>(ms) / reps;
 }
 
 void Engine::sync_ctl() {

@@ -92,6 +92,8 @@ class Engine {
                    bool canonical = false, bool download = true, const double* d_target = nullptr);
   void reset_state();  // scene's initial state, time 0, recorded frames dropped
   double time_solve(int reps, double* bytes);
+  double time_backbone(int reps, unsigned skip_mask);
+  void backbone_body(unsigned long long cond_handle, unsigned skip_mask);
   Vec solve_free(const double* rhs, const double* fixed_q);
   void set_young(const Vec& young, bool freeze);
 
@@ -150,6 +152,7 @@ class Engine {
   double *part_a_ = nullptr, *part_b_ = nullptr, *part_c_ = nullptr;
   double* cache_ = nullptr;  // 24 ne projection cache of the current step
   hdk_ctl* ctl_ = nullptr;
+  unsigned int* ticket_ = nullptr;  // last-block ticket of hdk_aa_dots_fused
   hdk_ctl* h_ctl_ = nullptr;  // pinned mirror
   double* hook_ = nullptr;    // 5 doubles device
 

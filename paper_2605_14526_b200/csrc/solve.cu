@@ -73,6 +73,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Same, with an L2 eviction-priority policy (createpolicy): the factor stream
+// is marked evict_first so the once-per-pass values do not push the vectors,
+// partials and the adjoint's element differentials out of L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
 // 8-byte asynchronous global->shared copy (LDGSTS); completion is tracked by
 // cp_async_arrive on an mbarrier.
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -140,6 +155,7 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
   const int n = c_end - c_beg;
   auto chunk_at = [&](int k) { return reverse ? c_end - 1 - k : c_beg + k; };
   hdk_chunk nxt = n > 0 ? f.chunk[chunk_at(0)] : hdk_chunk{};
+  const uint64_t pol = policy_evict_first();
   for (int k = 0; k < n; ++k) {
     const int st = k % S;
     const hdk_chunk ch = nxt;
@@ -149,7 +165,10 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
     r.info[st] = ChunkInfo{ch.nseg, ch.tile, ch.seg0, 0};
     const uint32_t vb = static_cast<uint32_t>(ch.len) * 8u, sb = static_cast<uint32_t>(ch.nseg) * 16u;
     mbar_expect_tx(&r.full[st], vb + sb);
-    if (vb) bulk_g2s(r.vals[st], f.sval + ch.off, vb, &r.full[st]);
+    if (vb) {
+      if (f.l2_hint) bulk_g2s_hint(r.vals[st], f.sval + ch.off, vb, &r.full[st], pol);
+      else bulk_g2s(r.vals[st], f.sval + ch.off, vb, &r.full[st]);
+    }
     bulk_g2s(r.segs[st], f.seg + ch.seg0, sb, &r.full[st]);
   }
 }
@@ -208,6 +227,7 @@ __device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S>& r, int c_
   if ((threadIdx.x & 31) != 0) return;
   const int n = c_end - c_beg;
   hdk_chunk nxt = n > 0 ? f.chunk[c_end - 1] : hdk_chunk{};
+  const uint64_t pol = policy_evict_first();
   for (int k = 0; k < n; ++k) {
     const int st = k % S;
     const hdk_chunk ch = nxt;
@@ -217,7 +237,10 @@ __device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S>& r, int c_
     r.info[st] = ChunkInfo{ch.nseg, ch.tile, ch.seg0, 0};
     const uint32_t vb = static_cast<uint32_t>(ch.len) * 8u, sb = static_cast<uint32_t>(ch.nseg) * 16u;
     mbar_expect_tx(&r.full[st], vb + sb);
-    if (vb) bulk_g2s(r.vals[st], f.sval + ch.off, vb, &r.full[st]);
+    if (vb) {
+      if (f.l2_hint) bulk_g2s_hint(r.vals[st], f.sval + ch.off, vb, &r.full[st], pol);
+      else bulk_g2s(r.vals[st], f.sval + ch.off, vb, &r.full[st]);
+    }
     bulk_g2s(r.segs[st], f.seg + ch.seg0, sb, &r.full[st]);
   }
 }
@@ -520,7 +543,8 @@ void pick_grids(const hdk_factor* f, int& g1, int& g2) {
   if (g2 > f->max_ctas) g2 = f->max_ctas;
 }
 
-int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatter, cudaStream_t st) {
+int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatter, cudaStream_t st,
+           bool fold = true) {
   if (f->n <= 0) return 0;
   if (f->tile_w != kW) return static_cast<int>(cudaErrorInvalidValue);
   const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem);
@@ -535,6 +559,7 @@ int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatte
   hdk::launch(k_rowdot<false>, dim3(g1), dim3(kThreads), s1, st, fl, rhs_perm);
   hdk::launch(k_zreduce, dim3((f->n * 8 + 255) / 256), dim3(256), 0, st, fl);
   hdk::launch(k_coltile<false>, dim3(g2), dim3(kThreads2), s2, st, fl);
+  if (!fold) return static_cast<int>(cudaGetLastError());
   if (scatter)
     hdk::launch(k_xreduce<true>, dim3((f->n + 255) / 256), dim3(256), 0, st, fl, g2, out);
   else
@@ -556,6 +581,10 @@ HDK_API int hdk_solve_grids(const hdk_factor* f, int* grid1, int* grid2) {
   if (grid1) *grid1 = g1;
   if (grid2) *grid2 = g2;
   return static_cast<int>(cudaGetLastError());
+}
+
+HDK_API int hdk_apply_inverse3_partial(const hdk_factor* f, const double* rhs_perm, void* stream) {
+  return launch(f, rhs_perm, nullptr, true, static_cast<cudaStream_t>(stream), false);
 }
 
 HDK_API int hdk_apply_inverse3_perm(const hdk_factor* f, const double* rhs_perm, double* out_perm, void* stream) {

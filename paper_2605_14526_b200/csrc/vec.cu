@@ -243,10 +243,13 @@ __global__ void __launch_bounds__(kT) k_aa_dots(hdk_vtx x, const hdk_ctl* ctl, c
 // diagonal pivoting (left-looking, pivots chosen on the untouched diagonal).
 // One warp: lane 0 does the short serial bookkeeping, the factorization runs
 // row-parallel over lanes; everything lives in shared memory.
-constexpr int kSolveT = 256;  // 8 warps fold the 18 partial sums
-__global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const double* partial, int mode) {
-  hdk::pdl_wait();
-  hdk::pdl_trigger();
+// Runs on one whole block of kT threads: inside k_aa_solve, or as the tail of
+// k_aa_dots_fused in whichever block finishes last.  mode 1 also sets the
+// adjoint loop's WHILE condition (the former k_bb_cond) when a graph handle
+// is given.
+constexpr int kSolveT = kT;  // 8 warps fold the 18 partial sums
+__device__ __noinline__ void aa_solve_block(hdk_ctl* gctl, const double* partial, int mode,
+                                            cudaGraphConditionalHandle handle, int use_handle) {
   __shared__ double s[2 * HDK_AA_MAX + 2];
   __shared__ hdk_ctl c;  // shared-memory copy of the control block
   __shared__ double A[HDK_AA_MAX][HDK_AA_MAX + 1], L[HDK_AA_MAX][HDK_AA_MAX + 1], d[HDK_AA_MAX], y[HDK_AA_MAX];
@@ -396,12 +399,102 @@ __global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const doubl
   }
 writeback:
   __syncthreads();
+  if (mode == 1 && threadIdx.x == 0) {  // adjoint loop condition (done / error)
+    c.cond = (!c.done && c.err == 0) ? 1 : 0;
+    if (use_handle) cudaGraphSetConditional(handle, c.cond);
+  }
+  __syncthreads();
   {
     const int* src = reinterpret_cast<const int*>(&c);
     int* dst = reinterpret_cast<int*>(gctl);
     #pragma unroll 1
     for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += blockDim.x) dst[i] = src[i];
   }
+}
+
+__global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const double* partial, int mode) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  aa_solve_block(gctl, partial, mode, 0, 0);
+}
+
+// Fused tail of one PD / adjoint iteration after the solve's column pass:
+//   * x-fold (the former k_xreduce): qhat at free vertex v is the fixed-order
+//     sum of the pass-2 tile partials of column p = v2p[v] — same terms, same
+//     order, so bitwise what k_xreduce scattered; fixed rows keep qhat;
+//   * the Anderson history update and dot partials (k_aa_dots);
+//   * the coefficient solve (k_aa_solve) in the block that finishes last
+//     (threadfence + ticket), and in mode 1 the loop condition.
+// One launch instead of four.
+__global__ void __launch_bounds__(kT) k_aa_dots_fused(hdk_vtx x, hdk_factor f, int g2, hdk_ctl* ctl,
+                                                      double* __restrict__ qhat, const double* __restrict__ qcur,
+                                                      double* last_q, double* last_g, double* dq, double* dg,
+                                                      double* partial, unsigned int* ticket, int mode,
+                                                      cudaGraphConditionalHandle handle, int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const size_t n3 = 3 * (size_t)x.nv;
+  const int m = ctl->window, c = ctl->count, h = ctl->head;
+  const bool push = ctl->has_last != 0;
+  int ns = 0, c2 = c, h2 = h;
+  if (push) {
+    ns = c < m ? (h + c) % m : h;
+    c2 = c < m ? c + 1 : m;
+    h2 = c < m ? h : (h + 1) % m;
+  }
+  double acc[2 * HDK_AA_MAX + 2];
+#pragma unroll
+  for (int q = 0; q < 2 * HDK_AA_MAX + 2; ++q) acc[q] = 0.0;
+  for (size_t i = blockIdx.x * kT + threadIdx.x; i < n3; i += (size_t)HDK_RED_BLOCKS * kT) {
+    const int v = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)v);
+    const int p = __ldg(x.v2p + v);
+    double th;
+    if (p >= 0) {
+      const int t = p / 256, cl = p - 256 * t;
+      const int b0 = f.tile_cta2 ? __ldg(f.tile_cta2 + 2 * t) : 0;
+      const int b1 = f.tile_cta2 ? __ldg(f.tile_cta2 + 2 * t + 1) : -1;
+      th = 0.0;
+      for (int b = b0; b <= b1; ++b) th += __ldcg(f.part2 + 3 * ((size_t)(t + b) * 256 + cl) + a);
+      qhat[i] = th;
+    } else {
+      th = qhat[i];
+    }
+    const double qc = qcur[i];
+    const double g = th - qc;
+    acc[2 * HDK_AA_MAX] += g * g;
+    acc[2 * HDK_AA_MAX + 1] += th * th;
+    if (push) {
+      const double dqn = qc - last_q[i];
+      const double dgn = g - last_g[i];
+      dq[ns * n3 + i] = dqn;
+      dg[ns * n3 + i] = dgn;
+#pragma unroll
+      for (int j = 0; j < HDK_AA_MAX; ++j) {
+        if (j < c2) {
+          const int ph = (h2 + j) % m;
+          const double dgj = ph == ns ? dgn : dg[ph * n3 + i];
+          acc[j] += dgn * dgj;
+          acc[HDK_AA_MAX + j] += dgj * g;
+        }
+      }
+    }
+    last_q[i] = qc;
+    last_g[i] = g;
+  }
+  block_partials<2 * HDK_AA_MAX + 2>(acc, partial);
+  // last block folds every partial and runs the coefficient solve
+  __shared__ int is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(ticket, 1u);
+    is_last = t == gridDim.x - 1;
+    if (is_last) *ticket = 0u;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  aa_solve_block(ctl, partial, mode, handle, use_handle);
 }
 
 __global__ void __launch_bounds__(kT) k_aa_mix(hdk_vtx x, hdk_ctl* ctl, const double* __restrict__ qhat, double* qcur,
@@ -706,6 +799,18 @@ HDK_API int hdk_aa_dots(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, cons
 
 HDK_API int hdk_aa_solve(hdk_ctl* ctl, const double* partial, int mode, void* stream) {
   hdk::launch(k_aa_solve, dim3(1), dim3(kSolveT), 0, S(stream), ctl, partial, mode);
+  return last();
+}
+
+HDK_API int hdk_aa_dots_fused(const hdk_vtx* x, const hdk_factor* f, hdk_ctl* ctl, double* qhat, const double* qcur,
+                              double* last_q, double* last_g, double* dq, double* dg, double* partial,
+                              unsigned int* ticket, int mode, unsigned long long cond_handle, void* stream) {
+  int g1 = 0, g2 = 0;
+  hdk_solve_grids(f, &g1, &g2);
+  if (!f->tile_cta2 || g2 != f->grid2) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_aa_dots_fused, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), *x, *f, g2, ctl, qhat, qcur, last_q,
+              last_g, dq, dg, partial, ticket, mode, static_cast<cudaGraphConditionalHandle>(cond_handle),
+              cond_handle != 0ULL ? 1 : 0);
   return last();
 }
 

@@ -72,6 +72,7 @@ SIGNATURES = {
     "hd_sim_stream": (_VP, [_VP]),
     "hd_sim_kernel_launches": (C.c_longlong, [_VP]),
     "hd_sim_time_solve": (C.c_int, [_VP, C.c_int, _D, _D]),
+    "hd_sim_time_backbone": (C.c_int, [_VP, C.c_int, C.c_uint, _D]),
     "hd_batch_create": (_VP, [_VP, C.c_int, _D, C.c_size_t, C.c_int]),
     "hd_batch_free": (None, [_VP]),
     "hd_batch_sample_count": (C.c_int, [_VP]),
@@ -314,6 +315,12 @@ class Sim:
         b = C.c_double()
         self.L.check(self.L.lib.hd_sim_time_solve(self.h, reps, C.byref(ms), C.byref(b)))
         return ms.value, b.value
+
+    def time_backbone(self, reps: int = 50, skip_mask: int = 0) -> float:
+        """ms per adjoint backbone iteration (profiling; see heterodyn.h)."""
+        ms = C.c_double()
+        self.L.check(self.L.lib.hd_sim_time_backbone(self.h, reps, skip_mask, C.byref(ms)))
+        return ms.value
 
     def solve_free(self, rhs, fixed_q=None):
         rhs = _f64(rhs, self.n)
