@@ -92,6 +92,7 @@ typedef struct hdk_factor {
   const int* first1;      /* grid1+1: first chunk of pass-1 CTA b */
   const int* first2;      /* grid2+1: first chunk of pass-2 CTA b */
   const int* tile_cta2;   /* 2*n_tiles: first and last pass-2 CTA touching tile t */
+  const int2* vfold;      /* nv: (first tile-partial slot of the vertex's column, slot count; 0 if fixed) */
 } hdk_factor;
 
 /* Scalar CSR in elimination order (a_free / a_free_fixed, factor.hpp:98-99). */

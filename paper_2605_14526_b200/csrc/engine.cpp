@@ -325,7 +325,17 @@ void Engine::build_factor_device() {
     df_.grid2 = g2;
     df_.first1 = A.upload(f1);
     df_.first2 = A.upload(f2);
-    df_.tile_cta2 = A.upload(tile_cta_ranges(F.tile_chunk, f2));
+    const std::vector<int> tc = tile_cta_ranges(F.tile_chunk, f2);
+    df_.tile_cta2 = A.upload(tc);
+    // per vertex: first pass-2 tile-partial slot of its column and how many
+    // CTAs wrote one (0 for fixed vertices) — the x-fold's one indirection
+    std::vector<int> vf(2 * static_cast<size_t>(scene_.mesh.nv), 0);
+    for (int c = 0; c < F.n; ++c) {
+      const int t = c / F.tile_w, v = F.p2v[c];
+      vf[2 * v] = (t + tc[2 * t]) * F.tile_w + (c - t * F.tile_w);
+      vf[2 * v + 1] = tc[2 * t + 1] - tc[2 * t] + 1;
+    }
+    df_.vfold = reinterpret_cast<const int2*>(A.upload(vf));
   }
   rhs_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
   fixc_ = A.alloc<double>(3 * static_cast<size_t>(F.n));

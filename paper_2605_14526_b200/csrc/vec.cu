@@ -40,6 +40,50 @@ __device__ __forceinline__ void block_partials(double (&v)[NQ], double* partial)
   }
 }
 
+// Same contract as block_partials for many quantities: a reduce-scatter
+// butterfly halves the list each level (18 -> 9 -> 5 -> 3 -> 2 -> 1: 20
+// shuffles instead of 18 x 5), after which lane l owns the warp sum of
+// quantity q(l); fixed lane/level order, so bitwise reproducible.
+template <int N, int O>
+__device__ __forceinline__ void rs_level(const double (&v)[N], double (&w)[(N + 1) / 2], int lane, int& q0,
+                                         int& len) {
+  constexpr int H = (N + 1) / 2;
+  const bool up = (lane & O) != 0;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const double lo = v[i];
+    const double hi = (i + H < N) ? v[i + H] : 0.0;
+    const double r = __shfl_xor_sync(0xffffffffu, up ? lo : hi, O);
+    w[i] = (up ? hi : lo) + r;
+  }
+  if (up) {
+    q0 += H;
+    len -= H;
+  } else if (len > H) {
+    len = H;
+  }
+}
+
+__device__ __forceinline__ void block_partials_18(const double (&v)[18], double* partial) {
+  __shared__ double sm[kT / 32][18];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int q0 = 0, len = 18;
+  double a9[9], a5[5], a3[3], a2[2], a1[1];
+  rs_level<18, 16>(v, a9, lane, q0, len);
+  rs_level<9, 8>(a9, a5, lane, q0, len);
+  rs_level<5, 4>(a5, a3, lane, q0, len);
+  rs_level<3, 2>(a3, a2, lane, q0, len);
+  rs_level<2, 1>(a2, a1, lane, q0, len);
+  if (len >= 1) sm[warp][q0] = a1[0];
+  __syncthreads();
+  if (threadIdx.x < 18) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) t += sm[w][threadIdx.x];
+    partial[blockIdx.x * HDK_RED_Q + threadIdx.x] = t;
+  }
+}
+
 // Single-block fold of partial slots [0, nq) over all blocks (fixed order):
 // warp w folds slots w, w + nwarps, ...; each lane issues all of its loads
 // before adding (no latency chain), then a fixed shuffle tree.  out must be
@@ -240,175 +284,256 @@ __global__ void __launch_bounds__(kT) k_aa_dots(hdk_vtx x, const hdk_ctl* ctl, c
 
 // Anderson coefficient solve (forward.cpp:31-47): M gamma = DG^T g with
 // M = DG^T DG + 1e-6 |DG|_F^2 / window I, by LDL^T with Eigen::LDLT's
-// diagonal pivoting (left-looking, pivots chosen on the untouched diagonal).
-// One warp: lane 0 does the short serial bookkeeping, the factorization runs
-// row-parallel over lanes; everything lives in shared memory.
-// Runs on one whole block of kT threads: inside k_aa_solve, or as the tail of
-// k_aa_dots_fused in whichever block finishes last.  mode 1 also sets the
-// adjoint loop's WHILE condition (the former k_bb_cond) when a graph handle
-// is given.
-constexpr int kSolveT = kT;  // 8 warps fold the 18 partial sums
-__device__ __noinline__ void aa_solve_block(hdk_ctl* gctl, const double* partial, int mode,
+// diagonal pivoting (left-looking; pivots chosen on the untouched diagonal).
+// Runs on one block of kT threads (inside k_aa_solve, or as the tail of
+// k_aa_dots_fused in the block that finishes last): all warps fold the
+// partial sums with every load in flight at once, then warp 0 alone does the
+// bookkeeping and the factorization in registers — lane i holds row i of the
+// Gram matrix and row rank(i) of L, pivot rows travel by shuffle, and the
+// pivot order, d and the substitution values are warp-uniform.  mode 1 also
+// evaluates the adjoint convergence test first (backward.cpp:191-193) and
+// sets the WHILE condition (graph handle given).
+constexpr int kSolveT = kT;
+constexpr int kNQ = 2 * HDK_AA_MAX + 2;
+__device__ __noinline__ void aa_solve_block(hdk_ctl* gctl, const double* __restrict__ partial, int mode,
                                             cudaGraphConditionalHandle handle, int use_handle) {
-  __shared__ double s[2 * HDK_AA_MAX + 2];
-  __shared__ hdk_ctl c;  // shared-memory copy of the control block
-  __shared__ double A[HDK_AA_MAX][HDK_AA_MAX + 1], L[HDK_AA_MAX][HDK_AA_MAX + 1], d[HDK_AA_MAX], y[HDK_AA_MAX];
-  __shared__ int perm[HDK_AA_MAX], solve_n, ok;
-  {
-    const int* src = reinterpret_cast<const int*>(gctl);
-    int* dst = reinterpret_cast<int*>(&c);
-    #pragma unroll 1
-    for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += blockDim.x) dst[i] = src[i];
+  constexpr int M = HDK_AA_MAX;
+  __shared__ double s[kNQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // warp 0: control scalars and its Gram rows, loaded ahead of the fold
+  int m = 1, count = 0, head = 0, has_last = 0, mixed = 0, kk = 0, iters = 0, err = 0, done = 0, k_max = 0;
+  double tol = 0.0, guard = 0.0;
+  double g[M];
+  if (warp == 0) {
+    m = gctl->window; count = gctl->count; head = gctl->head; has_last = gctl->has_last; mixed = gctl->mixed;
+    kk = gctl->k; iters = gctl->iterations; err = gctl->err; done = gctl->done; k_max = gctl->k_max;
+    tol = gctl->tol; guard = gctl->guard;
+#pragma unroll
+    for (int j = 0; j < M; ++j) g[j] = lane < M ? gctl->gram[lane * M + j] : 0.0;
   }
-  fold_all(partial, 2 * HDK_AA_MAX + 2, s);
-  __syncthreads();
-  if (threadIdx.x >= 32) goto writeback;
-  {
-    const int lane = threadIdx.x;
-    if (lane == 0) {
-      solve_n = 0;
-      bool skip = false;
-      if (mode == 1) {  // adjoint backbone: convergence test before mixing (backward.cpp:191-193)
-        c.iterations += 1;
-        const double diff = sqrt(s[2 * HDK_AA_MAX]);
-        const double base = fmax(sqrt(s[2 * HDK_AA_MAX + 1]), 1e-30);
-        c.k += 1;
-        if (diff <= c.tol * base) {
-          c.done = 1;
-          c.mixed = 0;
-          skip = true;
-        } else if (c.k >= c.k_max && c.err == 0) {
-          c.err = 10;  // AdjointDiverged (cap)
-        }
-      }
-      if (!skip) {
-        const int m = c.window;
-        if (c.has_last) {
-          const int n0 = c.count;
-          if (n0 < m) {
-            c.count = n0 + 1;
-          } else {
-            c.head = (c.head + 1) % m;
-            #pragma unroll 1
-            for (int i = 0; i + 1 < m; ++i)
-              #pragma unroll 1
-              for (int j = 0; j + 1 < m; ++j) c.gram[i * HDK_AA_MAX + j] = c.gram[(i + 1) * HDK_AA_MAX + (j + 1)];
-          }
-          const int n1 = c.count, j = n1 - 1;
-          #pragma unroll 1
-          for (int l = 0; l < n1; ++l) c.gram[j * HDK_AA_MAX + l] = c.gram[l * HDK_AA_MAX + j] = s[l];
-        }
-        c.has_last = 1;
-        c.mixed = 0;
-        const int n = c.count;
-        double fro2 = 0.0;
-        #pragma unroll 1
-        for (int j = 0; j < n; ++j) fro2 += c.gram[j * HDK_AA_MAX + j];
-        if (n > 0 && fro2 > 0.0) {
-          solve_n = n;
-          // pivot order: Eigen picks the largest |diagonal| among the remaining
-          // (untouched) diagonal entries, swapping it into place
-          double dg[HDK_AA_MAX];
-          #pragma unroll 1
-          for (int i = 0; i < n; ++i) {
-            perm[i] = i;
-            dg[i] = c.gram[i * HDK_AA_MAX + i] + 1e-6 * fro2 / m;
-          }
-          #pragma unroll 1
-          for (int k = 0; k < n; ++k) {
-            int piv = k;
-            double best = fabs(dg[k]);
-            #pragma unroll 1
-            for (int i = k + 1; i < n; ++i)
-              if (fabs(dg[i]) > best) { best = fabs(dg[i]); piv = i; }
-            const int tp = perm[k]; perm[k] = perm[piv]; perm[piv] = tp;
-            const double td = dg[k]; dg[k] = dg[piv]; dg[piv] = td;
-          }
-          y[0] = 1e-6 * fro2 / m;  // ridge, broadcast below
-        }
+  {  // fold: warp w owns quantities w, w + 8, w + 16; all loads issued first
+    constexpr int R = (kNQ + kT / 32 - 1) / (kT / 32);
+    double v[R][kFoldPerLane];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = warp + r * (kT / 32);
+#pragma unroll
+      for (int i = 0; i < kFoldPerLane; ++i) {
+        const int b = lane + 32 * i;
+        v[r][i] = (q < kNQ && b < HDK_RED_BLOCKS) ? __ldcg(partial + b * HDK_RED_Q + q) : 0.0;
       }
     }
-    __syncwarp();
-    const int n = solve_n;
-    if (n > 0) {
-      const double ridge = y[0];
-      __syncwarp();
-      // permuted matrix, rows over lanes
-      #pragma unroll 1
-      for (int e = lane; e < n * n; e += 32) {
-        const int i = e / n, j = e % n;
-        A[i][j] = c.gram[perm[i] * HDK_AA_MAX + perm[j]] + (perm[i] == perm[j] ? ridge : 0.0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double t = 0.0;
+#pragma unroll
+      for (int i = 0; i < kFoldPerLane; ++i) t += v[r][i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      const int q = warp + r * (kT / 32);
+      if (lane == 0 && q < kNQ) s[q] = t;
+    }
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  const unsigned F = 0xffffffffu;
+  bool skip = false;
+  if (mode == 1) {  // adjoint backbone: convergence test before mixing
+    iters += 1;
+    const double diff = sqrt(s[2 * M]);
+    const double base = fmax(sqrt(s[2 * M + 1]), 1e-30);
+    kk += 1;
+    if (diff <= tol * base) {
+      done = 1;
+      mixed = 0;
+      skip = true;
+    } else if (kk >= k_max && err == 0) {
+      err = 10;  // AdjointDiverged (cap)
+    }
+  }
+  int nsol = 0;
+  double gam[M];
+  if (!skip) {
+    if (has_last) {
+      if (count < m) {
+        count += 1;
+      } else {  // drop the oldest: gram[i][j] <- gram[i+1][j+1]
+        head = (head + 1) % m;
+        double nx[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) nx[j] = __shfl_down_sync(F, g[j], 1);
+#pragma unroll
+        for (int j = 0; j + 1 < M; ++j) g[j] = nx[j + 1];
       }
-      __syncwarp();
-      if (lane == 0) ok = 1;
-      __syncwarp();
-      #pragma unroll 1
-      for (int k = 0; k < n; ++k) {
-        if (lane == k) {
-          double dk = A[k][k];
-          #pragma unroll 1
-          for (int j = 0; j < k; ++j) dk -= L[k][j] * L[k][j] * d[j];
+      const int j0 = count - 1;  // newest row / column = DG^T dg_new
+#pragma unroll
+      for (int j = 0; j < M; ++j)
+        if (j == j0 && lane < count) g[j] = s[lane];
+      if (lane == j0)
+#pragma unroll
+        for (int l = 0; l < M; ++l)
+          if (l < count) g[l] = s[l];
+    }
+    has_last = 1;
+    mixed = 0;
+    const int n = count;
+    double mydiag = 0.0;
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+      if (j == lane) mydiag = g[j];
+    double fro2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const double dj = __shfl_sync(F, mydiag, j);
+      if (j < n) fro2 += dj;
+    }
+    if (n > 0 && fro2 > 0.0) {
+      nsol = n;
+      const double ridge = 1e-6 * fro2 / m;
+      // pivot order: largest |diagonal| among the remaining untouched ones,
+      // swapped into place (warp-uniform, registers only)
+      int perm[M];
+      double dv[M];
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        perm[i] = i;
+        dv[i] = __shfl_sync(F, mydiag, i) + ridge;
+      }
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        if (k < n) {
+          int piv = k;
+          double best = fabs(dv[k]);
+#pragma unroll
+          for (int i = k + 1; i < M; ++i)
+            if (i < n && fabs(dv[i]) > best) {
+              best = fabs(dv[i]);
+              piv = i;
+            }
+          const int pk = perm[k];
+          const double dk = dv[k];
+          int pp = pk;
+          double dp = dk;
+#pragma unroll
+          for (int i = k + 1; i < M; ++i)
+            if (i == piv) {
+              pp = perm[i];
+              dp = dv[i];
+              perm[i] = pk;
+              dv[i] = dk;
+            }
+          perm[k] = pp;
+          dv[k] = dp;
+        }
+      }
+      int rk = M;  // position of this lane's row in the pivot order
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        if (k < n && perm[k] == lane) rk = k;
+      // this lane's row of the permuted matrix: ap[j] = M(lane, perm[j])
+      double ap[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        double a = 0.0;
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+          if (c == perm[j]) a = g[c];
+        ap[j] = a + (perm[j] == lane ? ridge : 0.0);
+      }
+      double L[M], d[M];
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        L[k] = 0.0;
+        d[k] = 1.0;
+        if (k < n) {
+          const int pk = perm[k];
+          double Lp[M];
+#pragma unroll
+          for (int j = 0; j < k; ++j) Lp[j] = __shfl_sync(F, L[j], pk);
+          double dk = __shfl_sync(F, ap[k], pk);
+#pragma unroll
+          for (int j = 0; j < k; ++j) dk -= Lp[j] * Lp[j] * d[j];
           d[k] = dk;
-          if (!(fabs(dk) > 2.2250738585072014e-308)) ok = 0;
+          if (!(fabs(dk) > 2.2250738585072014e-308)) ok = false;
+          if (rk > k && rk < n) {
+            double v = ap[k];
+#pragma unroll
+            for (int j = 0; j < k; ++j) v -= L[j] * Lp[j] * d[j];
+            L[k] = v / dk;
+          }
         }
-        __syncwarp();
-        if (lane > k && lane < n) {
-          double v = A[lane][k];
-          #pragma unroll 1
-          for (int j = 0; j < k; ++j) v -= L[lane][j] * L[k][j] * d[j];
-          L[lane][k] = v / d[k];
-        }
-        __syncwarp();
       }
-      if (lane == 0) {
-        double gam[HDK_AA_MAX];
-        bool good = ok != 0;
-        if (good) {
-          #pragma unroll 1
-          for (int i = 0; i < n; ++i) y[i] = s[HDK_AA_MAX + perm[i]];
-          #pragma unroll 1
-          for (int i = 0; i < n; ++i)
-            #pragma unroll 1
-            for (int j = 0; j < i; ++j) y[i] -= L[i][j] * y[j];
-          #pragma unroll 1
-          for (int i = 0; i < n; ++i) y[i] /= d[i];
-          #pragma unroll 1
-          for (int i = n - 1; i >= 0; --i)
-            #pragma unroll 1
-            for (int j = i + 1; j < n; ++j) y[i] -= L[j][i] * y[j];
-          #pragma unroll 1
-          for (int i = 0; i < n; ++i) gam[perm[i]] = y[i];
-          #pragma unroll 1
-          for (int i = 0; i < n; ++i) good = good && isfinite(gam[i]);
+      // forward substitution, column-oriented (same subtraction order per row)
+      double y[M];
+      double acc = lane < M ? s[M + lane] : 0.0;
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        y[j] = 0.0;
+        if (j < n) {
+          y[j] = __shfl_sync(F, acc, perm[j]);
+          if (rk > j && rk < n) acc -= L[j] * y[j];
         }
-        double gn = 0.0;
-        if (good)
-          #pragma unroll 1
-          for (int i = 0; i < n; ++i) gn += gam[i] * gam[i];
-        if (!good || !(sqrt(gn) <= c.guard)) {  // guard: discard history (forward.cpp:43-47)
-          c.count = 0;
-          c.head = 0;
-          c.has_last = 0;
-        } else {
-          #pragma unroll 1
-          for (int i = 0; i < n; ++i) c.gamma[i] = gam[i];
-          c.mixed = 1;
+      }
+#pragma unroll
+      for (int i = 0; i < M; ++i)
+        if (i < n) y[i] /= d[i];
+      // back substitution: y[i] -= L[j][i] y[j], j ascending from i + 1
+#pragma unroll
+      for (int i = M - 2; i >= 0; --i) {
+#pragma unroll
+        for (int j = i + 1; j < M; ++j) {
+          const double lji = __shfl_sync(F, L[i], perm[j]);
+          if (i < n && j < n) y[i] -= lji * y[j];
         }
+      }
+#pragma unroll
+      for (int c = 0; c < M; ++c) gam[c] = 0.0;
+#pragma unroll
+      for (int i = 0; i < M; ++i)
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+          if (i < n && c == perm[i]) gam[c] = y[i];
+      bool good = ok;
+#pragma unroll
+      for (int i = 0; i < M; ++i)
+        if (i < n) good = good && isfinite(gam[i]);
+      double gn = 0.0;
+      if (good)
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+          if (i < n) gn += gam[i] * gam[i];
+      if (!good || !(sqrt(gn) <= guard)) {  // guard: discard history (forward.cpp:43-47)
+        count = 0;
+        head = 0;
+        has_last = 0;
+        nsol = 0;
+      } else {
+        mixed = 1;
       }
     }
   }
-writeback:
-  __syncthreads();
-  if (mode == 1 && threadIdx.x == 0) {  // adjoint loop condition (done / error)
-    c.cond = (!c.done && c.err == 0) ? 1 : 0;
-    if (use_handle) cudaGraphSetConditional(handle, c.cond);
-  }
-  __syncthreads();
-  {
-    const int* src = reinterpret_cast<const int*>(&c);
-    int* dst = reinterpret_cast<int*>(gctl);
-    #pragma unroll 1
-    for (int i = threadIdx.x; i < static_cast<int>(sizeof(hdk_ctl) / 4); i += blockDim.x) dst[i] = src[i];
+  if (lane < M)
+#pragma unroll
+    for (int j = 0; j < M; ++j) gctl->gram[lane * M + j] = g[j];
+  if (lane == 0) {
+    if (nsol > 0)
+#pragma unroll
+      for (int i = 0; i < M; ++i)
+        if (i < nsol) gctl->gamma[i] = gam[i];
+    gctl->count = count;
+    gctl->head = head;
+    gctl->has_last = has_last;
+    gctl->mixed = mixed;
+    gctl->k = kk;
+    gctl->iterations = iters;
+    gctl->err = err;
+    gctl->done = done;
+    if (mode == 1) {  // adjoint loop condition (done / error)
+      const int cond = (!done && err == 0) ? 1 : 0;
+      gctl->cond = cond;
+      if (use_handle) cudaGraphSetConditional(handle, cond);
+    }
   }
 }
 
@@ -447,14 +572,11 @@ __global__ void __launch_bounds__(kT) k_aa_dots_fused(hdk_vtx x, hdk_factor f, i
   for (int q = 0; q < 2 * HDK_AA_MAX + 2; ++q) acc[q] = 0.0;
   for (size_t i = blockIdx.x * kT + threadIdx.x; i < n3; i += (size_t)HDK_RED_BLOCKS * kT) {
     const int v = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)v);
-    const int p = __ldg(x.v2p + v);
+    const int2 vf = __ldg(f.vfold + v);
     double th;
-    if (p >= 0) {
-      const int t = p / 256, cl = p - 256 * t;
-      const int b0 = f.tile_cta2 ? __ldg(f.tile_cta2 + 2 * t) : 0;
-      const int b1 = f.tile_cta2 ? __ldg(f.tile_cta2 + 2 * t + 1) : -1;
+    if (vf.y > 0) {  // slots of consecutive CTAs are one tile (256 columns) apart
       th = 0.0;
-      for (int b = b0; b <= b1; ++b) th += __ldcg(f.part2 + 3 * ((size_t)(t + b) * 256 + cl) + a);
+      for (int b = 0; b < vf.y; ++b) th += __ldcg(f.part2 + 3 * ((size_t)vf.x + 256 * (size_t)b) + a);
       qhat[i] = th;
     } else {
       th = qhat[i];
@@ -481,7 +603,8 @@ __global__ void __launch_bounds__(kT) k_aa_dots_fused(hdk_vtx x, hdk_factor f, i
     last_q[i] = qc;
     last_g[i] = g;
   }
-  block_partials<2 * HDK_AA_MAX + 2>(acc, partial);
+  static_assert(2 * HDK_AA_MAX + 2 == 18, "butterfly sized for window 8");
+  block_partials_18(acc, partial);
   // last block folds every partial and runs the coefficient solve
   __shared__ int is_last;
   __threadfence();
@@ -807,7 +930,7 @@ HDK_API int hdk_aa_dots_fused(const hdk_vtx* x, const hdk_factor* f, hdk_ctl* ct
                               unsigned int* ticket, int mode, unsigned long long cond_handle, void* stream) {
   int g1 = 0, g2 = 0;
   hdk_solve_grids(f, &g1, &g2);
-  if (!f->tile_cta2 || g2 != f->grid2) return static_cast<int>(cudaErrorInvalidValue);
+  if (!f->vfold || g2 != f->grid2) return static_cast<int>(cudaErrorInvalidValue);
   hdk::launch(k_aa_dots_fused, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), *x, *f, g2, ctl, qhat, qcur, last_q,
               last_g, dq, dg, partial, ticket, mode, static_cast<cudaGraphConditionalHandle>(cond_handle),
               cond_handle != 0ULL ? 1 : 0);
