@@ -80,6 +80,8 @@ typedef struct hdk_factor {
   const hdk_chunk* chunk;
   const int* tile_chunk;  /* n_tiles+1: first chunk of each tile */
   const int* row_pslot;   /* n+1: partial-dot slots of row r */
+  int n_ztask;
+  const int2* ztask;      /* z-fold warp tasks: {row, -1} one long row, {first row, k} k <= 4 short rows */
   const int* p2v;         /* n: elimination position -> vertex */
   const int* v2p;         /* nv: vertex -> position or -1 (fixed) */
   double* part1;          /* 3*row_pslot[n] scratch */
@@ -114,6 +116,9 @@ HDK_API int hdk_solve_grids(const hdk_factor* f, int* grid1, int* grid2);
 /* Solve passes without the final fold: the tile partials stay in f->part2
  * for hdk_aa_dots_fused. */
 HDK_API int hdk_apply_inverse3_partial(const hdk_factor* f, const double* rhs_perm, void* stream);
+/* Profiling only: hdk_apply_inverse3_partial with passes dropped (bit 0 row
+ * dots, bit 1 z-fold, bit 2 column pass). */
+HDK_API int hdk_apply_inverse3_ablate(const hdk_factor* f, const double* rhs_perm, unsigned skip, void* stream);
 HDK_API int hdk_apply_inverse3_perm(const hdk_factor* f, const double* rhs_perm, double* out_perm, void* stream);
 
 /* Per-element local step (local_solve + the element part of pd_rhs,
@@ -170,6 +175,8 @@ typedef struct hdk_vtx {
   const double* mass;     /* nv */
   const int* inc_off;
   const int* inc;
+  const int* pinc_off;    /* n+1: incidence offsets in elimination order (optional) */
+  const int* pinc;        /* incidence lists concatenated in elimination order */
 } hdk_vtx;
 
 /* q~ = q + h v + h^2 (f_ext + hook) / m; q_cur = q~ with fixed rows pinned to q
@@ -187,6 +194,9 @@ HDK_API int hdk_gather_rhs(const hdk_vtx* x, const double* ef, double inv_h2, co
                            const double* fixcoup, double* b_prev, double* rhs_perm, double* partial, void* stream);
 /* rhs_perm[p] = base[p2v[p]] (+ element forces when ef != NULL). */
 HDK_API int hdk_gather_perm(const hdk_vtx* x, const double* base, const double* ef, double* rhs_perm, void* stream);
+/* rhs_perm[p] = base_perm[p] + element forces, through the elimination-order
+ * incidence (x->pinc_off / x->pinc): one dependent load fewer. */
+HDK_API int hdk_gather_pp(const hdk_vtx* x, const double* base_perm, const double* ef, double* rhs_perm, void* stream);
 /* fixcoup[p] = sum_k A_fd(p, k) q[fixed_k] (solve_free's coupling, factor.cpp:201-205). */
 HDK_API int hdk_fixed_coupling(const hdk_csr* a_fd, const int* fixed, const double* q, double* fixcoup, void* stream);
 /* Type-II Anderson mixing (forward.cpp:17-51) in three launches: history

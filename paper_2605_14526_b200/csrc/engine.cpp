@@ -304,6 +304,24 @@ void Engine::build_factor_device() {
   df_.chunk = ch;
   df_.tile_chunk = A.upload(F.tile_chunk);
   df_.row_pslot = A.upload(F.row_pslot);
+  {  // z-fold warp tasks (solve.cu zfold_task)
+    std::vector<int> zt;
+    for (int r = 0; r < F.n;) {
+      if (F.row_pslot[r + 1] - F.row_pslot[r] > 8) {
+        zt.push_back(r);
+        zt.push_back(-1);
+        ++r;
+        continue;
+      }
+      int k = 0;
+      while (k < 4 && r + k < F.n && F.row_pslot[r + k + 1] - F.row_pslot[r + k] <= 8) ++k;
+      zt.push_back(r);
+      zt.push_back(k);
+      r += k;
+    }
+    df_.n_ztask = static_cast<int>(zt.size() / 2);
+    df_.ztask = reinterpret_cast<const int2*>(A.upload(zt));
+  }
   df_.p2v = A.upload(F.p2v);
   df_.v2p = A.upload(F.v2p);
   df_.part1 = A.alloc<double>(3 * static_cast<size_t>(F.row_pslot.back()));
@@ -375,6 +393,30 @@ void Engine::build_factor_device() {
   dv_.mass = dm_.mass;
   dv_.inc_off = dm_.inc_off;
   dv_.inc = dm_.inc;
+  {  // incidence lists in elimination order (same per-vertex order)
+    const Mesh& m = scene_.mesh;
+    std::vector<int> cnt(m.nv, 0);
+    for (size_t e = 0; e < m.ne; ++e)
+      for (int k = 0; k < 4; ++k) ++cnt[m.el[e][k]];
+    std::vector<int> voff(m.nv + 1, 0);
+    for (int v = 0; v < m.nv; ++v) voff[v + 1] = voff[v] + cnt[v];
+    std::vector<int> vinc(voff[m.nv]);
+    {
+      std::vector<int> cur(voff.begin(), voff.end() - 1);
+      for (size_t e = 0; e < m.ne; ++e)
+        for (int k = 0; k < 4; ++k) vinc[cur[m.el[e][k]]++] = static_cast<int>(4 * e + k);
+    }
+    std::vector<int> poff(F.n + 1, 0), pinc;
+    pinc.reserve(vinc.size());
+    for (int p = 0; p < F.n; ++p) {
+      const int v = F.p2v[p];
+      pinc.insert(pinc.end(), vinc.begin() + voff[v], vinc.begin() + voff[v + 1]);
+      poff[p + 1] = static_cast<int>(pinc.size());
+    }
+    dv_.pinc_off = A.upload(poff);
+    dv_.pinc = A.upload(pinc.empty() ? std::vector<int>{0} : pinc);
+  }
+  seedp_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
 }
 
 void Engine::build_forward_graph() {
@@ -445,6 +487,7 @@ void Engine::build_backward_graph() {
     hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, qbar_, 1.0 / h, vbar_, seed_, s), "seed");
     cuda_check(cudaMemsetAsync(x_, 0, n3 * sizeof(double), st_), "x zero");
     cuda_check(cudaMemsetAsync(t_, 0, n3 * sizeof(double), st_), "t zero");
+    hdk_check(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
     hdk_check(hdk_gather_perm(&dv_, seed_, nullptr, rhs_, s), "x0 rhs");
     hdk_check(hdk_apply_inverse3(&df_, rhs_, x_, s), "x0 solve");
   }, &bk_pre_);
@@ -481,15 +524,21 @@ void Engine::build_backward_graph() {
 void Engine::backbone_body(unsigned long long handle, unsigned skip) {
   void* s = st_;
   if (!(skip & 1u)) hdk_check(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B x");
-  if (!(skip & 2u)) hdk_check(hdk_gather_perm(&dv_, seed_, ef_, rhs_, s), "rhs");
-  if (!(skip & 4u)) hdk_check(hdk_apply_inverse3_partial(&df_, rhs_, s), "solve");
+  if (!(skip & 2u)) hdk_check(hdk_gather_pp(&dv_, seedp_, ef_, rhs_, s), "rhs");
+  if (!(skip & 4u)) hdk_check(hdk_apply_inverse3_ablate(&df_, rhs_, (skip >> 6) & 7u, s), "solve");
   if (!(skip & 8u))
-    hdk_check(hdk_aa_dots_fused(&dv_, &df_, ctl_, t_, x_, lastq_, lastg_, dq_, dg_, part_b_, ticket_, 1, handle, s),
+    hdk_check(hdk_aa_dots_fused(&dv_, &df_, ctl_, t_, x_, lastq_, lastg_, dq_, dg_, part_b_, ticket_,
+                                (skip & 32u) ? 1 | 256 : 1, handle, s),
               "aa dots + solve + cond");
   if (!(skip & 16u)) hdk_check(hdk_aa_mix(&dv_, ctl_, t_, x_, nullptr, nullptr, dq_, dg_, part_c_, 1, s), "aa mix");
 }
 
 double Engine::time_backbone(int reps, unsigned skip) {
+  if (std::getenv("HETERODYN_BODY_DIRECT")) {  // plain stream launches (ncu cannot profile graph
+    for (int i = 0; i < reps; ++i) backbone_body(0ULL, skip);  // nodes that may set a condition)
+    cuda_check(cudaStreamSynchronize(st_), "direct body");
+    return 0.0;
+  }
   cudaGraphExec_t g = capture_exec(st_, [&] { backbone_body(0ULL, skip); }, nullptr);
   cudaEvent_t a, b;
   cuda_check(cudaEventCreate(&a), "event");

@@ -152,7 +152,8 @@ class Engine {
   double *part_a_ = nullptr, *part_b_ = nullptr, *part_c_ = nullptr;
   double* cache_ = nullptr;  // 24 ne projection cache of the current step
   hdk_ctl* ctl_ = nullptr;
-  unsigned int* ticket_ = nullptr;  // last-block ticket of hdk_aa_dots_fused
+  unsigned int* ticket_ = nullptr;
+  double* seedp_ = nullptr;  // adjoint seed in elimination order (3 n)  // last-block ticket of hdk_aa_dots_fused
   hdk_ctl* h_ctl_ = nullptr;  // pinned mirror
   double* hook_ = nullptr;    // 5 doubles device
 

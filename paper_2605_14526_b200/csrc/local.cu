@@ -16,6 +16,8 @@
 // bitwise reproducible (the reference's parallel_for contract, common.hpp:51-55).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "../../include/hdk.h"
 #include "launch.cuh"
 #include "dmath.cuh"
@@ -293,7 +295,12 @@ __global__ void __launch_bounds__(128) k_differential(hdk_mesh m, hdk_material m
 }
 
 // Element force of B x: P = U (D o (U^T F(x) V)) V^T, f_i = P g_i.
-__global__ void __launch_bounds__(128) k_bapply(hdk_mesh m, const double* __restrict__ dcomp, const double* __restrict__ x,
+// Latency-bound (dependent index -> vertex gathers).  The block shape is a
+// template for A/B runs (HETERODYN_BAPPLY): the unbounded 128-thread form
+// (118 registers, more loads in flight per thread) measured faster at C3
+// than register-capped single-wave shapes (10.0 vs 12.3 us per apply).
+template <int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __restrict__ dcomp, const double* __restrict__ x,
                                                  double* __restrict__ ef) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
@@ -414,7 +421,14 @@ HDK_API int hdk_differential(const hdk_mesh* m, const hdk_material* mat, const d
 }
 
 HDK_API int hdk_bapply(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force, void* stream) {
-  hdk::launch(k_bapply, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, dcomp, x, elem_force);
+  static const int variant = [] {
+    const char* v = std::getenv("HETERODYN_BAPPLY");
+    return v ? std::atoi(v) : 0;
+  }();
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (variant == 0) hdk::launch(k_bapply<128, 1>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, elem_force);
+  else if (variant == 2) hdk::launch(k_bapply<128, 6>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, elem_force);
+  else hdk::launch(k_bapply<64, 11>, dim3(blocks(m->ne, 64)), dim3(64), 0, st, *m, dcomp, x, elem_force);
   return static_cast<int>(cudaGetLastError());
 }
 

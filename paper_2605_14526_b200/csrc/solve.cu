@@ -115,6 +115,65 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// z-fold by warp tasks (host-built, hdk_factor::ztask): a task is either one
+// long row (more than 8 tile partials: the separator rows at the top of the
+// elimination tree, up to n/256 partials) folded by a whole warp, or up to
+// four consecutive short rows folded by eight lanes each.  Every lane issues
+// all of its loads before adding, so a task costs one L2 round trip, and
+// tasks are equal-cost, so warps stay balanced (a row-per-8-lanes split left
+// the few long rows as a 4x longer tail).  Fixed lane split and shuffle
+// tree: bitwise reproducible.
+constexpr int kZLong = 3;  // partials per lane held in flight (long rows up to 96 partials per round)
+__device__ __forceinline__ void zfold_task(const hdk_factor& f, int2 task) {
+  const int lane = threadIdx.x & 31;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  int r, stride, s0, s1;
+  bool writer;
+  if (task.y < 0) {  // long row: 32 lanes
+    r = task.x;
+    stride = 32;
+    writer = lane == 0;
+  } else {  // short rows: 8 lanes per row
+    r = task.x + (lane >> 3);
+    stride = 8;
+    writer = (lane & 7) == 0 && (lane >> 3) < task.y;
+  }
+  const bool live = task.y < 0 || (lane >> 3) < task.y;
+  s0 = live ? __ldg(f.row_pslot + r) : 0;
+  s1 = live ? __ldg(f.row_pslot + r + 1) : 0;
+  const int sub = lane & (stride - 1);
+  for (int s = s0 + sub; s < s1; s += kZLong * stride) {
+    double v[kZLong][3];
+#pragma unroll
+    for (int k = 0; k < kZLong; ++k) {
+      const int sk = s + k * stride;
+      const double* p = f.part1 + 3 * (size_t)sk;
+      v[k][0] = sk < s1 ? __ldcg(p) : 0.0;
+      v[k][1] = sk < s1 ? __ldcg(p + 1) : 0.0;
+      v[k][2] = sk < s1 ? __ldcg(p + 2) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kZLong; ++k) {
+      a0 += v[k][0];
+      a1 += v[k][1];
+      a2 += v[k][2];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    if (o >= stride) continue;
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+  }
+  if (writer) {
+    double* z = f.z + 3 * (size_t)r;
+    z[0] = a0;
+    z[1] = a1;
+    z[2] = a2;
+  }
+}
+
 // Balanced contiguous chunk ranges: CTA b of G owns [first(b), first(b+1)).
 __device__ __forceinline__ int range_first(long long b, int G, int C) { return static_cast<int>(b * C / G); }
 // The CTA owning chunk c (G <= C, so no range is empty).
@@ -246,13 +305,17 @@ __device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S>& r, int c_
 }
 
 // ---- pass 1 ------------------------------------------------------------------
+template <bool kDry>
+__device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages1>& ring, const double* __restrict__ rhs,
+                                               int c_beg, int c_end);
+
 template <bool kDry = false>  // kDry: stream only (microbenchmarks)
 __global__ void __launch_bounds__(kThreads, 2) k_rowdot(hdk_factor f, const double* __restrict__ rhs) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<kStages1>& ring = *reinterpret_cast<Ring<kStages1>*>(smem_raw);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5;
   unsigned long long* trace = HDK_TRACE_PTR;
   if (trace && threadIdx.x == 0) trace[2 * blockIdx.x] = globaltimer();
   ring_init(ring);
@@ -262,6 +325,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowdot(hdk_factor f, const doub
     produce(f, ring, c_beg, c_end, false);
     return;
   }
+  rowdot_consume<kDry>(f, ring, rhs, c_beg, c_end);
+  if (trace) {
+    consumers_sync();
+    if (threadIdx.x == 0) trace[2 * blockIdx.x + 1] = globaltimer();
+  }
+}
+
+template <bool kDry>
+__device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages1>& ring, const double* __restrict__ rhs,
+                                               int c_beg, int c_end) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double b0[kM], b1[kM], b2[kM];
   int tile = -1;
   for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
@@ -342,43 +416,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowdot(hdk_factor f, const doub
       if (lane == 0) mbar_arrive(&ring.empty[st]);
     }
   }
-  if (trace) {
-    consumers_sync();
-    if (threadIdx.x == 0) trace[2 * blockIdx.x + 1] = globaltimer();
-  }
 }
 
-// z_r = sum of the row's tile partials in tile order; eight lanes per row,
-// loads issued four at a time before adding.
+// z-fold: one warp per task.  (Folding z in the row-dot kernel's epilogue
+// behind a grid barrier measured 1-2 us slower than this separate launch.)
 __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
-  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = gid >> 3, sub = gid & 7;
-  const bool live = r < f.n;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  if (live) {
-    const int s1 = f.row_pslot[r + 1];
-#pragma unroll 4
-    for (int s = f.row_pslot[r] + sub; s < s1; s += 8) {
-      const double* p = f.part1 + 3 * (size_t)s;
-      a0 += __ldcg(p);
-      a1 += __ldcg(p + 1);
-      a2 += __ldcg(p + 2);
-    }
-  }
-#pragma unroll
-  for (int o = 4; o > 0; o >>= 1) {
-    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-  }
-  if (live && sub == 0) {
-    double* z = f.z + 3 * (size_t)r;
-    z[0] = a0;
-    z[1] = a1;
-    z[2] = a2;
-  }
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t < f.n_ztask) zfold_task(f, __ldg(f.ztask + t));
 }
 
 // ---- pass 2 ------------------------------------------------------------------
@@ -544,7 +590,7 @@ void pick_grids(const hdk_factor* f, int& g1, int& g2) {
 }
 
 int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatter, cudaStream_t st,
-           bool fold = true) {
+           bool fold = true, unsigned skip = 0u) {
   if (f->n <= 0) return 0;
   if (f->tile_w != kW) return static_cast<int>(cudaErrorInvalidValue);
   const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem);
@@ -556,9 +602,9 @@ int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatte
     fl.first2 = nullptr;
     fl.tile_cta2 = nullptr;
   }
-  hdk::launch(k_rowdot<false>, dim3(g1), dim3(kThreads), s1, st, fl, rhs_perm);
-  hdk::launch(k_zreduce, dim3((f->n * 8 + 255) / 256), dim3(256), 0, st, fl);
-  hdk::launch(k_coltile<false>, dim3(g2), dim3(kThreads2), s2, st, fl);
+  if (!(skip & 1u)) hdk::launch(k_rowdot<false>, dim3(g1), dim3(kThreads), s1, st, fl, rhs_perm);
+  if (!(skip & 2u)) hdk::launch(k_zreduce, dim3((f->n_ztask + 7) / 8), dim3(256), 0, st, fl);
+  if (!(skip & 4u)) hdk::launch(k_coltile<false>, dim3(g2), dim3(kThreads2), s2, st, fl);
   if (!fold) return static_cast<int>(cudaGetLastError());
   if (scatter)
     hdk::launch(k_xreduce<true>, dim3((f->n + 255) / 256), dim3(256), 0, st, fl, g2, out);
@@ -585,6 +631,10 @@ HDK_API int hdk_solve_grids(const hdk_factor* f, int* grid1, int* grid2) {
 
 HDK_API int hdk_apply_inverse3_partial(const hdk_factor* f, const double* rhs_perm, void* stream) {
   return launch(f, rhs_perm, nullptr, true, static_cast<cudaStream_t>(stream), false);
+}
+
+HDK_API int hdk_apply_inverse3_ablate(const hdk_factor* f, const double* rhs_perm, unsigned skip, void* stream) {
+  return launch(f, rhs_perm, nullptr, true, static_cast<cudaStream_t>(stream), false, skip);
 }
 
 HDK_API int hdk_apply_inverse3_perm(const hdk_factor* f, const double* rhs_perm, double* out_perm, void* stream) {

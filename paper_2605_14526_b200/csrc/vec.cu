@@ -220,6 +220,39 @@ __global__ void k_gather_perm(hdk_vtx x, const double* __restrict__ base, const 
   }
 }
 
+// k_gather_perm over the elimination-order incidence; same terms, same lane
+// split and fold, so bitwise the same sums.
+__global__ void k_gather_pp(hdk_vtx x, const double* __restrict__ basep, const double* __restrict__ ef,
+                            double* __restrict__ rhs) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = gid >> 3, sub = gid & 7;
+  const bool live = p < x.n;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  if (live) {
+    const int e = __ldg(x.pinc_off + p + 1);
+#pragma unroll 4
+    for (int j = __ldg(x.pinc_off + p) + sub; j < e; j += 8) {
+      const double* q = ef + 3 * (size_t)__ldg(x.pinc + j);
+      s0 += __ldg(q);
+      s1 += __ldg(q + 1);
+      s2 += __ldg(q + 2);
+    }
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (live && sub == 0) {
+    rhs[3 * (size_t)p] = basep[3 * (size_t)p] + s0;
+    rhs[3 * (size_t)p + 1] = basep[3 * (size_t)p + 1] + s1;
+    rhs[3 * (size_t)p + 2] = basep[3 * (size_t)p + 2] + s2;
+  }
+}
+
 __global__ void k_fixed_coupling(hdk_csr c, const int* fixed, const double* q, double* out) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
@@ -605,9 +638,11 @@ __global__ void __launch_bounds__(kT) k_aa_dots_fused(hdk_vtx x, hdk_factor f, i
   }
   static_assert(2 * HDK_AA_MAX + 2 == 18, "butterfly sized for window 8");
   block_partials_18(acc, partial);
-  // last block folds every partial and runs the coefficient solve
+  // last block folds every partial and runs the coefficient solve; only the
+  // partial writers need their stores visible before the ticket
+  if (mode & 256) return;  // profiling ablation: no tail
   __shared__ int is_last;
-  __threadfence();
+  if (threadIdx.x < 18) __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned int t = atomicAdd(ticket, 1u);
@@ -906,6 +941,12 @@ HDK_API int hdk_gather_rhs(const hdk_vtx* x, const double* ef, double inv_h2, co
 
 HDK_API int hdk_gather_perm(const hdk_vtx* x, const double* base, const double* ef, double* rhs_perm, void* stream) {
   hdk::launch(k_gather_perm, dim3(nb(8LL * x->n)), dim3(256), 0, S(stream), *x, base, ef, rhs_perm);
+  return last();
+}
+
+HDK_API int hdk_gather_pp(const hdk_vtx* x, const double* base_perm, const double* ef, double* rhs_perm, void* stream) {
+  if (!x->pinc_off || !x->pinc) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_gather_pp, dim3(nb(8LL * x->n)), dim3(256), 0, S(stream), *x, base_perm, ef, rhs_perm);
   return last();
 }
 

@@ -14,9 +14,12 @@ sim.record(True)
 sim.step()
 sim.backward_canonical(download=False)
 names = {0: "full body", 1: "-Bx", 2: "-gather", 4: "-solve", 8: "-dots/aasolve", 16: "-mix",
-         31 - 4: "solve only", 31: "empty"}
+         32: "-AA tail", 64: "-rowdot", 128: "-zreduce", 256: "-coltile", 31 - 4: "solve only", 31: "empty"}
 base = None
+only = [int(a) for a in sys.argv[2:]]
 for mask, name in names.items():
+    if only and mask not in only and mask != 0:
+        continue
     ms = sim.time_backbone(100, mask)
     if mask == 0:
         base = ms
