@@ -449,14 +449,23 @@ def main():
     stream = torch.cuda.ExternalStream(sim.stream)
 
     contacts = []
+    split = []  # (forward ms, backward ms) per timed step, CUDA events on the engine stream
 
-    def one_step():
+    def one_step(timed=False):
+        if timed:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record(stream)
         sim.record(True)
         sim.step()
         it_f = sim.last_iterations
         contacts.append(sim.last_contact_count)
+        if timed:
+            ev[1].record(stream)
         sim.backward_canonical(download=False)
         sim.record(False)
+        if timed:
+            ev[2].record(stream)
+            split.append(ev)
         return it_f
 
     for _ in range(max(args.warmup, 3)):
@@ -477,13 +486,15 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        fwd_its.append(one_step())
+        fwd_its.append(one_step(timed=True))
         bwd_its.append(lib.lib.hd_sim_backward_iterations(sim.h))
     e1.record(stream)
     e1.synchronize()
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
+    fwd_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in split]))
+    bwd_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in split]))
     launches = sim.kernel_launches - launches0
     solves = sim.solve_count - solves0
     from paper_2605_14526_b200.dist import max_over_ranks, replica_value
@@ -555,6 +566,7 @@ def main():
                        "l2_policy": "inputs larger than L2 (factor values %.0f MB > 126 MB L2)" % (nnz * 8 / 1e6),
                        "mean_forward_iterations": float(np.mean(fwd_its)),
                        "mean_adjoint_iterations": float(np.mean(bwd_its)),
+                       "forward_ms": fwd_ms, "backward_ms": bwd_ms,
                        "solves_per_step": solves / args.steps,
                        "mean_contacts": float(np.mean(contacts[-args.steps:])),
                        "solve_share_of_step_est": step_share},

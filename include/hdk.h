@@ -95,6 +95,7 @@ typedef struct hdk_factor {
   const int* first2;      /* grid2+1: first chunk of pass-2 CTA b */
   const int* tile_cta2;   /* 2*n_tiles: first and last pass-2 CTA touching tile t */
   const int2* vfold;      /* nv: (first tile-partial slot of the vertex's column, slot count; 0 if fixed) */
+  const int2* pfold;      /* n: the same by column (elimination order) */
 } hdk_factor;
 
 /* Scalar CSR in elimination order (a_free / a_free_fixed, factor.hpp:98-99). */
@@ -158,7 +159,7 @@ HDK_API int hdk_damping_elements(const hdk_mesh* m, const double* beta_vh, const
 typedef struct hdk_ctl {
   int k, k_max, iterations, converged;
   int err, done, bad, cond;
-  int window, count, head, has_last, mixed, pad0;
+  int window, count, head, has_last, mixed, nonfinite;  /* nonfinite: set by the backbone mix */
   double eps_rel, eps_abs, guard, tol;
   double gamma[HDK_AA_MAX];
   double gram[HDK_AA_MAX * HDK_AA_MAX];
@@ -214,6 +215,25 @@ HDK_API int hdk_aa_solve(hdk_ctl* ctl, const double* partial, int mode, void* st
 HDK_API int hdk_aa_dots_fused(const hdk_vtx* x, const hdk_factor* f, hdk_ctl* ctl, double* qhat, const double* qcur,
                               double* last_q, double* last_g, double* dq, double* dg, double* partial,
                               unsigned int* ticket, int mode, unsigned long long cond_handle, void* stream);
+/* Profiling: in-graph timeline of the backbone kernels (launch.cuh TraceId).
+ * hdk_trace_install_{local,vec,solve} point each translation unit at a
+ * buffer (NULL: off); hdk_trace_epoch advances its record slot. */
+HDK_API int hdk_trace_install_local(unsigned long long* buf);
+HDK_API int hdk_trace_install_vec(unsigned long long* buf);
+HDK_API int hdk_trace_install_solve(unsigned long long* buf);
+HDK_API int hdk_trace_epoch(unsigned long long* buf, void* stream);
+/* Adjoint backbone in elimination order ([n][3]).  hdk_bb_dots: t folded
+ * from the solve's tile partials by column, Anderson history update and dot
+ * partials; block 0 snapshots ctl into snap.  hdk_bb_mix: every block folds
+ * the partials and runs the coefficient solve from snap (mode 1: convergence
+ * test first), block 0 publishes the new state and the WHILE condition to
+ * ctl; then x <- t - sum gamma (dq + dg), also scattered to x_full. */
+HDK_API int hdk_bb_dots(const hdk_factor* f, hdk_ctl* ctl, hdk_ctl* snap, double* t_perm, const double* x_perm,
+                        double* last_q, double* last_g, double* dq, double* dg, double* partial, int mode,
+                        void* stream);
+HDK_API int hdk_bb_mix(const hdk_factor* f, hdk_ctl* ctl, const hdk_ctl* snap, const double* partial,
+                       const double* t_perm, double* x_perm, double* x_full, const double* dq, const double* dg,
+                       unsigned long long cond_handle, void* stream);
 HDK_API int hdk_aa_mix(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, double* qcur, double* qprev,
                        const double* qpin, const double* dq, const double* dg, double* partial, int mode, void* stream);
 /* Dual gate (forward.cpp:140-146) and loop condition for the graph while node. */

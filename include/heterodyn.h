@@ -171,6 +171,13 @@ HD_API hd_status hd_sim_time_solve(hd_sim* sim, int reps, double* ms_per_solve, 
  * bit 0 B x, bit 1 rhs gather, bit 2 solve passes, bit 3 fused AA dots/solve,
  * bit 4 AA mix.  Results of an ablated body are meaningless; only its time is. */
 HD_API hd_status hd_sim_time_backbone(hd_sim* sim, int reps, unsigned skip_mask, double* ms_per_iteration);
+/* Profiling: timeline of `reps` (<= 16) consecutive backbone iterations in
+ * one graph launch sequence; out receives reps x 12 records (B x, gather, row
+ * dots, z-fold, column pass, AA dots, AA mix: {first CTA resident, first CTA
+ * past its dependency wait, last CTA end}; then five point stamps in the
+ * third field: AA tail entry / folded / solved, AA dots loop done / partials
+ * written) in ns from the earliest stamp. */
+HD_API hd_status hd_sim_trace_backbone(hd_sim* sim, int reps, double* out, size_t capacity);
 
 /* ---- batched system-ID (config C5; new) --------------------------------
  * One process's share of a batch of material-parameter samples.  Sample s

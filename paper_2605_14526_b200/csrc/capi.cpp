@@ -296,6 +296,16 @@ hd_status hd_sim_time_backbone(hd_sim* sim, int reps, unsigned skip_mask, double
   return guarded([&] { *ms = sim->eng->time_backbone(reps, skip_mask); });
 }
 
+hd_status hd_sim_trace_backbone(hd_sim* sim, int reps, double* out, size_t capacity) {
+  if (!sim || !out || reps < 1) return bad_arg("hd_sim_trace_backbone: bad argument");
+  return guarded([&] {
+    std::vector<double> v;
+    sim->eng->trace_backbone(reps, v);
+    if (v.size() > capacity) raise(Code::InvalidArgument, "hd_sim_trace_backbone: capacity too small");
+    std::copy(v.begin(), v.end(), out);
+  });
+}
+
 long long hd_sim_factor_nnz(const hd_sim* sim) { return sim ? sim->eng->factor().row_off.back() : 0; }
 int hd_sim_free_count(const hd_sim* sim) { return sim ? sim->eng->factor().n : 0; }
 long long hd_sim_solve_count(const hd_sim* sim) { return sim ? sim->eng->solve_count : 0; }

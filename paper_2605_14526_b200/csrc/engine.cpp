@@ -214,6 +214,7 @@ void Engine::build_static() {
   cache_ = A.alloc<double>(24 * ne);
   ctl_ = A.alloc<hdk_ctl>(1);
   ticket_ = A.alloc<unsigned int>(1);
+  snap_ = A.alloc<hdk_ctl>(1);
   seed_ = A.alloc<double>(n3);
   x_ = A.alloc<double>(n3);
   t_ = A.alloc<double>(n3);
@@ -354,6 +355,13 @@ void Engine::build_factor_device() {
       vf[2 * v + 1] = tc[2 * t + 1] - tc[2 * t] + 1;
     }
     df_.vfold = reinterpret_cast<const int2*>(A.upload(vf));
+    std::vector<int> pf(2 * static_cast<size_t>(F.n), 0);
+    for (int c = 0; c < F.n; ++c) {
+      const int v = F.p2v[c];
+      pf[2 * c] = vf[2 * v];
+      pf[2 * c + 1] = vf[2 * v + 1];
+    }
+    df_.pfold = reinterpret_cast<const int2*>(A.upload(pf));
   }
   rhs_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
   fixc_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
@@ -417,6 +425,7 @@ void Engine::build_factor_device() {
     dv_.pinc = A.upload(pinc.empty() ? std::vector<int>{0} : pinc);
   }
   seedp_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
+  xp_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
 }
 
 void Engine::build_forward_graph() {
@@ -490,6 +499,7 @@ void Engine::build_backward_graph() {
     hdk_check(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
     hdk_check(hdk_gather_perm(&dv_, seed_, nullptr, rhs_, s), "x0 rhs");
     hdk_check(hdk_apply_inverse3(&df_, rhs_, x_, s), "x0 solve");
+    hdk_check(hdk_gather_perm(&dv_, x_, nullptr, xp_, s), "x0 in elimination order");
   }, &bk_pre_);
   // backbone fixed point x <- A^{-1}(seed + B x) with AA(8) (backward.cpp:170-204)
   auto pre = [&] { hdk_check(hdk_aa_reset(ctl_, HDK_AA_MAX, 1e8, 500, 1e-10, s), "aa reset"); };
@@ -527,10 +537,10 @@ void Engine::backbone_body(unsigned long long handle, unsigned skip) {
   if (!(skip & 2u)) hdk_check(hdk_gather_pp(&dv_, seedp_, ef_, rhs_, s), "rhs");
   if (!(skip & 4u)) hdk_check(hdk_apply_inverse3_ablate(&df_, rhs_, (skip >> 6) & 7u, s), "solve");
   if (!(skip & 8u))
-    hdk_check(hdk_aa_dots_fused(&dv_, &df_, ctl_, t_, x_, lastq_, lastg_, dq_, dg_, part_b_, ticket_,
-                                (skip & 32u) ? 1 | 256 : 1, handle, s),
-              "aa dots + solve + cond");
-  if (!(skip & 16u)) hdk_check(hdk_aa_mix(&dv_, ctl_, t_, x_, nullptr, nullptr, dq_, dg_, part_c_, 1, s), "aa mix");
+    hdk_check(hdk_bb_dots(&df_, ctl_, snap_, t_, xp_, lastq_, lastg_, dq_, dg_, part_b_, 1 | (skip & (512u | 1024u)), s),
+              "aa dots");
+  if (!(skip & 16u))
+    hdk_check(hdk_bb_mix(&df_, ctl_, snap_, part_b_, t_, xp_, x_, dq_, dg_, handle, s), "aa solve + mix + cond");
 }
 
 double Engine::time_backbone(int reps, unsigned skip) {
@@ -556,6 +566,49 @@ double Engine::time_backbone(int reps, unsigned skip) {
   return static_cast<double>(ms) / reps;
 }
 
+// Timeline of `reps` consecutive backbone iterations (profiling): per
+// iteration and kernel {first CTA resident, first CTA past its PDL wait, last
+// CTA end} in ns; out holds reps x kTrCount x 3 values relative to the first.
+void Engine::trace_backbone(int reps, std::vector<double>& out) {
+  constexpr int kSlots = 16, kK = 12;
+  reps = std::max(1, std::min(reps, kSlots));
+  const size_t words = 1 + 3 * static_cast<size_t>(kSlots) * kK;
+  unsigned long long* buf = nullptr;
+  cuda_check(cudaMalloc(&buf, words * 8), "trace buffer");
+  std::vector<unsigned long long> h(words);
+  for (size_t i = 1; i < words; i += 3) {
+    h[i] = ~0ULL;
+    h[i + 1] = ~0ULL;
+    h[i + 2] = 0ULL;
+  }
+  h[0] = kSlots - 1;  // first epoch bump lands on slot 0
+  cuda_check(cudaMemcpy(buf, h.data(), words * 8, cudaMemcpyHostToDevice), "trace init");
+  for (auto inst : {hdk_trace_install_local, hdk_trace_install_vec, hdk_trace_install_solve})
+    hdk_check(inst(buf), "trace install");
+  cudaGraphExec_t g = capture_exec(st_, [&] {
+    hdk_check(hdk_trace_epoch(buf, st_), "trace epoch");
+    const char* sk = std::getenv("HETERODYN_TRACE_SKIP");
+    backbone_body(0ULL, sk ? static_cast<unsigned>(std::atoi(sk)) : 0u);
+  }, nullptr);
+  for (int i = 0; i < reps; ++i) cuda_check(cudaGraphLaunch(g, st_), "traced body");
+  cuda_check(cudaStreamSynchronize(st_), "trace sync");
+  cudaGraphExecDestroy(g);
+  for (auto inst : {hdk_trace_install_local, hdk_trace_install_vec, hdk_trace_install_solve})
+    hdk_check(inst(nullptr), "trace uninstall");
+  cuda_check(cudaMemcpy(h.data(), buf, words * 8, cudaMemcpyDeviceToHost), "trace read");
+  cudaFree(buf);
+  unsigned long long t0 = ~0ULL;
+  for (int r = 0; r < reps; ++r)
+    for (int k = 0; k < kK; ++k) t0 = std::min(t0, h[1 + 3 * (r * kK + k)]);
+  out.assign(static_cast<size_t>(reps) * kK * 3, -1.0);
+  for (int r = 0; r < reps; ++r)
+    for (int k = 0; k < kK; ++k)
+      for (int j = 0; j < 3; ++j) {
+        const unsigned long long v = h[1 + 3 * (r * kK + k) + j];
+        if (v != ~0ULL && v != 0ULL) out[3 * (r * kK + k) + j] = static_cast<double>(v - t0);
+      }
+}
+
 void Engine::sync_ctl() {
   cuda_check(cudaMemcpyAsync(h_ctl_, ctl_, sizeof(hdk_ctl), cudaMemcpyDeviceToHost, st_), "ctl read");
   cuda_check(cudaStreamSynchronize(st_), "stream sync");
@@ -577,6 +630,7 @@ void Engine::run_graph(LoopGraph& g, const char* what) {
 }
 
 void Engine::check_ctl(const char* what) {
+  if (h_ctl_->err == 0 && h_ctl_->nonfinite) h_ctl_->err = 10;  // non-finite backbone iterate
   if (h_ctl_->err != 0) {
     const int c = h_ctl_->err;
     std::string msg = std::string(what) + ": ";

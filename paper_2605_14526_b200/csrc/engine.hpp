@@ -94,6 +94,7 @@ class Engine {
   double time_solve(int reps, double* bytes);
   double time_backbone(int reps, unsigned skip_mask);
   void backbone_body(unsigned long long cond_handle, unsigned skip_mask);
+  void trace_backbone(int reps, std::vector<double>& out);
   Vec solve_free(const double* rhs, const double* fixed_q);
   void set_young(const Vec& young, bool freeze);
 
@@ -153,7 +154,9 @@ class Engine {
   double* cache_ = nullptr;  // 24 ne projection cache of the current step
   hdk_ctl* ctl_ = nullptr;
   unsigned int* ticket_ = nullptr;
-  double* seedp_ = nullptr;  // adjoint seed in elimination order (3 n)  // last-block ticket of hdk_aa_dots_fused
+  hdk_ctl* snap_ = nullptr;  // control-block snapshot of the backbone (hdk_bb_dots -> hdk_bb_mix)
+  double* seedp_ = nullptr;  // adjoint seed in elimination order (3 n)
+  double* xp_ = nullptr;     // backbone iterate in elimination order (3 n); x_ holds it by vertex  // last-block ticket of hdk_aa_dots_fused
   hdk_ctl* h_ctl_ = nullptr;  // pinned mirror
   double* hook_ = nullptr;    // 5 doubles device
 

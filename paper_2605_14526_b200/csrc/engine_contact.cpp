@@ -263,11 +263,12 @@ void Engine::backward_frame(int t, GradOut& out) {
     for (int r = 0; r < k; ++r) {
       hdk_check(hdk_contact_column_init(&c->view, r, nv, df_.v2p, c->U, n, seed_, x_, st_), "column init");
       hdk_check(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, st_), "column seed in elimination order");
+      hdk_check(hdk_gather_perm(&dv_, x_, nullptr, xp_, st_), "column x0 in elimination order");
       run_graph(*bgraph_, "backbone column");
       sync_ctl();
       check_ctl("backward step");
       iters += h_ctl_->iterations;
-      kernel_launches += 2 + bgraph_->counts[0] + static_cast<long long>(bk_body_) * h_ctl_->iterations;
+      kernel_launches += 3 + bgraph_->counts[0] + static_cast<long long>(bk_body_) * h_ctl_->iterations;
       cuda_check(cudaMemcpyAsync(cX_ + n3 * r, x_, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st_), "column");
     }
     ensure_solver_workspace(k);

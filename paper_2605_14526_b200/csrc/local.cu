@@ -20,6 +20,8 @@
 
 #include "../../include/hdk.h"
 #include "launch.cuh"
+
+HDK_TRACE_TU(local)
 #include "dmath.cuh"
 
 using namespace hdk;
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(128) k_differential(hdk_mesh m, hdk_material m
 template <int T, int MINB>
 __global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __restrict__ dcomp, const double* __restrict__ x,
                                                  double* __restrict__ ef) {
-  hdk::pdl_wait();
+  HDK_TRACED_WAIT(hdk::kTrBapply);
   hdk::pdl_trigger();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m.ne) return;

@@ -28,6 +28,8 @@
 #include "../../include/hdk.h"
 #include "launch.cuh"
 
+HDK_TRACE_TU(solve)
+
 namespace {
 
 constexpr int kW = 256;       // tile width (columns)
@@ -148,9 +150,9 @@ __device__ __forceinline__ void zfold_task(const hdk_factor& f, int2 task) {
     for (int k = 0; k < kZLong; ++k) {
       const int sk = s + k * stride;
       const double* p = f.part1 + 3 * (size_t)sk;
-      v[k][0] = sk < s1 ? __ldcg(p) : 0.0;
-      v[k][1] = sk < s1 ? __ldcg(p + 1) : 0.0;
-      v[k][2] = sk < s1 ? __ldcg(p + 2) : 0.0;
+      v[k][0] = sk < s1 ? __ldg(p) : 0.0;
+      v[k][1] = sk < s1 ? __ldg(p + 1) : 0.0;
+      v[k][2] = sk < s1 ? __ldg(p + 2) : 0.0;
     }
 #pragma unroll
     for (int k = 0; k < kZLong; ++k) {
@@ -311,7 +313,7 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages
 
 template <bool kDry = false>  // kDry: stream only (microbenchmarks)
 __global__ void __launch_bounds__(kThreads, 2) k_rowdot(hdk_factor f, const double* __restrict__ rhs) {
-  hdk::pdl_wait();
+  HDK_TRACED_WAIT(hdk::kTrRowdot);
   hdk::pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<kStages1>& ring = *reinterpret_cast<Ring<kStages1>*>(smem_raw);
@@ -421,7 +423,7 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages
 // z-fold: one warp per task.  (Folding z in the row-dot kernel's epilogue
 // behind a grid barrier measured 1-2 us slower than this separate launch.)
 __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
-  hdk::pdl_wait();
+  HDK_TRACED_WAIT(hdk::kTrZfold);
   hdk::pdl_trigger();
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t < f.n_ztask) zfold_task(f, __ldg(f.ztask + t));
@@ -476,7 +478,7 @@ __device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& s
 
 template <bool kDry = false>
 __global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
-  hdk::pdl_wait();
+  HDK_TRACED_WAIT(hdk::kTrColtile);
   hdk::pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Pass2Smem& sm = *reinterpret_cast<Pass2Smem*>(smem_raw);

@@ -16,6 +16,8 @@
 #include "../../include/hdk.h"
 #include "launch.cuh"
 
+HDK_TRACE_TU(vec)
+
 namespace {
 
 constexpr int kT = 256;
@@ -40,7 +42,8 @@ __device__ __forceinline__ void block_partials(double (&v)[NQ], double* partial)
   }
 }
 
-// Same contract as block_partials for many quantities: a reduce-scatter
+// Block partials of the 18 Anderson quantities, stored quantity-major
+// (partial[q * HDK_RED_BLOCKS + block], read by aa_solve_block).  A reduce-scatter
 // butterfly halves the list each level (18 -> 9 -> 5 -> 3 -> 2 -> 1: 20
 // shuffles instead of 18 x 5), after which lane l owns the warp sum of
 // quantity q(l); fixed lane/level order, so bitwise reproducible.
@@ -80,7 +83,7 @@ __device__ __forceinline__ void block_partials_18(const double (&v)[18], double*
     double t = 0.0;
 #pragma unroll
     for (int w = 0; w < kT / 32; ++w) t += sm[w][threadIdx.x];
-    partial[blockIdx.x * HDK_RED_Q + threadIdx.x] = t;
+    partial[threadIdx.x * HDK_RED_BLOCKS + blockIdx.x] = t;  // quantity-major: coalesced folds
   }
 }
 
@@ -97,7 +100,7 @@ __device__ __forceinline__ void fold_all(const double* __restrict__ partial, int
 #pragma unroll
     for (int i = 0; i < kFoldPerLane; ++i) {
       const int b = lane + 32 * i;
-      v[i] = b < HDK_RED_BLOCKS ? __ldcg(partial + b * HDK_RED_Q + q) : 0.0;
+      v[i] = b < HDK_RED_BLOCKS ? __ldg(partial + b * HDK_RED_Q + q) : 0.0;
     }
     double s = 0.0;
 #pragma unroll
@@ -224,7 +227,7 @@ __global__ void k_gather_perm(hdk_vtx x, const double* __restrict__ base, const 
 // split and fold, so bitwise the same sums.
 __global__ void k_gather_pp(hdk_vtx x, const double* __restrict__ basep, const double* __restrict__ ef,
                             double* __restrict__ rhs) {
-  hdk::pdl_wait();
+  HDK_TRACED_WAIT(hdk::kTrGather);
   hdk::pdl_trigger();
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int p = gid >> 3, sub = gid & 7;
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(kT) k_aa_dots(hdk_vtx x, const hdk_ctl* ctl, c
     last_q[i] = qc;
     last_g[i] = g;
   }
-  block_partials<2 * HDK_AA_MAX + 2>(acc, partial);
+  block_partials_18(acc, partial);
 }
 
 // Anderson coefficient solve (forward.cpp:31-47): M gamma = DG^T g with
@@ -328,8 +331,19 @@ __global__ void __launch_bounds__(kT) k_aa_dots(hdk_vtx x, const hdk_ctl* ctl, c
 // sets the WHILE condition (graph handle given).
 constexpr int kSolveT = kT;
 constexpr int kNQ = 2 * HDK_AA_MAX + 2;
-__device__ __noinline__ void aa_solve_block(hdk_ctl* gctl, const double* __restrict__ partial, int mode,
-                                            cudaGraphConditionalHandle handle, int use_handle) {
+// What the mixing step of the calling block needs from the solve (shared).
+struct AaResult {
+  double gamma[HDK_AA_MAX];
+  int done, mixed, count, head, window, err;
+};
+
+// State is read from `in` and the updated state written to `out` (NULL: not
+// written), so a kernel whose every block solves redundantly can read a
+// snapshot while one block publishes (k_bb_mix).  `res` (shared memory,
+// optional) receives the mixing inputs for the calling block.
+__device__ __noinline__ void aa_solve_block(const hdk_ctl* in, hdk_ctl* gctl, const double* partial, int mode,
+                                            cudaGraphConditionalHandle handle, int use_handle,
+                                            AaResult* res = nullptr) {
   constexpr int M = HDK_AA_MAX;
   __shared__ double s[kNQ];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -338,11 +352,11 @@ __device__ __noinline__ void aa_solve_block(hdk_ctl* gctl, const double* __restr
   double tol = 0.0, guard = 0.0;
   double g[M];
   if (warp == 0) {
-    m = gctl->window; count = gctl->count; head = gctl->head; has_last = gctl->has_last; mixed = gctl->mixed;
-    kk = gctl->k; iters = gctl->iterations; err = gctl->err; done = gctl->done; k_max = gctl->k_max;
-    tol = gctl->tol; guard = gctl->guard;
+    m = in->window; count = in->count; head = in->head; has_last = in->has_last; mixed = in->mixed;
+    kk = in->k; iters = in->iterations; err = in->err; done = in->done; k_max = in->k_max;
+    tol = in->tol; guard = in->guard;
 #pragma unroll
-    for (int j = 0; j < M; ++j) g[j] = lane < M ? gctl->gram[lane * M + j] : 0.0;
+    for (int j = 0; j < M; ++j) g[j] = lane < M ? in->gram[lane * M + j] : 0.0;
   }
   {  // fold: warp w owns quantities w, w + 8, w + 16; all loads issued first
     constexpr int R = (kNQ + kT / 32 - 1) / (kT / 32);
@@ -353,7 +367,7 @@ __device__ __noinline__ void aa_solve_block(hdk_ctl* gctl, const double* __restr
 #pragma unroll
       for (int i = 0; i < kFoldPerLane; ++i) {
         const int b = lane + 32 * i;
-        v[r][i] = (q < kNQ && b < HDK_RED_BLOCKS) ? __ldcg(partial + b * HDK_RED_Q + q) : 0.0;
+        v[r][i] = (q < kNQ && b < HDK_RED_BLOCKS) ? partial[q * HDK_RED_BLOCKS + b] : 0.0;
       }
     }
 #pragma unroll
@@ -368,6 +382,7 @@ __device__ __noinline__ void aa_solve_block(hdk_ctl* gctl, const double* __restr
     }
   }
   __syncthreads();
+  hdk::trace_stamp(g_hdk_trace, hdk::kTrTail1);
   if (warp != 0) return;
   const unsigned F = 0xffffffffu;
   bool skip = false;
@@ -386,6 +401,8 @@ __device__ __noinline__ void aa_solve_block(hdk_ctl* gctl, const double* __restr
   }
   int nsol = 0;
   double gam[M];
+#pragma unroll
+  for (int c = 0; c < M; ++c) gam[c] = 0.0;
   if (!skip) {
     if (has_last) {
       if (count < m) {
@@ -546,6 +563,18 @@ __device__ __noinline__ void aa_solve_block(hdk_ctl* gctl, const double* __restr
       }
     }
   }
+  hdk::trace_stamp(g_hdk_trace, hdk::kTrTail2);
+  if (res && lane == 0) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) res->gamma[i] = gam[i];
+    res->done = done;
+    res->mixed = mixed;
+    res->count = count;
+    res->head = head;
+    res->window = m;
+    res->err = err;
+  }
+  if (!gctl) return;
   if (lane < M)
 #pragma unroll
     for (int j = 0; j < M; ++j) gctl->gram[lane * M + j] = g[j];
@@ -573,7 +602,7 @@ __device__ __noinline__ void aa_solve_block(hdk_ctl* gctl, const double* __restr
 __global__ void __launch_bounds__(kSolveT) k_aa_solve(hdk_ctl* gctl, const double* partial, int mode) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
-  aa_solve_block(gctl, partial, mode, 0, 0);
+  aa_solve_block(gctl, gctl, partial, mode, 0, 0);
 }
 
 // Fused tail of one PD / adjoint iteration after the solve's column pass:
@@ -609,7 +638,7 @@ __global__ void __launch_bounds__(kT) k_aa_dots_fused(hdk_vtx x, hdk_factor f, i
     double th;
     if (vf.y > 0) {  // slots of consecutive CTAs are one tile (256 columns) apart
       th = 0.0;
-      for (int b = 0; b < vf.y; ++b) th += __ldcg(f.part2 + 3 * ((size_t)vf.x + 256 * (size_t)b) + a);
+      for (int b = 0; b < vf.y; ++b) th += __ldg(f.part2 + 3 * ((size_t)vf.x + 256 * (size_t)b) + a);
       qhat[i] = th;
     } else {
       th = qhat[i];
@@ -652,7 +681,157 @@ __global__ void __launch_bounds__(kT) k_aa_dots_fused(hdk_vtx x, hdk_factor f, i
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  aa_solve_block(ctl, partial, mode, handle, use_handle);
+  aa_solve_block(ctl, ctl, partial, mode, handle, use_handle);
+}
+
+__global__ void k_trace_epoch(unsigned long long* buf) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  buf[0] += 1ULL;
+}
+
+// True in the block that arrives last.  The CTA barrier orders every
+// thread's partial stores before thread 0's acq_rel ticket (release), and the
+// last block's acquire orders its later loads of the others' partials — one
+// L2 round trip instead of an SC fence plus an atomic.
+__device__ __forceinline__ bool last_block_ticket(unsigned int* ticket) {
+  __shared__ int is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(ticket) : "memory");
+    is_last = t == gridDim.x - 1;
+    if (is_last) asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(ticket) : "memory");
+  }
+  __syncthreads();
+  return is_last != 0;
+}
+
+// ---- adjoint backbone in elimination order -----------------------------------
+// The backbone's Anderson vectors (t, x, last, history) live in elimination
+// order [n][3]: the solve's tile partials fold into t with contiguous loads,
+// and every Anderson access is coalesced with no vertex indirection.  Fixed
+// vertices carry t = x = 0 in the backbone (they contribute nothing to any
+// dot product), so dropping them changes no value, only the summation order.
+__global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ctl, hdk_ctl* snap, double* __restrict__ tp,
+                                                const double* __restrict__ xp, double* last_q, double* last_g,
+                                                double* dq, double* dg, double* partial, int mode) {
+  HDK_TRACED_WAIT(hdk::kTrDots);
+  hdk::pdl_trigger();
+  const size_t n3 = 3 * (size_t)n;
+  if (blockIdx.x == 0) {  // snapshot of the control block for k_bb_mix (which rewrites ctl)
+    if (threadIdx.x == 0 && ctl->nonfinite && ctl->err == 0) ctl->err = 10;  // AdjointDiverged
+    __syncthreads();
+    const int* src = reinterpret_cast<const int*>(ctl);
+    int* dst = reinterpret_cast<int*>(snap);
+    for (int w = threadIdx.x; w < static_cast<int>(sizeof(hdk_ctl) / 4); w += kT) dst[w] = src[w];
+  }
+  const int m = ctl->window, c = ctl->count, h = ctl->head;
+  const bool push = ctl->has_last != 0;
+  int ns = 0, c2 = c, h2 = h;
+  if (push) {
+    ns = c < m ? (h + c) % m : h;
+    c2 = c < m ? c + 1 : m;
+    h2 = c < m ? h : (h + 1) % m;
+  }
+  if (mode & 512) c2 = 0;  // profiling ablation
+  int ph[HDK_AA_MAX];
+#pragma unroll
+  for (int j = 0; j < HDK_AA_MAX; ++j) ph[j] = (h2 + j) % m;
+  double acc[2 * HDK_AA_MAX + 2];
+#pragma unroll
+  for (int q = 0; q < 2 * HDK_AA_MAX + 2; ++q) acc[q] = 0.0;
+  const unsigned long long pol = hdk::pol_keep();
+  for (size_t i = blockIdx.x * kT + threadIdx.x; i < n3; i += (size_t)HDK_RED_BLOCKS * kT) {
+    const int col = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)col);
+    const int tile = col >> 8;  // tile_cta2 is tiny and L1-resident (pfold would be an L2 round trip)
+    const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
+    int2 pf = make_int2((tile + tb0) * 256 + (col & 255), tb1 - tb0 + 1);
+    double th = 0.0;
+    if (mode & 1024) pf.y = 0;  // profiling ablation
+    for (int b0 = 0; b0 < pf.y; b0 += 4) {  // loads first, then the fixed-order adds
+      double v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        v[k] = b0 + k < pf.y ? __ldg(f.part2 + 3 * ((size_t)pf.x + 256 * (size_t)(b0 + k)) + a) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (b0 + k < pf.y) th += v[k];
+    }
+    hdk::st_keep(tp + i, th, pol);
+    const double qc = hdk::ld_keep(xp + i, pol);
+    const double g = th - qc;
+    acc[2 * HDK_AA_MAX] += g * g;
+    acc[2 * HDK_AA_MAX + 1] += th * th;
+    if (push) {
+      const double dqn = qc - hdk::ld_keep(last_q + i, pol);
+      const double dgn = g - hdk::ld_keep(last_g + i, pol);
+      hdk::st_keep(dq + ns * n3 + i, dqn, pol);
+      hdk::st_keep(dg + ns * n3 + i, dgn, pol);
+#pragma unroll
+      for (int j = 0; j < HDK_AA_MAX; ++j) {
+        if (j < c2) {
+          const double dgj = ph[j] == ns ? dgn : hdk::ld_keep(dg + ph[j] * n3 + i, pol);
+          acc[j] += dgn * dgj;
+          acc[HDK_AA_MAX + j] += dgj * g;
+        }
+      }
+    }
+    hdk::st_keep(last_q + i, qc, pol);
+    hdk::st_keep(last_g + i, g, pol);
+  }
+  static_assert(2 * HDK_AA_MAX + 2 == 18, "butterfly sized for window 8");
+  hdk::trace_stamp(g_hdk_trace, hdk::kTrDotsA);
+  block_partials_18(acc, partial);
+  hdk::trace_stamp(g_hdk_trace, hdk::kTrDotsB);
+}
+
+// x <- t - sum_j gamma_j (dq_j + dg_j) in elimination order, also scattered to
+// the full vertex vector the element kernels read.
+// Every block folds the dot partials and solves the Anderson system itself
+// (identical inputs, identical code: identical results) from the snapshot
+// k_bb_dots took, so no block waits on a last-block tail; block 0 publishes
+// the new state (and the WHILE condition) to ctl, which no block of this
+// launch reads.
+__global__ void __launch_bounds__(kT) k_bb_mix(int n, const int* __restrict__ p2v, hdk_ctl* ctl, const hdk_ctl* snap,
+                                               const double* partial, const double* __restrict__ tp, double* xp,
+                                               double* __restrict__ xv, const double* __restrict__ dq,
+                                               const double* __restrict__ dg, cudaGraphConditionalHandle handle,
+                                               int use_handle) {
+  HDK_TRACED_WAIT(hdk::kTrMix);
+  hdk::pdl_trigger();
+  const size_t n3 = 3 * (size_t)n;
+  __shared__ AaResult res;
+  aa_solve_block(snap, blockIdx.x == 0 ? ctl : nullptr, partial, 1, handle, use_handle, &res);
+  __syncthreads();
+  const bool done = res.done;
+  const int mixed = res.mixed, c = res.count, h = res.head, m = res.window;
+  double gam[HDK_AA_MAX];
+  int ph[HDK_AA_MAX];
+#pragma unroll
+  for (int j = 0; j < HDK_AA_MAX; ++j) {
+    gam[j] = j < c ? res.gamma[j] : 0.0;
+    ph[j] = (h + j) % m;
+  }
+  bool finite = true;
+  const size_t i = blockIdx.x * (size_t)kT + threadIdx.x;
+  if (i < n3) {
+    const unsigned long long pol = hdk::pol_keep();
+    const double qc = hdk::ld_keep(xp + i, pol), th = hdk::ld_keep(tp + i, pol);
+    double out = qc + (th - qc);
+    if (done) {
+      out = th;
+    } else if (mixed) {
+#pragma unroll
+      for (int j = 0; j < HDK_AA_MAX; ++j)
+        if (j < c) out -= gam[j] * (hdk::ld_keep(dq + ph[j] * n3 + i, pol) + hdk::ld_keep(dg + ph[j] * n3 + i, pol));
+    }
+    finite = isfinite(out);
+    hdk::st_keep(xp + i, out, pol);
+    const int col = static_cast<int>(i / 3);
+    xv[3 * (size_t)__ldg(p2v + col) + (i - 3 * (size_t)col)] = out;
+  }
+  if (!finite) atomicOr(&ctl->nonfinite, 1);
 }
 
 __global__ void __launch_bounds__(kT) k_aa_mix(hdk_vtx x, hdk_ctl* ctl, const double* __restrict__ qhat, double* qcur,
@@ -884,7 +1063,7 @@ __global__ void k_ctl_init(hdk_ctl* c, int window, double guard, int k_max, doub
   hdk::pdl_trigger();
   c->k = 0; c->k_max = k_max; c->iterations = it0; c->converged = 0;
   c->err = 0; c->done = 0; c->bad = 0; c->cond = 1;
-  c->window = window < 1 ? 1 : window; c->count = 0; c->head = 0; c->has_last = 0; c->mixed = 0;
+  c->window = window < 1 ? 1 : window; c->count = 0; c->head = 0; c->has_last = 0; c->mixed = 0; c->nonfinite = 0;
   c->eps_rel = er; c->eps_abs = ea; c->guard = guard; c->tol = tol;
   c->tau = 1.0; c->rho = 1.0; c->model = 0.0; c->eps_tr = eps_tr;
   for (int i = 0; i < HDK_AA_MAX; ++i) c->gamma[i] = 0.0;
@@ -896,7 +1075,7 @@ __global__ void k_aa_reset(hdk_ctl* c, int window, double guard, int k_max, doub
   hdk::pdl_wait();
   hdk::pdl_trigger();
   c->k = 0; c->k_max = k_max; c->iterations = 0; c->converged = 0; c->done = 0; c->cond = 1;
-  c->window = window < 1 ? 1 : window; c->count = 0; c->head = 0; c->has_last = 0; c->mixed = 0;
+  c->window = window < 1 ? 1 : window; c->count = 0; c->head = 0; c->has_last = 0; c->mixed = 0; c->nonfinite = 0;
   c->guard = guard; c->tol = tol;
 }
 
@@ -975,6 +1154,30 @@ HDK_API int hdk_aa_dots_fused(const hdk_vtx* x, const hdk_factor* f, hdk_ctl* ct
   hdk::launch(k_aa_dots_fused, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), *x, *f, g2, ctl, qhat, qcur, last_q,
               last_g, dq, dg, partial, ticket, mode, static_cast<cudaGraphConditionalHandle>(cond_handle),
               cond_handle != 0ULL ? 1 : 0);
+  return last();
+}
+
+HDK_API int hdk_trace_epoch(unsigned long long* buf, void* stream) {
+  hdk::launch(k_trace_epoch, dim3(1), dim3(1), 0, S(stream), buf);
+  return last();
+}
+
+HDK_API int hdk_bb_dots(const hdk_factor* f, hdk_ctl* ctl, hdk_ctl* snap, double* t_perm, const double* x_perm,
+                        double* last_q, double* last_g, double* dq, double* dg, double* partial, int mode,
+                        void* stream) {
+  int g1 = 0, g2 = 0;
+  hdk_solve_grids(f, &g1, &g2);
+  if (!f->tile_cta2 || g2 != f->grid2) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_bb_dots, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), f->n, *f, ctl, snap, t_perm, x_perm, last_q,
+              last_g, dq, dg, partial, mode);
+  return last();
+}
+
+HDK_API int hdk_bb_mix(const hdk_factor* f, hdk_ctl* ctl, const hdk_ctl* snap, const double* partial,
+                       const double* t_perm, double* x_perm, double* x_full, const double* dq, const double* dg,
+                       unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_bb_mix, dim3(nb(3LL * f->n)), dim3(kT), 0, S(stream), f->n, f->p2v, ctl, snap, partial, t_perm, x_perm,
+              x_full, dq, dg, static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle != 0ULL ? 1 : 0);
   return last();
 }
 
