@@ -73,6 +73,8 @@ typedef struct hdk_factor {
   int tile_w, n_tiles, n_chunks;
   int max_ctas;           /* part2 holds (n_tiles + max_ctas) tile partials */
   int l2_hint;            /* 1: stream the values with an L2 evict_first policy */
+  const int* run_flag;    /* optional: the passes do nothing while *run_flag == 0 (an unrolled
+                             iteration past convergence) */
   int grid_cap;           /* 0: one resident wave per pass; else at most this many CTAs per pass
                              (lets concurrent samples of a batch share the SMs) */
   const double* sval;     /* tile-major value stream */
@@ -141,6 +143,9 @@ HDK_API int hdk_differential(const hdk_mesh* m, const hdk_material* mat, const d
                              double* dcomp, int* err, void* stream);
 /* Element forces of B x (matrix-free assemble_db_dq + apply, backward.cpp:117-163). */
 HDK_API int hdk_bapply(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force, void* stream);
+/* hdk_bapply that does nothing while *run_flag == 0 (unrolled backbone). */
+HDK_API int hdk_bapply_flag(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
+                            const int* run_flag, void* stream);
 /* Per-element dL/dw (accumulated into dl_dw), dL/dE (accumulated into dl_de)
  * and the damping element force of mu (backward.cpp:311, 361-391). */
 HDK_API int hdk_route_elements(const hdk_mesh* m, const hdk_material* mat, const double* cache, const double* q_star,
@@ -195,9 +200,10 @@ HDK_API int hdk_gather_rhs(const hdk_vtx* x, const double* ef, double inv_h2, co
                            const double* fixcoup, double* b_prev, double* rhs_perm, double* partial, void* stream);
 /* rhs_perm[p] = base[p2v[p]] (+ element forces when ef != NULL). */
 HDK_API int hdk_gather_perm(const hdk_vtx* x, const double* base, const double* ef, double* rhs_perm, void* stream);
-/* rhs_perm[p] = base_perm[p] + element forces, through the elimination-order
- * incidence (x->pinc_off / x->pinc): one dependent load fewer. */
-HDK_API int hdk_gather_pp(const hdk_vtx* x, const double* base_perm, const double* ef, double* rhs_perm, void* stream);
+/* rhs_perm[p] = base_perm[p] (0 if base_perm is NULL) + element forces,
+ * through the elimination-order incidence (x->pinc_off / x->pinc). */
+HDK_API int hdk_gather_pp(const hdk_vtx* x, const double* base_perm, const double* ef, double* rhs_perm,
+                          const int* run_flag, void* stream);
 /* fixcoup[p] = sum_k A_fd(p, k) q[fixed_k] (solve_free's coupling, factor.cpp:201-205). */
 HDK_API int hdk_fixed_coupling(const hdk_csr* a_fd, const int* fixed, const double* q, double* fixcoup, void* stream);
 /* Type-II Anderson mixing (forward.cpp:17-51) in three launches: history
@@ -222,18 +228,28 @@ HDK_API int hdk_trace_install_local(unsigned long long* buf);
 HDK_API int hdk_trace_install_vec(unsigned long long* buf);
 HDK_API int hdk_trace_install_solve(unsigned long long* buf);
 HDK_API int hdk_trace_epoch(unsigned long long* buf, void* stream);
-/* Adjoint backbone in elimination order ([n][3]).  hdk_bb_dots: t folded
- * from the solve's tile partials by column, Anderson history update and dot
- * partials; block 0 snapshots ctl into snap.  hdk_bb_mix: every block folds
- * the partials and runs the coefficient solve from snap (mode 1: convergence
- * test first), block 0 publishes the new state and the WHILE condition to
- * ctl; then x <- t - sum gamma (dq + dg), also scattered to x_full. */
-HDK_API int hdk_bb_dots(const hdk_factor* f, hdk_ctl* ctl, hdk_ctl* snap, double* t_perm, const double* x_perm,
-                        double* last_q, double* last_g, double* dq, double* dg, double* partial, int mode,
-                        void* stream);
-HDK_API int hdk_bb_mix(const hdk_factor* f, hdk_ctl* ctl, const hdk_ctl* snap, const double* partial,
-                       const double* t_perm, double* x_perm, double* x_full, const double* dq, const double* dg,
-                       unsigned long long cond_handle, void* stream);
+/* Adjoint backbone in elimination order ([n][3]), one iteration =
+ *   solve -> hdk_bb_dots -> { hdk_bb_solve || B t, gather } -> hdk_bb_mix.
+ * hdk_bb_dots: t folded from the solve's tile partials by column (also
+ * written by vertex to t_full), Anderson history update and dot partials;
+ * block 0 snapshots ctl into snap.  hdk_bb_solve (1 block): coefficient
+ * solve from snap (convergence test first), publishes the new state and the
+ * WHILE condition to ctl, the mixing inputs to `result`
+ * (hdk_bb_result_bytes()).  The x-space ring `dq` of hdk_bb_dots holds
+ * s_j = dq_j + dg_j (sum_hist), `dg` holds dg_j.  hdk_bb_mix: x <- t -
+ * sum gamma s_j and, by linearity, R(x) <- R(t) - sum gamma R(s_j) with
+ * R = gather o B (rt_perm = R(t) from the branch; rsum_hist = R(s_j));
+ * rhs_perm = seed_perm + R(x). */
+HDK_API int hdk_bb_dots(const hdk_factor* f, hdk_ctl* ctl, hdk_ctl* snap, double* t_perm, double* t_full,
+                        const double* x_perm, double* last_q, double* last_g, double* dq, double* dg, double* partial,
+                        int mode, void* stream);
+HDK_API int hdk_bb_solve(hdk_ctl* ctl, const hdk_ctl* snap, const double* partial, void* result,
+                         unsigned long long cond_handle, void* stream);
+HDK_API size_t hdk_bb_result_bytes(void);
+HDK_API int hdk_bb_mix(const hdk_factor* f, hdk_ctl* ctl, const hdk_ctl* snap, const void* result,
+                       const double* t_perm, double* x_perm, double* x_full, const double* sum_hist,
+                       const double* rt_perm, double* rx_perm, double* last_rx, double* last_rg, double* rsum_hist,
+                       const double* seed_perm, double* rhs_perm, void* stream);
 HDK_API int hdk_aa_mix(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, double* qcur, double* qprev,
                        const double* qpin, const double* dq, const double* dg, double* partial, int mode, void* stream);
 /* Dual gate (forward.cpp:140-146) and loop condition for the graph while node. */

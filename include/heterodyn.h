@@ -172,12 +172,18 @@ HD_API hd_status hd_sim_time_solve(hd_sim* sim, int reps, double* ms_per_solve, 
  * bit 4 AA mix.  Results of an ablated body are meaningless; only its time is. */
 HD_API hd_status hd_sim_time_backbone(hd_sim* sim, int reps, unsigned skip_mask, double* ms_per_iteration);
 /* Profiling: timeline of `reps` (<= 16) consecutive backbone iterations in
- * one graph launch sequence; out receives reps x 12 records (B x, gather, row
+ * one graph launch sequence; out receives reps x 14 records (B x, gather, row
  * dots, z-fold, column pass, AA dots, AA mix: {first CTA resident, first CTA
- * past its dependency wait, last CTA end}; then five point stamps in the
- * third field: AA tail entry / folded / solved, AA dots loop done / partials
- * written) in ns from the earliest stamp. */
+ * past its dependency wait, last CTA end}; then seven point stamps in the
+ * third field: AA solve entry / folded / solved, AA dots loop done / partials
+ * written, AA bookkeeping done / factorization done) in ns from the earliest
+ * stamp. */
 HD_API hd_status hd_sim_trace_backbone(hd_sim* sim, int reps, double* out, size_t capacity);
+/* Profiling: the same records for the real backbone loop of one forward +
+ * backward step from the current state (state restored afterwards): the
+ * last min(iterations, 16) iterations, oldest first; *iterations receives
+ * how many records were written. */
+HD_API hd_status hd_sim_trace_loop(hd_sim* sim, double* out, size_t capacity, int* iterations);
 
 /* ---- batched system-ID (config C5; new) --------------------------------
  * One process's share of a batch of material-parameter samples.  Sample s

@@ -318,6 +318,9 @@ hd_status hd_sim_backward_canonical(hd_sim* sim, double* dl_dq0, double* dl_dv0,
 }
 void* hd_sim_stream(const hd_sim*) { return nullptr; }
 long long hd_sim_kernel_launches(const hd_sim*) { return 0; }
+hd_status hd_sim_trace_loop(hd_sim*, double*, size_t, int*) {
+  return null_arg("hd_sim_trace_loop: GPU profiling only");
+}
 hd_status hd_sim_trace_backbone(hd_sim*, int, double*, size_t) {
   return null_arg("hd_sim_trace_backbone: GPU profiling only");
 }

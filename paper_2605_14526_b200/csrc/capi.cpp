@@ -306,6 +306,17 @@ hd_status hd_sim_trace_backbone(hd_sim* sim, int reps, double* out, size_t capac
   });
 }
 
+hd_status hd_sim_trace_loop(hd_sim* sim, double* out, size_t capacity, int* iterations) {
+  if (!sim || !out) return bad_arg("hd_sim_trace_loop: bad argument");
+  return guarded([&] {
+    std::vector<double> v;
+    sim->eng->trace_loop(v);
+    if (v.size() > capacity) raise(Code::InvalidArgument, "hd_sim_trace_loop: capacity too small");
+    std::copy(v.begin(), v.end(), out);
+    if (iterations) *iterations = static_cast<int>(v.size() / 42);
+  });
+}
+
 long long hd_sim_factor_nnz(const hd_sim* sim) { return sim ? sim->eng->factor().row_off.back() : 0; }
 int hd_sim_free_count(const hd_sim* sim) { return sim ? sim->eng->factor().n : 0; }
 long long hd_sim_solve_count(const hd_sim* sim) { return sim ? sim->eng->solve_count : 0; }

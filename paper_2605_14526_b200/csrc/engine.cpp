@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 
@@ -128,6 +129,7 @@ cudaGraphExec_t capture_exec(cudaStream_t st, const std::function<void()>& fn, i
 Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas)
     : scene_(scene), mat_(scene.material), solve_ctas_(solve_ctas) {
   if (const char* c = std::getenv("HETERODYN_SOLVE_CTAS")) solve_ctas_ = std::atoi(c);
+  if (const char* u = std::getenv("HETERODYN_UNROLL")) unroll_ = std::max(1, std::atoi(u));
   if (young) mat_.set_young(*young, scene.mesh.vol);
   const char* nc = std::getenv("HETERODYN_NO_COND_GRAPH");
   use_cond_ = !(nc && std::atoi(nc) != 0);
@@ -135,7 +137,14 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas)
   if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
     raise(Code::InvalidArgument, "no CUDA device: the B200 engine has no CPU fallback");
   cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
   cuda_check(cudaMallocHost(&h_ctl_, sizeof(hdk_ctl)), "pinned ctl");
+  if (const char* pe = std::getenv("HETERODYN_PHASES"); pe && std::atoi(pe) != 0) {
+    ph_.on = true;
+    for (cudaEvent_t& e : ph_.ev) cuda_check(cudaEventCreate(&e), "phase event");
+  }
   fgraph_ = std::make_unique<LoopGraph>();
   bgraph_ = std::make_unique<LoopGraph>();
   hf_ = build_factor(scene.mesh, mat_, scene.solver.h, scene.fixed, scene.ordering);
@@ -147,7 +156,28 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas)
   time_ = 0;
 }
 
+void Engine::phase_mark(int i) {
+  if (ph_.on) cuda_check(cudaEventRecord(ph_.ev[i], st_), "phase event");
+}
+// after a stream sync: accumulate the intervals between consecutive marks
+void Engine::phase_collect(int first, int last) {
+  if (!ph_.on) return;
+  for (int i = first; i < last; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ph_.ev[i], ph_.ev[i + 1]) == cudaSuccess) ph_.ms[i] += ms;
+  }
+  if (first == 0) ++ph_.n;
+}
+
 Engine::~Engine() {
+  if (ph_.on && ph_.n > 0) {
+    static const char* names[7] = {"forward (graph + commit)", "-", "-", "backward pre", "backbone loop", "backward post",
+                                   "-"};
+    std::fprintf(stderr, "[heterodyn phases] %lld steps\n", ph_.n);
+    for (int i : {0, 3, 4, 5}) std::fprintf(stderr, "  %-26s %9.3f ms/step\n", names[i], ph_.ms[i] / ph_.n);
+  }
+  for (cudaEvent_t e : ph_.ev)
+    if (e) cudaEventDestroy(e);
   if (fgraph_) fgraph_->destroy();
   if (bgraph_) bgraph_->destroy();
   for (cudaGraphExec_t e : {bpre_, bpost_a_, bpost_b_, fpre_, fpost_})
@@ -161,6 +191,9 @@ Engine::~Engine() {
   fmem_.reset();
   mem_.reset();
   if (h_ctl_) cudaFreeHost(h_ctl_);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
+  if (st2_) cudaStreamDestroy(st2_);
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -426,6 +459,16 @@ void Engine::build_factor_device() {
   }
   seedp_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
   xp_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
+  {
+    const size_t n3p = 3 * static_cast<size_t>(F.n);
+    rt_ = A.alloc<double>(n3p);
+    rx_ = A.alloc<double>(n3p);
+    lrx_ = A.alloc<double>(n3p);
+    lrg_ = A.alloc<double>(n3p);
+    rsq_ = A.alloc<double>(HDK_AA_MAX * n3p);
+    tv_ = A.alloc<double>(3 * static_cast<size_t>(scene_.mesh.nv));
+    aares_ = A.raw(hdk_bb_result_bytes());
+  }
 }
 
 void Engine::build_forward_graph() {
@@ -496,14 +539,26 @@ void Engine::build_backward_graph() {
     hdk_check(hdk_axpby(static_cast<int>(n3), 1.0, qbar_, 1.0 / h, vbar_, seed_, s), "seed");
     cuda_check(cudaMemsetAsync(x_, 0, n3 * sizeof(double), st_), "x zero");
     cuda_check(cudaMemsetAsync(t_, 0, n3 * sizeof(double), st_), "t zero");
-    hdk_check(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
     hdk_check(hdk_gather_perm(&dv_, seed_, nullptr, rhs_, s), "x0 rhs");
     hdk_check(hdk_apply_inverse3(&df_, rhs_, x_, s), "x0 solve");
-    hdk_check(hdk_gather_perm(&dv_, x_, nullptr, xp_, s), "x0 in elimination order");
   }, &bk_pre_);
-  // backbone fixed point x <- A^{-1}(seed + B x) with AA(8) (backward.cpp:170-204)
-  auto pre = [&] { hdk_check(hdk_aa_reset(ctl_, HDK_AA_MAX, 1e8, 500, 1e-10, s), "aa reset"); };
-  auto body = [&](unsigned long long handle) { backbone_body(handle, 0u); };
+  // backbone fixed point x <- A^{-1}(seed + B x) with AA(8) (backward.cpp:170-204);
+  // the loop's pre step forms the first right-hand side seed + R(x0), R = gather o B
+  // (also run for each contact column, which re-seeds seed_ and x_)
+  auto pre = [&] {
+    hdk_check(hdk_aa_reset(ctl_, HDK_AA_MAX, 1e8, 500, 1e-10, s), "aa reset");
+    hdk_check(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
+    hdk_check(hdk_gather_perm(&dv_, x_, nullptr, xp_, s), "x0 in elimination order");
+    hdk_check(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B x0");
+    hdk_check(hdk_gather_pp(&dv_, nullptr, ef_, rx_, nullptr, s), "R(x0)");
+    hdk_check(hdk_axpby(3 * hf_.n, 1.0, seedp_, 1.0, rx_, rhs_, s), "rhs0");
+  };
+  auto body = [&](unsigned long long handle) {
+    for (int u = 0; u < unroll_; ++u) {
+      if (loop_trace_) hdk_check(hdk_trace_epoch(loop_trace_, s), "trace epoch");
+      backbone_body(handle, 0u);
+    }
+  };
   build_loop_graph(st_, use_cond_, pre, body, [] {}, *bgraph_);
   bk_body_ = bgraph_->counts[1];
   bk_pre_ += bgraph_->counts[0];
@@ -531,16 +586,31 @@ void Engine::build_backward_graph() {
 
 // One adjoint backbone iteration x <- A^{-1}(seed + B x) + AA(8)
 // (backward.cpp:170-204); skip bits drop kernels for timing ablations only.
+// The loop graph holds unroll_ copies of it; every kernel of a copy past
+// convergence returns at once (ctl->cond == 0), so one WHILE re-launch covers
+// unroll_ iterations.
+//   solve(rhs) -> dots(t) -> { coefficient solve || R(t) = gather(B t) } -> mix,
+// the coefficient solve on a second branch of the graph (st2_).
 void Engine::backbone_body(unsigned long long handle, unsigned skip) {
   void* s = st_;
-  if (!(skip & 1u)) hdk_check(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B x");
-  if (!(skip & 2u)) hdk_check(hdk_gather_pp(&dv_, seedp_, ef_, rhs_, s), "rhs");
-  if (!(skip & 4u)) hdk_check(hdk_apply_inverse3_ablate(&df_, rhs_, (skip >> 6) & 7u, s), "solve");
+  hdk_factor fb = df_;
+  fb.run_flag = &ctl_->cond;
+  const int* run_it = &snap_->cond;  // fixed for the iteration (ctl->cond moves with the branch's solve)
+  if (!(skip & 4u)) hdk_check(hdk_apply_inverse3_ablate(&fb, rhs_, (skip >> 6) & 7u, s), "solve");
   if (!(skip & 8u))
-    hdk_check(hdk_bb_dots(&df_, ctl_, snap_, t_, xp_, lastq_, lastg_, dq_, dg_, part_b_, 1 | (skip & (512u | 1024u)), s),
+    hdk_check(hdk_bb_dots(&df_, ctl_, snap_, t_, tv_, xp_, lastq_, lastg_, dq_, dg_, part_b_, 1 | (skip & (512u | 1024u)),
+                          s),
               "aa dots");
+  cuda_check(cudaEventRecord(ev_fork_, st_), "fork");
+  cuda_check(cudaStreamWaitEvent(st2_, ev_fork_, 0), "fork wait");
+  if (!(skip & 16u)) hdk_check(hdk_bb_solve(ctl_, snap_, part_b_, aares_, handle, st2_), "aa solve + cond");
+  if (!(skip & 1u)) hdk_check(hdk_bapply_flag(&dm_, dcomp_, tv_, ef_, run_it, s), "B t");
+  if (!(skip & 2u)) hdk_check(hdk_gather_pp(&dv_, nullptr, ef_, rt_, run_it, s), "R(t)");
+  cuda_check(cudaEventRecord(ev_join_, st2_), "join");
+  cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join wait");
   if (!(skip & 16u))
-    hdk_check(hdk_bb_mix(&df_, ctl_, snap_, part_b_, t_, xp_, x_, dq_, dg_, handle, s), "aa solve + mix + cond");
+    hdk_check(hdk_bb_mix(&df_, ctl_, snap_, aares_, t_, xp_, x_, dq_, rt_, rx_, lrx_, lrg_, rsq_, seedp_, rhs_, s),
+              "aa mix");
 }
 
 double Engine::time_backbone(int reps, unsigned skip) {
@@ -570,7 +640,7 @@ double Engine::time_backbone(int reps, unsigned skip) {
 // iteration and kernel {first CTA resident, first CTA past its PDL wait, last
 // CTA end} in ns; out holds reps x kTrCount x 3 values relative to the first.
 void Engine::trace_backbone(int reps, std::vector<double>& out) {
-  constexpr int kSlots = 16, kK = 12;
+  constexpr int kSlots = 16, kK = 14;
   reps = std::max(1, std::min(reps, kSlots));
   const size_t words = 1 + 3 * static_cast<size_t>(kSlots) * kK;
   unsigned long long* buf = nullptr;
@@ -607,6 +677,59 @@ void Engine::trace_backbone(int reps, std::vector<double>& out) {
         const unsigned long long v = h[1 + 3 * (r * kK + k) + j];
         if (v != ~0ULL && v != 0ULL) out[3 * (r * kK + k) + j] = static_cast<double>(v - t0);
       }
+}
+
+// Timeline of the real backbone WHILE loop (profiling): one recorded
+// forward step from the current state, then its backward with an epoch
+// kernel in front of every unrolled iteration; out receives the last
+// min(iterations, 16) iterations' records (same layout as trace_backbone,
+// oldest first).  The state is restored afterwards.
+void Engine::trace_loop(std::vector<double>& out) {
+  constexpr int kSlots = 16, kK = 14;
+  const size_t words = 1 + 3 * static_cast<size_t>(kSlots) * kK;
+  std::vector<unsigned long long> h(words);
+  for (size_t i = 1; i < words; i += 3) {
+    h[i] = ~0ULL;
+    h[i + 1] = ~0ULL;
+    h[i + 2] = 0ULL;
+  }
+  h[0] = kSlots - 1;
+  cuda_check(cudaMalloc(&loop_trace_, words * 8), "trace buffer");
+  cuda_check(cudaMemcpy(loop_trace_, h.data(), words * 8, cudaMemcpyHostToDevice), "trace init");
+  build_backward_graph();
+  const Vec q = positions(), v = velocities();
+  const double t = time_;
+  record(true);
+  step();
+  for (auto inst : {hdk_trace_install_local, hdk_trace_install_vec, hdk_trace_install_solve})
+    hdk_check(inst(loop_trace_), "trace install");
+  backward(nullptr, nullptr, nullptr, true, false, nullptr);
+  cuda_check(cudaStreamSynchronize(st_), "trace sync");
+  for (auto inst : {hdk_trace_install_local, hdk_trace_install_vec, hdk_trace_install_solve})
+    hdk_check(inst(nullptr), "trace uninstall");
+  cuda_check(cudaMemcpy(h.data(), loop_trace_, words * 8, cudaMemcpyDeviceToHost), "trace read");
+  cudaFree(loop_trace_);
+  loop_trace_ = nullptr;
+  build_backward_graph();
+  record(false);
+  set_state(q.data(), v.data(), t);
+  const int iters = last_backward_iterations_;
+  const int nrec = std::min(iters, kSlots);
+  const unsigned long long ep = h[0];  // slot of the last epoch
+  unsigned long long t0 = ~0ULL;
+  for (int k = 0; k < nrec; ++k) {
+    const int slot = static_cast<int>((ep + kSlots - (nrec - 1 - k)) % kSlots);
+    for (int j = 0; j < kK; ++j) t0 = std::min(t0, h[1 + 3 * (slot * kK + j)]);
+  }
+  out.assign(static_cast<size_t>(nrec) * kK * 3, -1.0);
+  for (int k = 0; k < nrec; ++k) {
+    const int slot = static_cast<int>((ep + kSlots - (nrec - 1 - k)) % kSlots);
+    for (int j = 0; j < kK; ++j)
+      for (int c = 0; c < 3; ++c) {
+        const unsigned long long val = h[1 + 3 * (slot * kK + j) + c];
+        if (val != ~0ULL && val != 0ULL) out[3 * (k * kK + j) + c] = static_cast<double>(val - t0);
+      }
+  }
 }
 
 void Engine::sync_ctl() {
@@ -646,6 +769,7 @@ void Engine::check_ctl(const char* what) {
 
 void Engine::step() {
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
+  phase_mark(0);
   std::shared_ptr<ContactFrame> contacts;
   if (!scene_.obstacles.empty()) {
     cuda_check(cudaGraphLaunch(fpre_, st_), "forward pre");
@@ -676,7 +800,9 @@ void Engine::step() {
     cp(fr.cache, cache_, 24 * ne);
   }
   hdk_check(hdk_commit(static_cast<int>(n3), ctl_, qcur_, scene_.solver.h, q_, v_, st_), "commit");
+  phase_mark(1);
   sync_ctl();
+  phase_collect(0, 1);
   if (!(contacts && contacts->k > 0)) {
     solve_count += h_ctl_->iterations;
     kernel_launches += fk_pre_ + static_cast<long long>(fk_body_) * h_ctl_->iterations + fk_post_ + 1;

@@ -94,7 +94,20 @@ class Engine {
   double time_solve(int reps, double* bytes);
   double time_backbone(int reps, unsigned skip_mask);
   void backbone_body(unsigned long long cond_handle, unsigned skip_mask);
+  // Profiling (HETERODYN_PHASES=1): CUDA-event time per step phase, summed
+  // and printed to stderr when the engine is destroyed.
+  struct Phases {
+    bool on = false;
+    cudaEvent_t ev[8] = {};
+    double ms[8] = {};
+    long long n = 0;
+  } ph_;
+  void phase_mark(int i);
+  void phase_collect(int first, int last);
   void trace_backbone(int reps, std::vector<double>& out);
+  void trace_loop(std::vector<double>& out);
+  unsigned long long* loop_trace_ = nullptr;  // set only while trace_loop runs
+  int last_backward_iterations_ = 0;
   Vec solve_free(const double* rhs, const double* fixed_q);
   void set_young(const Vec& young, bool freeze);
 
@@ -130,6 +143,8 @@ class Engine {
   Material mat_;
   HostFactor hf_;
   cudaStream_t st_ = nullptr;
+  cudaStream_t st2_ = nullptr;  // second branch of the backbone graph (coefficient solve)
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   std::unique_ptr<DevArena> mem_;      // mesh/material/state/work
   std::unique_ptr<DevArena> fmem_;     // factor (rebuilt on refresh)
   bool use_cond_ = true;
@@ -154,9 +169,14 @@ class Engine {
   double* cache_ = nullptr;  // 24 ne projection cache of the current step
   hdk_ctl* ctl_ = nullptr;
   unsigned int* ticket_ = nullptr;
-  hdk_ctl* snap_ = nullptr;  // control-block snapshot of the backbone (hdk_bb_dots -> hdk_bb_mix)
+  hdk_ctl* snap_ = nullptr;
+  int unroll_ = 4;  // backbone iterations per WHILE-loop body  // control-block snapshot of the backbone (hdk_bb_dots -> hdk_bb_mix)
   double* seedp_ = nullptr;  // adjoint seed in elimination order (3 n)
-  double* xp_ = nullptr;     // backbone iterate in elimination order (3 n); x_ holds it by vertex  // last-block ticket of hdk_aa_dots_fused
+  double* xp_ = nullptr;     // backbone iterate in elimination order (3 n); x_ holds it by vertex
+  // R = gather o B in elimination order: R(t), tracked R(x), last R(x) and R(g), R(dq_j + dg_j) ring
+  double *rt_ = nullptr, *rx_ = nullptr, *lrx_ = nullptr, *lrg_ = nullptr, *rsq_ = nullptr;
+  double* tv_ = nullptr;     // t by vertex (input of B t)
+  void* aares_ = nullptr;    // coefficient-solve result (hdk_bb_solve -> hdk_bb_mix)  // last-block ticket of hdk_aa_dots_fused
   hdk_ctl* h_ctl_ = nullptr;  // pinned mirror
   double* hook_ = nullptr;    // 5 doubles device
 

@@ -241,12 +241,16 @@ void Engine::contact_loop(ContactFrame& c) {
 void Engine::backward_frame(int t, GradOut& out) {
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
   const Frame& f = slots_[t];
+  phase_mark(3);
   cuda_check(cudaGraphLaunch(bpre_, st_), "backward pre");
+  phase_mark(4);
   run_graph(*bgraph_, "backbone");
+  phase_mark(5);
   sync_ctl();
   check_ctl("backward step");
   int iters = 1 + h_ctl_->iterations;  // the first solve of the backbone counts (backward.cpp:176-178)
-  kernel_launches += bk_pre_ + static_cast<long long>(bk_body_) * h_ctl_->iterations;
+  last_backward_iterations_ = h_ctl_->iterations;
+  kernel_launches += bk_pre_ + static_cast<long long>(bk_body_) * ((h_ctl_->iterations + unroll_ - 1) / unroll_);
   out.tau[t] = h_ctl_->tau;
   out.rho[t] = h_ctl_->rho;
   ContactFrame* c = f.contacts && f.contacts->k > 0 ? f.contacts.get() : nullptr;
@@ -262,13 +266,12 @@ void Engine::backward_frame(int t, GradOut& out) {
     // tangent columns x_c = (A - B)^{-1} j_c warm-started from a_c (backward.cpp:229-238)
     for (int r = 0; r < k; ++r) {
       hdk_check(hdk_contact_column_init(&c->view, r, nv, df_.v2p, c->U, n, seed_, x_, st_), "column init");
-      hdk_check(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, st_), "column seed in elimination order");
-      hdk_check(hdk_gather_perm(&dv_, x_, nullptr, xp_, st_), "column x0 in elimination order");
       run_graph(*bgraph_, "backbone column");
       sync_ctl();
       check_ctl("backward step");
       iters += h_ctl_->iterations;
-      kernel_launches += 3 + bgraph_->counts[0] + static_cast<long long>(bk_body_) * h_ctl_->iterations;
+      kernel_launches += 1 + bgraph_->counts[0] +
+                         static_cast<long long>(bk_body_) * ((h_ctl_->iterations + unroll_ - 1) / unroll_);
       cuda_check(cudaMemcpyAsync(cX_ + n3 * r, x_, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st_), "column");
     }
     ensure_solver_workspace(k);
@@ -288,11 +291,13 @@ void Engine::backward_frame(int t, GradOut& out) {
     ++kernel_launches;
   }
   cuda_check(cudaGraphLaunch(bpost_b_, st_), "backward post");
+  phase_mark(6);
   kernel_launches += bk_post_;
   ++a_spmv_count;
   solve_count += iters;
   out.adjoint_iterations += iters;
   sync_ctl();
+  phase_collect(3, 6);
   check_ctl("backward step");
 }
 

@@ -68,7 +68,7 @@ __device__ __forceinline__ void st_keep(double* a, double v, unsigned long long 
 // records, per kernel id, the earliest CTA start before and after its PDL
 // wait and the latest CTA end (thread 0, globaltimer ns).
 enum TraceId { kTrBapply, kTrGather, kTrRowdot, kTrZfold, kTrColtile, kTrDots, kTrMix,
-               kTrTail0, kTrTail1, kTrTail2, kTrDotsA, kTrDotsB, kTrCount };  // tail stamps: AA tail entry, after fold, after solve
+               kTrTail0, kTrTail1, kTrTail2, kTrDotsA, kTrDotsB, kTrTail3, kTrTail4, kTrCount };  // tail stamps: AA tail entry, after fold, after solve
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;

@@ -303,9 +303,10 @@ __global__ void __launch_bounds__(128) k_differential(hdk_mesh m, hdk_material m
 // than register-capped single-wave shapes (10.0 vs 12.3 us per apply).
 template <int T, int MINB>
 __global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __restrict__ dcomp, const double* __restrict__ x,
-                                                 double* __restrict__ ef) {
+                                                 double* __restrict__ ef, const int* run_flag) {
   HDK_TRACED_WAIT(hdk::kTrBapply);
   hdk::pdl_trigger();
+  if (run_flag && *run_flag == 0) return;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m.ne) return;
   const size_t n = m.ne;
@@ -423,14 +424,19 @@ HDK_API int hdk_differential(const hdk_mesh* m, const hdk_material* mat, const d
 }
 
 HDK_API int hdk_bapply(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force, void* stream) {
+  return hdk_bapply_flag(m, dcomp, x, elem_force, nullptr, stream);
+}
+
+HDK_API int hdk_bapply_flag(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
+                            const int* run_flag, void* stream) {
   static const int variant = [] {
     const char* v = std::getenv("HETERODYN_BAPPLY");
     return v ? std::atoi(v) : 0;
   }();
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (variant == 0) hdk::launch(k_bapply<128, 1>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, elem_force);
-  else if (variant == 2) hdk::launch(k_bapply<128, 6>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, elem_force);
-  else hdk::launch(k_bapply<64, 11>, dim3(blocks(m->ne, 64)), dim3(64), 0, st, *m, dcomp, x, elem_force);
+  if (variant == 0) hdk::launch(k_bapply<128, 1>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, elem_force, run_flag);
+  else if (variant == 2) hdk::launch(k_bapply<128, 6>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, elem_force, run_flag);
+  else hdk::launch(k_bapply<64, 11>, dim3(blocks(m->ne, 64)), dim3(64), 0, st, *m, dcomp, x, elem_force, run_flag);
   return static_cast<int>(cudaGetLastError());
 }
 

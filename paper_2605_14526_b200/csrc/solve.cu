@@ -315,6 +315,7 @@ template <bool kDry = false>  // kDry: stream only (microbenchmarks)
 __global__ void __launch_bounds__(kThreads, 2) k_rowdot(hdk_factor f, const double* __restrict__ rhs) {
   HDK_TRACED_WAIT(hdk::kTrRowdot);
   hdk::pdl_trigger();
+  if (f.run_flag && *f.run_flag == 0) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<kStages1>& ring = *reinterpret_cast<Ring<kStages1>*>(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -425,6 +426,7 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages
 __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
   HDK_TRACED_WAIT(hdk::kTrZfold);
   hdk::pdl_trigger();
+  if (f.run_flag && *f.run_flag == 0) return;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t < f.n_ztask) zfold_task(f, __ldg(f.ztask + t));
 }
@@ -480,6 +482,7 @@ template <bool kDry = false>
 __global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
   HDK_TRACED_WAIT(hdk::kTrColtile);
   hdk::pdl_trigger();
+  if (f.run_flag && *f.run_flag == 0) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Pass2Smem& sm = *reinterpret_cast<Pass2Smem*>(smem_raw);
   Ring2<kStages2>& ring = sm.ring;

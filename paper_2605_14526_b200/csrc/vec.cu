@@ -226,9 +226,10 @@ __global__ void k_gather_perm(hdk_vtx x, const double* __restrict__ base, const 
 // k_gather_perm over the elimination-order incidence; same terms, same lane
 // split and fold, so bitwise the same sums.
 __global__ void k_gather_pp(hdk_vtx x, const double* __restrict__ basep, const double* __restrict__ ef,
-                            double* __restrict__ rhs) {
+                            double* __restrict__ rhs, const int* run_flag) {
   HDK_TRACED_WAIT(hdk::kTrGather);
   hdk::pdl_trigger();
+  if (run_flag && *run_flag == 0) return;
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int p = gid >> 3, sub = gid & 7;
   const bool live = p < x.n;
@@ -250,9 +251,9 @@ __global__ void k_gather_pp(hdk_vtx x, const double* __restrict__ basep, const d
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   }
   if (live && sub == 0) {
-    rhs[3 * (size_t)p] = basep[3 * (size_t)p] + s0;
-    rhs[3 * (size_t)p + 1] = basep[3 * (size_t)p + 1] + s1;
-    rhs[3 * (size_t)p + 2] = basep[3 * (size_t)p + 2] + s2;
+    rhs[3 * (size_t)p] = (basep ? basep[3 * (size_t)p] : 0.0) + s0;
+    rhs[3 * (size_t)p + 1] = (basep ? basep[3 * (size_t)p + 1] : 0.0) + s1;
+    rhs[3 * (size_t)p + 2] = (basep ? basep[3 * (size_t)p + 2] : 0.0) + s2;
   }
 }
 
@@ -331,9 +332,13 @@ __global__ void __launch_bounds__(kT) k_aa_dots(hdk_vtx x, const hdk_ctl* ctl, c
 // sets the WHILE condition (graph handle given).
 constexpr int kSolveT = kT;
 constexpr int kNQ = 2 * HDK_AA_MAX + 2;
+// Barrier of threads 0..63 only (the factorization warps).
+__device__ __forceinline__ void named_bar64() { asm volatile("bar.sync 2, 64;" ::: "memory"); }
+
 // What the mixing step of the calling block needs from the solve (shared).
 struct AaResult {
   double gamma[HDK_AA_MAX];
+  double gslot[HDK_AA_MAX];  // gamma by history ring slot (0 for unused slots)
   int done, mixed, count, head, window, err;
 };
 
@@ -383,50 +388,56 @@ __device__ __noinline__ void aa_solve_block(const hdk_ctl* in, hdk_ctl* gctl, co
   }
   __syncthreads();
   hdk::trace_stamp(g_hdk_trace, hdk::kTrTail1);
-  if (warp != 0) return;
+  // ---- warp 0: convergence test, history bookkeeping, pivot order ----------
+  __shared__ double sG[M][M + 1], sA[M][M + 1], sd[M], sy[M], sgam[M];
+  __shared__ int sperm[M], sn, sok;
+  __shared__ double sridge;
   const unsigned F = 0xffffffffu;
   bool skip = false;
-  if (mode == 1) {  // adjoint backbone: convergence test before mixing
-    iters += 1;
-    const double diff = sqrt(s[2 * M]);
-    const double base = fmax(sqrt(s[2 * M + 1]), 1e-30);
-    kk += 1;
-    if (diff <= tol * base) {
-      done = 1;
-      mixed = 0;
-      skip = true;
-    } else if (kk >= k_max && err == 0) {
-      err = 10;  // AdjointDiverged (cap)
-    }
-  }
   int nsol = 0;
   double gam[M];
 #pragma unroll
   for (int c = 0; c < M; ++c) gam[c] = 0.0;
-  if (!skip) {
-    if (has_last) {
-      if (count < m) {
-        count += 1;
-      } else {  // drop the oldest: gram[i][j] <- gram[i+1][j+1]
-        head = (head + 1) % m;
-        double nx[M];
-#pragma unroll
-        for (int j = 0; j < M; ++j) nx[j] = __shfl_down_sync(F, g[j], 1);
-#pragma unroll
-        for (int j = 0; j + 1 < M; ++j) g[j] = nx[j + 1];
+  if (warp == 0) {
+    if (mode == 1) {  // adjoint backbone: convergence test before mixing
+      iters += 1;
+      const double diff = sqrt(s[2 * M]);
+      const double base = fmax(sqrt(s[2 * M + 1]), 1e-30);
+      kk += 1;
+      if (diff <= tol * base) {
+        done = 1;
+        mixed = 0;
+        skip = true;
+      } else if (kk >= k_max && err == 0) {
+        err = 10;  // AdjointDiverged (cap)
       }
-      const int j0 = count - 1;  // newest row / column = DG^T dg_new
-#pragma unroll
-      for (int j = 0; j < M; ++j)
-        if (j == j0 && lane < count) g[j] = s[lane];
-      if (lane == j0)
-#pragma unroll
-        for (int l = 0; l < M; ++l)
-          if (l < count) g[l] = s[l];
     }
-    has_last = 1;
-    mixed = 0;
-    const int n = count;
+    int n = 0;
+    if (!skip) {
+      if (has_last) {
+        if (count < m) {
+          count += 1;
+        } else {  // drop the oldest: gram[i][j] <- gram[i+1][j+1]
+          head = (head + 1) % m;
+          double nx[M];
+#pragma unroll
+          for (int j = 0; j < M; ++j) nx[j] = __shfl_down_sync(F, g[j], 1);
+#pragma unroll
+          for (int j = 0; j + 1 < M; ++j) g[j] = nx[j + 1];
+        }
+        const int j0 = count - 1;  // newest row / column = DG^T dg_new
+#pragma unroll
+        for (int j = 0; j < M; ++j)
+          if (j == j0 && lane < count) g[j] = s[lane];
+        if (lane == j0)
+#pragma unroll
+          for (int l = 0; l < M; ++l)
+            if (l < count) g[l] = s[l];
+      }
+      has_last = 1;
+      mixed = 0;
+      n = count;
+    }
     double mydiag = 0.0;
 #pragma unroll
     for (int j = 0; j < M; ++j)
@@ -441,7 +452,7 @@ __device__ __noinline__ void aa_solve_block(const hdk_ctl* in, hdk_ctl* gctl, co
       nsol = n;
       const double ridge = 1e-6 * fro2 / m;
       // pivot order: largest |diagonal| among the remaining untouched ones,
-      // swapped into place (warp-uniform, registers only)
+      // swapped into place (Eigen LDLT; warp-uniform, registers only)
       int perm[M];
       double dv[M];
 #pragma unroll
@@ -476,97 +487,87 @@ __device__ __noinline__ void aa_solve_block(const hdk_ctl* in, hdk_ctl* gctl, co
           dv[k] = dp;
         }
       }
-      int rk = M;  // position of this lane's row in the pivot order
-#pragma unroll
-      for (int k = 0; k < M; ++k)
-        if (k < n && perm[k] == lane) rk = k;
-      // this lane's row of the permuted matrix: ap[j] = M(lane, perm[j])
-      double ap[M];
-#pragma unroll
-      for (int j = 0; j < M; ++j) {
-        double a = 0.0;
-#pragma unroll
-        for (int c = 0; c < M; ++c)
-          if (c == perm[j]) a = g[c];
-        ap[j] = a + (perm[j] == lane ? ridge : 0.0);
-      }
-      double L[M], d[M];
-      bool ok = true;
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        L[k] = 0.0;
-        d[k] = 1.0;
-        if (k < n) {
-          const int pk = perm[k];
-          double Lp[M];
-#pragma unroll
-          for (int j = 0; j < k; ++j) Lp[j] = __shfl_sync(F, L[j], pk);
-          double dk = __shfl_sync(F, ap[k], pk);
-#pragma unroll
-          for (int j = 0; j < k; ++j) dk -= Lp[j] * Lp[j] * d[j];
-          d[k] = dk;
-          if (!(fabs(dk) > 2.2250738585072014e-308)) ok = false;
-          if (rk > k && rk < n) {
-            double v = ap[k];
-#pragma unroll
-            for (int j = 0; j < k; ++j) v -= L[j] * Lp[j] * d[j];
-            L[k] = v / dk;
-          }
-        }
-      }
-      // forward substitution, column-oriented (same subtraction order per row)
-      double y[M];
-      double acc = lane < M ? s[M + lane] : 0.0;
-#pragma unroll
-      for (int j = 0; j < M; ++j) {
-        y[j] = 0.0;
-        if (j < n) {
-          y[j] = __shfl_sync(F, acc, perm[j]);
-          if (rk > j && rk < n) acc -= L[j] * y[j];
-        }
-      }
+      if (lane == 0) sridge = ridge;
 #pragma unroll
       for (int i = 0; i < M; ++i)
-        if (i < n) y[i] /= d[i];
-      // back substitution: y[i] -= L[j][i] y[j], j ascending from i + 1
+        if (lane == i) sperm[i] = perm[i];
+      if (lane < M)
 #pragma unroll
-      for (int i = M - 2; i >= 0; --i) {
-#pragma unroll
-        for (int j = i + 1; j < M; ++j) {
-          const double lji = __shfl_sync(F, L[i], perm[j]);
-          if (i < n && j < n) y[i] -= lji * y[j];
-        }
+        for (int j = 0; j < M; ++j) sG[lane][j] = g[j];
+    }
+    if (lane == 0) sn = nsol;
+  }
+  hdk::trace_stamp(g_hdk_trace, hdk::kTrTail3);
+  __syncthreads();
+  // ---- threads 0..63: LDL^T of the permuted matrix in shared memory ---------
+  // Right-looking with the left-looking (Eigen) operation order per entry:
+  // A(i,k) -= (L(i,l) L(k,l)) d(l) for l = 0, 1, ...; then L(i,k) = A(i,k) / d(k).
+  const int ns = sn;
+  if (ns > 0 && threadIdx.x < 64) {
+    const int i = threadIdx.x >> 3, j = threadIdx.x & 7;
+    if (i < ns && j < ns) sA[i][j] = sG[sperm[i]][sperm[j]] + (i == j ? sridge : 0.0);
+    if (threadIdx.x == 0) sok = 1;
+    named_bar64();
+    for (int k = 0; k < ns; ++k) {
+      const double dk = sA[k][k];
+      if (j == k && i > k && i < ns) sA[i][k] = sA[i][k] / dk;  // L(i,k)
+      if (threadIdx.x == 0) {
+        sd[k] = dk;
+        if (!(fabs(dk) > 2.2250738585072014e-308)) sok = 0;
       }
+      named_bar64();
+      if (i > k && i < ns && j > k && j <= i) sA[i][j] -= sA[i][k] * sA[j][k] * dk;
+      named_bar64();
+    }
+    // y = L^{-1} P b (row order of subtractions as in the serial form)
+    const int t = threadIdx.x;
+    if (t < ns) sy[t] = s[M + sperm[t]];
+    named_bar64();
+    for (int k = 0; k < ns; ++k) {
+      if (t > k && t < ns) sy[t] -= sA[t][k] * sy[k];
+      named_bar64();
+    }
+    if (t < ns) sy[t] /= sd[t];
+    named_bar64();
+    for (int k = ns - 1; k > 0; --k) {  // L^T x = y, column-oriented
+      if (t < k) sy[t] -= sA[k][t] * sy[k];
+      named_bar64();
+    }
+    if (t < ns) sgam[sperm[t]] = sy[t];
+  }
+  hdk::trace_stamp(g_hdk_trace, hdk::kTrTail4);
+  __syncthreads();
+  if (warp != 0) return;
+  if (nsol > 0) {
 #pragma unroll
-      for (int c = 0; c < M; ++c) gam[c] = 0.0;
+    for (int c = 0; c < M; ++c) gam[c] = c < nsol ? sgam[c] : 0.0;
+    bool good = sok != 0;
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+      if (i < nsol) good = good && isfinite(gam[i]);
+    double gn = 0.0;
+    if (good)
 #pragma unroll
       for (int i = 0; i < M; ++i)
-#pragma unroll
-        for (int c = 0; c < M; ++c)
-          if (i < n && c == perm[i]) gam[c] = y[i];
-      bool good = ok;
-#pragma unroll
-      for (int i = 0; i < M; ++i)
-        if (i < n) good = good && isfinite(gam[i]);
-      double gn = 0.0;
-      if (good)
-#pragma unroll
-        for (int i = 0; i < M; ++i)
-          if (i < n) gn += gam[i] * gam[i];
-      if (!good || !(sqrt(gn) <= guard)) {  // guard: discard history (forward.cpp:43-47)
-        count = 0;
-        head = 0;
-        has_last = 0;
-        nsol = 0;
-      } else {
-        mixed = 1;
-      }
+        if (i < nsol) gn += gam[i] * gam[i];
+    if (!good || !(sqrt(gn) <= guard)) {  // guard: discard history (forward.cpp:43-47)
+      count = 0;
+      head = 0;
+      has_last = 0;
+      nsol = 0;
+    } else {
+      mixed = 1;
     }
   }
   hdk::trace_stamp(g_hdk_trace, hdk::kTrTail2);
   if (res && lane == 0) {
 #pragma unroll
-    for (int i = 0; i < M; ++i) res->gamma[i] = gam[i];
+    for (int i = 0; i < M; ++i) {
+      res->gamma[i] = gam[i];
+      res->gslot[i] = 0.0;
+    }
+    if (mixed)
+      for (int j = 0; j < count; ++j) res->gslot[(head + j) % m] = gam[j];
     res->done = done;
     res->mixed = mixed;
     res->count = count;
@@ -684,10 +685,18 @@ __global__ void __launch_bounds__(kT) k_aa_dots_fused(hdk_vtx x, hdk_factor f, i
   aa_solve_block(ctl, ctl, partial, mode, handle, use_handle);
 }
 
-__global__ void k_trace_epoch(unsigned long long* buf) {
+__global__ void k_trace_epoch(unsigned long long* buf) {  // advance and clear the next record slot
   hdk::pdl_wait();
   hdk::pdl_trigger();
-  buf[0] += 1ULL;
+  const unsigned long long ep = buf[0] + 1ULL;
+  unsigned long long* r = buf + 1 + 3 * ((ep % hdk::kTraceSlots) * hdk::kTrCount);
+  for (int i = 0; i < hdk::kTrCount; ++i) {
+    r[3 * i] = ~0ULL;
+    r[3 * i + 1] = ~0ULL;
+    r[3 * i + 2] = 0ULL;
+  }
+  __threadfence();
+  buf[0] = ep;
 }
 
 // True in the block that arrives last.  The CTA barrier orders every
@@ -714,18 +723,22 @@ __device__ __forceinline__ bool last_block_ticket(unsigned int* ticket) {
 // vertices carry t = x = 0 in the backbone (they contribute nothing to any
 // dot product), so dropping them changes no value, only the summation order.
 __global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ctl, hdk_ctl* snap, double* __restrict__ tp,
-                                                const double* __restrict__ xp, double* last_q, double* last_g,
-                                                double* dq, double* dg, double* partial, int mode) {
+                                                double* __restrict__ tv, const double* __restrict__ xp, double* last_q,
+                                                double* last_g, double* dq, double* dg, double* partial, int mode) {
   HDK_TRACED_WAIT(hdk::kTrDots);
   hdk::pdl_trigger();
   const size_t n3 = 3 * (size_t)n;
   if (blockIdx.x == 0) {  // snapshot of the control block for k_bb_mix (which rewrites ctl)
-    if (threadIdx.x == 0 && ctl->nonfinite && ctl->err == 0) ctl->err = 10;  // AdjointDiverged
+    if (threadIdx.x == 0 && ctl->nonfinite && ctl->err == 0) {  // AdjointDiverged
+      ctl->err = 10;
+      ctl->cond = 0;
+    }
     __syncthreads();
     const int* src = reinterpret_cast<const int*>(ctl);
     int* dst = reinterpret_cast<int*>(snap);
     for (int w = threadIdx.x; w < static_cast<int>(sizeof(hdk_ctl) / 4); w += kT) dst[w] = src[w];
   }
+  if (ctl->cond == 0) return;  // unrolled iteration past convergence (the snapshot still carries cond = 0)
   const int m = ctl->window, c = ctl->count, h = ctl->head;
   const bool push = ctl->has_last != 0;
   int ns = 0, c2 = c, h2 = h;
@@ -759,6 +772,7 @@ __global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ct
         if (b0 + k < pf.y) th += v[k];
     }
     hdk::st_keep(tp + i, th, pol);
+    tv[3 * (size_t)__ldg(f.p2v + col) + a] = th;  // by vertex, for B t
     const double qc = hdk::ld_keep(xp + i, pol);
     const double g = th - qc;
     acc[2 * HDK_AA_MAX] += g * g;
@@ -766,7 +780,7 @@ __global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ct
     if (push) {
       const double dqn = qc - hdk::ld_keep(last_q + i, pol);
       const double dgn = g - hdk::ld_keep(last_g + i, pol);
-      hdk::st_keep(dq + ns * n3 + i, dqn, pol);
+      hdk::st_keep(dq + ns * n3 + i, dqn + dgn, pol);  // the mix only ever uses dq_j + dg_j
       hdk::st_keep(dg + ns * n3 + i, dgn, pol);
 #pragma unroll
       for (int j = 0; j < HDK_AA_MAX; ++j) {
@@ -788,50 +802,88 @@ __global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ct
 
 // x <- t - sum_j gamma_j (dq_j + dg_j) in elimination order, also scattered to
 // the full vertex vector the element kernels read.
-// Every block folds the dot partials and solves the Anderson system itself
-// (identical inputs, identical code: identical results) from the snapshot
-// k_bb_dots took, so no block waits on a last-block tail; block 0 publishes
-// the new state (and the WHILE condition) to ctl, which no block of this
-// launch reads.
+// Anderson coefficient solve of the backbone on its own graph branch (one
+// block): runs while B t and its gather proceed on the main branch, reads
+// the snapshot k_bb_dots took, publishes the new state and the WHILE
+// condition to ctl and the mixing inputs to *res.
+__global__ void __launch_bounds__(kT) k_bb_solve(hdk_ctl* ctl, const hdk_ctl* snap, const double* partial,
+                                                 AaResult* out, cudaGraphConditionalHandle handle, int use_handle) {
+  HDK_TRACED_WAIT(hdk::kTrTail0);
+  hdk::pdl_trigger();
+  if (snap->cond == 0) return;  // unrolled iteration past convergence
+  __shared__ AaResult res;
+  aa_solve_block(snap, ctl, partial, 1, handle, use_handle, &res);
+  __syncthreads();
+  const int* src = reinterpret_cast<const int*>(&res);
+  int* dst = reinterpret_cast<int*>(out);
+  for (int w = threadIdx.x; w < static_cast<int>(sizeof(AaResult) / 4); w += kT) dst[w] = src[w];
+}
+
+// Anderson mix of the backbone, in elimination order, carried in two spaces:
+//   x_{k+1} = t_k - sum_j gamma_j (dq_j + dg_j)                 (backward.cpp:188-199)
+//   R(x_{k+1}) = R(t_k) - sum_j gamma_j R(dq_j + dg_j),  R = gather o B,
+// by linearity of R, so the next right-hand side seed + R(x_{k+1}) is ready
+// without applying B to the mixed iterate (B t_k ran beside the coefficient
+// solve).  The rings hold the sums s_j = dq_j + dg_j (k_bb_dots) and their
+// R-images (pushed here from the tracked R(x_k) and R(t_k), same slots); a
+// history reset restarts the R side from R(t_k) exactly.
 __global__ void __launch_bounds__(kT) k_bb_mix(int n, const int* __restrict__ p2v, hdk_ctl* ctl, const hdk_ctl* snap,
-                                               const double* partial, const double* __restrict__ tp, double* xp,
-                                               double* __restrict__ xv, const double* __restrict__ dq,
-                                               const double* __restrict__ dg, cudaGraphConditionalHandle handle,
-                                               int use_handle) {
+                                               const AaResult* __restrict__ res, const double* __restrict__ tp,
+                                               double* xp, double* __restrict__ xv, const double* __restrict__ sq,
+                                               const double* __restrict__ rt, double* rx, double* last_rx,
+                                               double* last_rg, double* rsq, const double* __restrict__ seedp,
+                                               double* __restrict__ rhs) {
   HDK_TRACED_WAIT(hdk::kTrMix);
   hdk::pdl_trigger();
+  if (snap->cond == 0) return;  // unrolled iteration past convergence
   const size_t n3 = 3 * (size_t)n;
-  __shared__ AaResult res;
-  aa_solve_block(snap, blockIdx.x == 0 ? ctl : nullptr, partial, 1, handle, use_handle, &res);
-  __syncthreads();
-  const bool done = res.done;
-  const int mixed = res.mixed, c = res.count, h = res.head, m = res.window;
-  double gam[HDK_AA_MAX];
-  int ph[HDK_AA_MAX];
-#pragma unroll
-  for (int j = 0; j < HDK_AA_MAX; ++j) {
-    gam[j] = j < c ? res.gamma[j] : 0.0;
-    ph[j] = (h + j) % m;
-  }
-  bool finite = true;
   const size_t i = blockIdx.x * (size_t)kT + threadIdx.x;
-  if (i < n3) {
-    const unsigned long long pol = hdk::pol_keep();
-    const double qc = hdk::ld_keep(xp + i, pol), th = hdk::ld_keep(tp + i, pol);
-    double out = qc + (th - qc);
-    if (done) {
-      out = th;
-    } else if (mixed) {
+  if (i >= n3) return;
+  const unsigned long long pol = hdk::pol_keep();
+  // ring slot of the entry pushed this iteration (state before the update, as k_bb_dots)
+  const int m = snap->window, c0 = snap->count, h0 = snap->head;
+  const bool push = snap->has_last != 0;
+  const int ns = push ? (c0 < m ? (h0 + c0) % m : h0) : -1;
+  const bool done = res->done != 0;
+  const int mixed = res->mixed, c = res->count;
+  double hs[HDK_AA_MAX], rs[HDK_AA_MAX];
 #pragma unroll
-      for (int j = 0; j < HDK_AA_MAX; ++j)
-        if (j < c) out -= gam[j] * (hdk::ld_keep(dq + ph[j] * n3 + i, pol) + hdk::ld_keep(dg + ph[j] * n3 + i, pol));
-    }
-    finite = isfinite(out);
-    hdk::st_keep(xp + i, out, pol);
-    const int col = static_cast<int>(i / 3);
-    xv[3 * (size_t)__ldg(p2v + col) + (i - 3 * (size_t)col)] = out;
+  for (int sl = 0; sl < HDK_AA_MAX; ++sl) {
+    hs[sl] = sl < m ? hdk::ld_keep(sq + sl * n3 + i, pol) : 0.0;
+    rs[sl] = sl < m && sl != ns ? hdk::ld_keep(rsq + sl * n3 + i, pol) : 0.0;
   }
-  if (!finite) atomicOr(&ctl->nonfinite, 1);
+  const double qc = hdk::ld_keep(xp + i, pol), th = hdk::ld_keep(tp + i, pol);
+  const double rxc = hdk::ld_keep(rx + i, pol), rth = hdk::ld_keep(rt + i, pol);
+  const double rgn = rth - rxc;
+  if (push) {
+    const double rdqn = rxc - hdk::ld_keep(last_rx + i, pol);
+    const double rdgn = rgn - hdk::ld_keep(last_rg + i, pol);
+    const double rsn = rdqn + rdgn;
+    hdk::st_keep(rsq + ns * n3 + i, rsn, pol);
+#pragma unroll
+    for (int sl = 0; sl < HDK_AA_MAX; ++sl)
+      if (sl == ns) rs[sl] = rsn;
+  }
+  hdk::st_keep(last_rx + i, rxc, pol);
+  hdk::st_keep(last_rg + i, rgn, pol);
+  double out = qc + (th - qc), rout = rxc + rgn;
+  if (done) {
+    out = th;
+    rout = rth;
+  } else if (mixed) {  // valid ring slots are 0..count-1 (head moves only once the ring is full)
+#pragma unroll
+    for (int sl = 0; sl < HDK_AA_MAX; ++sl)
+      if (sl < c) {
+        out -= res->gslot[sl] * hs[sl];
+        rout -= res->gslot[sl] * rs[sl];
+      }
+  }
+  hdk::st_keep(xp + i, out, pol);
+  hdk::st_keep(rx + i, rout, pol);
+  rhs[i] = seedp[i] + rout;
+  const int col = static_cast<int>(i / 3);
+  xv[3 * (size_t)__ldg(p2v + col) + (i - 3 * (size_t)col)] = out;
+  if (!isfinite(out) || !isfinite(rout)) atomicOr(&ctl->nonfinite, 1);
 }
 
 __global__ void __launch_bounds__(kT) k_aa_mix(hdk_vtx x, hdk_ctl* ctl, const double* __restrict__ qhat, double* qcur,
@@ -1123,9 +1175,10 @@ HDK_API int hdk_gather_perm(const hdk_vtx* x, const double* base, const double* 
   return last();
 }
 
-HDK_API int hdk_gather_pp(const hdk_vtx* x, const double* base_perm, const double* ef, double* rhs_perm, void* stream) {
+HDK_API int hdk_gather_pp(const hdk_vtx* x, const double* base_perm, const double* ef, double* rhs_perm,
+                          const int* run_flag, void* stream) {
   if (!x->pinc_off || !x->pinc) return static_cast<int>(cudaErrorInvalidValue);
-  hdk::launch(k_gather_pp, dim3(nb(8LL * x->n)), dim3(256), 0, S(stream), *x, base_perm, ef, rhs_perm);
+  hdk::launch(k_gather_pp, dim3(nb(8LL * x->n)), dim3(256), 0, S(stream), *x, base_perm, ef, rhs_perm, run_flag);
   return last();
 }
 
@@ -1162,22 +1215,33 @@ HDK_API int hdk_trace_epoch(unsigned long long* buf, void* stream) {
   return last();
 }
 
-HDK_API int hdk_bb_dots(const hdk_factor* f, hdk_ctl* ctl, hdk_ctl* snap, double* t_perm, const double* x_perm,
-                        double* last_q, double* last_g, double* dq, double* dg, double* partial, int mode,
-                        void* stream) {
+HDK_API int hdk_bb_dots(const hdk_factor* f, hdk_ctl* ctl, hdk_ctl* snap, double* t_perm, double* t_full,
+                        const double* x_perm, double* last_q, double* last_g, double* dq, double* dg, double* partial,
+                        int mode, void* stream) {
   int g1 = 0, g2 = 0;
   hdk_solve_grids(f, &g1, &g2);
   if (!f->tile_cta2 || g2 != f->grid2) return static_cast<int>(cudaErrorInvalidValue);
-  hdk::launch(k_bb_dots, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), f->n, *f, ctl, snap, t_perm, x_perm, last_q,
-              last_g, dq, dg, partial, mode);
+  hdk::launch(k_bb_dots, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), f->n, *f, ctl, snap, t_perm, t_full, x_perm,
+              last_q, last_g, dq, dg, partial, mode);
   return last();
 }
 
-HDK_API int hdk_bb_mix(const hdk_factor* f, hdk_ctl* ctl, const hdk_ctl* snap, const double* partial,
-                       const double* t_perm, double* x_perm, double* x_full, const double* dq, const double* dg,
-                       unsigned long long cond_handle, void* stream) {
-  hdk::launch(k_bb_mix, dim3(nb(3LL * f->n)), dim3(kT), 0, S(stream), f->n, f->p2v, ctl, snap, partial, t_perm, x_perm,
-              x_full, dq, dg, static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle != 0ULL ? 1 : 0);
+HDK_API int hdk_bb_solve(hdk_ctl* ctl, const hdk_ctl* snap, const double* partial, void* result,
+                         unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_bb_solve, dim3(1), dim3(kT), 0, S(stream), ctl, snap, partial, static_cast<AaResult*>(result),
+              static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle != 0ULL ? 1 : 0);
+  return last();
+}
+
+HDK_API size_t hdk_bb_result_bytes(void) { return sizeof(AaResult); }
+
+HDK_API int hdk_bb_mix(const hdk_factor* f, hdk_ctl* ctl, const hdk_ctl* snap, const void* result,
+                       const double* t_perm, double* x_perm, double* x_full, const double* sum_hist,
+                       const double* rt_perm, double* rx_perm, double* last_rx, double* last_rg, double* rsum_hist,
+                       const double* seed_perm, double* rhs_perm, void* stream) {
+  hdk::launch(k_bb_mix, dim3(nb(3LL * f->n)), dim3(kT), 0, S(stream), f->n, f->p2v, ctl, snap,
+              static_cast<const AaResult*>(result), t_perm, x_perm, x_full, sum_hist, rt_perm, rx_perm, last_rx,
+              last_rg, rsum_hist, seed_perm, rhs_perm);
   return last();
 }
 

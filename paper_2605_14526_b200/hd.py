@@ -74,6 +74,7 @@ SIGNATURES = {
     "hd_sim_time_solve": (C.c_int, [_VP, C.c_int, _D, _D]),
     "hd_sim_time_backbone": (C.c_int, [_VP, C.c_int, C.c_uint, _D]),
     "hd_sim_trace_backbone": (C.c_int, [_VP, C.c_int, _D, C.c_size_t]),
+    "hd_sim_trace_loop": (C.c_int, [_VP, _D, C.c_size_t, C.POINTER(C.c_int)]),
     "hd_batch_create": (_VP, [_VP, C.c_int, _D, C.c_size_t, C.c_int]),
     "hd_batch_free": (None, [_VP]),
     "hd_batch_sample_count": (C.c_int, [_VP]),
@@ -325,11 +326,19 @@ class Sim:
 
     def trace_backbone(self, reps: int = 8):
         """Per-iteration kernel timeline (profiling; see heterodyn.h): array
-        [reps, 12, 3] of ns (first resident, first past wait, last end)."""
+        [reps, 14, 3] of ns (first resident, first past wait, last end)."""
         import numpy as np
-        out = np.full(reps * 12 * 3, -1.0)
+        out = np.full(reps * 14 * 3, -1.0)
         self.L.check(self.L.lib.hd_sim_trace_backbone(self.h, reps, out.ctypes.data_as(_D), out.size))
-        return out.reshape(reps, 12, 3)
+        return out.reshape(reps, 14, 3)
+
+    def trace_loop(self):
+        """Records of the real backbone loop's last iterations (profiling)."""
+        import numpy as np
+        out = np.full(16 * 14 * 3, -1.0)
+        k = C.c_int()
+        self.L.check(self.L.lib.hd_sim_trace_loop(self.h, out.ctypes.data_as(_D), out.size, C.byref(k)))
+        return out[: k.value * 42].reshape(k.value, 14, 3)
 
     def solve_free(self, rhs, fixed_q=None):
         rhs = _f64(rhs, self.n)

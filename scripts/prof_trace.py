@@ -31,3 +31,19 @@ for it in range(4, 12):
         print("  AA dots: loop done %.2f  partials %.2f  | tail entry %.2f  folded %.2f  solved %.2f" %
               (t[10, 2] - base, t[11, 2] - base, t[7, 2] - base, t[8, 2] - base, t[9, 2] - base))
 print("iteration period (us):", " ".join(f"{p:.1f}" for p in per if p == p))
+
+# the real WHILE loop (unrolled body, conditional node)
+tl = sim.trace_loop()
+print(f"real loop: {len(tl)} traced iterations")
+starts = [tl[i][0, 1] / 1e3 for i in range(len(tl))]
+print("iteration period (us):", " ".join(f"{b - a:.1f}" for a, b in zip(starts, starts[1:])))
+for it in (len(tl) - 3, len(tl) - 2):
+    t = tl[it] / 1e3
+    base = t[0, 1]
+    print(f"loop iteration {it}: resident / start / end / busy")
+    for k, nm in enumerate(names):
+        print(f"  {nm:8s} {t[k, 0] - base:8.2f} {t[k, 1] - base:8.2f} {t[k, 2] - base:8.2f}  {t[k, 2] - t[k, 1]:7.2f}")
+for it in (len(tl) - 3, len(tl) - 2):
+    t = tl[it] / 1e3
+    base = t[0, 1]
+    print(f"loop iteration {it}: AA solve kernel resident {t[7, 0] - base:.2f} start {t[7, 1] - base:.2f} fold {t[8, 2] - base:.2f}  bookkeeping {t[12, 2] - base:.2f}  LDLT {t[13, 2] - base:.2f}  end {t[7, 2] - base:.2f}")
