@@ -561,7 +561,7 @@ def main():
             "config": {"workload": f"{args.config}: {scene_dict['name']} ({ne} tets, {sc.vertex_count} vertices, "
                                    f"{WORKLOADS.get(args.config.upper(), '')})",
                        "parallelism": "replicas" if world > 1 else "single",
-                       "factor": {"ordering": f"{args.ordering or 'nd-bfs'} (postordered)", "nnz_S": nnz, "free_vertices": sim.free_count,
+                       "factor": {"ordering": f"{args.ordering or 'nd-mvc'} (postordered)", "nnz_S": nnz, "free_vertices": sim.free_count,
                                   "build_s": t_fac},
                        "l2_policy": "inputs larger than L2 (factor values %.0f MB > 126 MB L2)" % (nnz * 8 / 1e6),
                        "mean_forward_iterations": float(np.mean(fwd_its)),

@@ -94,7 +94,7 @@ struct Scene {  // scene.hpp:14-34
   Vec q0, v0;
   std::vector<int> region;
   int region_count = 0;
-  std::string ordering = "nd-bfs";  // B200 extension: fill-reducing ordering of the factor
+  std::string ordering = "nd-mvc";  // B200 extension: fill-reducing ordering of the factor
 };
 Scene parse_scene(const std::string& text);
 Scene builtin_scene(const std::string& name);

@@ -600,8 +600,8 @@ void overrides(Scene& s, const json& j, bool gen, Errs& errs) {
   // B200 extension: {"factor": {"ordering": "nd-geometric" | "nd-bfs" | "metis"}}
   if (j.contains("factor") && j["factor"].is_object()) {
     const std::string o = j["factor"].value("ordering", s.ordering);
-    if (o != "nd-geometric" && o != "nd-bfs" && o != "metis")
-      errs.push_back("factor.ordering: expected \"nd-geometric\", \"nd-bfs\" or \"metis\"");
+    if (o != "nd-geometric" && o != "nd-bfs" && o != "metis" && o != "nd-mvc")
+      errs.push_back("factor.ordering: expected \"nd-geometric\", \"nd-bfs\", \"nd-mvc\" or \"metis\"");
     else s.ordering = o;
   }
 }
