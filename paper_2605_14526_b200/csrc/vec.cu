@@ -452,45 +452,62 @@ __device__ __noinline__ void aa_solve_block(const hdk_ctl* in, hdk_ctl* gctl, co
       nsol = n;
       const double ridge = 1e-6 * fro2 / m;
       // pivot order: largest |diagonal| among the remaining untouched ones,
-      // swapped into place (Eigen LDLT; warp-uniform, registers only)
-      int perm[M];
-      double dv[M];
+      // swapped into place (Eigen LDLT).  With distinct |diagonals| that is
+      // the descending order, found by ranks in one pass; ties (which the
+      // swaps resolve position-dependently) take the serial selection.
+      const double ad = lane < n ? fabs(mydiag + ridge) : -1.0;
+      int rank = 0;
+      bool tie = false;
 #pragma unroll
-      for (int i = 0; i < M; ++i) {
-        perm[i] = i;
-        dv[i] = __shfl_sync(F, mydiag, i) + ridge;
-      }
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        if (k < n) {
-          int piv = k;
-          double best = fabs(dv[k]);
-#pragma unroll
-          for (int i = k + 1; i < M; ++i)
-            if (i < n && fabs(dv[i]) > best) {
-              best = fabs(dv[i]);
-              piv = i;
-            }
-          const int pk = perm[k];
-          const double dk = dv[k];
-          int pp = pk;
-          double dp = dk;
-#pragma unroll
-          for (int i = k + 1; i < M; ++i)
-            if (i == piv) {
-              pp = perm[i];
-              dp = dv[i];
-              perm[i] = pk;
-              dv[i] = dk;
-            }
-          perm[k] = pp;
-          dv[k] = dp;
+      for (int j = 0; j < M; ++j) {
+        const double aj = __shfl_sync(F, ad, j);
+        if (j < n && lane < n) {
+          if (aj > ad) ++rank;
+          else if (aj == ad && j != lane) tie = true;
         }
       }
-      if (lane == 0) sridge = ridge;
+      if (!__any_sync(F, tie)) {
+        if (lane < n) sperm[rank] = lane;
+      } else {
+        int perm[M];
+        double dv[M];
 #pragma unroll
-      for (int i = 0; i < M; ++i)
-        if (lane == i) sperm[i] = perm[i];
+        for (int i = 0; i < M; ++i) {
+          perm[i] = i;
+          dv[i] = __shfl_sync(F, mydiag, i) + ridge;
+        }
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          if (k < n) {
+            int piv = k;
+            double best = fabs(dv[k]);
+#pragma unroll
+            for (int i = k + 1; i < M; ++i)
+              if (i < n && fabs(dv[i]) > best) {
+                best = fabs(dv[i]);
+                piv = i;
+              }
+            const int pk = perm[k];
+            const double dk = dv[k];
+            int pp = pk;
+            double dp = dk;
+#pragma unroll
+            for (int i = k + 1; i < M; ++i)
+              if (i == piv) {
+                pp = perm[i];
+                dp = dv[i];
+                perm[i] = pk;
+                dv[i] = dk;
+              }
+            perm[k] = pp;
+            dv[k] = dp;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+          if (lane == i) sperm[i] = perm[i];
+      }
+      if (lane == 0) sridge = ridge;
       if (lane < M)
 #pragma unroll
         for (int j = 0; j < M; ++j) sG[lane][j] = g[j];
