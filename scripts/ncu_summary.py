@@ -55,7 +55,7 @@ def report(path):
     return "\n".join(out)
 
 
-def traffic(path, kernels=("k_rowdot", "k_zreduce", "k_coltile", "k_xreduce")):
+def traffic(path, kernels=("k_rowdot", "k_zreduce", "k_coltile")):
     """DRAM bytes (read + write) of one 3-axis solve: the first capture of each
     solve kernel in a --set full report, summed."""
     txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
