@@ -210,6 +210,21 @@ __device__ __forceinline__ void ring_init(Ring<S>& r) {
 
 // Producer warp (one elected lane): keeps S chunks in flight; a stage is
 // refilled once all consumer warps have released it.
+// The first min(S, n) chunks are requested before the kernel's PDL wait: the
+// factor stream does not depend on the previous kernel, so the ring fills
+// while that kernel drains.  After the wait the producer honours the run
+// flag; an iteration that is skipped drains the requested stages first (no
+// bulk copy may be outstanding when the CTA exits).  Returns false if skipped.
+template <int S, class FullBars>
+__device__ __forceinline__ bool after_prefill(const hdk_factor& f, FullBars& full, int issued) {
+  hdk::pdl_wait();
+  if (f.run_flag && *f.run_flag == 0) {
+    for (int k = 0; k < issued; ++k) mbar_wait(&full[k % S], 0);
+    return false;
+  }
+  return true;
+}
+
 template <int S>
 __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_beg, int c_end, bool reverse) {
   if ((threadIdx.x & 31) != 0) return;
@@ -217,7 +232,10 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
   auto chunk_at = [&](int k) { return reverse ? c_end - 1 - k : c_beg + k; };
   hdk_chunk nxt = n > 0 ? f.chunk[chunk_at(0)] : hdk_chunk{};
   const uint64_t pol = policy_evict_first();
+  const int pre = n < S ? n : S;
+  if (pre == 0 && !after_prefill<S>(f, r.full, 0)) return;
   for (int k = 0; k < n; ++k) {
+    if (k == pre && !after_prefill<S>(f, r.full, pre)) return;
     const int st = k % S;
     const hdk_chunk ch = nxt;
     if (k + 1 < n) nxt = f.chunk[chunk_at(k + 1)];  // descriptor prefetch, off the critical path
@@ -232,6 +250,7 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
     }
     bulk_g2s(r.segs[st], f.seg + ch.seg0, sb, &r.full[st]);
   }
+  if (pre == n && n > 0) after_prefill<S>(f, r.full, n);
 }
 
 // Pass 2 ring: as Ring, plus the z rows of each staged chunk's segments,
@@ -289,7 +308,10 @@ __device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S>& r, int c_
   const int n = c_end - c_beg;
   hdk_chunk nxt = n > 0 ? f.chunk[c_end - 1] : hdk_chunk{};
   const uint64_t pol = policy_evict_first();
+  const int pre = n < S ? n : S;
+  if (pre == 0 && !after_prefill<S>(f, r.full, 0)) return;
   for (int k = 0; k < n; ++k) {
+    if (k == pre && !after_prefill<S>(f, r.full, pre)) return;
     const int st = k % S;
     const hdk_chunk ch = nxt;
     if (k + 1 < n) nxt = f.chunk[c_end - 2 - k];
@@ -304,6 +326,7 @@ __device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S>& r, int c_
     }
     bulk_g2s(r.segs[st], f.seg + ch.seg0, sb, &r.full[st]);
   }
+  if (pre == n && n > 0) after_prefill<S>(f, r.full, n);
 }
 
 // ---- pass 1 ------------------------------------------------------------------
@@ -313,9 +336,7 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages
 
 template <bool kDry = false>  // kDry: stream only (microbenchmarks)
 __global__ void __launch_bounds__(kThreads, 2) k_rowdot(hdk_factor f, const double* __restrict__ rhs) {
-  HDK_TRACED_WAIT(hdk::kTrRowdot);
-  hdk::pdl_trigger();
-  if (f.run_flag && *f.run_flag == 0) return;
+  hdk::pdl_trigger();  // the producer prefills before the PDL wait; consumers wait below
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<kStages1>& ring = *reinterpret_cast<Ring<kStages1>*>(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -328,6 +349,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowdot(hdk_factor f, const doub
     produce(f, ring, c_beg, c_end, false);
     return;
   }
+  HDK_TRACED_WAIT(hdk::kTrRowdot);
+  if (f.run_flag && *f.run_flag == 0) return;
   rowdot_consume<kDry>(f, ring, rhs, c_beg, c_end);
   if (trace) {
     consumers_sync();
@@ -480,9 +503,7 @@ __device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& s
 
 template <bool kDry = false>
 __global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
-  HDK_TRACED_WAIT(hdk::kTrColtile);
-  hdk::pdl_trigger();
-  if (f.run_flag && *f.run_flag == 0) return;
+  hdk::pdl_trigger();  // the producer prefills before the PDL wait; the others wait below
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Pass2Smem& sm = *reinterpret_cast<Pass2Smem*>(smem_raw);
   Ring2<kStages2>& ring = sm.ring;
@@ -498,6 +519,8 @@ __global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
     stream2(f, ring, c_beg, c_end);
     return;
   }
+  HDK_TRACED_WAIT(hdk::kTrColtile);
+  if (f.run_flag && *f.run_flag == 0) return;
   if (warp == kWarps + 1) {
     gather_z(f, ring, c_end - c_beg);
     return;
