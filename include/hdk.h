@@ -82,6 +82,7 @@ typedef struct hdk_factor {
   const hdk_chunk* chunk;
   const int* tile_chunk;  /* n_tiles+1: first chunk of each tile */
   const int* row_pslot;   /* n+1: partial-dot slots of row r */
+  int n_pslot;            /* row_pslot[n] */
   int n_ztask;
   const int2* ztask;      /* z-fold warp tasks: {row, -1} one long row, {first row, k} k <= 4 short rows */
   const int* p2v;         /* n: elimination position -> vertex */
@@ -119,6 +120,13 @@ HDK_API int hdk_solve_grids(const hdk_factor* f, int* grid1, int* grid2);
 /* Solve passes without the final fold: the tile partials stay in f->part2
  * for hdk_aa_dots_fused. */
 HDK_API int hdk_apply_inverse3_partial(const hdk_factor* f, const double* rhs_perm, void* stream);
+/* R independent right-hand sides (R = 1, 2, 4) through one stream of the
+ * factor: rhs_perm holds R vectors [n][3] back to back; part1, z and part2
+ * must be sized for R columns (column c's tile partials at
+ * part2 + c * hdk_factor_part2_stride(f)).  Leaves the tile partials for the
+ * callers' folds, like hdk_apply_inverse3_partial. */
+HDK_API int hdk_apply_inverse3_multi(const hdk_factor* f, const double* rhs_perm, int columns, void* stream);
+HDK_API size_t hdk_factor_part2_stride(const hdk_factor* f);
 /* Profiling only: hdk_apply_inverse3_partial with passes dropped (bit 0 row
  * dots, bit 1 z-fold, bit 2 column pass). */
 HDK_API int hdk_apply_inverse3_ablate(const hdk_factor* f, const double* rhs_perm, unsigned skip, void* stream);
@@ -246,6 +254,9 @@ HDK_API int hdk_bb_dots(const hdk_factor* f, hdk_ctl* ctl, hdk_ctl* snap, double
 HDK_API int hdk_bb_solve(hdk_ctl* ctl, const hdk_ctl* snap, const double* partial, void* result,
                          unsigned long long cond_handle, void* stream);
 HDK_API size_t hdk_bb_result_bytes(void);
+/* *any = OR over count (<= 32) control blocks of "still iterating"; sets the
+ * WHILE condition when cond_handle != 0 (multi-column contact adjoint). */
+HDK_API int hdk_any_cond(hdk_ctl* ctls, int count, int* any, unsigned long long cond_handle, void* stream);
 HDK_API int hdk_bb_mix(const hdk_factor* f, hdk_ctl* ctl, const hdk_ctl* snap, const void* result,
                        const double* t_perm, double* x_perm, double* x_full, const double* sum_hist,
                        const double* rt_perm, double* rx_perm, double* last_rx, double* last_rg, double* rsum_hist,

@@ -293,7 +293,11 @@ hd_status hd_sim_time_solve(hd_sim* sim, int reps, double* ms, double* bytes) {
 
 hd_status hd_sim_time_backbone(hd_sim* sim, int reps, unsigned skip_mask, double* ms) {
   if (!sim || !ms || reps < 1) return bad_arg("hd_sim_time_backbone: bad argument");
-  return guarded([&] { *ms = sim->eng->time_backbone(reps, skip_mask); });
+  return guarded([&] {
+    // bit 16: the multi-column contact-adjoint iteration instead (bits 17-18: skip solve / column kernels)
+    *ms = (skip_mask & 0x10000u) ? sim->eng->time_columns(reps, (skip_mask >> 17) & 3u)
+                                 : sim->eng->time_backbone(reps, skip_mask);
+  });
 }
 
 hd_status hd_sim_trace_backbone(hd_sim* sim, int reps, double* out, size_t capacity) {

@@ -72,6 +72,16 @@ cudaGraphExec_t instantiate(cudaGraph_t g) {
   return e;
 }
 
+
+cudaGraphExec_t capture_exec(cudaStream_t st, const std::function<void()>& fn, int* kernels) {
+  cudaGraph_t g = capture(st, fn);
+  if (kernels) *kernels = kernel_nodes(g);
+  cudaGraphExec_t e = instantiate(g);
+  cudaGraphDestroy(g);
+  return e;
+}
+}  // namespace
+
 void build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()>& pre,
                       const std::function<void(unsigned long long)>& body, const std::function<void()>& post,
                       LoopGraph& out) {
@@ -117,15 +127,6 @@ void build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()
   for (cudaGraph_t g : {gpre, gpost, top}) cudaGraphDestroy(g);
 }
 
-cudaGraphExec_t capture_exec(cudaStream_t st, const std::function<void()>& fn, int* kernels) {
-  cudaGraph_t g = capture(st, fn);
-  if (kernels) *kernels = kernel_nodes(g);
-  cudaGraphExec_t e = instantiate(g);
-  cudaGraphDestroy(g);
-  return e;
-}
-}  // namespace
-
 Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas)
     : scene_(scene), mat_(scene.material), solve_ctas_(solve_ctas) {
   if (const char* c = std::getenv("HETERODYN_SOLVE_CTAS")) solve_ctas_ = std::atoi(c);
@@ -170,11 +171,16 @@ void Engine::phase_collect(int first, int last) {
 }
 
 Engine::~Engine() {
+  cols_.reset();
   if (ph_.on && ph_.n > 0) {
     static const char* names[7] = {"forward (graph + commit)", "-", "-", "backward pre", "backbone loop", "backward post",
                                    "-"};
     std::fprintf(stderr, "[heterodyn phases] %lld steps\n", ph_.n);
     for (int i : {0, 3, 4, 5}) std::fprintf(stderr, "  %-26s %9.3f ms/step\n", names[i], ph_.ms[i] / ph_.n);
+    if (ph_.col_batches)
+      std::fprintf(stderr, "  contact columns: %lld batches of %d, %.3f ms total, %lld batched iterations "
+                   "(%.1f us each), %lld column iterations\n", ph_.col_batches, kColumns, ph_.col_ms,
+                   ph_.col_iters, 1e3 * ph_.col_ms / std::max(1LL, ph_.col_iters), ph_.col_real_iters);
   }
   for (cudaEvent_t e : ph_.ev)
     if (e) cudaEventDestroy(e);
@@ -338,6 +344,7 @@ void Engine::build_factor_device() {
   df_.chunk = ch;
   df_.tile_chunk = A.upload(F.tile_chunk);
   df_.row_pslot = A.upload(F.row_pslot);
+  df_.n_pslot = F.row_pslot.back();
   {  // z-fold warp tasks (solve.cu zfold_task)
     std::vector<int> zt;
     for (int r = 0; r < F.n;) {
@@ -961,6 +968,7 @@ void Engine::set_young(const Vec& young, bool freeze) {
   cuda_check(cudaStreamSynchronize(st_), "sync");
   hf_ = build_factor(scene_.mesh, mat_, scene_.solver.h, scene_.fixed, scene_.ordering);
   ++refactor_count;
+  cols_.reset();  // its graph bakes the old factor and material pointers
   // material arrays and factor live in fresh allocations; graphs bake pointers
   Vec q = positions(), v = velocities();
   const double t = time_;

@@ -9,6 +9,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -47,6 +48,12 @@ struct LoopGraph {
   }
 };
 
+
+// pre -> while(body) -> post as one executable graph with a device-driven
+// WHILE conditional node (engine.cpp).
+void build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()>& pre,
+                      const std::function<void(unsigned long long)>& body, const std::function<void()>& post,
+                      LoopGraph& out);
 
 // One step's contact set: host copy (reference layout) + device view, the
 // cached scalar inverse columns U = A_s^{-1} E of its unique vertices, and the
@@ -101,10 +108,28 @@ class Engine {
     cudaEvent_t ev[8] = {};
     double ms[8] = {};
     long long n = 0;
+    double col_ms = 0;  // contact columns: time, batches, batched and per-column iterations
+    long long col_batches = 0, col_iters = 0, col_real_iters = 0;
   } ph_;
   void phase_mark(int i);
   void phase_collect(int first, int last);
   void trace_backbone(int reps, std::vector<double>& out);
+  // Contact adjoint columns x_c = (A - B)^{-1} j_c (backward.cpp:229-238),
+  // kColumns at a time: one multi-column stream of the factor per iteration,
+  // each column's Anderson kernels on its own pair of streams
+  // (engine_columns.cpp).
+  static constexpr int kColumns = 4;
+  struct ColumnSet;
+  struct ColumnSetDeleter {
+    void operator()(ColumnSet* p) const;  // engine_columns.cpp
+  };
+  std::unique_ptr<ColumnSet, ColumnSetDeleter> cols_;
+  void build_columns();
+  // Solves rows [r0, r0 + kColumns) of contact frame c (rows past k repeat
+  // the last one); returns the iterations of the real columns.
+  int solve_columns(const ContactFrame& c, int r0);
+  void columns_body(unsigned long long cond_handle, unsigned skip);
+  double time_columns(int reps, unsigned skip);  // profiling: ms per multi-column iteration
   void trace_loop(std::vector<double>& out);
   unsigned long long* loop_trace_ = nullptr;  // set only while trace_loop runs
   int last_backward_iterations_ = 0;

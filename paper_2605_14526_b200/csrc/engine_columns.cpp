@@ -1,0 +1,222 @@
+// Contact adjoint columns, several at a time (reference backward.cpp:229-238:
+// x_c = (A - B)^{-1} j_c warm-started from the cached A^{-1} j_c, one
+// backbone fixed point per contact row).  Each column runs exactly the
+// single-column backbone of engine.cpp (same kernels, same Anderson state
+// layout, its own control block), but the global solve of all kColumns
+// columns is one multi-column stream of the factor (hdk_apply_inverse3_multi),
+// and the columns' vector kernels run on their own streams between two
+// solves.  The loop runs while any column is active; a column past
+// convergence skips its kernels (its control block's cond is 0).
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace hdb {
+
+static void hdk_ok(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
+
+struct Engine::ColumnSet {
+  struct Col {
+    hdk_ctl* ctl = nullptr;  // = ctls + c
+    hdk_ctl* snap = nullptr;
+    void* res = nullptr;
+    double *seed = nullptr, *x = nullptr, *seedp = nullptr, *xp = nullptr, *t = nullptr, *tv = nullptr;
+    double *lastq = nullptr, *lastg = nullptr, *dq = nullptr, *dg = nullptr;
+    double *rt = nullptr, *rx = nullptr, *lrx = nullptr, *lrg = nullptr, *rsq = nullptr, *ef = nullptr, *part = nullptr;
+    hdk_factor f{};  // the multi-column factor view of this column (part2 offset)
+    cudaStream_t s1 = nullptr, s2 = nullptr;
+    cudaEvent_t fork = nullptr, mid = nullptr, join = nullptr, end = nullptr;
+  };
+  std::unique_ptr<DevArena> mem;
+  hdk_factor f{};  // df_ with kColumns columns of solve scratch
+  Col col[kColumns];
+  hdk_ctl* ctls = nullptr;
+  hdk_ctl* h_ctls = nullptr;  // pinned mirror
+  double* rhs = nullptr;      // kColumns x 3n
+  int* any = nullptr;         // OR of the columns' cond
+  int* h_any = nullptr;
+  LoopGraph graph;
+  ~ColumnSet() {
+    graph.destroy();
+    for (Col& c : col) {
+      for (cudaEvent_t e : {c.fork, c.mid, c.join, c.end})
+        if (e) cudaEventDestroy(e);
+      for (cudaStream_t st : {c.s1, c.s2})
+        if (st) cudaStreamDestroy(st);
+    }
+    if (h_ctls) cudaFreeHost(h_ctls);
+    if (h_any) cudaFreeHost(h_any);
+  }
+};
+
+void Engine::ColumnSetDeleter::operator()(ColumnSet* p) const { delete p; }
+
+void Engine::build_columns() {
+  cols_.reset(new ColumnSet());
+  ColumnSet& S = *cols_;
+  S.mem = std::make_unique<DevArena>();
+  DevArena& A = *S.mem;
+  const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), n3p = 3 * static_cast<size_t>(hf_.n),
+               ne = scene_.mesh.ne;
+  S.f = df_;
+  S.f.part1 = A.alloc<double>(kColumns * 3 * static_cast<size_t>(df_.n_pslot));
+  S.f.z = A.alloc<double>(kColumns * n3p);
+  const size_t p2 = hdk_factor_part2_stride(&df_);
+  S.f.part2 = A.alloc<double>(kColumns * p2);
+  S.ctls = A.alloc<hdk_ctl>(kColumns);
+  S.rhs = A.alloc<double>(kColumns * n3p);
+  S.any = A.alloc<int>(1);
+  S.f.run_flag = S.any;
+  cuda_check(cudaMallocHost(&S.h_ctls, sizeof(hdk_ctl) * kColumns), "pinned ctl");
+  cuda_check(cudaMallocHost(&S.h_any, sizeof(int)), "pinned flag");
+  for (int c = 0; c < kColumns; ++c) {
+    ColumnSet::Col& C = S.col[c];
+    C.ctl = S.ctls + c;
+    C.snap = A.alloc<hdk_ctl>(1);
+    C.res = A.raw(hdk_bb_result_bytes());
+    C.seed = A.alloc<double>(n3);
+    C.x = A.alloc<double>(n3);
+    C.tv = A.alloc<double>(n3);
+    for (double** v : {&C.seedp, &C.xp, &C.t, &C.lastq, &C.lastg, &C.rt, &C.rx, &C.lrx, &C.lrg}) *v = A.alloc<double>(n3p);
+    C.dq = A.alloc<double>(HDK_AA_MAX * n3p);
+    C.dg = A.alloc<double>(HDK_AA_MAX * n3p);
+    C.rsq = A.alloc<double>(HDK_AA_MAX * n3p);
+    C.ef = A.alloc<double>(12 * ne);
+    C.part = A.alloc<double>(HDK_RED_BLOCKS * HDK_RED_Q);
+    C.f = S.f;
+    C.f.part2 = S.f.part2 + c * p2;
+    C.f.run_flag = nullptr;
+    cuda_check(cudaStreamCreateWithFlags(&C.s1, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&C.s2, cudaStreamNonBlocking), "stream");
+    for (cudaEvent_t* e : {&C.fork, &C.mid, &C.join, &C.end})
+      cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+  }
+  void* s = st_;
+  // first right-hand sides seed + R(x0) of every column
+  auto pre = [&] {
+    for (int c = 0; c < kColumns; ++c) {
+      ColumnSet::Col& C = S.col[c];
+      hdk_ok(hdk_aa_reset(C.ctl, HDK_AA_MAX, 1e8, 500, 1e-10, s), "aa reset");
+      hdk_ok(hdk_gather_perm(&dv_, C.seed, nullptr, C.seedp, s), "seed in elimination order");
+      hdk_ok(hdk_gather_perm(&dv_, C.x, nullptr, C.xp, s), "x0 in elimination order");
+      hdk_ok(hdk_bapply(&dm_, dcomp_, C.x, C.ef, s), "B x0");
+      hdk_ok(hdk_gather_pp(&dv_, nullptr, C.ef, C.rx, nullptr, s), "R(x0)");
+      hdk_ok(hdk_axpby(static_cast<int>(n3p), 1.0, C.seedp, 1.0, C.rx, S.rhs + c * n3p, s), "rhs0");
+    }
+    hdk_ok(hdk_any_cond(S.ctls, kColumns, S.any, 0ULL, s), "any");
+  };
+  auto body = [&](unsigned long long handle) {
+    for (int u = 0; u < unroll_; ++u) columns_body(handle, 0u);
+  };
+  build_loop_graph(st_, use_cond_, pre, body, [] {}, S.graph);
+}
+
+// One multi-column iteration; skip bits (profiling): 1 solve, 2 column kernels.
+void Engine::columns_body(unsigned long long handle, unsigned skip) {
+  ColumnSet& S = *cols_;
+  void* s = st_;
+  const size_t n3p = 3 * static_cast<size_t>(hf_.n);
+  {
+    {
+      if (!(skip & 1u)) hdk_ok(hdk_apply_inverse3_multi(&S.f, S.rhs, kColumns, s), "multi-column solve");
+      for (int c = 0; c < kColumns && !(skip & 2u); ++c) {
+        ColumnSet::Col& C = S.col[c];
+        cuda_check(cudaEventRecord(C.fork, st_), "fork");
+        cuda_check(cudaStreamWaitEvent(C.s1, C.fork, 0), "fork wait");
+        hdk_ok(hdk_bb_dots(&C.f, C.ctl, C.snap, C.t, C.tv, C.xp, C.lastq, C.lastg, C.dq, C.dg, C.part, 1, C.s1), "dots");
+        cuda_check(cudaEventRecord(C.mid, C.s1), "mid");
+        cuda_check(cudaStreamWaitEvent(C.s2, C.mid, 0), "mid wait");
+        hdk_ok(hdk_bb_solve(C.ctl, C.snap, C.part, C.res, 0ULL, C.s2), "coefficients");
+        cuda_check(cudaEventRecord(C.join, C.s2), "join");
+        hdk_ok(hdk_bapply_flag(&dm_, dcomp_, C.tv, C.ef, &C.snap->cond, C.s1), "B t");
+        hdk_ok(hdk_gather_pp(&dv_, nullptr, C.ef, C.rt, &C.snap->cond, C.s1), "R(t)");
+        cuda_check(cudaStreamWaitEvent(C.s1, C.join, 0), "join wait");
+        hdk_ok(hdk_bb_mix(&C.f, C.ctl, C.snap, C.res, C.t, C.xp, C.x, C.dq, C.rt, C.rx, C.lrx, C.lrg, C.rsq, C.seedp,
+                          S.rhs + c * n3p, C.s1),
+               "mix");
+        cuda_check(cudaEventRecord(C.end, C.s1), "end");
+        cuda_check(cudaStreamWaitEvent(st_, C.end, 0), "end wait");
+      }
+      hdk_ok(hdk_any_cond(S.ctls, kColumns, S.any, handle, s), "any");
+    }
+  }
+}
+
+double Engine::time_columns(int reps, unsigned skip) {
+  if (!cols_) build_columns();
+  cudaGraphExec_t g = nullptr;
+  {
+    cudaGraph_t gr = nullptr;
+    cuda_check(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "capture");
+    columns_body(0ULL, skip);
+    cuda_check(cudaStreamEndCapture(st_, &gr), "capture");
+    cuda_check(cudaGraphInstantiate(&g, gr, 0), "instantiate");
+    cudaGraphDestroy(gr);
+  }
+  cudaEvent_t a, b;
+  cuda_check(cudaEventCreate(&a), "event");
+  cuda_check(cudaEventCreate(&b), "event");
+  for (int i = 0; i < 3; ++i) cuda_check(cudaGraphLaunch(g, st_), "warm");
+  cuda_check(cudaEventRecord(a, st_), "event");
+  for (int i = 0; i < reps; ++i) cuda_check(cudaGraphLaunch(g, st_), "timed");
+  cuda_check(cudaEventRecord(b, st_), "event");
+  cuda_check(cudaEventSynchronize(b), "sync");
+  float ms = 0.f;
+  cuda_check(cudaEventElapsedTime(&ms, a, b), "elapsed");
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaGraphExecDestroy(g);
+  return static_cast<double>(ms) / reps;
+}
+
+int Engine::solve_columns(const ContactFrame& c, int r0) {
+  if (!cols_) build_columns();
+  ColumnSet& S = *cols_;
+  const int n = hf_.n, nv = scene_.mesh.nv;
+  for (int j = 0; j < kColumns; ++j) {
+    const int row = std::min(r0 + j, c.k - 1);
+    hdk_ok(hdk_contact_column_init(&c.view, row, nv, df_.v2p, c.U, n, S.col[j].seed, S.col[j].x, st_), "column init");
+  }
+  kernel_launches += kColumns;
+  if (ph_.on) cuda_check(cudaEventRecord(ph_.ev[6], st_), "phase event");
+  if (S.graph.exec) {
+    cuda_check(cudaGraphLaunch(S.graph.exec, st_), "columns");
+  } else {  // host-driven loop (profiling fallback)
+    if (S.graph.pre) cuda_check(cudaGraphLaunch(S.graph.pre, st_), "columns");
+    for (;;) {
+      cuda_check(cudaGraphLaunch(S.graph.body, st_), "columns");
+      cuda_check(cudaMemcpyAsync(S.h_any, S.any, sizeof(int), cudaMemcpyDeviceToHost, st_), "flag");
+      cuda_check(cudaStreamSynchronize(st_), "sync");
+      if (!*S.h_any) break;
+    }
+  }
+  if (ph_.on) cuda_check(cudaEventRecord(ph_.ev[7], st_), "phase event");
+  cuda_check(cudaMemcpyAsync(S.h_ctls, S.ctls, sizeof(hdk_ctl) * kColumns, cudaMemcpyDeviceToHost, st_), "ctl read");
+  cuda_check(cudaStreamSynchronize(st_), "columns sync");
+  if (ph_.on) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ph_.ev[6], ph_.ev[7]) == cudaSuccess) ph_.col_ms += ms;
+  }
+  int iters = 0, most = 0;
+  const size_t n3 = 3 * static_cast<size_t>(nv);
+  for (int j = 0; j < kColumns && r0 + j < c.k; ++j) {
+    hdk_ctl& h = S.h_ctls[j];
+    if (h.err == 0 && h.nonfinite) h.err = 10;
+    if (h.err != 0) {
+      std::memcpy(h_ctl_, &h, sizeof(hdk_ctl));
+      check_ctl("backward step (contact column)");
+    }
+    iters += h.iterations;
+    most = std::max(most, h.iterations);
+    cuda_check(cudaMemcpyAsync(cX_ + n3 * (r0 + j), S.col[j].x, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st_),
+               "column");
+  }
+  kernel_launches += S.graph.counts[0] + static_cast<long long>(S.graph.counts[1]) * ((most + unroll_ - 1) / unroll_);
+  ph_.col_batches += 1;
+  ph_.col_iters += most;
+  ph_.col_real_iters += iters;
+  return iters;
+}
+
+}  // namespace hdb

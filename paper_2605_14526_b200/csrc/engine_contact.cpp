@@ -255,7 +255,7 @@ void Engine::backward_frame(int t, GradOut& out) {
   out.rho[t] = h_ctl_->rho;
   ContactFrame* c = f.contacts && f.contacts->k > 0 ? f.contacts.get() : nullptr;
   if (c) {
-    const int k = c->k, n = hf_.n, nv = scene_.mesh.nv;
+    const int k = c->k;
     if (cX_cols_ < static_cast<size_t>(k)) {
       if (cX_) cudaFree(cX_);
       cuda_check(cudaMalloc(&cX_, sizeof(double) * n3 * k), "contact columns");
@@ -263,17 +263,9 @@ void Engine::backward_frame(int t, GradOut& out) {
     }
     if (!cz0_) cuda_check(cudaMalloc(&cz0_, sizeof(double) * n3), "z0");
     cuda_check(cudaMemcpyAsync(cz0_, x_, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st_), "z0");
-    // tangent columns x_c = (A - B)^{-1} j_c warm-started from a_c (backward.cpp:229-238)
-    for (int r = 0; r < k; ++r) {
-      hdk_check(hdk_contact_column_init(&c->view, r, nv, df_.v2p, c->U, n, seed_, x_, st_), "column init");
-      run_graph(*bgraph_, "backbone column");
-      sync_ctl();
-      check_ctl("backward step");
-      iters += h_ctl_->iterations;
-      kernel_launches += 1 + bgraph_->counts[0] +
-                         static_cast<long long>(bk_body_) * ((h_ctl_->iterations + unroll_ - 1) / unroll_);
-      cuda_check(cudaMemcpyAsync(cX_ + n3 * r, x_, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st_), "column");
-    }
+    // tangent columns x_c = (A - B)^{-1} j_c warm-started from a_c (backward.cpp:229-238),
+    // kColumns at a time through one multi-column stream of the factor
+    for (int r = 0; r < k; r += kColumns) iters += solve_columns(*c, r);
     ensure_solver_workspace(k);
     auto hnd = static_cast<cusolverDnHandle_t>(cusolver_);
     hdk_check(hdk_contact_reduced(&c->view, cX_, n3, c->omega, c->e_diag, cz0_, cM_, crhs_, st_), "reduced");

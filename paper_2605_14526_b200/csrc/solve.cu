@@ -126,8 +126,10 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // the few long rows as a 4x longer tail).  Fixed lane split and shuffle
 // tree: bitwise reproducible.
 constexpr int kZLong = 3;  // partials per lane held in flight (long rows up to 96 partials per round)
-__device__ __forceinline__ void zfold_task(const hdk_factor& f, int2 task) {
+__device__ __forceinline__ void zfold_task(const hdk_factor& f, int2 task, int column) {
   const int lane = threadIdx.x & 31;
+  const double* part1 = f.part1 + (size_t)column * 3 * (size_t)f.n_pslot;
+  double* zc = f.z + (size_t)column * 3 * (size_t)f.n;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   int r, stride, s0, s1;
   bool writer;
@@ -149,7 +151,7 @@ __device__ __forceinline__ void zfold_task(const hdk_factor& f, int2 task) {
 #pragma unroll
     for (int k = 0; k < kZLong; ++k) {
       const int sk = s + k * stride;
-      const double* p = f.part1 + 3 * (size_t)sk;
+      const double* p = part1 + 3 * (size_t)sk;
       v[k][0] = sk < s1 ? __ldg(p) : 0.0;
       v[k][1] = sk < s1 ? __ldg(p + 1) : 0.0;
       v[k][2] = sk < s1 ? __ldg(p + 2) : 0.0;
@@ -169,11 +171,19 @@ __device__ __forceinline__ void zfold_task(const hdk_factor& f, int2 task) {
     a2 += __shfl_xor_sync(0xffffffffu, a2, o);
   }
   if (writer) {
-    double* z = f.z + 3 * (size_t)r;
+    double* z = zc + 3 * (size_t)r;
     z[0] = a0;
     z[1] = a1;
     z[2] = a2;
   }
+}
+
+// Multi-column solves (hdk_apply_inverse3_multi): R independent 3-vector
+// right-hand sides share one stream of the factor.  Column c's rhs / z live at
+// +c * 3n, its row partials at +c * 3 * n_pslot, its tile partials at
+// +c * part2_stride(f).
+__host__ __device__ __forceinline__ size_t part2_stride(const hdk_factor& f) {
+  return 3 * (size_t)f.tile_w * (size_t)(f.n_tiles + f.max_ctas);
 }
 
 // Balanced contiguous chunk ranges: CTA b of G owns [first(b), first(b+1)).
@@ -256,19 +266,19 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
 // Pass 2 ring: as Ring, plus the z rows of each staged chunk's segments,
 // gathered into shared memory by the producer warp (zfull) so the consumers
 // never wait on a global load.
-template <int S>
+template <int S, int R>
 struct Ring2 {
   double vals[S][kVals];
   hdk_seg segs[S][kSegs];
-  double zs[S][kSegs][3];
+  double zs[S][kSegs][3 * R];
   ChunkInfo info[S];
   uint64_t full[S];
   uint64_t zfull[S];
   uint64_t empty[S];
 };
 
-template <int S>
-__device__ __forceinline__ void ring2_init(Ring2<S>& r) {
+template <int S, int R>
+__device__ __forceinline__ void ring2_init(Ring2<S, R>& r) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&r.full[s], 1);
@@ -285,25 +295,29 @@ __device__ __forceinline__ void ring2_init(Ring2<S>& r) {
 // gathers the z rows of its segments into zs with asynchronous 8-byte copies
 // that complete on zfull, so neither the stream nor the consumers wait on a
 // dependent global load.
-template <int S>
-__device__ __forceinline__ void gather_z(const hdk_factor& f, Ring2<S>& r, int n) {
+template <int S, int R>
+__device__ __forceinline__ void gather_z(const hdk_factor& f, Ring2<S, R>& r, int n) {
   const int lane = threadIdx.x & 31;
   for (int j = 0; j < n; ++j) {
     const int st = j % S;
     mbar_wait(&r.full[st], (j / S) & 1);
     const int nseg = r.info[st].nseg;
     for (int i = lane; i < nseg; i += 32) {
-      const double* z = f.z + 3 * (size_t)r.segs[st][i].row;
-      cp_async8(&r.zs[st][i][0], z);
-      cp_async8(&r.zs[st][i][1], z + 1);
-      cp_async8(&r.zs[st][i][2], z + 2);
+      const size_t row = 3 * (size_t)r.segs[st][i].row;
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+        const double* z = f.z + (size_t)c * 3 * (size_t)f.n + row;
+        cp_async8(&r.zs[st][i][3 * c], z);
+        cp_async8(&r.zs[st][i][3 * c + 1], z + 1);
+        cp_async8(&r.zs[st][i][3 * c + 2], z + 2);
+      }
     }
     cp_async_arrive(&r.zfull[st]);
   }
 }
 
-template <int S>
-__device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S>& r, int c_beg, int c_end) {
+template <int S, int R>
+__device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S, R>& r, int c_beg, int c_end) {
   if ((threadIdx.x & 31) != 0) return;
   const int n = c_end - c_beg;
   hdk_chunk nxt = n > 0 ? f.chunk[c_end - 1] : hdk_chunk{};
@@ -330,11 +344,14 @@ __device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S>& r, int c_
 }
 
 // ---- pass 1 ------------------------------------------------------------------
-template <bool kDry>
+template <bool kDry, int R>
 __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages1>& ring, const double* __restrict__ rhs,
                                                int c_beg, int c_end);
 
-template <bool kDry = false>  // kDry: stream only (microbenchmarks)
+// R columns: consumer warp w serves column w / (8 / R) and every (8 / R)-th
+// segment pair of each staged chunk, so the chunk is streamed once for all R
+// columns and a warp still holds one column's right-hand side tile.
+template <bool kDry = false, int R = 1>  // kDry: stream only (microbenchmarks)
 __global__ void __launch_bounds__(kThreads, 2) k_rowdot(hdk_factor f, const double* __restrict__ rhs) {
   hdk::pdl_trigger();  // the producer prefills before the PDL wait; consumers wait below
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -351,17 +368,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowdot(hdk_factor f, const doub
   }
   HDK_TRACED_WAIT(hdk::kTrRowdot);
   if (f.run_flag && *f.run_flag == 0) return;
-  rowdot_consume<kDry>(f, ring, rhs, c_beg, c_end);
+  rowdot_consume<kDry, R>(f, ring, rhs, c_beg, c_end);
   if (trace) {
     consumers_sync();
     if (threadIdx.x == 0) trace[2 * blockIdx.x + 1] = globaltimer();
   }
 }
 
-template <bool kDry>
+template <bool kDry, int R>
 __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages1>& ring, const double* __restrict__ rhs,
                                                int c_beg, int c_end) {
+  constexpr int WPC = kWarps / R;  // consumer warps per column
+  static_assert(WPC * R == kWarps, "columns must divide the consumer warps");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int colr = warp / WPC, sub = warp % WPC;
+  rhs += (size_t)colr * 3 * (size_t)f.n;
+  double* const part1 = f.part1 + (size_t)colr * 3 * (size_t)f.n_pslot;
   double b0[kM], b1[kM], b2[kM];
   int tile = -1;
   for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
@@ -386,7 +408,7 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages
     // registers, so the producer refills it while the arithmetic runs.
     const int npair = (ch.nseg + 1) >> 1;
     bool released = false;
-    for (int pi = (warp - (ch.seg0 >> 1)) & (kWarps - 1); pi < (kDry ? 0 : npair); pi += kWarps) {
+    for (int pi = (sub - (ch.seg0 >> 1)) & (WPC - 1); pi < (kDry ? 0 : npair); pi += WPC) {
       const int ia = 2 * pi, ib = ia + 1;
       const bool hasb = ib < ch.nseg;
       const hdk_seg sa = ring.segs[st][ia];
@@ -402,7 +424,7 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages
         wa[m] = (cl >= la && cl < ha) ? va[cl] : 0.0;
         wb[m] = (cl >= lb && cl < hb) ? vb[cl] : 0.0;
       }
-      if (pi + kWarps >= npair) {
+      if (pi + WPC >= npair) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&ring.empty[st]);
         released = true;
@@ -419,6 +441,8 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages
       }
       // reduce-scatter: lanes 0-15 keep segment a, lanes 16-31 segment b
       // after the first exchange, so the pair costs 15 shuffles, not 30
+      // (a full butterfly over the six sums, 8 shuffles, measured slower:
+      // more live registers, spills)
       const bool lo = lane < 16;
       double k0 = lo ? a0 : c0, k1 = lo ? a1 : c1, k2 = lo ? a2 : c2;
       k0 += __shfl_xor_sync(0xffffffffu, lo ? c0 : a0, 16);
@@ -431,7 +455,7 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages
         k2 += __shfl_xor_sync(0xffffffffu, k2, o);
       }
       if (lane == 0 || (lane == 16 && hasb)) {
-        double* p = f.part1 + 3 * (size_t)(lane == 0 ? sa.pslot : sb.pslot);
+        double* p = part1 + 3 * (size_t)(lane == 0 ? sa.pslot : sb.pslot);
         p[0] = k0;
         p[1] = k1;
         p[2] = k2;
@@ -451,47 +475,62 @@ __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
   hdk::pdl_trigger();
   if (f.run_flag && *f.run_flag == 0) return;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (t < f.n_ztask) zfold_task(f, __ldg(f.ztask + t));
+  if (t < f.n_ztask) zfold_task(f, __ldg(f.ztask + t), blockIdx.y);
 }
 
 // ---- pass 2 ------------------------------------------------------------------
+// Ring depth of pass 2 for R columns (the z rows of every column are staged
+// with each chunk; 227 KB of shared memory per CTA).
+template <int R>
+struct Stages2 {
+  static constexpr int value = R == 1 ? kStages2 : R == 2 ? 4 : 3;
+};
+
+template <int R>
 struct Pass2Smem {
-  Ring2<kStages2> ring;
+  Ring2<Stages2<R>::value, R> ring;
   double fold[kWarps / 2][3][kW];
 };
 
 // Fixed-order fold of the consumer warps' accumulators (4..7 into 0..3, 2..3
-// into 0..1, 1 into 0) and write of the tile partial; consumer warps only.
-__device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& sm, int slot, double (&x0)[kM],
+// into 0..1, 1 into 0; with R columns within each column's 8 / R warps) and
+// write of the tile partial; consumer warps only.
+template <int R>
+__device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem<R>& sm, int slot, double (&x0)[kM],
                                                double (&x1)[kM], double (&x2)[kM]) {
+  constexpr int WPC = kWarps / R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int colr = warp / WPC, sub = warp % WPC;
 #pragma unroll
-  for (int half = kWarps / 2; half >= 1; half >>= 1) {
+  for (int half = WPC / 2; half >= 1; half >>= 1) {
     consumers_sync();
-    if (warp >= half && warp < 2 * half) {
+    if (sub >= half && sub < 2 * half) {
+      const int fb = colr * (WPC / 2) + sub - half;
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
-        sm.fold[warp - half][0][cl] = x0[m];
-        sm.fold[warp - half][1][cl] = x1[m];
-        sm.fold[warp - half][2][cl] = x2[m];
+        sm.fold[fb][0][cl] = x0[m];
+        sm.fold[fb][1][cl] = x1[m];
+        sm.fold[fb][2][cl] = x2[m];
       }
     }
     consumers_sync();
-    if (warp < half) {
+    if (sub < half) {
+      const int fb = colr * (WPC / 2) + sub;
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
-        x0[m] += sm.fold[warp][0][cl];
-        x1[m] += sm.fold[warp][1][cl];
-        x2[m] += sm.fold[warp][2][cl];
+        x0[m] += sm.fold[fb][0][cl];
+        x1[m] += sm.fold[fb][1][cl];
+        x2[m] += sm.fold[fb][2][cl];
       }
     }
   }
-  if (warp == 0) {
+  if (sub == 0) {
+    double* const part2 = f.part2 + (size_t)colr * part2_stride(f);
 #pragma unroll
     for (int m = 0; m < kM; ++m) {
-      double* p = f.part2 + 3 * ((size_t)slot * kW + lane + 32 * m);
+      double* p = part2 + 3 * ((size_t)slot * kW + lane + 32 * m);
       p[0] = x0[m];
       p[1] = x1[m];
       p[2] = x2[m];
@@ -501,12 +540,13 @@ __device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem& s
   for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
 }
 
-template <bool kDry = false>
+template <bool kDry = false, int R = 1>
 __global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
+  constexpr int S = Stages2<R>::value, WPC = kWarps / R;
   hdk::pdl_trigger();  // the producer prefills before the PDL wait; the others wait below
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Pass2Smem& sm = *reinterpret_cast<Pass2Smem*>(smem_raw);
-  Ring2<kStages2>& ring = sm.ring;
+  Pass2Smem<R>& sm = *reinterpret_cast<Pass2Smem<R>*>(smem_raw);
+  Ring2<S, R>& ring = sm.ring;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long* trace = HDK_TRACE_PTR;
   if (trace && threadIdx.x == 0) trace[2 * blockIdx.x] = globaltimer();
@@ -530,20 +570,21 @@ __global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
   for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
   int tile = -1;
   for (int k = 0; k < c_end - c_beg; ++k) {
-    const int st = k % kStages2;
-    mbar_wait(&ring.zfull[st], (k / kStages2) & 1);
+    const int st = k % S;
+    mbar_wait(&ring.zfull[st], (k / S) & 1);
     const ChunkInfo ch = ring.info[st];
     if (ch.tile != tile) {  // partial of the previous tile: slot tile + b is unique
       if (tile >= 0) fold_and_write(f, sm, tile + blockIdx.x, x0, x1, x2);
       tile = ch.tile;
     }
     const double* vals = ring.vals[st];
-    const int i0 = (warp - ch.seg0) & (kWarps - 1);
-    for (int i = i0; i < (kDry ? 0 : ch.nseg); i += kWarps) {
+    const int i0 = (warp % WPC - ch.seg0) & (WPC - 1);
+    const int zc = 3 * (warp / WPC);
+    for (int i = i0; i < (kDry ? 0 : ch.nseg); i += WPC) {
       const hdk_seg sg = ring.segs[st][i];
       const int lo = sg.clo_len & 0xffff, hi = lo + (sg.clo_len >> 16);
       const double* v = vals + sg.coff - lo;
-      const double z0 = ring.zs[st][i][0], z1 = ring.zs[st][i][1], z2 = ring.zs[st][i][2];
+      const double z0 = ring.zs[st][i][zc], z1 = ring.zs[st][i][zc + 1], z2 = ring.zs[st][i][zc + 2];
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
@@ -596,9 +637,15 @@ struct Grids {
 // One resident wave per pass, computed once per process (thread-safe static).
 const Grids& grids() {
   static const Grids g = [] {
-    const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem);
+    const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem<1>);
     cudaFuncSetAttribute(k_rowdot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
     cudaFuncSetAttribute(k_coltile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s2));
+    cudaFuncSetAttribute(k_rowdot<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
+    cudaFuncSetAttribute(k_rowdot<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
+    cudaFuncSetAttribute(k_coltile<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(Pass2Smem<2>)));
+    cudaFuncSetAttribute(k_coltile<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(Pass2Smem<4>)));
     int dev = 0, sms = 148, b1 = 1, b2 = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -617,11 +664,25 @@ void pick_grids(const hdk_factor* f, int& g1, int& g2) {
   if (g2 > f->max_ctas) g2 = f->max_ctas;
 }
 
+// R-column passes only (tile partials left in part2 for the callers' folds).
+template <int R>
+int launch_multi(const hdk_factor* f, const double* rhs, cudaStream_t st) {
+  if (f->n <= 0) return 0;
+  if (f->tile_w != kW) return static_cast<int>(cudaErrorInvalidValue);
+  int g1, g2;
+  pick_grids(f, g1, g2);
+  if (g1 != f->grid1 || g2 != f->grid2) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_rowdot<false, R>, dim3(g1), dim3(kThreads), sizeof(Ring<kStages1>), st, *f, rhs);
+  hdk::launch(k_zreduce, dim3((f->n_ztask + 7) / 8, R), dim3(256), 0, st, *f);
+  hdk::launch(k_coltile<false, R>, dim3(g2), dim3(kThreads2), sizeof(Pass2Smem<R>), st, *f);
+  return static_cast<int>(cudaGetLastError());
+}
+
 int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatter, cudaStream_t st,
            bool fold = true, unsigned skip = 0u) {
   if (f->n <= 0) return 0;
   if (f->tile_w != kW) return static_cast<int>(cudaErrorInvalidValue);
-  const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem);
+  const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem<1>);
   int g1, g2;
   pick_grids(f, g1, g2);
   hdk_factor fl = *f;  // balanced ranges only if they were built for these grids
@@ -664,6 +725,18 @@ HDK_API int hdk_apply_inverse3_partial(const hdk_factor* f, const double* rhs_pe
 HDK_API int hdk_apply_inverse3_ablate(const hdk_factor* f, const double* rhs_perm, unsigned skip, void* stream) {
   return launch(f, rhs_perm, nullptr, true, static_cast<cudaStream_t>(stream), false, skip);
 }
+
+HDK_API int hdk_apply_inverse3_multi(const hdk_factor* f, const double* rhs_perm, int columns, void* stream) {
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (columns) {
+    case 1: return launch(f, rhs_perm, nullptr, true, st, false);
+    case 2: return launch_multi<2>(f, rhs_perm, st);
+    case 4: return launch_multi<4>(f, rhs_perm, st);
+    default: return static_cast<int>(cudaErrorInvalidValue);
+  }
+}
+
+HDK_API size_t hdk_factor_part2_stride(const hdk_factor* f) { return part2_stride(*f); }
 
 HDK_API int hdk_apply_inverse3_perm(const hdk_factor* f, const double* rhs_perm, double* out_perm, void* stream) {
   return launch(f, rhs_perm, out_perm, false, static_cast<cudaStream_t>(stream));

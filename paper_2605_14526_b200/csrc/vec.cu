@@ -733,6 +733,20 @@ __device__ __forceinline__ bool last_block_ticket(unsigned int* ticket) {
   return is_last != 0;
 }
 
+// OR of several backbone loops' conditions (multi-column contact adjoint).
+__global__ void k_any_cond(const hdk_ctl* ctls, int count, int* any, cudaGraphConditionalHandle handle,
+                           int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int c = threadIdx.x;
+  const int on = c < count && ctls[c].cond != 0 && ctls[c].err == 0 && ctls[c].nonfinite == 0;
+  const int a = __any_sync(0xffffffffu, on) ? 1 : 0;
+  if (threadIdx.x == 0) {
+    *any = a;
+    if (use_handle) cudaGraphSetConditional(handle, a);
+  }
+}
+
 // ---- adjoint backbone in elimination order -----------------------------------
 // The backbone's Anderson vectors (t, x, last, history) live in elimination
 // order [n][3]: the solve's tile partials fold into t with contiguous loads,
@@ -1229,6 +1243,12 @@ HDK_API int hdk_aa_dots_fused(const hdk_vtx* x, const hdk_factor* f, hdk_ctl* ct
 
 HDK_API int hdk_trace_epoch(unsigned long long* buf, void* stream) {
   hdk::launch(k_trace_epoch, dim3(1), dim3(1), 0, S(stream), buf);
+  return last();
+}
+
+HDK_API int hdk_any_cond(hdk_ctl* ctls, int count, int* any, unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_any_cond, dim3(1), dim3(32), 0, S(stream), ctls, count, any,
+              static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle != 0ULL ? 1 : 0);
   return last();
 }
 
