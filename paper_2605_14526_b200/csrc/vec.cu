@@ -15,6 +15,7 @@
 
 #include "../../include/hdk.h"
 #include "launch.cuh"
+#include "backbone.cuh"
 
 HDK_TRACE_TU(vec)
 
@@ -43,41 +44,14 @@ __device__ __forceinline__ void block_partials(double (&v)[NQ], double* partial)
 }
 
 // Block partials of the 18 Anderson quantities, stored quantity-major
-// (partial[q * HDK_RED_BLOCKS + block], read by aa_solve_block).  A reduce-scatter
-// butterfly halves the list each level (18 -> 9 -> 5 -> 3 -> 2 -> 1: 20
-// shuffles instead of 18 x 5), after which lane l owns the warp sum of
-// quantity q(l); fixed lane/level order, so bitwise reproducible.
-template <int N, int O>
-__device__ __forceinline__ void rs_level(const double (&v)[N], double (&w)[(N + 1) / 2], int lane, int& q0,
-                                         int& len) {
-  constexpr int H = (N + 1) / 2;
-  const bool up = (lane & O) != 0;
-#pragma unroll
-  for (int i = 0; i < H; ++i) {
-    const double lo = v[i];
-    const double hi = (i + H < N) ? v[i + H] : 0.0;
-    const double r = __shfl_xor_sync(0xffffffffu, up ? lo : hi, O);
-    w[i] = (up ? hi : lo) + r;
-  }
-  if (up) {
-    q0 += H;
-    len -= H;
-  } else if (len > H) {
-    len = H;
-  }
-}
-
+// (partial[q * HDK_RED_BLOCKS + block], read by aa_solve_block), via a
+// reduce-scatter butterfly (20 shuffles instead of 18 x 5; backbone.cuh).
 __device__ __forceinline__ void block_partials_18(const double (&v)[18], double* partial) {
   __shared__ double sm[kT / 32][18];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int q0 = 0, len = 18;
-  double a9[9], a5[5], a3[3], a2[2], a1[1];
-  rs_level<18, 16>(v, a9, lane, q0, len);
-  rs_level<9, 8>(a9, a5, lane, q0, len);
-  rs_level<5, 4>(a5, a3, lane, q0, len);
-  rs_level<3, 2>(a3, a2, lane, q0, len);
-  rs_level<2, 1>(a2, a1, lane, q0, len);
-  if (len >= 1) sm[warp][q0] = a1[0];
+  int q0, len;
+  const double w = hdk::warp_rs_18(v, lane, q0, len);
+  if (len >= 1) sm[warp][q0] = w;
   __syncthreads();
   if (threadIdx.x < 18) {
     double t = 0.0;
@@ -770,18 +744,9 @@ __global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ct
     for (int w = threadIdx.x; w < static_cast<int>(sizeof(hdk_ctl) / 4); w += kT) dst[w] = src[w];
   }
   if (ctl->cond == 0) return;  // unrolled iteration past convergence (the snapshot still carries cond = 0)
-  const int m = ctl->window, c = ctl->count, h = ctl->head;
-  const bool push = ctl->has_last != 0;
-  int ns = 0, c2 = c, h2 = h;
-  if (push) {
-    ns = c < m ? (h + c) % m : h;
-    c2 = c < m ? c + 1 : m;
-    h2 = c < m ? h : (h + 1) % m;
-  }
-  if (mode & 512) c2 = 0;  // profiling ablation
-  int ph[HDK_AA_MAX];
-#pragma unroll
-  for (int j = 0; j < HDK_AA_MAX; ++j) ph[j] = (h2 + j) % m;
+  hdk::BbState st = hdk::bb_state(ctl);
+  if (mode & 512) st.c2 = 0;  // profiling ablation
+  const hdk::BbArgs args{ctl, tp, tv, xp, last_q, last_g, dq, dg};
   double acc[2 * HDK_AA_MAX + 2];
 #pragma unroll
   for (int q = 0; q < 2 * HDK_AA_MAX + 2; ++q) acc[q] = 0.0;
@@ -802,28 +767,7 @@ __global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ct
       for (int k = 0; k < 4; ++k)
         if (b0 + k < pf.y) th += v[k];
     }
-    hdk::st_keep(tp + i, th, pol);
-    tv[3 * (size_t)__ldg(f.p2v + col) + a] = th;  // by vertex, for B t
-    const double qc = hdk::ld_keep(xp + i, pol);
-    const double g = th - qc;
-    acc[2 * HDK_AA_MAX] += g * g;
-    acc[2 * HDK_AA_MAX + 1] += th * th;
-    if (push) {
-      const double dqn = qc - hdk::ld_keep(last_q + i, pol);
-      const double dgn = g - hdk::ld_keep(last_g + i, pol);
-      hdk::st_keep(dq + ns * n3 + i, dqn + dgn, pol);  // the mix only ever uses dq_j + dg_j
-      hdk::st_keep(dg + ns * n3 + i, dgn, pol);
-#pragma unroll
-      for (int j = 0; j < HDK_AA_MAX; ++j) {
-        if (j < c2) {
-          const double dgj = ph[j] == ns ? dgn : hdk::ld_keep(dg + ph[j] * n3 + i, pol);
-          acc[j] += dgn * dgj;
-          acc[HDK_AA_MAX + j] += dgj * g;
-        }
-      }
-    }
-    hdk::st_keep(last_q + i, qc, pol);
-    hdk::st_keep(last_g + i, g, pol);
+    hdk::bb_dots_elem(args, st, f.p2v, n3, i, th, acc, pol);
   }
   static_assert(2 * HDK_AA_MAX + 2 == 18, "butterfly sized for window 8");
   hdk::trace_stamp(g_hdk_trace, hdk::kTrDotsA);
