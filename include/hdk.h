@@ -151,6 +151,12 @@ HDK_API int hdk_differential(const hdk_mesh* m, const hdk_material* mat, const d
                              double* dcomp, int* err, void* stream);
 /* Element forces of B x (matrix-free assemble_db_dq + apply, backward.cpp:117-163). */
 HDK_API int hdk_bapply(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force, void* stream);
+/* hdk_bapply with each corner force stored at its slot of the elimination-
+ * order incidence list (corner_pos[4 e + k] = index into hdk_vtx::pinc, -1
+ * for fixed vertices); read back by hdk_gather_sorted.  corner_pos NULL: the
+ * plain layout.  Does nothing while *run_flag == 0. */
+HDK_API int hdk_bapply_sorted(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
+                              const int* corner_pos, const int* run_flag, void* stream);
 /* hdk_bapply that does nothing while *run_flag == 0 (unrolled backbone). */
 HDK_API int hdk_bapply_flag(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
                             const int* run_flag, void* stream);
@@ -212,6 +218,10 @@ HDK_API int hdk_gather_perm(const hdk_vtx* x, const double* base, const double* 
  * through the elimination-order incidence (x->pinc_off / x->pinc). */
 HDK_API int hdk_gather_pp(const hdk_vtx* x, const double* base_perm, const double* ef, double* rhs_perm,
                           const int* run_flag, void* stream);
+/* Same sums from forces already in incidence order (hdk_bapply_sorted):
+ * contiguous reads, no index indirection; bitwise the same result. */
+HDK_API int hdk_gather_sorted(const hdk_vtx* x, const double* base_perm, const double* ef_sorted, double* rhs_perm,
+                              const int* run_flag, void* stream);
 /* fixcoup[p] = sum_k A_fd(p, k) q[fixed_k] (solve_free's coupling, factor.cpp:201-205). */
 HDK_API int hdk_fixed_coupling(const hdk_csr* a_fd, const int* fixed, const double* q, double* fixcoup, void* stream);
 /* Type-II Anderson mixing (forward.cpp:17-51) in three launches: history

@@ -463,6 +463,10 @@ void Engine::build_factor_device() {
     }
     dv_.pinc_off = A.upload(poff);
     dv_.pinc = A.upload(pinc.empty() ? std::vector<int>{0} : pinc);
+    // corner -> its slot in pinc (hdk_bapply_sorted); -1 for fixed vertices
+    std::vector<int> cpos(4 * static_cast<size_t>(m.ne), -1);
+    for (size_t j = 0; j < pinc.size(); ++j) cpos[pinc[j]] = static_cast<int>(j);
+    corner_pos_ = A.upload(cpos);
   }
   seedp_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
   xp_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
@@ -611,8 +615,8 @@ void Engine::backbone_body(unsigned long long handle, unsigned skip) {
   cuda_check(cudaEventRecord(ev_fork_, st_), "fork");
   cuda_check(cudaStreamWaitEvent(st2_, ev_fork_, 0), "fork wait");
   if (!(skip & 16u)) hdk_check(hdk_bb_solve(ctl_, snap_, part_b_, aares_, handle, st2_), "aa solve + cond");
-  if (!(skip & 1u)) hdk_check(hdk_bapply_flag(&dm_, dcomp_, tv_, ef_, run_it, s), "B t");
-  if (!(skip & 2u)) hdk_check(hdk_gather_pp(&dv_, nullptr, ef_, rt_, run_it, s), "R(t)");
+  if (!(skip & 1u)) hdk_check(hdk_bapply_sorted(&dm_, dcomp_, tv_, ef_, corner_pos_, run_it, s), "B t");
+  if (!(skip & 2u)) hdk_check(hdk_gather_sorted(&dv_, nullptr, ef_, rt_, run_it, s), "R(t)");
   cuda_check(cudaEventRecord(ev_join_, st2_), "join");
   cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join wait");
   if (!(skip & 16u))

@@ -76,6 +76,30 @@ __device__ __forceinline__ void write_force(const ElemGeom& g, const M3& p, doub
   }
 }
 
+// Same forces, each corner's three components stored at its slot of the
+// elimination-order incidence list (corner_pos[4 e + k], -1 for fixed
+// vertices), so the per-vertex gather reads one contiguous range.
+__device__ __forceinline__ void write_force_sorted(const ElemGeom& g, const M3& p, double* __restrict__ efs,
+                                                   const int* __restrict__ corner_pos, int e) {
+  double f[4][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) f[k + 1][r] = p(r, 0) * g.b[3 * k] + p(r, 1) * g.b[3 * k + 1] + p(r, 2) * g.b[3 * k + 2];
+    f[0][r] = -(f[1][r] + f[2][r] + f[3][r]);
+  }
+  const int4 pos = __ldg(reinterpret_cast<const int4*>(corner_pos) + e);
+  const int ps[4] = {pos.x, pos.y, pos.z, pos.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (ps[k] >= 0) {
+      double* o = efs + 3 * (size_t)ps[k];
+      o[0] = f[k][0];
+      o[1] = f[k][1];
+      o[2] = f[k][2];
+    }
+}
+
 __device__ __forceinline__ void set_err(int* err, int code) {
   if (err) atomicCAS(err, 0, code);
 }
@@ -303,7 +327,8 @@ __global__ void __launch_bounds__(128) k_differential(hdk_mesh m, hdk_material m
 // than register-capped single-wave shapes (10.0 vs 12.3 us per apply).
 template <int T, int MINB>
 __global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __restrict__ dcomp, const double* __restrict__ x,
-                                                 double* __restrict__ ef, const int* run_flag) {
+                                                 double* __restrict__ ef, const int* run_flag,
+                                                 const int* __restrict__ corner_pos) {
   HDK_TRACED_WAIT(hdk::kTrBapply);
   hdk::pdl_trigger();
   if (run_flag && *run_flag == 0) return;
@@ -333,7 +358,8 @@ __global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __
     o(j, i) = b * hat(i, j) + a * hat(j, i);
   }
   const M3 pm = mul_nt(mul(u, o), v);
-  write_force(g, pm, ef, e);
+  if (corner_pos) write_force_sorted(g, pm, ef, corner_pos, e);
+  else write_force(g, pm, ef, e);
 }
 
 // Per-element gradient routing (backward.cpp:361-391) and the damping
@@ -429,14 +455,22 @@ HDK_API int hdk_bapply(const hdk_mesh* m, const double* dcomp, const double* x, 
 
 HDK_API int hdk_bapply_flag(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
                             const int* run_flag, void* stream) {
+  return hdk_bapply_sorted(m, dcomp, x, elem_force, nullptr, run_flag, stream);
+}
+
+HDK_API int hdk_bapply_sorted(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
+                              const int* corner_pos, const int* run_flag, void* stream) {
   static const int variant = [] {
     const char* v = std::getenv("HETERODYN_BAPPLY");
     return v ? std::atoi(v) : 0;
   }();
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (variant == 0) hdk::launch(k_bapply<128, 1>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, elem_force, run_flag);
-  else if (variant == 2) hdk::launch(k_bapply<128, 6>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, elem_force, run_flag);
-  else hdk::launch(k_bapply<64, 11>, dim3(blocks(m->ne, 64)), dim3(64), 0, st, *m, dcomp, x, elem_force, run_flag);
+  if (variant == 0)
+    hdk::launch(k_bapply<128, 1>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, elem_force, run_flag, corner_pos);
+  else if (variant == 2)
+    hdk::launch(k_bapply<128, 6>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, elem_force, run_flag, corner_pos);
+  else
+    hdk::launch(k_bapply<64, 11>, dim3(blocks(m->ne, 64)), dim3(64), 0, st, *m, dcomp, x, elem_force, run_flag, corner_pos);
   return static_cast<int>(cudaGetLastError());
 }
 

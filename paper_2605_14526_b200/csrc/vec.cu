@@ -199,8 +199,10 @@ __global__ void k_gather_perm(hdk_vtx x, const double* __restrict__ base, const 
 
 // k_gather_perm over the elimination-order incidence; same terms, same lane
 // split and fold, so bitwise the same sums.
+// sorted != 0: ef holds the forces already in incidence order (hdk_bapply_sorted),
+// so the range is read directly.
 __global__ void k_gather_pp(hdk_vtx x, const double* __restrict__ basep, const double* __restrict__ ef,
-                            double* __restrict__ rhs, const int* run_flag) {
+                            double* __restrict__ rhs, const int* run_flag, int sorted) {
   HDK_TRACED_WAIT(hdk::kTrGather);
   hdk::pdl_trigger();
   if (run_flag && *run_flag == 0) return;
@@ -212,7 +214,7 @@ __global__ void k_gather_pp(hdk_vtx x, const double* __restrict__ basep, const d
     const int e = __ldg(x.pinc_off + p + 1);
 #pragma unroll 4
     for (int j = __ldg(x.pinc_off + p) + sub; j < e; j += 8) {
-      const double* q = ef + 3 * (size_t)__ldg(x.pinc + j);
+      const double* q = ef + 3 * (size_t)(sorted ? j : __ldg(x.pinc + j));
       s0 += __ldg(q);
       s1 += __ldg(q + 1);
       s2 += __ldg(q + 2);
@@ -1153,7 +1155,14 @@ HDK_API int hdk_gather_perm(const hdk_vtx* x, const double* base, const double* 
 HDK_API int hdk_gather_pp(const hdk_vtx* x, const double* base_perm, const double* ef, double* rhs_perm,
                           const int* run_flag, void* stream) {
   if (!x->pinc_off || !x->pinc) return static_cast<int>(cudaErrorInvalidValue);
-  hdk::launch(k_gather_pp, dim3(nb(8LL * x->n)), dim3(256), 0, S(stream), *x, base_perm, ef, rhs_perm, run_flag);
+  hdk::launch(k_gather_pp, dim3(nb(8LL * x->n)), dim3(256), 0, S(stream), *x, base_perm, ef, rhs_perm, run_flag, 0);
+  return last();
+}
+
+HDK_API int hdk_gather_sorted(const hdk_vtx* x, const double* base_perm, const double* ef_sorted, double* rhs_perm,
+                              const int* run_flag, void* stream) {
+  if (!x->pinc_off) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_gather_pp, dim3(nb(8LL * x->n)), dim3(256), 0, S(stream), *x, base_perm, ef_sorted, rhs_perm, run_flag, 1);
   return last();
 }
 
