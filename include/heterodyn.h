@@ -211,6 +211,10 @@ HD_API hd_status hd_batch_evaluate(hd_batch* batch, int frames, double* loss, si
  * every sample's stream; 0 for the oracle) and kernels launched so far. */
 HD_API double hd_batch_last_ms(const hd_batch* batch);
 HD_API long long hd_batch_kernel_launches(const hd_batch* batch);
+/* Global solves (3 axes) run by all samples so far, and the algorithmic bytes
+ * of one solve of one sample (16 nnz(S') + 96 n; samples share the pattern). */
+HD_API long long hd_batch_solve_count(const hd_batch* batch);
+HD_API double hd_batch_solve_bytes(const hd_batch* batch);
 
 #ifdef __cplusplus
 }

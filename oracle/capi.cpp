@@ -416,5 +416,7 @@ hd_status hd_batch_evaluate(hd_batch* b, int frames, double* loss, size_t loss_c
 }
 double hd_batch_last_ms(const hd_batch*) { return 0.0; }
 long long hd_batch_kernel_launches(const hd_batch*) { return 0; }
+long long hd_batch_solve_count(const hd_batch*) { return 0; }
+double hd_batch_solve_bytes(const hd_batch*) { return 0.0; }
 
 }  // extern "C"

@@ -135,6 +135,17 @@ void Batch::evaluate(int frames, double* loss, double* grad_sum, double* device_
   for (auto& e : done) cudaEventDestroy(e);
 }
 
+long long Batch::solve_count() const {
+  long long k = 0;
+  for (const auto& e : eng_) k += e->solve_count;
+  return k;
+}
+
+double Batch::solve_bytes() const {
+  const HostFactor& F = eng_.front()->factor();
+  return 16.0 * static_cast<double>(F.row_off.back()) + 96.0 * F.n;
+}
+
 long long Batch::kernel_launches() const {
   long long k = own_launches_;
   for (const auto& e : eng_) k += e->kernel_launches;

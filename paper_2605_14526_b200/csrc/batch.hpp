@@ -31,6 +31,8 @@ class Batch {
   // element_count doubles on this device) receives [sum L, sum dL/dE].
   void evaluate(int frames, double* loss, double* grad_sum, double* device_out);
   long long kernel_launches() const;
+  long long solve_count() const;      // 3-axis global solves over all samples so far
+  double solve_bytes() const;         // algorithmic bytes of one solve of one sample (16 nnz(S') + 96 n)
   cudaStream_t stream() const { return st_; }
   double last_ms = 0;  // device-side duration of the last evaluate (max over sample streams)
 

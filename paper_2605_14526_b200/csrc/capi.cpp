@@ -365,3 +365,5 @@ hd_status hd_batch_evaluate(hd_batch* batch, int frames, double* loss, size_t lo
 
 double hd_batch_last_ms(const hd_batch* batch) { return batch ? batch->b->last_ms : 0.0; }
 long long hd_batch_kernel_launches(const hd_batch* batch) { return batch ? batch->b->kernel_launches() : 0; }
+long long hd_batch_solve_count(const hd_batch* batch) { return batch ? batch->b->solve_count() : 0; }
+double hd_batch_solve_bytes(const hd_batch* batch) { return batch ? batch->b->solve_bytes() : 0.0; }

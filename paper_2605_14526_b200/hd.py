@@ -82,6 +82,8 @@ SIGNATURES = {
     "hd_batch_evaluate": (C.c_int, [_VP, C.c_int, _D, C.c_size_t, _D, C.c_size_t, _VP]),
     "hd_batch_last_ms": (C.c_double, [_VP]),
     "hd_batch_kernel_launches": (C.c_longlong, [_VP]),
+    "hd_batch_solve_count": (C.c_longlong, [_VP]),
+    "hd_batch_solve_bytes": (C.c_double, [_VP]),
 }
 
 
@@ -412,3 +414,11 @@ class Batch:
     @property
     def kernel_launches(self) -> int:
         return self.L.lib.hd_batch_kernel_launches(self.h)
+
+    @property
+    def solve_count(self) -> int:
+        return self.L.lib.hd_batch_solve_count(self.h)
+
+    @property
+    def solve_bytes(self) -> float:
+        return self.L.lib.hd_batch_solve_bytes(self.h)
