@@ -61,9 +61,9 @@ Batch::Batch(const Scene& scene, int samples, const double* young, int threads, 
   parallel_samples(samples, threads_, device_, [&](int s) {
     if (young) {
       Vec y(young + static_cast<size_t>(s) * ne, young + static_cast<size_t>(s + 1) * ne);
-      eng_[s] = std::make_unique<Engine>(scene, &y, solve_ctas);
+      eng_[s] = std::make_unique<Engine>(scene, &y, solve_ctas, true);
     } else {
-      eng_[s] = std::make_unique<Engine>(scene, nullptr, solve_ctas);
+      eng_[s] = std::make_unique<Engine>(scene, nullptr, solve_ctas, true);
     }
   });
   cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "batch stream");

@@ -127,8 +127,9 @@ void build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()
   for (cudaGraph_t g : {gpre, gpost, top}) cudaGraphDestroy(g);
 }
 
-Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas)
-    : scene_(scene), mat_(scene.material), solve_ctas_(solve_ctas) {
+Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared_device)
+    : scene_(scene), mat_(scene.material), solve_ctas_(solve_ctas), branch_(!shared_device) {
+  if (const char* br = std::getenv("HETERODYN_BRANCH")) branch_ = std::atoi(br) != 0;
   if (const char* c = std::getenv("HETERODYN_SOLVE_CTAS")) solve_ctas_ = std::atoi(c);
   if (const char* u = std::getenv("HETERODYN_UNROLL")) unroll_ = std::max(1, std::atoi(u));
   if (young) mat_.set_young(*young, scene.mesh.vol);
@@ -612,13 +613,20 @@ void Engine::backbone_body(unsigned long long handle, unsigned skip) {
     hdk_check(hdk_bb_dots(&df_, ctl_, snap_, t_, tv_, xp_, lastq_, lastg_, dq_, dg_, part_b_, 1 | (skip & (512u | 1024u)),
                           s),
               "aa dots");
-  cuda_check(cudaEventRecord(ev_fork_, st_), "fork");
-  cuda_check(cudaStreamWaitEvent(st2_, ev_fork_, 0), "fork wait");
-  if (!(skip & 16u)) hdk_check(hdk_bb_solve(ctl_, snap_, part_b_, aares_, handle, st2_), "aa solve + cond");
+  // a batch's engines keep one stream each (the device is already shared by
+  // many samples, and every extra stream competes for the hardware queues)
+  cudaStream_t sb = branch_ ? st2_ : st_;
+  if (branch_) {
+    cuda_check(cudaEventRecord(ev_fork_, st_), "fork");
+    cuda_check(cudaStreamWaitEvent(st2_, ev_fork_, 0), "fork wait");
+  }
+  if (!(skip & 16u)) hdk_check(hdk_bb_solve(ctl_, snap_, part_b_, aares_, handle, sb), "aa solve + cond");
   if (!(skip & 1u)) hdk_check(hdk_bapply_sorted(&dm_, dcomp_, tv_, ef_, corner_pos_, run_it, s), "B t");
   if (!(skip & 2u)) hdk_check(hdk_gather_sorted(&dv_, nullptr, ef_, rt_, run_it, s), "R(t)");
-  cuda_check(cudaEventRecord(ev_join_, st2_), "join");
-  cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join wait");
+  if (branch_) {
+    cuda_check(cudaEventRecord(ev_join_, st2_), "join");
+    cuda_check(cudaStreamWaitEvent(st_, ev_join_, 0), "join wait");
+  }
   if (!(skip & 16u))
     hdk_check(hdk_bb_mix(&df_, ctl_, snap_, aares_, t_, xp_, x_, dq_, rt_, rx_, lrx_, lrg_, rsq_, seedp_, rhs_, s),
               "aa mix");

@@ -83,7 +83,9 @@ class Engine {
   // young: optional per-element Young's moduli replacing the scene's (a
   // parameter sample of a batch); the factor is built once for them.
   // solve_ctas: cap on the CTAs of each solve pass (0 = one resident wave).
-  explicit Engine(const Scene& scene, const Vec* young = nullptr, int solve_ctas = 0);
+  // shared_device: other engines run concurrently on the device (a batch's
+  // samples): the backbone then stays on one stream.
+  explicit Engine(const Scene& scene, const Vec* young = nullptr, int solve_ctas = 0, bool shared_device = false);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -194,8 +196,9 @@ class Engine {
   double* cache_ = nullptr;  // 24 ne projection cache of the current step
   hdk_ctl* ctl_ = nullptr;
   unsigned int* ticket_ = nullptr;
-  hdk_ctl* snap_ = nullptr;
-  int unroll_ = 4;  // backbone iterations per WHILE-loop body  // control-block snapshot of the backbone (hdk_bb_dots -> hdk_bb_mix)
+  hdk_ctl* snap_ = nullptr;  // control-block snapshot of the backbone (hdk_bb_dots -> hdk_bb_mix)
+  int unroll_ = 4;           // backbone iterations per WHILE-loop body
+  bool branch_ = true;       // coefficient solve on its own graph branch (st2_)
   double* seedp_ = nullptr;  // adjoint seed in elimination order (3 n)
   double* xp_ = nullptr;     // backbone iterate in elimination order (3 n); x_ holds it by vertex
   int* corner_pos_ = nullptr;  // element corner -> slot in the elimination-order incidence list
