@@ -98,7 +98,6 @@ typedef struct hdk_factor {
   const int* first2;      /* grid2+1: first chunk of pass-2 CTA b */
   const int* tile_cta2;   /* 2*n_tiles: first and last pass-2 CTA touching tile t */
   const int2* vfold;      /* nv: (first tile-partial slot of the vertex's column, slot count; 0 if fixed) */
-  const int2* pfold;      /* n: the same by column (elimination order) */
 } hdk_factor;
 
 /* Scalar CSR in elimination order (a_free / a_free_fixed, factor.hpp:98-99). */
@@ -276,7 +275,7 @@ HDK_API int hdk_aa_mix(const hdk_vtx* x, hdk_ctl* ctl, const double* qhat, doubl
 /* Dual gate (forward.cpp:140-146) and loop condition for the graph while node. */
 HDK_API int hdk_gate(hdk_ctl* ctl, const double* partial_b, const double* partial_q, unsigned long long cond_handle,
                      void* stream);
-HDK_API int hdk_backbone_cond(hdk_ctl* ctl, unsigned long long cond_handle, void* stream);
+
 /* A_ff dq dot partials for the trust-region model (backward.cpp:77-79). */
 HDK_API int hdk_tr_model(const hdk_vtx* x, const hdk_csr* a_ff, const double* q_star, const double* q_prev,
                          double* dq_perm, double* partial, void* stream);

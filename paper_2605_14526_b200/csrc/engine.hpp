@@ -107,6 +107,7 @@ class Engine {
   // and printed to stderr when the engine is destroyed.
   struct Phases {
     bool on = false;
+    bool skip_first = true;
     cudaEvent_t ev[8] = {};
     double ms[8] = {};
     long long n = 0;

@@ -39,6 +39,12 @@ constexpr int kThreads = 32 * (kWarps + 1);  // + one producer warp
 constexpr int kVals = HDK_CHUNK_VALS;
 constexpr int kSegs = HDK_CHUNK_SEGS;
 constexpr int kStages1 = 3;   // pass 1 ring depth (2 CTAs / SM)
+// Pass 1 with W consumer warps: W = 8 runs 2 CTAs per SM with a 3-stage ring;
+// W = 16 (multi-column passes, which are compute-bound) 1 CTA per SM, 6 stages.
+template <int W>
+struct Pass1 {
+  static constexpr int threads = 32 * (W + 1), min_blocks = W == 8 ? 2 : 1, stages = W == 8 ? kStages1 : 6;
+};
 constexpr int kStages2 = 5;   // pass 2 ring depth (1 CTA / SM)
 constexpr int kThreads2 = 32 * (kWarps + 2);  // pass 2: + copy warp + z-gather warp
 
@@ -207,11 +213,11 @@ struct Ring {
 };
 
 template <int S>
-__device__ __forceinline__ void ring_init(Ring<S>& r) {
+__device__ __forceinline__ void ring_init(Ring<S>& r, int consumers = kWarps) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&r.full[s], 1);
-      mbar_init(&r.empty[s], kWarps);
+      mbar_init(&r.empty[s], consumers);
     }
     mbar_fence_init();
   }
@@ -344,42 +350,45 @@ __device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S, R>& r, int
 }
 
 // ---- pass 1 ------------------------------------------------------------------
-template <bool kDry, int R>
-__device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages1>& ring, const double* __restrict__ rhs,
-                                               int c_beg, int c_end);
+template <bool kDry, int R, int W>
+__device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<Pass1<W>::stages>& ring,
+                                               const double* __restrict__ rhs, int c_beg, int c_end);
 
-// R columns: consumer warp w serves column w / (8 / R) and every (8 / R)-th
+// R columns: consumer warp w serves column w / (W / R) and every (W / R)-th
 // segment pair of each staged chunk, so the chunk is streamed once for all R
 // columns and a warp still holds one column's right-hand side tile.
-template <bool kDry = false, int R = 1>  // kDry: stream only (microbenchmarks)
-__global__ void __launch_bounds__(kThreads, 2) k_rowdot(hdk_factor f, const double* __restrict__ rhs) {
+template <bool kDry = false, int R = 1, int W = kWarps>  // kDry: stream only (microbenchmarks)
+__global__ void __launch_bounds__(Pass1<W>::threads, Pass1<W>::min_blocks) k_rowdot(hdk_factor f,
+                                                                                   const double* __restrict__ rhs) {
+  constexpr int S = Pass1<W>::stages;
   hdk::pdl_trigger();  // the producer prefills before the PDL wait; consumers wait below
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Ring<kStages1>& ring = *reinterpret_cast<Ring<kStages1>*>(smem_raw);
+  Ring<S>& ring = *reinterpret_cast<Ring<S>*>(smem_raw);
   const int warp = threadIdx.x >> 5;
   unsigned long long* trace = HDK_TRACE_PTR;
   if (trace && threadIdx.x == 0) trace[2 * blockIdx.x] = globaltimer();
-  ring_init(ring);
+  ring_init(ring, W);
   const int c_beg = f.first1 ? f.first1[blockIdx.x] : range_first(blockIdx.x, gridDim.x, f.n_chunks);
   const int c_end = f.first1 ? f.first1[blockIdx.x + 1] : range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
-  if (warp == kWarps) {
+  if (warp == W) {
     produce(f, ring, c_beg, c_end, false);
     return;
   }
   HDK_TRACED_WAIT(hdk::kTrRowdot);
   if (f.run_flag && *f.run_flag == 0) return;
-  rowdot_consume<kDry, R>(f, ring, rhs, c_beg, c_end);
+  rowdot_consume<kDry, R, W>(f, ring, rhs, c_beg, c_end);
   if (trace) {
-    consumers_sync();
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * W) : "memory");
     if (threadIdx.x == 0) trace[2 * blockIdx.x + 1] = globaltimer();
   }
 }
 
-template <bool kDry, int R>
-__device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages1>& ring, const double* __restrict__ rhs,
-                                               int c_beg, int c_end) {
-  constexpr int WPC = kWarps / R;  // consumer warps per column
-  static_assert(WPC * R == kWarps, "columns must divide the consumer warps");
+template <bool kDry, int R, int W>
+__device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<Pass1<W>::stages>& ring,
+                                               const double* __restrict__ rhs, int c_beg, int c_end) {
+  constexpr int S = Pass1<W>::stages;
+  constexpr int WPC = W / R;  // consumer warps per column
+  static_assert(WPC * R == W, "columns must divide the consumer warps");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int colr = warp / WPC, sub = warp % WPC;
   rhs += (size_t)colr * 3 * (size_t)f.n;
@@ -387,8 +396,8 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<kStages
   double b0[kM], b1[kM], b2[kM];
   int tile = -1;
   for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
-    const int st = k % kStages1;
-    mbar_wait(&ring.full[st], (k / kStages1) & 1);
+    const int st = k % S;
+    mbar_wait(&ring.full[st], (k / S) & 1);
     const ChunkInfo ch = ring.info[st];
     if (ch.tile != tile) {  // right-hand side of the tile into registers
       tile = ch.tile;
@@ -640,8 +649,9 @@ const Grids& grids() {
     const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem<1>);
     cudaFuncSetAttribute(k_rowdot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
     cudaFuncSetAttribute(k_coltile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s2));
-    cudaFuncSetAttribute(k_rowdot<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
-    cudaFuncSetAttribute(k_rowdot<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
+    const int s16 = static_cast<int>(sizeof(Ring<Pass1<16>::stages>));
+    cudaFuncSetAttribute(k_rowdot<false, 2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, s16);
+    cudaFuncSetAttribute(k_rowdot<false, 4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, s16);
     cudaFuncSetAttribute(k_coltile<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(Pass2Smem<2>)));
     cudaFuncSetAttribute(k_coltile<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -672,7 +682,11 @@ int launch_multi(const hdk_factor* f, const double* rhs, cudaStream_t st) {
   int g1, g2;
   pick_grids(f, g1, g2);
   if (g1 != f->grid1 || g2 != f->grid2) return static_cast<int>(cudaErrorInvalidValue);
-  hdk::launch(k_rowdot<false, R>, dim3(g1), dim3(kThreads), sizeof(Ring<kStages1>), st, *f, rhs);
+  // pass 1 is compute-bound with R columns: 16 consumer warps, 1 CTA per SM,
+  // on pass 2's grid and chunk ranges
+  hdk_factor f1 = *f;
+  f1.first1 = f->first2;
+  hdk::launch(k_rowdot<false, R, 16>, dim3(g2), dim3(Pass1<16>::threads), sizeof(Ring<Pass1<16>::stages>), st, f1, rhs);
   hdk::launch(k_zreduce, dim3((f->n_ztask + 7) / 8, R), dim3(256), 0, st, *f);
   hdk::launch(k_coltile<false, R>, dim3(g2), dim3(kThreads2), sizeof(Pass2Smem<R>), st, *f);
   return static_cast<int>(cudaGetLastError());

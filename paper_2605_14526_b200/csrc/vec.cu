@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ct
   const unsigned long long pol = hdk::pol_keep();
   for (size_t i = blockIdx.x * kT + threadIdx.x; i < n3; i += (size_t)HDK_RED_BLOCKS * kT) {
     const int col = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)col);
-    const int tile = col >> 8;  // tile_cta2 is tiny and L1-resident (pfold would be an L2 round trip)
+    const int tile = col >> 8;  // tile_cta2 is tiny and L1-resident
     const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
     int2 pf = make_int2((tile + tb0) * 256 + (col & 255), tb1 - tb0 + 1);
     double th = 0.0;
@@ -926,13 +926,6 @@ __global__ void __launch_bounds__(kT) k_gate(hdk_ctl* ctl, const double* pb, con
   if (use_handle) cudaGraphSetConditional(handle, cont);
 }
 
-__global__ void k_bb_cond(hdk_ctl* ctl, cudaGraphConditionalHandle handle, int use_handle) {
-  hdk::pdl_wait();
-  hdk::pdl_trigger();
-  const int cont = (!ctl->done && ctl->err == 0) ? 1 : 0;
-  ctl->cond = cont;
-  if (use_handle) cudaGraphSetConditional(handle, cont);
-}
 
 // ---- trust-region ratio --------------------------------------------------------
 __global__ void k_tr_dq(hdk_vtx x, const double* qs, const double* qp, double* dq) {
@@ -1249,10 +1242,6 @@ HDK_API int hdk_gate(hdk_ctl* ctl, const double* partial_b, const double* partia
   return last();
 }
 
-HDK_API int hdk_backbone_cond(hdk_ctl* ctl, unsigned long long cond_handle, void* stream) {
-  hdk::launch(k_bb_cond, dim3(1), dim3(1), 0, S(stream), ctl, static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle != 0ULL);
-  return last();
-}
 
 HDK_API int hdk_tr_model(const hdk_vtx* x, const hdk_csr* a_ff, const double* q_star, const double* q_prev,
                          double* dq_perm, double* partial, void* stream) {
