@@ -143,6 +143,9 @@ HDK_API int hdk_local_step(const hdk_mesh* m, const hdk_material* mat, const dou
  * receives NON_POSITIVE_JACOBIAN (5) or PROX_DIVERGED (6). */
 HDK_API int hdk_element_energy(const hdk_mesh* m, const hdk_material* mat, const double* q, double* energy, int* bad,
                                void* stream);
+/* Both energies of the trust-region test (q*^{-1} and q*) in one launch. */
+HDK_API int hdk_element_energy2(const hdk_mesh* m, const hdk_material* mat, const double* q1, double* energy1,
+                                const double* q2, double* energy2, int* bad, void* stream);
 /* Compact prox differential per element from the projection cache and the
  * device scalar *tau (tr_blend + nh/polar/volume/barrier differentials,
  * localstep.cpp:276-423): 30 doubles SoA.  Errors: SINGULAR_FILTERED_HESSIAN. */

@@ -45,25 +45,43 @@ __device__ __forceinline__ BbState bb_state(const hdk_ctl* ctl) {
   return s;
 }
 
-__device__ __forceinline__ void bb_dots_elem(const BbArgs& a, const BbState& s, const int* __restrict__ p2v, size_t n3,
-                                             size_t i, double th, double (&acc)[2 * HDK_AA_MAX + 2],
-                                             unsigned long long pol) {
+// Loads of one element that do not depend on t (issued before t is folded).
+struct BbIn {
+  double qc, lq, lg;
+  double dgh[HDK_AA_MAX];
+};
+
+__device__ __forceinline__ BbIn bb_prefetch(const BbArgs& a, const BbState& s, size_t n3, size_t i,
+                                            unsigned long long pol) {
+  BbIn v;
+  v.qc = ld_keep(a.xp + i, pol);
+  v.lq = s.push ? ld_keep(a.last_q + i, pol) : 0.0;
+  v.lg = s.push ? ld_keep(a.last_g + i, pol) : 0.0;
+#pragma unroll
+  for (int j = 0; j < HDK_AA_MAX; ++j)
+    v.dgh[j] = (s.push && j < s.c2 && s.ph[j] != s.ns) ? ld_keep(a.dg + s.ph[j] * n3 + i, pol) : 0.0;
+  return v;
+}
+
+__device__ __forceinline__ void bb_dots_elem(const BbArgs& a, const BbState& s, const BbIn& v,
+                                             const int* __restrict__ p2v, size_t n3, size_t i, double th,
+                                             double (&acc)[2 * HDK_AA_MAX + 2], unsigned long long pol) {
   const int col = static_cast<int>(i / 3), ax = static_cast<int>(i - 3 * (size_t)col);
   st_keep(a.tp + i, th, pol);
   a.tv[3 * (size_t)__ldg(p2v + col) + ax] = th;
-  const double qc = ld_keep(a.xp + i, pol);
+  const double qc = v.qc;
   const double g = th - qc;
   acc[2 * HDK_AA_MAX] += g * g;
   acc[2 * HDK_AA_MAX + 1] += th * th;
   if (s.push) {
-    const double dqn = qc - ld_keep(a.last_q + i, pol);
-    const double dgn = g - ld_keep(a.last_g + i, pol);
+    const double dqn = qc - v.lq;
+    const double dgn = g - v.lg;
     st_keep(a.dq + s.ns * n3 + i, dqn + dgn, pol);  // the mix only ever uses dq_j + dg_j
     st_keep(a.dg + s.ns * n3 + i, dgn, pol);
 #pragma unroll
     for (int j = 0; j < HDK_AA_MAX; ++j) {
       if (j < s.c2) {
-        const double dgj = s.ph[j] == s.ns ? dgn : ld_keep(a.dg + s.ph[j] * n3 + i, pol);
+        const double dgj = s.ph[j] == s.ns ? dgn : v.dgh[j];
         acc[j] += dgn * dgj;
         acc[HDK_AA_MAX + j] += dgj * g;
       }

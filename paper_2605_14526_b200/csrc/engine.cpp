@@ -541,8 +541,7 @@ void Engine::build_backward_graph() {
   bpre_ = capture_exec(st_, [&] {
     hdk_check(hdk_ctl_init(ctl_, HDK_AA_MAX, 1e8, 500, 0.0, 0.0, 1e-10, so.eps_tr, 0, s), "ctl init");
     hdk_check(hdk_tr_model(&dv_, &a_ff_, bqstar_, bqprev_, dqp_, part_a_, s), "tr model");
-    hdk_check(hdk_element_energy(&dm_, &dmat_, bqprev_, eprev_, &ctl_->bad, s), "energy prev");
-    hdk_check(hdk_element_energy(&dm_, &dmat_, bqstar_, estar_, &ctl_->bad, s), "energy star");
+    hdk_check(hdk_element_energy2(&dm_, &dmat_, bqprev_, eprev_, bqstar_, estar_, &ctl_->bad, s), "energies");
     hdk_check(hdk_tr_select(&dv_, dm_.ne, eprev_, estar_, bqprev_, bqstar_, bqtil_, 1.0 / (h * h), part_a_, part_b_,
                             ctl_, s), "tr select");
     hdk_check(hdk_differential(&dm_, &dmat_, bcache_, &ctl_->tau, dcomp_, &ctl_->err, s), "differential");

@@ -160,10 +160,15 @@ __global__ void __launch_bounds__(128) k_local(hdk_mesh m, hdk_material mat, con
 
 // V_e times the model density at the element's projection (backward.cpp:23-45);
 // flags NonPositiveJacobian / ProxDiverged (tr_select_tau maps both to rho = inf).
-__global__ void __launch_bounds__(128) k_energy(hdk_mesh m, hdk_material mat, const double* __restrict__ q,
-                                                 double* __restrict__ energy, int* bad) {
+// blockIdx.y selects one of two (q, energy) pairs: both TR energies of a
+// backward frame in one launch (q2/energy2 unused when gridDim.y == 1).
+__global__ void __launch_bounds__(128) k_energy(hdk_mesh m, hdk_material mat, const double* __restrict__ q1,
+                                                 double* __restrict__ energy1, const double* __restrict__ q2,
+                                                 double* __restrict__ energy2, int* bad) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
+  const double* __restrict__ q = blockIdx.y ? q2 : q1;
+  double* __restrict__ energy = blockIdx.y ? energy2 : energy1;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m.ne) return;
   const ElemGeom g = load_geom(m, e);
@@ -439,7 +444,15 @@ HDK_API int hdk_local_step(const hdk_mesh* m, const hdk_material* mat, const dou
 
 HDK_API int hdk_element_energy(const hdk_mesh* m, const hdk_material* mat, const double* q, double* energy, int* bad,
                                void* stream) {
-  hdk::launch(k_energy, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q, energy, bad);
+  hdk::launch(k_energy, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q, energy,
+              q, energy, bad);
+  return static_cast<int>(cudaGetLastError());
+}
+
+HDK_API int hdk_element_energy2(const hdk_mesh* m, const hdk_material* mat, const double* q1, double* energy1,
+                                const double* q2, double* energy2, int* bad, void* stream) {
+  hdk::launch(k_energy, dim3(blocks(m->ne, 128), 2), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q1,
+              energy1, q2, energy2, bad);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -755,6 +755,7 @@ __global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ct
   const unsigned long long pol = hdk::pol_keep();
   for (size_t i = blockIdx.x * kT + threadIdx.x; i < n3; i += (size_t)HDK_RED_BLOCKS * kT) {
     const int col = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)col);
+    const hdk::BbIn pre = hdk::bb_prefetch(args, st, n3, i, pol);
     const int tile = col >> 8;  // tile_cta2 is tiny and L1-resident
     const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
     int2 pf = make_int2((tile + tb0) * 256 + (col & 255), tb1 - tb0 + 1);
@@ -769,7 +770,7 @@ __global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ct
       for (int k = 0; k < 4; ++k)
         if (b0 + k < pf.y) th += v[k];
     }
-    hdk::bb_dots_elem(args, st, f.p2v, n3, i, th, acc, pol);
+    hdk::bb_dots_elem(args, st, pre, f.p2v, n3, i, th, acc, pol);
   }
   static_assert(2 * HDK_AA_MAX + 2 == 18, "butterfly sized for window 8");
   hdk::trace_stamp(g_hdk_trace, hdk::kTrDotsA);
