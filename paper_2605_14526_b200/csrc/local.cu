@@ -334,23 +334,30 @@ template <int T, int MINB>
 __global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __restrict__ dcomp, const double* __restrict__ x,
                                                  double* __restrict__ ef, const int* run_flag,
                                                  const int* __restrict__ corner_pos) {
-  HDK_TRACED_WAIT(hdk::kTrBapply);
+  // The element's geometry and differential do not depend on the previous
+  // kernel (only x does): load them before the PDL wait, so they arrive
+  // while that kernel drains.
   hdk::pdl_trigger();
-  if (run_flag && *run_flag == 0) return;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= m.ne) return;
+  const bool live = e < m.ne;
   const size_t n = m.ne;
-  const ElemGeom g = load_geom(m, e);
+  const int ee = live ? e : 0;
+  const ElemGeom g = load_geom(m, ee);
+  double d[30];
+#pragma unroll
+  for (int i = 0; i < 30; ++i) d[i] = __ldg(dcomp + i * n + ee);
+  HDK_TRACED_WAIT(hdk::kTrBapply);
+  if (run_flag && *run_flag == 0) return;
+  if (!live) return;
   const M3 df = def_grad(g, x);
   M3 u, v;
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
-    u.m[i] = __ldg(dcomp + i * n + e);
-    v.m[i] = __ldg(dcomp + (9 + i) * n + e);
+    u.m[i] = d[i];
+    v.m[i] = d[9 + i];
   }
   const M3 hat = mul(mul_tn(u, df), v);
-  const double j00 = __ldg(dcomp + 18 * n + e), j11 = __ldg(dcomp + 19 * n + e), j22 = __ldg(dcomp + 20 * n + e);
-  const double j01 = __ldg(dcomp + 21 * n + e), j02 = __ldg(dcomp + 22 * n + e), j12 = __ldg(dcomp + 23 * n + e);
+  const double j00 = d[18], j11 = d[19], j22 = d[20], j01 = d[21], j02 = d[22], j12 = d[23];
   M3 o;
   o(0, 0) = j00 * hat(0, 0) + j01 * hat(1, 1) + j02 * hat(2, 2);
   o(1, 1) = j01 * hat(0, 0) + j11 * hat(1, 1) + j12 * hat(2, 2);
@@ -358,7 +365,7 @@ __global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __
 #pragma unroll
   for (int p = 0; p < 3; ++p) {
     const int i = p == 2 ? 1 : 0, j = p == 0 ? 1 : 2;
-    const double a = __ldg(dcomp + (24 + p) * n + e), b = __ldg(dcomp + (27 + p) * n + e);
+    const double a = d[24 + p], b = d[27 + p];
     o(i, j) = a * hat(i, j) + b * hat(j, i);
     o(j, i) = b * hat(i, j) + a * hat(j, i);
   }
