@@ -222,17 +222,15 @@ hd_status hd_sim_backward(hd_sim* sim, const double* direct, const double* dq_fi
                           size_t dl_dw_capacity) {
   if (!sim) return bad_arg("hd_sim_backward: sim is NULL");
   return guarded([&] {
-    GradOut g = sim->eng->backward(direct, dq_final, dv_final);
-    if (dl_dw && dl_dw_capacity < g.dl_dw.size()) raise(Code::InvalidArgument, "hd_sim_backward: dl_dw buffer too small");
-    const auto put = [](double* d, const Vec& v) {
-      if (d) std::memcpy(d, v.data(), v.size() * sizeof(double));
-    };
-    put(dl_dq0, g.dl_dq0);
-    put(dl_dv0, g.dl_dv0);
-    put(dl_df_ext, g.dl_df_ext);
-    put(dl_de, g.dl_de);
-    put(dl_dw, g.dl_dw);
-    sim->last_grad = std::move(g);
+    if (dl_dw && dl_dw_capacity < sim->eng->dw_count())
+      raise(Code::InvalidArgument, "hd_sim_backward: dl_dw buffer too small");
+    Engine::GradSinks sinks;
+    sinks.dq0 = dl_dq0;
+    sinks.dv0 = dl_dv0;
+    sinks.df_ext = dl_df_ext;
+    sinks.de = dl_de;
+    sinks.dw = dl_dw;
+    sim->last_grad = sim->eng->backward(direct, dq_final, dv_final, false, true, nullptr, &sinks);
   });
 }
 
@@ -267,19 +265,14 @@ hd_status hd_sim_backward_canonical(hd_sim* sim, double* dl_dq0, double* dl_dv0,
   if (!sim) return bad_arg("hd_sim_backward_canonical: sim is NULL");
   return guarded([&] {
     const bool any = dl_dq0 || dl_dv0 || dl_df_ext || dl_de || dl_dw;
-    GradOut g = sim->eng->backward(nullptr, nullptr, nullptr, true, any);
-    if (any) {
-      if (dl_dw && dl_dw_capacity < g.dl_dw.size()) raise(Code::InvalidArgument, "dl_dw buffer too small");
-      const auto put = [](double* d, const Vec& v) {
-        if (d) std::memcpy(d, v.data(), v.size() * sizeof(double));
-      };
-      put(dl_dq0, g.dl_dq0);
-      put(dl_dv0, g.dl_dv0);
-      put(dl_df_ext, g.dl_df_ext);
-      put(dl_de, g.dl_de);
-      put(dl_dw, g.dl_dw);
-    }
-    sim->last_grad = std::move(g);
+    if (dl_dw && dl_dw_capacity < sim->eng->dw_count()) raise(Code::InvalidArgument, "dl_dw buffer too small");
+    Engine::GradSinks sinks;
+    sinks.dq0 = dl_dq0;
+    sinks.dv0 = dl_dv0;
+    sinks.df_ext = dl_df_ext;
+    sinks.de = dl_de;
+    sinks.dw = dl_dw;
+    sim->last_grad = sim->eng->backward(nullptr, nullptr, nullptr, true, false, nullptr, any ? &sinks : nullptr);
   });
 }
 

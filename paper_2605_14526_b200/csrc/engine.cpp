@@ -879,8 +879,10 @@ Vec Engine::velocities() const {
   return out;
 }
 
+size_t Engine::dw_count() const { return (mat_.kind == Kind::Corotated ? 2 : 1) * static_cast<size_t>(scene_.mesh.ne); }
+
 GradOut Engine::backward(const double* direct, const double* dq_final, const double* dv_final, bool canonical,
-                         bool download, const double* d_target) {
+                         bool download, const double* d_target, const GradSinks* sinks) {
   const int T = nrec_;
   if (T == 0) raise(Code::InvalidArgument, "hd_sim_backward: no recorded frames");
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
@@ -920,17 +922,29 @@ GradOut Engine::backward(const double* direct, const double* dq_final, const dou
     if (direct) cuda_check(cudaMemcpyAsync(direct_, direct + static_cast<size_t>(t) * n3, B, cudaMemcpyHostToDevice, st_), "direct");
     backward_frame(t, out);
   }
-  if (!download) return out;
-  const auto d2h = [&](Vec& v, const double* d, size_t n) {
-    v.resize(n);
-    cuda_check(cudaMemcpyAsync(v.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost, st_), "grad download");
-    cuda_check(cudaStreamSynchronize(st_), "grad download");
+  if (!download && !sinks) return out;
+  const auto d2h = [&](double* h, const double* d, size_t n) {
+    if (h) cuda_check(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, st_), "grad download");
   };
-  d2h(out.dl_dq0, qbar_, n3);
-  d2h(out.dl_dv0, vbar_, n3);
-  d2h(out.dl_df_ext, dfacc_, n3);
-  d2h(out.dl_de, dle_, ne);
-  d2h(out.dl_dw, dlw_, (mat_.kind == Kind::Corotated ? 2 : 1) * ne);
+  if (sinks) {
+    d2h(sinks->dq0, qbar_, n3);
+    d2h(sinks->dv0, vbar_, n3);
+    d2h(sinks->df_ext, dfacc_, n3);
+    d2h(sinks->de, dle_, ne);
+    d2h(sinks->dw, dlw_, dw_count());
+  } else {
+    out.dl_dq0.resize(n3);
+    out.dl_dv0.resize(n3);
+    out.dl_df_ext.resize(n3);
+    out.dl_de.resize(ne);
+    out.dl_dw.resize(dw_count());
+    d2h(out.dl_dq0.data(), qbar_, n3);
+    d2h(out.dl_dv0.data(), vbar_, n3);
+    d2h(out.dl_df_ext.data(), dfacc_, n3);
+    d2h(out.dl_de.data(), dle_, ne);
+    d2h(out.dl_dw.data(), dlw_, dw_count());
+  }
+  cuda_check(cudaStreamSynchronize(st_), "grad download");
   return out;
 }
 

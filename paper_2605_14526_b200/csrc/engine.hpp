@@ -97,8 +97,16 @@ class Engine {
   void set_state(const double* q, const double* v, double time);
   // canonical: seed from device state, L = 1/2|q_T - ref|^2 (+ 1/2|v_T|^2 when
   // d_target is null and ref is the rest shape); d_target is a device array.
+  // sinks: host buffers (any may be NULL) the gradients are copied into
+  // directly, with one stream synchronisation; without sinks and with
+  // download, GradOut's vectors are filled instead.
+  struct GradSinks {
+    double *dq0 = nullptr, *dv0 = nullptr, *df_ext = nullptr, *de = nullptr, *dw = nullptr;
+  };
   GradOut backward(const double* dl_dq_direct, const double* dl_dq_final, const double* dl_dv_final,
-                   bool canonical = false, bool download = true, const double* d_target = nullptr);
+                   bool canonical = false, bool download = true, const double* d_target = nullptr,
+                   const GradSinks* sinks = nullptr);
+  size_t dw_count() const;  // entries of dL/dw (2 n_e corotated, n_e Neo-Hookean)
   void reset_state();  // scene's initial state, time 0, recorded frames dropped
   double time_solve(int reps, double* bytes);
   double time_backbone(int reps, unsigned skip_mask);
