@@ -65,11 +65,6 @@ char* dup(const std::string& s) {
   return p;
 }
 
-hd_status copy_out(const Vec& v, double* out, size_t cap, const char* who) {
-  if (!out || cap < v.size()) return bad_arg(std::string(who) + ": output buffer too small");
-  std::memcpy(out, v.data(), v.size() * sizeof(double));
-  return HD_OK;
-}
 
 template <class Make>
 hd_scene* make_scene(const char* who, const void* arg, Make&& make) {
@@ -130,17 +125,17 @@ hd_status hd_sim_step(hd_sim* sim) {
 }
 double hd_sim_time(const hd_sim* sim) { return sim ? sim->eng->time() : 0.0; }
 int hd_sim_dof_count(const hd_sim* sim) { return sim ? sim->eng->dofs() : 0; }
+// capacity check first (capi.cpp:63-72 of the reference), then one copy
+// straight into the caller's buffer
 hd_status hd_sim_positions(const hd_sim* sim, double* out, size_t cap) {
   if (!sim) return bad_arg("hd_sim_positions: sim is NULL");
-  Vec q;
-  const hd_status st = guarded([&] { q = sim->eng->positions(); });
-  return st != HD_OK ? st : copy_out(q, out, cap, "hd_sim_positions");
+  if (!out || cap < sim->eng->dof_count()) return bad_arg("hd_sim_positions: output buffer too small");
+  return guarded([&] { sim->eng->positions_into(out); });
 }
 hd_status hd_sim_velocities(const hd_sim* sim, double* out, size_t cap) {
   if (!sim) return bad_arg("hd_sim_velocities: sim is NULL");
-  Vec v;
-  const hd_status st = guarded([&] { v = sim->eng->velocities(); });
-  return st != HD_OK ? st : copy_out(v, out, cap, "hd_sim_velocities");
+  if (!out || cap < sim->eng->dof_count()) return bad_arg("hd_sim_velocities: output buffer too small");
+  return guarded([&] { sim->eng->velocities_into(out); });
 }
 int hd_sim_last_iterations(const hd_sim* sim) { return sim ? sim->eng->last_iterations : 0; }
 int hd_sim_last_converged(const hd_sim* sim) { return sim && sim->eng->last_converged ? 1 : 0; }

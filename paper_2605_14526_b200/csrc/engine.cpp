@@ -872,6 +872,14 @@ Vec Engine::positions() const {
   cuda_check(cudaStreamSynchronize(st_), "read state");
   return out;
 }
+void Engine::positions_into(double* host) const {
+  cuda_check(cudaMemcpyAsync(host, q_, dof_count() * sizeof(double), cudaMemcpyDeviceToHost, st_), "read state");
+  cuda_check(cudaStreamSynchronize(st_), "read state");
+}
+void Engine::velocities_into(double* host) const {
+  cuda_check(cudaMemcpyAsync(host, v_, dof_count() * sizeof(double), cudaMemcpyDeviceToHost, st_), "read state");
+  cuda_check(cudaStreamSynchronize(st_), "read state");
+}
 Vec Engine::velocities() const {
   Vec out(3 * static_cast<size_t>(scene_.mesh.nv));
   cuda_check(cudaMemcpyAsync(out.data(), v_, out.size() * sizeof(double), cudaMemcpyDeviceToHost, st_), "read state");

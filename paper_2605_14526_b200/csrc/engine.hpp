@@ -149,6 +149,10 @@ class Engine {
 
   Vec positions() const;
   Vec velocities() const;
+  // the same straight into a host buffer of 3 n_v doubles (one stream sync)
+  void positions_into(double* host) const;
+  void velocities_into(double* host) const;
+  size_t dof_count() const { return 3 * static_cast<size_t>(scene_.mesh.nv); }
   double time() const { return time_; }
   int dofs() const { return 3 * mesh().nv; }
   int last_iterations = 0, last_converged = 0, last_contacts = 0;

@@ -252,3 +252,18 @@ def test_backbone_unroll_and_ordering_invariance(prod, monkeypatch):
     for k in GRADS:
         if np.linalg.norm(gb[k]) > 0:
             assert rel2(out["4"][1][k], gb[k]) <= 1e-9, (k, rel2(out["4"][1][k], gb[k]))
+
+
+def test_state_download_capacity(prod):
+    """hd_sim_positions / _velocities: capacity below 3 n_v is
+    HD_ERR_INVALID_ARGUMENT and leaves the buffer untouched (capi.cpp:63-72)."""
+    import ctypes as C
+    sim = prod.scene(scenes.block_scene(dims=(3, 2, 2))).sim()
+    n = sim.n
+    buf = np.full(n, -7.0)
+    ptr = buf.ctypes.data_as(C.POINTER(C.c_double))
+    assert prod.lib.hd_sim_positions(sim.h, ptr, n - 1) == 13  # HD_ERR_INVALID_ARGUMENT
+    assert np.all(buf == -7.0)
+    assert prod.lib.hd_sim_velocities(sim.h, ptr, n - 1) == 13
+    assert prod.lib.hd_sim_positions(sim.h, ptr, n) == 0
+    np.testing.assert_array_equal(buf, sim.positions())
