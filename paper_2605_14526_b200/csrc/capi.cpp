@@ -190,6 +190,12 @@ hd_status hd_factor_stats(const hd_scene* scene, char** stats_json) {
     j["factor_fill_ratio"] = static_cast<double>(F.row_off.back()) / (static_cast<double>(F.n) * F.n);
     j["l_nnz"] = F.l_nnz;
     j["factor_millis"] = F.millis;
+    {  // host build phases (ms): assembly, ordering, elimination tree, LDL^T, S' values, packing
+      const double* c = F.ms_phase;
+      j["factor_phase_millis"] = {{"assembly", c[0]}, {"ordering", c[1] - c[0]}, {"etree", c[2] - c[1]},
+                                  {"ldlt", c[3] - c[2]}, {"inverse_values", c[4] - c[3]},
+                                  {"stream_packing", F.millis - c[4]}};
+    }
     j["segments"] = F.seg.size();
     j["chunks"] = F.chunks.size();
     j["stream_values"] = F.stream.size();

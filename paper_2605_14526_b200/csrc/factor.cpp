@@ -453,6 +453,11 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
       if (w >= 0 && w != i) g[i].push_back(w);
     }
   }
+  const auto lap = [&t0](double& acc) {
+    const auto now = std::chrono::steady_clock::now();
+    acc = std::chrono::duration<double, std::milli>(now - t0).count();
+  };
+  lap(F.ms_phase[0]);  // assembly
   // 1. fill-reducing order (free index space)
   std::vector<int> order;
   order.reserve(n);
@@ -480,6 +485,7 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
   }
   std::vector<int> pos(n);
   for (int p = 0; p < n; ++p) pos[order[p]] = p;
+  lap(F.ms_phase[1]);  // ordering
   // 2. elimination tree of the ordered matrix (Liu, with path compression)
   auto etree = [&](const std::vector<int>& ps, std::vector<int>& parent) {
     std::vector<int> anc(n, -1);
@@ -545,6 +551,7 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
     F.p2v[pos[i]] = freev[i];
     F.v2p[freev[i]] = pos[i];
   }
+  lap(F.ms_phase[2]);  // etree, postorder
   // 4. permuted matrix rows (lower triangle incl. diagonal) and LDL^T (up-looking)
   std::vector<std::vector<std::pair<int, double>>> rowl(n);
   for (int i = 0; i < n; ++i) {
@@ -603,6 +610,7 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
       raise(Code::NotPositiveDefinite, "non-positive pivot " + std::to_string(dk) + " at position " + std::to_string(k));
     d[k] = dk;
   }
+  lap(F.ms_phase[3]);  // LDL^T
   // 5. S' rows: column c of L^{-1} lives on c's ancestor path; every entry of
   //    L(:, v) for v on that path is also on it, so a dense scratch suffices.
   F.row_len = sz;
@@ -624,6 +632,7 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
       }
     }
   });
+  lap(F.ms_phase[4]);  // S' values
   // 6. segments (row parts inside 256-column tiles)
   const int W = F.tile_w;
   const int ntiles = (n + W - 1) / W;

@@ -129,6 +129,7 @@ struct HostFactor {
   Csr a_fd;  // free rows (elimination order) x fixed columns (index into fixed)
   long long l_nnz = 0;
   double millis = 0;
+  double ms_phase[5] = {};  // cumulative ms after assembly, ordering, etree, LDL^T, S' values
   std::string ordering;
   double weight_contrast = 1;
 };
