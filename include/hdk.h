@@ -108,6 +108,26 @@ typedef struct hdk_csr {
   const double* val;
 } hdk_csr;
 
+/* Device build of the factor values (inverse.cu): S' = D^{-1/2} L^{-1}
+ * column by column along the elimination tree, written straight into the
+ * tile-major stream (zero-initialised, stream_len values).  Bitwise the host
+ * build's values; fails with cudaErrorInvalidValue if the tree is too deep
+ * for a path to fit in shared memory. */
+typedef struct hdk_inverse_build {
+  int n, max_depth, tile_w;
+  const int* parent;       /* n, postordered elimination tree, -1 at roots */
+  const int* depth;        /* n, distance to the root */
+  const long long* lp;     /* n+1, L by columns */
+  const int* ldist;        /* depth(v) - depth(row) of each entry of L(:, v) */
+  const double* lx;        /* L values */
+  const double* dis;       /* D^{-1/2} */
+  const int* row_first;    /* n, first column of row r of S' */
+  const int* row_pslot;    /* n+1, (row, tile) segment slots */
+  const long long* seg_off;  /* per slot: stream index of the segment's first value */
+  const int* seg_clo;      /* per slot: its first column */
+} hdk_inverse_build;
+HDK_API int hdk_inverse_values(const hdk_inverse_build* b, double* stream, void* stream_handle);
+
 /* Solve x = A^{-1} rhs on 3 axes: rhs in elimination order [n][3]; the result
  * is scattered into out_full[3*v+a] for free vertices (fixed entries are not
  * touched).  Replaces GlobalSystem::solve_free (factor.cpp:196-208). */

@@ -130,6 +130,7 @@ void build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()
 Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared_device)
     : scene_(scene), mat_(scene.material), solve_ctas_(solve_ctas), branch_(!shared_device) {
   if (const char* br = std::getenv("HETERODYN_BRANCH")) branch_ = std::atoi(br) != 0;
+  if (const char* dv = std::getenv("HETERODYN_HOST_FACTOR_VALUES")) device_values_ = std::atoi(dv) == 0;
   if (const char* c = std::getenv("HETERODYN_SOLVE_CTAS")) solve_ctas_ = std::atoi(c);
   if (const char* u = std::getenv("HETERODYN_UNROLL")) unroll_ = std::max(1, std::atoi(u));
   if (young) mat_.set_young(*young, scene.mesh.vol);
@@ -149,7 +150,7 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared
   }
   fgraph_ = std::make_unique<LoopGraph>();
   bgraph_ = std::make_unique<LoopGraph>();
-  hf_ = build_factor(scene.mesh, mat_, scene.solver.h, scene.fixed, scene.ordering);
+  hf_ = build_factor(scene.mesh, mat_, scene.solver.h, scene.fixed, scene.ordering, device_values_);
   refactor_count = 1;
   build_static();
   build_factor_device();
@@ -338,7 +339,30 @@ void Engine::build_factor_device() {
     const char* hint = std::getenv("HETERODYN_L2_HINT");
     df_.l2_hint = hint ? std::atoi(hint) : 1;
   }
-  df_.sval = A.upload(F.stream);
+  if (F.stream.empty() && F.stream_len > 0) {  // values built on the device (inverse.cu)
+    double* sv = A.alloc<double>(static_cast<size_t>(F.stream_len));
+    DevArena T;  // builder inputs, freed after the build
+    const DeviceBuild& B = F.build;
+    hdk_inverse_build b{};
+    b.n = F.n;
+    b.max_depth = B.max_depth;
+    b.tile_w = F.tile_w;
+    b.parent = T.upload(B.parent);
+    b.depth = T.upload(B.depth);
+    b.lp = T.upload(B.lp);
+    b.ldist = T.upload(B.ldist.empty() ? std::vector<int>{0} : B.ldist);
+    b.lx = T.upload(B.lx.empty() ? Vec{0.0} : B.lx);
+    b.dis = T.upload(B.dis);
+    b.row_first = T.upload(B.row_first);
+    b.row_pslot = T.upload(F.row_pslot);
+    b.seg_off = T.upload(B.seg_off);
+    b.seg_clo = T.upload(B.seg_clo);
+    hdk_check(hdk_inverse_values(&b, sv, st_), "device factor values");
+    cuda_check(cudaStreamSynchronize(st_), "device factor values");
+    df_.sval = sv;
+  } else {
+    df_.sval = A.upload(F.stream);
+  }
   static_assert(sizeof(hdk_seg) == sizeof(SegDesc), "segment descriptor layout");
   static_assert(sizeof(hdk_chunk) == sizeof(ChunkDesc), "chunk descriptor layout");
   hdk_seg* segs = A.alloc<hdk_seg>(F.sdesc.size());
@@ -997,7 +1021,7 @@ void Engine::set_young(const Vec& young, bool freeze) {
   if (freeze) mat_.freeze();
   mat_.set_young(young, scene_.mesh.vol);
   cuda_check(cudaStreamSynchronize(st_), "sync");
-  hf_ = build_factor(scene_.mesh, mat_, scene_.solver.h, scene_.fixed, scene_.ordering);
+  hf_ = build_factor(scene_.mesh, mat_, scene_.solver.h, scene_.fixed, scene_.ordering, device_values_);
   ++refactor_count;
   cols_.reset();  // its graph bakes the old factor and material pointers
   // material arrays and factor live in fresh allocations; graphs bake pointers

@@ -212,6 +212,7 @@ class Engine {
   hdk_ctl* snap_ = nullptr;  // control-block snapshot of the backbone (hdk_bb_dots -> hdk_bb_mix)
   int unroll_ = 4;           // backbone iterations per WHILE-loop body
   bool branch_ = true;       // coefficient solve on its own graph branch (st2_)
+  bool device_values_ = true;  // factor values built on the device (inverse.cu)
   double* seedp_ = nullptr;  // adjoint seed in elimination order (3 n)
   double* xp_ = nullptr;     // backbone iterate in elimination order (3 n); x_ holds it by vertex
   int* corner_pos_ = nullptr;  // element corner -> slot in the elimination-order incidence list

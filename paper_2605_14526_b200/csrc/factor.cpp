@@ -424,7 +424,7 @@ void metis_nd(const Graph& g, std::vector<int>& out) {
 }  // namespace
 
 HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const std::vector<int>& fixed,
-                        const std::string& ordering) {
+                        const std::string& ordering, bool device_values) {
   const auto t0 = std::chrono::steady_clock::now();
   HostFactor F;
   F.nv = mesh.nv;
@@ -616,9 +616,24 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
   F.row_len = sz;
   F.row_off.assign(n + 1, 0);
   for (int r = 0; r < n; ++r) F.row_off[r + 1] = F.row_off[r] + sz[r];
-  F.sval.assign(static_cast<size_t>(F.row_off[n]), 0.0);
   Vec dis(n);
   for (int i = 0; i < n; ++i) dis[i] = 1.0 / std::sqrt(d[i]);
+  if (device_values) {  // the values are computed on the device (inverse.cu): hand over the builder inputs
+    DeviceBuild& B = F.build;
+    B.parent = parent;
+    B.depth.assign(n, 0);
+    for (int v = n - 1; v >= 0; --v) B.depth[v] = parent[v] < 0 ? 0 : B.depth[parent[v]] + 1;  // parent > v
+    B.max_depth = n ? *std::max_element(B.depth.begin(), B.depth.end()) : 0;
+    B.lp = lp;
+    B.ldist.resize(li.size());
+    for (int v = 0; v < n; ++v)
+      for (long long p = lp[v]; p < lp[v + 1]; ++p) B.ldist[p] = B.depth[v] - B.depth[li[p]];
+    B.lx = lx;
+    B.dis = dis;
+    B.row_first.resize(n);
+    for (int r = 0; r < n; ++r) B.row_first[r] = r - sz[r] + 1;
+  } else {
+  F.sval.assign(static_cast<size_t>(F.row_off[n]), 0.0);
   parallel_chunks(n, [&](int lo, int hi, int) {
     Vec work(n, 0.0);
     for (int c = lo; c < hi; ++c) {
@@ -632,6 +647,7 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
       }
     }
   });
+  }
   lap(F.ms_phase[4]);  // S' values
   // 6. segments (row parts inside 256-column tiles)
   const int W = F.tile_w;
@@ -652,30 +668,42 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
   //     chunk 16-byte aligned, descriptors contiguous per chunk
   {
     F.tile_chunk.assign(ntiles + 1, 0);
-    F.stream.reserve(static_cast<size_t>(F.row_off[n] * 1.02) + 16);
+    if (!device_values) F.stream.reserve(static_cast<size_t>(F.row_off[n] * 1.02) + 16);
+    else {
+      F.build.seg_off.assign(F.row_pslot[n], 0);
+      F.build.seg_clo.assign(F.row_pslot[n], 0);
+    }
+    long long slen = 0;
     for (int t = 0; t < ntiles; ++t) {
       const auto& list = per_tile[t];
       size_t s = 0;
       while (s < list.size()) {
-        ChunkDesc c{static_cast<long long>(F.stream.size()), 0, static_cast<int>(F.sdesc.size()), 0, t};
+        ChunkDesc c{slen, 0, static_cast<int>(F.sdesc.size()), 0, t};
         int vals = 0;
         while (s < list.size() && c.nseg < HDK_SEGS && vals + list[s].len <= HDK_VALS) {
           const Segment& g = list[s];
           F.sdesc.push_back({g.row, g.pslot, (g.clo - t * W) | (g.len << 16), vals});
-          F.stream.insert(F.stream.end(), F.sval.begin() + g.off, F.sval.begin() + g.off + g.len);
+          if (device_values) {
+            F.build.seg_off[g.pslot] = slen + vals;
+            F.build.seg_clo[g.pslot] = g.clo;
+          } else {
+            F.stream.insert(F.stream.end(), F.sval.begin() + g.off, F.sval.begin() + g.off + g.len);
+          }
           vals += g.len;
           ++c.nseg;
           ++s;
         }
         if (vals & 1) {
-          F.stream.push_back(0.0);
+          if (!device_values) F.stream.push_back(0.0);
           ++vals;
         }
         c.len = vals;
+        slen += vals;
         F.chunks.push_back(c);
       }
       F.tile_chunk[t + 1] = static_cast<int>(F.chunks.size());
     }
+    F.stream_len = slen;
   }
   // 7. A_ff and A_fd in elimination order (apply_a_free / fixed coupling)
   F.a_ff.rows = F.a_ff.cols = n;

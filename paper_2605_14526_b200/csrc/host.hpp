@@ -111,6 +111,15 @@ struct Csr {
 struct Segment { long long off; int row, clo, len, pslot; };  // off: row-major sval
 struct SegDesc { int row, pslot, clo_len, coff; };              // device descriptor (hdk_seg)
 struct ChunkDesc { long long off; int len, seg0, nseg, tile; };  // device chunk (hdk_chunk)
+// Inputs of the device-side S' value build (inverse.cu): the postordered
+// elimination tree, L by columns with each entry's depth distance, D^{-1/2},
+// and where every (row, tile) segment sits in the value stream.
+struct DeviceBuild {
+  std::vector<int> parent, depth, ldist, row_first, seg_clo;
+  std::vector<long long> lp, seg_off;
+  Vec lx, dis;
+  int max_depth = 0;
+};
 struct HostFactor {
   int n = 0, nv = 0;
   std::vector<int> p2v, v2p, fixed;
@@ -128,6 +137,8 @@ struct HostFactor {
   Csr a_ff;  // free x free, elimination order
   Csr a_fd;  // free rows (elimination order) x fixed columns (index into fixed)
   long long l_nnz = 0;
+  long long stream_len = 0;  // values in the tile-major stream (F.stream holds them unless built on the device)
+  DeviceBuild build;         // filled when build_factor(..., device_values = true)
   double millis = 0;
   double ms_phase[5] = {};  // cumulative ms after assembly, ordering, etree, LDL^T, S' values
   std::string ordering;
@@ -144,6 +155,6 @@ std::vector<int> tile_cta_ranges(const std::vector<int>& tile_chunk, const std::
 // |A_ff S'^T S' b - b| / |b| for a deterministic b (no solve path runs here).
 double factor_inverse_residual(const HostFactor& F);
 HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const std::vector<int>& fixed,
-                        const std::string& ordering);
+                        const std::string& ordering, bool device_values = false);
 
 }  // namespace hdb

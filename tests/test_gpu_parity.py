@@ -267,3 +267,18 @@ def test_state_download_capacity(prod):
     assert prod.lib.hd_sim_velocities(sim.h, ptr, n - 1) == 13
     assert prod.lib.hd_sim_positions(sim.h, ptr, n) == 0
     np.testing.assert_array_equal(buf, sim.positions())
+
+
+def test_device_factor_values_bitwise(prod, monkeypatch):
+    """The factor values built on the device (inverse.cu) are bitwise the host
+    build's: solves through either are identical."""
+    scene = scenes.config_scene("C1")
+    rng = np.random.default_rng(3)
+    sims = {}
+    for host in ("1", "0"):
+        monkeypatch.setenv("HETERODYN_HOST_FACTOR_VALUES", host)
+        sims[host] = prod.scene(scene).sim()
+    monkeypatch.delenv("HETERODYN_HOST_FACTOR_VALUES")
+    for _ in range(2):
+        b = rng.standard_normal(sims["0"].n)
+        np.testing.assert_array_equal(sims["0"].solve_free(b), sims["1"].solve_free(b))
