@@ -150,7 +150,7 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared
   }
   fgraph_ = std::make_unique<LoopGraph>();
   bgraph_ = std::make_unique<LoopGraph>();
-  hf_ = build_factor(scene.mesh, mat_, scene.solver.h, scene.fixed, scene.ordering, device_values_);
+  hf_ = build_factor(scene.mesh, mat_, scene.solver.h, scene.fixed, scene.ordering, device_values_, &order_cache_);
   refactor_count = 1;
   build_static();
   build_factor_device();
@@ -283,7 +283,36 @@ void Engine::build_static() {
   bqstar_ = A.alloc<double>(n3);
   bcache_ = A.alloc<double>(24 * ne);
   mu_ = x_;
-  // material (weights with volume folded in)
+  dmat_.w1 = A.alloc<double>(ne);
+  dmat_.w2 = A.alloc<double>(ne);
+  dmat_.mu_e = A.alloc<double>(ne);
+  dmat_.lambda_e = A.alloc<double>(ne);
+  dmat_.beta_vh = mat_.beta0 > 0 ? A.alloc<double>(ne) : nullptr;
+  dmat_.vol = A.upload(m.vol);
+  upload_material();
+  const double hk[5] = {scene_.hook_anchor.x, scene_.hook_anchor.y, scene_.hook_anchor.z, scene_.hook_k, scene_.hook_d};
+  hook_ = A.alloc<double>(5);
+  DevArena::copy_h2d(hook_, hk, sizeof(hk));
+  // obstacles: {kind, nx, ny, nz, offset|radius, cx, cy, cz}
+  Vec ob;
+  for (const Obstacle& o : scene_.obstacles) {
+    const double rec[8] = {static_cast<double>(o.kind), o.normal.x, o.normal.y, o.normal.z,
+                           o.kind == 0 ? o.offset : o.radius, o.center.x, o.center.y, o.center.z};
+    ob.insert(ob.end(), rec, rec + 8);
+  }
+  obst_ = A.upload(ob);
+  flags_ = A.alloc<unsigned char>(static_cast<size_t>(nv) * std::max<size_t>(1, scene_.obstacles.size()));
+  q0c_ = A.alloc<double>(n3);
+  aa_window_ = scene_.solver.aa_window > 0 ? scene_.solver.aa_window : (mat_.contrast() > 10.0 ? 1 : 5);
+  aa_window_ = std::min(aa_window_, HDK_AA_MAX);
+}
+
+// Material arrays (weights with volume folded in) and scalars into the
+// existing device buffers; also the Anderson window, which follows the
+// weight contrast (forward.cpp:56-83).
+void Engine::upload_material() {
+  const Mesh& m = scene_.mesh;
+  const size_t ne = m.ne;
   Vec w1(ne), w2(ne), bvh(ne);
   const double h = scene_.solver.h;
   for (size_t e = 0; e < ne; ++e) {
@@ -302,27 +331,44 @@ void Engine::build_static() {
   dmat_.mu_bar = mat_.mu_bar;
   dmat_.lambda_bar = mat_.lambda_bar;
   dmat_.k_bar = mat_.k_bar;
-  dmat_.w1 = A.upload(w1);
-  dmat_.w2 = A.upload(w2);
-  dmat_.mu_e = A.upload(mat_.mu);
-  dmat_.lambda_e = A.upload(mat_.lambda);
-  dmat_.beta_vh = mat_.beta0 > 0 ? A.upload(bvh) : nullptr;
-  dmat_.vol = A.upload(m.vol);
-  const double hk[5] = {scene_.hook_anchor.x, scene_.hook_anchor.y, scene_.hook_anchor.z, scene_.hook_k, scene_.hook_d};
-  hook_ = A.alloc<double>(5);
-  DevArena::copy_h2d(hook_, hk, sizeof(hk));
-  // obstacles: {kind, nx, ny, nz, offset|radius, cx, cy, cz}
-  Vec ob;
-  for (const Obstacle& o : scene_.obstacles) {
-    const double rec[8] = {static_cast<double>(o.kind), o.normal.x, o.normal.y, o.normal.z,
-                           o.kind == 0 ? o.offset : o.radius, o.center.x, o.center.y, o.center.z};
-    ob.insert(ob.end(), rec, rec + 8);
-  }
-  obst_ = A.upload(ob);
-  flags_ = A.alloc<unsigned char>(static_cast<size_t>(nv) * std::max<size_t>(1, scene_.obstacles.size()));
-  q0c_ = A.alloc<double>(n3);
+  const auto put = [&](const double* d, const Vec& v) {
+    DevArena::copy_h2d(const_cast<double*>(d), v.data(), v.size() * sizeof(double));
+  };
+  put(dmat_.w1, w1);
+  put(dmat_.w2, w2);
+  put(dmat_.mu_e, mat_.mu);
+  put(dmat_.lambda_e, mat_.lambda);
+  if (dmat_.beta_vh) put(dmat_.beta_vh, bvh);
   aa_window_ = scene_.solver.aa_window > 0 ? scene_.solver.aa_window : (mat_.contrast() > 10.0 ? 1 : 5);
   aa_window_ = std::min(aa_window_, HDK_AA_MAX);
+}
+
+// S' values of hf_ into the existing stream buffer (device build when the
+// host left them to the device).
+void Engine::fill_factor_values(double* sv) {
+  const HostFactor& F = hf_;
+  if (!F.stream.empty() || F.stream_len == 0) {
+    DevArena::copy_h2d(sv, F.stream.data(), F.stream.size() * sizeof(double));
+    return;
+  }
+  DevArena T;  // builder inputs, freed after the build
+  const DeviceBuild& B = F.build;
+  hdk_inverse_build b{};
+  b.n = F.n;
+  b.max_depth = B.max_depth;
+  b.tile_w = F.tile_w;
+  b.parent = T.upload(B.parent);
+  b.depth = T.upload(B.depth);
+  b.lp = T.upload(B.lp);
+  b.ldist = T.upload(B.ldist.empty() ? std::vector<int>{0} : B.ldist);
+  b.lx = T.upload(B.lx.empty() ? Vec{0.0} : B.lx);
+  b.dis = T.upload(B.dis);
+  b.row_first = T.upload(B.row_first);
+  b.row_pslot = T.upload(F.row_pslot);
+  b.seg_off = T.upload(B.seg_off);
+  b.seg_clo = T.upload(B.seg_clo);
+  hdk_check(hdk_inverse_values(&b, sv, st_), "device factor values");
+  cuda_check(cudaStreamSynchronize(st_), "device factor values");
 }
 
 void Engine::build_factor_device() {
@@ -339,29 +385,10 @@ void Engine::build_factor_device() {
     const char* hint = std::getenv("HETERODYN_L2_HINT");
     df_.l2_hint = hint ? std::atoi(hint) : 1;
   }
-  if (F.stream.empty() && F.stream_len > 0) {  // values built on the device (inverse.cu)
-    double* sv = A.alloc<double>(static_cast<size_t>(F.stream_len));
-    DevArena T;  // builder inputs, freed after the build
-    const DeviceBuild& B = F.build;
-    hdk_inverse_build b{};
-    b.n = F.n;
-    b.max_depth = B.max_depth;
-    b.tile_w = F.tile_w;
-    b.parent = T.upload(B.parent);
-    b.depth = T.upload(B.depth);
-    b.lp = T.upload(B.lp);
-    b.ldist = T.upload(B.ldist.empty() ? std::vector<int>{0} : B.ldist);
-    b.lx = T.upload(B.lx.empty() ? Vec{0.0} : B.lx);
-    b.dis = T.upload(B.dis);
-    b.row_first = T.upload(B.row_first);
-    b.row_pslot = T.upload(F.row_pslot);
-    b.seg_off = T.upload(B.seg_off);
-    b.seg_clo = T.upload(B.seg_clo);
-    hdk_check(hdk_inverse_values(&b, sv, st_), "device factor values");
-    cuda_check(cudaStreamSynchronize(st_), "device factor values");
+  {
+    double* sv = A.alloc<double>(static_cast<size_t>(std::max<long long>(F.stream_len, F.stream.size())));
+    fill_factor_values(sv);
     df_.sval = sv;
-  } else {
-    df_.sval = A.upload(F.stream);
   }
   static_assert(sizeof(hdk_seg) == sizeof(SegDesc), "segment descriptor layout");
   static_assert(sizeof(hdk_chunk) == sizeof(ChunkDesc), "chunk descriptor layout");
@@ -1017,13 +1044,52 @@ double Engine::time_solve(int reps, double* bytes) {
   return static_cast<double>(ms) / reps;
 }
 
+namespace {
+// Same factor structure (ordering, pattern, stream layout, A_ff / A_fd
+// patterns): only values differ, so the device buffers can be refilled.
+bool same_structure(const HostFactor& a, const HostFactor& b) {
+  const auto eq_bytes = [](const auto& x, const auto& y) {
+    return x.size() == y.size() && (x.empty() || std::memcmp(x.data(), y.data(), sizeof(x[0]) * x.size()) == 0);
+  };
+  return a.n == b.n && a.stream_len == b.stream_len && a.p2v == b.p2v && a.row_pslot == b.row_pslot &&
+         eq_bytes(a.sdesc, b.sdesc) && eq_bytes(a.chunks, b.chunks) && a.tile_chunk == b.tile_chunk &&
+         a.a_ff.off == b.a_ff.off && a.a_ff.col == b.a_ff.col && a.a_fd.off == b.a_fd.off && a.a_fd.col == b.a_fd.col;
+}
+}  // namespace
+
 void Engine::set_young(const Vec& young, bool freeze) {
   if (freeze) mat_.freeze();
   mat_.set_young(young, scene_.mesh.vol);
   cuda_check(cudaStreamSynchronize(st_), "sync");
-  hf_ = build_factor(scene_.mesh, mat_, scene_.solver.h, scene_.fixed, scene_.ordering, device_values_);
+  HostFactor nf = build_factor(scene_.mesh, mat_, scene_.solver.h, scene_.fixed, scene_.ordering, device_values_,
+                               &order_cache_);
   ++refactor_count;
   cols_.reset();  // its graph bakes the old factor and material pointers
+  if (same_structure(hf_, nf)) {
+    // values only: refill the existing buffers, keep every allocation, and
+    // re-capture the graphs (they bake the material scalars by value)
+    hf_ = std::move(nf);
+    upload_material();
+    fill_factor_values(const_cast<double*>(df_.sval));
+    DevArena::copy_h2d(const_cast<double*>(a_ff_.val), hf_.a_ff.val.data(), hf_.a_ff.val.size() * sizeof(double));
+    if (!hf_.a_fd.val.empty()) {
+      DevArena::copy_h2d(const_cast<double*>(a_fd_.val), hf_.a_fd.val.data(), hf_.a_fd.val.size() * sizeof(double));
+      Vec tv(hf_.a_fd.val.size());  // A_df = A_fd^T values, in the transpose's order
+      std::vector<int> cur(hf_.a_fd.cols + 1, 0);
+      for (int c : hf_.a_fd.col) ++cur[c + 1];
+      for (int r = 0; r < hf_.a_fd.cols; ++r) cur[r + 1] += cur[r];
+      for (int p = 0; p < hf_.a_fd.rows; ++p)
+        for (int k = hf_.a_fd.off[p]; k < hf_.a_fd.off[p + 1]; ++k) tv[cur[hf_.a_fd.col[k]]++] = hf_.a_fd.val[k];
+      DevArena::copy_h2d(const_cast<double*>(a_df_.val), tv.data(), tv.size() * sizeof(double));
+    }
+    slots_.clear();
+    frame_mem_.clear();
+    nrec_ = 0;
+    build_forward_graph();
+    build_backward_graph();
+    return;
+  }
+  hf_ = std::move(nf);
   // material arrays and factor live in fresh allocations; graphs bake pointers
   Vec q = positions(), v = velocities();
   const double t = time_;

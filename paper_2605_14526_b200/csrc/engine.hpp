@@ -169,6 +169,8 @@ class Engine {
   void add_slot();
   void build_static();
   void build_factor_device();
+  void upload_material();                 // material arrays + scalars into the existing buffers
+  void fill_factor_values(double* sval);  // hf_'s S' values into a stream buffer
   void build_forward_graph();
   void build_backward_graph();
   void run_graph(LoopGraph& g, const char* what);
@@ -213,6 +215,7 @@ class Engine {
   int unroll_ = 4;           // backbone iterations per WHILE-loop body
   bool branch_ = true;       // coefficient solve on its own graph branch (st2_)
   bool device_values_ = true;  // factor values built on the device (inverse.cu)
+  std::vector<int> order_cache_;  // fill-reducing ordering, reused by every refactorization
   double* seedp_ = nullptr;  // adjoint seed in elimination order (3 n)
   double* xp_ = nullptr;     // backbone iterate in elimination order (3 n); x_ holds it by vertex
   int* corner_pos_ = nullptr;  // element corner -> slot in the elimination-order incidence list

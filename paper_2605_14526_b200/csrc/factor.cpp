@@ -424,7 +424,7 @@ void metis_nd(const Graph& g, std::vector<int>& out) {
 }  // namespace
 
 HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const std::vector<int>& fixed,
-                        const std::string& ordering, bool device_values) {
+                        const std::string& ordering, bool device_values, std::vector<int>* order_cache) {
   const auto t0 = std::chrono::steady_clock::now();
   HostFactor F;
   F.nv = mesh.nv;
@@ -461,7 +461,9 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
   // 1. fill-reducing order (free index space)
   std::vector<int> order;
   order.reserve(n);
-  {
+  if (order_cache && static_cast<int>(order_cache->size()) == n) {
+    order = *order_cache;  // the ordering depends only on the free-vertex graph: reuse it on refactorization
+  } else {
     std::vector<int> all(n);
     std::iota(all.begin(), all.end(), 0);
     if (ordering == "nd-bfs") {
@@ -482,6 +484,7 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
       std::vector<char> side(n, 0);
       nd_geometric(g, x, all, order, side);
     }
+    if (order_cache) *order_cache = order;
   }
   std::vector<int> pos(n);
   for (int p = 0; p < n; ++p) pos[order[p]] = p;

@@ -154,7 +154,11 @@ std::vector<int> tile_cta_ranges(const std::vector<int>& tile_chunk, const std::
 // Setup-time self-check of a built factor on the host: max over three axes of
 // |A_ff S'^T S' b - b| / |b| for a deterministic b (no solve path runs here).
 double factor_inverse_residual(const HostFactor& F);
+// order_cache: when it holds an ordering of the same size it is used as is
+// (the ordering depends only on the graph of the free vertices); otherwise
+// the computed ordering is stored into it.
 HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const std::vector<int>& fixed,
-                        const std::string& ordering, bool device_values = false);
+                        const std::string& ordering, bool device_values = false,
+                        std::vector<int>* order_cache = nullptr);
 
 }  // namespace hdb
