@@ -354,6 +354,12 @@ def run_batch(args, world, rank):
     ms_e2e = max_over_ranks(e2.elapsed_time(e3))
     e2e = units / (ms_e2e / 1e3)
 
+    # one system-ID parameter update: every sample of this rank refactors
+    t_ref = time.perf_counter()
+    b.set_young(young[mine.start:mine.stop] * 1.0001)
+    t_ref = time.perf_counter() - t_ref
+    b.set_young(young[mine.start:mine.stop])
+
     # roofline: aggregate factor streaming of all sample solves in the timed
     # region (this rank's solves x algorithmic bytes per solve / step time);
     # the single-sample solve timed alone is reported beside it
@@ -385,7 +391,8 @@ def run_batch(args, world, rank):
                        "parallelism": f"samples sharded dp{world}, NCCL all-reduce of [loss, dL/dE] "
                                       f"({(1 + ne) * 8} B) per step",
                        "samples_per_rank": len(mine), "host_threads_per_rank": threads,
-                       "engine_build_s": t_build, "l2_policy": "per-sample factors 64 x ~%.0f MB exceed L2" %
+                       "engine_build_s": t_build, "set_young_s": t_ref,
+                       "l2_policy": "per-sample factors 64 x ~%.0f MB exceed L2" %
                                                                (probe.factor_nnz * 8 / 1e6),
                        "device_busy_ms_per_step": dev_ms / args.steps,
                        "loss_sum": float(total[0])},

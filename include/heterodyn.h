@@ -205,6 +205,11 @@ HD_API hd_batch* hd_batch_create(const hd_scene* scene, int samples, const doubl
 HD_API void hd_batch_free(hd_batch* batch);
 HD_API int hd_batch_sample_count(const hd_batch* batch);
 HD_API hd_status hd_batch_set_target(hd_batch* batch, const double* q_target, size_t count);
+/* New per-sample Young's moduli (samples x element_count values, the layout of
+ * hd_batch_create): every sample refactors (MaterialField::set_young +
+ * refresh, material.cpp:75-86), in parallel over the batch's host threads —
+ * one system-ID parameter update. */
+HD_API hd_status hd_batch_set_young(hd_batch* batch, const double* young, size_t count, int freeze_means);
 HD_API hd_status hd_batch_evaluate(hd_batch* batch, int frames, double* loss, size_t loss_capacity,
                                    double* dl_de_sum, size_t dl_de_capacity, void* device_out);
 /* Device time of the last evaluation in milliseconds (CUDA events spanning

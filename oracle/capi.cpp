@@ -356,6 +356,7 @@ struct hd_batch {
   int samples = 0;
   std::vector<double> young;  // samples x ne, empty = scene's
   std::vector<double> target;
+  int freeze = 0;             // freeze_means of the last hd_batch_set_young
 };
 
 hd_batch* hd_batch_create(const hd_scene* scene, int samples, const double* young, size_t young_count, int) {
@@ -383,6 +384,16 @@ hd_status hd_batch_set_target(hd_batch* b, const double* q, size_t count) {
   b->target.assign(q, q + count);
   return HD_OK;
 }
+hd_status hd_batch_set_young(hd_batch* b, const double* young, size_t count, int freeze_means) {
+  if (!b || !young) return null_arg("hd_batch_set_young");
+  if (count != b->scene->spec.mesh.element_count() * static_cast<size_t>(b->samples)) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_batch_set_young: young must hold samples x element_count values");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  b->young.assign(young, young + count);
+  b->freeze = freeze_means != 0;
+  return HD_OK;
+}
 hd_status hd_batch_evaluate(hd_batch* b, int frames, double* loss, size_t loss_cap, double* grad, size_t grad_cap,
                             void* device_out) {
   if (!b) return null_arg("hd_batch_evaluate");
@@ -396,7 +407,7 @@ hd_status hd_batch_evaluate(hd_batch* b, int frames, double* loss, size_t loss_c
     hd_sim* sim = hd_sim_create(b->scene);
     if (!sim) return static_cast<hd_status>(hd_last_error_code());
     hd_status st = HD_OK;
-    if (!b->young.empty()) st = hd_sim_set_young(sim, b->young.data() + s * ne, ne, 0);
+    if (!b->young.empty()) st = hd_sim_set_young(sim, b->young.data() + s * ne, ne, b->freeze);
     if (st == HD_OK) st = hd_sim_record(sim, 1);
     for (int f = 0; f < frames && st == HD_OK; ++f) st = hd_sim_step(sim);
     if (st == HD_OK) st = hd_sim_positions(sim, q.data(), n);

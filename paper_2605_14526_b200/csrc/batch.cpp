@@ -135,6 +135,14 @@ void Batch::evaluate(int frames, double* loss, double* grad_sum, double* device_
   for (auto& e : done) cudaEventDestroy(e);
 }
 
+void Batch::set_young(const double* young, bool freeze_means) {
+  const int ne = scene_.mesh.ne;
+  parallel_samples(samples(), threads_, device_, [&](int s) {
+    const Vec y(young + static_cast<size_t>(s) * ne, young + static_cast<size_t>(s + 1) * ne);
+    eng_[s]->set_young(y, freeze_means);
+  });
+}
+
 long long Batch::solve_count() const {
   long long k = 0;
   for (const auto& e : eng_) k += e->solve_count;

@@ -26,6 +26,9 @@ class Batch {
 
   int samples() const { return static_cast<int>(eng_.size()); }
   void set_target(const double* q_target);
+  // New per-sample Young's moduli (samples x element_count): every sample
+  // refactors (Engine::set_young), in parallel over the host threads.
+  void set_young(const double* young, bool freeze_means);
   // Runs every sample's trajectory + adjoint; loss (samples) and grad_sum
   // (element_count) are host outputs and may be null; device_out (1 +
   // element_count doubles on this device) receives [sum L, sum dL/dE].

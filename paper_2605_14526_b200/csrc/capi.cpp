@@ -347,6 +347,13 @@ hd_status hd_batch_set_target(hd_batch* batch, const double* q, size_t count) {
   return guarded([&] { batch->b->set_target(q); });
 }
 
+hd_status hd_batch_set_young(hd_batch* batch, const double* young, size_t count, int freeze_means) {
+  if (!batch || !young) return bad_arg("hd_batch_set_young: NULL argument");
+  if (count != static_cast<size_t>(batch->b->samples()) * batch->scene->spec.mesh.ne)
+    return bad_arg("hd_batch_set_young: young must hold samples x element_count values");
+  return guarded([&] { batch->b->set_young(young, freeze_means != 0); });
+}
+
 hd_status hd_batch_evaluate(hd_batch* batch, int frames, double* loss, size_t loss_cap, double* grad, size_t grad_cap,
                             void* device_out) {
   if (!batch) return bad_arg("hd_batch_evaluate: batch is NULL");

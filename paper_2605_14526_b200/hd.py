@@ -83,6 +83,7 @@ SIGNATURES = {
     "hd_batch_last_ms": (C.c_double, [_VP]),
     "hd_batch_kernel_launches": (C.c_longlong, [_VP]),
     "hd_batch_solve_count": (C.c_longlong, [_VP]),
+    "hd_batch_set_young": (C.c_int, [_VP, _D, C.c_size_t, C.c_int]),
     "hd_batch_solve_bytes": (C.c_double, [_VP]),
 }
 
@@ -414,6 +415,11 @@ class Batch:
     @property
     def kernel_launches(self) -> int:
         return self.L.lib.hd_batch_kernel_launches(self.h)
+
+    def set_young(self, young, freeze_means: bool = False):
+        """One system-ID parameter update: every sample refactors."""
+        y = _f64(young)
+        self.L.check(self.L.lib.hd_batch_set_young(self.h, _ptr(y), y.size, 1 if freeze_means else 0))
 
     @property
     def solve_count(self) -> int:

@@ -229,6 +229,16 @@ def test_batch_matches_oracle_and_is_deterministic(prod, orc):
         rp2 = bp.evaluate(3)
         np.testing.assert_array_equal(rp2["dl_de"], rp["dl_de"])
     np.testing.assert_array_equal(results[0]["dl_de"], results[1]["dl_de"])
+    # a parameter update (hd_batch_set_young): every sample refactors
+    young2 = young * 1.3
+    bo.set_young(young2)
+    ro2 = bo.evaluate(3)
+    bp = sp.batch(6, young, threads=4)
+    bp.set_target(target)
+    bp.set_young(young2)
+    rp2 = bp.evaluate(3)
+    assert rel2(rp2["loss"], ro2["loss"]) <= 1e-6
+    assert rel2(rp2["dl_de"], ro2["dl_de"]) <= 1e-6
 
 
 def test_backbone_unroll_and_ordering_invariance(prod, monkeypatch):
