@@ -97,6 +97,15 @@ HD_API hd_status hd_factor_stats(const hd_scene* scene, char** stats_json);
 
 /* ---- B200 extensions (new; no reference counterpart in the ABI) ---------- */
 
+/* Scene data the system-identification driver needs (drivers.cpp:710-803):
+ * element regions (scene.hpp region_of_element / region_count), rest
+ * positions (3 doubles per vertex) and lumped vertex masses (one per vertex,
+ * TetMesh::vertex_mass).  Capacities are checked. */
+HD_API int hd_scene_region_count(const hd_scene* scene);
+HD_API hd_status hd_scene_regions(const hd_scene* scene, int* region_of_element, size_t capacity);
+HD_API hd_status hd_scene_rest_positions(const hd_scene* scene, double* out, size_t capacity);
+HD_API hd_status hd_scene_vertex_masses(const hd_scene* scene, double* out, size_t capacity);
+
 /* Records every subsequent frame's adjoint cache (the reference's
  * roll(keep_caches=true), drivers.cpp:31-54).  enable=0 stops recording and
  * discards recorded frames. */

@@ -9,6 +9,8 @@
 
 #include <nlohmann/json.hpp>
 
+#include "../paper_2605_14526_b200/csrc/identify.hpp"
+
 #include "../include/heterodyn.h"
 #include "oracle.hpp"
 
@@ -105,6 +107,33 @@ int hd_scene_element_count(const hd_scene* s) { return s ? s->spec.mesh.element_
 int hd_scene_frame_count(const hd_scene* s) { return s ? s->spec.frames : 0; }
 const char* hd_scene_name(const hd_scene* s) { return s ? s->spec.name.c_str() : ""; }
 
+int hd_scene_region_count(const hd_scene* s) { return s ? s->spec.region_count : 0; }
+hd_status hd_scene_regions(const hd_scene* s, int* out, size_t cap) {
+  if (!s) return null_arg("hd_scene_regions");
+  const size_t ne = static_cast<size_t>(s->spec.mesh.element_count());
+  if (!out || cap < ne) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_scene_regions: output buffer too small");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  const auto& r = s->spec.region_of_element;
+  for (size_t e = 0; e < ne; ++e) out[e] = e < r.size() ? r[e] : 0;
+  return HD_OK;
+}
+hd_status hd_scene_rest_positions(const hd_scene* s, double* out, size_t cap) {
+  if (!s) return null_arg("hd_scene_rest_positions");
+  return copy_vector(s->spec.mesh.rest_vector(), out, cap, "hd_scene_rest_positions");
+}
+hd_status hd_scene_vertex_masses(const hd_scene* s, double* out, size_t cap) {
+  if (!s) return null_arg("hd_scene_vertex_masses");
+  const int nv = s->spec.mesh.vertex_count();
+  if (!out || cap < static_cast<size_t>(nv)) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_scene_vertex_masses: output buffer too small");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  for (int v = 0; v < nv; ++v) out[v] = s->spec.mesh.vertex_mass(v);
+  return HD_OK;
+}
+
 hd_sim* hd_sim_create(const hd_scene* scene) {
   if (!scene) { null_arg("hd_sim_create"); return nullptr; }
   hd_sim* sim = new hd_sim;
@@ -155,7 +184,7 @@ int hd_sim_last_iterations(const hd_sim* sim) { return sim ? sim->last_iteration
 int hd_sim_last_converged(const hd_sim* sim) { return sim && sim->last_converged ? 1 : 0; }
 int hd_sim_last_contact_count(const hd_sim* sim) { return sim ? sim->last_contact_count : 0; }
 
-// ---- drivers: simulate only (gradcheck/identify are out of scope here) ----
+// ---- drivers: simulate, identify (gradcheck is out of scope here) ----
 hd_status hd_run_simulate(const hd_scene* scene, const char* out_dir, char** summary_json) {
   if (!scene) return null_arg("hd_run_simulate");
   return guarded([&] {
@@ -193,13 +222,32 @@ hd_status hd_run_gradcheck(const hd_scene*, const char*, const char*, char**, in
   set_error(HD_ERR_INVALID_ARGUMENT, "hd_run_gradcheck: not provided by the oracle library");
   return HD_ERR_INVALID_ARGUMENT;
 }
-hd_status hd_run_identify(const char*, const char*, char**, int*) {
-  set_error(HD_ERR_INVALID_ARGUMENT, "hd_run_identify: not provided by the oracle library");
-  return HD_ERR_INVALID_ARGUMENT;
+// System identification: the product's L-BFGS driver (identify.cpp, written
+// against the public ABI only) linked over this library's CPU restatement, so
+// the parity tests compare the solvers underneath one optimizer.
+static hd_status identify_finish(int code, const std::string& out, bool st, const std::string& err, char** result_json,
+                          int* stalled) {
+  if (code != HD_OK) {
+    set_error(code, err);
+    return static_cast<hd_status>(code);
+  }
+  if (result_json) *result_json = copy_string(out);
+  if (stalled) *stalled = st ? 1 : 0;
+  return HD_OK;
 }
-hd_status hd_run_identify_file(const char*, const char*, char**, int*) {
-  set_error(HD_ERR_INVALID_ARGUMENT, "hd_run_identify_file: not provided by the oracle library");
-  return HD_ERR_INVALID_ARGUMENT;
+hd_status hd_run_identify(const char* problem_json, const char* out_dir, char** result_json, int* stalled) {
+  if (!problem_json) return null_arg("hd_run_identify");
+  std::string out, err;
+  bool st = false;
+  const int code = heterodyn_driver::run_identify(problem_json, out_dir ? out_dir : "", &out, &st, &err);
+  return identify_finish(code, out, st, err, result_json, stalled);
+}
+hd_status hd_run_identify_file(const char* problem_path, const char* out_dir, char** result_json, int* stalled) {
+  if (!problem_path) return null_arg("hd_run_identify_file");
+  std::string out, err;
+  bool st = false;
+  const int code = heterodyn_driver::run_identify_file(problem_path, out_dir ? out_dir : "", &out, &st, &err);
+  return identify_finish(code, out, st, err, result_json, stalled);
 }
 hd_status hd_factor_stats(const hd_scene* scene, char** stats_json) {
   if (!scene) return null_arg("hd_factor_stats");

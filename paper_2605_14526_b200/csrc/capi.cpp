@@ -13,6 +13,7 @@
 #include "../../include/heterodyn.h"
 #include "batch.hpp"
 #include "engine.hpp"
+#include "identify.hpp"
 
 using namespace hdb;
 
@@ -107,6 +108,29 @@ int hd_scene_element_count(const hd_scene* s) { return s ? s->spec.mesh.ne : 0; 
 int hd_scene_frame_count(const hd_scene* s) { return s ? s->spec.frames : 0; }
 const char* hd_scene_name(const hd_scene* s) { return s ? s->spec.name.c_str() : ""; }
 
+int hd_scene_region_count(const hd_scene* s) { return s ? s->spec.region_count : 0; }
+hd_status hd_scene_regions(const hd_scene* s, int* out, size_t cap) {
+  if (!s) return bad_arg("hd_scene_regions: scene is NULL");
+  const size_t ne = static_cast<size_t>(s->spec.mesh.ne);
+  if (!out || cap < ne) return bad_arg("hd_scene_regions: output buffer too small");
+  for (size_t e = 0; e < ne; ++e) out[e] = e < s->spec.region.size() ? s->spec.region[e] : 0;
+  return HD_OK;
+}
+hd_status hd_scene_rest_positions(const hd_scene* s, double* out, size_t cap) {
+  if (!s) return bad_arg("hd_scene_rest_positions: scene is NULL");
+  const Vec& r = s->spec.mesh.rest;
+  if (!out || cap < r.size()) return bad_arg("hd_scene_rest_positions: output buffer too small");
+  std::copy(r.begin(), r.end(), out);
+  return HD_OK;
+}
+hd_status hd_scene_vertex_masses(const hd_scene* s, double* out, size_t cap) {
+  if (!s) return bad_arg("hd_scene_vertex_masses: scene is NULL");
+  const Vec& m = s->spec.mesh.mass;
+  if (!out || cap < m.size()) return bad_arg("hd_scene_vertex_masses: output buffer too small");
+  std::copy(m.begin(), m.end(), out);
+  return HD_OK;
+}
+
 hd_sim* hd_sim_create(const hd_scene* scene) {
   if (!scene) {
     bad_arg("hd_sim_create: scene is NULL");
@@ -166,11 +190,31 @@ hd_status hd_run_simulate(const hd_scene* scene, const char* out_dir, char** sum
 hd_status hd_run_gradcheck(const hd_scene*, const char*, const char*, char**, int*) {
   return bad_arg("hd_run_gradcheck: finite-difference driver is outside this build's scope (use hd_sim_backward)");
 }
-hd_status hd_run_identify(const char*, const char*, char**, int*) {
-  return bad_arg("hd_run_identify: system-identification driver is outside this build's scope");
+// System identification: the L-BFGS driver over this library's own ABI
+// (identify.cpp; reference capi.cpp:279-308).
+static hd_status identify_finish(int code, const std::string& out, bool st, const std::string& err, char** result_json,
+                          int* stalled) {
+  if (code != HD_OK) {
+    set_error(code, err);
+    return static_cast<hd_status>(code);
+  }
+  if (result_json) *result_json = dup(out);
+  if (stalled) *stalled = st ? 1 : 0;
+  return HD_OK;
 }
-hd_status hd_run_identify_file(const char*, const char*, char**, int*) {
-  return bad_arg("hd_run_identify_file: system-identification driver is outside this build's scope");
+hd_status hd_run_identify(const char* problem_json, const char* out_dir, char** result_json, int* stalled) {
+  if (!problem_json) return bad_arg("hd_run_identify: problem is NULL");
+  std::string out, err;
+  bool st = false;
+  const int code = heterodyn_driver::run_identify(problem_json, out_dir ? out_dir : "", &out, &st, &err);
+  return identify_finish(code, out, st, err, result_json, stalled);
+}
+hd_status hd_run_identify_file(const char* problem_path, const char* out_dir, char** result_json, int* stalled) {
+  if (!problem_path) return bad_arg("hd_run_identify_file: path is NULL");
+  std::string out, err;
+  bool st = false;
+  const int code = heterodyn_driver::run_identify_file(problem_path, out_dir ? out_dir : "", &out, &st, &err);
+  return identify_finish(code, out, st, err, result_json, stalled);
 }
 
 // Host-only: builds the factor without touching the GPU (drivers.cpp:990-1006).

@@ -40,6 +40,10 @@ SIGNATURES = {
     "hd_scene_element_count": (C.c_int, [_VP]),
     "hd_scene_frame_count": (C.c_int, [_VP]),
     "hd_scene_name": (C.c_char_p, [_VP]),
+    "hd_scene_region_count": (C.c_int, [_VP]),
+    "hd_scene_regions": (C.c_int, [_VP, C.POINTER(C.c_int), C.c_size_t]),
+    "hd_scene_rest_positions": (C.c_int, [_VP, _D, C.c_size_t]),
+    "hd_scene_vertex_masses": (C.c_int, [_VP, _D, C.c_size_t]),
     "hd_sim_create": (_VP, [_VP]),
     "hd_sim_free": (None, [_VP]),
     "hd_sim_step": (C.c_int, [_VP]),
@@ -146,6 +150,21 @@ class Library:
             raise HdError(self.lib.hd_last_error_code(), self.lib.hd_last_error().decode())
         return Scene(self, h)
 
+    def run_identify(self, problem, out_dir: str | None = None) -> tuple[dict, bool]:
+        """hd_run_identify: L-BFGS system identification (drivers.cpp:805-979);
+        returns (result, stalled)."""
+        text = problem if isinstance(problem, str) else json.dumps(problem)
+        p, st = _VP(), C.c_int(-1)
+        self.check(self.lib.hd_run_identify(text.encode(), out_dir.encode() if out_dir else None,
+                                            C.byref(p), C.byref(st)))
+        return json.loads(self._take_string(p)), bool(st.value)
+
+    def run_identify_file(self, path: str, out_dir: str | None = None) -> tuple[dict, bool]:
+        p, st = _VP(), C.c_int(-1)
+        self.check(self.lib.hd_run_identify_file(path.encode(), out_dir.encode() if out_dir else None,
+                                                 C.byref(p), C.byref(st)))
+        return json.loads(self._take_string(p)), bool(st.value)
+
     def load(self, path: str) -> "Scene":
         h = self.lib.hd_scene_load(path.encode())
         if not h:
@@ -181,6 +200,25 @@ class Scene:
     @property
     def name(self):
         return self.L.lib.hd_scene_name(self.h).decode()
+
+    @property
+    def region_count(self):
+        return self.L.lib.hd_scene_region_count(self.h)
+
+    def regions(self):
+        out = np.zeros(self.element_count, dtype=np.int32)
+        self.L.check(self.L.lib.hd_scene_regions(self.h, out.ctypes.data_as(C.POINTER(C.c_int)), out.size))
+        return out
+
+    def rest_positions(self):
+        out = np.zeros(3 * self.vertex_count)
+        self.L.check(self.L.lib.hd_scene_rest_positions(self.h, _ptr(out), out.size))
+        return out
+
+    def vertex_masses(self):
+        out = np.zeros(self.vertex_count)
+        self.L.check(self.L.lib.hd_scene_vertex_masses(self.h, _ptr(out), out.size))
+        return out
 
     def factor_stats(self) -> dict:
         p = _VP()

@@ -321,3 +321,35 @@ def test_set_young_refactor_matches_oracle(prod, orc):
     sim.record(True)
     sim.step(2)
     np.testing.assert_allclose(sim.positions(), qp, rtol=0, atol=1e-12 * np.abs(qp).max())
+
+
+@pytest.mark.parametrize("case", ["v0-trajectory", "regions", "young-block", "v0-contact"])
+def test_identify_matches_oracle(prod, orc, case, tmp_path):
+    """hd_run_identify (drivers.cpp:805-979) on the device engine: the same
+    L-BFGS driver over the oracle takes the same path — evaluation count,
+    refactorizations, loss curve and recovered parameters."""
+    two_tet = {"mesh": {"generator": "two-tet"}}
+    opt = {"max_evals": 40, "grad_tol": 1e-12}
+    problem = {
+        "v0-trajectory": {"scene": two_tet, "design": {"variable": "v0", "initial": [0, 0, 0]},
+                          "true": [0.3, -0.1, 0.2], "loss": {"kind": "trajectory"}, "optimizer": opt},
+        "regions": {"scene": two_tet, "design": {"variable": "young_regions", "initial": [5e5, 5e5]},
+                    "true": [1e6, 2e5], "loss": {"kind": "trajectory"}, "optimizer": opt},
+        "young-block": {"scene": scenes.block_scene(dims=(4, 3, 2), contrast=10.0, beta0=0.0, frames=3),
+                        "design": {"variable": "young", "initial": 3e4}, "true": 5e4,
+                        "loss": {"kind": "final_pose"}, "optimizer": {"max_evals": 12, "grad_tol": 1e-14}},
+        "v0-contact": {"scene": scenes.block_scene(dims=(3, 2, 2), floor=True, frames=3),
+                       "design": {"variable": "v0", "initial": [0, 0, 0]}, "true": [0.05, 0.0, -0.1],
+                       "loss": {"kind": "trajectory"}, "optimizer": {"max_evals": 15, "grad_tol": 1e-12}},
+    }[case]
+    rp, sp = prod.run_identify(problem, str(tmp_path / "prod"))
+    ro, so = orc.run_identify(problem, str(tmp_path / "oracle"))
+    for k in ("evaluations", "factorizations", "material_updates", "converged", "stalled"):
+        assert rp[k] == ro[k], (k, rp[k], ro[k])
+    assert sp == so
+    assert rel2(rp["recovered"], ro["recovered"]) <= 1e-6
+    cp = np.loadtxt(tmp_path / "prod" / "loss_curve.csv", delimiter=",", skiprows=1, ndmin=2)
+    co = np.loadtxt(tmp_path / "oracle" / "loss_curve.csv", delimiter=",", skiprows=1, ndmin=2)
+    assert cp.shape == co.shape
+    scale = max(co[0, 1], 1e-300)
+    assert np.max(np.abs(cp[:, 1] - co[:, 1])) <= 1e-6 * scale
