@@ -347,7 +347,7 @@ def test_identify_matches_oracle(prod, orc, case, tmp_path):
     for k in ("evaluations", "factorizations", "material_updates", "converged", "stalled"):
         assert rp[k] == ro[k], (k, rp[k], ro[k])
     assert sp == so
-    assert rel2(rp["recovered"], ro["recovered"]) <= 1e-6
+    assert rel2(np.array(rp["recovered"]), np.array(ro["recovered"])) <= 1e-6
     cp = np.loadtxt(tmp_path / "prod" / "loss_curve.csv", delimiter=",", skiprows=1, ndmin=2)
     co = np.loadtxt(tmp_path / "oracle" / "loss_curve.csv", delimiter=",", skiprows=1, ndmin=2)
     assert cp.shape == co.shape
