@@ -5,7 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
-#include <sstream>
+
 
 #include <nlohmann/json.hpp>
 

@@ -4,9 +4,8 @@
 // backward chain, state control and counters.
 #include <cstdlib>
 #include <cstring>
-#include <fstream>
+#include <cstdio>
 #include <memory>
-#include <sstream>
 
 #include <nlohmann/json.hpp>
 
@@ -78,12 +77,16 @@ hd_scene* make_scene(const char* who, const void* arg, Make&& make) {
   return s.release();
 }
 
+// stdio, not iostreams: the library links its own libstdc++, whose stream
+// locale state is not set up when it is dlopen'ed next to another one.
 std::string read_file(const char* path) {
-  std::ifstream in(path);
-  if (!in) raise(Code::Io, std::string("cannot open scene file: ") + path);
-  std::stringstream b;
-  b << in.rdbuf();
-  return b.str();
+  FILE* f = std::fopen(path, "rb");
+  if (!f) raise(Code::Io, std::string("cannot open scene file: ") + path);
+  std::string text;
+  char buf[65536];
+  for (size_t n; (n = std::fread(buf, 1, sizeof buf, f)) > 0;) text.append(buf, n);
+  std::fclose(f);
+  return text;
 }
 }  // namespace
 

@@ -8,7 +8,7 @@
 #include <limits>
 #include <map>
 #include <set>
-#include <sstream>
+
 
 #include <nlohmann/json.hpp>
 

@@ -121,3 +121,21 @@ def test_scene_data_accessors_agree(orc, prod):
         assert np.array_equal(a.regions(), b.regions())
         assert np.array_equal(a.rest_positions(), b.rest_positions())
         assert np.allclose(a.vertex_masses(), b.vertex_masses(), rtol=1e-14, atol=0)
+
+
+def test_scene_and_problem_files(orc, prod, tmp_path):
+    """hd_scene_load and hd_run_identify_file read real files inside a Python
+    process (stdio readers; the libraries carry their own libstdc++)."""
+    scene_path = tmp_path / "scene.json"
+    scene_path.write_text(json.dumps(TWO_TET))
+    for L in (orc, prod):
+        sc = L.load(str(scene_path))
+        assert (sc.vertex_count, sc.element_count) == (5, 2)
+    problem = {"scene_file": str(scene_path), "design": {"variable": "v0", "initial": [0, 0, 0]},
+               "true": [0.1, 0.0, 0.0], "optimizer": {"max_evals": 40, "grad_tol": 1e-12}}
+    path = tmp_path / "problem.json"
+    path.write_text(json.dumps(problem))
+    r, stalled = orc.run_identify_file(str(path), str(tmp_path / "out" / "nested"))
+    assert r["converged"] and not stalled
+    assert abs(r["recovered"][0] - 0.1) <= 1e-8
+    assert (tmp_path / "out" / "nested" / "result.json").exists()
