@@ -105,6 +105,15 @@ HD_API int hd_scene_region_count(const hd_scene* scene);
 HD_API hd_status hd_scene_regions(const hd_scene* scene, int* region_of_element, size_t capacity);
 HD_API hd_status hd_scene_rest_positions(const hd_scene* scene, double* out, size_t capacity);
 HD_API hd_status hd_scene_vertex_masses(const hd_scene* scene, double* out, size_t capacity);
+/* Per-element Young's moduli of the scene's material (MaterialField::young). */
+HD_API hd_status hd_scene_young_moduli(const hd_scene* scene, double* out, size_t capacity);
+
+/* The external force f_ext the sim steps with (dof doubles; initially the
+ * scene's gravity + point forces, scene_external_force scene.cpp:530-540):
+ * read it, or replace it for subsequent steps (the gradcheck driver's f_ext
+ * perturbations, drivers.cpp:471-483). */
+HD_API hd_status hd_sim_external_force(const hd_sim* sim, double* out, size_t capacity);
+HD_API hd_status hd_sim_set_external_force(hd_sim* sim, const double* f_ext, size_t count);
 
 /* Records every subsequent frame's adjoint cache (the reference's
  * roll(keep_caches=true), drivers.cpp:31-54).  enable=0 stops recording and

@@ -9,7 +9,7 @@
 
 #include <nlohmann/json.hpp>
 
-#include "../paper_2605_14526_b200/csrc/identify.hpp"
+#include "../paper_2605_14526_b200/csrc/drivers.hpp"
 
 #include "../include/heterodyn.h"
 #include "oracle.hpp"
@@ -134,6 +134,17 @@ hd_status hd_scene_vertex_masses(const hd_scene* s, double* out, size_t cap) {
   return HD_OK;
 }
 
+hd_status hd_scene_young_moduli(const hd_scene* s, double* out, size_t cap) {
+  if (!s) return null_arg("hd_scene_young_moduli");
+  const int ne = s->spec.material.element_count();
+  if (!out || cap < static_cast<size_t>(ne)) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_scene_young_moduli: output buffer too small");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  for (int e = 0; e < ne; ++e) out[e] = s->spec.material.young(e);
+  return HD_OK;
+}
+
 hd_sim* hd_sim_create(const hd_scene* scene) {
   if (!scene) { null_arg("hd_sim_create"); return nullptr; }
   hd_sim* sim = new hd_sim;
@@ -218,11 +229,21 @@ hd_status hd_run_simulate(const hd_scene* scene, const char* out_dir, char** sum
     (void)out_dir;
   });
 }
-hd_status hd_run_gradcheck(const hd_scene*, const char*, const char*, char**, int*) {
-  set_error(HD_ERR_INVALID_ARGUMENT, "hd_run_gradcheck: not provided by the oracle library");
-  return HD_ERR_INVALID_ARGUMENT;
+hd_status hd_run_gradcheck(const hd_scene* scene, const char* vars_csv, const char* out_path, char** report_json,
+                           int* pass) {
+  if (!scene) return null_arg("hd_run_gradcheck");
+  std::string out, err;
+  bool ok = false;
+  const int code = heterodyn_driver::run_gradcheck(scene, vars_csv, out_path, &out, &ok, &err);
+  if (code != HD_OK) {
+    set_error(code, err);
+    return static_cast<hd_status>(code);
+  }
+  if (report_json) *report_json = copy_string(out);
+  if (pass) *pass = ok ? 1 : 0;
+  return HD_OK;
 }
-// System identification: the product's L-BFGS driver (identify.cpp, written
+// System identification: the product's L-BFGS driver (drivers.cpp, written
 // against the public ABI only) linked over this library's CPU restatement, so
 // the parity tests compare the solvers underneath one optimizer.
 static hd_status identify_finish(int code, const std::string& out, bool st, const std::string& err, char** result_json,
@@ -288,6 +309,20 @@ hd_status hd_sim_set_state(hd_sim* sim, const double* q, const double* v, double
   if (v) sim->state.v.assign(v, v + n);
   sim->state.time = time;
   sim->caches.clear();
+  return HD_OK;
+}
+
+hd_status hd_sim_external_force(const hd_sim* sim, double* out, size_t cap) {
+  if (!sim) return null_arg("hd_sim_external_force");
+  return copy_vector(sim->f_ext, out, cap, "hd_sim_external_force");
+}
+hd_status hd_sim_set_external_force(hd_sim* sim, const double* f, size_t count) {
+  if (!sim) return null_arg("hd_sim_set_external_force");
+  if (!f || count != static_cast<size_t>(sim->f_ext.size())) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_sim_set_external_force: expected dof doubles");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  sim->f_ext.assign(f, f + count);
   return HD_OK;
 }
 

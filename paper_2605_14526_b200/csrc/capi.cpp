@@ -12,7 +12,7 @@
 #include "../../include/heterodyn.h"
 #include "batch.hpp"
 #include "engine.hpp"
-#include "identify.hpp"
+#include "drivers.hpp"
 
 using namespace hdb;
 
@@ -134,6 +134,14 @@ hd_status hd_scene_vertex_masses(const hd_scene* s, double* out, size_t cap) {
   return HD_OK;
 }
 
+hd_status hd_scene_young_moduli(const hd_scene* s, double* out, size_t cap) {
+  if (!s) return bad_arg("hd_scene_young_moduli: scene is NULL");
+  const Vec& y = s->spec.material.young;
+  if (!out || cap < y.size()) return bad_arg("hd_scene_young_moduli: output buffer too small");
+  std::copy(y.begin(), y.end(), out);
+  return HD_OK;
+}
+
 hd_sim* hd_sim_create(const hd_scene* scene) {
   if (!scene) {
     bad_arg("hd_sim_create: scene is NULL");
@@ -190,11 +198,22 @@ hd_status hd_run_simulate(const hd_scene* scene, const char* out_dir, char** sum
   });
 }
 
-hd_status hd_run_gradcheck(const hd_scene*, const char*, const char*, char**, int*) {
-  return bad_arg("hd_run_gradcheck: finite-difference driver is outside this build's scope (use hd_sim_backward)");
+hd_status hd_run_gradcheck(const hd_scene* scene, const char* vars_csv, const char* out_path, char** report_json,
+                           int* pass) {
+  if (!scene) return bad_arg("hd_run_gradcheck: scene is NULL");
+  std::string out, err;
+  bool ok = false;
+  const int code = heterodyn_driver::run_gradcheck(scene, vars_csv, out_path, &out, &ok, &err);
+  if (code != HD_OK) {
+    set_error(code, err);
+    return static_cast<hd_status>(code);
+  }
+  if (report_json) *report_json = dup(out);
+  if (pass) *pass = ok ? 1 : 0;
+  return HD_OK;
 }
 // System identification: the L-BFGS driver over this library's own ABI
-// (identify.cpp; reference capi.cpp:279-308).
+// (drivers.cpp; reference capi.cpp:279-308).
 static hd_status identify_finish(int code, const std::string& out, bool st, const std::string& err, char** result_json,
                           int* stalled) {
   if (code != HD_OK) {
@@ -263,6 +282,17 @@ int hd_sim_recorded_frames(const hd_sim* sim) { return sim ? sim->eng->recorded(
 hd_status hd_sim_set_state(hd_sim* sim, const double* q, const double* v, double time) {
   if (!sim) return bad_arg("hd_sim_set_state: sim is NULL");
   return guarded([&] { sim->eng->set_state(q, v, time); });
+}
+
+hd_status hd_sim_external_force(const hd_sim* sim, double* out, size_t cap) {
+  if (!sim) return bad_arg("hd_sim_external_force: sim is NULL");
+  if (!out || cap < sim->eng->dof_count()) return bad_arg("hd_sim_external_force: output buffer too small");
+  return guarded([&] { sim->eng->external_force_into(out); });
+}
+hd_status hd_sim_set_external_force(hd_sim* sim, const double* f, size_t count) {
+  if (!sim) return bad_arg("hd_sim_set_external_force: sim is NULL");
+  if (!f || count != sim->eng->dof_count()) return bad_arg("hd_sim_set_external_force: expected dof doubles");
+  return guarded([&] { sim->eng->set_external_force(f); });
 }
 
 hd_status hd_sim_backward(hd_sim* sim, const double* direct, const double* dq_final, const double* dv_final,

@@ -1,5 +1,6 @@
-// System-identification driver (the reference's run_identify,
-// drivers.cpp:570-979, with lbfgs_minimize, lbfgs.cpp:40-143).
+// Host drivers of the reference ABI: system identification (run_identify,
+// drivers.cpp:570-979, with lbfgs_minimize, lbfgs.cpp:40-143) and the
+// finite-difference gradient check (run_gradcheck, drivers.cpp:367-531).
 //
 // Written against the public C ABI only (heterodyn.h: scenes, hd_sim_step,
 // hd_sim_set_young, hd_sim_set_state, hd_sim_record, hd_sim_backward), so the
@@ -8,7 +9,7 @@
 // through whichever library this file is linked into (the device engine in
 // libheterodyn_b200.so; the CPU restatement in the oracle library, which links
 // the same driver so the tests compare the solvers underneath it).
-#include "identify.hpp"
+#include "drivers.hpp"
 
 #include <algorithm>
 #include <array>
@@ -640,6 +641,196 @@ int run_identify_file(const std::string& path, const std::string& out_dir, std::
   for (size_t n; (n = std::fread(buf, 1, sizeof buf, f)) > 0;) text.append(buf, n);
   std::fclose(f);
   return run_identify(text, out_dir, result, stalled, error);
+}
+
+namespace {
+
+// ---- gradient check (drivers.cpp:367-531) ----------------------------------
+// sample_indices (drivers.cpp:174-181): at most `cap` evenly spaced indices
+std::vector<int> sample_indices(int n, int cap) {
+  const int m = std::min(n, cap);
+  std::vector<int> idx(m);
+  for (int k = 0; k < m; ++k) idx[k] = static_cast<int>((static_cast<long long>(k) * n) / m);
+  return idx;
+}
+
+double norm(const V& a) { return std::sqrt(dot(a, a)); }
+
+std::vector<std::string> split_csv(const char* csv) {  // capi.cpp:74-90
+  std::vector<std::string> out;
+  if (!csv) return out;
+  const std::string text(csv);
+  for (size_t start = 0; start <= text.size();) {
+    size_t comma = text.find(',', start);
+    if (comma == std::string::npos) comma = text.size();
+    const std::string item = text.substr(start, comma - start);
+    const size_t a = item.find_first_not_of(" \t"), b = item.find_last_not_of(" \t");
+    if (a != std::string::npos) out.push_back(item.substr(a, b - a + 1));
+    start = comma + 1;
+  }
+  return out;
+}
+
+std::string gradcheck(const hd_scene* sc, std::vector<std::string> vars, const std::string& out_path, bool* pass) {
+  if (vars.empty()) vars = {"q0", "v0", "f_ext", "E"};  // capi.cpp:269
+  for (const auto& v : vars)
+    if (v != "q0" && v != "v0" && v != "f_ext" && v != "E" && v != "w")
+      fail(HD_ERR_INVALID_ARGUMENT, "gradcheck: unknown variable \"" + v + "\" (expected q0, v0, f_ext, E, w)");
+  const int nv = hd_scene_vertex_count(sc), ne = hd_scene_element_count(sc), frames = hd_scene_frame_count(sc);
+  const size_t n = 3 * static_cast<size_t>(nv);
+  SimPtr sim(hd_sim_create(sc));
+  if (!sim) fail(hd_last_error_code(), hd_last_error());
+  hd_sim* s = sim.get();
+  V q0(n), v0(n), f0(n), rest(n), young(ne);
+  check(hd_sim_positions(s, q0.data(), n));
+  check(hd_sim_velocities(s, v0.data(), n));
+  check(hd_sim_external_force(s, f0.data(), n));
+  check(hd_scene_rest_positions(sc, rest.data(), n));
+  check(hd_scene_young_moduli(sc, young.data(), young.size()));
+  // FD convention: the mesh-wide prox means stay at the scene's values while
+  // single moduli move (drivers.cpp:384-387)
+  check(hd_sim_set_young(s, young.data(), young.size(), 1));
+
+  // L = 1/2 |q_T - rest|^2 + 1/2 |v_T|^2 of a rollout (drivers.cpp:400-406)
+  V qf(n), vf(n);
+  std::vector<int> iterations;
+  const auto rollout = [&](const V& q, const V& v, const V& f, bool record) {
+    check(hd_sim_set_external_force(s, f.data(), n));
+    check(hd_sim_set_state(s, q.data(), v.data(), 0.0));
+    check(hd_sim_record(s, 0));
+    if (record) check(hd_sim_record(s, 1));
+    for (int t = 0; t < frames; ++t) {
+      check(hd_sim_step(s));
+      if (record) iterations.push_back(hd_sim_last_iterations(s));
+    }
+    check(hd_sim_positions(s, qf.data(), n));
+    check(hd_sim_velocities(s, vf.data(), n));
+    double l = 0;
+    for (size_t k = 0; k < n; ++k) l += 0.5 * (qf[k] - rest[k]) * (qf[k] - rest[k]) + 0.5 * vf[k] * vf[k];
+    return l;
+  };
+  const auto loss_of = [&](const V& q, const V& v, const V& f) { return rollout(q, v, f, false); };
+
+  // analytic pass: recorded rollout + chained adjoint (drivers.cpp:408-415)
+  rollout(q0, v0, f0, true);
+  V seed_q(n);
+  for (size_t k = 0; k < n; ++k) seed_q[k] = qf[k] - rest[k];
+  V g_q0(n), g_v0(n), g_f(n), g_e(ne), g_w(2 * static_cast<size_t>(ne), 0.0);
+  check(hd_sim_backward(s, nullptr, seed_q.data(), vf.data(), g_q0.data(), g_v0.data(), g_f.data(), g_e.data(),
+                        g_w.data(), g_w.size()));
+  V tau(frames), rho(frames);
+  check(hd_sim_backward_tau(s, tau.data(), rho.data(), frames));
+
+  json grad_norms = json::object(), per_var = json::object();
+  double max_rel = 0;
+  std::string worst_param;
+  const auto check_var = [&](const std::string& var, const V& analytic, int count, auto&& eval_at) {
+    grad_norms[var] = norm(analytic);
+    double scale = 0;
+    for (double a : analytic) scale = std::max(scale, std::abs(a));
+    scale = std::max(scale, 1e-30);
+    double worst = 0;
+    int worst_i = -1;
+    for (int i : sample_indices(count, 24)) {
+      const auto [fd, g] = eval_at(i, analytic);
+      const double denom = std::max({std::abs(fd), std::abs(g), 1e-4 * scale, 1e-12});
+      const double rel = std::abs(fd - g) / denom;
+      if (rel > worst) {
+        worst = rel;
+        worst_i = i;
+      }
+    }
+    per_var[var] = worst;
+    if (worst > max_rel) {
+      max_rel = worst;
+      worst_param = var + "[" + std::to_string(worst_i) + "]";
+    }
+  };
+  for (const auto& var : vars) {
+    if (var == "q0" || var == "v0" || var == "f_ext") {
+      const V& analytic = var == "q0" ? g_q0 : var == "v0" ? g_v0 : g_f;
+      const V& center = var == "q0" ? q0 : var == "v0" ? v0 : f0;
+      double cscale = 0;  // step floor tied to the variable's magnitude (drivers.cpp:462-466)
+      for (double c : center) cscale = std::max(cscale, std::abs(c));
+      check_var(var, analytic, static_cast<int>(n), [&](int i, const V& g) {
+        const double step = std::max({1e-6 * std::abs(center[i]), 1e-4 * cscale, 1e-7});
+        V plus = center, minus = center;
+        plus[i] += step;
+        minus[i] -= step;
+        double lp, lm;
+        if (var == "q0") {
+          lp = loss_of(plus, v0, f0);
+          lm = loss_of(minus, v0, f0);
+        } else if (var == "v0") {
+          lp = loss_of(q0, plus, f0);
+          lm = loss_of(q0, minus, f0);
+        } else {
+          lp = loss_of(q0, v0, plus);
+          lm = loss_of(q0, v0, minus);
+        }
+        return std::pair<double, double>{(lp - lm) / (2 * step), g[i]};
+      });
+    } else if (var == "E") {
+      check_var("E", g_e, ne, [&](int e, const V& g) {
+        const double step = 1e-4 * young[e];
+        V y = young;
+        y[e] = young[e] + step;
+        check(hd_sim_set_young(s, y.data(), y.size(), 1));
+        const double lp = loss_of(q0, v0, f0);
+        y[e] = young[e] - step;
+        check(hd_sim_set_young(s, y.data(), y.size(), 1));
+        const double lm = loss_of(q0, v0, f0);
+        check(hd_sim_set_young(s, young.data(), young.size(), 1));
+        return std::pair<double, double>{(lp - lm) / (2 * step), g[e]};
+      });
+    } else {  // "w": norm only (the weights are linear images of the moduli)
+      grad_norms["w"] = norm(g_w);
+    }
+  }
+  json j;  // report_to_json (drivers.cpp:517-531)
+  j["vars"] = vars;
+  j["tau"] = tau;
+  j["rho"] = rho;
+  j["iterations"] = iterations;
+  j["grad_norms"] = grad_norms;
+  json fd;
+  fd["max_rel_err"] = max_rel;
+  fd["worst_param"] = worst_param;
+  fd["per_var_max_rel_err"] = per_var;
+  j["fd_check"] = fd;
+  j["pass"] = max_rel <= 2e-3;
+  *pass = max_rel <= 2e-3;
+  const std::string out = j.dump(2);
+  if (!out_path.empty()) {
+    const size_t slash = out_path.rfind('/');
+    if (slash != std::string::npos && slash > 0) {  // create the parent directories
+      const std::string dir = out_path.substr(0, slash);
+      for (size_t pos = dir.find('/', 1); pos != std::string::npos; pos = dir.find('/', pos + 1))
+        ::mkdir(dir.substr(0, pos).c_str(), 0755);
+      ::mkdir(dir.c_str(), 0755);
+    }
+    FILE* f = std::fopen(out_path.c_str(), "w");
+    if (!f) fail(HD_ERR_IO, "cannot open output file: " + out_path);
+    std::fprintf(f, "%s\n", out.c_str());
+    std::fclose(f);
+  }
+  return out;
+}
+
+}  // namespace
+
+int run_gradcheck(const hd_scene* scene, const char* vars_csv, const char* out_path, std::string* report,
+                  bool* pass, std::string* error) {
+  try {
+    *report = gradcheck(scene, split_csv(vars_csv), out_path ? out_path : "", pass);
+    return HD_OK;
+  } catch (const Failure& f) {
+    *error = f.msg;
+    return f.code;
+  } catch (const std::exception& e) {
+    *error = e.what();
+    return HD_ERR_INVALID_ARGUMENT;
+  }
 }
 
 }  // namespace heterodyn_driver

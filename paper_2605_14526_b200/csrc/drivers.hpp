@@ -1,8 +1,11 @@
-// System-identification driver over the public C ABI (identify.cpp); linked
-// into both the product and the oracle library, each wrapping it as
-// hd_run_identify / hd_run_identify_file.
+// Host drivers over the public C ABI (drivers.cpp): system identification and
+// the finite-difference gradient check.  Linked into both the product and the
+// oracle library, each wrapping them as hd_run_identify(_file) /
+// hd_run_gradcheck.
 #pragma once
 #include <string>
+
+struct hd_scene;
 
 namespace heterodyn_driver {
 // Returns an hd_status; on failure *error holds the message.
@@ -10,4 +13,6 @@ int run_identify(const std::string& problem_text, const std::string& out_dir, st
                  std::string* error);
 int run_identify_file(const std::string& path, const std::string& out_dir, std::string* result, bool* stalled,
                       std::string* error);
+int run_gradcheck(const hd_scene* scene, const char* vars_csv, const char* out_path, std::string* report,
+                  bool* pass, std::string* error);
 }  // namespace heterodyn_driver

@@ -915,6 +915,18 @@ void Engine::set_state(const double* q, const double* v, double time) {
   nrec_ = 0;
 }
 
+void Engine::set_external_force(const double* f) {
+  const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
+  cuda_check(cudaMemcpyAsync(fext_, f, n3 * sizeof(double), cudaMemcpyHostToDevice, st_), "set f_ext");
+  cuda_check(cudaStreamSynchronize(st_), "set f_ext");
+}
+
+void Engine::external_force_into(double* out) const {
+  const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
+  cuda_check(cudaMemcpyAsync(out, fext_, n3 * sizeof(double), cudaMemcpyDeviceToHost, st_), "get f_ext");
+  cuda_check(cudaStreamSynchronize(st_), "get f_ext");
+}
+
 void Engine::reset_state() { set_state(scene_.q0.data(), scene_.v0.data(), 0.0); }
 
 Vec Engine::positions() const {

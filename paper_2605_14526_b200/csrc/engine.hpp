@@ -95,6 +95,8 @@ class Engine {
   void reserve_frames(int frames);  // allocate recorded-frame slots ahead of time
   int recorded() const { return nrec_; }
   void set_state(const double* q, const double* v, double time);
+  void set_external_force(const double* f);  // dof doubles into the device f_ext the graphs read
+  void external_force_into(double* out) const;
   // canonical: seed from device state, L = 1/2|q_T - ref|^2 (+ 1/2|v_T|^2 when
   // d_target is null and ref is the rest shape); d_target is a device array.
   // sinks: host buffers (any may be NULL) the gradients are copied into

@@ -44,6 +44,9 @@ SIGNATURES = {
     "hd_scene_regions": (C.c_int, [_VP, C.POINTER(C.c_int), C.c_size_t]),
     "hd_scene_rest_positions": (C.c_int, [_VP, _D, C.c_size_t]),
     "hd_scene_vertex_masses": (C.c_int, [_VP, _D, C.c_size_t]),
+    "hd_scene_young_moduli": (C.c_int, [_VP, _D, C.c_size_t]),
+    "hd_sim_external_force": (C.c_int, [_VP, _D, C.c_size_t]),
+    "hd_sim_set_external_force": (C.c_int, [_VP, _D, C.c_size_t]),
     "hd_sim_create": (_VP, [_VP]),
     "hd_sim_free": (None, [_VP]),
     "hd_sim_step": (C.c_int, [_VP]),
@@ -230,6 +233,19 @@ class Scene:
         self.L.check(self.L.lib.hd_run_simulate(self.h, out_dir.encode() if out_dir else None, C.byref(p)))
         return json.loads(self.L._take_string(p))
 
+    def run_gradcheck(self, variables: str | None = None, out_path: str | None = None) -> tuple[dict, bool]:
+        """hd_run_gradcheck: adjoint vs central differences (drivers.cpp:367-515);
+        returns (report, pass)."""
+        p, ok = _VP(), C.c_int(-1)
+        self.L.check(self.L.lib.hd_run_gradcheck(self.h, variables.encode() if variables is not None else None,
+                                                 out_path.encode() if out_path else None, C.byref(p), C.byref(ok)))
+        return json.loads(self.L._take_string(p)), bool(ok.value)
+
+    def young_moduli(self):
+        out = np.zeros(self.element_count)
+        self.L.check(self.L.lib.hd_scene_young_moduli(self.h, _ptr(out), out.size))
+        return out
+
     def batch(self, samples: int, young=None, threads: int = 8) -> "Batch":
         """hd_batch_create: `samples` parameter samples of this scene; young is a
         (samples, element_count) array of per-element Young's moduli or None."""
@@ -387,6 +403,15 @@ class Sim:
         out = np.empty(self.n)
         self.L.check(self.L.lib.hd_sim_solve_free(self.h, _ptr(rhs), _ptr(fq), _ptr(out)))
         return out
+
+    def external_force(self):
+        out = np.zeros(self.n)
+        self.L.check(self.L.lib.hd_sim_external_force(self.h, _ptr(out), out.size))
+        return out
+
+    def set_external_force(self, f):
+        f = _f64(f, self.n)
+        self.L.check(self.L.lib.hd_sim_set_external_force(self.h, _ptr(f), f.size))
 
     def set_young(self, young, freeze_means: bool = False):
         y = _f64(young)

@@ -353,3 +353,25 @@ def test_identify_matches_oracle(prod, orc, case, tmp_path):
     assert cp.shape == co.shape
     scale = max(co[0, 1], 1e-300)
     assert np.max(np.abs(cp[:, 1] - co[:, 1])) <= 1e-6 * scale
+
+
+@pytest.mark.parametrize("case", ["two-tet", "floor-contact", "corotated-pinned"])
+def test_gradcheck_matches_oracle(prod, orc, case):
+    """hd_run_gradcheck (drivers.cpp:367-531) on the device engine: same pass
+    verdict, per-frame tau and forward iteration counts as the oracle, the
+    same adjoint gradient norms (1e-6) and the same finite-difference errors
+    (the FD quotients amplify solver rounding, so to 1e-4 absolute)."""
+    scene = {"two-tet": None,
+             "floor-contact": scenes.block_scene(dims=(3, 2, 2), floor=True, frames=3),
+             "corotated-pinned": scenes.block_scene(dims=(3, 2, 2), kind="corotated", fix_x0_face=True, frames=2)}[case]
+    reps = {}
+    for name, lib in (("prod", prod), ("oracle", orc)):
+        sc = lib.builtin("two-tet") if scene is None else lib.scene(scene)
+        reps[name] = sc.run_gradcheck("q0,v0,f_ext,E,w")
+    (rp, okp), (ro, oko) = reps["prod"], reps["oracle"]
+    assert okp == oko == True
+    assert rp["tau"] == ro["tau"] and rp["iterations"] == ro["iterations"]
+    for k, v in ro["grad_norms"].items():
+        assert abs(rp["grad_norms"][k] - v) <= 1e-6 * max(abs(v), 1e-300), (k, rp["grad_norms"][k], v)
+    for k, v in ro["fd_check"]["per_var_max_rel_err"].items():
+        assert abs(rp["fd_check"]["per_var_max_rel_err"][k] - v) <= 1e-4, (k, rp["fd_check"], ro["fd_check"])

@@ -1,5 +1,5 @@
 """System-identification driver (hd_run_identify; reference drivers.cpp:570-979,
-lbfgs.cpp:40-143).  The driver (csrc/identify.cpp) is host logic over the
+lbfgs.cpp:40-143).  The driver (csrc/drivers.cpp) is host logic over the
 public ABI, linked into both libraries: on CPU it is checked through the
 oracle against the reference's own test (test_capi.cpp:241-284) and the
 other design variables by inverse-crime recovery; the product's problem
