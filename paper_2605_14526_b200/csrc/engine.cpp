@@ -1074,7 +1074,7 @@ void Engine::set_young(const Vec& young, bool freeze) {
   mat_.set_young(young, scene_.mesh.vol);
   cuda_check(cudaStreamSynchronize(st_), "sync");
   HostFactor nf = build_factor(scene_.mesh, mat_, scene_.solver.h, scene_.fixed, scene_.ordering, device_values_,
-                               &order_cache_);
+                               &order_cache_, &hf_);
   ++refactor_count;
   cols_.reset();  // its graph bakes the old factor and material pointers
   if (same_structure(hf_, nf)) {

@@ -20,8 +20,11 @@
 //    16-byte aligned chunks that the two streaming passes (solve.cu) split
 //    evenly over persistent CTAs.
 #include <algorithm>
+#include <atomic>
+#include <exception>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <numeric>
@@ -60,42 +63,74 @@ void parallel_chunks(int n, F&& fn) {
 
 // Scalar operator over all vertices; duplicates summed in sorted order and
 // exact zeros dropped (csr.cpp:7-32), so the graph matches the reference's.
+// Row-parallel assembly: each vertex row gathers its incident elements'
+// contributions (vertex -> element incidence), sums equal columns in a fixed
+// order (inertia first, then elements ascending) and drops exact zeros like
+// csr.cpp:24.  Same operator as the triplet sort of csr.cpp:9-31; the
+// summation order within an entry is fixed here instead of sort-dependent.
 Csr assemble(const Mesh& m, const Material& mat, double h) {
   if (!(h > 0)) raise(Code::Validation, "step size must be positive");
-  struct T { int r, c; double v; };
-  std::vector<T> t;
-  t.reserve(m.nv + 16 * static_cast<size_t>(m.ne));
+  const int nv = m.nv, ne = m.ne;
+  std::vector<int> inc_off(nv + 1, 0), inc(4 * static_cast<size_t>(ne));
+  for (int e = 0; e < ne; ++e)
+    for (int i = 0; i < 4; ++i) ++inc_off[m.el[e][i] + 1];
+  for (int v = 0; v < nv; ++v) inc_off[v + 1] += inc_off[v];
+  {
+    std::vector<int> cur(inc_off.begin(), inc_off.end() - 1);
+    for (int e = 0; e < ne; ++e)
+      for (int i = 0; i < 4; ++i) inc[cur[m.el[e][i]]++] = 4 * e + i;  // ascending e per vertex
+  }
+  // per element: w_e V_e and the four shape gradients
+  std::vector<double> G(12 * static_cast<size_t>(ne)), W(ne);
+  parallel_chunks(ne, [&](int lo, int hi, int) {
+    for (int e = lo; e < hi; ++e) {
+      W[e] = (mat.weight(e) + mat.beta[e] / h) * m.vol[e];
+      const double* b = &m.bm[9 * static_cast<size_t>(e)];
+      double* g = &G[12 * static_cast<size_t>(e)];
+      for (int c = 0; c < 3; ++c) {
+        g[3 + c] = b[0 * 3 + c];
+        g[6 + c] = b[1 * 3 + c];
+        g[9 + c] = b[2 * 3 + c];
+        g[c] = -(g[3 + c] + g[6 + c] + g[9 + c]);
+      }
+    }
+  });
   const double inertia = (1.0 + mat.alpha * h) / (h * h);
-  for (int v = 0; v < m.nv; ++v) t.push_back({v, v, inertia * m.mass[v]});
-  for (int e = 0; e < m.ne; ++e) {
-    const double w = (mat.weight(e) + mat.beta[e] / h) * m.vol[e];
-    const double* b = &m.bm[9 * static_cast<size_t>(e)];
-    double g[4][3];
-    for (int c = 0; c < 3; ++c) {
-      g[1][c] = b[0 * 3 + c];
-      g[2][c] = b[1 * 3 + c];
-      g[3][c] = b[2 * 3 + c];
-      g[0][c] = -(g[1][c] + g[2][c] + g[3][c]);
+  std::vector<std::vector<std::pair<int, double>>> rows(nv);
+  parallel_chunks(nv, [&](int lo, int hi, int) {
+    std::vector<std::pair<int, double>> t;
+    for (int v = lo; v < hi; ++v) {
+      t.clear();
+      t.push_back({v, inertia * m.mass[v]});
+      for (int k = inc_off[v]; k < inc_off[v + 1]; ++k) {
+        const int e = inc[k] >> 2, i = inc[k] & 3;
+        const double* g = &G[12 * static_cast<size_t>(e)];
+        for (int j = 0; j < 4; ++j)
+          t.push_back({m.el[e][j], W[e] * (g[3 * i] * g[3 * j] + g[3 * i + 1] * g[3 * j + 1] + g[3 * i + 2] * g[3 * j + 2])});
+      }
+      std::stable_sort(t.begin(), t.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      auto& r = rows[v];
+      for (size_t q = 0; q < t.size();) {
+        const int c = t[q].first;
+        double sum = 0;
+        while (q < t.size() && t[q].first == c) sum += t[q++].second;
+        if (sum != 0.0) r.push_back({c, sum});
+      }
     }
-    for (int i = 0; i < 4; ++i)
-      for (int j = 0; j < 4; ++j)
-        t.push_back({m.el[e][i], m.el[e][j], w * (g[i][0] * g[j][0] + g[i][1] * g[j][1] + g[i][2] * g[j][2])});
-  }
-  std::sort(t.begin(), t.end(), [](const T& a, const T& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; });
+  });
   Csr a;
-  a.rows = a.cols = m.nv;
-  a.off.assign(m.nv + 1, 0);
-  for (size_t i = 0; i < t.size();) {
-    const int r = t[i].r, c = t[i].c;
-    double s = 0;
-    while (i < t.size() && t[i].r == r && t[i].c == c) s += t[i++].v;
-    if (s != 0.0) {
-      a.col.push_back(c);
-      a.val.push_back(s);
-      ++a.off[r + 1];
-    }
-  }
-  for (int r = 0; r < m.nv; ++r) a.off[r + 1] += a.off[r];
+  a.rows = a.cols = nv;
+  a.off.assign(nv + 1, 0);
+  for (int v = 0; v < nv; ++v) a.off[v + 1] = a.off[v] + static_cast<int>(rows[v].size());
+  a.col.resize(a.off[nv]);
+  a.val.resize(a.off[nv]);
+  parallel_chunks(nv, [&](int lo, int hi, int) {
+    for (int v = lo; v < hi; ++v)
+      for (size_t q = 0; q < rows[v].size(); ++q) {
+        a.col[a.off[v] + q] = rows[v][q].first;
+        a.val[a.off[v] + q] = rows[v][q].second;
+      }
+  });
   return a;
 }
 
@@ -424,7 +459,8 @@ void metis_nd(const Graph& g, std::vector<int>& out) {
 }  // namespace
 
 HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const std::vector<int>& fixed,
-                        const std::string& ordering, bool device_values, std::vector<int>* order_cache) {
+                        const std::string& ordering, bool device_values, std::vector<int>* order_cache,
+                        const HostFactor* prev) {
   const auto t0 = std::chrono::steady_clock::now();
   HostFactor F;
   F.nv = mesh.nv;
@@ -581,37 +617,93 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
   F.l_nnz = lp[n];
   std::vector<int> li(static_cast<size_t>(lp[n]));
   Vec lx(static_cast<size_t>(lp[n])), d(n), y(n, 0.0);
-  std::vector<int> pattern(n), fill(n, 0);
-  for (int k = 0; k < n; ++k) {
-    int top = n;
-    flag[k] = k;
-    y[k] = 0.0;
-    for (const auto& [j0, val] : rowl[k]) {
-      y[j0] += val;
-      int len = 0;
-      for (int i = j0; flag[i] != k; i = parent[i]) {
-        pattern[len++] = i;
-        flag[i] = k;
+  std::vector<int> fill(n, 0);
+  // Up-looking row k touches only its own elimination subtree (its pattern,
+  // the columns it appends to and the y entries it scatters into are all
+  // descendants of k), so disjoint subtrees factor concurrently; the rows
+  // above them (the top separators) follow serially in elimination order.
+  const auto up_rows = [&](int r0, int r1, std::vector<int>& pattern) {
+    for (int k = r0; k <= r1; ++k) {
+      int top = n;
+      flag[k] = k;
+      y[k] = 0.0;
+      for (const auto& [j0, val] : rowl[k]) {
+        y[j0] += val;
+        int len = 0;
+        for (int i = j0; flag[i] != k; i = parent[i]) {
+          pattern[len++] = i;
+          flag[i] = k;
+        }
+        while (len > 0) pattern[--top] = pattern[--len];
       }
-      while (len > 0) pattern[--top] = pattern[--len];
+      double dk = y[k];
+      y[k] = 0.0;
+      for (; top < n; ++top) {
+        const int i = pattern[top];
+        const double yi = y[i];
+        y[i] = 0.0;
+        const long long end = lp[i] + fill[i];
+        for (long long p = lp[i]; p < end; ++p) y[li[p]] -= lx[p] * yi;
+        const double l = yi / d[i];
+        dk -= l * yi;
+        li[end] = k;
+        lx[end] = l;
+        ++fill[i];
+      }
+      if (!(dk > 0.0))
+        raise(Code::NotPositiveDefinite, "non-positive pivot " + std::to_string(dk) + " at position " + std::to_string(k));
+      d[k] = dk;
     }
-    double dk = y[k];
-    y[k] = 0.0;
-    for (; top < n; ++top) {
-      const int i = pattern[top];
-      const double yi = y[i];
-      y[i] = 0.0;
-      const long long end = lp[i] + fill[i];
-      for (long long p = lp[i]; p < end; ++p) y[li[p]] -= lx[p] * yi;
-      const double l = yi / d[i];
-      dk -= l * yi;
-      li[end] = k;
-      lx[end] = l;
-      ++fill[i];
+  };
+  {
+    // subtree tasks: split the costliest subtree (cost ~ sum of cnt^2) into
+    // its children until there are enough balanced tasks
+    std::vector<double> cost(n);
+    for (int j = 0; j < n; ++j) cost[j] = 1.0 + static_cast<double>(cnt[j]) * cnt[j];
+    for (int j = 0; j < n; ++j)
+      if (parent[j] >= 0) cost[parent[j]] += cost[j];
+    std::vector<std::vector<int>> kids(n);
+    std::vector<int> roots;
+    for (int j = 0; j < n; ++j) (parent[j] >= 0 ? kids[parent[j]] : roots).push_back(j);
+    const int T = hw_threads();
+    std::vector<int> tasks = roots;
+    std::vector<char> is_top(n, 0);
+    double total = 0;
+    for (int r : roots) total += cost[r];
+    for (;;) {
+      auto it = std::max_element(tasks.begin(), tasks.end(), [&](int a, int b) { return cost[a] < cost[b]; });
+      if (it == tasks.end() || static_cast<int>(tasks.size()) >= 8 * T || cost[*it] < total / (4.0 * T) ||
+          kids[*it].empty())
+        break;
+      const int r = *it;
+      tasks.erase(it);
+      is_top[r] = 1;
+      tasks.insert(tasks.end(), kids[r].begin(), kids[r].end());
     }
-    if (!(dk > 0.0))
-      raise(Code::NotPositiveDefinite, "non-positive pivot " + std::to_string(dk) + " at position " + std::to_string(k));
-    d[k] = dk;
+    std::sort(tasks.begin(), tasks.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+
+    std::vector<std::exception_ptr> err(T);
+    std::atomic<int> next{0};
+    std::vector<std::thread> pool;
+    const int workers = std::min<int>(T, static_cast<int>(tasks.size()));
+    for (int t = 0; t < workers; ++t)
+      pool.emplace_back([&, t] {
+        std::vector<int> pattern(n);
+        try {
+          for (int q; (q = next.fetch_add(1)) < static_cast<int>(tasks.size());) {
+            const int r = tasks[q];
+            up_rows(r - sz[r] + 1, r, pattern);
+          }
+        } catch (...) {
+          err[t] = std::current_exception();
+        }
+      });
+    for (auto& th : pool) th.join();
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
+    std::vector<int> pattern(n);
+    for (int k = 0; k < n; ++k)
+      if (is_top[k]) up_rows(k, k, pattern);
   }
   lap(F.ms_phase[3]);  // LDL^T
   // 5. S' rows: column c of L^{-1} lives on c's ancestor path; every entry of
@@ -652,63 +744,80 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
   });
   }
   lap(F.ms_phase[4]);  // S' values
-  // 6. segments (row parts inside 256-column tiles)
-  const int W = F.tile_w;
-  const int ntiles = (n + W - 1) / W;
-  F.row_pslot.assign(n + 1, 0);
-  std::vector<std::vector<Segment>> per_tile(ntiles);
-  for (int r = 0; r < n; ++r) {
-    const int first = r - sz[r] + 1;
-    const int t0 = first / W, t1 = r / W;
-    F.row_pslot[r + 1] = F.row_pslot[r] + (t1 - t0 + 1);
-    for (int t = t0; t <= t1; ++t) {
-      const int clo = std::max(first, t * W), chi = std::min(r, t * W + W - 1);
-      per_tile[t].push_back({F.row_off[r] + (clo - first), r, clo, chi - clo + 1, F.row_pslot[r] + (t - t0)});
-    }
-  }
-  for (int t = 0; t < ntiles; ++t) F.seg.insert(F.seg.end(), per_tile[t].begin(), per_tile[t].end());
-  // 6b. tile-major value stream: per tile, chunks of whole segments, every
-  //     chunk 16-byte aligned, descriptors contiguous per chunk
-  {
-    F.tile_chunk.assign(ntiles + 1, 0);
-    if (!device_values) F.stream.reserve(static_cast<size_t>(F.row_off[n] * 1.02) + 16);
-    else {
-      F.build.seg_off.assign(F.row_pslot[n], 0);
-      F.build.seg_clo.assign(F.row_pslot[n], 0);
-    }
-    long long slen = 0;
-    for (int t = 0; t < ntiles; ++t) {
-      const auto& list = per_tile[t];
-      size_t s = 0;
-      while (s < list.size()) {
-        ChunkDesc c{slen, 0, static_cast<int>(F.sdesc.size()), 0, t};
-        int vals = 0;
-        while (s < list.size() && c.nseg < HDK_SEGS && vals + list[s].len <= HDK_VALS) {
-          const Segment& g = list[s];
-          F.sdesc.push_back({g.row, g.pslot, (g.clo - t * W) | (g.len << 16), vals});
-          if (device_values) {
-            F.build.seg_off[g.pslot] = slen + vals;
-            F.build.seg_clo[g.pslot] = g.clo;
-          } else {
-            F.stream.insert(F.stream.end(), F.sval.begin() + g.off, F.sval.begin() + g.off + g.len);
-          }
-          vals += g.len;
-          ++c.nseg;
-          ++s;
-        }
-        if (vals & 1) {
-          if (!device_values) F.stream.push_back(0.0);
-          ++vals;
-        }
-        c.len = vals;
-        slen += vals;
-        F.chunks.push_back(c);
+  // 6. segments (row parts inside 256-column tiles).  The layout depends only
+  //    on the elimination order and the row lengths, so a refactorization
+  //    whose structure is unchanged takes it from the previous factor.
+  const bool reuse = device_values && prev && prev->n == n && prev->tile_w == F.tile_w && prev->p2v == F.p2v &&
+                     prev->row_len == F.row_len && !prev->row_pslot.empty() &&
+                     prev->build.seg_off.size() == static_cast<size_t>(prev->row_pslot.back());
+  if (reuse) {
+    F.row_pslot = prev->row_pslot;
+    F.seg = prev->seg;
+    F.sdesc = prev->sdesc;
+    F.chunks = prev->chunks;
+    F.tile_chunk = prev->tile_chunk;
+    F.stream_len = prev->stream_len;
+    F.build.seg_off = prev->build.seg_off;
+    F.build.seg_clo = prev->build.seg_clo;
+  } else {
+    const int W = F.tile_w;
+    const int ntiles = (n + W - 1) / W;
+    F.row_pslot.assign(n + 1, 0);
+    std::vector<std::vector<Segment>> per_tile(ntiles);
+    for (int r = 0; r < n; ++r) {
+      const int first = r - sz[r] + 1;
+      const int t0 = first / W, t1 = r / W;
+      F.row_pslot[r + 1] = F.row_pslot[r] + (t1 - t0 + 1);
+      for (int t = t0; t <= t1; ++t) {
+        const int clo = std::max(first, t * W), chi = std::min(r, t * W + W - 1);
+        per_tile[t].push_back({F.row_off[r] + (clo - first), r, clo, chi - clo + 1, F.row_pslot[r] + (t - t0)});
       }
-      F.tile_chunk[t + 1] = static_cast<int>(F.chunks.size());
     }
-    F.stream_len = slen;
+    for (int t = 0; t < ntiles; ++t) F.seg.insert(F.seg.end(), per_tile[t].begin(), per_tile[t].end());
+    // 6b. tile-major value stream: per tile, chunks of whole segments, every
+    //     chunk 16-byte aligned, descriptors contiguous per chunk
+    {
+      F.tile_chunk.assign(ntiles + 1, 0);
+      if (!device_values) F.stream.reserve(static_cast<size_t>(F.row_off[n] * 1.02) + 16);
+      else {
+        F.build.seg_off.assign(F.row_pslot[n], 0);
+        F.build.seg_clo.assign(F.row_pslot[n], 0);
+      }
+      long long slen = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const auto& list = per_tile[t];
+        size_t s = 0;
+        while (s < list.size()) {
+          ChunkDesc c{slen, 0, static_cast<int>(F.sdesc.size()), 0, t};
+          int vals = 0;
+          while (s < list.size() && c.nseg < HDK_SEGS && vals + list[s].len <= HDK_VALS) {
+            const Segment& g = list[s];
+            F.sdesc.push_back({g.row, g.pslot, (g.clo - t * W) | (g.len << 16), vals});
+            if (device_values) {
+              F.build.seg_off[g.pslot] = slen + vals;
+              F.build.seg_clo[g.pslot] = g.clo;
+            } else {
+              F.stream.insert(F.stream.end(), F.sval.begin() + g.off, F.sval.begin() + g.off + g.len);
+            }
+            vals += g.len;
+            ++c.nseg;
+            ++s;
+          }
+          if (vals & 1) {
+            if (!device_values) F.stream.push_back(0.0);
+            ++vals;
+          }
+          c.len = vals;
+          slen += vals;
+          F.chunks.push_back(c);
+        }
+        F.tile_chunk[t + 1] = static_cast<int>(F.chunks.size());
+      }
+      F.stream_len = slen;
+    }
   }
-  // 7. A_ff and A_fd in elimination order (apply_a_free / fixed coupling)
+  // 7. A_ff and A_fd in elimination order (apply_a_free / fixed coupling):
+  //    row sizes first, then rows filled in parallel
   F.a_ff.rows = F.a_ff.cols = n;
   F.a_ff.off.assign(n + 1, 0);
   F.a_fd.rows = n;
@@ -716,18 +825,36 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
   F.a_fd.off.assign(n + 1, 0);
   for (int p = 0; p < n; ++p) {
     const int v = F.p2v[p];
-    std::vector<std::pair<int, double>> ff, fd;
-    for (int k = A.off[v]; k < A.off[v + 1]; ++k) {
-      const int w = A.col[k];
-      if (F.v2p[w] >= 0) ff.push_back({F.v2p[w], A.val[k]});
-      else fd.push_back({fixed_idx[w], A.val[k]});
-    }
-    std::sort(ff.begin(), ff.end());
-    for (auto& [c, val] : ff) { F.a_ff.col.push_back(c); F.a_ff.val.push_back(val); }
-    for (auto& [c, val] : fd) { F.a_fd.col.push_back(c); F.a_fd.val.push_back(val); }
-    F.a_ff.off[p + 1] = static_cast<int>(F.a_ff.col.size());
-    F.a_fd.off[p + 1] = static_cast<int>(F.a_fd.col.size());
+    int ff = 0, fd = 0;
+    for (int k = A.off[v]; k < A.off[v + 1]; ++k) (F.v2p[A.col[k]] >= 0 ? ff : fd) += 1;
+    F.a_ff.off[p + 1] = F.a_ff.off[p] + ff;
+    F.a_fd.off[p + 1] = F.a_fd.off[p] + fd;
   }
+  F.a_ff.col.resize(F.a_ff.off[n]);
+  F.a_ff.val.resize(F.a_ff.off[n]);
+  F.a_fd.col.resize(F.a_fd.off[n]);
+  F.a_fd.val.resize(F.a_fd.off[n]);
+  parallel_chunks(n, [&](int lo, int hi, int) {
+    std::vector<std::pair<int, double>> ff;
+    for (int p = lo; p < hi; ++p) {
+      const int v = F.p2v[p];
+      ff.clear();
+      int q = F.a_fd.off[p];
+      for (int k = A.off[v]; k < A.off[v + 1]; ++k) {
+        const int w = A.col[k];
+        if (F.v2p[w] >= 0) ff.push_back({F.v2p[w], A.val[k]});
+        else {
+          F.a_fd.col[q] = fixed_idx[w];
+          F.a_fd.val[q++] = A.val[k];
+        }
+      }
+      std::sort(ff.begin(), ff.end());
+      for (size_t i = 0; i < ff.size(); ++i) {
+        F.a_ff.col[F.a_ff.off[p] + i] = ff[i].first;
+        F.a_ff.val[F.a_ff.off[p] + i] = ff[i].second;
+      }
+    }
+  });
   F.millis = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return F;
 }

@@ -156,9 +156,11 @@ std::vector<int> tile_cta_ranges(const std::vector<int>& tile_chunk, const std::
 double factor_inverse_residual(const HostFactor& F);
 // order_cache: when it holds an ordering of the same size it is used as is
 // (the ordering depends only on the graph of the free vertices); otherwise
-// the computed ordering is stored into it.
+// the computed ordering is stored into it.  prev: the factor being replaced;
+// its stream layout is reused when the new elimination order and row lengths
+// match (device-built values only).
 HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const std::vector<int>& fixed,
                         const std::string& ordering, bool device_values = false,
-                        std::vector<int>* order_cache = nullptr);
+                        std::vector<int>* order_cache = nullptr, const HostFactor* prev = nullptr);
 
 }  // namespace hdb
