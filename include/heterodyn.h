@@ -105,6 +105,8 @@ HD_API int hd_scene_region_count(const hd_scene* scene);
 HD_API hd_status hd_scene_regions(const hd_scene* scene, int* region_of_element, size_t capacity);
 HD_API hd_status hd_scene_rest_positions(const hd_scene* scene, double* out, size_t capacity);
 HD_API hd_status hd_scene_vertex_masses(const hd_scene* scene, double* out, size_t capacity);
+/* Element connectivity (4 vertex indices per element). */
+HD_API hd_status hd_scene_elements(const hd_scene* scene, int* out, size_t capacity);
 /* Per-element Young's moduli of the scene's material (MaterialField::young). */
 HD_API hd_status hd_scene_young_moduli(const hd_scene* scene, double* out, size_t capacity);
 
@@ -114,6 +116,12 @@ HD_API hd_status hd_scene_young_moduli(const hd_scene* scene, double* out, size_
  * perturbations, drivers.cpp:471-483). */
 HD_API hd_status hd_sim_external_force(const hd_sim* sim, double* out, size_t capacity);
 HD_API hd_status hd_sim_set_external_force(hd_sim* sim, const double* f_ext, size_t count);
+/* Frame diagnostics of the simulate driver: the largest |Fischer-Burmeister
+ * residual| over the normal contacts of the last step (max_normal_fb_residual,
+ * drivers.cpp:147-159) and the current state's deepest obstacle penetration
+ * (max_penetration_at, drivers.cpp:101-111). */
+HD_API double hd_sim_last_fb_residual(const hd_sim* sim);
+HD_API double hd_sim_penetration(const hd_sim* sim);
 
 /* Records every subsequent frame's adjoint cache (the reference's
  * roll(keep_caches=true), drivers.cpp:31-54).  enable=0 stops recording and

@@ -31,6 +31,7 @@ struct hd_sim {
   int last_iterations = 0;
   bool last_converged = false;
   int last_contact_count = 0;
+  double last_fb_residual = 0;
   bool record = false;
   std::vector<ForwardCache> caches;
   std::vector<double> tau, rho;
@@ -134,6 +135,17 @@ hd_status hd_scene_vertex_masses(const hd_scene* s, double* out, size_t cap) {
   return HD_OK;
 }
 
+hd_status hd_scene_elements(const hd_scene* s, int* out, size_t cap) {
+  if (!s) return null_arg("hd_scene_elements");
+  const auto& el = s->spec.mesh.elements();
+  if (!out || cap < 4 * el.size()) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_scene_elements: output buffer too small");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  for (size_t e = 0; e < el.size(); ++e)
+    for (int k = 0; k < 4; ++k) out[4 * e + k] = el[e][k];
+  return HD_OK;
+}
 hd_status hd_scene_young_moduli(const hd_scene* s, double* out, size_t cap) {
   if (!s) return null_arg("hd_scene_young_moduli");
   const int ne = s->spec.material.element_count();
@@ -178,6 +190,13 @@ hd_status hd_sim_step(hd_sim* sim) {
     sim->last_iterations = cache.iteration_count;
     sim->last_converged = cache.converged;
     sim->last_contact_count = cache.contacts.normal_count();
+    double fb = 0;  // max_normal_fb_residual (drivers.cpp:147-159)
+    for (int c = 0; c < cache.contacts.normal_count(); ++c) {
+      const ContactPoint& cp = cache.contacts.contacts[c];
+      const double delta = cp.normal.dot(seg3(cache.q_star, cp.vertex)) - cp.gap_offset;
+      fb = std::max(fb, std::abs(fb_residual(delta, cp.r_n, cache.lambda_star[c])));
+    }
+    sim->last_fb_residual = fb;
     if (sim->record) sim->caches.push_back(std::move(cache));
   });
 }
@@ -194,40 +213,27 @@ hd_status hd_sim_velocities(const hd_sim* sim, double* out, size_t cap) {
 int hd_sim_last_iterations(const hd_sim* sim) { return sim ? sim->last_iterations : 0; }
 int hd_sim_last_converged(const hd_sim* sim) { return sim && sim->last_converged ? 1 : 0; }
 int hd_sim_last_contact_count(const hd_sim* sim) { return sim ? sim->last_contact_count : 0; }
+double hd_sim_last_fb_residual(const hd_sim* sim) { return sim ? sim->last_fb_residual : 0.0; }
+double hd_sim_penetration(const hd_sim* sim) {  // max_penetration_at (drivers.cpp:101-111)
+  if (!sim) return 0.0;
+  double pen = 0;
+  for (const auto& ob : sim->scene->spec.obstacles)
+    for (int v = 0; v < sim->scene->spec.mesh.vertex_count(); ++v)
+      pen = std::max(pen, -obstacle_signed_distance(ob, seg3(sim->state.q, v)));
+  return pen;
+}
 
-// ---- drivers: simulate, identify (gradcheck is out of scope here) ----
+// ---- drivers: simulate, gradcheck, identify (the shared drivers.cpp) ----
 hd_status hd_run_simulate(const hd_scene* scene, const char* out_dir, char** summary_json) {
   if (!scene) return null_arg("hd_run_simulate");
-  return guarded([&] {
-    const SceneSpec& s = scene->spec;
-    GlobalSystem sys;
-    MaterialField mat = s.material;
-    StateForce hs;
-    const StateForce* hook = nullptr;
-    if (s.has_hook) { hs = make_hook(s); hook = &hs; }
-    const VecX f = scene_external_force(s);
-    SimState st;
-    st.q = s.q0;
-    st.v = s.v0;
-    nlohmann::json sum;
-    std::vector<int> iters;
-    bool all = true;
-    double pen = 0;
-    for (int t = 0; t < s.frames; ++t) {
-      ForwardCache c = forward_step(s.mesh, mat, sys, s.solver, s.obstacles, s.fixed_vertices, st, f, hook);
-      iters.push_back(c.iteration_count);
-      all = all && c.converged;
-      for (const auto& ob : s.obstacles)
-        for (int v = 0; v < s.mesh.vertex_count(); ++v) pen = std::max(pen, -obstacle_signed_distance(ob, seg3(st.q, v)));
-    }
-    sum["frames"] = s.frames;
-    sum["iterations"] = iters;
-    sum["refactorizations"] = sys.refactor_count();
-    sum["all_converged"] = all;
-    sum["max_penetration"] = pen;
-    if (summary_json) *summary_json = copy_string(sum.dump(2));
-    (void)out_dir;
-  });
+  std::string out, err;
+  const int code = heterodyn_driver::run_simulate(scene, out_dir, &out, &err);
+  if (code != HD_OK) {
+    set_error(code, err);
+    return static_cast<hd_status>(code);
+  }
+  if (summary_json) *summary_json = copy_string(out);
+  return HD_OK;
 }
 hd_status hd_run_gradcheck(const hd_scene* scene, const char* vars_csv, const char* out_path, char** report_json,
                            int* pass) {

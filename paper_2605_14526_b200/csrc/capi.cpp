@@ -134,6 +134,14 @@ hd_status hd_scene_vertex_masses(const hd_scene* s, double* out, size_t cap) {
   return HD_OK;
 }
 
+hd_status hd_scene_elements(const hd_scene* s, int* out, size_t cap) {
+  if (!s) return bad_arg("hd_scene_elements: scene is NULL");
+  const auto& el = s->spec.mesh.el;
+  if (!out || cap < 4 * el.size()) return bad_arg("hd_scene_elements: output buffer too small");
+  for (size_t e = 0; e < el.size(); ++e)
+    for (int k = 0; k < 4; ++k) out[4 * e + k] = el[e][k];
+  return HD_OK;
+}
 hd_status hd_scene_young_moduli(const hd_scene* s, double* out, size_t cap) {
   if (!s) return bad_arg("hd_scene_young_moduli: scene is NULL");
   const Vec& y = s->spec.material.young;
@@ -175,27 +183,29 @@ hd_status hd_sim_velocities(const hd_sim* sim, double* out, size_t cap) {
 int hd_sim_last_iterations(const hd_sim* sim) { return sim ? sim->eng->last_iterations : 0; }
 int hd_sim_last_converged(const hd_sim* sim) { return sim && sim->eng->last_converged ? 1 : 0; }
 int hd_sim_last_contact_count(const hd_sim* sim) { return sim ? sim->eng->last_contacts : 0; }
+double hd_sim_last_fb_residual(const hd_sim* sim) {
+  double r = 0.0;
+  if (sim) guarded([&] { r = sim->eng->last_fb_residual(); });
+  return r;
+}
+double hd_sim_penetration(const hd_sim* sim) {
+  double r = 0.0;
+  if (sim) guarded([&] { r = sim->eng->penetration(); });
+  return r;
+}
 
+// The simulate driver (drivers.cpp; reference drivers.cpp:238-365): summary
+// JSON, and trajectory.jsonl / metrics.csv / summary.json under out_dir.
 hd_status hd_run_simulate(const hd_scene* scene, const char* out_dir, char** summary_json) {
   if (!scene) return bad_arg("hd_run_simulate: scene is NULL");
-  return guarded([&] {
-    Engine eng(scene->spec);
-    nlohmann::json s;
-    std::vector<int> its;
-    bool all = true;
-    for (int t = 0; t < scene->spec.frames; ++t) {
-      eng.step();
-      its.push_back(eng.last_iterations);
-      all = all && eng.last_converged;
-    }
-    s["frames"] = scene->spec.frames;
-    s["iterations"] = its;
-    s["refactorizations"] = eng.refactor_count;
-    s["all_converged"] = all;
-    s["max_penetration"] = 0.0;
-    (void)out_dir;
-    if (summary_json) *summary_json = dup(s.dump(2));
-  });
+  std::string out, err;
+  const int code = heterodyn_driver::run_simulate(scene, out_dir, &out, &err);
+  if (code != HD_OK) {
+    set_error(code, err);
+    return static_cast<hd_status>(code);
+  }
+  if (summary_json) *summary_json = dup(out);
+  return HD_OK;
 }
 
 hd_status hd_run_gradcheck(const hd_scene* scene, const char* vars_csv, const char* out_path, char** report_json,

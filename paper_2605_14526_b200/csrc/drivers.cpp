@@ -1,6 +1,7 @@
 // Host drivers of the reference ABI: system identification (run_identify,
-// drivers.cpp:570-979, with lbfgs_minimize, lbfgs.cpp:40-143) and the
-// finite-difference gradient check (run_gradcheck, drivers.cpp:367-531).
+// drivers.cpp:570-979, with lbfgs_minimize, lbfgs.cpp:40-143), the
+// finite-difference gradient check (run_gradcheck, drivers.cpp:367-531) and
+// the simulate driver's outputs (run_simulate, drivers.cpp:238-365).
 //
 // Written against the public C ABI only (heterodyn.h: scenes, hd_sim_step,
 // hd_sim_set_young, hd_sim_set_state, hd_sim_record, hd_sim_backward), so the
@@ -823,6 +824,235 @@ int run_gradcheck(const hd_scene* scene, const char* vars_csv, const char* out_p
                   bool* pass, std::string* error) {
   try {
     *report = gradcheck(scene, split_csv(vars_csv), out_path ? out_path : "", pass);
+    return HD_OK;
+  } catch (const Failure& f) {
+    *error = f.msg;
+    return f.code;
+  } catch (const std::exception& e) {
+    *error = e.what();
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+}
+
+namespace {
+
+// ---- simulate (drivers.cpp:238-365) -----------------------------------------
+// Worst vertex distance to the group's best rigid fit from rest (Kabsch,
+// drivers.cpp:115-145): one-sided Jacobi SVD of the 3x3 cross-covariance.
+double rigid_fit_residual(const std::vector<int>& verts, const V& rest, const V& q) {
+  if (verts.empty()) return 0.0;
+  double rc[3] = {0, 0, 0}, qc[3] = {0, 0, 0};
+  for (int v : verts)
+    for (int k = 0; k < 3; ++k) {
+      rc[k] += rest[3 * v + k];
+      qc[k] += q[3 * v + k];
+    }
+  for (int k = 0; k < 3; ++k) {
+    rc[k] /= verts.size();
+    qc[k] /= verts.size();
+  }
+  double a[3][3] = {}, vm[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};  // a = H = sum (r - rc)(q - qc)^T
+  for (int v : verts)
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) a[i][j] += (rest[3 * v + i] - rc[i]) * (q[3 * v + j] - qc[j]);
+  for (int sweep = 0; sweep < 60; ++sweep) {  // rotate column pairs of a until orthogonal: a = U S, H = U S V^T
+    double off = 0;
+    for (int p = 0; p < 2; ++p)
+      for (int r = p + 1; r < 3; ++r) {
+        double al = 0, be = 0, ga = 0;
+        for (int i = 0; i < 3; ++i) {
+          al += a[i][p] * a[i][p];
+          be += a[i][r] * a[i][r];
+          ga += a[i][p] * a[i][r];
+        }
+        if (std::abs(ga) <= 1e-15 * std::sqrt(al * be) || ga == 0.0) continue;
+        off = std::max(off, std::abs(ga) / std::sqrt(al * be));
+        const double z = (be - al) / (2 * ga);
+        const double t = (z >= 0 ? 1.0 : -1.0) / (std::abs(z) + std::sqrt(1 + z * z));
+        const double c = 1 / std::sqrt(1 + t * t), s = c * t;
+        for (int i = 0; i < 3; ++i) {
+          const double x = a[i][p], y = a[i][r];
+          a[i][p] = c * x - s * y;
+          a[i][r] = s * x + c * y;
+          const double vx = vm[i][p], vy = vm[i][r];
+          vm[i][p] = c * vx - s * vy;
+          vm[i][r] = s * vx + c * vy;
+        }
+      }
+    if (off <= 1e-15) break;
+  }
+  double sig[3];
+  int ord[3] = {0, 1, 2};
+  for (int k = 0; k < 3; ++k) sig[k] = std::sqrt(a[0][k] * a[0][k] + a[1][k] * a[1][k] + a[2][k] * a[2][k]);
+  std::sort(ord, ord + 3, [&](int x, int y) { return sig[x] > sig[y]; });
+  double u[3][3], w[3][3];  // sorted U, V columns
+  for (int k = 0; k < 3; ++k)
+    for (int i = 0; i < 3; ++i) {
+      u[i][k] = sig[ord[k]] > 0 ? a[i][ord[k]] / sig[ord[k]] : 0.0;
+      w[i][k] = vm[i][ord[k]];
+    }
+  const double tiny = 1e-12 * std::max(sig[ord[0]], 1e-300);
+  if (sig[ord[1]] <= tiny) {  // rank <= 1: complete U from the first column
+    const double* u0 = nullptr;
+    double c0[3] = {u[0][0], u[1][0], u[2][0]};
+    if (sig[ord[0]] <= 0) c0[0] = 1, c0[1] = 0, c0[2] = 0;
+    u0 = c0;
+    const double e[3] = {std::abs(u0[0]) < 0.9 ? 1.0 : 0.0, std::abs(u0[0]) < 0.9 ? 0.0 : 1.0, 0.0};
+    double c1[3] = {u0[1] * e[2] - u0[2] * e[1], u0[2] * e[0] - u0[0] * e[2], u0[0] * e[1] - u0[1] * e[0]};
+    const double nn = std::sqrt(c1[0] * c1[0] + c1[1] * c1[1] + c1[2] * c1[2]);
+    for (int i = 0; i < 3; ++i) {
+      u[i][0] = u0[i];
+      u[i][1] = c1[i] / nn;
+    }
+  }
+  if (sig[ord[2]] <= tiny) {  // rank <= 2: third column of U = first x second
+    u[0][2] = u[1][0] * u[2][1] - u[2][0] * u[1][1];
+    u[1][2] = u[2][0] * u[0][1] - u[0][0] * u[2][1];
+    u[2][2] = u[0][0] * u[1][1] - u[1][0] * u[0][1];
+  }
+  double rot[3][3];  // V U^T, reflected on the smallest singular direction if det < 0
+  const auto build = [&](double sgn) {
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) rot[i][j] = w[i][0] * u[j][0] + w[i][1] * u[j][1] + sgn * w[i][2] * u[j][2];
+  };
+  build(1.0);
+  const double det = rot[0][0] * (rot[1][1] * rot[2][2] - rot[1][2] * rot[2][1]) -
+                     rot[0][1] * (rot[1][0] * rot[2][2] - rot[1][2] * rot[2][0]) +
+                     rot[0][2] * (rot[1][0] * rot[2][1] - rot[1][1] * rot[2][0]);
+  if (det < 0) build(-1.0);
+  double worst = 0;
+  for (int v : verts) {
+    const double d[3] = {rest[3 * v] - rc[0], rest[3 * v + 1] - rc[1], rest[3 * v + 2] - rc[2]};
+    double e2 = 0;
+    for (int i = 0; i < 3; ++i) {
+      const double fit = rot[i][0] * d[0] + rot[i][1] * d[1] + rot[i][2] * d[2] + qc[i];
+      e2 += (q[3 * v + i] - fit) * (q[3 * v + i] - fit);
+    }
+    worst = std::max(worst, std::sqrt(e2));
+  }
+  return worst;
+}
+
+std::string simulate(const hd_scene* sc, const std::string& out_dir) {
+  const int nv = hd_scene_vertex_count(sc), ne = hd_scene_element_count(sc), frames = hd_scene_frame_count(sc);
+  const int nreg = hd_scene_region_count(sc);
+  const size_t n = 3 * static_cast<size_t>(nv);
+  V rest(n), young(ne);
+  std::vector<int> region(ne), el(4 * static_cast<size_t>(ne));
+  check(hd_scene_rest_positions(sc, rest.data(), n));
+  check(hd_scene_young_moduli(sc, young.data(), young.size()));
+  check(hd_scene_regions(sc, region.data(), region.size()));
+  check(hd_scene_elements(sc, el.data(), el.size()));
+  // region deformation tracking: softest and stiffest regions by mean modulus
+  std::vector<std::vector<int>> rverts;
+  std::vector<char> soft, stiff;
+  bool track = false;
+  if (nreg >= 2) {
+    V mean(nreg, 0.0);
+    std::vector<int> count(nreg, 0);
+    rverts.assign(nreg, {});
+    std::vector<std::vector<char>> seen(nreg, std::vector<char>(nv, 0));
+    for (int e = 0; e < ne; ++e) {
+      const int r = region[e];
+      mean[r] += young[e];
+      ++count[r];
+      for (int k = 0; k < 4; ++k) {
+        const int v = el[4 * e + k];
+        if (!seen[r][v]) {
+          seen[r][v] = 1;
+          rverts[r].push_back(v);
+        }
+      }
+    }
+    for (int r = 0; r < nreg; ++r)
+      if (count[r] > 0) mean[r] /= count[r];
+    const double lo = *std::min_element(mean.begin(), mean.end()), hi = *std::max_element(mean.begin(), mean.end());
+    soft.assign(nreg, 0);
+    stiff.assign(nreg, 0);
+    for (int r = 0; r < nreg; ++r) {
+      if (count[r] == 0) continue;
+      if (mean[r] <= lo * (1 + 1e-9)) soft[r] = 1;
+      if (mean[r] >= hi * (1 - 1e-9)) stiff[r] = 1;
+    }
+    track = hi > lo * (1 + 1e-9);
+  }
+  SimPtr sim(hd_sim_create(sc));
+  if (!sim) fail(hd_last_error_code(), hd_last_error());
+  hd_sim* s = sim.get();
+  FILE* traj = nullptr;
+  FILE* metrics = nullptr;
+  const bool emit = !out_dir.empty();
+  struct Closer {
+    FILE*& f;
+    ~Closer() {
+      if (f) std::fclose(f);
+    }
+  } c1{traj}, c2{metrics};
+  if (emit) {
+    for (size_t pos = out_dir.find('/', 1); pos != std::string::npos; pos = out_dir.find('/', pos + 1))
+      ::mkdir(out_dir.substr(0, pos).c_str(), 0755);
+    ::mkdir(out_dir.c_str(), 0755);
+    traj = std::fopen((out_dir + "/trajectory.jsonl").c_str(), "w");
+    metrics = std::fopen((out_dir + "/metrics.csv").c_str(), "w");
+    if (!traj || !metrics) fail(HD_ERR_IO, "cannot open output file in: " + out_dir);
+    std::fprintf(metrics, "frame,time,iterations,converged,contact_count,max_fb_residual,max_penetration\n");
+  }
+  std::vector<int> iterations;
+  bool all = true;
+  double max_pen = 0, soft_d = 0, stiff_d = 0;
+  V q(n), v(n);
+  for (int t = 0; t < frames; ++t) {
+    check(hd_sim_step(s));
+    const int it = hd_sim_last_iterations(s);
+    const bool conv = hd_sim_last_converged(s) != 0;
+    iterations.push_back(it);
+    all = all && conv;
+    const double pen = hd_sim_penetration(s);
+    max_pen = std::max(max_pen, pen);
+    if (track || emit) check(hd_sim_positions(s, q.data(), n));
+    if (track)
+      for (int r = 0; r < nreg; ++r) {
+        if (!soft[r] && !stiff[r]) continue;
+        const double d = rigid_fit_residual(rverts[r], rest, q);
+        if (soft[r]) soft_d = std::max(soft_d, d);
+        if (stiff[r]) stiff_d = std::max(stiff_d, d);
+      }
+    if (emit) {
+      check(hd_sim_velocities(s, v.data(), n));
+      json rec;
+      rec["time"] = hd_sim_time(s);
+      rec["q"] = q;
+      rec["v"] = v;
+      rec["iterations"] = it;
+      rec["converged"] = conv;
+      rec["contact_count"] = hd_sim_last_contact_count(s);
+      std::fprintf(traj, "%s\n", rec.dump().c_str());
+      std::fprintf(metrics, "%d,%g,%d,%d,%d,%g,%g\n", t + 1, hd_sim_time(s), it, conv ? 1 : 0,
+                   hd_sim_last_contact_count(s), hd_sim_last_fb_residual(s), pen);
+    }
+  }
+  json sum;  // summary_to_json (drivers.cpp:352-365)
+  sum["frames"] = frames;
+  sum["iterations"] = iterations;
+  sum["refactorizations"] = hd_sim_refactor_count(s);
+  sum["all_converged"] = all;
+  sum["max_penetration"] = max_pen;
+  if (track && stiff_d > 0) sum["displacement_ratio"] = soft_d / stiff_d;
+  const std::string out = sum.dump(2);
+  if (emit) {
+    FILE* f = std::fopen((out_dir + "/summary.json").c_str(), "w");
+    if (!f) fail(HD_ERR_IO, "cannot open output file: " + out_dir + "/summary.json");
+    std::fprintf(f, "%s\n", out.c_str());
+    std::fclose(f);
+  }
+  return out;
+}
+
+}  // namespace
+
+int run_simulate(const hd_scene* scene, const char* out_dir, std::string* summary, std::string* error) {
+  try {
+    *summary = simulate(scene, out_dir ? out_dir : "");
     return HD_OK;
   } catch (const Failure& f) {
     *error = f.msg;

@@ -15,4 +15,5 @@ int run_identify_file(const std::string& path, const std::string& out_dir, std::
                       std::string* error);
 int run_gradcheck(const hd_scene* scene, const char* vars_csv, const char* out_path, std::string* report,
                   bool* pass, std::string* error);
+int run_simulate(const hd_scene* scene, const char* out_dir, std::string* summary, std::string* error);
 }  // namespace heterodyn_driver

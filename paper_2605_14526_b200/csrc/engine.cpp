@@ -878,6 +878,7 @@ void Engine::step() {
   last_iterations = h_ctl_->iterations;
   last_converged = h_ctl_->converged;
   last_contacts = contacts ? contacts->nc : 0;
+  cur_contacts_ = contacts;
   if (recording_) slots_[nrec_].contacts = contacts;
   time_ += scene_.solver.h;
   if (recording_) ++nrec_;

@@ -97,6 +97,8 @@ class Engine {
   void set_state(const double* q, const double* v, double time);
   void set_external_force(const double* f);  // dof doubles into the device f_ext the graphs read
   void external_force_into(double* out) const;
+  double last_fb_residual() const;  // max |FB residual| over the last step's normal contacts
+  double penetration() const;       // deepest obstacle penetration of the current state
   // canonical: seed from device state, L = 1/2|q_T - ref|^2 (+ 1/2|v_T|^2 when
   // d_target is null and ref is the rest shape); d_target is a device array.
   // sinks: host buffers (any may be NULL) the gradients are copied into

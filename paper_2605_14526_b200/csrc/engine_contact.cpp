@@ -293,4 +293,33 @@ void Engine::backward_frame(int t, GradOut& out) {
   check_ctl("backward step");
 }
 
+// Simulate-driver diagnostics (drivers.cpp:101-111, 147-159), read on the
+// host after a step.
+double Engine::last_fb_residual() const {
+  const ContactFrame* c = cur_contacts_.get();
+  if (!c || c->nc == 0) return 0.0;
+  const Vec q = positions();
+  Vec lam(c->k);
+  cuda_check(cudaMemcpyAsync(lam.data(), c->lambda, c->k * sizeof(double), cudaMemcpyDeviceToHost, st_), "lambda");
+  cuda_check(cudaStreamSynchronize(st_), "lambda");
+  double worst = 0;
+  for (int i = 0; i < c->nc; ++i) {
+    const int v = c->vertex[i];
+    const double delta = c->normal[3 * i] * q[3 * v] + c->normal[3 * i + 1] * q[3 * v + 1] +
+                         c->normal[3 * i + 2] * q[3 * v + 2] - c->gap[i];
+    const double r = c->r_n[i], l = lam[i];
+    worst = std::max(worst, std::fabs(delta + r * l - std::sqrt(delta * delta + r * r * l * l)));
+  }
+  return worst;
+}
+
+double Engine::penetration() const {
+  if (scene_.obstacles.empty()) return 0.0;
+  const Vec q = positions();
+  double pen = 0;
+  for (const Obstacle& ob : scene_.obstacles)
+    for (int v = 0; v < scene_.mesh.nv; ++v) pen = std::max(pen, -signed_distance(ob, {q[3 * v], q[3 * v + 1], q[3 * v + 2]}));
+  return pen;
+}
+
 }  // namespace hdb

@@ -45,6 +45,9 @@ SIGNATURES = {
     "hd_scene_rest_positions": (C.c_int, [_VP, _D, C.c_size_t]),
     "hd_scene_vertex_masses": (C.c_int, [_VP, _D, C.c_size_t]),
     "hd_scene_young_moduli": (C.c_int, [_VP, _D, C.c_size_t]),
+    "hd_scene_elements": (C.c_int, [_VP, C.POINTER(C.c_int), C.c_size_t]),
+    "hd_sim_last_fb_residual": (C.c_double, [_VP]),
+    "hd_sim_penetration": (C.c_double, [_VP]),
     "hd_sim_external_force": (C.c_int, [_VP, _D, C.c_size_t]),
     "hd_sim_set_external_force": (C.c_int, [_VP, _D, C.c_size_t]),
     "hd_sim_create": (_VP, [_VP]),
@@ -240,6 +243,11 @@ class Scene:
         self.L.check(self.L.lib.hd_run_gradcheck(self.h, variables.encode() if variables is not None else None,
                                                  out_path.encode() if out_path else None, C.byref(p), C.byref(ok)))
         return json.loads(self.L._take_string(p)), bool(ok.value)
+
+    def elements(self):
+        out = np.zeros((self.element_count, 4), dtype=np.int32)
+        self.L.check(self.L.lib.hd_scene_elements(self.h, out.ctypes.data_as(C.POINTER(C.c_int)), out.size))
+        return out
 
     def young_moduli(self):
         out = np.zeros(self.element_count)

@@ -375,3 +375,25 @@ def test_gradcheck_matches_oracle(prod, orc, case):
         assert abs(rp["grad_norms"][k] - v) <= 1e-6 * max(abs(v), 1e-300), (k, rp["grad_norms"][k], v)
     for k, v in ro["fd_check"]["per_var_max_rel_err"].items():
         assert abs(rp["fd_check"]["per_var_max_rel_err"][k] - v) <= 1e-4, (k, rp["fd_check"], ro["fd_check"])
+
+
+@pytest.mark.parametrize("name", ["two-tet", "cantilever3", "ball-drop", "slab-on-sphere"])
+def test_simulate_matches_oracle(prod, orc, name, tmp_path):
+    """hd_run_simulate (drivers.cpp:238-365) on the device engine: the same
+    summary (iteration counts, refactorizations, penetration, displacement
+    ratio) and metrics as the oracle."""
+    out = {}
+    for tag, lib in (("prod", prod), ("oracle", orc)):
+        s = lib.builtin(name).run_simulate(str(tmp_path / tag))
+        m = np.loadtxt(tmp_path / tag / "metrics.csv", delimiter=",", skiprows=1, ndmin=2)
+        out[tag] = (s, m)
+    (sp, mp), (so, mo) = out["prod"], out["oracle"]
+    for k in ("frames", "iterations", "refactorizations", "all_converged"):
+        assert sp[k] == so[k], k
+    assert ("displacement_ratio" in sp) == ("displacement_ratio" in so)
+    if "displacement_ratio" in so:
+        assert abs(sp["displacement_ratio"] - so["displacement_ratio"]) <= 1e-6 * so["displacement_ratio"]
+    assert abs(sp["max_penetration"] - so["max_penetration"]) <= 1e-9
+    np.testing.assert_array_equal(mp[:, [0, 2, 3, 4]], mo[:, [0, 2, 3, 4]])
+    np.testing.assert_allclose(mp[:, 1], mo[:, 1], rtol=1e-5)
+    assert np.max(np.abs(mp[:, 5] - mo[:, 5])) <= 1e-8
