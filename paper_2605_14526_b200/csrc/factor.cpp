@@ -21,6 +21,8 @@
 //    evenly over persistent CTAs.
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <mutex>
 #include <exception>
 #include <chrono>
 #include <cmath>
@@ -656,54 +658,84 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
     }
   };
   {
-    // subtree tasks: split the costliest subtree (cost ~ sum of cnt^2) into
-    // its children until there are enough balanced tasks
+    // Dependency-driven schedule over the elimination tree (subtree cost
+    // proxy: sum of cnt^2; the scatter work of a column is actually spent by
+    // the rows above it, so the separator rows weigh more than this says):
+    // a subtree cheaper than `thresh` is one unit
+    // (its rows in order); every costlier node is a unit of its own, ready
+    // once all its children's units are done.  Sibling separators and their
+    // subtrees factor concurrently; only the chain above the first branching
+    // point stays serial.  A worker that completes a node's last child
+    // continues with that node directly.
     std::vector<double> cost(n);
+    std::vector<int> nkids(n, 0);
     for (int j = 0; j < n; ++j) cost[j] = 1.0 + static_cast<double>(cnt[j]) * cnt[j];
     for (int j = 0; j < n; ++j)
-      if (parent[j] >= 0) cost[parent[j]] += cost[j];
-    std::vector<std::vector<int>> kids(n);
-    std::vector<int> roots;
-    for (int j = 0; j < n; ++j) (parent[j] >= 0 ? kids[parent[j]] : roots).push_back(j);
-    const int T = hw_threads();
-    std::vector<int> tasks = roots;
-    std::vector<char> is_top(n, 0);
+      if (parent[j] >= 0) {
+        cost[parent[j]] += cost[j];
+        ++nkids[parent[j]];
+      }
     double total = 0;
-    for (int r : roots) total += cost[r];
-    for (;;) {
-      auto it = std::max_element(tasks.begin(), tasks.end(), [&](int a, int b) { return cost[a] < cost[b]; });
-      if (it == tasks.end() || static_cast<int>(tasks.size()) >= 8 * T || cost[*it] < total / (4.0 * T) ||
-          kids[*it].empty())
-        break;
-      const int r = *it;
-      tasks.erase(it);
-      is_top[r] = 1;
-      tasks.insert(tasks.end(), kids[r].begin(), kids[r].end());
+    for (int j = 0; j < n; ++j)
+      if (parent[j] < 0) total += cost[j];
+    const int T = hw_threads();
+    const double thresh = total / (16.0 * T);
+    std::vector<int> pending(n, 0), ready;
+    int units = 0;
+    for (int j = 0; j < n; ++j) {
+      if (cost[j] >= thresh) {
+        ++units;
+        pending[j] = nkids[j];
+        if (nkids[j] == 0) ready.push_back(j);
+      } else if (parent[j] < 0 || cost[parent[j]] >= thresh) {
+        ++units;
+        ready.push_back(j);
+      }
     }
-    std::sort(tasks.begin(), tasks.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-
-    std::vector<std::exception_ptr> err(T);
-    std::atomic<int> next{0};
-    std::vector<std::thread> pool;
-    const int workers = std::min<int>(T, static_cast<int>(tasks.size()));
-    for (int t = 0; t < workers; ++t)
-      pool.emplace_back([&, t] {
-        std::vector<int> pattern(n);
-        try {
-          for (int q; (q = next.fetch_add(1)) < static_cast<int>(tasks.size());) {
-            const int r = tasks[q];
-            up_rows(r - sz[r] + 1, r, pattern);
-          }
-        } catch (...) {
-          err[t] = std::current_exception();
+    std::sort(ready.begin(), ready.end(), [&](int x, int y) { return cost[x] < cost[y]; });  // costliest popped first
+    std::mutex mu;
+    std::condition_variable cv;
+    int done = 0;
+    bool abort = false;
+    std::exception_ptr err;
+    const auto worker = [&] {
+      std::vector<int> pattern(n);
+      int j = -1;
+      for (;;) {
+        if (j < 0) {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return abort || done == units || !ready.empty(); });
+          if (abort || ready.empty()) return;
+          j = ready.back();
+          ready.pop_back();
         }
-      });
+        try {
+          if (cost[j] < thresh) up_rows(j - sz[j] + 1, j, pattern);
+          else up_rows(j, j, pattern);
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(mu);
+          if (!err) err = std::current_exception();
+          abort = true;
+          cv.notify_all();
+          return;
+        }
+        const int p = parent[j];
+        std::lock_guard<std::mutex> lk(mu);
+        ++done;
+        j = -1;
+        if (p >= 0 && --pending[p] == 0) j = p;  // continue with the parent
+        if (done == units) cv.notify_all();
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(worker);
+    worker();
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      cv.notify_all();
+    }
     for (auto& th : pool) th.join();
-    for (auto& e : err)
-      if (e) std::rethrow_exception(e);
-    std::vector<int> pattern(n);
-    for (int k = 0; k < n; ++k)
-      if (is_top[k]) up_rows(k, k, pattern);
+    if (err) std::rethrow_exception(err);
   }
   lap(F.ms_phase[3]);  // LDL^T
   // 5. S' rows: column c of L^{-1} lives on c's ancestor path; every entry of
