@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/hdk.h"
 #include "launch.cuh"
@@ -477,6 +478,137 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<Pass1<W
   }
 }
 
+// Multi-column pass 1 with two columns per warp (R = 2 or 4): each staged
+// value is loaded from shared memory once per column pair, and the twelve
+// sums of a segment pair (2 segments x 2 columns x 3 axes) share one
+// reduce-scatter tree (18 shuffles instead of 30).  8 consumer warps, 1 CTA
+// per SM (~170 registers per thread), 6-stage ring.
+constexpr int kStagesC2 = 6;
+template <int R>
+__device__ __forceinline__ void rowdot_consume_c2(const hdk_factor& f, Ring<kStagesC2>& ring,
+                                                  const double* __restrict__ rhs, int c_beg, int c_end) {
+  constexpr int S = kStagesC2, W = kWarps, G = R / 2;
+  constexpr int WPC = W / G;  // consumer warps per column pair
+  static_assert(G * 2 == R && WPC * G == W, "column pairs must divide the consumer warps");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pair = warp / WPC, sub = warp % WPC;
+  const double* r0 = rhs + (size_t)(2 * pair) * 3 * (size_t)f.n;
+  const double* r1 = r0 + 3 * (size_t)f.n;
+  double* const pa = f.part1 + (size_t)(2 * pair) * 3 * (size_t)f.n_pslot;
+  double* const pb = pa + 3 * (size_t)f.n_pslot;
+  double b[2][3][kM];
+  int tile = -1;
+  for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
+    const int st = k % S;
+    mbar_wait(&ring.full[st], (k / S) & 1);
+    const ChunkInfo ch = ring.info[st];
+    if (ch.tile != tile) {
+      tile = ch.tile;
+#pragma unroll
+      for (int m = 0; m < kM; ++m) {
+        const int col = tile * kW + lane + 32 * m;
+        const bool ok = col < f.n;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          b[0][a][m] = ok ? __ldg(r0 + 3 * (size_t)col + a) : 0.0;
+          b[1][a][m] = ok ? __ldg(r1 + 3 * (size_t)col + a) : 0.0;
+        }
+      }
+    }
+    const double* vals = ring.vals[st];
+    const int npair = (ch.nseg + 1) >> 1;
+    bool released = false;
+    for (int pi = (sub - (ch.seg0 >> 1)) & (WPC - 1); pi < npair; pi += WPC) {
+      const int ia = 2 * pi, ib = ia + 1;
+      const bool hasb = ib < ch.nseg;
+      const hdk_seg sa = ring.segs[st][ia];
+      const hdk_seg sb = hasb ? ring.segs[st][ib] : sa;
+      const int la = sa.clo_len & 0xffff, ha = la + (sa.clo_len >> 16);
+      const int lb = sb.clo_len & 0xffff, hb = hasb ? lb + (sb.clo_len >> 16) : lb;
+      const double* va = vals + sa.coff - la;
+      const double* vb = vals + sb.coff - lb;
+      double wa[kM], wb[kM];
+#pragma unroll
+      for (int m = 0; m < kM; ++m) {
+        const int cl = lane + 32 * m;
+        wa[m] = (cl >= la && cl < ha) ? va[cl] : 0.0;
+        wb[m] = (cl >= lb && cl < hb) ? vb[cl] : 0.0;
+      }
+      if (pi + WPC >= npair) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ring.empty[st]);
+        released = true;
+      }
+      double acc[2][2][3];  // [segment][column][axis]
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) acc[0][q][a] = acc[1][q][a] = 0.0;
+#pragma unroll
+      for (int m = 0; m < kM; ++m)
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            acc[0][q][a] += wa[m] * b[q][a][m];
+            acc[1][q][a] += wb[m] * b[q][a][m];
+          }
+      // reduce-scatter: offset 16 splits the segments, offset 8 the columns,
+      // then a butterfly over the remaining 8 lanes
+      const bool lo = lane < 16, c0 = (lane & 8) == 0;
+      double kq[2][3];
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          kq[q][a] = (lo ? acc[0][q][a] : acc[1][q][a]) +
+                     __shfl_xor_sync(0xffffffffu, lo ? acc[1][q][a] : acc[0][q][a], 16);
+      double h[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        h[a] = (c0 ? kq[0][a] : kq[1][a]) + __shfl_xor_sync(0xffffffffu, c0 ? kq[1][a] : kq[0][a], 8);
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) h[a] += __shfl_xor_sync(0xffffffffu, h[a], o);
+      if ((lane & 7) == 0 && (lo || hasb)) {
+        double* p = (c0 ? pa : pb) + 3 * (size_t)(lo ? sa.pslot : sb.pslot);
+        p[0] = h[0];
+        p[1] = h[1];
+        p[2] = h[2];
+      }
+    }
+    if (!released) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ring.empty[st]);
+    }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kThreads, 1) k_rowdot_c2(hdk_factor f, const double* __restrict__ rhs) {
+  hdk::pdl_trigger();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Ring<kStagesC2>& ring = *reinterpret_cast<Ring<kStagesC2>*>(smem_raw);
+  const int warp = threadIdx.x >> 5;
+  unsigned long long* trace = HDK_TRACE_PTR;
+  if (trace && threadIdx.x == 0) trace[2 * blockIdx.x] = globaltimer();
+  ring_init(ring, kWarps);
+  const int c_beg = f.first1 ? f.first1[blockIdx.x] : range_first(blockIdx.x, gridDim.x, f.n_chunks);
+  const int c_end = f.first1 ? f.first1[blockIdx.x + 1] : range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
+  if (warp == kWarps) {
+    produce(f, ring, c_beg, c_end, false);
+    return;
+  }
+  HDK_TRACED_WAIT(hdk::kTrRowdot);
+  if (f.run_flag && *f.run_flag == 0) return;
+  rowdot_consume_c2<R>(f, ring, rhs, c_beg, c_end);
+  if (trace) {
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kWarps) : "memory");
+    if (threadIdx.x == 0) trace[2 * blockIdx.x + 1] = globaltimer();
+  }
+}
+
 // z-fold: one warp per task.  (Folding z in the row-dot kernel's epilogue
 // behind a grid barrier measured 1-2 us slower than this separate launch.)
 __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
@@ -652,6 +784,9 @@ const Grids& grids() {
     const int s16 = static_cast<int>(sizeof(Ring<Pass1<16>::stages>));
     cudaFuncSetAttribute(k_rowdot<false, 2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, s16);
     cudaFuncSetAttribute(k_rowdot<false, 4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, s16);
+    const int sc2 = static_cast<int>(sizeof(Ring<kStagesC2>));
+    cudaFuncSetAttribute(k_rowdot_c2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc2);
+    cudaFuncSetAttribute(k_rowdot_c2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc2);
     cudaFuncSetAttribute(k_coltile<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(Pass2Smem<2>)));
     cudaFuncSetAttribute(k_coltile<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -686,7 +821,12 @@ int launch_multi(const hdk_factor* f, const double* rhs, cudaStream_t st) {
   // on pass 2's grid and chunk ranges
   hdk_factor f1 = *f;
   f1.first1 = f->first2;
-  hdk::launch(k_rowdot<false, R, 16>, dim3(g2), dim3(Pass1<16>::threads), sizeof(Ring<Pass1<16>::stages>), st, f1, rhs);
+  static const bool c2 = [] {
+    const char* e = std::getenv("HETERODYN_ROWDOT_C2");  // "0": one column per warp (A/B)
+    return !(e && e[0] == '0');
+  }();
+  if (c2) hdk::launch(k_rowdot_c2<R>, dim3(g2), dim3(kThreads), sizeof(Ring<kStagesC2>), st, f1, rhs);
+  else hdk::launch(k_rowdot<false, R, 16>, dim3(g2), dim3(Pass1<16>::threads), sizeof(Ring<Pass1<16>::stages>), st, f1, rhs);
   hdk::launch(k_zreduce, dim3((f->n_ztask + 7) / 8, R), dim3(256), 0, st, *f);
   hdk::launch(k_coltile<false, R>, dim3(g2), dim3(kThreads2), sizeof(Pass2Smem<R>), st, *f);
   return static_cast<int>(cudaGetLastError());
