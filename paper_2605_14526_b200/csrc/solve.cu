@@ -747,6 +747,128 @@ __global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
   }
 }
 
+// Multi-column pass 2 with two columns per warp (R = 2 or 4): each staged
+// value is loaded once per column pair and feeds six accumulator rows; the
+// 8 / (R / 2) warps of a pair fold each column in turn through the same
+// shared buffer as fold_and_write.
+template <int WPC>
+__device__ __forceinline__ void fold_write_col(const hdk_factor& f, double (*fold)[3][kW], int slot, int col,
+                                               int pair, int sub, double (&x0)[kM], double (&x1)[kM],
+                                               double (&x2)[kM]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int half = WPC / 2; half >= 1; half >>= 1) {
+    consumers_sync();
+    if (sub >= half && sub < 2 * half) {
+      const int fb = pair * (WPC / 2) + sub - half;
+#pragma unroll
+      for (int m = 0; m < kM; ++m) {
+        const int cl = lane + 32 * m;
+        fold[fb][0][cl] = x0[m];
+        fold[fb][1][cl] = x1[m];
+        fold[fb][2][cl] = x2[m];
+      }
+    }
+    consumers_sync();
+    if (sub < half) {
+      const int fb = pair * (WPC / 2) + sub;
+#pragma unroll
+      for (int m = 0; m < kM; ++m) {
+        const int cl = lane + 32 * m;
+        x0[m] += fold[fb][0][cl];
+        x1[m] += fold[fb][1][cl];
+        x2[m] += fold[fb][2][cl];
+      }
+    }
+  }
+  if (sub == 0) {
+    double* const part2 = f.part2 + (size_t)col * part2_stride(f);
+#pragma unroll
+    for (int m = 0; m < kM; ++m) {
+      double* p = part2 + 3 * ((size_t)slot * kW + lane + 32 * m);
+      p[0] = x0[m];
+      p[1] = x1[m];
+      p[2] = x2[m];
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
+}
+
+template <int R>
+__global__ void __launch_bounds__(kThreads2, 1) k_coltile_c2(hdk_factor f) {
+  constexpr int S = Stages2<R>::value, G = R / 2, WPC = kWarps / G;
+  static_assert(G * 2 == R && WPC * G == kWarps && WPC / 2 * G <= kWarps / 2, "column pairs");
+  hdk::pdl_trigger();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Pass2Smem<R>& sm = *reinterpret_cast<Pass2Smem<R>*>(smem_raw);
+  Ring2<S, R>& ring = sm.ring;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long* trace = HDK_TRACE_PTR;
+  if (trace && threadIdx.x == 0) trace[2 * blockIdx.x] = globaltimer();
+  ring2_init(ring);
+  const int c_beg = f.first2 ? f.first2[blockIdx.x] : range_first(blockIdx.x, gridDim.x, f.n_chunks);
+  const int c_end = f.first2 ? f.first2[blockIdx.x + 1] : range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
+  if (warp == kWarps) {
+    stream2(f, ring, c_beg, c_end);
+    return;
+  }
+  HDK_TRACED_WAIT(hdk::kTrColtile);
+  if (f.run_flag && *f.run_flag == 0) return;
+  if (warp == kWarps + 1) {
+    gather_z(f, ring, c_end - c_beg);
+    return;
+  }
+  const int pair = warp / WPC, sub = warp % WPC;
+  double x0[kM], x1[kM], x2[kM], y0[kM], y1[kM], y2[kM];
+#pragma unroll
+  for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = y0[m] = y1[m] = y2[m] = 0.0;
+  const auto flush = [&](int slot) {
+    fold_write_col<WPC>(f, sm.fold, slot, 2 * pair, pair, sub, x0, x1, x2);
+    fold_write_col<WPC>(f, sm.fold, slot, 2 * pair + 1, pair, sub, y0, y1, y2);
+  };
+  int tile = -1;
+  for (int k = 0; k < c_end - c_beg; ++k) {
+    const int st = k % S;
+    mbar_wait(&ring.zfull[st], (k / S) & 1);
+    const ChunkInfo ch = ring.info[st];
+    if (ch.tile != tile) {
+      if (tile >= 0) flush(tile + blockIdx.x);
+      tile = ch.tile;
+    }
+    const double* vals = ring.vals[st];
+    const int i0 = (sub - ch.seg0) & (WPC - 1);
+    const int zc = 6 * pair;
+    for (int i = i0; i < ch.nseg; i += WPC) {
+      const hdk_seg sg = ring.segs[st][i];
+      const int lo = sg.clo_len & 0xffff, hi = lo + (sg.clo_len >> 16);
+      const double* v = vals + sg.coff - lo;
+      const double* z = ring.zs[st][i] + zc;
+      const double z0 = z[0], z1 = z[1], z2 = z[2], z3 = z[3], z4 = z[4], z5 = z[5];
+#pragma unroll
+      for (int m = 0; m < kM; ++m) {
+        const int cl = lane + 32 * m;
+        if (cl >= lo && cl < hi) {
+          const double w = v[cl];
+          x0[m] += w * z0;
+          x1[m] += w * z1;
+          x2[m] += w * z2;
+          y0[m] += w * z3;
+          y1[m] += w * z4;
+          y2[m] += w * z5;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[st]);
+  }
+  if (tile >= 0) flush(tile + blockIdx.x);
+  if (trace) {
+    consumers_sync();
+    if (threadIdx.x == 0) trace[2 * blockIdx.x + 1] = globaltimer();
+  }
+}
+
 // x_c = sum of the tile partials of the CTAs whose chunk ranges touch the
 // column's tile (CTA order), scattered to the full vector.
 template <bool kScatter>
@@ -791,6 +913,10 @@ const Grids& grids() {
                          static_cast<int>(sizeof(Pass2Smem<2>)));
     cudaFuncSetAttribute(k_coltile<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(Pass2Smem<4>)));
+    cudaFuncSetAttribute(k_coltile_c2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(Pass2Smem<2>)));
+    cudaFuncSetAttribute(k_coltile_c2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(Pass2Smem<4>)));
     int dev = 0, sms = 148, b1 = 1, b2 = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -828,7 +954,12 @@ int launch_multi(const hdk_factor* f, const double* rhs, cudaStream_t st) {
   if (c2) hdk::launch(k_rowdot_c2<R>, dim3(g2), dim3(kThreads), sizeof(Ring<kStagesC2>), st, f1, rhs);
   else hdk::launch(k_rowdot<false, R, 16>, dim3(g2), dim3(Pass1<16>::threads), sizeof(Ring<Pass1<16>::stages>), st, f1, rhs);
   hdk::launch(k_zreduce, dim3((f->n_ztask + 7) / 8, R), dim3(256), 0, st, *f);
-  hdk::launch(k_coltile<false, R>, dim3(g2), dim3(kThreads2), sizeof(Pass2Smem<R>), st, *f);
+  static const bool t2 = [] {
+    const char* e = std::getenv("HETERODYN_COLTILE_C2");  // "0": one column per warp (A/B)
+    return !(e && e[0] == '0');
+  }();
+  if (t2) hdk::launch(k_coltile_c2<R>, dim3(g2), dim3(kThreads2), sizeof(Pass2Smem<R>), st, *f);
+  else hdk::launch(k_coltile<false, R>, dim3(g2), dim3(kThreads2), sizeof(Pass2Smem<R>), st, *f);
   return static_cast<int>(cudaGetLastError());
 }
 
