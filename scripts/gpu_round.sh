@@ -15,4 +15,5 @@ HETERODYN_PHASES=1 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-ba
 HETERODYN_NO_COND_GRAPH=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
 HETERODYN_NO_COND_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_rowdot|k_zreduce|k_coltile|k_bb_dots|k_bb_mix|k_bapply|k_gather_pp" -s 200 -c 7 -o gpurun_out/backbone_prof python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 HETERODYN_NO_COND_GRAPH=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_local|k_differential|k_energy" -s 3 -c 3 -o gpurun_out/local_prof python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_local.log 2>&1
+HETERODYN_NO_COND_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:c2<\(int\)4" -s 4 -c 2 -o gpurun_out/c4_columns python bench.py --config C4 --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_c4.log 2>&1
 ls -la gpurun_out
