@@ -124,8 +124,8 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    p = os.path.join(HERE, "profiles", "solve_traffic.json")
+def ncu_traffic(name="solve_traffic.json"):
+    p = os.path.join(HERE, "profiles", name)
     try:
         with open(p) as f:
             return json.load(f).get("traffic_bytes_per_solve")
@@ -399,7 +399,9 @@ def run_batch(args, world, rank):
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 3 * nv * 8,
                     "d2h_bytes_per_step": (len(mine) + ne) * 8 + (1 + ne) * 8},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None,
+                         "traffic": ncu_traffic("solve_traffic_c5.json"),
+                         "traffic_scope": "DRAM bytes of one sample's solve (ncu capture, profiles/solve_traffic_c5.json)"
+                                          " vs bytes_per_launch",
                          "kernel": "hdk_apply_inverse3 over all sample factors (aggregate bytes of the timed "
                                    "region's solves / step time, rank 0)",
                          "solves_per_step": solves / args.steps, "bytes_per_launch": b.solve_bytes,
