@@ -386,6 +386,27 @@ HDK_API int hdk_contact_column_init(const hdk_contacts* c, int row, int nv, cons
 HDK_API int hdk_contact_friction_pushback(const hdk_contacts* c, const double* omega, const double* y, double* dl_dq,
                                           void* stream);
 
+/* Contact-adjoint columns (engine_columns.cpp): the per-column backbone
+ * buffers of HDK_BB_COLUMNS columns, so each backbone stage is one launch
+ * for all columns (blockIdx.y / blockIdx.x = column). */
+#define HDK_BB_COLUMNS 4
+typedef struct hdk_bb_column {
+  hdk_factor f;  /* the column's view of the multi-column factor (part2 offset) */
+  hdk_ctl* ctl;
+  hdk_ctl* snap;
+  void* res;
+  double *t, *tv, *xp, *x, *lastq, *lastg, *dq, *dg, *part, *rt, *rx, *lrx, *lrg, *rsq, *ef, *rhs;
+  const double* seedp;
+} hdk_bb_column;
+typedef struct hdk_bb_columns {
+  hdk_bb_column col[HDK_BB_COLUMNS];
+} hdk_bb_columns;
+HDK_API int hdk_bb_columns_dots(const hdk_bb_columns* c, int mode, void* stream);
+HDK_API int hdk_bb_columns_solve(const hdk_bb_columns* c, void* stream);
+HDK_API int hdk_bb_columns_bapply(const hdk_mesh* m, const double* dcomp, const hdk_bb_columns* c, void* stream);
+HDK_API int hdk_bb_columns_gather(const hdk_vtx* x, const hdk_bb_columns* c, void* stream);
+HDK_API int hdk_bb_columns_mix(const hdk_bb_columns* c, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace hdb {
@@ -37,6 +38,7 @@ struct Engine::ColumnSet {
   int* any = nullptr;         // OR of the columns' cond
   int* h_any = nullptr;
   LoopGraph graph;
+  hdk_bb_columns bb{};  // every column's backbone buffers, for the one-launch-per-stage body
   ~ColumnSet() {
     graph.destroy();
     for (Col& c : col) {
@@ -92,6 +94,32 @@ void Engine::build_columns() {
     for (cudaEvent_t* e : {&C.fork, &C.mid, &C.join, &C.end})
       cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
   }
+  static_assert(kColumns == HDK_BB_COLUMNS, "column batch width");
+  for (int c = 0; c < kColumns; ++c) {
+    const ColumnSet::Col& C = S.col[c];
+    hdk_bb_column& k = S.bb.col[c];
+    k.f = C.f;
+    k.ctl = C.ctl;
+    k.snap = C.snap;
+    k.res = C.res;
+    k.t = C.t;
+    k.tv = C.tv;
+    k.xp = C.xp;
+    k.x = C.x;
+    k.lastq = C.lastq;
+    k.lastg = C.lastg;
+    k.dq = C.dq;
+    k.dg = C.dg;
+    k.part = C.part;
+    k.rt = C.rt;
+    k.rx = C.rx;
+    k.lrx = C.lrx;
+    k.lrg = C.lrg;
+    k.rsq = C.rsq;
+    k.ef = C.ef;
+    k.rhs = S.rhs + c * 3 * static_cast<size_t>(hf_.n);
+    k.seedp = C.seedp;
+  }
   void* s = st_;
   // first right-hand sides seed + R(x0) of every column
   auto pre = [&] {
@@ -120,7 +148,25 @@ void Engine::columns_body(unsigned long long handle, unsigned skip) {
   {
     {
       if (!(skip & 1u)) hdk_ok(hdk_apply_inverse3_multi(&S.f, S.rhs, kColumns, s), "multi-column solve");
-      for (int c = 0; c < kColumns && !(skip & 2u); ++c) {
+      static const bool batched = [] {
+        const char* e = std::getenv("HETERODYN_COLVEC");  // "0": one stream pair per column (A/B)
+        return !(e && e[0] == '0');
+      }();
+      if (batched && !(skip & 2u)) {
+        // one launch per backbone stage for all columns; the coefficient
+        // solves run on a second branch beside B t and its gather
+        ColumnSet::Col& C0 = S.col[0];
+        hdk_ok(hdk_bb_columns_dots(&S.bb, 1, s), "dots (columns)");
+        cuda_check(cudaEventRecord(C0.mid, st_), "mid");
+        cuda_check(cudaStreamWaitEvent(C0.s2, C0.mid, 0), "mid wait");
+        hdk_ok(hdk_bb_columns_solve(&S.bb, C0.s2), "coefficients (columns)");
+        cuda_check(cudaEventRecord(C0.join, C0.s2), "join");
+        hdk_ok(hdk_bb_columns_bapply(&dm_, dcomp_, &S.bb, s), "B t (columns)");
+        hdk_ok(hdk_bb_columns_gather(&dv_, &S.bb, s), "R(t) (columns)");
+        cuda_check(cudaStreamWaitEvent(st_, C0.join, 0), "join wait");
+        hdk_ok(hdk_bb_columns_mix(&S.bb, s), "mix (columns)");
+      }
+      for (int c = 0; c < kColumns && !(skip & 2u) && !batched; ++c) {
         ColumnSet::Col& C = S.col[c];
         cuda_check(cudaEventRecord(C.fork, st_), "fork");
         cuda_check(cudaStreamWaitEvent(C.s1, C.fork, 0), "fork wait");

@@ -330,10 +330,9 @@ __global__ void __launch_bounds__(128) k_differential(hdk_mesh m, hdk_material m
 // template for A/B runs (HETERODYN_BAPPLY): the unbounded 128-thread form
 // (118 registers, more loads in flight per thread) measured faster at C3
 // than register-capped single-wave shapes (10.0 vs 12.3 us per apply).
-template <int T, int MINB>
-__global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __restrict__ dcomp, const double* __restrict__ x,
-                                                 double* __restrict__ ef, const int* run_flag,
-                                                 const int* __restrict__ corner_pos) {
+__device__ __forceinline__ void bapply_body(const hdk_mesh& m, const double* __restrict__ dcomp,
+                                            const double* __restrict__ x, double* __restrict__ ef, const int* run_flag,
+                                            const int* __restrict__ corner_pos) {
   // The element's geometry and differential do not depend on the previous
   // kernel (only x does): load them before the PDL wait, so they arrive
   // while that kernel drains.
@@ -372,6 +371,19 @@ __global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __
   const M3 pm = mul_nt(mul(u, o), v);
   if (corner_pos) write_force_sorted(g, pm, ef, corner_pos, e);
   else write_force(g, pm, ef, e);
+}
+
+template <int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __restrict__ dcomp, const double* __restrict__ x,
+                                                 double* __restrict__ ef, const int* run_flag,
+                                                 const int* __restrict__ corner_pos) {
+  bapply_body(m, dcomp, x, ef, run_flag, corner_pos);
+}
+
+// B t of the contact-adjoint columns, blockIdx.y = column.
+__global__ void __launch_bounds__(128) k_bapply_bbcols(hdk_mesh m, const double* __restrict__ dcomp, hdk_bb_columns c) {
+  const hdk_bb_column& k = c.col[blockIdx.y];
+  bapply_body(m, dcomp, k.tv, k.ef, &k.snap->cond, nullptr);
 }
 
 // Per-element gradient routing (backward.cpp:361-391) and the damping
@@ -491,6 +503,12 @@ HDK_API int hdk_bapply_sorted(const hdk_mesh* m, const double* dcomp, const doub
     hdk::launch(k_bapply<128, 6>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, elem_force, run_flag, corner_pos);
   else
     hdk::launch(k_bapply<64, 11>, dim3(blocks(m->ne, 64)), dim3(64), 0, st, *m, dcomp, x, elem_force, run_flag, corner_pos);
+  return static_cast<int>(cudaGetLastError());
+}
+
+HDK_API int hdk_bb_columns_bapply(const hdk_mesh* m, const double* dcomp, const hdk_bb_columns* c, void* stream) {
+  hdk::launch(k_bapply_bbcols, dim3(blocks(m->ne, 128), HDK_BB_COLUMNS), dim3(128), 0,
+              static_cast<cudaStream_t>(stream), *m, dcomp, *c);
   return static_cast<int>(cudaGetLastError());
 }
 

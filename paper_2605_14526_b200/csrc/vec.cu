@@ -201,7 +201,7 @@ __global__ void k_gather_perm(hdk_vtx x, const double* __restrict__ base, const 
 // split and fold, so bitwise the same sums.
 // sorted != 0: ef holds the forces already in incidence order (hdk_bapply_sorted),
 // so the range is read directly.
-__global__ void k_gather_pp(hdk_vtx x, const double* __restrict__ basep, const double* __restrict__ ef,
+__device__ __forceinline__ void gather_pp_body(hdk_vtx x, const double* __restrict__ basep, const double* __restrict__ ef,
                             double* __restrict__ rhs, const int* run_flag, int sorted) {
   HDK_TRACED_WAIT(hdk::kTrGather);
   hdk::pdl_trigger();
@@ -231,6 +231,10 @@ __global__ void k_gather_pp(hdk_vtx x, const double* __restrict__ basep, const d
     rhs[3 * (size_t)p + 1] = (basep ? basep[3 * (size_t)p + 1] : 0.0) + s1;
     rhs[3 * (size_t)p + 2] = (basep ? basep[3 * (size_t)p + 2] : 0.0) + s2;
   }
+}
+__global__ void k_gather_pp(hdk_vtx x, const double* __restrict__ basep, const double* __restrict__ ef,
+                            double* __restrict__ rhs, const int* run_flag, int sorted) {
+  gather_pp_body(x, basep, ef, rhs, run_flag, sorted);
 }
 
 __global__ void k_fixed_coupling(hdk_csr c, const int* fixed, const double* q, double* out) {
@@ -729,7 +733,7 @@ __global__ void k_any_cond(const hdk_ctl* ctls, int count, int* any, cudaGraphCo
 // and every Anderson access is coalesced with no vertex indirection.  Fixed
 // vertices carry t = x = 0 in the backbone (they contribute nothing to any
 // dot product), so dropping them changes no value, only the summation order.
-__global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ctl, hdk_ctl* snap, double* __restrict__ tp,
+__device__ __forceinline__ void bb_dots_body(int n, hdk_factor f, hdk_ctl* ctl, hdk_ctl* snap, double* __restrict__ tp,
                                                 double* __restrict__ tv, const double* __restrict__ xp, double* last_q,
                                                 double* last_g, double* dq, double* dg, double* partial, int mode) {
   HDK_TRACED_WAIT(hdk::kTrDots);
@@ -777,6 +781,11 @@ __global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ct
   block_partials_18(acc, partial);
   hdk::trace_stamp(g_hdk_trace, hdk::kTrDotsB);
 }
+__global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ctl, hdk_ctl* snap, double* __restrict__ tp,
+                                                double* __restrict__ tv, const double* __restrict__ xp, double* last_q,
+                                                double* last_g, double* dq, double* dg, double* partial, int mode) {
+  bb_dots_body(n, f, ctl, snap, tp, tv, xp, last_q, last_g, dq, dg, partial, mode);
+}
 
 // x <- t - sum_j gamma_j (dq_j + dg_j) in elimination order, also scattered to
 // the full vertex vector the element kernels read.
@@ -784,7 +793,7 @@ __global__ void __launch_bounds__(kT) k_bb_dots(int n, hdk_factor f, hdk_ctl* ct
 // block): runs while B t and its gather proceed on the main branch, reads
 // the snapshot k_bb_dots took, publishes the new state and the WHILE
 // condition to ctl and the mixing inputs to *res.
-__global__ void __launch_bounds__(kT) k_bb_solve(hdk_ctl* ctl, const hdk_ctl* snap, const double* partial,
+__device__ __forceinline__ void bb_solve_body(hdk_ctl* ctl, const hdk_ctl* snap, const double* partial,
                                                  AaResult* out, cudaGraphConditionalHandle handle, int use_handle) {
   HDK_TRACED_WAIT(hdk::kTrTail0);
   hdk::pdl_trigger();
@@ -796,6 +805,10 @@ __global__ void __launch_bounds__(kT) k_bb_solve(hdk_ctl* ctl, const hdk_ctl* sn
   int* dst = reinterpret_cast<int*>(out);
   for (int w = threadIdx.x; w < static_cast<int>(sizeof(AaResult) / 4); w += kT) dst[w] = src[w];
 }
+__global__ void __launch_bounds__(kT) k_bb_solve(hdk_ctl* ctl, const hdk_ctl* snap, const double* partial,
+                                                 AaResult* out, cudaGraphConditionalHandle handle, int use_handle) {
+  bb_solve_body(ctl, snap, partial, out, handle, use_handle);
+}
 
 // Anderson mix of the backbone, in elimination order, carried in two spaces:
 //   x_{k+1} = t_k - sum_j gamma_j (dq_j + dg_j)                 (backward.cpp:188-199)
@@ -805,7 +818,7 @@ __global__ void __launch_bounds__(kT) k_bb_solve(hdk_ctl* ctl, const hdk_ctl* sn
 // solve).  The rings hold the sums s_j = dq_j + dg_j (k_bb_dots) and their
 // R-images (pushed here from the tracked R(x_k) and R(t_k), same slots); a
 // history reset restarts the R side from R(t_k) exactly.
-__global__ void __launch_bounds__(kT) k_bb_mix(int n, const int* __restrict__ p2v, hdk_ctl* ctl, const hdk_ctl* snap,
+__device__ __forceinline__ void bb_mix_body(int n, const int* __restrict__ p2v, hdk_ctl* ctl, const hdk_ctl* snap,
                                                const AaResult* __restrict__ res, const double* __restrict__ tp,
                                                double* xp, double* __restrict__ xv, const double* __restrict__ sq,
                                                const double* __restrict__ rt, double* rx, double* last_rx,
@@ -862,6 +875,14 @@ __global__ void __launch_bounds__(kT) k_bb_mix(int n, const int* __restrict__ p2
   const int col = static_cast<int>(i / 3);
   xv[3 * (size_t)__ldg(p2v + col) + (i - 3 * (size_t)col)] = out;
   if (!isfinite(out) || !isfinite(rout)) atomicOr(&ctl->nonfinite, 1);
+}
+__global__ void __launch_bounds__(kT) k_bb_mix(int n, const int* __restrict__ p2v, hdk_ctl* ctl, const hdk_ctl* snap,
+                                               const AaResult* __restrict__ res, const double* __restrict__ tp,
+                                               double* xp, double* __restrict__ xv, const double* __restrict__ sq,
+                                               const double* __restrict__ rt, double* rx, double* last_rx,
+                                               double* last_rg, double* rsq, const double* __restrict__ seedp,
+                                               double* __restrict__ rhs) {
+  bb_mix_body(n, p2v, ctl, snap, res, tp, xp, xv, sq, rt, rx, last_rx, last_rg, rsq, seedp, rhs);
 }
 
 __global__ void __launch_bounds__(kT) k_aa_mix(hdk_vtx x, hdk_ctl* ctl, const double* __restrict__ qhat, double* qcur,
@@ -1118,6 +1139,29 @@ inline int last() { return static_cast<int>(cudaGetLastError()); }
 
 }  // namespace
 
+
+// ---- contact-adjoint columns, one launch per stage for all columns ---------
+// blockIdx.y selects the column (hdk_bb_columns); the bodies are the
+// single-column kernels', so every column computes exactly what its own
+// launch would.
+__global__ void __launch_bounds__(kT) k_bb_dots_cols(int n, hdk_bb_columns c, int mode) {
+  const hdk_bb_column& k = c.col[blockIdx.y];
+  bb_dots_body(n, k.f, k.ctl, k.snap, k.t, k.tv, k.xp, k.lastq, k.lastg, k.dq, k.dg, k.part, mode);
+}
+__global__ void __launch_bounds__(kT) k_bb_solve_cols(hdk_bb_columns c) {
+  const hdk_bb_column& k = c.col[blockIdx.x];
+  bb_solve_body(k.ctl, k.snap, k.part, static_cast<AaResult*>(k.res), 0ULL, 0);
+}
+__global__ void k_gather_pp_cols(hdk_vtx x, hdk_bb_columns c) {
+  const hdk_bb_column& k = c.col[blockIdx.y];
+  gather_pp_body(x, nullptr, k.ef, k.rt, &k.snap->cond, 0);
+}
+__global__ void __launch_bounds__(kT) k_bb_mix_cols(int n, const int* __restrict__ p2v, hdk_bb_columns c) {
+  const hdk_bb_column& k = c.col[blockIdx.y];
+  bb_mix_body(n, p2v, k.ctl, k.snap, static_cast<const AaResult*>(k.res), k.t, k.xp, k.x, k.dq, k.rt, k.rx, k.lrx,
+              k.lrg, k.rsq, k.seedp, k.rhs);
+}
+
 extern "C" {
 
 HDK_API int hdk_free_fall(const hdk_vtx* x, const double* q, const double* v, const double* f_ext, double h,
@@ -1300,4 +1344,27 @@ HDK_API int hdk_commit(int n, const hdk_ctl* ctl, const double* q_star, double h
   return last();
 }
 
+
+HDK_API int hdk_bb_columns_dots(const hdk_bb_columns* c, int mode, void* stream) {
+  const hdk_factor* f = &c->col[0].f;
+  int g1 = 0, g2 = 0;
+  hdk_solve_grids(f, &g1, &g2);
+  if (!f->tile_cta2 || g2 != f->grid2) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_bb_dots_cols, dim3(HDK_RED_BLOCKS, HDK_BB_COLUMNS), dim3(kT), 0, S(stream), f->n, *c, mode);
+  return last();
+}
+HDK_API int hdk_bb_columns_solve(const hdk_bb_columns* c, void* stream) {
+  hdk::launch(k_bb_solve_cols, dim3(HDK_BB_COLUMNS), dim3(kT), 0, S(stream), *c);
+  return last();
+}
+HDK_API int hdk_bb_columns_gather(const hdk_vtx* x, const hdk_bb_columns* c, void* stream) {
+  if (!x->pinc_off || !x->pinc) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_gather_pp_cols, dim3(nb(8LL * x->n), HDK_BB_COLUMNS), dim3(256), 0, S(stream), *x, *c);
+  return last();
+}
+HDK_API int hdk_bb_columns_mix(const hdk_bb_columns* c, void* stream) {
+  const hdk_factor* f = &c->col[0].f;
+  hdk::launch(k_bb_mix_cols, dim3(nb(3LL * f->n), HDK_BB_COLUMNS), dim3(kT), 0, S(stream), f->n, f->p2v, *c);
+  return last();
+}
 }  // extern "C"
