@@ -892,13 +892,11 @@ double rigid_fit_residual(const std::vector<int>& verts, const V& rest, const V&
       w[i][k] = vm[i][ord[k]];
     }
   const double tiny = 1e-12 * std::max(sig[ord[0]], 1e-300);
-  if (sig[ord[1]] <= tiny) {  // rank <= 1: complete U from the first column
-    const double* u0 = nullptr;
-    double c0[3] = {u[0][0], u[1][0], u[2][0]};
-    if (sig[ord[0]] <= 0) c0[0] = 1, c0[1] = 0, c0[2] = 0;
-    u0 = c0;
+  if (sig[ord[1]] <= tiny) {  // rank <= 1: complete U from its first column (or e_x)
+    double u0[3] = {u[0][0], u[1][0], u[2][0]};
+    if (sig[ord[0]] <= 0) u0[0] = 1, u0[1] = 0, u0[2] = 0;
     const double e[3] = {std::abs(u0[0]) < 0.9 ? 1.0 : 0.0, std::abs(u0[0]) < 0.9 ? 0.0 : 1.0, 0.0};
-    double c1[3] = {u0[1] * e[2] - u0[2] * e[1], u0[2] * e[0] - u0[0] * e[2], u0[0] * e[1] - u0[1] * e[0]};
+    const double c1[3] = {u0[1] * e[2] - u0[2] * e[1], u0[2] * e[0] - u0[0] * e[2], u0[0] * e[1] - u0[1] * e[0]};
     const double nn = std::sqrt(c1[0] * c1[0] + c1[1] * c1[1] + c1[2] * c1[2]);
     for (int i = 0; i < 3; ++i) {
       u[i][0] = u0[i];
