@@ -160,6 +160,18 @@ def test_deterministic_reruns(prod):
         assert np.array_equal(a[1][k], b[1][k])
 
 
+def test_deterministic_contact_reruns(prod):
+    """The contact adjoint (multi-column passes, batched column stages) gives
+    bit-identical q, v and gradients on a rerun."""
+    scene, frames = CONTACT_CASES["C4-reduced"]
+    a = run(prod, scene, frames)
+    b = run(prod, scene, frames)
+    for (qa, va, _, _), (qb, vb, _, _) in zip(a[0], b[0]):
+        assert np.array_equal(qa, qb) and np.array_equal(va, vb)
+    for k in GRADS:
+        assert np.array_equal(a[1][k], b[1][k]), k
+
+
 def test_pinned_bitwise_and_cap(prod):
     """test_forward.cpp:334-378 on the device path."""
     s = scenes.block_scene(fix_x0_face=True, v0_amp=0.0, gravity_z=-2.0, eps_rel=1e-6, eps_abs=1e-10)
