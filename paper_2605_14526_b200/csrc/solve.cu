@@ -823,17 +823,16 @@ __global__ void __launch_bounds__(kThreads2, 1) k_coltile_c2(hdk_factor f) {
   double x0[kM], x1[kM], x2[kM], y0[kM], y1[kM], y2[kM];
 #pragma unroll
   for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = y0[m] = y1[m] = y2[m] = 0.0;
-  const auto flush = [&](int slot) {
-    fold_write_col<WPC>(f, sm.fold, slot, 2 * pair, pair, sub, x0, x1, x2);
-    fold_write_col<WPC>(f, sm.fold, slot, 2 * pair + 1, pair, sub, y0, y1, y2);
-  };
   int tile = -1;
   for (int k = 0; k < c_end - c_beg; ++k) {
     const int st = k % S;
     mbar_wait(&ring.zfull[st], (k / S) & 1);
     const ChunkInfo ch = ring.info[st];
     if (ch.tile != tile) {
-      if (tile >= 0) flush(tile + blockIdx.x);
+      if (tile >= 0) {
+        fold_write_col<WPC>(f, sm.fold, tile + blockIdx.x, 2 * pair, pair, sub, x0, x1, x2);
+        fold_write_col<WPC>(f, sm.fold, tile + blockIdx.x, 2 * pair + 1, pair, sub, y0, y1, y2);
+      }
       tile = ch.tile;
     }
     const double* vals = ring.vals[st];
@@ -862,7 +861,10 @@ __global__ void __launch_bounds__(kThreads2, 1) k_coltile_c2(hdk_factor f) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[st]);
   }
-  if (tile >= 0) flush(tile + blockIdx.x);
+  if (tile >= 0) {
+    fold_write_col<WPC>(f, sm.fold, tile + blockIdx.x, 2 * pair, pair, sub, x0, x1, x2);
+    fold_write_col<WPC>(f, sm.fold, tile + blockIdx.x, 2 * pair + 1, pair, sub, y0, y1, y2);
+  }
   if (trace) {
     consumers_sync();
     if (threadIdx.x == 0) trace[2 * blockIdx.x + 1] = globaltimer();
