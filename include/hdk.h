@@ -337,54 +337,131 @@ HDK_API int hdk_axpby(int n, double a, const double* x, double b, const double* 
 HDK_API int hdk_velocity(int n, const double* q_star, const double* q_t, double h, double* v_star, void* stream);
 
 /* ---- contact (contact.cu) ------------------------------------------------ */
-/* Device view of one step's contact set in the reference's stacked row order:
- * nc normal rows, then two tangent rows per frictional contact (contact.hpp:59-88). */
+/* One step's contact set on the device, in the reference's stacked row order:
+ * nc normal rows, then two tangent rows per frictional contact
+ * (contact.hpp:59-88).  Every array is sized for the capacities; the live
+ * counts are device-resident (cnt), written by hdk_contact_setup, so the
+ * whole contact step runs inside the forward CUDA graph without a host round
+ * trip.  cnt: HDK_CNT_* below. */
+#define HDK_CNT_NC 0
+#define HDK_CNT_NF 1
+#define HDK_CNT_K 2
+#define HDK_CNT_NU 3
+#define HDK_CNT_OVERFLOW 4   /* capacities exceeded: the step is voided (ctl->err = HDK_ERR_CAPACITY) */
+#define HDK_CNT_SPIKE 5      /* next unique slot of the inverse-column loop */
+#define HDK_CNT_SPIKE_COND 6 /* inverse-column loop still running */
+#define HDK_CNT_NEED_C 7     /* counts that overflowed: contacts, rows, unique vertices */
+#define HDK_CNT_NEED_K 8
+#define HDK_CNT_NEED_U 9
+#define HDK_CNT_INTS 16
+#define HDK_ERR_CAPACITY 100 /* internal: grow the contact capacities and re-run the step */
+
 typedef struct hdk_contacts {
-  int nc, nf, k, nu;          /* normal contacts, frictional contacts, rows, unique vertices */
-  const int* vertex;          /* nc */
-  const double* normal;       /* 3 nc */
-  const double* t1;           /* 3 nc */
-  const double* t2;           /* 3 nc */
-  const double* gap;          /* nc: gap offsets */
-  const double* mu;           /* nc: friction coefficients */
-  const double* r_n;          /* nc: h^2 W_nn */
-  const double* r_f;          /* nc: h^2 mean tangent W */
-  const int* fric;            /* nf: contact index of the f-th frictional contact */
-  const int* row_unique;      /* k: unique-vertex slot of each row */
-  const int* urow_off;        /* nu+1 */
-  const int* urow;            /* k: rows of each unique vertex, ascending */
+  int cap_c, cap_k, cap_u;  /* capacities: contacts, rows, unique vertices */
+  int n;                    /* free vertices (leading dimension of U) */
+  int* cnt;                 /* HDK_CNT_INTS device counters */
+  int* vertex;              /* cap_c: contact vertex (vertex-major, obstacle-minor scan order) */
+  int* obstacle;            /* cap_c: obstacle id */
+  double* normal;           /* 3 cap_c */
+  double* t1;               /* 3 cap_c */
+  double* t2;               /* 3 cap_c */
+  double* gap;              /* cap_c: gap offsets n.x - sd */
+  double* mu;               /* cap_c: friction coefficients */
+  double* r_n;              /* cap_c: h^2 W_nn */
+  double* r_f;              /* cap_c: h^2 mean tangent W */
+  int* fric;                /* cap_c: contact index of the f-th frictional contact */
+  int* fpre;                /* cap_c+1: frictional contacts before contact i */
+  int* row_unique;          /* cap_k: unique-vertex slot of each row */
+  int* urow_off;            /* cap_u+1 */
+  int* urow;                /* cap_k: rows of each unique vertex, ascending */
+  int* unique_pos;          /* cap_u: elimination position of each unique vertex */
+  int* nfirst;              /* cap_u+1: first contact of each unique vertex */
+  double* U;                /* n x cap_u scalar inverse columns A_s^{-1} e_{p(u)} (column-major) */
+  double* W;                /* k x k Delassus matrix (leading dimension k) within cap_k^2 */
+  double* lambda;           /* cap_k multipliers */
+  double* omega;            /* cap_k NCP weights (weights_star after the step) */
+  double* e_diag;           /* cap_k */
+  double* g;                /* 3 cap_u: per unique vertex sum of omega lambda d over its rows */
+  double* y;                /* cap_k: reduced adjoint multipliers (backward) */
 } hdk_contacts;
 
-/* flags[v * n_obstacles + o] = signed distance <= margin for free vertices
- * (detect_contacts, contact.cpp:117-144); obstacles: 8 doubles each
- * {kind(0 half-space, 1 sphere), nx, ny, nz, offset|radius, cx, cy, cz}. */
-HDK_API int hdk_contact_detect(int nv, const int* v2p, const double* q, int n_obstacles, const double* obstacles,
-                               double margin, unsigned char* flags, void* stream);
-HDK_API int hdk_contact_weights(const hdk_contacts* c, const double* q, const double* q_t, const double* lambda,
-                                double* omega, double* e_diag, void* stream);
-HDK_API int hdk_contact_jq(const hdk_contacts* c, const double* q, double* jq, void* stream);
-/* Lifted multiplier system of contact_iteration (column-major M). */
-HDK_API int hdk_contact_system(const hdk_contacts* c, const double* W, const double* omega, const double* e_diag,
-                               const double* lambda, const double* jq0, const double* q_t, double* M, double* rhs,
-                               void* stream);
-HDK_API int hdk_contact_project(const hdk_contacts* c, const double* step, double* lambda, int* err, void* stream);
-/* out = base + A^{-1} J^T (scale * omega o lambda) through the cached scalar
- * columns U (n x nu, column-major); g is 3 nu scratch. */
-HDK_API int hdk_contact_correct(const hdk_contacts* c, int n, const int* p2v, const double* U, const double* omega,
-                                const double* lambda, double scale, double* g, const double* base, double* out,
+/* Device bytes of a contact block with these capacities, and the carving of
+ * one such block (base: that many bytes, 256-aligned) into *c. */
+HDK_API size_t hdk_contact_block_bytes(int cap_c, int cap_k, int cap_u, int n);
+HDK_API void hdk_contact_block_layout(void* base, int cap_c, int cap_k, int cap_u, int n, hdk_contacts* c);
+
+/* Per-iteration contact trace (parity observability, B200 extension): the
+ * decision values of project_multipliers (contact.cpp:218-235) —
+ * clamp[it * cap_c + i] = normal multiplier i before the clamp of iteration
+ * it (clamped iff < 0), cone[it * cap_c + f] = (|lambda_t| - mu lambda_n) /
+ * (mu lambda_n) of frictional contact f before the projection (projected iff
+ * > 0; -1 when mu lambda_n = 0, where the pair is zeroed either way).
+ * Iterations >= cap are not recorded. */
+typedef struct hdk_contact_trace {
+  double* clamp;
+  double* cone;
+  int cap;
+} hdk_contact_trace;
+
+/* Detection at q (free vertices x obstacles, vertex-major / obstacle-minor,
+ * signed distance <= margin: detect_contacts contact.cpp:117-144), the
+ * order-preserving compaction, the contact geometry (normal, gap offset,
+ * tangent basis, contact.cpp:39-66), the frictional list, the unique-vertex
+ * rows, zero multipliers and the counts, in one single-CTA kernel.
+ * obstacles: HDK_OBSTACLE_DOUBLES each {kind(0 half-space, 1 sphere), nx, ny,
+ * nz, offset|radius, cx, cy, cz, friction, -, -, -}.  Sets the inverse-column
+ * loop's WHILE condition (nu > 0) when cond_handle != 0.  On overflow the
+ * counts read 0, HDK_CNT_NEED_* hold the sizes and ctl->err =
+ * HDK_ERR_CAPACITY. */
+#define HDK_OBSTACLE_DOUBLES 12
+HDK_API int hdk_contact_setup(int nv, const int* v2p, const double* q, int n_obstacles, const double* obstacles,
+                              double margin, const hdk_contacts* c, hdk_ctl* ctl, unsigned long long cond_handle,
+                              void* stream);
+/* Inverse-column loop body (factor.cpp:237-289): unit spikes of the next
+ * three unique vertices into the three axes of rhs_perm; after the solve,
+ * their columns into U and the loop advanced (WHILE condition). */
+HDK_API int hdk_contact_spikes(const hdk_contacts* c, double* rhs_perm, void* stream);
+HDK_API int hdk_contact_unspike(const hdk_contacts* c, const double* x_perm, unsigned long long cond_handle,
                                 void* stream);
-HDK_API int hdk_contact_spikes(int n, const int* unique_pos, int u0, int count, double* rhs_perm, void* stream);
-HDK_API int hdk_contact_unspike(int n, const double* x_perm, int u0, int count, double* U, void* stream);
-HDK_API int hdk_contact_delassus(const hdk_contacts* c, const double* U, int n, const int* unique_pos, double* W,
-                                 void* stream);
-HDK_API int hdk_contact_reduced(const hdk_contacts* c, const double* X, size_t ldx, const double* omega,
-                                const double* e_diag, const double* z0, double* M, double* rhs, void* stream);
-HDK_API int hdk_contact_combine(int n3, const double* z0, const double* X, size_t ldx, int k, const double* omega,
-                                const double* y, double* mu, int* err, void* stream);
-HDK_API int hdk_contact_column_init(const hdk_contacts* c, int row, int nv, const int* v2p, const double* U, int n,
-                                    double* rhs, double* x0, void* stream);
-HDK_API int hdk_contact_friction_pushback(const hdk_contacts* c, const double* omega, const double* y, double* dl_dq,
-                                          void* stream);
+/* W(r, s) = (d_r . d_s) U[p(u_s), u_r] and r_n = h^2 W_nn, r_f = h^2 (W_t1t1 + W_t2t2)/2
+ * (Delassus, factor.cpp:237-289; forward.cpp:178-193). */
+HDK_API int hdk_contact_delassus(const hdk_contacts* c, double h, void* stream);
+/* NCP weights at (q, q_t, lambda) into omega / e_diag (contact_weights,
+ * contact.cpp:160-196); the post-loop weights_star. */
+HDK_API int hdk_contact_weights(const hdk_contacts* c, const double* q, const double* q_t, void* stream);
+/* One multiplier update of the PD loop (forward.cpp:226-235): NCP weights at
+ * q_cur, J q_mid = J q0 + W (omega o lambda), the lifted system
+ * M = Omega W Omega + E + lift I and offset vector (contact_iteration /
+ * offset_vector, contact.cpp:198-256), its LDL^T solve (dense.cuh), the
+ * projection (contact.cpp:218-235) and the per-unique-vertex coefficients g
+ * of the corrected iterate.  One CTA.  Errors: SINGULAR_CONTACT_SYSTEM (9).
+ * trace may be NULL. */
+HDK_API int hdk_contact_ncp(const hdk_contacts* c, const double* q_cur, const double* q_t, const double* q0,
+                            double* M_scratch, hdk_ctl* ctl, const hdk_contact_trace* trace, void* stream);
+/* Scratch doubles hdk_contact_ncp / hdk_contact_reduced need in global memory
+ * for these capacities (0 when the system fits in shared memory). */
+HDK_API size_t hdk_contact_scratch_doubles(int cap_k);
+/* Test hook: out[i] = hypot(x[i], y[i]) as the contact kernels compute it
+ * (glibc-exact, dense.cuh); device arrays. */
+HDK_API int hdk_test_hypot(const double* x, const double* y, double* out, int n, void* stream);
+/* Largest row capacity whose system factors in shared memory. */
+HDK_API int hdk_contact_smem_rows(void);
+/* out = q0 + A^{-1} J^T (omega o lambda) on free vertices through U
+ * (contact_corrected, forward.cpp:196-206). */
+HDK_API int hdk_contact_correct(const hdk_contacts* c, const int* p2v, const double* q0, double* out, void* stream);
+/* Reduced adjoint multiplier system (backward.cpp:240-262): w_tan(d, c) =
+ * d_d . X_c[v_d], symmetrised; M = Omega sym Omega + E + lift I; rhs =
+ * omega o (J z0); LDL^T solve into c->y.  Errors: ADJOINT_DIVERGED (10). */
+HDK_API int hdk_contact_reduced(const hdk_contacts* c, const double* X, size_t ldx, const double* z0,
+                                double* M_scratch, int* err, void* stream);
+/* mu = z0 - sum_c (omega_c y_c) X_c (backward.cpp:266-268). */
+HDK_API int hdk_contact_combine(const hdk_contacts* c, int n3, const double* z0, const double* X, size_t ldx,
+                                double* mu, void* stream);
+/* Right-hand side e_v d_row and warm start a_row (backward.cpp:229-238) of one column. */
+HDK_API int hdk_contact_column_init(const hdk_contacts* c, int row, int nv, const int* v2p, double* rhs, double* x0,
+                                    void* stream);
+/* Friction rows push back into dL/dq_t (backward.cpp:342-356). */
+HDK_API int hdk_contact_friction_pushback(const hdk_contacts* c, double* dl_dq, void* stream);
 
 /* Contact-adjoint columns (engine_columns.cpp): the per-column backbone
  * buffers of HDK_BB_COLUMNS columns, so each backbone stage is one launch

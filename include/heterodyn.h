@@ -121,6 +121,20 @@ HD_API hd_status hd_sim_set_external_force(hd_sim* sim, const double* f_ext, siz
  * drivers.cpp:147-159) and the current state's deepest obstacle penetration
  * (max_penetration_at, drivers.cpp:101-111). */
 HD_API double hd_sim_last_fb_residual(const hd_sim* sim);
+/* Contact trace of the last step (B200 extension; parity observability for
+ * the contact path): the contacts' (vertex, obstacle) pairs in row order
+ * (detect_contacts' vertex-major / obstacle-minor scan, contact.cpp:117-144)
+ * and, per forward iteration, the decision values of project_multipliers
+ * (contact.cpp:218-235): clamp[it * nc + i] = normal multiplier i before the
+ * clamp (clamped at zero iff < 0); cone[it * nf + f] = (|lambda_t| -
+ * mu lambda_n) / (mu lambda_n) of frictional contact f before the projection
+ * (projected onto the Coulomb cone iff > 0; -1 when mu lambda_n = 0, where the
+ * pair is zeroed whatever its value).  counts[3] (may be NULL) receives
+ * {nc, nf, iterations}; any buffer may be NULL; capacities (in doubles) are
+ * checked (HD_ERR_INVALID_ARGUMENT). */
+HD_API hd_status hd_sim_contact_trace(const hd_sim* sim, int* vertex, int* obstacle, size_t row_capacity,
+                                      double* clamp, size_t clamp_capacity, double* cone, size_t cone_capacity,
+                                      int* counts);
 HD_API double hd_sim_penetration(const hd_sim* sim);
 
 /* Records every subsequent frame's adjoint cache (the reference's

@@ -32,6 +32,9 @@ struct hd_sim {
   bool last_converged = false;
   int last_contact_count = 0;
   double last_fb_residual = 0;
+  std::vector<int> trace_vertex, trace_obstacle;
+  std::vector<double> trace_clamp, trace_cone;
+  int trace_nf = 0;
   bool record = false;
   std::vector<ForwardCache> caches;
   std::vector<double> tau, rho;
@@ -197,6 +200,15 @@ hd_status hd_sim_step(hd_sim* sim) {
       fb = std::max(fb, std::abs(fb_residual(delta, cp.r_n, cache.lambda_star[c])));
     }
     sim->last_fb_residual = fb;
+    sim->trace_vertex.clear();
+    sim->trace_obstacle.clear();
+    for (const ContactPoint& cp : cache.contacts.contacts) {
+      sim->trace_vertex.push_back(cp.vertex);
+      sim->trace_obstacle.push_back(cp.obstacle_id);
+    }
+    sim->trace_nf = cache.contacts.friction_pair_count();
+    sim->trace_clamp = cache.trace_clamp;
+    sim->trace_cone = cache.trace_cone;
     if (sim->record) sim->caches.push_back(std::move(cache));
   });
 }
@@ -213,6 +225,31 @@ hd_status hd_sim_velocities(const hd_sim* sim, double* out, size_t cap) {
 int hd_sim_last_iterations(const hd_sim* sim) { return sim ? sim->last_iterations : 0; }
 int hd_sim_last_converged(const hd_sim* sim) { return sim && sim->last_converged ? 1 : 0; }
 int hd_sim_last_contact_count(const hd_sim* sim) { return sim ? sim->last_contact_count : 0; }
+hd_status hd_sim_contact_trace(const hd_sim* sim, int* vertex, int* obstacle, size_t row_capacity,
+                               double* clamp, size_t clamp_capacity, double* cone, size_t cone_capacity,
+                               int* counts) {
+  if (!sim) return null_arg("hd_sim_contact_trace");
+  const int nc = static_cast<int>(sim->trace_vertex.size()), nf = sim->trace_nf;
+  const int iters = nc > 0 ? static_cast<int>(sim->trace_clamp.size() / nc) : 0;
+  if (counts) {
+    counts[0] = nc;
+    counts[1] = nf;
+    counts[2] = iters;
+  }
+  if ((vertex || obstacle) && row_capacity < static_cast<size_t>(nc)) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_sim_contact_trace: row capacity too small");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  if ((clamp && clamp_capacity < sim->trace_clamp.size()) || (cone && cone_capacity < sim->trace_cone.size())) {
+    set_error(HD_ERR_INVALID_ARGUMENT, "hd_sim_contact_trace: pattern capacity too small");
+    return HD_ERR_INVALID_ARGUMENT;
+  }
+  if (vertex) std::copy(sim->trace_vertex.begin(), sim->trace_vertex.end(), vertex);
+  if (obstacle) std::copy(sim->trace_obstacle.begin(), sim->trace_obstacle.end(), obstacle);
+  if (clamp) std::copy(sim->trace_clamp.begin(), sim->trace_clamp.end(), clamp);
+  if (cone) std::copy(sim->trace_cone.begin(), sim->trace_cone.end(), cone);
+  return HD_OK;
+}
 double hd_sim_last_fb_residual(const hd_sim* sim) { return sim ? sim->last_fb_residual : 0.0; }
 double hd_sim_penetration(const hd_sim* sim) {  // max_penetration_at (drivers.cpp:101-111)
   if (!sim) return 0.0;

@@ -314,7 +314,7 @@ WeightSet contact_weights(const ContactSet& s, const VecX& q, const VecX& q_t, c
 VecX offset_vector(const ContactSet& s, const WeightSet& w, const VecX& q_t);                       // :198-216
 VecX project_multipliers(const ContactSet& s, VecX lambda);                                         // :218-235
 VecX contact_iteration(const ContactSet& s, const MatX& w, const WeightSet& wt, const VecX& h_vec,
-                       const VecX& jq_mid, const VecX& lambda);                                     // :237-256
+                       const VecX& jq_mid, const VecX& lambda, VecX* unprojected = nullptr);        // :237-256
 
 // ---- forward.hpp:19-139 ----------------------------------------------------
 struct SolverConfig {
@@ -357,6 +357,10 @@ struct ForwardCache {  // forward.hpp:86-102
   std::vector<VecX> cached_columns;
   int iteration_count = 0;
   bool converged = false;
+  // Parity observability (not in the reference cache): per iteration, the
+  // decision values of project_multipliers (contact.cpp:218-235), see
+  // hd_sim_contact_trace.
+  std::vector<double> trace_clamp, trace_cone;
 };
 VecX free_fall_target(const TetMesh& mesh, const SimState& st, const VecX& f_ext, const StateForce* hook, double h);  // forward.cpp:59-68
 std::vector<ElementProjection> local_solve(const TetMesh& mesh, const MaterialField& mat, const VecX& q);           // :70-94

@@ -183,6 +183,30 @@ hd_status hd_sim_velocities(const hd_sim* sim, double* out, size_t cap) {
 int hd_sim_last_iterations(const hd_sim* sim) { return sim ? sim->eng->last_iterations : 0; }
 int hd_sim_last_converged(const hd_sim* sim) { return sim && sim->eng->last_converged ? 1 : 0; }
 int hd_sim_last_contact_count(const hd_sim* sim) { return sim ? sim->eng->last_contacts : 0; }
+hd_status hd_sim_contact_trace(const hd_sim* sim, int* vertex, int* obstacle, size_t row_capacity,
+                               double* clamp, size_t clamp_capacity, double* cone, size_t cone_capacity,
+                               int* counts) {
+  if (!sim) return bad_arg("hd_sim_contact_trace: sim is NULL");
+  return guarded([&] {
+    std::vector<int> v, o;
+    std::vector<double> cl, co;
+    int nc = 0, nf = 0, iters = 0;
+    sim->eng->contact_trace(v, o, cl, co, nc, nf, iters);
+    if (counts) {
+      counts[0] = nc;
+      counts[1] = nf;
+      counts[2] = iters;
+    }
+    if ((vertex || obstacle) && row_capacity < v.size())
+      hdb::raise(hdb::Code::InvalidArgument, "hd_sim_contact_trace: row capacity too small");
+    if ((clamp && clamp_capacity < cl.size()) || (cone && cone_capacity < co.size()))
+      hdb::raise(hdb::Code::InvalidArgument, "hd_sim_contact_trace: pattern capacity too small");
+    if (vertex) std::copy(v.begin(), v.end(), vertex);
+    if (obstacle) std::copy(o.begin(), o.end(), obstacle);
+    if (clamp) std::copy(cl.begin(), cl.end(), clamp);
+    if (cone) std::copy(co.begin(), co.end(), cone);
+  });
+}
 double hd_sim_last_fb_residual(const hd_sim* sim) {
   double r = 0.0;
   if (sim) guarded([&] { r = sim->eng->last_fb_residual(); });

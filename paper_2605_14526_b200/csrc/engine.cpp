@@ -8,7 +8,6 @@
 #include <cstring>
 #include <functional>
 
-#include <cusolverDn.h>
 
 namespace hdb {
 
@@ -127,6 +126,59 @@ void build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()
   for (cudaGraph_t g : {gpre, gpost, top}) cudaGraphDestroy(g);
 }
 
+void build_seq_graph(cudaStream_t st, bool use_cond, std::vector<SeqGraph::Seg> segs, SeqGraph& out) {
+  out.destroy();
+  const size_t ns = segs.size();
+  out.kernels.assign(ns, 0);
+  if (!use_cond) {
+    out.parts.assign(ns, nullptr);
+    for (size_t i = 0; i < ns; ++i) {
+      cudaGraph_t g = capture(st, [&] { segs[i].fn(0ULL); });
+      out.kernels[i] = kernel_nodes(g);
+      out.parts[i] = instantiate(g);
+      cudaGraphDestroy(g);
+    }
+  } else {
+    cudaGraph_t top = nullptr;
+    cuda_check(cudaGraphCreate(&top, 0), "graph create");
+    std::vector<cudaGraphConditionalHandle> hs(ns, 0);
+    for (size_t i = 0; i < ns; ++i)
+      if (segs[i].loop)
+        cuda_check(cudaGraphConditionalHandleCreate(&hs[i], top, segs[i].check_first ? 0 : 1, cudaGraphCondAssignDefault),
+                   "cond handle");
+    cudaGraphNode_t prev = nullptr;
+    for (size_t i = 0; i < ns; ++i) {
+      cudaGraphNode_t node = nullptr;
+      if (!segs[i].loop) {
+        const unsigned long long next = (i + 1 < ns && segs[i + 1].loop) ? static_cast<unsigned long long>(hs[i + 1]) : 0ULL;
+        cudaGraph_t g = capture(st, [&] { segs[i].fn(next); });
+        out.kernels[i] = kernel_nodes(g);
+        size_t nn = 0;
+        cuda_check(cudaGraphGetNodes(g, nullptr, &nn), "graph nodes");
+        if (nn) {
+          cuda_check(cudaGraphAddChildGraphNode(&node, top, prev ? &prev : nullptr, prev ? 1 : 0, g), "add segment");
+          prev = node;
+        }
+        cudaGraphDestroy(g);
+        continue;
+      }
+      cudaGraphNodeParams p{};
+      p.type = cudaGraphNodeTypeConditional;
+      p.conditional.handle = hs[i];
+      p.conditional.type = cudaGraphCondTypeWhile;
+      p.conditional.size = 1;
+      cuda_check(cudaGraphAddNode(&node, top, prev ? &prev : nullptr, prev ? 1 : 0, &p), "add while");
+      capture_into(st, p.conditional.phGraph_out[0], [&] { segs[i].fn(static_cast<unsigned long long>(hs[i])); });
+      out.kernels[i] = kernel_nodes(p.conditional.phGraph_out[0]);
+      prev = node;
+    }
+    out.exec = instantiate(top);
+    cudaGraphDestroy(top);
+  }
+  for (auto& sg : segs) sg.fn = nullptr;  // captured; the closures may reference the caller's locals
+  out.segs = std::move(segs);
+}
+
 Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared_device)
     : scene_(scene), mat_(scene.material), solve_ctas_(solve_ctas), branch_(!shared_device) {
   if (const char* br = std::getenv("HETERODYN_BRANCH")) branch_ = std::atoi(br) != 0;
@@ -192,13 +244,12 @@ Engine::~Engine() {
     if (e) cudaEventDestroy(e);
   if (fgraph_) fgraph_->destroy();
   if (bgraph_) bgraph_->destroy();
-  for (cudaGraphExec_t e : {bpre_, bpost_a_, bpost_b_, fpre_, fpost_})
+  cgraph_.destroy();
+  for (cudaGraphExec_t e : {bpre_, bpost_a_, bpost_b_})
     if (e) cudaGraphExecDestroy(e);
-  for (void* p : {static_cast<void*>(cjq_), static_cast<void*>(cM_), static_cast<void*>(crhs_), static_cast<void*>(cg_),
-                  static_cast<void*>(cX_), static_cast<void*>(cz0_), static_cast<void*>(cwork_),
-                  static_cast<void*>(cinfo_)})
+  for (void* p : {static_cast<void*>(cM_), static_cast<void*>(cX_), static_cast<void*>(cz0_), ctr_mem_})
     if (p) cudaFree(p);
-  if (cusolver_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(cusolver_));
+  if (h_cnt_) cudaFreeHost(h_cnt_);
   frame_mem_.clear();
   fmem_.reset();
   mem_.reset();
@@ -293,15 +344,15 @@ void Engine::build_static() {
   const double hk[5] = {scene_.hook_anchor.x, scene_.hook_anchor.y, scene_.hook_anchor.z, scene_.hook_k, scene_.hook_d};
   hook_ = A.alloc<double>(5);
   DevArena::copy_h2d(hook_, hk, sizeof(hk));
-  // obstacles: {kind, nx, ny, nz, offset|radius, cx, cy, cz}
+  // obstacles: {kind, nx, ny, nz, offset|radius, cx, cy, cz, friction, 0, 0, 0}
   Vec ob;
   for (const Obstacle& o : scene_.obstacles) {
-    const double rec[8] = {static_cast<double>(o.kind), o.normal.x, o.normal.y, o.normal.z,
-                           o.kind == 0 ? o.offset : o.radius, o.center.x, o.center.y, o.center.z};
-    ob.insert(ob.end(), rec, rec + 8);
+    const double rec[HDK_OBSTACLE_DOUBLES] = {static_cast<double>(o.kind), o.normal.x, o.normal.y, o.normal.z,
+                                              o.kind == 0 ? o.offset : o.radius, o.center.x, o.center.y, o.center.z,
+                                              o.friction, 0.0, 0.0, 0.0};
+    ob.insert(ob.end(), rec, rec + HDK_OBSTACLE_DOUBLES);
   }
   obst_ = A.upload(ob);
-  flags_ = A.alloc<unsigned char>(static_cast<size_t>(nv) * std::max<size_t>(1, scene_.obstacles.size()));
   q0c_ = A.alloc<double>(n3);
   aa_window_ = scene_.solver.aa_window > 0 ? scene_.solver.aa_window : (mat_.contrast() > 10.0 ? 1 : 5);
   aa_window_ = std::min(aa_window_, HDK_AA_MAX);
@@ -561,15 +612,7 @@ void Engine::build_forward_graph() {
     hdk_check(hdk_local_step(&dm_, &dmat_, qcur_, ef_, cache_, &ctl_->err, s), "cache sweep");
   };
   build_loop_graph(st_, use_cond_, pre, body, post, *fgraph_);
-  for (cudaGraphExec_t* e : {&fpre_, &fpost_})
-    if (*e) {
-      cudaGraphExecDestroy(*e);
-      *e = nullptr;
-    }
-  if (!scene_.obstacles.empty()) {
-    fpre_ = capture_exec(st_, pre, nullptr);
-    fpost_ = capture_exec(st_, post, nullptr);
-  }
+  if (cw_.base) build_contact_graph();  // scenes with obstacles (engine_contact.cpp)
   fk_pre_ = fgraph_->counts[0];
   fk_body_ = fgraph_->counts[1];
   fk_post_ = fgraph_->counts[2];
@@ -827,6 +870,7 @@ void Engine::check_ctl(const char* what) {
     switch (c) {
       case 6: msg += "local stretch solve did not reach stationarity"; break;
       case 7: msg += "filtered prox Hessian is numerically singular"; break;
+      case 9: msg += "contact system is singular even after the diagonal lift"; break;
       case 10: msg += "adjoint backbone iteration did not settle (cap or non-finite values)"; break;
       default: msg += "device solver error"; break;
     }
@@ -836,23 +880,10 @@ void Engine::check_ctl(const char* what) {
 
 void Engine::step() {
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
+  const bool contact_scene = !scene_.obstacles.empty();
   phase_mark(0);
-  std::shared_ptr<ContactFrame> contacts;
-  if (!scene_.obstacles.empty()) {
-    cuda_check(cudaGraphLaunch(fpre_, st_), "forward pre");
-    kernel_launches += fk_pre_;
-    contacts = detect_and_setup();
-  }
-  if (contacts && contacts->k > 0) {
-    contact_loop(*contacts);
-    cuda_check(cudaGraphLaunch(fpost_, st_), "forward post");
-    // weights at the converged state (forward.cpp:258-262)
-    hdk_check(hdk_contact_weights(&contacts->view, qcur_, q_, contacts->lambda, contacts->omega, contacts->e_diag, st_),
-              "weights star");
-    kernel_launches += fk_post_ + 1;
-  } else {
-    run_graph(*fgraph_, "forward graph");
-  }
+  if (contact_scene) run_contact_step();
+  else run_graph(*fgraph_, "forward graph");
   if (recording_) {
     if (static_cast<int>(slots_.size()) <= nrec_) add_slot();
     const Frame& fr = slots_[nrec_];
@@ -868,18 +899,51 @@ void Engine::step() {
   }
   hdk_check(hdk_commit(static_cast<int>(n3), ctl_, qcur_, scene_.solver.h, q_, v_, st_), "commit");
   phase_mark(1);
+  if (contact_scene)
+    cuda_check(cudaMemcpyAsync(h_cnt_, cw_.view.cnt, sizeof(int) * HDK_CNT_INTS, cudaMemcpyDeviceToHost, st_),
+               "contact counts");
   sync_ctl();
+  if (contact_scene && h_ctl_->err == HDK_ERR_CAPACITY) {
+    // more contacts than the working set holds: nothing was committed; grow and re-run
+    ensure_contact_capacity(h_cnt_[HDK_CNT_NEED_C], h_cnt_[HDK_CNT_NEED_K], h_cnt_[HDK_CNT_NEED_U]);
+    step();
+    return;
+  }
   phase_collect(0, 1);
-  if (!(contacts && contacts->k > 0)) {
-    solve_count += h_ctl_->iterations;
-    kernel_launches += fk_pre_ + static_cast<long long>(fk_body_) * h_ctl_->iterations + fk_post_ + 1;
+  const int iters = h_ctl_->iterations;
+  if (contact_scene) {
+    cw_.nc = h_cnt_[HDK_CNT_NC];
+    cw_.nf = h_cnt_[HDK_CNT_NF];
+    cw_.k = h_cnt_[HDK_CNT_K];
+    cw_.nu = h_cnt_[HDK_CNT_NU];
+    trace_iters_ = std::min(iters, ctr_.cap);
+    const int spikes = (cw_.nu + 2) / 3;
+    solve_count += iters + spikes;
+    kernel_launches += fc_kernels_[0] + static_cast<long long>(fc_kernels_[1]) * spikes + fc_kernels_[2] +
+                       static_cast<long long>(fc_kernels_[3]) * iters + fc_kernels_[4] + 1;
+  } else {
+    solve_count += iters;
+    kernel_launches += fk_pre_ + static_cast<long long>(fk_body_) * iters + fk_post_ + 1;
   }
   check_ctl("forward step");
-  last_iterations = h_ctl_->iterations;
+  last_iterations = iters;
   last_converged = h_ctl_->converged;
-  last_contacts = contacts ? contacts->nc : 0;
-  cur_contacts_ = contacts;
-  if (recording_) slots_[nrec_].contacts = contacts;
+  last_contacts = contact_scene ? cw_.nc : 0;
+  cur_has_contacts_ = contact_scene && cw_.k > 0;
+  if (recording_) {
+    Frame& fr = slots_[nrec_];
+    fr.has_contacts = cur_has_contacts_;
+    if (cur_has_contacts_) {  // the adjoint's copy of this step's contact set
+      if (!fr.contacts) fr.contacts = std::make_shared<ContactFrame>();
+      ContactFrame& c = *fr.contacts;
+      c.allocate(cw_.view.cap_c, cw_.view.cap_k, cw_.view.cap_u, cw_.view.n);
+      cuda_check(cudaMemcpyAsync(c.base, cw_.base, cw_.bytes, cudaMemcpyDeviceToDevice, st_), "record contacts");
+      c.nc = cw_.nc;
+      c.nf = cw_.nf;
+      c.k = cw_.k;
+      c.nu = cw_.nu;
+    }
+  }
   time_ += scene_.solver.h;
   if (recording_) ++nrec_;
 }

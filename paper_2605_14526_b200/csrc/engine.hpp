@@ -55,22 +55,49 @@ void build_loop_graph(cudaStream_t st, bool use_cond, const std::function<void()
                       const std::function<void(unsigned long long)>& body, const std::function<void()>& post,
                       LoopGraph& out);
 
-// One step's contact set: host copy (reference layout) + device view, the
-// cached scalar inverse columns U = A_s^{-1} E of its unique vertices, and the
-// converged multipliers / NCP weights consumed by the adjoint.
+// A contact set in device memory: one allocation carved by
+// hdk_contact_block_layout (capacities, counts, rows, inverse columns, W,
+// multipliers, weights).  The engine's working set is one; every recorded
+// frame with contacts keeps a copy for the adjoint (same capacities, one D2D
+// copy).  nc/nf/k/nu are host copies of the device counts, valid after the
+// step's status read.
 struct ContactFrame {
   int nc = 0, nf = 0, k = 0, nu = 0;
-  std::vector<int> vertex, fric, row_unique, urow_off, urow, unique_vertex, unique_pos;
-  Vec normal, t1, t2, gap, mu, r_n, r_f;
-  std::unique_ptr<DevArena> mem;
+  void* base = nullptr;
+  size_t bytes = 0;
   hdk_contacts view{};
-  double* U = nullptr;        // n x nu, column-major (elimination order rows)
-  int* unique_pos_d = nullptr;
-  double* W = nullptr;        // k x k
-  double* lambda = nullptr;   // k
-  double* omega = nullptr;    // k (weights_star after the step)
-  double* e_diag = nullptr;   // k
+  ContactFrame() = default;
+  ContactFrame(const ContactFrame&) = delete;
+  ContactFrame& operator=(const ContactFrame&) = delete;
+  ~ContactFrame();
+  void allocate(int cap_c, int cap_k, int cap_u, int n);  // (re)allocates when the layout differs
 };
+
+// pre -> [while] -> ... as one executable graph: segments in order, a loop
+// segment is a WHILE conditional node whose body the segment's function
+// captures (it receives the node's handle and sets the condition on the
+// device).  Without conditional nodes (HETERODYN_NO_COND_GRAPH=1) every
+// segment is its own executable and the host drives the loops from `flag`.
+struct SeqGraph {
+  struct Seg {
+    bool loop = false;
+    bool check_first = false;     // loop condition set before the node (else it starts at 1)
+    const int* flag = nullptr;    // device word holding the loop condition (host-driven mode)
+    std::function<void(unsigned long long)> fn;
+  };
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaGraphExec_t> parts;
+  std::vector<Seg> segs;
+  std::vector<int> kernels;  // kernel nodes per segment
+  void destroy() {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    for (cudaGraphExec_t e : parts)
+      if (e) cudaGraphExecDestroy(e);
+    parts.clear();
+  }
+};
+void build_seq_graph(cudaStream_t st, bool use_cond, std::vector<SeqGraph::Seg> segs, SeqGraph& out);
 
 struct GradOut {
   Vec dl_dq0, dl_dv0, dl_df_ext, dl_de, dl_dw;
@@ -98,6 +125,10 @@ class Engine {
   void set_external_force(const double* f);  // dof doubles into the device f_ext the graphs read
   void external_force_into(double* out) const;
   double last_fb_residual() const;  // max |FB residual| over the last step's normal contacts
+  // Contact rows (vertex, obstacle) of the last step and its per-iteration
+  // clamp / cone decision values ([iteration][nc], [iteration][nf], hdk_contact_trace).
+  void contact_trace(std::vector<int>& vertex, std::vector<int>& obstacle, std::vector<double>& clamp,
+                     std::vector<double>& cone, int& nc, int& nf, int& iterations) const;
   double penetration() const;       // deepest obstacle penetration of the current state
   // canonical: seed from device state, L = 1/2|q_T - ref|^2 (+ 1/2|v_T|^2 when
   // d_target is null and ref is the rest shape); d_target is a device array.
@@ -179,9 +210,6 @@ class Engine {
   void build_backward_graph();
   void run_graph(LoopGraph& g, const char* what);
   void backward_frame(int t, GradOut& out);
-  std::shared_ptr<ContactFrame> detect_and_setup();
-  void contact_loop(ContactFrame& cf);
-  void ensure_solver_workspace(int k);
   void sync_ctl();
   void check_ctl(const char* what);
 
@@ -239,7 +267,8 @@ class Engine {
 
   struct Frame {
     double *q_t, *v_t, *qtil, *qprev, *qstar, *cache;
-    std::shared_ptr<ContactFrame> contacts;
+    std::shared_ptr<ContactFrame> contacts;  // reused across recordings
+    bool has_contacts = false;
   };
   std::vector<Frame> slots_;  // device storage of recorded frames (reused)
   std::vector<std::unique_ptr<DevArena>> frame_mem_;
@@ -251,19 +280,24 @@ class Engine {
   int fk_pre_ = 0, fk_body_ = 0, fk_post_ = 0, bk_pre_ = 0, bk_body_ = 0, bk_post_ = 0;
   std::unique_ptr<LoopGraph> fgraph_, bgraph_;
   cudaGraphExec_t bpre_ = nullptr, bpost_a_ = nullptr, bpost_b_ = nullptr;
-  cudaGraphExec_t fpre_ = nullptr, fpost_ = nullptr;  // pieces of the forward graph (contact path)
-  // contact
-  double* obst_ = nullptr;  // 8 doubles per obstacle
-  unsigned char* flags_ = nullptr;
+  // contact: working set of the current step, its trace and scratch
+  double* obst_ = nullptr;  // HDK_OBSTACLE_DOUBLES per obstacle
   double* q0c_ = nullptr;   // contact-free solve result of one iteration (full)
-  double *cjq_ = nullptr, *cM_ = nullptr, *crhs_ = nullptr, *cg_ = nullptr, *cX_ = nullptr, *cz0_ = nullptr;
+  ContactFrame cw_;
+  int* h_cnt_ = nullptr;    // pinned mirror of cw_.view.cnt
+  double* cM_ = nullptr;    // global scratch of the dense systems when they exceed shared memory
+  size_t cM_len_ = 0;
+  hdk_contact_trace ctr_{};
+  void* ctr_mem_ = nullptr;
+  int trace_iters_ = 0;     // iterations recorded in ctr_ by the last step
+  double *cX_ = nullptr, *cz0_ = nullptr;
   size_t cX_cols_ = 0;
-  int c_cap_ = 0;
-  void* cusolver_ = nullptr;
-  double* cwork_ = nullptr;
-  int cwork_len_ = 0;
-  int* cinfo_ = nullptr;
-  std::shared_ptr<ContactFrame> cur_contacts_;
+  SeqGraph cgraph_;         // forward graph of scenes with obstacles
+  int fc_kernels_[5] = {0, 0, 0, 0, 0};
+  void ensure_contact_capacity(int need_c, int need_k, int need_u);
+  void build_contact_graph();
+  bool run_contact_step();  // false: capacities grown, step must be re-run
+  bool cur_has_contacts_ = false;
 };
 
 }  // namespace hdb

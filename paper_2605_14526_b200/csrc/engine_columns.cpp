@@ -219,10 +219,10 @@ double Engine::time_columns(int reps, unsigned skip) {
 int Engine::solve_columns(const ContactFrame& c, int r0) {
   if (!cols_) build_columns();
   ColumnSet& S = *cols_;
-  const int n = hf_.n, nv = scene_.mesh.nv;
+  const int nv = scene_.mesh.nv;
   for (int j = 0; j < kColumns; ++j) {
     const int row = std::min(r0 + j, c.k - 1);
-    hdk_ok(hdk_contact_column_init(&c.view, row, nv, df_.v2p, c.U, n, S.col[j].seed, S.col[j].x, st_), "column init");
+    hdk_ok(hdk_contact_column_init(&c.view, row, nv, df_.v2p, S.col[j].seed, S.col[j].x, st_), "column init");
   }
   kernel_launches += kColumns;
   if (ph_.on) cuda_check(cudaEventRecord(ph_.ev[6], st_), "phase event");

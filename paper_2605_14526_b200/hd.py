@@ -47,6 +47,8 @@ SIGNATURES = {
     "hd_scene_young_moduli": (C.c_int, [_VP, _D, C.c_size_t]),
     "hd_scene_elements": (C.c_int, [_VP, C.POINTER(C.c_int), C.c_size_t]),
     "hd_sim_last_fb_residual": (C.c_double, [_VP]),
+    "hd_sim_contact_trace": (C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_size_t,
+                                      _D, C.c_size_t, _D, C.c_size_t, C.POINTER(C.c_int)]),
     "hd_sim_penetration": (C.c_double, [_VP]),
     "hd_sim_external_force": (C.c_int, [_VP, _D, C.c_size_t]),
     "hd_sim_set_external_force": (C.c_int, [_VP, _D, C.c_size_t]),
@@ -318,6 +320,24 @@ class Sim:
     @property
     def last_contact_count(self):
         return self.L.lib.hd_sim_last_contact_count(self.h)
+
+    def contact_trace(self) -> dict:
+        """Last step's contact rows and per-iteration decision values
+        (hd_sim_contact_trace): vertex, obstacle (nc,), clamp (iterations, nc:
+        clamped iff < 0), cone (iterations, nf: projected iff > 0)."""
+        lib = self.L.lib
+        cnt = (C.c_int * 3)()
+        self.L.check(lib.hd_sim_contact_trace(self.h, None, None, 0, None, 0, None, 0, cnt))
+        nc, nf, it = cnt[0], cnt[1], cnt[2]
+        v = np.zeros(max(nc, 1), dtype=np.int32)
+        o = np.zeros(max(nc, 1), dtype=np.int32)
+        cl = np.zeros(max(it * nc, 1))
+        co = np.zeros(max(it * nf, 1))
+        ip = C.POINTER(C.c_int)
+        self.L.check(lib.hd_sim_contact_trace(self.h, v.ctypes.data_as(ip), o.ctypes.data_as(ip), v.size,
+                                              _ptr(cl), cl.size, _ptr(co), co.size, cnt))
+        return {"vertex": v[:nc], "obstacle": o[:nc], "clamp": cl[:it * nc].reshape(it, nc),
+                "cone": co[:it * nf].reshape(it, nf), "iterations": it}
 
     def record(self, enable: bool = True):
         self.L.check(self.L.lib.hd_sim_record(self.h, 1 if enable else 0))

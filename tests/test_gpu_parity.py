@@ -95,50 +95,6 @@ def test_trajectory_and_gradients(prod, orc, name):
         assert rel2(gp[k], go[k]) <= tol[k], (k, rel2(gp[k], go[k]), tol[k])
 
 
-CONTACT_CASES = {
-    "C4-reduced": (scenes.config_scene("C4", dims=(10, 6, 6), frames=4,
-                                       solver={"eps_rel": 1e-8, "eps_abs": 1e-14}), 4),
-    "block-floor-friction": (scenes.block_scene(floor=True, friction=0.5, v0_amp=0.0, gravity_z=-2.0), 4),
-    "resting-box": ({"mesh": {"generator": "resting-box"}, "frames": 4,
-                     "solver": {"eps_rel": 1e-12, "eps_abs": 1e-14}}, 4),
-    "ball-drop": ({"mesh": {"generator": "ball-drop"}, "frames": 4, "initial": {"velocity": [0, 0, -20.0]},
-                   "solver": {"eps_rel": 1e-12, "eps_abs": 1e-14}}, 4),
-    "slab-on-sphere": ({"mesh": {"generator": "slab-on-sphere"}, "frames": 3, "gravity": [0, 0, -9.81],
-                        "initial": {"position_offset": [0, 0, -0.005]},
-                        "solver": {"eps_rel": 1e-12, "eps_abs": 1e-14}}, 3),
-}
-
-
-@pytest.mark.parametrize("name", list(CONTACT_CASES))
-def test_contact_trajectory_and_gradients(prod, orc, name):
-    """Contact sets per frame identical; state and chained gradients through the
-    frictional contact path (backward.cpp:227-283) within max(1e-6, 10x the
-    oracle's own sensitivity to a 1e-15 input perturbation).  The NCP contact
-    iteration converges linearly, so where the dual gate stops moves with
-    rounding: on the reduced C4 pad the oracle's v moves by ~1e-5 under a
-    1e-15 perturbation of q0 (iteration counts 69 vs 77)."""
-    scene, frames = CONTACT_CASES[name]
-    cp_, co_, cs_ = [], [], []
-    tp, gp = run(prod, scene, frames, contacts=cp_)
-    to, go = run(orc, scene, frames, contacts=co_)
-    ts, gs = run(orc, scene, frames, perturb=1e-15, contacts=cs_)
-    assert cp_ == co_, (cp_, co_)
-    assert max(co_) > 0, "scene must exercise contact"
-    for f, ((qp, vp, ip, cpf), (qo, vo, io, cof), (qs, vs, _, _)) in enumerate(zip(tp, to, ts)):
-        assert cpf == cof
-        tq = max(1e-6, 10 * rel2(qs, qo))
-        assert rel2(qp, qo) <= tq, (f, rel2(qp, qo), tq)
-        if np.linalg.norm(vo) > 1e-8:
-            tv = max(1e-6, 10 * rel2(vs, vo))
-            assert rel2(vp, vo) <= tv, (f, rel2(vp, vo), tv)
-    np.testing.assert_array_equal(gp["tau"], go["tau"])
-    for k in GRADS:
-        if np.linalg.norm(go[k]) == 0:
-            continue
-        tol = max(1e-6, 10 * rel2(gs[k], go[k]))
-        assert rel2(gp[k], go[k]) <= tol, (k, rel2(gp[k], go[k]), tol)
-
-
 def test_solve_matches_oracle_and_inverts(prod, orc):
     scene = scenes.config_scene("C1")
     ps, os_ = prod.scene(scene).sim(), orc.scene(scene).sim()
@@ -158,18 +114,6 @@ def test_deterministic_reruns(prod):
         assert np.array_equal(qa, qb) and np.array_equal(va, vb)
     for k in GRADS:
         assert np.array_equal(a[1][k], b[1][k])
-
-
-def test_deterministic_contact_reruns(prod):
-    """The contact adjoint (multi-column passes, batched column stages) gives
-    bit-identical q, v and gradients on a rerun."""
-    scene, frames = CONTACT_CASES["C4-reduced"]
-    a = run(prod, scene, frames)
-    b = run(prod, scene, frames)
-    for (qa, va, _, _), (qb, vb, _, _) in zip(a[0], b[0]):
-        assert np.array_equal(qa, qb) and np.array_equal(va, vb)
-    for k in GRADS:
-        assert np.array_equal(a[1][k], b[1][k]), k
 
 
 def test_pinned_bitwise_and_cap(prod):
@@ -350,7 +294,10 @@ def test_identify_matches_oracle(prod, orc, case, tmp_path):
         "young-block": {"scene": scenes.block_scene(dims=(4, 3, 2), contrast=10.0, beta0=0.0, frames=3),
                         "design": {"variable": "young", "initial": 3e4}, "true": 5e4,
                         "loss": {"kind": "final_pose"}, "optimizer": {"max_evals": 12, "grad_tol": 1e-14}},
-        "v0-contact": {"scene": scenes.block_scene(dims=(3, 2, 2), floor=True, frames=3),
+        # gravity with a tangential part: the mirror-symmetric drop of a block
+        # straight onto the floor puts Coulomb-cone decisions on exact ties
+        "v0-contact": {"scene": dict(scenes.block_scene(dims=(3, 2, 2), floor=True, frames=3),
+                                     gravity=[0.7, 0.3, -9.81]),
                        "design": {"variable": "v0", "initial": [0, 0, 0]}, "true": [0.05, 0.0, -0.1],
                        "loss": {"kind": "trajectory"}, "optimizer": {"max_evals": 15, "grad_tol": 1e-12}},
     }[case]
