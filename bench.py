@@ -9,10 +9,14 @@ Neo-Hookean crab-like block with Rayleigh damping folded into the factor.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N>1 runs under torchrun as N independent replicas (one trajectory does not
-shard: SURVEY.md §8(e)); the timing is the max over ranks.  The reference arm
-times the CPU restatement of the reference (oracle/, the reference itself
-cannot be built here: Eigen is absent) on the host cores.
+N>1 (re-executed under torchrun when started plainly) runs the batched
+system-ID configuration C5 — 64 parameter samples of the 30k-tet mesh sharded
+over the ranks, one NCCL all-reduce of [loss, dL/dE] per evaluation — since a
+single trajectory does not shard; --replicas keeps N
+independent C3 trajectories instead.  Timing is the max over ranks.  The
+reference arm times the CPU restatement of the reference (oracle/; the
+reference itself cannot be built here: Eigen is absent) on the host cores,
+the same warm-up and timed steps from the same start state.
 """
 from __future__ import annotations
 
@@ -50,6 +54,10 @@ def parse():
     ap.add_argument("--frames", type=int, default=10, help="frames per sample trajectory (batch workload)")
     ap.add_argument("--ordering", default=None, help="factor ordering: nd-bfs (default), nd-geometric or metis")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=150.0,
+                    help="seconds the CPU-baseline child may spend on its one fwd+bwd step (C4: ~2400)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: N independent trajectories instead of the C5 batch shard")
     return ap.parse_args()
 
 
@@ -189,6 +197,10 @@ WORKLOADS = {
 
 
 def run_reference(args, scene_dict, world, rank):
+    """Reference arm: the CPU restatement of the reference (oracle/) runs the
+    GPU arm's schedule — W untimed warm-up steps from the scene's initial
+    state, then K timed fwd+bwd steps (factorization excluded, as in the GPU
+    arm) — on every host core of rank 0."""
     if rank != 0:
         return
     from paper_2605_14526_b200.hd import Library
@@ -197,15 +209,13 @@ def run_reference(args, scene_dict, world, rank):
     t_fac = time.perf_counter()
     sim = sc.sim()
     t_fac = time.perf_counter() - t_fac
-    budget = 150.0
-    warm = min(args.warmup, 1)
+    warm = max(args.warmup, 3)
     for _ in range(warm):
         sim.record(True)
         sim.step()
         sim.backward_canonical(download=False)
         sim.record(False)
     times = []
-    t_all = time.perf_counter()
     for _ in range(args.steps):
         sim.record(True)
         t0 = time.perf_counter()
@@ -213,19 +223,17 @@ def run_reference(args, scene_dict, world, rank):
         sim.backward_canonical(download=False)
         times.append(time.perf_counter() - t0)
         sim.record(False)
-        if time.perf_counter() - t_all > budget:
-            break
     total = sum(times)
     val = len(times) / total
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": len(times),
         "warmup": warm, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {scene_dict['name']}", "requested_steps": args.steps,
-                   "factorization_s": t_fac},
+        "config": {"workload": f"{args.config}: {scene_dict['name']}", "factorization_s": t_fac},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                         "sample": f"{len(times)} fwd+bwd steps (time budget {budget:.0f} s), CPU restatement of the "
-                                   f"reference (Eigen absent: reference not buildable), HETERODYN_THREADS="
+                         "sample": f"{warm} warm-up + {len(times)} timed fwd+bwd steps from the scene's initial "
+                                   f"state (the GPU arm's schedule), CPU restatement of the reference (Eigen absent: "
+                                   f"reference not buildable), HETERODYN_THREADS="
                                    f"{os.environ.get('HETERODYN_THREADS', 'all')}"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -307,9 +315,13 @@ def run_batch(args, world, rank):
     t_build = time.perf_counter() - t_build
     b.set_target(target)
     buf = torch.zeros(1 + ne, dtype=torch.float64, device="cuda")
+    def reduced():  # the all-reduce reads buf: finish it before the next evaluation writes buf
+        allreduce_loss_grad(buf)
+        torch.cuda.current_stream().synchronize()
+
     for _ in range(max(args.warmup, 3)):
         b.evaluate(args.frames, device_out=buf.data_ptr(), want_host=False)
-        allreduce_loss_grad(buf)
+        reduced()
     launches0 = b.kernel_launches
     solves0 = b.solve_count
     if world > 1:
@@ -324,7 +336,7 @@ def run_batch(args, world, rank):
     for _ in range(args.steps):
         b.evaluate(args.frames, device_out=buf.data_ptr(), want_host=False)
         dev_ms += b.last_ms
-        allreduce_loss_grad(buf)
+        reduced()
     e1.record()
     e1.synchronize()
     torch.cuda.synchronize()
@@ -347,7 +359,7 @@ def run_batch(args, world, rank):
     for _ in range(args.steps):
         b.set_target(t_h.numpy())
         r = b.evaluate(args.frames, device_out=buf.data_ptr(), want_host=True)
-        allreduce_loss_grad(buf)
+        reduced()
         host_total = buf.cpu()
     e3.record()
     e3.synchronize()
@@ -417,9 +429,28 @@ def run_batch(args, world, rank):
         dist.destroy_process_group()
 
 
+def relaunch_under_torchrun(args):
+    """--gpus N > 1 outside torchrun: re-exec this script as N ranks (one
+    process per GPU) on 127.0.0.1, the way the driver launches it."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
     world, rank, local = dist_env()
+    if world > 1 and args.workload == "trajectory" and not args.replicas:
+        # one trajectory does not shard (SURVEY.md §8(e)): the multi-GPU
+        # configuration is the batched system-ID C5 (samples sharded, NCCL
+        # all-reduce of [loss, dL/dE]); --replicas keeps N C3 trajectories
+        args.workload = "batch"
     pin_device(local, world)
     from paper_2605_14526_b200 import scenes
     if args.workload == "batch":
@@ -565,7 +596,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(scene_dict, q_start, v_start)
+            cpu = cpu_baseline(scene_dict, q_start, v_start, max_seconds=args.cpu_budget)
         except Exception as exc:  # reported, never fatal for the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
 

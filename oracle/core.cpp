@@ -27,9 +27,12 @@ int worker_count() {
 
 // common.cpp:23-41 — one std::thread per chunk on every call, like the
 // reference (its spawn cost is part of the baseline being timed).
+namespace {
+thread_local bool t_in_worker = false;  // nested parallel_for runs serially inside a worker
+}
 void parallel_for(int n, const std::function<void(int)>& fn) {
   const int workers = std::min(worker_count(), n);
-  if (workers <= 1 || n < 64) {
+  if (workers <= 1 || n < 64 || t_in_worker) {
     for (int i = 0; i < n; ++i) fn(i);
     return;
   }
@@ -38,8 +41,29 @@ void parallel_for(int n, const std::function<void(int)>& fn) {
   for (int w = 0; w < workers; ++w) {
     const int lo = w * chunk, hi = std::min(n, lo + chunk);
     if (lo >= hi) break;
-    pool.emplace_back([lo, hi, &fn] { for (int i = lo; i < hi; ++i) fn(i); });
+    pool.emplace_back([lo, hi, &fn] {
+      t_in_worker = true;
+      for (int i = lo; i < hi; ++i) fn(i);
+    });
   }
+  for (auto& t : pool) t.join();
+}
+
+// One task per index on up to worker_count() threads (dynamic assignment);
+// used for independent work items larger than an element (contact columns).
+void parallel_tasks(int n, const std::function<void(int)>& fn) {
+  const int workers = std::min(worker_count(), n);
+  if (workers <= 1 || t_in_worker) {
+    for (int i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::atomic<int> next{0};
+  std::vector<std::thread> pool;
+  for (int w = 0; w < workers; ++w)
+    pool.emplace_back([&] {
+      t_in_worker = true;
+      for (int i = next++; i < n; i = next++) fn(i);
+    });
   for (auto& t : pool) t.join();
 }
 

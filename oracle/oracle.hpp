@@ -5,6 +5,8 @@
 // bench.py's cpu_baseline leg may load the library built from this directory.
 #pragma once
 
+#include <atomic>
+
 #include <array>
 #include <cstdint>
 #include <functional>
@@ -38,6 +40,7 @@ class Error : public std::runtime_error {
 // common.cpp:9-41 — deterministic fork/join over contiguous chunks.
 int worker_count();
 void parallel_for(int n, const std::function<void(int)>& fn);
+void parallel_tasks(int n, const std::function<void(int)>& fn);
 
 // ---- vector helpers ------------------------------------------------------
 inline VecX zeros(int n) { return VecX(static_cast<size_t>(n), 0.0); }
@@ -171,7 +174,7 @@ class SparseFactor {  // factor.hpp:13-50
   double factor_millis() const { return factor_ms_; }
   long long l_nnz() const { return l_nnz_; }
   const std::vector<int>& perm() const { return perm_; }
-  mutable std::uint64_t apply_inverse_count = 0;
+  mutable std::atomic<std::uint64_t> apply_inverse_count{0};  // atomic: the oracle solves contact columns in parallel
  private:
   int n_ = 0;
   std::vector<int> perm_;

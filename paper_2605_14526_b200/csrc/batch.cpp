@@ -97,10 +97,22 @@ void Batch::evaluate(int frames, double* loss, double* grad_sum, double* device_
   const int n3 = 3 * scene_.mesh.nv;
   // frame slots are allocated up front, never while other samples' graphs run
   parallel_samples(S, threads_, device_, [&](int s) { eng_[s]->reserve_frames(frames); });
-  cudaEvent_t start, stop;
+  struct Events {  // destroyed on every exit path (a failing sample rethrows)
+    cudaEvent_t start = nullptr, stop = nullptr;
+    std::vector<cudaEvent_t> done;
+    ~Events() {
+      for (cudaEvent_t e : done)
+        if (e) cudaEventDestroy(e);
+      if (start) cudaEventDestroy(start);
+      if (stop) cudaEventDestroy(stop);
+    }
+  } ev;
+  ev.done.assign(S, nullptr);
+  cudaEvent_t& start = ev.start;
+  cudaEvent_t& stop = ev.stop;
+  std::vector<cudaEvent_t>& done = ev.done;
   cuda_check(cudaEventCreate(&start), "event");
   cuda_check(cudaEventCreate(&stop), "event");
-  std::vector<cudaEvent_t> done(S);
   for (auto& e : done) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   cuda_check(cudaEventRecord(start, st_), "event");
   for (int s = 0; s < S; ++s) cuda_check(cudaStreamWaitEvent(eng_[s]->stream(), start, 0), "wait");
@@ -130,9 +142,6 @@ void Batch::evaluate(int frames, double* loss, double* grad_sum, double* device_
   float ms = 0;
   cuda_check(cudaEventElapsedTime(&ms, start, stop), "elapsed");
   last_ms = ms;
-  cudaEventDestroy(start);
-  cudaEventDestroy(stop);
-  for (auto& e : done) cudaEventDestroy(e);
 }
 
 void Batch::set_young(const double* young, bool freeze_means) {

@@ -418,13 +418,15 @@ __global__ void __launch_bounds__(kNcpT) k_ncp(hdk_contacts c, const double* __r
   const hdk::Packed Mp{s.M, k};
   if (!bad) {
     // P M P^T, lower triangle, and the permuted right-hand side
-    for (int t = threadIdx.x; t < k * k; t += kNcpT) {
-      const int i = t % k, j = t / k;
-      if (i < j) continue;
-      const int r = s.perm[i], q = s.perm[j];
-      double m = mul(mul(s.om[r], c.W[(size_t)q * k + r]), s.om[q]);
-      if (i == j) m = add(add(m, s.ed[r]), lift);
-      Mp(i, j) = m;
+    for (int j = threadIdx.x >> 5; j < k; j += kNcpT / 32) {  // column j by one warp
+      const int q = s.perm[j];
+      const double* wq = c.W + (size_t)q * k;
+      for (int i = j + (threadIdx.x & 31); i < k; i += 32) {
+        const int r = s.perm[i];
+        double m = mul(mul(s.om[r], wq[r]), s.om[q]);
+        if (i == j) m = add(add(m, s.ed[r]), lift);
+        Mp(i, j) = m;
+      }
     }
     for (int i = threadIdx.x; i < k; i += kNcpT) s.wl[i] = s.rhs[s.perm[i]];
     __syncthreads();
@@ -499,8 +501,21 @@ __global__ void k_corrected(hdk_contacts c, const int* __restrict__ p2v, const d
   if (p >= c.n) return;
   const int nu = c.cnt[HDK_CNT_NU];
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  for (int u = 0; u < nu; ++u) {
-    const double w = c.U[(size_t)u * c.n + p];
+  const double* up = c.U + p;
+  int u = 0;
+  for (; u + 8 <= nu; u += 8) {  // eight independent column loads in flight, sums in u order
+    double w[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) w[t] = up[(size_t)(u + t) * c.n];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      s0 = add(s0, mul(w[t], c.g[3 * (u + t)]));
+      s1 = add(s1, mul(w[t], c.g[3 * (u + t) + 1]));
+      s2 = add(s2, mul(w[t], c.g[3 * (u + t) + 2]));
+    }
+  }
+  for (; u < nu; ++u) {
+    const double w = up[(size_t)u * c.n];
     s0 = add(s0, mul(w, c.g[3 * u]));
     s1 = add(s1, mul(w, c.g[3 * u + 1]));
     s2 = add(s2, mul(w, c.g[3 * u + 2]));
@@ -550,7 +565,7 @@ __global__ void __launch_bounds__(kNcpT) k_reduced(hdk_contacts c, const double*
   int bad = hdk::ldlt_pivots(k, s.diag, s.perm, s.byval, s.gsz, s.pos, s.at);
   const hdk::Packed Mp{s.M, k};
   if (!bad) {
-    for (int t = threadIdx.x; t < k * k; t += kNcpT) {
+    for (int t = threadIdx.x; t < k * k; t += kNcpT) {  // once per backward frame
       const int i = t % k, j = t / k;
       if (i < j) continue;
       const int r = s.perm[i], q = s.perm[j];

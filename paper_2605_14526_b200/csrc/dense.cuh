@@ -153,12 +153,12 @@ __device__ int ldlt_factor(Packed A) {
     }
     for (int i = j + 1 + threadIdx.x; i < k; i += blockDim.x) colj[i] = colj[i] / dj;
     __syncthreads();
-    const int m = k - j - 1;  // trailing (i, l), j < l <= i < k
-    for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
-      const int i = j + 1 + t % m, l = j + 1 + t / m;
-      if (i < l) continue;
-      double& a = A(i, l);
-      a = sub(a, mul(mul(colj[i], colj[l]), dj));
+    // trailing update, column l by one warp (round robin), rows i >= l by its lanes
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (int l = j + 1 + warp; l < k; l += nwarps) {
+      const double llj = colj[l];
+      double* coll = A.a + A.col(l);
+      for (int i = l + lane; i < k; i += 32) coll[i] = sub(coll[i], mul(mul(colj[i], llj), dj));
     }
     __syncthreads();
   }

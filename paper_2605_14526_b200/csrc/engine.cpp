@@ -1168,11 +1168,14 @@ void Engine::set_young(const Vec& young, bool freeze) {
   }
   hf_ = std::move(nf);
   // material arrays and factor live in fresh allocations; graphs bake pointers
-  Vec q = positions(), v = velocities();
+  // (the state and any f_ext set through hd_sim_set_external_force survive)
+  Vec q = positions(), v = velocities(), f(dof_count());
+  external_force_into(f.data());
   const double t = time_;
   build_static();
   build_factor_device();
   set_state(q.data(), v.data(), t);
+  set_external_force(f.data());
   slots_.clear();
   frame_mem_.clear();
   nrec_ = 0;
