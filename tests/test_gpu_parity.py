@@ -142,19 +142,6 @@ def test_ballistic_closed_form(prod):
     np.testing.assert_allclose(v[2::3], -0.06, rtol=1e-10)
 
 
-def test_c3_full_size_step(prod, orc):
-    """Full-size (103,680 tets) forward+backward step against the oracle."""
-    scene = scenes.config_scene("C3", frames=1)
-    tp, gp = run(prod, scene, 1)
-    to, go = run(orc, scene, 1)
-    (qp, vp, ip, cp), (qo, vo, io, co) = tp[0], to[0]
-    assert ip == io and cp == co  # default tolerance: counts agree exactly
-    assert rel2(qp, qo) <= 1e-6 and rel2(vp, vo) <= 1e-6
-    np.testing.assert_array_equal(gp["tau"], go["tau"])
-    for k in GRADS:
-        assert rel2(gp[k], go[k]) <= 1e-6, (k, rel2(gp[k], go[k]))
-
-
 @pytest.mark.gpu
 def test_batch_matches_oracle_and_is_deterministic(prod, orc):
     """Batched system-ID (config C5 on a small mesh): per-sample losses and the
