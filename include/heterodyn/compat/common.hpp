@@ -1,0 +1,4 @@
+// Reference include name (/root/reference/proj/src/common.hpp) for drop-in callers:
+// compile with -I include/heterodyn/compat.  Everything is declared in ../solver.hpp.
+#pragma once
+#include "../solver.hpp"

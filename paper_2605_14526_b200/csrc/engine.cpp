@@ -202,6 +202,7 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared
   }
   fgraph_ = std::make_unique<LoopGraph>();
   bgraph_ = std::make_unique<LoopGraph>();
+  eps_tr_ = scene.solver.eps_tr;
   hf_ = build_factor(scene.mesh, mat_, scene.solver.h, scene.fixed, scene.ordering, device_values_, &order_cache_);
   refactor_count = 1;
   build_static();
@@ -633,7 +634,7 @@ void Engine::build_backward_graph() {
     }
   // tr_select_tau, differential, seed and the backbone's first solve
   bpre_ = capture_exec(st_, [&] {
-    hdk_check(hdk_ctl_init(ctl_, HDK_AA_MAX, 1e8, 500, 0.0, 0.0, 1e-10, so.eps_tr, 0, s), "ctl init");
+    hdk_check(hdk_ctl_init(ctl_, HDK_AA_MAX, 1e8, 500, 0.0, 0.0, 1e-10, eps_tr_, 0, s), "ctl init");
     hdk_check(hdk_tr_model(&dv_, &a_ff_, bqstar_, bqprev_, dqp_, part_a_, s), "tr model");
     hdk_check(hdk_element_energy2(&dm_, &dmat_, bqprev_, eprev_, bqstar_, estar_, &ctl_->bad, s), "energies");
     hdk_check(hdk_tr_select(&dv_, dm_.ne, eprev_, estar_, bqprev_, bqstar_, bqtil_, 1.0 / (h * h), part_a_, part_b_,
@@ -884,9 +885,11 @@ void Engine::step() {
   phase_mark(0);
   if (contact_scene) run_contact_step();
   else run_graph(*fgraph_, "forward graph");
-  if (recording_) {
-    if (static_cast<int>(slots_.size()) <= nrec_) add_slot();
-    const Frame& fr = slots_[nrec_];
+  const bool rec = recording_ || force_slot_ >= 0;
+  const int slot = force_slot_ >= 0 ? force_slot_ : nrec_;
+  if (rec) {
+    while (static_cast<int>(slots_.size()) <= slot) add_slot();
+    const Frame& fr = slots_[slot];
     const auto cp = [&](double* d, const double* src, size_t n) {
       cuda_check(cudaMemcpyAsync(d, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st_), "record");
     };
@@ -930,8 +933,8 @@ void Engine::step() {
   last_converged = h_ctl_->converged;
   last_contacts = contact_scene ? cw_.nc : 0;
   cur_has_contacts_ = contact_scene && cw_.k > 0;
-  if (recording_) {
-    Frame& fr = slots_[nrec_];
+  if (rec) {
+    Frame& fr = slots_[slot];
     fr.has_contacts = cur_has_contacts_;
     if (cur_has_contacts_) {  // the adjoint's copy of this step's contact set
       if (!fr.contacts) fr.contacts = std::make_shared<ContactFrame>();
@@ -945,7 +948,19 @@ void Engine::step() {
     }
   }
   time_ += scene_.solver.h;
-  if (recording_) ++nrec_;
+  if (recording_ && force_slot_ < 0) ++nrec_;
+}
+
+void Engine::step_into(int slot) {
+  if (slot < 0) raise(Code::InvalidArgument, "step_into: negative frame slot");
+  force_slot_ = slot;
+  try {
+    step();
+  } catch (...) {
+    force_slot_ = -1;
+    throw;
+  }
+  force_slot_ = -1;
 }
 
 void Engine::add_slot() {
@@ -971,13 +986,13 @@ void Engine::record(bool on) {
   if (!on) nrec_ = 0;
 }
 
-void Engine::set_state(const double* q, const double* v, double time) {
+void Engine::set_state(const double* q, const double* v, double time, bool keep_frames) {
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
   if (q) cuda_check(cudaMemcpyAsync(q_, q, n3 * sizeof(double), cudaMemcpyHostToDevice, st_), "set q");
   if (v) cuda_check(cudaMemcpyAsync(v_, v, n3 * sizeof(double), cudaMemcpyHostToDevice, st_), "set v");
   cuda_check(cudaStreamSynchronize(st_), "set state");
   time_ = time;
-  nrec_ = 0;
+  if (!keep_frames) nrec_ = 0;
 }
 
 void Engine::set_external_force(const double* f) {
@@ -1045,16 +1060,7 @@ GradOut Engine::backward(const double* direct, const double* dq_final, const dou
   out.tau.assign(T, 1.0);
   out.rho.assign(T, 1.0);
   for (int t = T - 1; t >= 0; --t) {
-    const Frame& f = slots_[t];
-    const auto cp = [&](double* d, const double* s, size_t n) {
-      cuda_check(cudaMemcpyAsync(d, s, n * sizeof(double), cudaMemcpyDeviceToDevice, st_), "frame copy");
-    };
-    cp(bq_t_, f.q_t, n3);
-    cp(bv_t_, f.v_t, n3);
-    cp(bqtil_, f.qtil, n3);
-    cp(bqprev_, f.qprev, n3);
-    cp(bqstar_, f.qstar, n3);
-    cp(bcache_, f.cache, 24 * ne);
+    load_frame(t);
     if (direct) cuda_check(cudaMemcpyAsync(direct_, direct + static_cast<size_t>(t) * n3, B, cudaMemcpyHostToDevice, st_), "direct");
     backward_frame(t, out);
   }
@@ -1084,11 +1090,82 @@ GradOut Engine::backward(const double* direct, const double* dq_final, const dou
   return out;
 }
 
+void Engine::load_frame(int t) {
+  const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
+  const Frame& f = slots_[t];
+  const auto cp = [&](double* d, const double* s, size_t n) {
+    cuda_check(cudaMemcpyAsync(d, s, n * sizeof(double), cudaMemcpyDeviceToDevice, st_), "frame copy");
+  };
+  cp(bq_t_, f.q_t, n3);
+  cp(bv_t_, f.v_t, n3);
+  cp(bqtil_, f.qtil, n3);
+  cp(bqprev_, f.qprev, n3);
+  cp(bqstar_, f.qstar, n3);
+  cp(bcache_, f.cache, 24 * ne);
+}
+
+GradOut Engine::backward_slot(int slot, const double* dq_next, const double* dv_next) {
+  if (slot < 0 || slot >= static_cast<int>(slots_.size()))
+    raise(Code::InvalidArgument, "backward_step: the cache's frame slot is not recorded");
+  const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
+  const size_t B = n3 * sizeof(double);
+  const auto h2d = [&](double* d, const double* h) {
+    if (h) cuda_check(cudaMemcpyAsync(d, h, B, cudaMemcpyHostToDevice, st_), "seed upload");
+    else cuda_check(cudaMemsetAsync(d, 0, B, st_), "seed zero");
+  };
+  h2d(qbar_, dq_next);
+  h2d(vbar_, dv_next);
+  cuda_check(cudaMemsetAsync(dfacc_, 0, B, st_), "zero");
+  cuda_check(cudaMemsetAsync(dlw_, 0, 2 * ne * sizeof(double), st_), "zero");
+  cuda_check(cudaMemsetAsync(dle_, 0, ne * sizeof(double), st_), "zero");
+  cuda_check(cudaMemsetAsync(direct_, 0, B, st_), "zero");
+  GradOut out;
+  out.tau.assign(slots_.size(), 1.0);
+  out.rho.assign(slots_.size(), 1.0);
+  load_frame(slot);
+  backward_frame(slot, out);
+  out.tau = {out.tau[slot]};
+  out.rho = {out.rho[slot]};
+  out.dl_dq0.resize(n3);
+  out.dl_dv0.resize(n3);
+  out.dl_df_ext.resize(n3);
+  out.dl_de.resize(ne);
+  out.dl_dw.resize(dw_count());
+  const auto d2h = [&](double* h, const double* d, size_t n) {
+    cuda_check(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, st_), "grad download");
+  };
+  d2h(out.dl_dq0.data(), qbar_, n3);
+  d2h(out.dl_dv0.data(), vbar_, n3);
+  d2h(out.dl_df_ext.data(), dfacc_, n3);
+  d2h(out.dl_de.data(), dle_, ne);
+  d2h(out.dl_dw.data(), dlw_, dw_count());
+  cuda_check(cudaStreamSynchronize(st_), "grad download");
+  return out;
+}
+
+Vec Engine::frame_vector(int slot, int which) const {
+  if (slot < 0 || slot >= static_cast<int>(slots_.size())) raise(Code::InvalidArgument, "frame slot not recorded");
+  Vec out(dof_count());
+  const double* src = which == 0 ? slots_[slot].qtil : slots_[slot].qprev;
+  cuda_check(cudaMemcpyAsync(out.data(), src, out.size() * sizeof(double), cudaMemcpyDeviceToHost, st_), "frame read");
+  cuda_check(cudaStreamSynchronize(st_), "frame read");
+  return out;
+}
+
+void Engine::set_eps_tr(double eps_tr) {
+  if (eps_tr == eps_tr_) return;
+  eps_tr_ = eps_tr;
+  cuda_check(cudaStreamSynchronize(st_), "sync");
+  build_backward_graph();
+}
+
 Vec Engine::solve_free(const double* rhs, const double* fixed_q) {
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
-  cuda_check(cudaMemcpy(seed_, rhs, n3 * sizeof(double), cudaMemcpyHostToDevice), "rhs");
-  if (fixed_q) cuda_check(cudaMemcpy(t_, fixed_q, n3 * sizeof(double), cudaMemcpyHostToDevice), "fixed q");
-  else cuda_check(cudaMemset(t_, 0, n3 * sizeof(double)), "fixed q");
+  // on the engine's (non-blocking) stream: the legacy-stream cudaMemcpy would
+  // not order against it
+  cuda_check(cudaMemcpyAsync(seed_, rhs, n3 * sizeof(double), cudaMemcpyHostToDevice, st_), "rhs");
+  if (fixed_q) cuda_check(cudaMemcpyAsync(t_, fixed_q, n3 * sizeof(double), cudaMemcpyHostToDevice, st_), "fixed q");
+  else cuda_check(cudaMemsetAsync(t_, 0, n3 * sizeof(double), st_), "fixed q");
   hdk_check(hdk_gather_perm(&dv_, seed_, nullptr, rhs_, st_), "rhs gather");
   if (!hf_.fixed.empty()) {
     hdk_check(hdk_fixed_coupling(&a_fd_, d_fixed_, t_, fixc_, st_), "coupling");

@@ -121,7 +121,24 @@ class Engine {
   void record(bool on);
   void reserve_frames(int frames);  // allocate recorded-frame slots ahead of time
   int recorded() const { return nrec_; }
-  void set_state(const double* q, const double* v, double time);
+  // keep_frames: recorded frames stay valid (the C++ solver API sets the
+  // state of every step from the caller's SimState)
+  void set_state(const double* q, const double* v, double time, bool keep_frames = false);
+  // One forward step recorded into frame slot `slot` (allocated on demand)
+  // instead of the append position: the C++ solver API's ForwardCache owns a
+  // slot until it is destroyed (solver_api.cpp).
+  void step_into(int slot);
+  // backward_step (backward.cpp:396-414) for the frame in `slot` alone, seeded
+  // with dL/dq_{t+1}, dL/dv_{t+1} (host, NULL = zero); GradOut holds the step's
+  // input gradients (dl_dq0/dl_dv0 = dL/dq_t, dL/dv_t), tau/rho one entry.
+  GradOut backward_slot(int slot, const double* dl_dq_next, const double* dl_dv_next);
+  // trust-region band of the adjoint (SolverConfig::eps_tr); re-captures the
+  // backward graphs when it changes
+  void set_eps_tr(double eps_tr);
+  double eps_tr() const { return eps_tr_; }
+  int slot_count() const { return static_cast<int>(slots_.size()); }
+  // host copy of a recorded frame's q~ (which = 0) or next-to-last iterate (1)
+  Vec frame_vector(int slot, int which) const;
   void set_external_force(const double* f);  // dof doubles into the device f_ext the graphs read
   void external_force_into(double* out) const;
   double last_fb_residual() const;  // max |FB residual| over the last step's normal contacts
@@ -210,6 +227,7 @@ class Engine {
   void build_backward_graph();
   void run_graph(LoopGraph& g, const char* what);
   void backward_frame(int t, GradOut& out);
+  void load_frame(int t);  // frame slot t into the backward working buffers
   void sync_ctl();
   void check_ctl(const char* what);
 
@@ -274,6 +292,8 @@ class Engine {
   std::vector<std::unique_ptr<DevArena>> frame_mem_;
   int nrec_ = 0;
   bool recording_ = false;
+  int force_slot_ = -1;  // step_into: the slot this step records into
+  double eps_tr_ = 0.1;
   int aa_window_ = 1;
 
   double* rest_ = nullptr;  // rest positions (canonical loss seed)
