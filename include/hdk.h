@@ -40,6 +40,12 @@ typedef struct hdk_material {
   const double* lambda_e;
   const double* beta_vh;  /* beta_e V / h, or NULL when beta0 == 0 */
   const double* vol;      /* rest volumes */
+  /* Segmented batch (lockstep C5 engine): seg_ne elements per sample; the
+   * prox means of sample s are seg_means[3 s .. 3 s + 2] (mu, lambda, k),
+   * and hdk_differential reads sample s's tau at tau[s * tau_stride].
+   * seg_means == NULL: the scalars above, one tau. */
+  const double* seg_means;
+  int seg_ne, tau_stride;
 } hdk_material;
 
 /* Explicit inverse factor A^{-1} = S'^T S' in postordered elimination order.
@@ -483,6 +489,63 @@ HDK_API int hdk_bb_columns_solve(const hdk_bb_columns* c, void* stream);
 HDK_API int hdk_bb_columns_bapply(const hdk_mesh* m, const double* dcomp, const hdk_bb_columns* c, void* stream);
 HDK_API int hdk_bb_columns_gather(const hdk_vtx* x, const hdk_bb_columns* c, void* stream);
 HDK_API int hdk_bb_columns_mix(const hdk_bb_columns* c, void* stream);
+
+/* ---- segmented batch (lockstep C5 engine, engine.cpp segments > 1) --------
+ * S samples of one mesh as one concatenated problem: sample s owns vertices
+ * [s nv, (s+1) nv), elements [s ne, (s+1) ne) and elimination positions
+ * [s n, (s+1) n) (the factor is block diagonal).  Element- and vertex-
+ * parallel kernels run on the concatenation unchanged; these launchers are
+ * the per-sample reductions and loop control: grid (HDK_SEG_RB, S), sample in
+ * blockIdx.y, one hdk_ctl per sample, partials at partial + s HDK_SEG_PSTRIDE
+ * (folded over HDK_SEG_RB blocks; the 18-quantity Anderson partials are
+ * quantity-major over HDK_RED_BLOCKS and their unused slots must be zero).
+ * A sample whose loop has ended (ctl[s].cond == 0) is skipped, so each
+ * sample stops at its own iteration count; `any` (device int) is the OR over
+ * the samples, which drives the WHILE node and the solve passes' run flag. */
+#define HDK_SEG_RB 16
+#define HDK_SEG_PSTRIDE (HDK_RED_BLOCKS * HDK_RED_Q)
+typedef struct hdk_segs {
+  int count;   /* samples */
+  int nv, n, ne;  /* per sample: vertices, free vertices, elements */
+} hdk_segs;
+HDK_API int hdk_seg_ctl_init(hdk_ctl* ctl, const hdk_segs* g, const int* windows, double guard, int k_max,
+                             double eps_rel, double eps_abs, double tol, double eps_tr, int* any, void* stream);
+HDK_API int hdk_seg_aa_reset(hdk_ctl* ctl, const hdk_segs* g, int window, double guard, int k_max, double tol,
+                             int* any, void* stream);
+HDK_API int hdk_seg_gather_rhs(const hdk_vtx* x, const hdk_segs* g, const hdk_ctl* ctl, const double* ef,
+                               double inv_h2, const double* q_tilde, const double* damp, double* b_prev,
+                               double* rhs_perm, double* partial, void* stream);
+HDK_API int hdk_seg_aa_dots_fused(const hdk_vtx* x, const hdk_factor* f, const hdk_segs* g, hdk_ctl* ctl,
+                                  double* qhat, const double* qcur, double* last_q, double* last_g, double* dq,
+                                  double* dg, double* partial18, unsigned int* tickets, void* stream);
+HDK_API int hdk_seg_aa_mix(const hdk_vtx* x, const hdk_segs* g, hdk_ctl* ctl, const double* qhat, double* qcur,
+                           double* qprev, const double* dq, const double* dg, double* partial, void* stream);
+HDK_API int hdk_seg_gate(hdk_ctl* ctl, const hdk_segs* g, const double* partial_b, const double* partial_q, int* any,
+                         unsigned int* ticket, unsigned long long cond_handle, void* stream);
+HDK_API int hdk_seg_commit(const hdk_segs* g, const hdk_ctl* ctl, const double* q_star, double h, double* q, double* v,
+                           void* stream);
+HDK_API int hdk_seg_tr_model(const hdk_vtx* x, const hdk_segs* g, const hdk_csr* a_ff, const double* q_star,
+                             const double* q_prev, double* dq_perm, double* partial, void* stream);
+HDK_API int hdk_seg_tr_select(const hdk_vtx* x, const hdk_segs* g, const double* e_prev, const double* e_star,
+                              const double* q_prev, const double* q_star, const double* q_tilde, double inv_h2,
+                              const double* model_partial, double* partial, hdk_ctl* ctl, void* stream);
+HDK_API int hdk_seg_bb_dots(const hdk_factor* f, const hdk_segs* g, hdk_ctl* ctl, hdk_ctl* snap, double* t_perm,
+                            double* t_full, const double* x_perm, double* last_q, double* last_g, double* dq,
+                            double* dg, double* partial18, void* stream);
+HDK_API int hdk_seg_bb_solve(hdk_ctl* ctl, const hdk_segs* g, const hdk_ctl* snap, const double* partial18,
+                             void* results, void* stream);
+HDK_API int hdk_seg_bb_mix(const hdk_factor* f, const hdk_segs* g, hdk_ctl* ctl, const hdk_ctl* snap,
+                           const void* results, const double* t_perm, double* x_perm, double* x_full,
+                           const double* sum_hist, const double* rt_perm, double* rx_perm, double* last_rx,
+                           double* last_rg, double* rsum_hist, const double* seed_perm, double* rhs_perm,
+                           void* stream);
+/* any = OR over the samples of "still iterating" (cond, no error, finite);
+ * sets the WHILE condition when cond_handle != 0. */
+HDK_API int hdk_seg_any(const hdk_ctl* ctl, const hdk_segs* g, int* any, unsigned long long cond_handle, void* stream);
+/* out[s] = 1/2 |q_s - ref_s|^2 per sample (3 nv doubles each). */
+HDK_API int hdk_seg_half_sqdist(const hdk_segs* g, const double* q, const double* ref, double* out, void* stream);
+/* out[0] = sum_s loss[s]; out[1 + i] = sum_s vec[s ne + i], in sample order. */
+HDK_API int hdk_seg_sum(const hdk_segs* g, const double* vec, const double* loss, double* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -2,6 +2,8 @@
 #include "batch.hpp"
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <atomic>
 #include <exception>
 #include <mutex>
@@ -52,6 +54,20 @@ Batch::Batch(const Scene& scene, int samples, const double* young, int threads, 
   if (!scene.obstacles.empty())
     raise(Code::InvalidArgument, "hd_batch_create: batched system-ID runs contact-free scenes (config C5)");
   cuda_check(cudaGetDevice(&device_), "get device");
+  samples_ = samples;
+  const char* mode = std::getenv("HETERODYN_BATCH");
+  const bool streams = (mode && std::string(mode) == "streams") || !scene.fixed.empty() || scene.hook;
+  if (!streams) {  // all samples in one segmented engine
+    seg_scene_ = std::make_unique<Scene>(make_segmented_scene(scene, samples, young));
+    lock_ = std::make_unique<Engine>(*seg_scene_, nullptr, solve_ctas, false, samples);
+    st_ = lock_->stream();
+    const size_t n3 = 3 * static_cast<size_t>(scene.mesh.nv) * samples;
+    cuda_check(cudaMalloc(&target_, n3 * sizeof(double)), "target");
+    cuda_check(cudaMemcpy(target_, seg_scene_->q0.data(), n3 * sizeof(double), cudaMemcpyHostToDevice), "target");
+    cuda_check(cudaMalloc(&loss_, samples * sizeof(double)), "loss");
+    cuda_check(cudaMalloc(&out_, (1 + static_cast<size_t>(scene.mesh.ne)) * sizeof(double)), "out");
+    return;
+  }
   threads_ = std::max(1, std::min(threads, samples));
   // Several samples' solves share the SMs: cap each pass at a quarter wave
   // (measured on C5: 975 ms -> 778 ms per 64 x 10-frame evaluation).
@@ -83,16 +99,23 @@ Batch::~Batch() {
   for (void* p : {static_cast<void*>(target_), static_cast<void*>(loss_), static_cast<void*>(out_),
                   static_cast<void*>(grads_)})
     if (p) cudaFree(p);
-  if (st_) cudaStreamDestroy(st_);
+  if (st_ && !lock_) cudaStreamDestroy(st_);  // lockstep: the engine's stream
+  lock_.reset();
 }
 
 void Batch::set_target(const double* q) {
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
-  cuda_check(cudaMemcpy(target_, q, n3 * sizeof(double), cudaMemcpyHostToDevice), "target");
+  const int copies = lock_ ? samples_ : 1;  // lockstep: one copy per sample
+  for (int k = 0; k < copies; ++k)
+    cuda_check(cudaMemcpy(target_ + k * n3, q, n3 * sizeof(double), cudaMemcpyHostToDevice), "target");
 }
 
 void Batch::evaluate(int frames, double* loss, double* grad_sum, double* device_out) {
   if (frames < 1) raise(Code::InvalidArgument, "hd_batch_evaluate: frames must be >= 1");
+  if (lock_) {
+    evaluate_lockstep(frames, loss, grad_sum, device_out);
+    return;
+  }
   const int S = samples(), ne = scene_.mesh.ne;
   const int n3 = 3 * scene_.mesh.nv;
   // frame slots are allocated up front, never while other samples' graphs run
@@ -144,8 +167,49 @@ void Batch::evaluate(int frames, double* loss, double* grad_sum, double* device_
   last_ms = ms;
 }
 
+void Batch::evaluate_lockstep(int frames, double* loss, double* grad_sum, double* device_out) {
+  Engine& e = *lock_;
+  const int ne = scene_.mesh.ne;
+  const hdk_segs& g = e.segs();
+  e.reserve_frames(frames);
+  struct Events {
+    cudaEvent_t start = nullptr, stop = nullptr;
+    ~Events() {
+      if (start) cudaEventDestroy(start);
+      if (stop) cudaEventDestroy(stop);
+    }
+  } ev;
+  cuda_check(cudaEventCreate(&ev.start), "event");
+  cuda_check(cudaEventCreate(&ev.stop), "event");
+  cuda_check(cudaEventRecord(ev.start, st_), "event");
+  e.reset_state();
+  e.record(false);
+  e.record(true);
+  for (int f = 0; f < frames; ++f) e.step();
+  hdk_check_b(hdk_seg_half_sqdist(&g, e.d_positions(), target_, loss_, st_), "loss");
+  e.backward(nullptr, nullptr, nullptr, true, false, target_);  // L_s = 1/2 |q_T,s - q_target|^2 seeds
+  e.record(false);
+  hdk_check_b(hdk_seg_sum(&g, e.d_dl_de(), loss_, out_, st_), "batch sum");
+  own_launches_ += 2;
+  if (device_out)
+    cuda_check(cudaMemcpyAsync(device_out, out_, (1 + static_cast<size_t>(ne)) * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st_), "device out");
+  cuda_check(cudaEventRecord(ev.stop, st_), "event");
+  if (loss) cuda_check(cudaMemcpyAsync(loss, loss_, samples_ * sizeof(double), cudaMemcpyDeviceToHost, st_), "loss out");
+  if (grad_sum)
+    cuda_check(cudaMemcpyAsync(grad_sum, out_ + 1, ne * sizeof(double), cudaMemcpyDeviceToHost, st_), "grad out");
+  cuda_check(cudaStreamSynchronize(st_), "batch sync");
+  float ms = 0;
+  cuda_check(cudaEventElapsedTime(&ms, ev.start, ev.stop), "elapsed");
+  last_ms = ms;
+}
+
 void Batch::set_young(const double* young, bool freeze_means) {
   const int ne = scene_.mesh.ne;
+  if (lock_) {
+    lock_->set_young(Vec(young, young + static_cast<size_t>(ne) * samples_), freeze_means);
+    return;
+  }
   parallel_samples(samples(), threads_, device_, [&](int s) {
     const Vec y(young + static_cast<size_t>(s) * ne, young + static_cast<size_t>(s + 1) * ne);
     eng_[s]->set_young(y, freeze_means);
@@ -153,17 +217,23 @@ void Batch::set_young(const double* young, bool freeze_means) {
 }
 
 long long Batch::solve_count() const {
+  if (lock_) return lock_->solve_count * samples_;  // every lockstep solve streams all samples' factors
   long long k = 0;
   for (const auto& e : eng_) k += e->solve_count;
   return k;
 }
 
 double Batch::solve_bytes() const {
+  if (lock_) {  // one sample's share of the block-diagonal stream
+    const HostFactor& F = lock_->factor();
+    return (16.0 * static_cast<double>(F.row_off.back()) + 96.0 * F.n) / samples_;
+  }
   const HostFactor& F = eng_.front()->factor();
   return 16.0 * static_cast<double>(F.row_off.back()) + 96.0 * F.n;
 }
 
 long long Batch::kernel_launches() const {
+  if (lock_) return own_launches_ + lock_->kernel_launches;
   long long k = own_launches_;
   for (const auto& e : eng_) k += e->kernel_launches;
   return k;

@@ -1,8 +1,11 @@
 // Batched system-ID evaluation: one GPU's
-// share of a batch of material-parameter samples.  Each sample owns a
-// device-resident engine (its own factor: a per-sample E is a per-sample A)
-// on its own CUDA stream; host worker threads drive the samples concurrently
-// so their latency-bound iterations overlap on the device.  One evaluation is
+// share of a batch of material-parameter samples.  Default (lockstep): all
+// samples are one segmented engine (engine_seg.cpp) — concatenated index
+// spaces, one block-diagonal factor stream, per-sample loop control — so
+// every kernel processes all of the GPU's samples in one launch.  Scenes the
+// segmented engine does not take (contact, Dirichlet vertices, hooks) and
+// HETERODYN_BATCH=streams use one engine per sample on its own CUDA stream,
+// driven concurrently by host worker threads.  One evaluation is
 // the reference's identify objective for every sample (run_identify,
 // drivers.cpp:848-851; roll + chain_backward, drivers.cpp:31-99):
 //   L_s = 1/2 |q_T(E_s) - q_target|^2,  dL_s/dE_s  (per element)
@@ -24,7 +27,7 @@ class Batch {
   Batch(const Batch&) = delete;
   Batch& operator=(const Batch&) = delete;
 
-  int samples() const { return static_cast<int>(eng_.size()); }
+  int samples() const { return samples_; }
   void set_target(const double* q_target);
   // New per-sample Young's moduli (samples x element_count): every sample
   // refactors (Engine::set_young), in parallel over the host threads.
@@ -34,14 +37,21 @@ class Batch {
   // element_count doubles on this device) receives [sum L, sum dL/dE].
   void evaluate(int frames, double* loss, double* grad_sum, double* device_out);
   long long kernel_launches() const;
+  void evaluate_lockstep(int frames, double* loss, double* grad_sum, double* device_out);
   long long solve_count() const;      // 3-axis global solves over all samples so far
   double solve_bytes() const;         // algorithmic bytes of one solve of one sample (16 nnz(S') + 96 n)
   cudaStream_t stream() const { return st_; }
+  bool lockstep() const { return lock_ != nullptr; }
+  // lockstep: sum over samples of their own (fwd + adjoint) iteration counts
+  long long sample_iterations() const { return lock_ ? lock_->seg_sample_iterations : solve_count(); }
   double last_ms = 0;  // device-side duration of the last evaluate (max over sample streams)
 
  private:
   const Scene& scene_;
   std::vector<std::unique_ptr<Engine>> eng_;
+  std::unique_ptr<Scene> seg_scene_;  // lockstep: the concatenated scene (outlives lock_)
+  std::unique_ptr<Engine> lock_;
+  int samples_ = 0;
   int threads_ = 1, device_ = 0;
   cudaStream_t st_ = nullptr;
   double* target_ = nullptr;   // 3 nv

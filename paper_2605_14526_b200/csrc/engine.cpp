@@ -179,8 +179,16 @@ void build_seq_graph(cudaStream_t st, bool use_cond, std::vector<SeqGraph::Seg> 
   out.segs = std::move(segs);
 }
 
-Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared_device)
-    : scene_(scene), mat_(scene.material), solve_ctas_(solve_ctas), branch_(!shared_device) {
+Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared_device, int segments)
+    : scene_(scene), mat_(scene.material), solve_ctas_(solve_ctas), branch_(!shared_device), segs_(segments) {
+  if (segs_ < 1) raise(Code::InvalidArgument, "engine: segments must be >= 1");
+  if (segs_ > 1) {
+    if (!scene.obstacles.empty() || !scene.fixed.empty() || scene.hook || young)
+      raise(Code::InvalidArgument, "segmented batch: contact-free scenes without Dirichlet vertices or hooks");
+    if (scene.mesh.nv % segs_ || scene.mesh.ne % segs_ ||
+        mat_.seg_means.size() != 3 * static_cast<size_t>(segs_))
+      raise(Code::InvalidArgument, "segmented batch: the scene is not make_segmented_scene's");
+  }
   if (const char* br = std::getenv("HETERODYN_BRANCH")) branch_ = std::atoi(br) != 0;
   if (const char* dv = std::getenv("HETERODYN_HOST_FACTOR_VALUES")) device_values_ = std::atoi(dv) == 0;
   if (const char* c = std::getenv("HETERODYN_SOLVE_CTAS")) solve_ctas_ = std::atoi(c);
@@ -195,7 +203,7 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared
   cuda_check(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "stream");
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
-  cuda_check(cudaMallocHost(&h_ctl_, sizeof(hdk_ctl)), "pinned ctl");
+  cuda_check(cudaMallocHost(&h_ctl_, sizeof(hdk_ctl) * segs_), "pinned ctl");
   if (const char* pe = std::getenv("HETERODYN_PHASES"); pe && std::atoi(pe) != 0) {
     ph_.on = true;
     for (cudaEvent_t& e : ph_.ev) cuda_check(cudaEventCreate(&e), "phase event");
@@ -203,6 +211,26 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared
   fgraph_ = std::make_unique<LoopGraph>();
   bgraph_ = std::make_unique<LoopGraph>();
   eps_tr_ = scene.solver.eps_tr;
+  if (segs_ > 1) {
+    // the fill-reducing order of one copy, repeated per copy: the factor of
+    // the block-diagonal operator is then block diagonal in sample order
+    const int nvs = scene.mesh.nv / segs_, nes = scene.mesh.ne / segs_;
+    Mesh m1;
+    m1.nv = nvs;
+    m1.ne = nes;
+    m1.rest.assign(scene.mesh.rest.begin(), scene.mesh.rest.begin() + 3 * nvs);
+    m1.el.assign(scene.mesh.el.begin(), scene.mesh.el.begin() + nes);
+    m1.bm.assign(scene.mesh.bm.begin(), scene.mesh.bm.begin() + 9 * nes);
+    m1.vol.assign(scene.mesh.vol.begin(), scene.mesh.vol.begin() + nes);
+    m1.mass.assign(scene.mesh.mass.begin(), scene.mesh.mass.begin() + nvs);
+    Material a1 = mat_;
+    for (Vec* v : {&a1.young, &a1.mu, &a1.lambda, &a1.beta}) v->resize(nes);
+    std::vector<int> ord1;
+    build_factor(m1, a1, scene.solver.h, {}, scene.ordering, true, &ord1);
+    order_cache_.resize(static_cast<size_t>(nvs) * segs_);
+    for (int k = 0; k < segs_; ++k)
+      for (int p = 0; p < nvs; ++p) order_cache_[static_cast<size_t>(k) * nvs + p] = k * nvs + ord1[p];
+  }
   hf_ = build_factor(scene.mesh, mat_, scene.solver.h, scene.fixed, scene.ordering, device_values_, &order_cache_);
   refactor_count = 1;
   build_static();
@@ -305,13 +333,25 @@ void Engine::build_static() {
   lastg_ = A.alloc<double>(n3);
   dq_ = A.alloc<double>(HDK_AA_MAX * n3);
   dg_ = A.alloc<double>(HDK_AA_MAX * n3);
-  part_a_ = A.alloc<double>(HDK_RED_BLOCKS * HDK_RED_Q);
-  part_b_ = A.alloc<double>(HDK_RED_BLOCKS * HDK_RED_Q);
-  part_c_ = A.alloc<double>(HDK_RED_BLOCKS * HDK_RED_Q);
+  part_a_ = A.alloc<double>(static_cast<size_t>(HDK_SEG_PSTRIDE) * segs_);
+  part_b_ = A.alloc<double>(static_cast<size_t>(HDK_SEG_PSTRIDE) * segs_);
+  part_c_ = A.alloc<double>(static_cast<size_t>(HDK_SEG_PSTRIDE) * segs_);
   cache_ = A.alloc<double>(24 * ne);
-  ctl_ = A.alloc<hdk_ctl>(1);
-  ticket_ = A.alloc<unsigned int>(1);
-  snap_ = A.alloc<hdk_ctl>(1);
+  ctl_ = A.alloc<hdk_ctl>(segs_);
+  ticket_ = A.alloc<unsigned int>(segs_);
+  snap_ = A.alloc<hdk_ctl>(segs_);
+  if (segs_ > 1) {
+    part18_ = A.alloc<double>(static_cast<size_t>(HDK_SEG_PSTRIDE) * segs_);
+    cuda_check(cudaMemset(part18_, 0, sizeof(double) * HDK_SEG_PSTRIDE * segs_), "zero partials");
+    any_ = A.alloc<int>(1);
+    gate_ticket_ = A.alloc<unsigned int>(1);
+    cuda_check(cudaMemset(gate_ticket_, 0, sizeof(unsigned int)), "zero ticket");
+    seg_windows_ = A.alloc<int>(2 * static_cast<size_t>(segs_));
+    seg_means_dev_ = A.alloc<double>(3 * static_cast<size_t>(segs_));
+  }
+  dseg_.count = segs_;  // (a single problem is one segment for the hdk_seg_* loss / sum kernels)
+  dseg_.nv = m.nv / segs_;
+  dseg_.ne = m.ne / segs_;
   seed_ = A.alloc<double>(n3);
   x_ = A.alloc<double>(n3);
   t_ = A.alloc<double>(n3);
@@ -339,6 +379,7 @@ void Engine::build_static() {
   dmat_.w2 = A.alloc<double>(ne);
   dmat_.mu_e = A.alloc<double>(ne);
   dmat_.lambda_e = A.alloc<double>(ne);
+  cuda_check(cudaMemset(ticket_, 0, sizeof(unsigned int) * segs_), "zero tickets");
   dmat_.beta_vh = mat_.beta0 > 0 ? A.alloc<double>(ne) : nullptr;
   dmat_.vol = A.upload(m.vol);
   upload_material();
@@ -393,6 +434,23 @@ void Engine::upload_material() {
   if (dmat_.beta_vh) put(dmat_.beta_vh, bvh);
   aa_window_ = scene_.solver.aa_window > 0 ? scene_.solver.aa_window : (mat_.contrast() > 10.0 ? 1 : 5);
   aa_window_ = std::min(aa_window_, HDK_AA_MAX);
+  if (segs_ > 1) {  // per-sample prox means and Anderson windows (each copy's own weight contrast)
+    put(seg_means_dev_, mat_.seg_means);
+    dmat_.seg_means = seg_means_dev_;
+    dmat_.seg_ne = dseg_.ne;
+    dmat_.tau_stride = static_cast<int>(sizeof(hdk_ctl) / sizeof(double));
+    std::vector<int> win(2 * static_cast<size_t>(segs_), HDK_AA_MAX);
+    for (int k = 0; k < segs_; ++k) {
+      double lo = mat_.weight(k * dseg_.ne), hi = lo;
+      for (int e = k * dseg_.ne; e < (k + 1) * dseg_.ne; ++e) {
+        lo = std::min(lo, mat_.weight(e));
+        hi = std::max(hi, mat_.weight(e));
+      }
+      const int w = scene_.solver.aa_window > 0 ? scene_.solver.aa_window : (hi / lo > 10.0 ? 1 : 5);
+      win[k] = std::min(w, HDK_AA_MAX);
+    }
+    DevArena::copy_h2d(seg_windows_, win.data(), win.size() * sizeof(int));
+  }
 }
 
 // S' values of hf_ into the existing stream buffer (device build when the
@@ -572,6 +630,14 @@ void Engine::build_factor_device() {
   }
   seedp_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
   xp_ = A.alloc<double>(3 * static_cast<size_t>(F.n));
+  dseg_.n = F.n / segs_;
+  if (segs_ > 1) {  // the postordered elimination order must keep every sample's block contiguous
+    const int ns = F.n / segs_, nvs = scene_.mesh.nv / segs_;
+    bool ok = F.n % segs_ == 0;
+    for (int p = 0; ok && p < F.n; ++p) ok = F.p2v[p] / nvs == p / ns;
+    if (!ok) raise(Code::InvalidArgument, "segmented batch: elimination order mixes samples");
+    dseg_.n = ns;
+  }
   {
     const size_t n3p = 3 * static_cast<size_t>(F.n);
     rt_ = A.alloc<double>(n3p);
@@ -580,11 +646,15 @@ void Engine::build_factor_device() {
     lrg_ = A.alloc<double>(n3p);
     rsq_ = A.alloc<double>(HDK_AA_MAX * n3p);
     tv_ = A.alloc<double>(3 * static_cast<size_t>(scene_.mesh.nv));
-    aares_ = A.raw(hdk_bb_result_bytes());
+    aares_ = A.raw(hdk_bb_result_bytes() * segs_);
   }
 }
 
 void Engine::build_forward_graph() {
+  if (segs_ > 1) {
+    build_forward_graph_seg();
+    return;
+  }
   const Solver& so = scene_.solver;
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
   const double h = so.h;
@@ -620,6 +690,10 @@ void Engine::build_forward_graph() {
 }
 
 void Engine::build_backward_graph() {
+  if (segs_ > 1) {
+    build_backward_graph_seg();
+    return;
+  }
   const Solver& so = scene_.solver;
   const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
   const double h = so.h;
@@ -844,7 +918,7 @@ void Engine::trace_loop(std::vector<double>& out) {
 }
 
 void Engine::sync_ctl() {
-  cuda_check(cudaMemcpyAsync(h_ctl_, ctl_, sizeof(hdk_ctl), cudaMemcpyDeviceToHost, st_), "ctl read");
+  cuda_check(cudaMemcpyAsync(h_ctl_, ctl_, sizeof(hdk_ctl) * segs_, cudaMemcpyDeviceToHost, st_), "ctl read");
   cuda_check(cudaStreamSynchronize(st_), "stream sync");
 }
 
@@ -858,16 +932,18 @@ void Engine::run_graph(LoopGraph& g, const char* what) {
   for (;;) {
     cuda_check(cudaGraphLaunch(g.body, st_), what);
     sync_ctl();
-    if (!h_ctl_->cond) break;
+    if (segs_ > 1 ? !host_any() : !h_ctl_->cond) break;
   }
   if (g.post) cuda_check(cudaGraphLaunch(g.post, st_), what);
 }
 
 void Engine::check_ctl(const char* what) {
-  if (h_ctl_->err == 0 && h_ctl_->nonfinite) h_ctl_->err = 10;  // non-finite backbone iterate
-  if (h_ctl_->err != 0) {
-    const int c = h_ctl_->err;
-    std::string msg = std::string(what) + ": ";
+  for (int k = 0; k < segs_; ++k) {
+    hdk_ctl* hc = h_ctl_ + k;
+    if (hc->err == 0 && hc->nonfinite) hc->err = 10;  // non-finite backbone iterate
+    if (hc->err == 0) continue;
+    const int c = hc->err;
+    std::string msg = std::string(what) + (segs_ > 1 ? " (sample " + std::to_string(k) + ")" : std::string()) + ": ";
     switch (c) {
       case 6: msg += "local stretch solve did not reach stationarity"; break;
       case 7: msg += "filtered prox Hessian is numerically singular"; break;
@@ -900,7 +976,8 @@ void Engine::step() {
     cp(fr.qstar, qcur_, n3);
     cp(fr.cache, cache_, 24 * ne);
   }
-  hdk_check(hdk_commit(static_cast<int>(n3), ctl_, qcur_, scene_.solver.h, q_, v_, st_), "commit");
+  if (segs_ > 1) hdk_check(hdk_seg_commit(&dseg_, ctl_, qcur_, scene_.solver.h, q_, v_, st_), "commit");
+  else hdk_check(hdk_commit(static_cast<int>(n3), ctl_, qcur_, scene_.solver.h, q_, v_, st_), "commit");
   phase_mark(1);
   if (contact_scene)
     cuda_check(cudaMemcpyAsync(h_cnt_, cw_.view.cnt, sizeof(int) * HDK_CNT_INTS, cudaMemcpyDeviceToHost, st_),
@@ -913,7 +990,17 @@ void Engine::step() {
     return;
   }
   phase_collect(0, 1);
-  const int iters = h_ctl_->iterations;
+  int iters = h_ctl_->iterations;
+  if (segs_ > 1) {  // lockstep: the loop ran until the slowest sample finished
+    seg_iterations.resize(segs_);
+    seg_converged.resize(segs_);
+    for (int k = 0; k < segs_; ++k) {
+      seg_iterations[k] = h_ctl_[k].iterations;
+      seg_converged[k] = h_ctl_[k].converged;
+      iters = std::max(iters, h_ctl_[k].iterations);
+      seg_sample_iterations += h_ctl_[k].iterations;
+    }
+  }
   if (contact_scene) {
     cw_.nc = h_cnt_[HDK_CNT_NC];
     cw_.nf = h_cnt_[HDK_CNT_NF];
@@ -931,6 +1018,7 @@ void Engine::step() {
   check_ctl("forward step");
   last_iterations = iters;
   last_converged = h_ctl_->converged;
+  for (int k = 1; k < segs_; ++k) last_converged = last_converged && h_ctl_[k].converged;
   last_contacts = contact_scene ? cw_.nc : 0;
   cur_has_contacts_ = contact_scene && cw_.k > 0;
   if (rec) {
@@ -1213,7 +1301,8 @@ bool same_structure(const HostFactor& a, const HostFactor& b) {
 
 void Engine::set_young(const Vec& young, bool freeze) {
   if (freeze) mat_.freeze();
-  mat_.set_young(young, scene_.mesh.vol);
+  if (segs_ > 1) segmented_set_young(mat_, young, scene_.mesh.vol, segs_);
+  else mat_.set_young(young, scene_.mesh.vol);
   cuda_check(cudaStreamSynchronize(st_), "sync");
   HostFactor nf = build_factor(scene_.mesh, mat_, scene_.solver.h, scene_.fixed, scene_.ordering, device_values_,
                                &order_cache_, &hf_);

@@ -112,7 +112,11 @@ class Engine {
   // solve_ctas: cap on the CTAs of each solve pass (0 = one resident wave).
   // shared_device: other engines run concurrently on the device (a batch's
   // samples): the backbone then stays on one stream.
-  explicit Engine(const Scene& scene, const Vec* young = nullptr, int solve_ctas = 0, bool shared_device = false);
+  // segments > 1: `scene` is a lockstep batch of that many copies of one mesh
+  // (make_segmented_scene): one block-diagonal factor, per-sample loop
+  // control (hdk_seg_*), every sample stopping at its own iteration count.
+  explicit Engine(const Scene& scene, const Vec* young = nullptr, int solve_ctas = 0, bool shared_device = false,
+                  int segments = 1);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -208,6 +212,12 @@ class Engine {
   double time() const { return time_; }
   int dofs() const { return 3 * mesh().nv; }
   int last_iterations = 0, last_converged = 0, last_contacts = 0;
+  int segments() const { return segs_; }
+  const hdk_segs& segs() const { return dseg_; }
+  std::vector<int> seg_iterations;   // segmented batch: forward iterations of the last step, per sample
+  std::vector<int> seg_converged;
+  std::vector<double> seg_tau;       // segmented batch: tau of the last backward frame, per sample
+  long long seg_sample_iterations = 0;  // sum over samples of their own iteration counts (fwd solves + adjoint)
   long long solve_count = 0, a_spmv_count = 0, refactor_count = 0, kernel_launches = 0;
   const HostFactor& factor() const { return hf_; }
   const Mesh& mesh() const { return scene_.mesh; }
@@ -227,6 +237,11 @@ class Engine {
   void build_backward_graph();
   void run_graph(LoopGraph& g, const char* what);
   void backward_frame(int t, GradOut& out);
+  // segmented batch (engine_seg.cpp)
+  void build_forward_graph_seg();
+  void build_backward_graph_seg();
+  void backbone_body_seg(unsigned long long cond_handle);
+  bool host_any() const;
   void load_frame(int t);  // frame slot t into the backward working buffers
   void sync_ctl();
   void check_ctl(const char* what);
@@ -293,6 +308,13 @@ class Engine {
   int nrec_ = 0;
   bool recording_ = false;
   int force_slot_ = -1;  // step_into: the slot this step records into
+  int segs_ = 1;         // samples of a lockstep batch (1: a single problem)
+  hdk_segs dseg_{};
+  int* any_ = nullptr;                // OR over the samples' loop conditions
+  unsigned int* gate_ticket_ = nullptr;
+  double* part18_ = nullptr;          // quantity-major Anderson partials (zero-initialised)
+  int* seg_windows_ = nullptr;        // per-sample Anderson window (forward)
+  double* seg_means_dev_ = nullptr;   // per-sample prox means
   double eps_tr_ = 0.1;
   int aa_window_ = 1;
 

@@ -208,7 +208,15 @@ void Engine::backward_frame(int t, GradOut& out) {
   sync_ctl();
   check_ctl("backward step");
   int iters = 1 + h_ctl_->iterations;  // the first solve of the backbone counts (backward.cpp:176-178)
-  last_backward_iterations_ = h_ctl_->iterations;
+  if (segs_ > 1) {  // lockstep: every sample's own count, the loop ran to the largest
+    seg_tau.resize(segs_);
+    for (int k = 0; k < segs_; ++k) {
+      iters = std::max(iters, 1 + h_ctl_[k].iterations);
+      seg_sample_iterations += 1 + h_ctl_[k].iterations;
+      seg_tau[k] = h_ctl_[k].tau;
+    }
+  }
+  last_backward_iterations_ = iters - 1;
   kernel_launches += bk_pre_ + static_cast<long long>(bk_body_) * ((h_ctl_->iterations + unroll_ - 1) / unroll_);
   out.tau[t] = h_ctl_->tau;
   out.rho[t] = h_ctl_->rho;

@@ -53,6 +53,7 @@ struct Material {
   double mu_bar = 0, lambda_bar = 0, k_bar = 0;
   bool frozen = false;
   std::uint64_t version = 0;
+  Vec seg_means;  // lockstep batch: (mu, lambda, k) prox means per sample (empty otherwise)
   double weight(int e) const { return 2.0 * mu[e] + lambda[e]; }
   double contrast() const;
   void set_young(const Vec& y, const Vec& vol);
@@ -99,6 +100,13 @@ struct Scene {  // scene.hpp:14-34
 Scene parse_scene(const std::string& text);
 Scene builtin_scene(const std::string& name);
 Vec external_force(const Scene& s);  // gravity lumped + point forces (scene.cpp:530-540)
+// A lockstep batch of `samples` copies of `s` (contact-free, no Dirichlet
+// vertices, no state hook): vertex / element index spaces concatenated, each
+// copy's material built from its own moduli (young: samples x ne, NULL = the
+// scene's), per-copy prox means kept in material.seg_means (engine.cpp
+// segments > 1).
+Scene make_segmented_scene(const Scene& s, int samples, const double* young);
+void segmented_set_young(Material& mat, const Vec& young, const Vec& vol, int samples);
 
 // Scalar CSR (rows in elimination order).
 struct Csr {

@@ -100,6 +100,17 @@ __device__ __forceinline__ void write_force_sorted(const ElemGeom& g, const M3& 
     }
 }
 
+// Prox means of element e: the material's scalars, or its sample's in a
+// segmented batch (hdk_material::seg_means).
+struct Means {
+  double mu, lambda, k;
+};
+__device__ __forceinline__ Means means_of(const hdk_material& mat, int e) {
+  if (!mat.seg_means) return Means{mat.mu_bar, mat.lambda_bar, mat.k_bar};
+  const double* p = mat.seg_means + 3 * (e / mat.seg_ne);
+  return Means{__ldg(p), __ldg(p + 1), __ldg(p + 2)};
+}
+
 __device__ __forceinline__ void set_err(int* err, int code) {
   if (err) atomicCAS(err, 0, code);
 }
@@ -110,8 +121,9 @@ __device__ __forceinline__ void set_err(int* err, int code) {
 __device__ __forceinline__ bool project(const hdk_material& mat, int e, const V3& sf, V3& s) {
   int it = 0;
   if (mat.kind == 1) {
-    const StretchNH den{mat.mu_bar, mat.lambda_bar};
-    return newton_stretch(sf, mat.k_bar, den, s, it);
+    const Means mb = means_of(mat, e);
+    const StretchNH den{mb.mu, mb.lambda};
+    return newton_stretch(sf, mb.k, den, s, it);
   }
   if (mat.barrier) {
     const double mu = mat.mu_e[e], la = mat.lambda_e[e];
@@ -173,6 +185,9 @@ __global__ void __launch_bounds__(128) k_energy(hdk_mesh m, hdk_material mat, co
   if (e >= m.ne) return;
   const ElemGeom g = load_geom(m, e);
   const M3 f = def_grad(g, q);
+  // a segmented batch flags the element's own sample (hdk_ctl::bad of ctl[s],
+  // sizeof(hdk_ctl) = 2 tau_stride ints apart)
+  if (mat.seg_means) bad += (e / mat.seg_ne) * 2 * mat.tau_stride;
   if (!(det3(f) > 0.0)) {
     atomicCAS(bad, 0, 5);
     energy[e] = 0.0;
@@ -190,9 +205,10 @@ __global__ void __launch_bounds__(128) k_energy(hdk_mesh m, hdk_material mat, co
   double dens;
   const V3 d = v3(s[0] - sf[0], s[1] - sf[1], s[2] - sf[2]);
   if (mat.kind == 1) {
-    const StretchNH den{mat.mu_bar, mat.lambda_bar};
-    const double env = 0.5 * mat.k_bar * dot3(d, d) + den.value(s);
-    dens = mat.w1[e] / mat.k_bar * env;  // w1 carries V
+    const Means mb = means_of(mat, e);
+    const StretchNH den{mb.mu, mb.lambda};
+    const double env = 0.5 * mb.k * dot3(d, d) + den.value(s);
+    dens = mat.w1[e] / mb.k * env;  // w1 carries V
   } else {
     const V3 dev = v3(sf[0] - 1.0, sf[1] - 1.0, sf[2] - 1.0);
     dens = 0.5 * mat.w1[e] * dot3(dev, dev);  // mu_e V |sigma_F - 1|^2
@@ -235,8 +251,10 @@ __global__ void __launch_bounds__(128) k_differential(hdk_mesh m, hdk_material m
   M3 jac = m3_zero();
   double pa[3], pb[3];
   if (mat.kind == 1) {
-    const double tau = *tau_ptr, k = mat.k_bar, w = mat.w1[e];
-    const StretchNH den{mat.mu_bar, mat.lambda_bar};
+    const Means mb = means_of(mat, e);
+    const double tau = mat.seg_means ? tau_ptr[(e / mat.seg_ne) * mat.tau_stride] : *tau_ptr;
+    const double k = mb.k, w = mat.w1[e];
+    const StretchNH den{mb.mu, mb.lambda};
     M3 h = den.hessian(s);
     h(0, 0) += k; h(1, 1) += k; h(2, 2) += k;
     if (tau != 0.0) {  // tr_blend (localstep.cpp:286-303)

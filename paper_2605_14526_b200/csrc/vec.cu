@@ -733,9 +733,13 @@ __global__ void k_any_cond(const hdk_ctl* ctls, int count, int* any, cudaGraphCo
 // and every Anderson access is coalesced with no vertex indirection.  Fixed
 // vertices carry t = x = 0 in the backbone (they contribute nothing to any
 // dot product), so dropping them changes no value, only the summation order.
+// i0 / nseg3: the index range of one sample of a segmented batch (the
+// history rings keep the whole vector's stride n3); a single problem passes
+// 0 / 3 n.
 __device__ __forceinline__ void bb_dots_body(int n, hdk_factor f, hdk_ctl* ctl, hdk_ctl* snap, double* __restrict__ tp,
                                                 double* __restrict__ tv, const double* __restrict__ xp, double* last_q,
-                                                double* last_g, double* dq, double* dg, double* partial, int mode) {
+                                                double* last_g, double* dq, double* dg, double* partial, int mode,
+                                                size_t i0 = 0, size_t nseg3 = 0) {
   HDK_TRACED_WAIT(hdk::kTrDots);
   hdk::pdl_trigger();
   const size_t n3 = 3 * (size_t)n;
@@ -757,7 +761,8 @@ __device__ __forceinline__ void bb_dots_body(int n, hdk_factor f, hdk_ctl* ctl, 
 #pragma unroll
   for (int q = 0; q < 2 * HDK_AA_MAX + 2; ++q) acc[q] = 0.0;
   const unsigned long long pol = hdk::pol_keep();
-  for (size_t i = blockIdx.x * kT + threadIdx.x; i < n3; i += (size_t)HDK_RED_BLOCKS * kT) {
+  const size_t iend = i0 + (nseg3 ? nseg3 : n3);
+  for (size_t i = i0 + blockIdx.x * kT + threadIdx.x; i < iend; i += (size_t)gridDim.x * kT) {
     const int col = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)col);
     const hdk::BbIn pre = hdk::bb_prefetch(args, st, n3, i, pol);
     const int tile = col >> 8;  // tile_cta2 is tiny and L1-resident
@@ -823,13 +828,14 @@ __device__ __forceinline__ void bb_mix_body(int n, const int* __restrict__ p2v, 
                                                double* xp, double* __restrict__ xv, const double* __restrict__ sq,
                                                const double* __restrict__ rt, double* rx, double* last_rx,
                                                double* last_rg, double* rsq, const double* __restrict__ seedp,
-                                               double* __restrict__ rhs) {
+                                               double* __restrict__ rhs, size_t i0 = 0, size_t nseg3 = 0) {
   HDK_TRACED_WAIT(hdk::kTrMix);
   hdk::pdl_trigger();
   if (snap->cond == 0) return;  // unrolled iteration past convergence
   const size_t n3 = 3 * (size_t)n;
-  const size_t i = blockIdx.x * (size_t)kT + threadIdx.x;
-  if (i >= n3) return;
+  const size_t il = blockIdx.x * (size_t)kT + threadIdx.x;
+  if (il >= (nseg3 ? nseg3 : n3)) return;
+  const size_t i = i0 + il;
   const unsigned long long pol = hdk::pol_keep();
   // ring slot of the entry pushed this iteration (state before the update, as k_bb_dots)
   const int m = snap->window, c0 = snap->count, h0 = snap->head;
@@ -1367,4 +1373,504 @@ HDK_API int hdk_bb_columns_mix(const hdk_bb_columns* c, void* stream) {
   hdk::launch(k_bb_mix_cols, dim3(nb(3LL * f->n), HDK_BB_COLUMNS), dim3(kT), 0, S(stream), f->n, f->p2v, *c);
   return last();
 }
+}  // extern "C"
+
+// ---- segmented batch: per-sample reductions and loop control ---------------
+// (hdk.h "segmented batch"; the lockstep C5 engine, engine.cpp segments > 1).
+// Sample s = blockIdx.y; its blocks stride over its own index range, so each
+// sample's sums are fixed-order and independent of the others.
+namespace {
+
+constexpr int kRB = HDK_SEG_RB;
+constexpr size_t kPS = HDK_SEG_PSTRIDE;
+
+// Fold of block-major partials (partial[b * HDK_RED_Q + q]) over kRB blocks.
+__device__ __forceinline__ void fold_rb(const double* __restrict__ partial, int nq, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int q = warp; q < nq; q += nw) {
+    double v = lane < kRB ? partial[lane * HDK_RED_Q + q] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) out[q] = v;
+  }
+}
+
+__device__ __forceinline__ void ctl_init_one(hdk_ctl* c, int window, double guard, int k_max, double er, double ea,
+                                             double tol, double eps_tr) {
+  c->k = 0; c->k_max = k_max; c->iterations = 0; c->converged = 0;
+  c->err = 0; c->done = 0; c->bad = 0; c->cond = 1;
+  c->window = window < 1 ? 1 : window; c->count = 0; c->head = 0; c->has_last = 0; c->mixed = 0; c->nonfinite = 0;
+  c->eps_rel = er; c->eps_abs = ea; c->guard = guard; c->tol = tol;
+  c->tau = 1.0; c->rho = 1.0; c->model = 0.0; c->eps_tr = eps_tr;
+  for (int i = 0; i < HDK_AA_MAX; ++i) c->gamma[i] = 0.0;
+  for (int i = 0; i < HDK_AA_MAX * HDK_AA_MAX; ++i) c->gram[i] = 0.0;
+}
+
+__global__ void k_seg_ctl_init(hdk_ctl* ctl, hdk_segs g, const int* windows, double guard, int k_max, double er,
+                               double ea, double tol, double eps_tr, int* any) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  for (int s = threadIdx.x; s < g.count; s += blockDim.x)
+    ctl_init_one(ctl + s, windows[s], guard, k_max, er, ea, tol, eps_tr);
+  if (threadIdx.x == 0) *any = 1;
+}
+
+__global__ void k_seg_aa_reset(hdk_ctl* ctl, hdk_segs g, int window, double guard, int k_max, double tol, int* any) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  for (int s = threadIdx.x; s < g.count; s += blockDim.x) {
+    hdk_ctl* c = ctl + s;
+    c->k = 0; c->k_max = k_max; c->iterations = 0; c->converged = 0; c->done = 0; c->cond = 1;
+    c->window = window < 1 ? 1 : window; c->count = 0; c->head = 0; c->has_last = 0; c->mixed = 0; c->nonfinite = 0;
+    c->guard = guard; c->tol = tol;
+  }
+  if (threadIdx.x == 0) *any = 1;
+}
+
+__global__ void __launch_bounds__(kT) k_seg_gather_rhs(hdk_vtx x, hdk_segs g, const double* __restrict__ ef,
+                                                       double inv_h2, const double* __restrict__ qt,
+                                                       const double* __restrict__ damp, double* bprev, double* rhs,
+                                                       double* partial, const hdk_ctl* ctl) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int s = blockIdx.y;
+  if (ctl[s].cond == 0) return;
+  double acc[2] = {0.0, 0.0};
+  const int v0 = s * g.nv, v1 = v0 + g.nv;
+  for (int v = v0 + blockIdx.x * kT + threadIdx.x; v < v1; v += gridDim.x * kT) {
+    const int p = x.v2p[v];
+    const double m = x.mass[v];
+    double gg[3];
+    gather_vtx(x, ef, v, gg[0], gg[1], gg[2]);
+    for (int a = 0; a < 3; ++a) {
+      const size_t i = 3 * (size_t)v + a;
+      double b = m * qt[i] * inv_h2;
+      b += gg[a];
+      b += damp[i];
+      const double d = b - bprev[i];
+      acc[0] += d * d;
+      acc[1] += b * b;
+      bprev[i] = b;
+      if (p >= 0) rhs[3 * (size_t)p + a] = b;
+    }
+  }
+  block_partials<2>(acc, partial + s * kPS);
+}
+
+__global__ void __launch_bounds__(kT) k_seg_aa_dots_fused(hdk_vtx x, hdk_factor f, hdk_segs g, hdk_ctl* ctls,
+                                                          double* __restrict__ qhat, const double* __restrict__ qcur,
+                                                          double* last_q, double* last_g, double* dq, double* dg,
+                                                          double* partial18, unsigned int* tickets) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int s = blockIdx.y;
+  hdk_ctl* ctl = ctls + s;
+  if (ctl->cond == 0) return;  // this sample's loop has ended
+  const size_t n3 = 3 * (size_t)x.nv;  // ring stride: the whole batch
+  const size_t i0 = 3 * (size_t)s * g.nv, i1 = i0 + 3 * (size_t)g.nv;
+  const int m = ctl->window, c = ctl->count, h = ctl->head;
+  const bool push = ctl->has_last != 0;
+  int ns = 0, c2 = c, h2 = h;
+  if (push) {
+    ns = c < m ? (h + c) % m : h;
+    c2 = c < m ? c + 1 : m;
+    h2 = c < m ? h : (h + 1) % m;
+  }
+  double acc[2 * HDK_AA_MAX + 2];
+#pragma unroll
+  for (int q = 0; q < 2 * HDK_AA_MAX + 2; ++q) acc[q] = 0.0;
+  for (size_t i = i0 + blockIdx.x * kT + threadIdx.x; i < i1; i += (size_t)gridDim.x * kT) {
+    const int v = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)v);
+    const int2 vf = __ldg(f.vfold + v);
+    double th;
+    if (vf.y > 0) {
+      th = 0.0;
+      for (int b = 0; b < vf.y; ++b) th += __ldg(f.part2 + 3 * ((size_t)vf.x + 256 * (size_t)b) + a);
+      qhat[i] = th;
+    } else {
+      th = qhat[i];
+    }
+    const double qc = qcur[i];
+    const double gv = th - qc;
+    acc[2 * HDK_AA_MAX] += gv * gv;
+    acc[2 * HDK_AA_MAX + 1] += th * th;
+    if (push) {
+      const double dqn = qc - last_q[i];
+      const double dgn = gv - last_g[i];
+      dq[ns * n3 + i] = dqn;
+      dg[ns * n3 + i] = dgn;
+#pragma unroll
+      for (int j = 0; j < HDK_AA_MAX; ++j) {
+        if (j < c2) {
+          const int ph = (h2 + j) % m;
+          const double dgj = ph == ns ? dgn : dg[ph * n3 + i];
+          acc[j] += dgn * dgj;
+          acc[HDK_AA_MAX + j] += dgj * gv;
+        }
+      }
+    }
+    last_q[i] = qc;
+    last_g[i] = gv;
+  }
+  double* part = partial18 + s * kPS;
+  block_partials_18(acc, part);
+  __shared__ int is_last;
+  if (threadIdx.x < 18) __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(tickets + s, 1u);
+    is_last = t == gridDim.x - 1;
+    if (is_last) tickets[s] = 0u;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  aa_solve_block(ctl, ctl, part, 0, 0, 0);
+}
+
+__global__ void __launch_bounds__(kT) k_seg_aa_mix(hdk_vtx x, hdk_segs g, hdk_ctl* ctls, const double* __restrict__ qhat,
+                                                   double* qcur, double* qprev, const double* __restrict__ dq,
+                                                   const double* __restrict__ dg, double* partial) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int s = blockIdx.y;
+  const hdk_ctl* ctl = ctls + s;
+  if (ctl->cond == 0) return;
+  const size_t n3 = 3 * (size_t)x.nv;
+  const size_t i0 = 3 * (size_t)s * g.nv, i1 = i0 + 3 * (size_t)g.nv;
+  const int mixed = ctl->mixed, c = ctl->count, h = ctl->head, m = ctl->window;
+  double gam[HDK_AA_MAX];
+#pragma unroll
+  for (int j = 0; j < HDK_AA_MAX; ++j) gam[j] = j < c ? ctl->gamma[j] : 0.0;
+  double acc[2] = {0.0, 0.0};
+  for (size_t i = i0 + blockIdx.x * kT + threadIdx.x; i < i1; i += (size_t)gridDim.x * kT) {
+    const double qc = qcur[i], th = qhat[i];
+    double out = qc + (th - qc);
+    if (mixed) {
+#pragma unroll
+      for (int j = 0; j < HDK_AA_MAX; ++j)
+        if (j < c) {
+          const int ph = (h + j) % m;
+          out -= gam[j] * (dq[ph * n3 + i] + dg[ph * n3 + i]);
+        }
+    }
+    const double d = out - qc;
+    acc[0] += d * d;
+    acc[1] += qc * qc;
+    qprev[i] = qc;
+    qcur[i] = out;
+  }
+  block_partials<2>(acc, partial + s * kPS);
+}
+
+// OR over the samples of "still iterating" (thread-strided, block-wide).
+__device__ __forceinline__ int seg_any_value(const hdk_ctl* ctl, int count) {
+  int on = 0;
+  for (int t = threadIdx.x; t < count; t += blockDim.x)
+    on |= (ctl[t].cond != 0 && ctl[t].err == 0 && ctl[t].nonfinite == 0) ? 1 : 0;
+  return __syncthreads_or(on);
+}
+
+__global__ void __launch_bounds__(kT) k_seg_gate(hdk_ctl* ctls, hdk_segs g, const double* pb, const double* pq,
+                                                 int* any, unsigned int* ticket, cudaGraphConditionalHandle handle,
+                                                 int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int s = blockIdx.x;
+  hdk_ctl* ctl = ctls + s;
+  __shared__ double sb[2], sq[2];
+  if (ctl->cond != 0) {  // uniform per block
+    fold_rb(pb + s * kPS, 2, sb);
+    fold_rb(pq + s * kPS, 2, sq);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double db = sb[0], bb = sb[1], dqq = sq[0], qq = sq[1];
+      const int k = ctl->k;
+      const double er = ctl->eps_rel, ea = ctl->eps_abs;
+      const bool gate = k >= 1 && sqrt(dqq) <= er * sqrt(qq) + ea && sqrt(db) <= er * sqrt(bb) + ea;
+      ctl->k = k + 1;
+      ctl->iterations = k + 1;
+      if (gate) ctl->converged = 1;
+      ctl->cond = (!gate && k + 1 < ctl->k_max && ctl->err == 0) ? 1 : 0;
+    }
+  }
+  __shared__ int is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int t = atomicAdd(ticket, 1u);
+    is_last = t == gridDim.x - 1;
+    if (is_last) *ticket = 0u;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  const int a = seg_any_value(ctls, g.count);
+  if (threadIdx.x == 0) {
+    *any = a;
+    if (use_handle) cudaGraphSetConditional(handle, a);
+  }
+}
+
+__global__ void k_seg_any(const hdk_ctl* ctls, hdk_segs g, int* any, cudaGraphConditionalHandle handle,
+                          int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int a = seg_any_value(ctls, g.count);
+  if (threadIdx.x == 0) {
+    *any = a;
+    if (use_handle) cudaGraphSetConditional(handle, a);
+  }
+}
+
+__global__ void k_seg_commit(hdk_segs g, const hdk_ctl* ctl, const double* qs, double h, double* q, double* v) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const size_t per = 3 * (size_t)g.nv;
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= per * g.count || ctl[i / per].err != 0) return;
+  const double sq = qs[i];
+  v[i] = (sq - q[i]) / h;
+  q[i] = sq;
+}
+
+__global__ void __launch_bounds__(kT) k_seg_tr_spmv(hdk_csr A, hdk_segs g, const double* __restrict__ dq,
+                                                    double* partial) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int s = blockIdx.y;
+  double acc[1] = {0.0};
+  const int p0 = s * g.n, p1 = p0 + g.n;
+  for (int p = p0 + blockIdx.x * kT + threadIdx.x; p < p1; p += gridDim.x * kT) {
+    double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+    for (int k = A.off[p]; k < A.off[p + 1]; ++k) {
+      const double w = A.val[k];
+      const double* d = dq + 3 * (size_t)A.col[k];
+      y0 += w * d[0];
+      y1 += w * d[1];
+      y2 += w * d[2];
+    }
+    const double* d = dq + 3 * (size_t)p;
+    acc[0] += d[0] * y0 + d[1] * y1 + d[2] * y2;
+  }
+  block_partials<1>(acc, partial + s * kPS);
+}
+
+__global__ void __launch_bounds__(kT) k_seg_tr_partials(hdk_vtx x, hdk_segs g, const double* ep, const double* es,
+                                                        const double* qp, const double* qs, const double* qt,
+                                                        double* partial) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int s = blockIdx.y;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int n = max(g.ne, g.nv);
+  for (int il = blockIdx.x * kT + threadIdx.x; il < n; il += gridDim.x * kT) {
+    if (il < g.ne) {
+      acc[0] += ep[(size_t)s * g.ne + il];
+      acc[1] += es[(size_t)s * g.ne + il];
+    }
+    const int i = s * g.nv + il;
+    if (il < g.nv && x.v2p[i] >= 0) {
+      const double m = x.mass[i];
+      for (int a = 0; a < 3; ++a) {
+        const size_t j = 3 * (size_t)i + a;
+        const double d0 = qp[j] - qt[j], d1 = qs[j] - qt[j];
+        acc[2] += d0 * m * d0;
+        acc[3] += d1 * m * d1;
+      }
+    }
+  }
+  block_partials<4>(acc, partial + s * kPS);
+}
+
+__global__ void __launch_bounds__(kT) k_seg_tr_final(hdk_ctl* ctls, const double* pm, const double* pe,
+                                                     double inv_h2) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int s = blockIdx.x;
+  hdk_ctl* ctl = ctls + s;
+  __shared__ double sm_[1], se[4];
+  fold_rb(pm + s * kPS, 1, sm_);
+  fold_rb(pe + s * kPS, 4, se);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const double model_raw = sm_[0], e_prev = se[0], e_star = se[1], i_prev = se[2], i_star = se[3];
+  const double model = 0.5 * fabs(model_raw);
+  double rho = 1.0;
+  if (model >= 1e-12) {
+    if (ctl->bad != 0) {
+      rho = INFINITY;
+    } else {
+      const double phi_prev = 0.5 * inv_h2 * i_prev + e_prev;
+      const double phi_star = 0.5 * inv_h2 * i_star + e_star;
+      rho = (phi_prev - phi_star) / model;
+    }
+  }
+  ctl->model = model;
+  ctl->rho = rho;
+  ctl->tau = fabs(rho - 1.0) <= ctl->eps_tr ? 0.5 : 1.0;
+}
+
+__global__ void __launch_bounds__(kT) k_seg_bb_dots(int n, hdk_factor f, hdk_segs g, hdk_ctl* ctl, hdk_ctl* snap,
+                                                    double* __restrict__ tp, double* __restrict__ tv,
+                                                    const double* __restrict__ xp, double* last_q, double* last_g,
+                                                    double* dq, double* dg, double* partial18) {
+  const int s = blockIdx.y;
+  bb_dots_body(n, f, ctl + s, snap + s, tp, tv, xp, last_q, last_g, dq, dg, partial18 + s * kPS, 0,
+               3 * (size_t)s * g.n, 3 * (size_t)g.n);
+}
+
+__global__ void __launch_bounds__(kT) k_seg_bb_solve(hdk_ctl* ctl, const hdk_ctl* snap, const double* partial18,
+                                                     AaResult* out) {
+  const int s = blockIdx.x;
+  bb_solve_body(ctl + s, snap + s, partial18 + s * kPS, out + s, 0, 0);
+}
+
+__global__ void __launch_bounds__(kT) k_seg_bb_mix(int n, const int* __restrict__ p2v, hdk_segs g, hdk_ctl* ctl,
+                                                   const hdk_ctl* snap, const AaResult* __restrict__ res,
+                                                   const double* __restrict__ tp, double* xp, double* __restrict__ xv,
+                                                   const double* __restrict__ sq, const double* __restrict__ rt,
+                                                   double* rx, double* last_rx, double* last_rg, double* rsq,
+                                                   const double* __restrict__ seedp, double* __restrict__ rhs) {
+  const int s = blockIdx.y;
+  bb_mix_body(n, p2v, ctl + s, snap + s, res + s, tp, xp, xv, sq, rt, rx, last_rx, last_rg, rsq, seedp, rhs,
+              3 * (size_t)s * g.n, 3 * (size_t)g.n);
+}
+
+constexpr int kSumT = 1024;
+__global__ void __launch_bounds__(kSumT) k_seg_half_sqdist(hdk_segs g, const double* __restrict__ q,
+                                                           const double* __restrict__ ref, double* out) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  __shared__ double sh[32];
+  const size_t per = 3 * (size_t)g.nv, base = blockIdx.x * per;
+  double v = 0.0;
+  for (size_t i = threadIdx.x; i < per; i += kSumT) {
+    const double d = q[base + i] - ref[base + i];
+    v += d * d;
+  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  v = threadIdx.x < kSumT / 32 ? sh[threadIdx.x] : 0.0;
+  if (w == 0)
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (threadIdx.x == 0) out[blockIdx.x] = 0.5 * v;
+}
+
+__global__ void k_seg_sum(hdk_segs g, const double* __restrict__ vec, const double* __restrict__ loss,
+                          double* __restrict__ out) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    double l = 0;
+    for (int s = 0; s < g.count; ++s) l += loss[s];
+    out[0] = l;
+  }
+  if (i < g.ne) {
+    double a = 0;
+    for (int s = 0; s < g.count; ++s) a += vec[(size_t)s * g.ne + i];
+    out[1 + i] = a;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+HDK_API int hdk_seg_ctl_init(hdk_ctl* ctl, const hdk_segs* g, const int* windows, double guard, int k_max,
+                             double eps_rel, double eps_abs, double tol, double eps_tr, int* any, void* stream) {
+  hdk::launch(k_seg_ctl_init, dim3(1), dim3(256), 0, S(stream), ctl, *g, windows, guard, k_max, eps_rel, eps_abs, tol,
+              eps_tr, any);
+  return last();
+}
+HDK_API int hdk_seg_aa_reset(hdk_ctl* ctl, const hdk_segs* g, int window, double guard, int k_max, double tol,
+                             int* any, void* stream) {
+  hdk::launch(k_seg_aa_reset, dim3(1), dim3(256), 0, S(stream), ctl, *g, window, guard, k_max, tol, any);
+  return last();
+}
+HDK_API int hdk_seg_gather_rhs(const hdk_vtx* x, const hdk_segs* g, const hdk_ctl* ctl, const double* ef,
+                               double inv_h2, const double* q_tilde, const double* damp, double* b_prev,
+                               double* rhs_perm, double* partial, void* stream) {
+  hdk::launch(k_seg_gather_rhs, dim3(kRB, g->count), dim3(kT), 0, S(stream), *x, *g, ef, inv_h2, q_tilde, damp, b_prev,
+              rhs_perm, partial, ctl);
+  return last();
+}
+HDK_API int hdk_seg_aa_dots_fused(const hdk_vtx* x, const hdk_factor* f, const hdk_segs* g, hdk_ctl* ctl,
+                                  double* qhat, const double* qcur, double* last_q, double* last_g, double* dq,
+                                  double* dg, double* partial18, unsigned int* tickets, void* stream) {
+  hdk::launch(k_seg_aa_dots_fused, dim3(kRB, g->count), dim3(kT), 0, S(stream), *x, *f, *g, ctl, qhat, qcur, last_q,
+              last_g, dq, dg, partial18, tickets);
+  return last();
+}
+HDK_API int hdk_seg_aa_mix(const hdk_vtx* x, const hdk_segs* g, hdk_ctl* ctl, const double* qhat, double* qcur,
+                           double* qprev, const double* dq, const double* dg, double* partial, void* stream) {
+  hdk::launch(k_seg_aa_mix, dim3(kRB, g->count), dim3(kT), 0, S(stream), *x, *g, ctl, qhat, qcur, qprev, dq, dg,
+              partial);
+  return last();
+}
+HDK_API int hdk_seg_gate(hdk_ctl* ctl, const hdk_segs* g, const double* partial_b, const double* partial_q, int* any,
+                         unsigned int* ticket, unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_seg_gate, dim3(g->count), dim3(kT), 0, S(stream), ctl, *g, partial_b, partial_q, any, ticket,
+              static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle ? 1 : 0);
+  return last();
+}
+HDK_API int hdk_seg_commit(const hdk_segs* g, const hdk_ctl* ctl, const double* q_star, double h, double* q, double* v,
+                           void* stream) {
+  hdk::launch(k_seg_commit, dim3(nb(3LL * g->nv * g->count)), dim3(256), 0, S(stream), *g, ctl, q_star, h, q, v);
+  return last();
+}
+HDK_API int hdk_seg_tr_model(const hdk_vtx* x, const hdk_segs* g, const hdk_csr* a_ff, const double* q_star,
+                             const double* q_prev, double* dq_perm, double* partial, void* stream) {
+  hdk::launch(k_tr_dq, dim3(nb(x->n)), dim3(256), 0, S(stream), *x, q_star, q_prev, dq_perm);
+  hdk::launch(k_seg_tr_spmv, dim3(kRB, g->count), dim3(kT), 0, S(stream), *a_ff, *g, dq_perm, partial);
+  return last();
+}
+HDK_API int hdk_seg_tr_select(const hdk_vtx* x, const hdk_segs* g, const double* e_prev, const double* e_star,
+                              const double* q_prev, const double* q_star, const double* q_tilde, double inv_h2,
+                              const double* model_partial, double* partial, hdk_ctl* ctl, void* stream) {
+  hdk::launch(k_seg_tr_partials, dim3(kRB, g->count), dim3(kT), 0, S(stream), *x, *g, e_prev, e_star, q_prev, q_star,
+              q_tilde, partial);
+  hdk::launch(k_seg_tr_final, dim3(g->count), dim3(kT), 0, S(stream), ctl, model_partial, partial, inv_h2);
+  return last();
+}
+HDK_API int hdk_seg_bb_dots(const hdk_factor* f, const hdk_segs* g, hdk_ctl* ctl, hdk_ctl* snap, double* t_perm,
+                            double* t_full, const double* x_perm, double* last_q, double* last_g, double* dq,
+                            double* dg, double* partial18, void* stream) {
+  hdk::launch(k_seg_bb_dots, dim3(kRB, g->count), dim3(kT), 0, S(stream), f->n, *f, *g, ctl, snap, t_perm, t_full,
+              x_perm, last_q, last_g, dq, dg, partial18);
+  return last();
+}
+HDK_API int hdk_seg_bb_solve(hdk_ctl* ctl, const hdk_segs* g, const hdk_ctl* snap, const double* partial18,
+                             void* results, void* stream) {
+  hdk::launch(k_seg_bb_solve, dim3(g->count), dim3(kT), 0, S(stream), ctl, snap, partial18,
+              static_cast<AaResult*>(results));
+  return last();
+}
+HDK_API int hdk_seg_bb_mix(const hdk_factor* f, const hdk_segs* g, hdk_ctl* ctl, const hdk_ctl* snap,
+                           const void* results, const double* t_perm, double* x_perm, double* x_full,
+                           const double* sum_hist, const double* rt_perm, double* rx_perm, double* last_rx,
+                           double* last_rg, double* rsum_hist, const double* seed_perm, double* rhs_perm,
+                           void* stream) {
+  hdk::launch(k_seg_bb_mix, dim3(nb(3LL * g->n), g->count), dim3(kT), 0, S(stream), f->n, f->p2v, *g, ctl, snap,
+              static_cast<const AaResult*>(results), t_perm, x_perm, x_full, sum_hist, rt_perm, rx_perm, last_rx,
+              last_rg, rsum_hist, seed_perm, rhs_perm);
+  return last();
+}
+HDK_API int hdk_seg_any(const hdk_ctl* ctl, const hdk_segs* g, int* any, unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_seg_any, dim3(1), dim3(256), 0, S(stream), ctl, *g, any,
+              static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle ? 1 : 0);
+  return last();
+}
+HDK_API int hdk_seg_half_sqdist(const hdk_segs* g, const double* q, const double* ref, double* out, void* stream) {
+  hdk::launch(k_seg_half_sqdist, dim3(g->count), dim3(kSumT), 0, S(stream), *g, q, ref, out);
+  return last();
+}
+HDK_API int hdk_seg_sum(const hdk_segs* g, const double* vec, const double* loss, double* out, void* stream) {
+  hdk::launch(k_seg_sum, dim3(nb(g->ne > 0 ? g->ne : 1)), dim3(256), 0, S(stream), *g, vec, loss, out);
+  return last();
+}
+
 }  // extern "C"

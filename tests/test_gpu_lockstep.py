@@ -1,0 +1,87 @@
+"""The lockstep batch (engine_seg.cpp): a GPU's system-ID samples as one
+segmented problem — concatenated vertex / element / elimination index
+spaces, one block-diagonal factor stream, per-sample loop control
+(hdk_seg_*).  Each sample must follow its own reference trajectory
+(forward.cpp:148-272, backward.cpp:170-204 per sample; drivers.cpp:848-907
+sums the samples), so the batch is compared sample by sample with the CPU
+oracle's batch and with the one-engine-per-sample path
+(HETERODYN_BATCH=streams).
+
+The samples differ in more than a scale factor here: per-element moduli with
+a per-sample contrast either side of the Anderson-window switch (weight
+contrast 10, forward.cpp:56-83), and stiffness damping beta0 > 0 whose
+beta_e = beta0 mu_e / max mu is per sample (material.cpp:48-73)."""
+import numpy as np
+import pytest
+
+from paper_2605_14526_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+
+
+def rel2(a, b):
+    return np.linalg.norm(np.asarray(a) - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def heterogeneous_young(samples, ne, seed=7):
+    rng = np.random.default_rng(seed)
+    y = np.empty((samples, ne))
+    for s in range(samples):
+        spread = 0.2 if s % 2 == 0 else 1.5  # contrast ~2 vs ~> 10: Anderson window 5 vs 1
+        y[s] = 5e4 * np.exp(spread * rng.standard_normal(ne))
+    return y
+
+
+@pytest.mark.parametrize("beta0", [0.0, 0.05])
+def test_lockstep_matches_oracle_and_per_sample_engines(prod, orc, monkeypatch, beta0):
+    scene = scenes.block_scene(dims=(4, 3, 2), frames=3, gravity_z=-9.81, alpha=0.02, beta0=beta0, v0_amp=0.05)
+    sp, so = prod.scene(scene), orc.scene(scene)
+    ne = sp.element_count
+    young = heterogeneous_young(5, ne)
+    target = np.asarray(so.sim().positions()) + 1e-3
+    bo = so.batch(5, young)
+    bo.set_target(target)
+    ro = bo.evaluate(3)
+
+    monkeypatch.delenv("HETERODYN_BATCH", raising=False)
+    bl = sp.batch(5, young, threads=1)
+    bl.set_target(target)
+    rl = bl.evaluate(3)
+    monkeypatch.setenv("HETERODYN_BATCH", "streams")
+    bs = sp.batch(5, young, threads=4)
+    bs.set_target(target)
+    rs = bs.evaluate(3)
+
+    for k in ("loss", "dl_de"):
+        assert rel2(rl[k], ro[k]) <= 1e-6, (k, rel2(rl[k], ro[k]))
+        assert rel2(rl[k], rs[k]) <= 1e-9, (k, rel2(rl[k], rs[k]))
+    # per-sample losses, one by one
+    for s in range(5):
+        assert abs(rl["loss"][s] - ro["loss"][s]) <= 1e-6 * abs(ro["loss"][s])
+    # deterministic rerun, and a parameter update refactors every sample
+    np.testing.assert_array_equal(bl.evaluate(3)["dl_de"], rl["dl_de"])
+    young2 = young * np.linspace(0.8, 1.2, 5)[:, None]
+    bo.set_young(young2)
+    bl.set_young(young2)
+    ro2, rl2 = bo.evaluate(3), bl.evaluate(3)
+    assert rel2(rl2["loss"], ro2["loss"]) <= 1e-6
+    assert rel2(rl2["dl_de"], ro2["dl_de"]) <= 1e-6
+
+
+def test_lockstep_single_sample_equals_engine(prod, monkeypatch):
+    """S = 1: the segmented path is one sample's algorithm; against the
+    per-sample engine only the reduction grouping differs."""
+    scene = scenes.block_scene(dims=(3, 3, 2), frames=2, gravity_z=-9.81, alpha=0.02, v0_amp=0.05)
+    sp = prod.scene(scene)
+    young = heterogeneous_young(1, sp.element_count)
+    target = np.asarray(sp.sim().positions()) - 2e-3
+    monkeypatch.delenv("HETERODYN_BATCH", raising=False)
+    bl = sp.batch(1, young)
+    bl.set_target(target)
+    rl = bl.evaluate(2)
+    monkeypatch.setenv("HETERODYN_BATCH", "streams")
+    bs = sp.batch(1, young)
+    bs.set_target(target)
+    rs = bs.evaluate(2)
+    assert rel2(rl["loss"], rs["loss"]) <= 1e-10
+    assert rel2(rl["dl_de"], rs["dl_de"]) <= 1e-9
