@@ -372,13 +372,17 @@ def run_batch(args, world, rank):
     t_ref = time.perf_counter() - t_ref
     b.set_young(young[mine.start:mine.stop])
 
-    # roofline: aggregate factor streaming of all sample solves in the timed
-    # region (this rank's solves x algorithmic bytes per solve / step time);
-    # the single-sample solve timed alone is reported beside it
+    # roofline of the dominant kernel: the batch's solve (lockstep: one
+    # launch per pass streams every sample's block of the block-diagonal
+    # factor), timed alone with CUDA events on the engine's stream; the
+    # aggregate solve streaming over the whole step and the single-sample
+    # solve are reported beside it
+    ms_launch, bytes_launch = b.time_solve(20)
     probe = sc.sim()
     ms_solve, bytes_solve = probe.time_solve(50)
     peak, peak_kind = measured_peak()
-    achieved = solves * b.solve_bytes / (ms / 1e3) / 1e9
+    achieved = bytes_launch / (ms_launch / 1e3) / 1e9
+    step_solve_gbs = solves * b.solve_bytes / (ms / 1e3) / 1e9
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -403,6 +407,7 @@ def run_batch(args, world, rank):
                        "parallelism": f"samples sharded dp{world}, NCCL all-reduce of [loss, dL/dE] "
                                       f"({(1 + ne) * 8} B) per step",
                        "samples_per_rank": len(mine), "host_threads_per_rank": threads,
+                       "batch_engine": "lockstep (one segmented engine per rank)" if b.lockstep else "one engine per sample",
                        "engine_build_s": t_build, "set_young_s": t_ref,
                        "l2_policy": "per-sample factors 64 x ~%.0f MB exceed L2" %
                                                                (probe.factor_nnz * 8 / 1e6),
@@ -413,10 +418,14 @@ def run_batch(args, world, rank):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": ncu_traffic("solve_traffic_c5.json"),
                          "traffic_scope": "DRAM bytes of one sample's solve (ncu capture, profiles/solve_traffic_c5.json)"
-                                          " vs bytes_per_launch",
-                         "kernel": "hdk_apply_inverse3 over all sample factors (aggregate bytes of the timed "
-                                   "region's solves / step time, rank 0)",
-                         "solves_per_step": solves / args.steps, "bytes_per_launch": b.solve_bytes,
+                                          " vs its algorithmic bytes",
+                         "kernel": ("hdk_apply_inverse3 on the lockstep batch's block-diagonal factor (all of the rank's "
+                                    "samples in one launch per pass)" if b.lockstep else
+                                    "hdk_apply_inverse3 of one sample's factor"),
+                         "bytes_per_launch": bytes_launch, "ms_per_launch": ms_launch,
+                         "step_solve_streaming_gbs": step_solve_gbs,
+                         "step_solve_streaming_frac": step_solve_gbs / peak,
+                         "sample_solves_per_step": solves / args.steps,
                          "single_sample_solve_ms": ms_solve, "single_sample_solve_gbs": bytes_solve / (ms_solve / 1e3) / 1e9,
                          "peak_source": peak_kind},
             "cpu_baseline": cpu,

@@ -259,6 +259,11 @@ HD_API long long hd_batch_kernel_launches(const hd_batch* batch);
 /* Global solves (3 axes) run by all samples so far, and the algorithmic bytes
  * of one solve of one sample (16 nnz(S') + 96 n; samples share the pattern). */
 HD_API long long hd_batch_solve_count(const hd_batch* batch);
+/* ms per solve of the batch's solve path (the lockstep engine's block-diagonal
+ * factor: all samples in one launch per pass) and its algorithmic bytes. */
+HD_API hd_status hd_batch_time_solve(hd_batch* batch, int reps, double* ms_per_solve, double* bytes_per_solve);
+/* 1 when the batch runs as one lockstep segmented engine, 0 for per-sample engines. */
+HD_API int hd_batch_lockstep(const hd_batch* batch);
 HD_API double hd_batch_solve_bytes(const hd_batch* batch);
 
 #ifdef __cplusplus

@@ -555,5 +555,13 @@ double hd_batch_last_ms(const hd_batch*) { return 0.0; }
 long long hd_batch_kernel_launches(const hd_batch*) { return 0; }
 long long hd_batch_solve_count(const hd_batch*) { return 0; }
 double hd_batch_solve_bytes(const hd_batch*) { return 0.0; }
+// profiling hooks of the device batch: nothing to time on the CPU checker
+hd_status hd_batch_time_solve(hd_batch* batch, int reps, double* ms, double* bytes) {
+  if (!batch || !ms || reps < 1) return null_arg("hd_batch_time_solve");
+  *ms = 0.0;
+  if (bytes) *bytes = 0.0;
+  return HD_OK;
+}
+int hd_batch_lockstep(const hd_batch*) { return 0; }
 
 }  // extern "C"

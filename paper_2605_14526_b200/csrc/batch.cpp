@@ -216,6 +216,10 @@ void Batch::set_young(const double* young, bool freeze_means) {
   });
 }
 
+double Batch::time_solve(int reps, double* bytes) {
+  return lock_ ? lock_->time_solve(reps, bytes) : eng_.front()->time_solve(reps, bytes);
+}
+
 long long Batch::solve_count() const {
   if (lock_) return lock_->solve_count * samples_;  // every lockstep solve streams all samples' factors
   long long k = 0;

@@ -37,6 +37,10 @@ class Batch {
   // element_count doubles on this device) receives [sum L, sum dL/dE].
   void evaluate(int frames, double* loss, double* grad_sum, double* device_out);
   long long kernel_launches() const;
+  // ms per solve (reps after warm-up) of the batch's solve path: the lockstep
+  // engine's block-diagonal factor (every sample in one launch per pass), or
+  // sample 0's factor; *bytes: that solve's algorithmic bytes
+  double time_solve(int reps, double* bytes);
   void evaluate_lockstep(int frames, double* loss, double* grad_sum, double* device_out);
   long long solve_count() const;      // 3-axis global solves over all samples so far
   double solve_bytes() const;         // algorithmic bytes of one solve of one sample (16 nnz(S') + 96 n)

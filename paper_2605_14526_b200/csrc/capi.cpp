@@ -478,4 +478,9 @@ hd_status hd_batch_evaluate(hd_batch* batch, int frames, double* loss, size_t lo
 double hd_batch_last_ms(const hd_batch* batch) { return batch ? batch->b->last_ms : 0.0; }
 long long hd_batch_kernel_launches(const hd_batch* batch) { return batch ? batch->b->kernel_launches() : 0; }
 long long hd_batch_solve_count(const hd_batch* batch) { return batch ? batch->b->solve_count() : 0; }
+hd_status hd_batch_time_solve(hd_batch* batch, int reps, double* ms, double* bytes) {
+  if (!batch || !ms || reps < 1) return bad_arg("hd_batch_time_solve: bad argument");
+  return guarded([&] { *ms = batch->b->time_solve(reps, bytes); });
+}
+int hd_batch_lockstep(const hd_batch* batch) { return batch && batch->b->lockstep() ? 1 : 0; }
 double hd_batch_solve_bytes(const hd_batch* batch) { return batch ? batch->b->solve_bytes() : 0.0; }

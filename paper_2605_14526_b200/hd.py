@@ -84,6 +84,8 @@ SIGNATURES = {
     "hd_sim_stream": (_VP, [_VP]),
     "hd_sim_kernel_launches": (C.c_longlong, [_VP]),
     "hd_sim_time_solve": (C.c_int, [_VP, C.c_int, _D, _D]),
+    "hd_batch_time_solve": (C.c_int, [_VP, C.c_int, _D, _D]),
+    "hd_batch_lockstep": (C.c_int, [_VP]),
     "hd_sim_time_backbone": (C.c_int, [_VP, C.c_int, C.c_uint, _D]),
     "hd_sim_trace_backbone": (C.c_int, [_VP, C.c_int, _D, C.c_size_t]),
     "hd_sim_trace_loop": (C.c_int, [_VP, _D, C.c_size_t, C.POINTER(C.c_int)]),
@@ -515,6 +517,16 @@ class Batch:
     @property
     def solve_count(self) -> int:
         return self.L.lib.hd_batch_solve_count(self.h)
+
+    @property
+    def lockstep(self) -> bool:
+        return bool(self.L.lib.hd_batch_lockstep(self.h))
+
+    def time_solve(self, reps: int = 20):
+        """(ms per solve, algorithmic bytes per solve) of the batch's solve path."""
+        ms, b = C.c_double(0.0), C.c_double(0.0)
+        self.L.check(self.L.lib.hd_batch_time_solve(self.h, reps, C.byref(ms), C.byref(b)))
+        return ms.value, b.value
 
     @property
     def solve_bytes(self) -> float:
