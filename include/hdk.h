@@ -490,6 +490,43 @@ HDK_API int hdk_bb_columns_bapply(const hdk_mesh* m, const double* dcomp, const 
 HDK_API int hdk_bb_columns_gather(const hdk_vtx* x, const hdk_bb_columns* c, void* stream);
 HDK_API int hdk_bb_columns_mix(const hdk_bb_columns* c, void* stream);
 
+/* ---- device refactorization (refactor.cu, refactor.hpp) -------------------
+ * A's values for a fixed pattern (factor.cpp assemble, same order), the
+ * multifrontal LDL^T over the supernodal elimination tree (one CTA per front,
+ * one launch per tree level, panels of HDK_MF_PANEL pivot columns) and
+ * D^{-1/2}; L lands in the host factor's column layout (lp), ready for
+ * hdk_inverse_values.  Replaces SparseFactor::factorize (factor.cpp:11-104)
+ * and assemble_global_scalar (factor.cpp:121-136) on a refactorization. */
+#define HDK_MF_PANEL 8
+typedef struct hdk_mf {
+  int n, nsuper, nlevels;
+  const int* sfirst;      /* nsuper + 1 */
+  const int* fm;          /* front order per supernode */
+  const long long* foff;  /* front offset in pool (m x m column-major) */
+  const int* level_off;   /* nlevels + 1 */
+  const int* level_node;
+  const int* child_off;
+  const int* child;
+  const int* emap_off;
+  const int* emap;        /* update rows -> parent front positions */
+  const int* aent_off;
+  const int* aent_src;    /* a_ff value index */
+  const int* aent_dst;    /* front offset */
+  const long long* lp;    /* L by columns */
+  double* pool;
+  const int* h_level_off; /* host copy of level_off (launch grids) */
+} hdk_mf;
+/* W_e = (2 mu_e + lambda_e + beta_e / h) V_e */
+HDK_API int hdk_asm_weights(int ne, const double* mu, const double* lambda, const double* beta, const double* vol,
+                            double h, double* w, void* stream);
+/* out[k] = [diag[k] >= 0] inertia m + sum over corner pairs pair[off[k]..off[k+1]) ((4e+i) << 2 | j) of W_e g_i.g_j */
+HDK_API int hdk_asm_values(int count, const int* off, const int* pair, const int* diag, const double* mass,
+                           double inertia, const double* w, const double* g, double* out, void* stream);
+HDK_API int hdk_gather_values(int count, const int* from, const double* src, double* dst, void* stream);
+/* L (lx, host layout), D and D^{-1/2}; a non-positive pivot sets *err = 8 (NotPositiveDefinite). */
+HDK_API int hdk_mf_factor(const hdk_mf* p, const double* aval, double* lx, double* d, double* dis, int* err,
+                          void* stream);
+
 /* ---- segmented batch (lockstep C5 engine, engine.cpp segments > 1) --------
  * S samples of one mesh as one concatenated problem: sample s owns vertices
  * [s nv, (s+1) nv), elements [s ne, (s+1) ne) and elimination positions

@@ -3,6 +3,8 @@
 // exceptions never cross the boundary); B200 extensions: recorded frames,
 // backward chain, state control and counters.
 #include <cstdlib>
+#include <chrono>
+#include <cmath>
 #include <cstring>
 #include <cstdio>
 #include <memory>
@@ -13,6 +15,7 @@
 #include "batch.hpp"
 #include "engine.hpp"
 #include "drivers.hpp"
+#include "refactor.hpp"
 
 using namespace hdb;
 
@@ -302,6 +305,32 @@ hd_status hd_factor_stats(const hd_scene* scene, char** stats_json) {
     j["weight_contrast"] = s.material.contrast();
     j["refactorizations"] = 1;
     j["inverse_residual"] = factor_inverse_residual(F);
+    if (const char* mc = std::getenv("HETERODYN_MF_CHECK"); mc && std::atoi(mc) != 0) {
+      // the device refactorization's plan and its CPU reference against the host LDL^T
+      const HostFactor G = build_factor(s.mesh, s.material, s.solver.h, s.fixed, s.ordering, true);
+      const auto t0 = std::chrono::steady_clock::now();
+      const MfPlan P = mf_plan(G);
+      Vec lx, d;
+      mf_factor_host(P, G.a_ff.val, lx, d);
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      double lmax = 0, dmax = 0, lnorm = 0;
+      for (size_t k = 0; k < lx.size(); ++k) {
+        lmax = std::max(lmax, std::fabs(lx[k] - G.build.lx[k]));
+        lnorm = std::max(lnorm, std::fabs(G.build.lx[k]));
+      }
+      for (int i = 0; i < G.n; ++i) {
+        const double di = 1.0 / std::sqrt(d[i]);
+        dmax = std::max(dmax, std::fabs(di - G.build.dis[i]) / G.build.dis[i]);
+      }
+      long long flops = 0;
+      for (int q = 0; q < P.nsuper; ++q) {
+        const long long m = P.fm[q], p = P.sfirst[q + 1] - P.sfirst[q];
+        for (long long c = 0; c < p; ++c) flops += (m - c) * (m - c);
+      }
+      j["mf_check"] = {{"supernodes", P.nsuper}, {"levels", P.nlevels}, {"pool_doubles", P.pool},
+                       {"max_front", P.max_front}, {"lx_max_abs_diff_rel", lnorm > 0 ? lmax / lnorm : 0.0},
+                       {"dis_max_rel_diff", dmax}, {"host_ms", ms}, {"front_update_flops", flops}};
+    }
     if (stats_json) *stats_json = dup(j.dump(2));
   });
 }

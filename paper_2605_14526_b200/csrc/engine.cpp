@@ -1,6 +1,8 @@
 // Device-resident forward/backward engine (see engine.hpp).
 #include "engine.hpp"
 
+#include <chrono>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -1300,10 +1302,27 @@ bool same_structure(const HostFactor& a, const HostFactor& b) {
 }  // namespace
 
 void Engine::set_young(const Vec& young, bool freeze) {
+  const auto t0 = std::chrono::steady_clock::now();
   if (freeze) mat_.freeze();
   if (segs_ > 1) segmented_set_young(mat_, young, scene_.mesh.vol, segs_);
   else mat_.set_young(young, scene_.mesh.vol);
   cuda_check(cudaStreamSynchronize(st_), "sync");
+  if (refactor_on_device()) {
+    // same pattern, ordering and stream layout: values only, all on the device
+    upload_material();
+    refactor_device_values();
+    ++refactor_count;
+    cols_.reset();
+    slots_.clear();
+    frame_mem_.clear();
+    nrec_ = 0;
+    build_forward_graph();
+    build_backward_graph();
+    last_refactor_device = true;
+    last_refactor_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return;
+  }
+  last_refactor_device = false;
   HostFactor nf = build_factor(scene_.mesh, mat_, scene_.solver.h, scene_.fixed, scene_.ordering, device_values_,
                                &order_cache_, &hf_);
   ++refactor_count;

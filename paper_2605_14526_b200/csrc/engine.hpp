@@ -202,6 +202,17 @@ class Engine {
   int last_backward_iterations_ = 0;
   Vec solve_free(const double* rhs, const double* fixed_q);
   void set_young(const Vec& young, bool freeze);
+  // Device refactorization (engine_refactor.cpp, refactor.cu): the numeric
+  // part of a same-pattern set_young on the GPU.  Plans are built on first use.
+  struct DeviceRefactor;
+  struct DeviceRefactorDeleter {
+    void operator()(DeviceRefactor* p) const;
+  };
+  std::unique_ptr<DeviceRefactor, DeviceRefactorDeleter> drf_;
+  bool refactor_on_device();  // false: this factor cannot (host path)
+  void refactor_device_values();
+  double last_refactor_ms = 0;  // host wall time of the last set_young
+  bool last_refactor_device = false;
 
   Vec positions() const;
   Vec velocities() const;

@@ -752,6 +752,7 @@ HostFactor build_factor(const Mesh& mesh, const Material& mat, double h, const s
     for (int v = n - 1; v >= 0; --v) B.depth[v] = parent[v] < 0 ? 0 : B.depth[parent[v]] + 1;  // parent > v
     B.max_depth = n ? *std::max_element(B.depth.begin(), B.depth.end()) : 0;
     B.lp = lp;
+    B.li = li;
     B.ldist.resize(li.size());
     for (int v = 0; v < n; ++v)
       for (long long p = lp[v]; p < lp[v + 1]; ++p) B.ldist[p] = B.depth[v] - B.depth[li[p]];

@@ -125,6 +125,7 @@ struct ChunkDesc { long long off; int len, seg0, nseg, tile; };  // device chunk
 struct DeviceBuild {
   std::vector<int> parent, depth, ldist, row_first, seg_clo;
   std::vector<long long> lp, seg_off;
+  std::vector<int> li;  // L row indices by column (the device refactorization's symbolic input)
   Vec lx, dis;
   int max_depth = 0;
 };
