@@ -515,6 +515,7 @@ typedef struct hdk_mf {
   const long long* lp;    /* L by columns */
   double* pool;
   const int* h_level_off; /* host copy of level_off (launch grids) */
+  const int* h_level_maxm; /* host: largest front per level (CTA width) */
 } hdk_mf;
 /* W_e = (2 mu_e + lambda_e + beta_e / h) V_e */
 HDK_API int hdk_asm_weights(int ne, const double* mu, const double* lambda, const double* beta, const double* vol,

@@ -1309,8 +1309,14 @@ void Engine::set_young(const Vec& young, bool freeze) {
   cuda_check(cudaStreamSynchronize(st_), "sync");
   if (refactor_on_device()) {
     // same pattern, ordering and stream layout: values only, all on the device
+    const auto lap = [&t0] {
+      return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    };
+    const double t_mat = lap();
     upload_material();
+    const double t_up = lap();
     refactor_device_values();
+    const double t_num = lap();
     ++refactor_count;
     cols_.reset();
     slots_.clear();
@@ -1319,7 +1325,10 @@ void Engine::set_young(const Vec& young, bool freeze) {
     build_forward_graph();
     build_backward_graph();
     last_refactor_device = true;
-    last_refactor_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    last_refactor_ms = lap();
+    if (const char* tr = std::getenv("HETERODYN_REFACTOR_TRACE"); tr && std::atoi(tr) != 0)
+      std::fprintf(stderr, "[refactor] material %.2f ms, upload %.2f ms, device numeric %.2f ms, graphs %.2f ms\n",
+                   t_mat, t_up - t_mat, t_num - t_up, last_refactor_ms - t_num);
     return;
   }
   last_refactor_device = false;

@@ -4,7 +4,9 @@
 // is re-assembled, LDL^T re-factored (multifrontal) and S' rebuilt on the
 // GPU, straight into the engine's buffers.  Reference: factor.cpp:11-136
 // (SparseFactor::factorize, assemble_global_scalar), material.cpp set_young.
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "engine.hpp"
@@ -19,7 +21,7 @@ void hdk_check_r(int e, const char* what) { cuda_check(static_cast<cudaError_t>(
 struct Engine::DeviceRefactor {
   DevArena mem;
   hdk_mf mf{};
-  std::vector<int> h_level_off;
+  std::vector<int> h_level_off, h_level_maxm;
   hdk_inverse_build build{};
   double *lx = nullptr, *d = nullptr, *dis = nullptr, *g = nullptr, *w = nullptr, *beta = nullptr;
   double* fd_tmp = nullptr;
@@ -61,6 +63,11 @@ bool Engine::refactor_on_device() {
   v.pool = A.alloc<double>(static_cast<size_t>(P.pool));
   R->h_level_off = P.level_off;
   v.h_level_off = R->h_level_off.data();
+  R->h_level_maxm.assign(P.nlevels, 0);
+  for (int L = 0; L < P.nlevels; ++L)
+    for (int q = P.level_off[L]; q < P.level_off[L + 1]; ++q)
+      R->h_level_maxm[L] = std::max(R->h_level_maxm[L], P.fm[P.level_node[q]]);
+  v.h_level_maxm = R->h_level_maxm.data();
   R->lx = A.alloc<double>(static_cast<size_t>(P.lp[P.n]));
   R->d = A.alloc<double>(P.n);
   R->dis = A.alloc<double>(P.n);
@@ -127,8 +134,25 @@ void Engine::refactor_device_values() {
                                const_cast<double*>(a_fd_.val), s), "A_fd values");
     hdk_check_r(hdk_gather_values(R.n_fd, R.df_from, a_fd_.val, const_cast<double*>(a_df_.val), s), "A_df values");
   }
+  const bool trace = std::getenv("HETERODYN_REFACTOR_TRACE") != nullptr;
+  cudaEvent_t ev[4] = {};
+  if (trace)
+    for (cudaEvent_t& e : ev) cuda_check(cudaEventCreate(&e), "event");
+  if (trace) cuda_check(cudaEventRecord(ev[0], st_), "event");
   hdk_check_r(hdk_mf_factor(&R.mf, a_ff_.val, R.lx, R.d, R.dis, R.err, s), "multifrontal LDL^T");
+  if (trace) cuda_check(cudaEventRecord(ev[1], st_), "event");
   hdk_check_r(hdk_inverse_values(&R.build, const_cast<double*>(df_.sval), s), "S' values");
+  if (trace) {
+    cuda_check(cudaEventRecord(ev[2], st_), "event");
+    cuda_check(cudaEventSynchronize(ev[2]), "event");
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    std::fprintf(stderr, "[refactor] device: multifrontal LDL^T %.3f ms (%d levels, %d fronts), S' values %.3f ms\n", a,
+                 R.mf.nlevels, R.mf.nsuper, b);
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  }
   int err = 0;
   cuda_check(cudaMemcpyAsync(&err, R.err, sizeof(int), cudaMemcpyDeviceToHost, st_), "refactor status");
   cuda_check(cudaStreamSynchronize(st_), "refactor");

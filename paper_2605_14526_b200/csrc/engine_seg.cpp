@@ -84,8 +84,14 @@ void segmented_set_young(Material& mat, const Vec& young, const Vec& vol, int sa
     raise(Code::Validation, "set_young: element count mismatch");
   const Vec vol1(vol.begin(), vol.begin() + ne);
   for (int k = 0; k < samples; ++k) {
-    Material mk = mat;
-    for (Vec* v : {&mk.young, &mk.mu, &mk.lambda, &mk.beta}) v->assign(v->begin() + k * ne, v->begin() + (k + 1) * ne);
+    Material mk;  // the copy's scalars and its slices (not the whole concatenation)
+    mk.kind = mat.kind;
+    mk.barrier = mat.barrier;
+    mk.poisson = mat.poisson;
+    mk.alpha = mat.alpha;
+    mk.beta0 = mat.beta0;
+    mk.frozen = mat.frozen;
+    mk.young.assign(mat.young.begin() + k * ne, mat.young.begin() + (k + 1) * ne);
     if (mat.frozen) {
       mk.mu_bar = mat.seg_means[3 * k];
       mk.lambda_bar = mat.seg_means[3 * k + 1];

@@ -11,7 +11,6 @@
 
 namespace {
 
-constexpr int kT = 256;
 constexpr int kPanel = HDK_MF_PANEL;
 
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
@@ -53,6 +52,7 @@ __global__ void k_gather_values(int count, const int* __restrict__ from, const d
 
 // One front per CTA: assembly (A entries, children's update blocks in
 // order), blocked partial LDL^T of the pivot columns, L and D written out.
+template <int kT>
 __global__ void __launch_bounds__(kT) k_mf_level(hdk_mf p, int level, const double* __restrict__ aval,
                                                  double* __restrict__ lx, double* __restrict__ d, int* err) {
   const int s = p.level_node[p.level_off[level] + blockIdx.x];
@@ -154,9 +154,10 @@ HDK_API int hdk_gather_values(int count, const int* from, const double* src, dou
 
 HDK_API int hdk_mf_factor(const hdk_mf* p, const double* aval, double* lx, double* d, double* dis, int* err,
                           void* stream) {
-  for (int L = 0; L < p->nlevels; ++L) {
+  for (int L = 0; L < p->nlevels; ++L) {  // wide CTAs where the fronts are large (the top levels)
     const int fronts = p->h_level_off[L + 1] - p->h_level_off[L];
-    k_mf_level<<<fronts, kT, 0, S(stream)>>>(*p, L, aval, lx, d, err);
+    if (p->h_level_maxm[L] >= 192) k_mf_level<1024><<<fronts, 1024, 0, S(stream)>>>(*p, L, aval, lx, d, err);
+    else k_mf_level<256><<<fronts, 256, 0, S(stream)>>>(*p, L, aval, lx, d, err);
   }
   k_dis<<<nb(p->n), 256, 0, S(stream)>>>(p->n, d, dis);
   return last();
