@@ -370,6 +370,21 @@ def run_batch(args, world, rank):
     t_ref = time.perf_counter()
     b.set_young(young[mine.start:mine.stop] * 1.0001)
     t_ref = time.perf_counter() - t_ref
+    # L-BFGS-shaped steps: a parameter update (device refactorization of every
+    # sample) before each evaluation — the throughput a system-ID loop sees
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e4 = torch.cuda.Event(enable_timing=True)
+    e5 = torch.cuda.Event(enable_timing=True)
+    e4.record()
+    for k in range(args.steps):
+        b.set_young(young[mine.start:mine.stop] * (1.0 + 1e-4 * (k + 2)))
+        b.evaluate(args.frames, device_out=buf.data_ptr(), want_host=False)
+        reduced()
+    e5.record()
+    e5.synchronize()
+    ms_upd = max_over_ranks(e4.elapsed_time(e5))
     b.set_young(young[mine.start:mine.stop])
 
     # roofline of the dominant kernel: the batch's solve (lockstep: one
@@ -409,6 +424,7 @@ def run_batch(args, world, rank):
                        "samples_per_rank": len(mine), "host_threads_per_rank": threads,
                        "batch_engine": "lockstep (one segmented engine per rank)" if b.lockstep else "one engine per sample",
                        "engine_build_s": t_build, "set_young_s": t_ref,
+                       "steps_per_s_with_refactorization": units / (ms_upd / 1e3),
                        "l2_policy": "per-sample factors 64 x ~%.0f MB exceed L2" %
                                                                (probe.factor_nnz * 8 / 1e6),
                        "device_busy_ms_per_step": dev_ms / args.steps,

@@ -609,6 +609,133 @@ __global__ void __launch_bounds__(kThreads, 1) k_rowdot_c2(hdk_factor f, const d
   }
 }
 
+// ---- pass 1 of the multi-column solve on the FP64 tensor cores ---------------
+// With R columns every staged value of S' meets 3R right-hand sides.  Eight
+// segments of a chunk form the rows of an m8n8k4 DMMA tile: A = their values
+// over four tile columns (zero outside each row's range), B = those columns'
+// right-hand sides staged per tile in shared memory, D accumulates the eight
+// row dots of up to eight right-hand sides in registers over the group's
+// column range — no per-lane predicated FMA sweep over all 256 columns and no
+// shuffle reduction per segment, and the small register footprint lets 16
+// consumer warps hide the shared-memory latency.  Fragment layout
+// (mma.m8n8k4.row.col.f64): A(g, t), B(t, g), D(g, 2t + i) with
+// g = lane / 4, t = lane % 4.  The sums run in k order inside the tensor core:
+// same values as the FMA passes up to rounding.
+constexpr int kWarpsMma = 16;
+constexpr int kStagesMma = 6;
+template <int R>
+struct MmaPass1Smem {
+  // row pitch 8 NB + 4: the 16 lanes of a half-warp (4 t x 4 g) hit 16 distinct 8-byte banks
+  static constexpr int NQ = 3 * R, NB = (NQ + 7) / 8, LD = 8 * NB + 4;
+  Ring<kStagesMma> ring;
+  double bt[kW * LD];  // the tile's right-hand sides: bt[col * LD + q], q = 3 column + axis
+};
+
+__device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void mma_consumers_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarpsMma) : "memory");
+}
+
+template <int R>
+__global__ void __launch_bounds__(32 * (kWarpsMma + 1), 1) k_rowdot_mma(hdk_factor f, const double* __restrict__ rhs) {
+  using Sm = MmaPass1Smem<R>;
+  constexpr int NQ = Sm::NQ, NB = Sm::NB, LD = Sm::LD, S = kStagesMma, W = kWarpsMma;
+  hdk::pdl_trigger();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
+  Ring<S>& ring = sm.ring;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  ring_init(ring, W);
+  const int c_beg = f.first1 ? f.first1[blockIdx.x] : range_first(blockIdx.x, gridDim.x, f.n_chunks);
+  const int c_end = f.first1 ? f.first1[blockIdx.x + 1] : range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
+  if (warp == W) {
+    produce(f, ring, c_beg, c_end, false);
+    return;
+  }
+  HDK_TRACED_WAIT(hdk::kTrRowdot);
+  if (f.run_flag && *f.run_flag == 0) return;
+  const int g = lane >> 2, t = lane & 3;
+  const size_t ps = 3 * (size_t)f.n_pslot;
+  int tile = -1;
+  for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
+    const int st = k % S;
+    mbar_wait(&ring.full[st], (k / S) & 1);
+    const ChunkInfo ch = ring.info[st];
+    if (ch.tile != tile) {  // every consumer warp reaches the new tile at this chunk
+      mma_consumers_sync();
+      tile = ch.tile;
+      for (int e = threadIdx.x; e < kW * 8 * NB; e += 32 * W) {
+        const int col = e / (8 * NB), q = e - col * (8 * NB);
+        const int gc = tile * kW + col;
+        double v = 0.0;
+        if (q < NQ && gc < f.n) v = __ldg(rhs + (size_t)(q / 3) * 3 * (size_t)f.n + 3 * (size_t)gc + (q % 3));
+        sm.bt[col * LD + q] = v;
+      }
+      mma_consumers_sync();
+    }
+    const double* vals = ring.vals[st];
+    const int ngroups = (ch.nseg + 7) >> 3;
+    for (int grp = (warp - (ch.seg0 >> 3)) & (W - 1); grp < ngroups; grp += W) {
+      const int i = 8 * grp + g;
+      const bool live = i < ch.nseg;
+      const hdk_seg sg = ring.segs[st][live ? i : 0];
+      const int lo = live ? (sg.clo_len & 0xffff) : kW;
+      const int hi = live ? lo + (sg.clo_len >> 16) : 0;
+      int ulo = lo, uhi = hi;
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        ulo = min(ulo, __shfl_xor_sync(0xffffffffu, ulo, o));
+        uhi = max(uhi, __shfl_xor_sync(0xffffffffu, uhi, o));
+      }
+      const double* v = vals + sg.coff - lo;
+      // four accumulator sets over consecutive k-steps: four independent DMMA
+      // chains per n-block instead of one (the tensor core's latency, not its
+      // rate, bounded the single chain)
+      constexpr int kAcc = 4;
+      double d[kAcc][NB][2];
+#pragma unroll
+      for (int u = 0; u < kAcc; ++u)
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) d[u][nb][0] = d[u][nb][1] = 0.0;
+      int kc = ulo & ~3;
+      for (; kc + 4 * (kAcc - 1) < uhi; kc += 4 * kAcc) {
+#pragma unroll
+        for (int u = 0; u < kAcc; ++u) {
+          const int col = kc + 4 * u + t;
+          const double a = (col >= lo && col < hi) ? v[col] : 0.0;
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) dmma_m8n8k4(d[u][nb], a, sm.bt[col * LD + 8 * nb + g]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kAcc - 1; ++u) {  // remainder: at most kAcc - 1 k-steps (warp-uniform bound)
+        if (kc + 4 * u >= uhi) break;
+        const int col = kc + 4 * u + t;
+        const double a = (col >= lo && col < hi) ? v[col] : 0.0;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) dmma_m8n8k4(d[u][nb], a, sm.bt[col * LD + 8 * nb + g]);
+      }
+      if (live) {
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int q = 8 * nb + 2 * t + j;
+            if (q < NQ)
+              f.part1[(size_t)(q / 3) * ps + 3 * (size_t)sg.pslot + (q % 3)] =
+                  ((d[0][nb][j] + d[1][nb][j]) + d[2][nb][j]) + d[3][nb][j];
+          }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[st]);
+  }
+}
+
 // z-fold: one warp per task.  (Folding z in the row-dot kernel's epilogue
 // behind a grid barrier measured 1-2 us slower than this separate launch.)
 __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
@@ -871,6 +998,122 @@ __global__ void __launch_bounds__(kThreads2, 1) k_coltile_c2(hdk_factor f) {
   }
 }
 
+// ---- pass 2 of the multi-column solve on the FP64 tensor cores ---------------
+// x_tile (256 columns x 3R) += S'(segments, tile)^T z(segments): an m8n8k4
+// DMMA takes eight tile columns (M), four segments (K) and eight right-hand
+// sides (N).  Consumer warp w owns tile columns [16 w, 16 w + 16) for the
+// whole tile, so its accumulators stay in registers (no cross-warp fold) and
+// are written as the CTA's tile partial when the tile ends; a group of four
+// segments that misses the warp's columns is skipped.  z rows are staged by
+// the gather warp exactly as for the FMA pass.
+constexpr int kWarpsMma2 = 16;
+template <int R>
+struct MmaPass2Smem {
+  Ring2<Stages2<R>::value, R> ring;
+};
+
+template <int R>
+__device__ __forceinline__ void coltile_mma_write(const hdk_factor& f, int slot, int warp, double (&d)[2][(3 * R + 7) / 8][2]) {
+  constexpr int NQ = 3 * R, NB = (NQ + 7) / 8;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int mb = 0; mb < 2; ++mb) {
+    const int col = 16 * warp + 8 * mb + g;
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int q = 8 * nb + 2 * t + j;
+        if (q < NQ) f.part2[(size_t)(q / 3) * part2_stride(f) + 3 * ((size_t)slot * kW + col) + (q % 3)] = d[mb][nb][j];
+        d[mb][nb][j] = 0.0;
+      }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(32 * (kWarpsMma2 + 2), 1) k_coltile_mma(hdk_factor f) {
+  constexpr int S = Stages2<R>::value, NQ = 3 * R, NB = (NQ + 7) / 8, W = kWarpsMma2;
+  static_assert(W * 16 == kW, "16 columns per consumer warp");
+  hdk::pdl_trigger();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  MmaPass2Smem<R>& sm = *reinterpret_cast<MmaPass2Smem<R>*>(smem_raw);
+  Ring2<S, R>& ring = sm.ring;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < S; ++st) {
+      mbar_init(&ring.full[st], 1);
+      mbar_init(&ring.zfull[st], 32);
+      mbar_init(&ring.empty[st], W);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int c_beg = f.first2 ? f.first2[blockIdx.x] : range_first(blockIdx.x, gridDim.x, f.n_chunks);
+  const int c_end = f.first2 ? f.first2[blockIdx.x + 1] : range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
+  if (warp == W) {
+    stream2(f, ring, c_beg, c_end);
+    return;
+  }
+  HDK_TRACED_WAIT(hdk::kTrColtile);
+  if (f.run_flag && *f.run_flag == 0) return;
+  if (warp == W + 1) {
+    gather_z(f, ring, c_end - c_beg);
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  const int wlo = 16 * warp, whi = wlo + 16;
+  double d[2][NB][2];
+#pragma unroll
+  for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) d[mb][nb][0] = d[mb][nb][1] = 0.0;
+  int tile = -1;
+  for (int k = 0; k < c_end - c_beg; ++k) {
+    const int st = k % S;
+    mbar_wait(&ring.zfull[st], (k / S) & 1);
+    const ChunkInfo ch = ring.info[st];
+    if (ch.tile != tile) {
+      if (tile >= 0) coltile_mma_write<R>(f, tile + blockIdx.x, warp, d);
+      tile = ch.tile;
+    }
+    const double* vals = ring.vals[st];
+    for (int kg = 0; 4 * kg < ch.nseg; ++kg) {
+      const int i = 4 * kg + t;
+      const bool live = i < ch.nseg;
+      const hdk_seg sg = ring.segs[st][live ? i : 0];
+      const int lo = live ? (sg.clo_len & 0xffff) : kW;
+      const int hi = live ? lo + (sg.clo_len >> 16) : 0;
+      int ulo = lo, uhi = hi;
+      ulo = min(ulo, __shfl_xor_sync(0xffffffffu, ulo, 1));
+      uhi = max(uhi, __shfl_xor_sync(0xffffffffu, uhi, 1));
+      ulo = min(ulo, __shfl_xor_sync(0xffffffffu, ulo, 2));
+      uhi = max(uhi, __shfl_xor_sync(0xffffffffu, uhi, 2));
+      if (uhi <= wlo || ulo >= whi) continue;  // no column of this warp (uniform over the warp)
+      double b[NB];
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        const int q = 8 * nb + g;
+        b[nb] = (live && q < NQ) ? ring.zs[st][i][q] : 0.0;
+      }
+      const double* v = vals + sg.coff - lo;
+#pragma unroll
+      for (int mb = 0; mb < 2; ++mb) {
+        const int c0 = wlo + 8 * mb;
+        if (uhi <= c0 || ulo >= c0 + 8) continue;
+        const int col = c0 + g;
+        // A(m = g, k = t) = S'(segment t, column c0 + g): each lane needs its
+        // segment t's value at column col (lanes of one t share a segment)
+        const double a = (col >= lo && col < hi) ? v[col] : 0.0;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) dmma_m8n8k4(d[mb][nb], a, b[nb]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[st]);
+  }
+  if (tile >= 0) coltile_mma_write<R>(f, tile + blockIdx.x, warp, d);
+}
+
 // x_c = sum of the tile partials of the CTAs whose chunk ranges touch the
 // column's tile (CTA order), scattered to the full vector.
 template <bool kScatter>
@@ -911,6 +1154,14 @@ const Grids& grids() {
     const int sc2 = static_cast<int>(sizeof(Ring<kStagesC2>));
     cudaFuncSetAttribute(k_rowdot_c2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc2);
     cudaFuncSetAttribute(k_rowdot_c2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc2);
+    cudaFuncSetAttribute(k_coltile_mma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(MmaPass2Smem<2>)));
+    cudaFuncSetAttribute(k_coltile_mma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(MmaPass2Smem<4>)));
+    cudaFuncSetAttribute(k_rowdot_mma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(MmaPass1Smem<2>)));
+    cudaFuncSetAttribute(k_rowdot_mma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(MmaPass1Smem<4>)));
     cudaFuncSetAttribute(k_coltile<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(Pass2Smem<2>)));
     cudaFuncSetAttribute(k_coltile<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -949,18 +1200,26 @@ int launch_multi(const hdk_factor* f, const double* rhs, cudaStream_t st) {
   // on pass 2's grid and chunk ranges
   hdk_factor f1 = *f;
   f1.first1 = f->first2;
-  static const bool c2 = [] {
-    const char* e = std::getenv("HETERODYN_ROWDOT_C2");  // "0": one column per warp (A/B)
-    return !(e && e[0] == '0');
+  static const int mode1 = [] {  // pass 1: 2 = FP64 tensor cores (default), 1 = two columns per warp, 0 = one
+    const char* e = std::getenv("HETERODYN_ROWDOT");
+    if (e) return std::atoi(e);
+    const char* c = std::getenv("HETERODYN_ROWDOT_C2");
+    return (c && c[0] == '0') ? 0 : 2;
   }();
-  if (c2) hdk::launch(k_rowdot_c2<R>, dim3(g2), dim3(kThreads), sizeof(Ring<kStagesC2>), st, f1, rhs);
+  if (mode1 == 2)
+    hdk::launch(k_rowdot_mma<R>, dim3(g2), dim3(32 * (kWarpsMma + 1)), sizeof(MmaPass1Smem<R>), st, f1, rhs);
+  else if (mode1 == 1) hdk::launch(k_rowdot_c2<R>, dim3(g2), dim3(kThreads), sizeof(Ring<kStagesC2>), st, f1, rhs);
   else hdk::launch(k_rowdot<false, R, 16>, dim3(g2), dim3(Pass1<16>::threads), sizeof(Ring<Pass1<16>::stages>), st, f1, rhs);
   hdk::launch(k_zreduce, dim3((f->n_ztask + 7) / 8, R), dim3(256), 0, st, *f);
-  static const bool t2 = [] {
-    const char* e = std::getenv("HETERODYN_COLTILE_C2");  // "0": one column per warp (A/B)
-    return !(e && e[0] == '0');
+  static const int mode2 = [] {  // pass 2: 1 = two columns per warp (default), 2 = FP64 tensor cores, 0 = one
+    const char* e = std::getenv("HETERODYN_COLTILE");
+    if (e) return std::atoi(e);
+    const char* c = std::getenv("HETERODYN_COLTILE_C2");
+    return (c && c[0] == '0') ? 0 : 1;
   }();
-  if (t2) hdk::launch(k_coltile_c2<R>, dim3(g2), dim3(kThreads2), sizeof(Pass2Smem<R>), st, *f);
+  if (mode2 == 2)
+    hdk::launch(k_coltile_mma<R>, dim3(g2), dim3(32 * (kWarpsMma2 + 2)), sizeof(MmaPass2Smem<R>), st, *f);
+  else if (mode2 == 1) hdk::launch(k_coltile_c2<R>, dim3(g2), dim3(kThreads2), sizeof(Pass2Smem<R>), st, *f);
   else hdk::launch(k_coltile<false, R>, dim3(g2), dim3(kThreads2), sizeof(Pass2Smem<R>), st, *f);
   return static_cast<int>(cudaGetLastError());
 }
