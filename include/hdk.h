@@ -295,6 +295,10 @@ HDK_API size_t hdk_bb_result_bytes(void);
 /* *any = OR over count (<= 32) control blocks of "still iterating"; sets the
  * WHILE condition when cond_handle != 0 (multi-column contact adjoint). */
 HDK_API int hdk_any_cond(hdk_ctl* ctls, int count, int* any, unsigned long long cond_handle, void* stream);
+/* *any = 1 while exactly *expected (> 0) of the count columns are still iterating
+ * (the contact-adjoint column refill loop); sets the WHILE condition. */
+HDK_API int hdk_cols_cond(hdk_ctl* ctls, int count, const int* expected, int* any, unsigned long long cond_handle,
+                          void* stream);
 HDK_API int hdk_bb_mix(const hdk_factor* f, hdk_ctl* ctl, const hdk_ctl* snap, const void* result,
                        const double* t_perm, double* x_perm, double* x_full, const double* sum_hist,
                        const double* rt_perm, double* rx_perm, double* last_rx, double* last_rg, double* rsum_hist,

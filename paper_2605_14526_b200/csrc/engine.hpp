@@ -195,6 +195,13 @@ class Engine {
   // Solves rows [r0, r0 + kColumns) of contact frame c (rows past k repeat
   // the last one); returns the iterations of the real columns.
   int solve_columns(const ContactFrame& c, int r0);
+  // All K columns of contact frame c through the kColumns slots, a finished
+  // slot refilled with the next row (the loop exits when a column finishes);
+  // returns the columns' iterations.  Opt-in (HETERODYN_COLUMN_REFILL=1): the
+  // per-refill host round trip cost more than the idle slots it saved; the
+  // default is batches of kColumns rows (solve_columns).
+  int solve_all_columns(const ContactFrame& c);
+  void column_pre(int slot);
   void columns_body(unsigned long long cond_handle, unsigned skip);
   double time_columns(int reps, unsigned skip);  // profiling: ms per multi-column iteration
   void trace_loop(std::vector<double>& out);

@@ -38,9 +38,14 @@ struct Engine::ColumnSet {
   int* any = nullptr;         // OR of the columns' cond
   int* h_any = nullptr;
   LoopGraph graph;
+  LoopGraph rgraph;          // refill loop: one iteration per body, exits when a column finishes
+  int* expected = nullptr;   // columns iterating at launch (device)
+  int* h_expected = nullptr;
   hdk_bb_columns bb{};  // every column's backbone buffers, for the one-launch-per-stage body
   ~ColumnSet() {
     graph.destroy();
+    rgraph.destroy();
+    if (h_expected) cudaFreeHost(h_expected);
     for (Col& c : col) {
       for (cudaEvent_t e : {c.fork, c.mid, c.join, c.end})
         if (e) cudaEventDestroy(e);
@@ -69,6 +74,8 @@ void Engine::build_columns() {
   S.ctls = A.alloc<hdk_ctl>(kColumns);
   S.rhs = A.alloc<double>(kColumns * n3p);
   S.any = A.alloc<int>(1);
+  S.expected = A.alloc<int>(1);
+  cuda_check(cudaMallocHost(&S.h_expected, sizeof(int)), "pinned expected");
   S.f.run_flag = S.any;
   cuda_check(cudaMallocHost(&S.h_ctls, sizeof(hdk_ctl) * kColumns), "pinned ctl");
   cuda_check(cudaMallocHost(&S.h_any, sizeof(int)), "pinned flag");
@@ -138,9 +145,96 @@ void Engine::build_columns() {
     for (int u = 0; u < unroll_; ++u) columns_body(handle, 0u);
   };
   build_loop_graph(st_, use_cond_, pre, body, [] {}, S.graph);
+  // refill loop: no pre (slots are initialised one by one), one iteration per body
+  auto rbody = [&](unsigned long long handle) { columns_body(handle, 4u); };
+  build_loop_graph(st_, use_cond_, [] {}, rbody, [] {}, S.rgraph);
 }
 
-// One multi-column iteration; skip bits (profiling): 1 solve, 2 column kernels.
+// First right-hand side seed + R(x0) of one slot (the pre step of the loop, per column).
+void Engine::column_pre(int j) {
+  ColumnSet& S = *cols_;
+  ColumnSet::Col& C = S.col[j];
+  void* s = st_;
+  const size_t n3p = 3 * static_cast<size_t>(hf_.n);
+  hdk_ok(hdk_aa_reset(C.ctl, HDK_AA_MAX, 1e8, 500, 1e-10, s), "aa reset");
+  hdk_ok(hdk_gather_perm(&dv_, C.seed, nullptr, C.seedp, s), "seed in elimination order");
+  hdk_ok(hdk_gather_perm(&dv_, C.x, nullptr, C.xp, s), "x0 in elimination order");
+  hdk_ok(hdk_bapply(&dm_, dcomp_, C.x, C.ef, s), "B x0");
+  hdk_ok(hdk_gather_pp(&dv_, nullptr, C.ef, C.rx, nullptr, s), "R(x0)");
+  hdk_ok(hdk_axpby(static_cast<int>(n3p), 1.0, C.seedp, 1.0, C.rx, S.rhs + j * n3p, s), "rhs0");
+  kernel_launches += 6;
+}
+
+int Engine::solve_all_columns(const ContactFrame& c) {
+  if (!cols_) build_columns();
+  ColumnSet& S = *cols_;
+  const int nv = scene_.mesh.nv;
+  const size_t n3 = 3 * static_cast<size_t>(nv);
+  int slot_row[kColumns];
+  int next = 0, active = 0, iters = 0;
+  const auto assign = [&](int j) {
+    if (next < c.k) {
+      slot_row[j] = next;
+      hdk_ok(hdk_contact_column_init(&c.view, next, nv, df_.v2p, S.col[j].seed, S.col[j].x, st_), "column init");
+      column_pre(j);
+      ++next;
+      ++active;
+    } else {
+      slot_row[j] = -1;
+      cuda_check(cudaMemsetAsync(&S.col[j].ctl->cond, 0, sizeof(int), st_), "idle slot");
+    }
+  };
+  for (int j = 0; j < kColumns; ++j) assign(j);
+  if (ph_.on) cuda_check(cudaEventRecord(ph_.ev[6], st_), "phase event");
+  long long rounds = 0;
+  while (active > 0) {
+    *S.h_expected = active;
+    cuda_check(cudaMemcpyAsync(S.expected, S.h_expected, sizeof(int), cudaMemcpyHostToDevice, st_), "expected");
+    const int one = 1;
+    cuda_check(cudaMemcpyAsync(S.any, &one, sizeof(int), cudaMemcpyHostToDevice, st_), "run flag");
+    if (S.rgraph.exec) {
+      cuda_check(cudaGraphLaunch(S.rgraph.exec, st_), "columns");
+    } else {  // host-driven loop (profiling fallback)
+      for (;;) {
+        cuda_check(cudaGraphLaunch(S.rgraph.body, st_), "columns");
+        cuda_check(cudaMemcpyAsync(S.h_any, S.any, sizeof(int), cudaMemcpyDeviceToHost, st_), "flag");
+        cuda_check(cudaStreamSynchronize(st_), "sync");
+        if (!*S.h_any) break;
+      }
+    }
+    ++rounds;
+    cuda_check(cudaMemcpyAsync(S.h_ctls, S.ctls, sizeof(hdk_ctl) * kColumns, cudaMemcpyDeviceToHost, st_), "ctl read");
+    cuda_check(cudaStreamSynchronize(st_), "columns sync");
+    for (int j = 0; j < kColumns; ++j) {
+      if (slot_row[j] < 0) continue;
+      hdk_ctl& h = S.h_ctls[j];
+      if (h.err == 0 && h.nonfinite) h.err = 10;
+      if (h.err != 0) {
+        std::memcpy(h_ctl_, &h, sizeof(hdk_ctl));
+        check_ctl("backward step (contact column)");
+      }
+      if (h.cond != 0) continue;  // still iterating
+      iters += h.iterations;
+      ph_.col_real_iters += h.iterations;
+      cuda_check(cudaMemcpyAsync(cX_ + n3 * slot_row[j], S.col[j].x, n3 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 st_), "column");
+      --active;
+      assign(j);
+    }
+  }
+  if (ph_.on) {
+    cuda_check(cudaEventRecord(ph_.ev[7], st_), "phase event");
+    cuda_check(cudaEventSynchronize(ph_.ev[7]), "phase event");
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ph_.ev[6], ph_.ev[7]) == cudaSuccess) ph_.col_ms += ms;
+  }
+  kernel_launches += static_cast<long long>(S.rgraph.counts[1]) * (iters / kColumns + rounds);
+  ph_.col_batches += rounds;
+  return iters;
+}
+
+// One multi-column iteration; skip bits (profiling): 1 solve, 2 column kernels;
+// bit 4: the refill loop's condition (exit when a column finishes).
 void Engine::columns_body(unsigned long long handle, unsigned skip) {
   ColumnSet& S = *cols_;
   void* s = st_;
@@ -184,7 +278,8 @@ void Engine::columns_body(unsigned long long handle, unsigned skip) {
         cuda_check(cudaEventRecord(C.end, C.s1), "end");
         cuda_check(cudaStreamWaitEvent(st_, C.end, 0), "end wait");
       }
-      hdk_ok(hdk_any_cond(S.ctls, kColumns, S.any, handle, s), "any");
+      if (skip & 4u) hdk_ok(hdk_cols_cond(S.ctls, kColumns, S.expected, S.any, handle, s), "refill cond");
+      else hdk_ok(hdk_any_cond(S.ctls, kColumns, S.any, handle, s), "any");
     }
   }
 }

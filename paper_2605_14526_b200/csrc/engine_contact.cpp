@@ -26,6 +26,8 @@
 
 #include "engine.hpp"
 
+#include <cstdlib>
+
 namespace hdb {
 
 namespace {
@@ -232,7 +234,13 @@ void Engine::backward_frame(int t, GradOut& out) {
     cuda_check(cudaMemcpyAsync(cz0_, x_, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st_), "z0");
     // tangent columns x_c = (A - B)^{-1} j_c warm-started from a_c (backward.cpp:229-238),
     // kColumns at a time through one multi-column stream of the factor
-    for (int r = 0; r < k; r += kColumns) iters += solve_columns(*c, r);
+    static const bool refill = [] {  // opt-in: measured slower
+      const char* e = std::getenv("HETERODYN_COLUMN_REFILL");
+      return e && e[0] == '1';
+    }();
+    if (refill) iters += solve_all_columns(*c);
+    else
+      for (int r = 0; r < k; r += kColumns) iters += solve_columns(*c, r);
     const size_t ms = hdk_contact_scratch_doubles(c->view.cap_k);
     if (ms > cM_len_) {
       if (cM_) cudaFree(cM_);

@@ -713,6 +713,24 @@ __device__ __forceinline__ bool last_block_ticket(unsigned int* ticket) {
   return is_last != 0;
 }
 
+// Refill loop of the contact-adjoint columns: continue while every column
+// that was iterating at launch still is (*expected of them), so the loop
+// exits right after a column finishes and the host hands its slot the next
+// contact row.  *any doubles as the solve's run flag.
+__global__ void k_cols_cond(const hdk_ctl* ctls, int count, const int* expected, int* any,
+                            cudaGraphConditionalHandle handle, int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int c = threadIdx.x;
+  const int on = c < count && ctls[c].cond != 0 && ctls[c].err == 0 && ctls[c].nonfinite == 0;
+  const int active = __popc(__ballot_sync(0xffffffffu, on));
+  if (threadIdx.x == 0) {
+    const int a = (active > 0 && active == *expected) ? 1 : 0;
+    *any = a;
+    if (use_handle) cudaGraphSetConditional(handle, a);
+  }
+}
+
 // OR of several backbone loops' conditions (multi-column contact adjoint).
 __global__ void k_any_cond(const hdk_ctl* ctls, int count, int* any, cudaGraphConditionalHandle handle,
                            int use_handle) {
@@ -1240,6 +1258,13 @@ HDK_API int hdk_aa_dots_fused(const hdk_vtx* x, const hdk_factor* f, hdk_ctl* ct
 
 HDK_API int hdk_trace_epoch(unsigned long long* buf, void* stream) {
   hdk::launch(k_trace_epoch, dim3(1), dim3(1), 0, S(stream), buf);
+  return last();
+}
+
+HDK_API int hdk_cols_cond(hdk_ctl* ctls, int count, const int* expected, int* any, unsigned long long cond_handle,
+                          void* stream) {
+  hdk::launch(k_cols_cond, dim3(1), dim3(32), 0, S(stream), ctls, count, expected, any,
+              static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle != 0ULL ? 1 : 0);
   return last();
 }
 
