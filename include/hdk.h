@@ -162,6 +162,9 @@ HDK_API int hdk_apply_inverse3_perm(const hdk_factor* f, const double* rhs_perm,
  * (12 doubles per element) and, when cache != NULL, the projection cache
  * (24 doubles per element: sigma*, sigma_F, U, V; corotated adds 3 more for
  * the volume target).  Errors: PROX_DIVERGED (6) into *err. */
+/* A/B switch of the local step's Newton direction: 1 = always the 3x3
+ * eigen-solve, 0 = Sherman-Morrison when the eigenvalue floor is inactive. */
+HDK_API int hdk_set_newton_eigen(int on);
 HDK_API int hdk_local_step(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
                            double* cache, int* err, void* stream);
 
@@ -476,7 +479,7 @@ HDK_API int hdk_contact_friction_pushback(const hdk_contacts* c, double* dl_dq, 
 /* Contact-adjoint columns (engine_columns.cpp): the per-column backbone
  * buffers of HDK_BB_COLUMNS columns, so each backbone stage is one launch
  * for all columns (blockIdx.y / blockIdx.x = column). */
-#define HDK_BB_COLUMNS 4
+#define HDK_BB_COLUMNS 8
 typedef struct hdk_bb_column {
   hdk_factor f;  /* the column's view of the multi-column factor (part2 offset) */
   hdk_ctl* ctl;

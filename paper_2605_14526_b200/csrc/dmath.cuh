@@ -267,6 +267,15 @@ struct StretchNH {
       }
     return h;
   }
+  // The same Hessian as diag(d) + lambda u u^T, u_i = 1 / s_i.
+  __device__ __forceinline__ void diag_rank1(const V3& s, V3& d, V3& u) const {
+    const double L = log(s[0] * s[1] * s[2]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      u[i] = 1.0 / s[i];
+      d[i] = mu * (1.0 + u[i] * u[i]) - lambda * L * (u[i] * u[i]);
+    }
+  }
 };
 struct StretchBarrier {
   double mu, lambda;
@@ -293,6 +302,14 @@ struct StretchBarrier {
       }
     return h;
   }
+  __device__ __forceinline__ void diag_rank1(const V3& s, V3& d, V3& u) const {
+    const double L = log(s[0] * s[1] * s[2]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      u[i] = 1.0 / s[i];
+      d[i] = (mu - lambda * L) * (u[i] * u[i]);
+    }
+  }
 };
 
 constexpr double kSigmaFloor = 1e-6;
@@ -304,6 +321,10 @@ __device__ __forceinline__ V3 vmax_floor(const V3& s) { return v3(fmax(s[0], kSi
 // Safeguarded Newton on the principal stretches (newton_on_stretches,
 // localstep.cpp:35-83).  Returns false when stationarity is not reached
 // (ProxDiverged).
+// 1: always take the eigen path (A/B of the Sherman-Morrison direction; set by
+// hdk_set_newton_eigen from HETERODYN_NEWTON_EIGEN).
+__device__ int g_newton_eigen = 0;
+
 template <class D>
 __device__ __forceinline__ bool newton_stretch(const V3& sf, double k, const D& den, V3& s_out, int& iters) {
   V3 s = vmax_floor(sf);
@@ -314,18 +335,33 @@ __device__ __forceinline__ bool newton_stretch(const V3& sf, double k, const D& 
     const V3 r = v3(k * (s[0] - sf[0]) + g[0], k * (s[1] - sf[1]) + g[1], k * (s[2] - sf[2]) + g[2]);
     const double r0 = norm3(r);
     if (r0 <= tol) break;
-    M3 h = den.hessian(s);
-    h(0, 0) += k; h(1, 1) += k; h(2, 2) += k;
-    V3 lam;
-    M3 ev;
-    sym_eig(h, lam, ev);
     const double lo = 1e-8 * k;
-    V3 pr;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) pr[i] = (ev(0, i) * r[0] + ev(1, i) * r[1] + ev(2, i) * r[2]) / fmax(lam[i], lo);
     V3 dir;
+    // H + k I = diag(D) + lambda u u^T.  With lambda >= 0 its eigenvalues are
+    // at least min D (interlacing), so when min D >= the floor 1e-8 k the
+    // floored eigen-solve of localstep.cpp:57-66 is the plain inverse:
+    // Sherman-Morrison, no 3x3 eigen-decomposition.  Otherwise the floor can
+    // act and the eigen path runs as in the reference.
+    V3 dd, u;
+    den.diag_rank1(s, dd, u);
+    const double D0 = dd[0] + k, D1 = dd[1] + k, D2 = dd[2] + k;
+    if (!g_newton_eigen && den.lambda >= 0.0 && fmin(D0, fmin(D1, D2)) >= lo) {
+      const V3 a = v3(r[0] / D0, r[1] / D1, r[2] / D2), b = v3(u[0] / D0, u[1] / D1, u[2] / D2);
+      const double c = den.lambda * dot3(u, a) / (1.0 + den.lambda * dot3(u, b));
 #pragma unroll
-    for (int i = 0; i < 3; ++i) dir[i] = -(ev(i, 0) * pr[0] + ev(i, 1) * pr[1] + ev(i, 2) * pr[2]);
+      for (int i = 0; i < 3; ++i) dir[i] = -(a[i] - b[i] * c);
+    } else {
+      M3 h = den.hessian(s);
+      h(0, 0) += k; h(1, 1) += k; h(2, 2) += k;
+      V3 lam;
+      M3 ev;
+      sym_eig(h, lam, ev);
+      V3 pr;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) pr[i] = (ev(0, i) * r[0] + ev(1, i) * r[1] + ev(2, i) * r[2]) / fmax(lam[i], lo);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) dir[i] = -(ev(i, 0) * pr[0] + ev(i, 1) * pr[1] + ev(i, 2) * pr[2]);
+    }
     const V3 d0 = v3(s[0] - sf[0], s[1] - sf[1], s[2] - sf[2]);
     const double f0 = 0.5 * k * dot3(d0, d0) + den.value(s);
     const double slope = dot3(r, dir);

@@ -201,6 +201,8 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared
   int dev_count = 0;
   if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
     raise(Code::InvalidArgument, "no CUDA device: the B200 engine has no CPU fallback");
+  if (const char* ne = std::getenv("HETERODYN_NEWTON_EIGEN"))
+    hdk_check(hdk_set_newton_eigen(std::atoi(ne) != 0 ? 1 : 0), "newton mode");
   cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "stream");
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");

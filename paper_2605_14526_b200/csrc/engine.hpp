@@ -185,7 +185,7 @@ class Engine {
   // kColumns at a time: one multi-column stream of the factor per iteration,
   // each column's Anderson kernels on its own pair of streams
   // (engine_columns.cpp).
-  static constexpr int kColumns = 4;
+  static constexpr int kColumns = HDK_BB_COLUMNS;
   struct ColumnSet;
   struct ColumnSetDeleter {
     void operator()(ColumnSet* p) const;  // engine_columns.cpp

@@ -473,6 +473,10 @@ inline int blocks(int n, int t) { return (n + t - 1) / t; }
 
 extern "C" {
 
+HDK_API int hdk_set_newton_eigen(int on) {
+  return static_cast<int>(cudaMemcpyToSymbol(g_newton_eigen, &on, sizeof(int)));
+}
+
 HDK_API int hdk_local_step(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
                            double* cache, int* err, void* stream) {
   hdk::launch(k_local, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q, elem_force, cache, err);

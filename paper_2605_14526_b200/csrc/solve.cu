@@ -622,12 +622,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_rowdot_c2(hdk_factor f, const d
 // g = lane / 4, t = lane % 4.  The sums run in k order inside the tensor core:
 // same values as the FMA passes up to rounding.
 constexpr int kWarpsMma = 16;
-constexpr int kStagesMma = 6;
 template <int R>
 struct MmaPass1Smem {
+  static constexpr int S = R >= 8 ? 5 : 6;  // ring depth (the B tile grows with R)
   // row pitch 8 NB + 4: the 16 lanes of a half-warp (4 t x 4 g) hit 16 distinct 8-byte banks
   static constexpr int NQ = 3 * R, NB = (NQ + 7) / 8, LD = 8 * NB + 4;
-  Ring<kStagesMma> ring;
+  Ring<S> ring;
   double bt[kW * LD];  // the tile's right-hand sides: bt[col * LD + q], q = 3 column + axis
 };
 
@@ -643,7 +643,7 @@ __device__ __forceinline__ void mma_consumers_sync() {
 template <int R>
 __global__ void __launch_bounds__(32 * (kWarpsMma + 1), 1) k_rowdot_mma(hdk_factor f, const double* __restrict__ rhs) {
   using Sm = MmaPass1Smem<R>;
-  constexpr int NQ = Sm::NQ, NB = Sm::NB, LD = Sm::LD, S = kStagesMma, W = kWarpsMma;
+  constexpr int NQ = Sm::NQ, NB = Sm::NB, LD = Sm::LD, S = Sm::S, W = kWarpsMma;
   hdk::pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(32 * (kWarpsMma + 1), 1) k_rowdot_mma(hdk_fact
       // four accumulator sets over consecutive k-steps: four independent DMMA
       // chains per n-block instead of one (the tensor core's latency, not its
       // rate, bounded the single chain)
-      constexpr int kAcc = 4;
+      constexpr int kAcc = NB >= 3 ? 2 : 4;  // register budget of 16 consumer warps
       double d[kAcc][NB][2];
 #pragma unroll
       for (int u = 0; u < kAcc; ++u)
@@ -725,9 +725,12 @@ __global__ void __launch_bounds__(32 * (kWarpsMma + 1), 1) k_rowdot_mma(hdk_fact
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int q = 8 * nb + 2 * t + j;
-            if (q < NQ)
-              f.part1[(size_t)(q / 3) * ps + 3 * (size_t)sg.pslot + (q % 3)] =
-                  ((d[0][nb][j] + d[1][nb][j]) + d[2][nb][j]) + d[3][nb][j];
+            if (q < NQ) {
+              double sum = d[0][nb][j];
+#pragma unroll
+              for (int u = 1; u < kAcc; ++u) sum = sum + d[u][nb][j];  // fixed order
+              f.part1[(size_t)(q / 3) * ps + 3 * (size_t)sg.pslot + (q % 3)] = sum;
+            }
           }
       }
     }
@@ -751,7 +754,7 @@ __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
 // with each chunk; 227 KB of shared memory per CTA).
 template <int R>
 struct Stages2 {
-  static constexpr int value = R == 1 ? kStages2 : R == 2 ? 4 : 3;
+  static constexpr int value = R == 1 ? kStages2 : R == 2 ? 4 : R == 4 ? 3 : 2;
 };
 
 template <int R>
@@ -1162,6 +1165,16 @@ const Grids& grids() {
                          static_cast<int>(sizeof(MmaPass1Smem<2>)));
     cudaFuncSetAttribute(k_rowdot_mma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(MmaPass1Smem<4>)));
+    cudaFuncSetAttribute(k_rowdot_mma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(MmaPass1Smem<8>)));
+    cudaFuncSetAttribute(k_coltile_c2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(Pass2Smem<8>)));
+    cudaFuncSetAttribute(k_rowdot_c2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc2);
+    cudaFuncSetAttribute(k_rowdot<false, 8, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, s16);
+    cudaFuncSetAttribute(k_coltile<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(Pass2Smem<8>)));
+    cudaFuncSetAttribute(k_coltile_mma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(MmaPass2Smem<8>)));
     cudaFuncSetAttribute(k_coltile<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(Pass2Smem<2>)));
     cudaFuncSetAttribute(k_coltile<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1278,6 +1291,7 @@ HDK_API int hdk_apply_inverse3_multi(const hdk_factor* f, const double* rhs_perm
     case 1: return launch(f, rhs_perm, nullptr, true, st, false);
     case 2: return launch_multi<2>(f, rhs_perm, st);
     case 4: return launch_multi<4>(f, rhs_perm, st);
+    case 8: return launch_multi<8>(f, rhs_perm, st);
     default: return static_cast<int>(cudaErrorInvalidValue);
   }
 }
