@@ -1321,9 +1321,7 @@ void Engine::set_young(const Vec& young, bool freeze) {
     const double t_num = lap();
     ++refactor_count;
     cols_.reset();
-    slots_.clear();
-    frame_mem_.clear();
-    nrec_ = 0;
+    nrec_ = 0;  // recorded frames are stale; their slots (sized by the mesh) are reused
     build_forward_graph();
     build_backward_graph();
     last_refactor_device = true;
@@ -1355,9 +1353,7 @@ void Engine::set_young(const Vec& young, bool freeze) {
         for (int k = hf_.a_fd.off[p]; k < hf_.a_fd.off[p + 1]; ++k) tv[cur[hf_.a_fd.col[k]]++] = hf_.a_fd.val[k];
       DevArena::copy_h2d(const_cast<double*>(a_df_.val), tv.data(), tv.size() * sizeof(double));
     }
-    slots_.clear();
-    frame_mem_.clear();
-    nrec_ = 0;
+    nrec_ = 0;  // recorded frames are stale; their slots (sized by the mesh) are reused
     build_forward_graph();
     build_backward_graph();
     return;
@@ -1372,9 +1368,7 @@ void Engine::set_young(const Vec& young, bool freeze) {
   build_factor_device();
   set_state(q.data(), v.data(), t);
   set_external_force(f.data());
-  slots_.clear();
-  frame_mem_.clear();
-  nrec_ = 0;
+  nrec_ = 0;  // recorded frames are stale; their slots (sized by the mesh) are reused
   build_forward_graph();
   build_backward_graph();
 }
