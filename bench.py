@@ -627,6 +627,20 @@ def main():
 
     if rank == 0:
         step_share = ms_solve * solves / args.steps / (ms / args.steps)
+        # whole-step algorithmic bytes (SURVEY.md §8(d) with this layout: S' read
+        # twice per solve at 8 B per value, no indices): solves x solve bytes +
+        # per adjoint iteration a B apply (320 B/element) and the Anderson
+        # vectors with their R-space twin (2 x (2m + 4) x 24 B per vertex, m = 8)
+        # + per forward iteration a local sweep (100 B/element) and its vectors
+        # (20 x 24 B per vertex) + the cache / energy sweeps (3 x 100 B/element)
+        n_fwd, n_bwd = float(np.mean(fwd_its)), float(np.mean(bwd_its))
+        nv = sc.vertex_count
+        step_bytes = (solves / args.steps * bytes_solve + n_bwd * (320.0 * ne + 960.0 * nv)
+                      + n_fwd * (100.0 * ne + 480.0 * nv) + 300.0 * ne)
+        step_gbs = step_bytes / (ms / args.steps / 1e3) / 1e9
+        step_roofline = {"bytes_per_step": step_bytes, "achieved_gbs": step_gbs, "frac": step_gbs / peak,
+                         "formula": "solves*(16 nnz(S')+96 n) + N_bwd*(320 n_e + 960 n_v) + N_fwd*(100 n_e + 480 n_v)"
+                                    " + 300 n_e"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -642,7 +656,8 @@ def main():
                        "forward_ms": fwd_ms, "backward_ms": bwd_ms,
                        "solves_per_step": solves / args.steps,
                        "mean_contacts": float(np.mean(contacts[-args.steps:])),
-                       "solve_share_of_step_est": step_share},
+                       "solve_share_of_step_est": step_share,
+                       "step_roofline": step_roofline},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "roofline": roofline,
             "cpu_baseline": cpu,
