@@ -229,7 +229,10 @@ def run_reference(args, scene_dict, world, rank):
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": len(times),
         "warmup": warm, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {scene_dict['name']}", "factorization_s": t_fac},
+        # the GPU arm's workload description, verbatim (same scene, same schedule)
+        "config": {"workload": f"{args.config}: {scene_dict['name']} ({sc.element_count} tets, {sc.vertex_count} vertices, "
+                               f"{WORKLOADS.get(args.config.upper(), '')})",
+                   "parallelism": "replicas" if world > 1 else "single", "factorization_s": t_fac},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                          "sample": f"{warm} warm-up + {len(times)} timed fwd+bwd steps from the scene's initial "
                                    f"state (the GPU arm's schedule), CPU restatement of the reference (Eigen absent: "
