@@ -535,6 +535,30 @@ HDK_API int hdk_gather_values(int count, const int* from, const double* src, dou
 HDK_API int hdk_mf_factor(const hdk_mf* p, const double* aval, double* lx, double* d, double* dis, int* err,
                           void* stream);
 
+/* ---- adjoint backbone by preconditioned CG (pcg.cu) ----------------------
+ * (A - B) x = s with the preconditioner A^{-1}: z = A^{-1} r is the
+ * reference's t - x, so the loop stops on the reference's test
+ * ||z|| <= tol ||x + z|| and returns x + z.  Vectors in elimination order
+ * [n][3]; state on the device; err = -1: p.q <= 0 (not positive definite
+ * along p, the caller falls back to the Anderson backbone), 10: cap. */
+typedef struct hdk_pcg {
+  double rz, pq, alpha, beta, tol;
+  int iter, k_max, done, err, cond;
+} hdk_pcg;
+HDK_API int hdk_pcg_init(hdk_pcg* st, double tol, int k_max, void* stream);
+HDK_API int hdk_pcg_r0(int n3, const double* s, const double* ax, const double* rx, double* r, void* stream);
+HDK_API int hdk_pcg_spmv(const hdk_csr* a, const double* p, double* y, const hdk_pcg* st, void* stream);
+HDK_API int hdk_pcg_rz(int n3, const double* r, const double* z, const double* x, double* partial,
+                       unsigned int* ticket, hdk_pcg* st, void* stream);
+HDK_API int hdk_pcg_cond(const hdk_pcg* st, unsigned long long cond_handle, void* stream);
+HDK_API int hdk_pcg_p(int n, const double* z, double* p, double* pv, const int* p2v, const hdk_pcg* st,
+                      void* stream);
+HDK_API int hdk_pcg_q(int n3, const double* ap, const double* rp, const double* p, double* q, double* partial,
+                      unsigned int* ticket, hdk_pcg* st, void* stream);
+HDK_API int hdk_pcg_xr(int n3, double* x, double* r, const double* p, const double* q, const hdk_pcg* st,
+                       void* stream);
+HDK_API int hdk_pcg_final(int n, const double* x, const double* z, double* x_full, const int* p2v, void* stream);
+
 /* ---- segmented batch (lockstep C5 engine, engine.cpp segments > 1) --------
  * S samples of one mesh as one concatenated problem: sample s owns vertices
  * [s nv, (s+1) nv), elements [s ne, (s+1) ne) and elimination positions

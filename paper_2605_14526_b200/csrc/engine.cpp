@@ -196,6 +196,7 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared
   if (const char* c = std::getenv("HETERODYN_SOLVE_CTAS")) solve_ctas_ = std::atoi(c);
   if (const char* u = std::getenv("HETERODYN_UNROLL")) unroll_ = std::max(1, std::atoi(u));
   if (young) mat_.set_young(*young, scene.mesh.vol);
+  if (const char* ad = std::getenv("HETERODYN_ADJOINT")) use_pcg_ = std::string(ad) == "pcg";
   const char* nc = std::getenv("HETERODYN_NO_COND_GRAPH");
   use_cond_ = !(nc && std::atoi(nc) != 0);
   int dev_count = 0;
@@ -277,6 +278,8 @@ Engine::~Engine() {
     if (e) cudaEventDestroy(e);
   if (fgraph_) fgraph_->destroy();
   if (bgraph_) bgraph_->destroy();
+  if (pgraph_) pgraph_->destroy();
+  if (h_pcg_) cudaFreeHost(h_pcg_);
   cgraph_.destroy();
   for (cudaGraphExec_t e : {bpre_, bpost_a_, bpost_b_})
     if (e) cudaGraphExecDestroy(e);
@@ -694,6 +697,8 @@ void Engine::build_forward_graph() {
 }
 
 void Engine::build_backward_graph() {
+  if (pgraph_) pgraph_->destroy();  // rebuilt on first use (it bakes factor and material pointers)
+  pgraph_.reset();
   if (segs_ > 1) {
     build_backward_graph_seg();
     return;

@@ -259,6 +259,19 @@ class Engine {
   void build_forward_graph_seg();
   void build_backward_graph_seg();
   void backbone_body_seg(unsigned long long cond_handle);
+  // adjoint backbone by preconditioned CG (pcg.cu, engine_pcg.cpp):
+  // HETERODYN_ADJOINT=pcg; falls back to the Anderson loop when A - B is
+  // not positive definite along a search direction
+  bool use_pcg_ = false;
+  std::unique_ptr<LoopGraph> pgraph_;
+  hdk_pcg* pcg_ = nullptr;
+  hdk_pcg* h_pcg_ = nullptr;
+  double *pcg_part_ = nullptr, *pr_ = nullptr, *pz_ = nullptr, *pp_ = nullptr, *pq_ = nullptr, *pap_ = nullptr,
+         *prp_ = nullptr, *ppv_ = nullptr;
+  unsigned int* pcg_ticket_ = nullptr;
+  long long pcg_fallbacks = 0;
+  void build_pcg_graph();
+  bool run_pcg(int& iterations);  // false: fall back to the Anderson backbone
   bool host_any() const;
   void load_frame(int t);  // frame slot t into the backward working buffers
   void sync_ctl();

@@ -205,11 +205,12 @@ void Engine::backward_frame(int t, GradOut& out) {
   phase_mark(3);
   cuda_check(cudaGraphLaunch(bpre_, st_), "backward pre");
   phase_mark(4);
-  run_graph(*bgraph_, "backbone");
+  int pcg_iters = -1;
+  if (!(use_pcg_ && segs_ == 1 && run_pcg(pcg_iters))) run_graph(*bgraph_, "backbone");
   phase_mark(5);
   sync_ctl();
   check_ctl("backward step");
-  int iters = 1 + h_ctl_->iterations;  // the first solve of the backbone counts (backward.cpp:176-178)
+  int iters = pcg_iters >= 0 ? pcg_iters : 1 + h_ctl_->iterations;  // the first solve counts (backward.cpp:176-178)
   if (segs_ > 1) {  // lockstep: every sample's own count, the loop ran to the largest
     seg_tau.resize(segs_);
     for (int k = 0; k < segs_; ++k) {

@@ -1,0 +1,90 @@
+// The adjoint backbone by preconditioned conjugate gradients (pcg.cu): the
+// same linear system and the same stopping test as the reference's Anderson
+// fixed point (backward.cpp:170-204), a Krylov method instead of the
+// window-8 mixing.  One iteration: B p (matrix-free, engine layout), A p
+// (A_ff SpMV), q = A p - B p, the CG updates, one global solve z = A^{-1} r.
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "engine.hpp"
+
+namespace hdb {
+
+namespace {
+void hdk_check_p(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
+}  // namespace
+
+void Engine::build_pcg_graph() {
+  const size_t n3p = 3 * static_cast<size_t>(hf_.n), n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
+  if (!pcg_) {
+    DevArena& A = *mem_;
+    pcg_ = A.alloc<hdk_pcg>(1);
+    pcg_part_ = A.alloc<double>(4 * HDK_RED_BLOCKS);
+    pcg_ticket_ = A.alloc<unsigned int>(1);
+    cuda_check(cudaMemset(pcg_ticket_, 0, sizeof(unsigned int)), "zero ticket");
+    for (double** v : {&pr_, &pz_, &pp_, &pq_, &pap_, &prp_}) *v = A.alloc<double>(n3p);
+    ppv_ = A.alloc<double>(n3);
+    cuda_check(cudaMemset(ppv_, 0, n3 * sizeof(double)), "zero pv");  // fixed vertices stay 0
+    cuda_check(cudaMallocHost(&h_pcg_, sizeof(hdk_pcg)), "pinned pcg");
+  }
+  if (!pgraph_) pgraph_ = std::make_unique<LoopGraph>();
+  void* s = st_;
+  const int n = hf_.n;
+  hdk_factor fs = df_;
+  fs.run_flag = &pcg_->cond;
+  auto pre = [&] {
+    hdk_check_p(hdk_pcg_init(pcg_, 1e-10, 500, s), "pcg init");
+    hdk_check_p(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
+    hdk_check_p(hdk_gather_perm(&dv_, x_, nullptr, xp_, s), "x0 in elimination order");
+    hdk_check_p(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B x0");
+    hdk_check_p(hdk_gather_pp(&dv_, nullptr, ef_, rx_, nullptr, s), "R(x0)");
+    hdk_check_p(hdk_pcg_spmv(&a_ff_, xp_, pap_, pcg_, s), "A x0");
+    hdk_check_p(hdk_pcg_r0(static_cast<int>(n3p), seedp_, pap_, rx_, pr_, s), "r0");
+    hdk_check_p(hdk_apply_inverse3_perm(&fs, pr_, pz_, s), "z0 = A^-1 r0");
+    hdk_check_p(hdk_pcg_rz(static_cast<int>(n3p), pr_, pz_, xp_, pcg_part_, pcg_ticket_, pcg_, s), "rz");
+    hdk_check_p(hdk_pcg_p(n, pz_, pp_, ppv_, df_.p2v, pcg_, s), "p");
+  };
+  auto body = [&](unsigned long long handle) {
+    hdk_check_p(hdk_bapply_sorted(&dm_, dcomp_, ppv_, ef_, corner_pos_, &pcg_->cond, s), "B p");
+    hdk_check_p(hdk_gather_sorted(&dv_, nullptr, ef_, prp_, &pcg_->cond, s), "R(p)");
+    hdk_check_p(hdk_pcg_spmv(&a_ff_, pp_, pap_, pcg_, s), "A p");
+    hdk_check_p(hdk_pcg_q(static_cast<int>(n3p), pap_, prp_, pp_, pq_, pcg_part_, pcg_ticket_, pcg_, s), "q");
+    hdk_check_p(hdk_pcg_xr(static_cast<int>(n3p), xp_, pr_, pp_, pq_, pcg_, s), "x, r");
+    hdk_check_p(hdk_apply_inverse3_perm(&fs, pr_, pz_, s), "z = A^-1 r");
+    hdk_check_p(hdk_pcg_rz(static_cast<int>(n3p), pr_, pz_, xp_, pcg_part_, pcg_ticket_, pcg_, s), "rz");
+    hdk_check_p(hdk_pcg_p(n, pz_, pp_, ppv_, df_.p2v, pcg_, s), "p");
+    hdk_check_p(hdk_pcg_cond(pcg_, handle, s), "cond");
+  };
+  build_loop_graph(st_, use_cond_, pre, body, [] {}, *pgraph_);
+}
+
+bool Engine::run_pcg(int& iterations) {
+  if (!pgraph_ || (!pgraph_->exec && !pgraph_->body)) build_pcg_graph();
+  LoopGraph& g = *pgraph_;
+  if (g.exec) {
+    cuda_check(cudaGraphLaunch(g.exec, st_), "pcg");
+  } else {  // host-driven loop (profiling fallback)
+    if (g.pre) cuda_check(cudaGraphLaunch(g.pre, st_), "pcg");
+    for (;;) {
+      cuda_check(cudaMemcpyAsync(h_pcg_, pcg_, sizeof(hdk_pcg), cudaMemcpyDeviceToHost, st_), "pcg state");
+      cuda_check(cudaStreamSynchronize(st_), "pcg");
+      if (!h_pcg_->cond) break;
+      cuda_check(cudaGraphLaunch(g.body, st_), "pcg");
+    }
+  }
+  cuda_check(cudaMemcpyAsync(h_pcg_, pcg_, sizeof(hdk_pcg), cudaMemcpyDeviceToHost, st_), "pcg state");
+  cuda_check(cudaStreamSynchronize(st_), "pcg");
+  if (h_pcg_->err == -1) {  // not positive definite along a direction: the reference's Anderson loop
+    ++pcg_fallbacks;
+    return false;
+  }
+  if (h_pcg_->err != 0)
+    raise(Code::AdjointDiverged, "backward step: adjoint CG did not settle (cap or non-finite values)");
+  hdk_check_p(hdk_pcg_final(hf_.n, xp_, pz_, x_, df_.p2v, st_), "x = x + z");
+  iterations = 1 + h_pcg_->iter;  // the first solve x0 = A^{-1} s and one solve per CG step
+  kernel_launches += g.counts[0] + static_cast<long long>(g.counts[1]) * h_pcg_->iter + 2;
+  return true;
+}
+
+}  // namespace hdb

@@ -1,0 +1,269 @@
+// Preconditioned conjugate gradients for the adjoint backbone (the B200
+// alternative to the reference's Anderson fixed point, backward.cpp:170-204):
+// the backbone solves (A - B) x = s, and the reference iterates
+// x <- A^{-1}(s + B x) with AA(8) until ||t - x|| <= 1e-10 ||t||,
+// t = A^{-1}(s + B x).  Since t - x = A^{-1}(s - (A - B) x) = A^{-1} r is the
+// A^{-1}-preconditioned residual z of CG on the same system, CG with the
+// same preconditioner stops on exactly the reference's test and returns
+// x + z (the reference's t).  A - B is symmetric (backward.cpp:117-163);
+// where it is not positive definite along a search direction (p.q <= 0) the
+// iteration reports it and the engine falls back to the Anderson backbone.
+//
+// Vectors are in elimination order [n][3] (the solve's layout); reductions
+// are fixed-grid partials folded by the last block (ticket), so results are
+// bitwise reproducible.
+#include <cuda_runtime.h>
+
+#include "../../include/hdk.h"
+#include "launch.cuh"
+
+namespace {
+
+constexpr int kT = 256;
+constexpr int kB = HDK_RED_BLOCKS;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block partial sums of NQ quantities into partial[q * kB + block].
+template <int NQ>
+__device__ __forceinline__ void block_store(const double (&v)[NQ], double* partial) {
+  __shared__ double sm[kT / 32][NQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const double s = warp_sum(v[q]);
+    if (lane == 0) sm[warp][q] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < NQ) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) s += sm[w][threadIdx.x];
+    partial[threadIdx.x * kB + blockIdx.x] = s;
+  }
+}
+
+// True in the block that finishes last (its loads of the others' partials
+// are ordered after their stores).
+__device__ __forceinline__ bool last_block(unsigned int* ticket) {
+  __shared__ int is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(ticket, 1u);
+    is_last = t == gridDim.x - 1;
+    if (is_last) *ticket = 0u;
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last != 0;
+}
+
+// Fixed-order fold of partial quantity q over the kB blocks (one warp).
+__device__ __forceinline__ double fold(const double* partial, int q) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int b = lane; b < kB; b += 32) s += partial[q * kB + b];
+  return warp_sum(s);
+}
+
+// r = s - A x0 + R(x0) (R = gather o B): the residual of x0 = A^{-1} s.
+__global__ void k_pcg_r0(int n3, const double* __restrict__ s, const double* __restrict__ ax,
+                         const double* __restrict__ rx, double* __restrict__ r) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n3) r[i] = (s[i] - ax[i]) + rx[i];
+}
+
+// y = A p on the three axes (A_ff in elimination order, columns are positions).
+__global__ void k_pcg_spmv(hdk_csr A, const double* __restrict__ p, double* __restrict__ y, const hdk_pcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (st->cond == 0) return;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= A.rows) return;
+  double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+  for (int k = A.off[row]; k < A.off[row + 1]; ++k) {
+    const double w = A.val[k];
+    const double* v = p + 3 * (size_t)A.col[k];
+    y0 += w * v[0];
+    y1 += w * v[1];
+    y2 += w * v[2];
+  }
+  y[3 * (size_t)row] = y0;
+  y[3 * (size_t)row + 1] = y1;
+  y[3 * (size_t)row + 2] = y2;
+}
+
+// After z = A^{-1} r: rz = r.z, the reference's convergence test on
+// (x, z), beta, and the WHILE condition.
+__global__ void __launch_bounds__(kT) k_pcg_rz(int n3, const double* __restrict__ r, const double* __restrict__ z,
+                                               const double* __restrict__ x, double* partial, unsigned int* ticket,
+                                               hdk_pcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (st->cond == 0) return;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int i = blockIdx.x * kT + threadIdx.x; i < n3; i += kB * kT) {
+    const double zi = z[i], t = x[i] + zi;
+    acc[0] += r[i] * zi;
+    acc[1] += zi * zi;
+    acc[2] += t * t;
+  }
+  block_store<3>(acc, partial);
+  if (!last_block(ticket)) return;
+  if (threadIdx.x >= 32) return;
+  const double rz = fold(partial, 0), zz = fold(partial, 1), tt = fold(partial, 2);
+  if (threadIdx.x != 0) return;
+  const int it = st->iter + 1;  // solves so far
+  st->iter = it;
+  const bool done = sqrt(zz) <= st->tol * fmax(sqrt(tt), 1e-30);
+  st->beta = st->rz > 0.0 && it > 1 ? rz / st->rz : 0.0;
+  st->rz = rz;
+  st->done = done ? 1 : 0;
+  if (!done && it >= st->k_max) st->err = 10;  // AdjointDiverged (cap)
+  if (!isfinite(rz)) st->err = 10;
+  st->cond = (!done && st->err == 0) ? 1 : 0;
+}
+
+// The WHILE condition from the state (last kernel of the loop body; any
+// kernel above may have ended the loop).
+__global__ void k_pcg_cond(const hdk_pcg* st, cudaGraphConditionalHandle handle, int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (use_handle) cudaGraphSetConditional(handle, st->cond);
+}
+
+// p = z + beta p, and p by vertex (the B apply's input; fixed vertices stay 0).
+__global__ void k_pcg_p(int n, const double* __restrict__ z, double* __restrict__ p, double* __restrict__ pv,
+                        const int* __restrict__ p2v, const hdk_pcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (st->cond == 0) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * n) return;
+  const double b = st->beta;
+  const double v = z[i] + b * p[i];
+  p[i] = v;
+  const int row = i / 3;
+  pv[3 * (size_t)__ldg(p2v + row) + (i - 3 * row)] = v;
+}
+
+// q = A p - R(p), p.q, alpha = rz / p.q (last block); p.q <= 0 ends the loop
+// with err = -1 (the engine falls back to the Anderson backbone).
+__global__ void __launch_bounds__(kT) k_pcg_q(int n3, const double* __restrict__ ap, const double* __restrict__ rp,
+                                              const double* __restrict__ p, double* __restrict__ q, double* partial,
+                                              unsigned int* ticket, hdk_pcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (st->cond == 0) return;
+  double acc[1] = {0.0};
+  for (int i = blockIdx.x * kT + threadIdx.x; i < n3; i += kB * kT) {
+    const double qi = ap[i] - rp[i];
+    q[i] = qi;
+    acc[0] += p[i] * qi;
+  }
+  block_store<1>(acc, partial);
+  if (!last_block(ticket)) return;
+  if (threadIdx.x >= 32) return;
+  const double pq = fold(partial, 0);
+  if (threadIdx.x != 0) return;
+  st->pq = pq;
+  if (!(pq > 0.0)) {
+    st->err = -1;
+    st->cond = 0;
+  } else {
+    st->alpha = st->rz / pq;
+  }
+}
+
+// x += alpha p, r -= alpha q.
+__global__ void k_pcg_xr(int n3, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                         const double* __restrict__ q, const hdk_pcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (st->cond == 0) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  const double a = st->alpha;
+  x[i] += a * p[i];
+  r[i] -= a * q[i];
+}
+
+// x_full = x + z by vertex (the reference returns t = x + A^{-1} r).
+__global__ void k_pcg_final(int n, const double* __restrict__ x, const double* __restrict__ z, double* __restrict__ xv,
+                            const int* __restrict__ p2v) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * n) return;
+  const int row = i / 3;
+  xv[3 * (size_t)__ldg(p2v + row) + (i - 3 * row)] = x[i] + z[i];
+}
+
+__global__ void k_pcg_init(hdk_pcg* st, double tol, int k_max) {
+  st->rz = st->pq = st->alpha = st->beta = 0.0;
+  st->tol = tol;
+  st->iter = 0;
+  st->k_max = k_max;
+  st->done = 0;
+  st->err = 0;
+  st->cond = 1;
+}
+
+inline int nb(long long n) { return static_cast<int>((n + 255) / 256 > 0 ? (n + 255) / 256 : 1); }
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+inline int last() { return static_cast<int>(cudaGetLastError()); }
+
+}  // namespace
+
+extern "C" {
+
+HDK_API int hdk_pcg_init(hdk_pcg* st, double tol, int k_max, void* stream) {
+  hdk::launch(k_pcg_init, dim3(1), dim3(1), 0, S(stream), st, tol, k_max);
+  return last();
+}
+HDK_API int hdk_pcg_r0(int n3, const double* s, const double* ax, const double* rx, double* r, void* stream) {
+  hdk::launch(k_pcg_r0, dim3(nb(n3)), dim3(256), 0, S(stream), n3, s, ax, rx, r);
+  return last();
+}
+HDK_API int hdk_pcg_spmv(const hdk_csr* a, const double* p, double* y, const hdk_pcg* st, void* stream) {
+  hdk::launch(k_pcg_spmv, dim3(nb(a->rows)), dim3(256), 0, S(stream), *a, p, y, st);
+  return last();
+}
+HDK_API int hdk_pcg_rz(int n3, const double* r, const double* z, const double* x, double* partial,
+                       unsigned int* ticket, hdk_pcg* st, void* stream) {
+  hdk::launch(k_pcg_rz, dim3(kB), dim3(kT), 0, S(stream), n3, r, z, x, partial, ticket, st);
+  return last();
+}
+HDK_API int hdk_pcg_cond(const hdk_pcg* st, unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_pcg_cond, dim3(1), dim3(1), 0, S(stream), st, static_cast<cudaGraphConditionalHandle>(cond_handle),
+              cond_handle ? 1 : 0);
+  return last();
+}
+HDK_API int hdk_pcg_p(int n, const double* z, double* p, double* pv, const int* p2v, const hdk_pcg* st,
+                      void* stream) {
+  hdk::launch(k_pcg_p, dim3(nb(3LL * n)), dim3(256), 0, S(stream), n, z, p, pv, p2v, st);
+  return last();
+}
+HDK_API int hdk_pcg_q(int n3, const double* ap, const double* rp, const double* p, double* q, double* partial,
+                      unsigned int* ticket, hdk_pcg* st, void* stream) {
+  hdk::launch(k_pcg_q, dim3(kB), dim3(kT), 0, S(stream), n3, ap, rp, p, q, partial, ticket, st);
+  return last();
+}
+HDK_API int hdk_pcg_xr(int n3, double* x, double* r, const double* p, const double* q, const hdk_pcg* st,
+                       void* stream) {
+  hdk::launch(k_pcg_xr, dim3(nb(n3)), dim3(256), 0, S(stream), n3, x, r, p, q, st);
+  return last();
+}
+HDK_API int hdk_pcg_final(int n, const double* x, const double* z, double* x_full, const int* p2v, void* stream) {
+  hdk::launch(k_pcg_final, dim3(nb(3LL * n)), dim3(256), 0, S(stream), n, x, z, x_full, p2v);
+  return last();
+}
+
+}  // extern "C"
