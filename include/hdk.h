@@ -551,8 +551,12 @@ HDK_API int hdk_pcg_spmv(const hdk_csr* a, const double* p, double* y, const hdk
 HDK_API int hdk_pcg_rz(int n3, const double* r, const double* z, const double* x, double* partial,
                        unsigned int* ticket, hdk_pcg* st, void* stream);
 HDK_API int hdk_pcg_cond(const hdk_pcg* st, unsigned long long cond_handle, void* stream);
+/* p = z + beta p (and by vertex); sets the WHILE condition (last kernel of the body). */
 HDK_API int hdk_pcg_p(int n, const double* z, double* p, double* pv, const int* p2v, const hdk_pcg* st,
-                      void* stream);
+                      unsigned long long cond_handle, void* stream);
+/* q = A p - gather(B p) from the sorted element forces, p.q, alpha (one launch). */
+HDK_API int hdk_pcg_apply(const hdk_vtx* x, const hdk_csr* a, const double* ef_sorted, const double* p, double* q,
+                          double* partial, unsigned int* ticket, hdk_pcg* st, void* stream);
 HDK_API int hdk_pcg_q(int n3, const double* ap, const double* rp, const double* p, double* q, double* partial,
                       unsigned int* ticket, hdk_pcg* st, void* stream);
 HDK_API int hdk_pcg_xr(int n3, double* x, double* r, const double* p, const double* q, const hdk_pcg* st,

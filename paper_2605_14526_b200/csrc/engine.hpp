@@ -259,10 +259,11 @@ class Engine {
   void build_forward_graph_seg();
   void build_backward_graph_seg();
   void backbone_body_seg(unsigned long long cond_handle);
-  // adjoint backbone by preconditioned CG (pcg.cu, engine_pcg.cpp):
-  // HETERODYN_ADJOINT=pcg; falls back to the Anderson loop when A - B is
-  // not positive definite along a search direction
-  bool use_pcg_ = false;
+  // adjoint backbone by preconditioned CG (pcg.cu, engine_pcg.cpp), the
+  // default for a single problem (HETERODYN_ADJOINT=aa: the reference's
+  // Anderson loop); falls back to the Anderson loop when A - B is not
+  // positive definite along a search direction
+  bool use_pcg_ = true;
   std::unique_ptr<LoopGraph> pgraph_;
   hdk_pcg* pcg_ = nullptr;
   hdk_pcg* h_pcg_ = nullptr;

@@ -43,18 +43,16 @@ void Engine::build_pcg_graph() {
     hdk_check_p(hdk_pcg_r0(static_cast<int>(n3p), seedp_, pap_, rx_, pr_, s), "r0");
     hdk_check_p(hdk_apply_inverse3_perm(&fs, pr_, pz_, s), "z0 = A^-1 r0");
     hdk_check_p(hdk_pcg_rz(static_cast<int>(n3p), pr_, pz_, xp_, pcg_part_, pcg_ticket_, pcg_, s), "rz");
-    hdk_check_p(hdk_pcg_p(n, pz_, pp_, ppv_, df_.p2v, pcg_, s), "p");
+    hdk_check_p(hdk_pcg_p(n, pz_, pp_, ppv_, df_.p2v, pcg_, 0ULL, s), "p");
   };
+  // B p, then one fused launch for gather(B p), A p, q and alpha
   auto body = [&](unsigned long long handle) {
     hdk_check_p(hdk_bapply_sorted(&dm_, dcomp_, ppv_, ef_, corner_pos_, &pcg_->cond, s), "B p");
-    hdk_check_p(hdk_gather_sorted(&dv_, nullptr, ef_, prp_, &pcg_->cond, s), "R(p)");
-    hdk_check_p(hdk_pcg_spmv(&a_ff_, pp_, pap_, pcg_, s), "A p");
-    hdk_check_p(hdk_pcg_q(static_cast<int>(n3p), pap_, prp_, pp_, pq_, pcg_part_, pcg_ticket_, pcg_, s), "q");
+    hdk_check_p(hdk_pcg_apply(&dv_, &a_ff_, ef_, pp_, pq_, pcg_part_, pcg_ticket_, pcg_, s), "q = (A - B) p");
     hdk_check_p(hdk_pcg_xr(static_cast<int>(n3p), xp_, pr_, pp_, pq_, pcg_, s), "x, r");
     hdk_check_p(hdk_apply_inverse3_perm(&fs, pr_, pz_, s), "z = A^-1 r");
     hdk_check_p(hdk_pcg_rz(static_cast<int>(n3p), pr_, pz_, xp_, pcg_part_, pcg_ticket_, pcg_, s), "rz");
-    hdk_check_p(hdk_pcg_p(n, pz_, pp_, ppv_, df_.p2v, pcg_, s), "p");
-    hdk_check_p(hdk_pcg_cond(pcg_, handle, s), "cond");
+    hdk_check_p(hdk_pcg_p(n, pz_, pp_, ppv_, df_.p2v, pcg_, handle, s), "p + cond");
   };
   build_loop_graph(st_, use_cond_, pre, body, [] {}, *pgraph_);
 }

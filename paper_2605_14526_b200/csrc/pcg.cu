@@ -141,9 +141,12 @@ __global__ void k_pcg_cond(const hdk_pcg* st, cudaGraphConditionalHandle handle,
 
 // p = z + beta p, and p by vertex (the B apply's input; fixed vertices stay 0).
 __global__ void k_pcg_p(int n, const double* __restrict__ z, double* __restrict__ p, double* __restrict__ pv,
-                        const int* __restrict__ p2v, const hdk_pcg* st) {
+                        const int* __restrict__ p2v, const hdk_pcg* st, cudaGraphConditionalHandle handle,
+                        int use_handle) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
+  // the loop body's last kernel: the WHILE condition is final here
+  if (use_handle && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, st->cond);
   if (st->cond == 0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 3 * n) return;
@@ -167,6 +170,71 @@ __global__ void __launch_bounds__(kT) k_pcg_q(int n3, const double* __restrict__
     const double qi = ap[i] - rp[i];
     q[i] = qi;
     acc[0] += p[i] * qi;
+  }
+  block_store<1>(acc, partial);
+  if (!last_block(ticket)) return;
+  if (threadIdx.x >= 32) return;
+  const double pq = fold(partial, 0);
+  if (threadIdx.x != 0) return;
+  st->pq = pq;
+  if (!(pq > 0.0)) {
+    st->err = -1;
+    st->cond = 0;
+  } else {
+    st->alpha = st->rz / pq;
+  }
+}
+
+// Fused: R(p) = gather o B p from the sorted element forces (8 lanes per row,
+// the gather's lane split and fold), A p (A_ff row, 8 lanes), q = A p - R(p),
+// p.q and alpha = rz / p.q (last block).
+__global__ void __launch_bounds__(kT) k_pcg_apply(hdk_vtx x, hdk_csr A, const double* __restrict__ ef,
+                                                  const double* __restrict__ p, double* __restrict__ q, double* partial,
+                                                  unsigned int* ticket, hdk_pcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (st->cond == 0) return;
+  const int sub = threadIdx.x & 7, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[1] = {0.0};
+  // a warp takes four consecutive rows per round (warp-uniform loop: the
+  // shuffle folds below need every lane)
+  for (int rb = blockIdx.x * (kT / 8) + 4 * warp; rb < x.n; rb += kB * (kT / 8)) {
+    const int row = rb + (lane >> 3);
+    const bool live = row < x.n;
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    const int e = live ? __ldg(x.pinc_off + row + 1) : 0;
+    for (int j = (live ? __ldg(x.pinc_off + row) : 0) + sub; j < e; j += 8) {
+      const double* f = ef + 3 * (size_t)j;
+      r0 += __ldg(f);
+      r1 += __ldg(f + 1);
+      r2 += __ldg(f + 2);
+    }
+    const int ke = live ? __ldg(A.off + row + 1) : 0;
+    for (int k = (live ? __ldg(A.off + row) : 0) + sub; k < ke; k += 8) {
+      const double w = __ldg(A.val + k);
+      const double* v = p + 3 * (size_t)__ldg(A.col + k);
+      a0 += w * v[0];
+      a1 += w * v[1];
+      a2 += w * v[2];
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      r0 += __shfl_xor_sync(0xffffffffu, r0, o);
+      r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+      r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (sub == 0 && live) {
+      const double q0 = a0 - r0, q1 = a1 - r1, q2 = a2 - r2;
+      double* qr = q + 3 * (size_t)row;
+      qr[0] = q0;
+      qr[1] = q1;
+      qr[2] = q2;
+      const double* pr = p + 3 * (size_t)row;
+      acc[0] += (pr[0] * q0 + pr[1] * q1) + pr[2] * q2;
+    }
   }
   block_store<1>(acc, partial);
   if (!last_block(ticket)) return;
@@ -247,8 +315,15 @@ HDK_API int hdk_pcg_cond(const hdk_pcg* st, unsigned long long cond_handle, void
   return last();
 }
 HDK_API int hdk_pcg_p(int n, const double* z, double* p, double* pv, const int* p2v, const hdk_pcg* st,
-                      void* stream) {
-  hdk::launch(k_pcg_p, dim3(nb(3LL * n)), dim3(256), 0, S(stream), n, z, p, pv, p2v, st);
+                      unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_pcg_p, dim3(nb(3LL * n)), dim3(256), 0, S(stream), n, z, p, pv, p2v, st,
+              static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle ? 1 : 0);
+  return last();
+}
+HDK_API int hdk_pcg_apply(const hdk_vtx* x, const hdk_csr* a, const double* ef_sorted, const double* p, double* q,
+                          double* partial, unsigned int* ticket, hdk_pcg* st, void* stream) {
+  if (!x->pinc_off) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_pcg_apply, dim3(kB), dim3(kT), 0, S(stream), *x, *a, ef_sorted, p, q, partial, ticket, st);
   return last();
 }
 HDK_API int hdk_pcg_q(int n3, const double* ap, const double* rp, const double* p, double* q, double* partial,

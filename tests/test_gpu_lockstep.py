@@ -48,6 +48,7 @@ def test_lockstep_matches_oracle_and_per_sample_engines(prod, orc, monkeypatch, 
     bl.set_target(target)
     rl = bl.evaluate(3)
     monkeypatch.setenv("HETERODYN_BATCH", "streams")
+    monkeypatch.setenv("HETERODYN_ADJOINT", "aa")  # the lockstep backbone is the Anderson loop: like for like
     bs = sp.batch(5, young, threads=4)
     bs.set_target(target)
     rs = bs.evaluate(3)
@@ -80,6 +81,7 @@ def test_lockstep_single_sample_equals_engine(prod, monkeypatch):
     bl.set_target(target)
     rl = bl.evaluate(2)
     monkeypatch.setenv("HETERODYN_BATCH", "streams")
+    monkeypatch.setenv("HETERODYN_ADJOINT", "aa")
     bs = sp.batch(1, young)
     bs.set_target(target)
     rs = bs.evaluate(2)
