@@ -77,6 +77,7 @@ def test_lockstep_single_sample_equals_engine(prod, monkeypatch):
     young = heterogeneous_young(1, sp.element_count)
     target = np.asarray(sp.sim().positions()) - 2e-3
     monkeypatch.delenv("HETERODYN_BATCH", raising=False)
+    monkeypatch.setenv("HETERODYN_ADJOINT", "aa")  # one sample is a plain engine: compare Anderson with Anderson
     bl = sp.batch(1, young)
     bl.set_target(target)
     rl = bl.evaluate(2)
