@@ -562,6 +562,20 @@ HDK_API int hdk_pcg_q(int n3, const double* ap, const double* rp, const double* 
 HDK_API int hdk_pcg_xr(int n3, double* x, double* r, const double* p, const double* q, const hdk_pcg* st,
                        void* stream);
 HDK_API int hdk_pcg_final(int n, const double* x, const double* z, double* x_full, const int* p2v, void* stream);
+/* Segmented batch: one CG per sample (sample s owns rows [s ns, (s+1) ns)),
+ * count states, per-sample partials at HDK_SEG_PSTRIDE and tickets; *any is
+ * the OR of the samples' conditions (solve run flag, WHILE condition). */
+HDK_API int hdk_spcg_init(hdk_pcg* st, int count, double tol, int k_max, int* any, void* stream);
+HDK_API int hdk_spcg_spmv(const hdk_csr* a, int ns, const double* p, double* y, const hdk_pcg* st, void* stream);
+HDK_API int hdk_spcg_apply(const hdk_vtx* x, const hdk_csr* a, int ns, int count, const double* ef_sorted,
+                           const double* p, double* q, double* partial, unsigned int* tickets, hdk_pcg* st,
+                           void* stream);
+HDK_API int hdk_spcg_xr(int n3s, int n3, double* x, double* r, const double* p, const double* q, const hdk_pcg* st,
+                        void* stream);
+HDK_API int hdk_spcg_rz(int n3s, int count, const double* r, const double* z, const double* x, double* partial,
+                        unsigned int* tickets, hdk_pcg* st, void* stream);
+HDK_API int hdk_spcg_p(int n3s, int n3, const double* z, double* p, double* pv, const int* p2v, const hdk_pcg* st,
+                       int count, int* any, unsigned long long cond_handle, void* stream);
 
 /* ---- segmented batch (lockstep C5 engine, engine.cpp segments > 1) --------
  * S samples of one mesh as one concatenated problem: sample s owns vertices

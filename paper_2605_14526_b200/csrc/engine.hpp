@@ -272,6 +272,7 @@ class Engine {
   unsigned int* pcg_ticket_ = nullptr;
   long long pcg_fallbacks = 0;
   void build_pcg_graph();
+  void build_pcg_graph_seg();
   bool run_pcg(int& iterations);  // false: fall back to the Anderson backbone
   bool host_any() const;
   void load_frame(int t);  // frame slot t into the backward working buffers

@@ -206,7 +206,7 @@ void Engine::backward_frame(int t, GradOut& out) {
   cuda_check(cudaGraphLaunch(bpre_, st_), "backward pre");
   phase_mark(4);
   int pcg_iters = -1;
-  if (!(use_pcg_ && segs_ == 1 && run_pcg(pcg_iters))) run_graph(*bgraph_, "backbone");
+  if (!(use_pcg_ && run_pcg(pcg_iters))) run_graph(*bgraph_, "backbone");
   phase_mark(5);
   sync_ctl();
   check_ctl("backward step");
@@ -214,8 +214,10 @@ void Engine::backward_frame(int t, GradOut& out) {
   if (segs_ > 1) {  // lockstep: every sample's own count, the loop ran to the largest
     seg_tau.resize(segs_);
     for (int k = 0; k < segs_; ++k) {
-      iters = std::max(iters, 1 + h_ctl_[k].iterations);
-      seg_sample_iterations += 1 + h_ctl_[k].iterations;
+      if (pcg_iters < 0) {  // (the CG path counted its samples in run_pcg)
+        iters = std::max(iters, 1 + h_ctl_[k].iterations);
+        seg_sample_iterations += 1 + h_ctl_[k].iterations;
+      }
       seg_tau[k] = h_ctl_[k].tau;
     }
   }

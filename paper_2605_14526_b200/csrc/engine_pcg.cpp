@@ -3,6 +3,7 @@
 // fixed point (backward.cpp:170-204), a Krylov method instead of the
 // window-8 mixing.  One iteration: B p (matrix-free, engine layout), A p
 // (A_ff SpMV), q = A p - B p, the CG updates, one global solve z = A^{-1} r.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -19,16 +20,20 @@ void Engine::build_pcg_graph() {
   const size_t n3p = 3 * static_cast<size_t>(hf_.n), n3 = 3 * static_cast<size_t>(scene_.mesh.nv);
   if (!pcg_) {
     DevArena& A = *mem_;
-    pcg_ = A.alloc<hdk_pcg>(1);
-    pcg_part_ = A.alloc<double>(4 * HDK_RED_BLOCKS);
-    pcg_ticket_ = A.alloc<unsigned int>(1);
-    cuda_check(cudaMemset(pcg_ticket_, 0, sizeof(unsigned int)), "zero ticket");
+    pcg_ = A.alloc<hdk_pcg>(segs_);
+    pcg_part_ = A.alloc<double>(segs_ > 1 ? static_cast<size_t>(HDK_SEG_PSTRIDE) * segs_ : 4 * HDK_RED_BLOCKS);
+    pcg_ticket_ = A.alloc<unsigned int>(segs_);
+    cuda_check(cudaMemset(pcg_ticket_, 0, sizeof(unsigned int) * segs_), "zero ticket");
     for (double** v : {&pr_, &pz_, &pp_, &pq_, &pap_, &prp_}) *v = A.alloc<double>(n3p);
     ppv_ = A.alloc<double>(n3);
     cuda_check(cudaMemset(ppv_, 0, n3 * sizeof(double)), "zero pv");  // fixed vertices stay 0
-    cuda_check(cudaMallocHost(&h_pcg_, sizeof(hdk_pcg)), "pinned pcg");
+    cuda_check(cudaMallocHost(&h_pcg_, sizeof(hdk_pcg) * segs_), "pinned pcg");
   }
   if (!pgraph_) pgraph_ = std::make_unique<LoopGraph>();
+  if (segs_ > 1) {
+    build_pcg_graph_seg();
+    return;
+  }
   void* s = st_;
   const int n = hf_.n;
   hdk_factor fs = df_;
@@ -57,6 +62,37 @@ void Engine::build_pcg_graph() {
   build_loop_graph(st_, use_cond_, pre, body, [] {}, *pgraph_);
 }
 
+// Lockstep batch: one CG per sample, every stage one launch for all samples
+// (hdk_spcg_*); the solve runs while any sample iterates.
+void Engine::build_pcg_graph_seg() {
+  const size_t n3p = 3 * static_cast<size_t>(hf_.n);
+  void* s = st_;
+  const int S = segs_, ns = dseg_.n, n3s = 3 * dseg_.n, n3 = static_cast<int>(n3p);
+  hdk_factor fs = df_;
+  fs.run_flag = any_;
+  auto pre = [&] {
+    hdk_check_p(hdk_spcg_init(pcg_, S, 1e-10, 500, any_, s), "pcg init");
+    hdk_check_p(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
+    hdk_check_p(hdk_gather_perm(&dv_, x_, nullptr, xp_, s), "x0 in elimination order");
+    hdk_check_p(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B x0");
+    hdk_check_p(hdk_gather_pp(&dv_, nullptr, ef_, rx_, nullptr, s), "R(x0)");
+    hdk_check_p(hdk_spcg_spmv(&a_ff_, ns, xp_, pap_, pcg_, s), "A x0");
+    hdk_check_p(hdk_pcg_r0(n3, seedp_, pap_, rx_, pr_, s), "r0");
+    hdk_check_p(hdk_apply_inverse3_perm(&fs, pr_, pz_, s), "z0 = A^-1 r0");
+    hdk_check_p(hdk_spcg_rz(n3s, S, pr_, pz_, xp_, pcg_part_, pcg_ticket_, pcg_, s), "rz");
+    hdk_check_p(hdk_spcg_p(n3s, n3, pz_, pp_, ppv_, df_.p2v, pcg_, S, any_, 0ULL, s), "p");
+  };
+  auto body = [&](unsigned long long handle) {
+    hdk_check_p(hdk_bapply_sorted(&dm_, dcomp_, ppv_, ef_, corner_pos_, any_, s), "B p");
+    hdk_check_p(hdk_spcg_apply(&dv_, &a_ff_, ns, S, ef_, pp_, pq_, pcg_part_, pcg_ticket_, pcg_, s), "q = (A - B) p");
+    hdk_check_p(hdk_spcg_xr(n3s, n3, xp_, pr_, pp_, pq_, pcg_, s), "x, r");
+    hdk_check_p(hdk_apply_inverse3_perm(&fs, pr_, pz_, s), "z = A^-1 r");
+    hdk_check_p(hdk_spcg_rz(n3s, S, pr_, pz_, xp_, pcg_part_, pcg_ticket_, pcg_, s), "rz");
+    hdk_check_p(hdk_spcg_p(n3s, n3, pz_, pp_, ppv_, df_.p2v, pcg_, S, any_, handle, s), "p + any");
+  };
+  build_loop_graph(st_, use_cond_, pre, body, [] {}, *pgraph_);
+}
+
 bool Engine::run_pcg(int& iterations) {
   if (!pgraph_ || (!pgraph_->exec && !pgraph_->body)) build_pcg_graph();
   LoopGraph& g = *pgraph_;
@@ -65,23 +101,32 @@ bool Engine::run_pcg(int& iterations) {
   } else {  // host-driven loop (profiling fallback)
     if (g.pre) cuda_check(cudaGraphLaunch(g.pre, st_), "pcg");
     for (;;) {
-      cuda_check(cudaMemcpyAsync(h_pcg_, pcg_, sizeof(hdk_pcg), cudaMemcpyDeviceToHost, st_), "pcg state");
+      cuda_check(cudaMemcpyAsync(h_pcg_, pcg_, sizeof(hdk_pcg) * segs_, cudaMemcpyDeviceToHost, st_), "pcg state");
       cuda_check(cudaStreamSynchronize(st_), "pcg");
-      if (!h_pcg_->cond) break;
+      bool on = false;
+      for (int k = 0; k < segs_; ++k) on = on || (h_pcg_[k].cond && h_pcg_[k].err == 0);
+      if (!on) break;
       cuda_check(cudaGraphLaunch(g.body, st_), "pcg");
     }
   }
-  cuda_check(cudaMemcpyAsync(h_pcg_, pcg_, sizeof(hdk_pcg), cudaMemcpyDeviceToHost, st_), "pcg state");
+  cuda_check(cudaMemcpyAsync(h_pcg_, pcg_, sizeof(hdk_pcg) * segs_, cudaMemcpyDeviceToHost, st_), "pcg state");
   cuda_check(cudaStreamSynchronize(st_), "pcg");
-  if (h_pcg_->err == -1) {  // not positive definite along a direction: the reference's Anderson loop
-    ++pcg_fallbacks;
-    return false;
+  int most = 0;
+  for (int k = 0; k < segs_; ++k) {
+    const hdk_pcg& h = h_pcg_[k];
+    if (h.err == -1) {  // not positive definite along a direction: the reference's Anderson loop (all samples)
+      ++pcg_fallbacks;
+      return false;
+    }
+    if (h.err != 0)
+      raise(Code::AdjointDiverged, "backward step: adjoint CG did not settle (cap or non-finite values)" +
+                                       (segs_ > 1 ? " in sample " + std::to_string(k) : std::string()));
+    most = std::max(most, h.iter);
+    if (segs_ > 1) seg_sample_iterations += 1 + h.iter;
   }
-  if (h_pcg_->err != 0)
-    raise(Code::AdjointDiverged, "backward step: adjoint CG did not settle (cap or non-finite values)");
   hdk_check_p(hdk_pcg_final(hf_.n, xp_, pz_, x_, df_.p2v, st_), "x = x + z");
-  iterations = 1 + h_pcg_->iter;  // the first solve x0 = A^{-1} s and one solve per CG step
-  kernel_launches += g.counts[0] + static_cast<long long>(g.counts[1]) * h_pcg_->iter + 2;
+  iterations = 1 + most;  // the first solve x0 = A^{-1} s and one solve per CG step (the slowest sample)
+  kernel_launches += g.counts[0] + static_cast<long long>(g.counts[1]) * most + 2;
   return true;
 }
 

@@ -342,3 +342,243 @@ HDK_API int hdk_pcg_final(int n, const double* x, const double* z, double* x_ful
 }
 
 }  // extern "C"
+
+// ---- segmented batch (lockstep engine): one CG per sample ---------------------
+// Sample s owns elimination rows [s n, (s+1) n); its reductions run on blockIdx.y
+// = s with their own partials (stride HDK_SEG_PSTRIDE) and ticket; every kernel
+// skips a sample whose loop has ended.  *any (the solve's run flag and the WHILE
+// condition) is the OR over the samples.
+namespace {
+
+constexpr int kSRB = HDK_SEG_RB;
+
+template <int NQ>
+__device__ __forceinline__ void block_store_rb(const double (&v)[NQ], double* partial) {
+  __shared__ double sm[kT / 32][NQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const double s = warp_sum(v[q]);
+    if (lane == 0) sm[warp][q] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < NQ) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) s += sm[w][threadIdx.x];
+    partial[threadIdx.x * kSRB + blockIdx.x] = s;
+  }
+}
+__device__ __forceinline__ double fold_rb(const double* partial, int q) {
+  const int lane = threadIdx.x & 31;
+  const double v = lane < kSRB ? partial[q * kSRB + lane] : 0.0;
+  return warp_sum(v);
+}
+
+__global__ void k_spcg_init(hdk_pcg* st, int count, double tol, int k_max, int* any) {
+  for (int s = threadIdx.x; s < count; s += blockDim.x) {
+    hdk_pcg* c = st + s;
+    c->rz = c->pq = c->alpha = c->beta = 0.0;
+    c->tol = tol;
+    c->iter = 0;
+    c->k_max = k_max;
+    c->done = 0;
+    c->err = 0;
+    c->cond = 1;
+  }
+  if (threadIdx.x == 0) *any = 1;
+}
+
+__global__ void k_spcg_spmv(hdk_csr A, int ns, const double* __restrict__ p, double* __restrict__ y,
+                            const hdk_pcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= A.rows || st[row / ns].cond == 0) return;
+  double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+  for (int k = A.off[row]; k < A.off[row + 1]; ++k) {
+    const double w = A.val[k];
+    const double* v = p + 3 * (size_t)A.col[k];
+    y0 += w * v[0];
+    y1 += w * v[1];
+    y2 += w * v[2];
+  }
+  y[3 * (size_t)row] = y0;
+  y[3 * (size_t)row + 1] = y1;
+  y[3 * (size_t)row + 2] = y2;
+}
+
+__global__ void __launch_bounds__(kT) k_spcg_apply(hdk_vtx x, hdk_csr A, int ns, const double* __restrict__ ef,
+                                                   const double* __restrict__ p, double* __restrict__ q,
+                                                   double* partial, unsigned int* tickets, hdk_pcg* sts) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int smp = blockIdx.y;
+  hdk_pcg* st = sts + smp;
+  if (st->cond == 0) return;
+  const int sub = threadIdx.x & 7, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0_ = smp * ns, r1_ = r0_ + ns;
+  double acc[1] = {0.0};
+  for (int rb = r0_ + blockIdx.x * (kT / 8) + 4 * warp; rb < r1_; rb += kSRB * (kT / 8)) {
+    const int row = rb + (lane >> 3);
+    const bool live = row < r1_;
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    const int e = live ? __ldg(x.pinc_off + row + 1) : 0;
+    for (int j = (live ? __ldg(x.pinc_off + row) : 0) + sub; j < e; j += 8) {
+      const double* f = ef + 3 * (size_t)j;
+      c0 += __ldg(f);
+      c1 += __ldg(f + 1);
+      c2 += __ldg(f + 2);
+    }
+    const int ke = live ? __ldg(A.off + row + 1) : 0;
+    for (int k = (live ? __ldg(A.off + row) : 0) + sub; k < ke; k += 8) {
+      const double w = __ldg(A.val + k);
+      const double* v = p + 3 * (size_t)__ldg(A.col + k);
+      a0 += w * v[0];
+      a1 += w * v[1];
+      a2 += w * v[2];
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+      c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+      c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (sub == 0 && live) {
+      const double q0 = a0 - c0, q1 = a1 - c1, q2 = a2 - c2;
+      double* qr = q + 3 * (size_t)row;
+      qr[0] = q0;
+      qr[1] = q1;
+      qr[2] = q2;
+      const double* pr = p + 3 * (size_t)row;
+      acc[0] += (pr[0] * q0 + pr[1] * q1) + pr[2] * q2;
+    }
+  }
+  double* part = partial + (size_t)smp * HDK_SEG_PSTRIDE;
+  block_store_rb<1>(acc, part);
+  if (!last_block(tickets + smp)) return;
+  if (threadIdx.x >= 32) return;
+  const double pq = fold_rb(part, 0);
+  if (threadIdx.x != 0) return;
+  st->pq = pq;
+  if (!(pq > 0.0)) {
+    st->err = -1;
+    st->cond = 0;
+  } else {
+    st->alpha = st->rz / pq;
+  }
+}
+
+__global__ void k_spcg_xr(int n3s, int n3, double* __restrict__ x, double* __restrict__ r,
+                          const double* __restrict__ p, const double* __restrict__ q, const hdk_pcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  const hdk_pcg& c = st[i / n3s];
+  if (c.cond == 0) return;
+  const double a = c.alpha;
+  x[i] += a * p[i];
+  r[i] -= a * q[i];
+}
+
+__global__ void __launch_bounds__(kT) k_spcg_rz(int n3s, const double* __restrict__ r, const double* __restrict__ z,
+                                                const double* __restrict__ x, double* partial, unsigned int* tickets,
+                                                hdk_pcg* sts) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int smp = blockIdx.y;
+  hdk_pcg* st = sts + smp;
+  if (st->cond == 0) return;
+  double acc[3] = {0.0, 0.0, 0.0};
+  const int i0 = smp * n3s, i1 = i0 + n3s;
+  for (int i = i0 + blockIdx.x * kT + threadIdx.x; i < i1; i += kSRB * kT) {
+    const double zi = z[i], t = x[i] + zi;
+    acc[0] += r[i] * zi;
+    acc[1] += zi * zi;
+    acc[2] += t * t;
+  }
+  double* part = partial + (size_t)smp * HDK_SEG_PSTRIDE;
+  block_store_rb<3>(acc, part);
+  if (!last_block(tickets + smp)) return;
+  if (threadIdx.x >= 32) return;
+  const double rz = fold_rb(part, 0), zz = fold_rb(part, 1), tt = fold_rb(part, 2);
+  if (threadIdx.x != 0) return;
+  const int it = st->iter + 1;
+  st->iter = it;
+  const bool done = sqrt(zz) <= st->tol * fmax(sqrt(tt), 1e-30);
+  st->beta = st->rz > 0.0 && it > 1 ? rz / st->rz : 0.0;
+  st->rz = rz;
+  st->done = done ? 1 : 0;
+  if (!done && it >= st->k_max) st->err = 10;
+  if (!isfinite(rz)) st->err = 10;
+  st->cond = (!done && st->err == 0) ? 1 : 0;
+}
+
+// p = z + beta p per sample; block 0 first publishes the OR of the samples'
+// conditions (run flag + WHILE condition).
+__global__ void k_spcg_p(int n3s, int n3, const double* __restrict__ z, double* __restrict__ p,
+                         double* __restrict__ pv, const int* __restrict__ p2v, const hdk_pcg* st, int count, int* any,
+                         cudaGraphConditionalHandle handle, int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (blockIdx.x == 0) {
+    int on = 0;
+    for (int s = threadIdx.x; s < count; s += blockDim.x) on |= (st[s].cond != 0 && st[s].err == 0) ? 1 : 0;
+    const int a = __syncthreads_or(on);
+    if (threadIdx.x == 0) {
+      *any = a;
+      if (use_handle) cudaGraphSetConditional(handle, a);
+    }
+  }
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  const hdk_pcg& c = st[i / n3s];
+  if (c.cond == 0) return;
+  const double v = z[i] + c.beta * p[i];
+  p[i] = v;
+  const int row = i / 3;
+  pv[3 * (size_t)__ldg(p2v + row) + (i - 3 * row)] = v;
+}
+
+}  // namespace
+
+extern "C" {
+
+HDK_API int hdk_spcg_init(hdk_pcg* st, int count, double tol, int k_max, int* any, void* stream) {
+  hdk::launch(k_spcg_init, dim3(1), dim3(256), 0, S(stream), st, count, tol, k_max, any);
+  return last();
+}
+HDK_API int hdk_spcg_spmv(const hdk_csr* a, int ns, const double* p, double* y, const hdk_pcg* st, void* stream) {
+  hdk::launch(k_spcg_spmv, dim3(nb(a->rows)), dim3(256), 0, S(stream), *a, ns, p, y, st);
+  return last();
+}
+HDK_API int hdk_spcg_apply(const hdk_vtx* x, const hdk_csr* a, int ns, int count, const double* ef_sorted,
+                           const double* p, double* q, double* partial, unsigned int* tickets, hdk_pcg* st,
+                           void* stream) {
+  if (!x->pinc_off) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_spcg_apply, dim3(kSRB, count), dim3(kT), 0, S(stream), *x, *a, ns, ef_sorted, p, q, partial, tickets,
+              st);
+  return last();
+}
+HDK_API int hdk_spcg_xr(int n3s, int n3, double* x, double* r, const double* p, const double* q, const hdk_pcg* st,
+                        void* stream) {
+  hdk::launch(k_spcg_xr, dim3(nb(n3)), dim3(256), 0, S(stream), n3s, n3, x, r, p, q, st);
+  return last();
+}
+HDK_API int hdk_spcg_rz(int n3s, int count, const double* r, const double* z, const double* x, double* partial,
+                        unsigned int* tickets, hdk_pcg* st, void* stream) {
+  hdk::launch(k_spcg_rz, dim3(kSRB, count), dim3(kT), 0, S(stream), n3s, r, z, x, partial, tickets, st);
+  return last();
+}
+HDK_API int hdk_spcg_p(int n3s, int n3, const double* z, double* p, double* pv, const int* p2v, const hdk_pcg* st,
+                       int count, int* any, unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_spcg_p, dim3(nb(n3)), dim3(256), 0, S(stream), n3s, n3, z, p, pv, p2v, st, count, any,
+              static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle ? 1 : 0);
+  return last();
+}
+
+}  // extern "C"

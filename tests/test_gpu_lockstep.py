@@ -32,8 +32,9 @@ def heterogeneous_young(samples, ne, seed=7):
     return y
 
 
+@pytest.mark.parametrize("adjoint", ["pcg", "aa"])
 @pytest.mark.parametrize("beta0", [0.0, 0.05])
-def test_lockstep_matches_oracle_and_per_sample_engines(prod, orc, monkeypatch, beta0):
+def test_lockstep_matches_oracle_and_per_sample_engines(prod, orc, monkeypatch, beta0, adjoint):
     scene = scenes.block_scene(dims=(4, 3, 2), frames=3, gravity_z=-9.81, alpha=0.02, beta0=beta0, v0_amp=0.05)
     sp, so = prod.scene(scene), orc.scene(scene)
     ne = sp.element_count
@@ -44,18 +45,22 @@ def test_lockstep_matches_oracle_and_per_sample_engines(prod, orc, monkeypatch, 
     ro = bo.evaluate(3)
 
     monkeypatch.delenv("HETERODYN_BATCH", raising=False)
+    monkeypatch.setenv("HETERODYN_ADJOINT", adjoint)  # the same backbone in both batch forms
     bl = sp.batch(5, young, threads=1)
     bl.set_target(target)
     rl = bl.evaluate(3)
     monkeypatch.setenv("HETERODYN_BATCH", "streams")
-    monkeypatch.setenv("HETERODYN_ADJOINT", "aa")  # the lockstep backbone is the Anderson loop: like for like
     bs = sp.batch(5, young, threads=4)
     bs.set_target(target)
     rs = bs.evaluate(3)
 
+    # Anderson: the same arithmetic up to the reduction grouping (1e-9); CG:
+    # the grouping also changes the Krylov iterates, which agree to the
+    # stopping tolerance times the conditioning (1e-6, as against the oracle)
+    bar = 1e-9 if adjoint == "aa" else 1e-6
     for k in ("loss", "dl_de"):
         assert rel2(rl[k], ro[k]) <= 1e-6, (k, rel2(rl[k], ro[k]))
-        assert rel2(rl[k], rs[k]) <= 1e-9, (k, rel2(rl[k], rs[k]))
+        assert rel2(rl[k], rs[k]) <= bar, (k, rel2(rl[k], rs[k]))
     # per-sample losses, one by one
     for s in range(5):
         assert abs(rl["loss"][s] - ro["loss"][s]) <= 1e-6 * abs(ro["loss"][s])
