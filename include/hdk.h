@@ -576,6 +576,24 @@ HDK_API int hdk_spcg_rz(int n3s, int count, const double* r, const double* z, co
                         unsigned int* tickets, hdk_pcg* st, void* stream);
 HDK_API int hdk_spcg_p(int n3s, int n3, const double* z, double* p, double* pv, const int* p2v, const hdk_pcg* st,
                        int count, int* any, unsigned long long cond_handle, void* stream);
+/* Contact-adjoint columns: one CG per column, all columns per launch (column
+ * c's vectors at base + c 3n, by vertex at + c 3nv, sorted element forces at
+ * + c ef_stride); z = A^{-1} r folded from hdk_apply_inverse3_multi's tile
+ * partials. */
+HDK_API int hdk_cpcg_spmv(const hdk_csr* a, int columns, const double* p, double* y, const hdk_pcg* st,
+                          void* stream);
+HDK_API int hdk_cpcg_apply(const hdk_vtx* x, const hdk_csr* a, int columns, const double* ef_sorted,
+                           size_t ef_stride, const double* p, double* q, double* partial, unsigned int* tickets,
+                           hdk_pcg* st, void* stream);
+HDK_API int hdk_cpcg_rz(const hdk_factor* f, int columns, const double* r, double* z, const double* x,
+                        double* partial, unsigned int* tickets, hdk_pcg* st, void* stream);
+HDK_API int hdk_cpcg_p(int n, int nv, int columns, const double* z, double* p, double* pv, const int* p2v,
+                       const hdk_pcg* st, int* any, unsigned long long cond_handle, void* stream);
+HDK_API int hdk_cpcg_final(int n, int nv, int columns, const double* x, const double* z, double* xv, const int* p2v,
+                           void* stream);
+HDK_API int hdk_bapply_cols_sorted(const hdk_mesh* m, const double* dcomp, const double* x, size_t x_stride,
+                                   double* ef, size_t ef_stride, const int* corner_pos, const int* cond0,
+                                   int cond_stride, int columns, void* stream);
 
 /* ---- segmented batch (lockstep C5 engine, engine.cpp segments > 1) --------
  * S samples of one mesh as one concatenated problem: sample s owns vertices

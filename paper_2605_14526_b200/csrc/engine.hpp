@@ -195,6 +195,10 @@ class Engine {
   // Solves rows [r0, r0 + kColumns) of contact frame c (rows past k repeat
   // the last one); returns the iterations of the real columns.
   int solve_columns(const ContactFrame& c, int r0);
+  // The same rows by column-batched CG (the default with use_pcg_); false
+  // when a column's p.q <= 0 (the caller runs the Anderson columns).
+  bool solve_columns_pcg(const ContactFrame& c, int r0, int& iterations);
+  void build_columns_pcg();
   // All K columns of contact frame c through the kColumns slots, a finished
   // slot refilled with the next row (the loop exits when a column finishes);
   // returns the columns' iterations.  Opt-in (HETERODYN_COLUMN_REFILL=1): the

@@ -42,7 +42,20 @@ struct Engine::ColumnSet {
   int* expected = nullptr;   // columns iterating at launch (device)
   int* h_expected = nullptr;
   hdk_bb_columns bb{};  // every column's backbone buffers, for the one-launch-per-stage body
+  // Column-batched CG (the default backbone, engine_pcg.cpp's algorithm per
+  // column): the columns' seed / x by vertex, their seedp / xp / R(x0) in
+  // elimination order and their element forces are contiguous [kColumns][..]
+  // (Col's pointers index into them); r is rhs.
+  double *seed_all = nullptr, *x_all = nullptr, *seedp_all = nullptr, *xp_all = nullptr, *rx_all = nullptr,
+         *ef_all = nullptr;
+  double *cz = nullptr, *cp = nullptr, *cq = nullptr, *cax = nullptr, *cpv = nullptr, *cpart = nullptr;
+  hdk_pcg* cst = nullptr;
+  hdk_pcg* h_cst = nullptr;
+  unsigned int* ctickets = nullptr;
+  LoopGraph pgraph;
   ~ColumnSet() {
+    pgraph.destroy();
+    if (h_cst) cudaFreeHost(h_cst);
     graph.destroy();
     rgraph.destroy();
     if (h_expected) cudaFreeHost(h_expected);
@@ -79,19 +92,28 @@ void Engine::build_columns() {
   S.f.run_flag = S.any;
   cuda_check(cudaMallocHost(&S.h_ctls, sizeof(hdk_ctl) * kColumns), "pinned ctl");
   cuda_check(cudaMallocHost(&S.h_any, sizeof(int)), "pinned flag");
+  S.seed_all = A.alloc<double>(kColumns * n3);
+  S.x_all = A.alloc<double>(kColumns * n3);
+  S.seedp_all = A.alloc<double>(kColumns * n3p);
+  S.xp_all = A.alloc<double>(kColumns * n3p);
+  S.rx_all = A.alloc<double>(kColumns * n3p);
+  S.ef_all = A.alloc<double>(kColumns * 12 * ne);
   for (int c = 0; c < kColumns; ++c) {
     ColumnSet::Col& C = S.col[c];
     C.ctl = S.ctls + c;
     C.snap = A.alloc<hdk_ctl>(1);
     C.res = A.raw(hdk_bb_result_bytes());
-    C.seed = A.alloc<double>(n3);
-    C.x = A.alloc<double>(n3);
+    C.seed = S.seed_all + c * n3;
+    C.x = S.x_all + c * n3;
     C.tv = A.alloc<double>(n3);
-    for (double** v : {&C.seedp, &C.xp, &C.t, &C.lastq, &C.lastg, &C.rt, &C.rx, &C.lrx, &C.lrg}) *v = A.alloc<double>(n3p);
+    C.seedp = S.seedp_all + c * n3p;
+    C.xp = S.xp_all + c * n3p;
+    C.rx = S.rx_all + c * n3p;
+    for (double** v : {&C.t, &C.lastq, &C.lastg, &C.rt, &C.lrx, &C.lrg}) *v = A.alloc<double>(n3p);
     C.dq = A.alloc<double>(HDK_AA_MAX * n3p);
     C.dg = A.alloc<double>(HDK_AA_MAX * n3p);
     C.rsq = A.alloc<double>(HDK_AA_MAX * n3p);
-    C.ef = A.alloc<double>(12 * ne);
+    C.ef = S.ef_all + c * 12 * ne;
     C.part = A.alloc<double>(HDK_RED_BLOCKS * HDK_RED_Q);
     C.f = S.f;
     C.f.part2 = S.f.part2 + c * p2;
@@ -311,8 +333,118 @@ double Engine::time_columns(int reps, unsigned skip) {
   return static_cast<double>(ms) / reps;
 }
 
+// The columns' CG loop (engine_pcg.cpp's algorithm, one CG per column, every
+// stage one launch for all kColumns columns): B p by column (blockIdx.y),
+// q = A p - gather(B p) with p.q, x / r, the multi-column solve z = A^{-1} r
+// folded per column with r.z and the stopping test, p = z + beta p.  The
+// multi-column solve runs while any column iterates.
+void Engine::build_columns_pcg() {
+  ColumnSet& S = *cols_;
+  DevArena& A = *S.mem;
+  const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), n3p = 3 * static_cast<size_t>(hf_.n),
+               ne = scene_.mesh.ne;
+  const int n = hf_.n, nv = scene_.mesh.nv, K = kColumns;
+  for (double** v : {&S.cz, &S.cp, &S.cq, &S.cax}) *v = A.alloc<double>(K * n3p);
+  S.cpv = A.alloc<double>(K * n3);
+  cuda_check(cudaMemset(S.cpv, 0, K * n3 * sizeof(double)), "zero pv");  // fixed vertices stay 0
+  S.cpart = A.alloc<double>(static_cast<size_t>(HDK_SEG_PSTRIDE) * K);
+  S.cst = A.alloc<hdk_pcg>(K);
+  S.ctickets = A.alloc<unsigned int>(K);
+  cuda_check(cudaMemset(S.ctickets, 0, sizeof(unsigned int) * K), "zero tickets");
+  cuda_check(cudaMallocHost(&S.h_cst, sizeof(hdk_pcg) * K), "pinned pcg");
+  void* s = st_;
+  const int cstride = static_cast<int>(sizeof(hdk_pcg) / sizeof(int));
+  auto pre = [&] {
+    hdk_ok(hdk_spcg_init(S.cst, K, 1e-10, 500, S.any, s), "pcg init");
+    for (int c = 0; c < K; ++c) {
+      ColumnSet::Col& C = S.col[c];
+      hdk_ok(hdk_gather_perm(&dv_, C.seed, nullptr, C.seedp, s), "seed in elimination order");
+      hdk_ok(hdk_gather_perm(&dv_, C.x, nullptr, C.xp, s), "x0 in elimination order");
+      hdk_ok(hdk_bapply(&dm_, dcomp_, C.x, C.ef, s), "B x0");
+      hdk_ok(hdk_gather_pp(&dv_, nullptr, C.ef, C.rx, nullptr, s), "R(x0)");
+    }
+    hdk_ok(hdk_cpcg_spmv(&a_ff_, K, S.xp_all, S.cax, S.cst, s), "A x0");
+    hdk_ok(hdk_pcg_r0(static_cast<int>(K * n3p), S.seedp_all, S.cax, S.rx_all, S.rhs, s), "r0");
+    hdk_ok(hdk_apply_inverse3_multi(&S.f, S.rhs, K, s), "z0 = A^-1 r0");
+    hdk_ok(hdk_cpcg_rz(&S.f, K, S.rhs, S.cz, S.xp_all, S.cpart, S.ctickets, S.cst, s), "rz");
+    hdk_ok(hdk_cpcg_p(n, nv, K, S.cz, S.cp, S.cpv, df_.p2v, S.cst, S.any, 0ULL, s), "p");
+  };
+  auto body = [&](unsigned long long handle) {
+    hdk_ok(hdk_bapply_cols_sorted(&dm_, dcomp_, S.cpv, n3, S.ef_all, 12 * ne, corner_pos_, &S.cst->cond, cstride, K,
+                                  s),
+           "B p (columns)");
+    hdk_ok(hdk_cpcg_apply(&dv_, &a_ff_, K, S.ef_all, 12 * ne, S.cp, S.cq, S.cpart, S.ctickets, S.cst, s),
+           "q = (A - B) p (columns)");
+    hdk_ok(hdk_spcg_xr(static_cast<int>(n3p), static_cast<int>(K * n3p), S.xp_all, S.rhs, S.cp, S.cq, S.cst, s),
+           "x, r (columns)");
+    hdk_ok(hdk_apply_inverse3_multi(&S.f, S.rhs, K, s), "z = A^-1 r (columns)");
+    hdk_ok(hdk_cpcg_rz(&S.f, K, S.rhs, S.cz, S.xp_all, S.cpart, S.ctickets, S.cst, s), "rz (columns)");
+    hdk_ok(hdk_cpcg_p(n, nv, K, S.cz, S.cp, S.cpv, df_.p2v, S.cst, S.any, handle, s), "p + any (columns)");
+  };
+  build_loop_graph(st_, use_cond_, pre, body, [] {}, S.pgraph);
+}
+
+bool Engine::solve_columns_pcg(const ContactFrame& c, int r0, int& iterations) {
+  ColumnSet& S = *cols_;
+  if (!S.cst) build_columns_pcg();
+  const int nv = scene_.mesh.nv, K = kColumns;
+  const size_t n3 = 3 * static_cast<size_t>(nv);
+  for (int j = 0; j < K; ++j) {
+    const int row = std::min(r0 + j, c.k - 1);
+    hdk_ok(hdk_contact_column_init(&c.view, row, nv, df_.v2p, S.col[j].seed, S.col[j].x, st_), "column init");
+  }
+  kernel_launches += K;
+  if (ph_.on) cuda_check(cudaEventRecord(ph_.ev[6], st_), "phase event");
+  LoopGraph& g = S.pgraph;
+  if (g.exec) {
+    cuda_check(cudaGraphLaunch(g.exec, st_), "columns (CG)");
+  } else {  // host-driven loop (profiling fallback)
+    if (g.pre) cuda_check(cudaGraphLaunch(g.pre, st_), "columns (CG)");
+    for (;;) {
+      cuda_check(cudaMemcpyAsync(S.h_any, S.any, sizeof(int), cudaMemcpyDeviceToHost, st_), "flag");
+      cuda_check(cudaStreamSynchronize(st_), "sync");
+      if (!*S.h_any) break;
+      cuda_check(cudaGraphLaunch(g.body, st_), "columns (CG)");
+    }
+  }
+  cuda_check(cudaMemcpyAsync(S.h_cst, S.cst, sizeof(hdk_pcg) * K, cudaMemcpyDeviceToHost, st_), "pcg state");
+  cuda_check(cudaStreamSynchronize(st_), "columns (CG) sync");
+  const int real = std::min(K, c.k - r0);
+  int iters = 0, most = 0;
+  for (int j = 0; j < real; ++j) {
+    const hdk_pcg& h = S.h_cst[j];
+    if (h.err == -1) {  // not positive definite along a direction: Anderson for this batch
+      ++pcg_fallbacks;
+      return false;
+    }
+    if (h.err != 0) raise(Code::AdjointDiverged, "backward step: contact column CG did not settle (cap or non-finite values)");
+    iters += 1 + h.iter;
+    most = std::max(most, h.iter);
+  }
+  for (int j = real; j < K; ++j) most = std::max(most, S.h_cst[j].iter);
+  hdk_ok(hdk_cpcg_final(hf_.n, nv, K, S.xp_all, S.cz, S.x_all, df_.p2v, st_), "x = x + z (columns)");
+  cuda_check(cudaMemcpyAsync(cX_ + n3 * r0, S.x_all, n3 * real * sizeof(double), cudaMemcpyDeviceToDevice, st_),
+             "columns");
+  if (ph_.on) {
+    cuda_check(cudaEventRecord(ph_.ev[7], st_), "phase event");
+    cuda_check(cudaEventSynchronize(ph_.ev[7]), "phase event");
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ph_.ev[6], ph_.ev[7]) == cudaSuccess) ph_.col_ms += ms;
+  }
+  kernel_launches += g.counts[0] + static_cast<long long>(g.counts[1]) * most + 1;
+  ph_.col_batches += 1;
+  ph_.col_iters += 1 + most;
+  ph_.col_real_iters += iters;
+  iterations = iters;
+  return true;
+}
+
 int Engine::solve_columns(const ContactFrame& c, int r0) {
   if (!cols_) build_columns();
+  if (use_pcg_) {
+    int it = 0;
+    if (solve_columns_pcg(c, r0, it)) return it;
+  }
   ColumnSet& S = *cols_;
   const int nv = scene_.mesh.nv;
   for (int j = 0; j < kColumns; ++j) {

@@ -398,6 +398,19 @@ __global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __
   bapply_body(m, dcomp, x, ef, run_flag, corner_pos);
 }
 
+// B p of the contact-adjoint columns' CG (blockIdx.y = column): each column's
+// direction by vertex at x + c x_stride, its sorted element forces at
+// ef + c ef_stride; a column whose CG has ended (run flag at
+// cond0[c cond_stride] == 0) does nothing.
+__global__ void __launch_bounds__(128) k_bapply_cols_sorted(hdk_mesh m, const double* __restrict__ dcomp,
+                                                            const double* __restrict__ x, size_t x_stride,
+                                                            double* __restrict__ ef, size_t ef_stride,
+                                                            const int* __restrict__ corner_pos, const int* cond0,
+                                                            int cond_stride) {
+  const int c = blockIdx.y;
+  bapply_body(m, dcomp, x + c * x_stride, ef + c * ef_stride, cond0 + (size_t)c * cond_stride, corner_pos);
+}
+
 // B t of the contact-adjoint columns, blockIdx.y = column.
 __global__ void __launch_bounds__(128) k_bapply_bbcols(hdk_mesh m, const double* __restrict__ dcomp, hdk_bb_columns c) {
   const hdk_bb_column& k = c.col[blockIdx.y];
@@ -510,6 +523,14 @@ HDK_API int hdk_bapply(const hdk_mesh* m, const double* dcomp, const double* x, 
 HDK_API int hdk_bapply_flag(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
                             const int* run_flag, void* stream) {
   return hdk_bapply_sorted(m, dcomp, x, elem_force, nullptr, run_flag, stream);
+}
+
+HDK_API int hdk_bapply_cols_sorted(const hdk_mesh* m, const double* dcomp, const double* x, size_t x_stride,
+                                   double* ef, size_t ef_stride, const int* corner_pos, const int* cond0,
+                                   int cond_stride, int columns, void* stream) {
+  hdk::launch(k_bapply_cols_sorted, dim3(blocks(m->ne, 128), columns), dim3(128), 0, static_cast<cudaStream_t>(stream),
+              *m, dcomp, x, x_stride, ef, ef_stride, corner_pos, cond0, cond_stride);
+  return static_cast<int>(cudaGetLastError());
 }
 
 HDK_API int hdk_bapply_sorted(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,

@@ -582,3 +582,224 @@ HDK_API int hdk_spcg_p(int n3s, int n3, const double* z, double* p, double* pv, 
 }
 
 }  // extern "C"
+
+// ---- contact-adjoint columns: one CG per column, all columns per launch -------
+// Column c's vectors (elimination order) at base + c n3 (n3 = 3 n); its
+// direction by vertex at pv + c n3v; its sorted element forces at
+// ef + c ef_stride; z = A^{-1} r is folded per column from the multi-column
+// solve's tile partials (part2 + c part2_stride, as the backbone dots fold t).
+namespace {
+
+__global__ void k_cpcg_spmv(hdk_csr A, int n3, const double* __restrict__ p, double* __restrict__ y,
+                            const hdk_pcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int c = blockIdx.y;
+  if (st[c].cond == 0) return;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= A.rows) return;
+  const double* pc = p + (size_t)c * n3;
+  double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+  for (int k = A.off[row]; k < A.off[row + 1]; ++k) {
+    const double w = A.val[k];
+    const double* v = pc + 3 * (size_t)A.col[k];
+    y0 += w * v[0];
+    y1 += w * v[1];
+    y2 += w * v[2];
+  }
+  double* yc = y + (size_t)c * n3 + 3 * (size_t)row;
+  yc[0] = y0;
+  yc[1] = y1;
+  yc[2] = y2;
+}
+
+__global__ void __launch_bounds__(kT) k_cpcg_apply(hdk_vtx x, hdk_csr A, int n3, const double* __restrict__ ef,
+                                                   size_t ef_stride, const double* __restrict__ p,
+                                                   double* __restrict__ q, double* partial, unsigned int* tickets,
+                                                   hdk_pcg* sts) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int c = blockIdx.y;
+  hdk_pcg* st = sts + c;
+  if (st->cond == 0) return;
+  const double* efc = ef + c * ef_stride;
+  const double* pc = p + (size_t)c * n3;
+  double* qc = q + (size_t)c * n3;
+  const int sub = threadIdx.x & 7, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[1] = {0.0};
+  for (int rb = blockIdx.x * (kT / 8) + 4 * warp; rb < x.n; rb += kSRB * (kT / 8)) {
+    const int row = rb + (lane >> 3);
+    const bool live = row < x.n;
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    const int e = live ? __ldg(x.pinc_off + row + 1) : 0;
+    for (int j = (live ? __ldg(x.pinc_off + row) : 0) + sub; j < e; j += 8) {
+      const double* f = efc + 3 * (size_t)j;
+      c0 += __ldg(f);
+      c1 += __ldg(f + 1);
+      c2 += __ldg(f + 2);
+    }
+    const int ke = live ? __ldg(A.off + row + 1) : 0;
+    for (int k = (live ? __ldg(A.off + row) : 0) + sub; k < ke; k += 8) {
+      const double w = __ldg(A.val + k);
+      const double* v = pc + 3 * (size_t)__ldg(A.col + k);
+      a0 += w * v[0];
+      a1 += w * v[1];
+      a2 += w * v[2];
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+      c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+      c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (sub == 0 && live) {
+      const double q0 = a0 - c0, q1 = a1 - c1, q2 = a2 - c2;
+      double* qr = qc + 3 * (size_t)row;
+      qr[0] = q0;
+      qr[1] = q1;
+      qr[2] = q2;
+      const double* pr = pc + 3 * (size_t)row;
+      acc[0] += (pr[0] * q0 + pr[1] * q1) + pr[2] * q2;
+    }
+  }
+  double* part = partial + (size_t)c * HDK_SEG_PSTRIDE;
+  block_store_rb<1>(acc, part);
+  if (!last_block(tickets + c)) return;
+  if (threadIdx.x >= 32) return;
+  const double pq = fold_rb(part, 0);
+  if (threadIdx.x != 0) return;
+  st->pq = pq;
+  if (!(pq > 0.0)) {
+    st->err = -1;
+    st->cond = 0;
+  } else {
+    st->alpha = st->rz / pq;
+  }
+}
+
+// z = A^{-1} r folded per column from the multi-column solve's tile partials
+// (the fold of hdk_bb_dots), then r.z, the stopping test and beta.
+__global__ void __launch_bounds__(kT) k_cpcg_rz(hdk_factor f, size_t part2_stride, const double* __restrict__ r,
+                                                double* __restrict__ z, const double* __restrict__ x, double* partial,
+                                                unsigned int* tickets, hdk_pcg* sts) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int c = blockIdx.y;
+  hdk_pcg* st = sts + c;
+  if (st->cond == 0) return;
+  const size_t n3 = 3 * (size_t)f.n;
+  const double* p2 = f.part2 + c * part2_stride;
+  const double* rc = r + c * n3;
+  const double* xc = x + c * n3;
+  double* zc = z + c * n3;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (size_t i = blockIdx.x * kT + threadIdx.x; i < n3; i += (size_t)kSRB * kT) {
+    const int col = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)col);
+    const int tile = col >> 8;
+    const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
+    const size_t base = (size_t)(tile + tb0) * 256 + (col & 255);
+    double zi = 0.0;
+    for (int b = 0; b <= tb1 - tb0; ++b) zi += __ldg(p2 + 3 * (base + 256 * (size_t)b) + a);
+    zc[i] = zi;
+    const double t = xc[i] + zi;
+    acc[0] += rc[i] * zi;
+    acc[1] += zi * zi;
+    acc[2] += t * t;
+  }
+  double* part = partial + (size_t)c * HDK_SEG_PSTRIDE;
+  block_store_rb<3>(acc, part);
+  if (!last_block(tickets + c)) return;
+  if (threadIdx.x >= 32) return;
+  const double rz = fold_rb(part, 0), zz = fold_rb(part, 1), tt = fold_rb(part, 2);
+  if (threadIdx.x != 0) return;
+  const int it = st->iter + 1;
+  st->iter = it;
+  const bool done = sqrt(zz) <= st->tol * fmax(sqrt(tt), 1e-30);
+  st->beta = st->rz > 0.0 && it > 1 ? rz / st->rz : 0.0;
+  st->rz = rz;
+  st->done = done ? 1 : 0;
+  if (!done && it >= st->k_max) st->err = 10;
+  if (!isfinite(rz)) st->err = 10;
+  st->cond = (!done && st->err == 0) ? 1 : 0;
+}
+
+// p = z + beta p per column and by vertex; block (0, 0) publishes the OR of
+// the columns' conditions (the multi-column solve's run flag, the WHILE condition).
+__global__ void k_cpcg_p(int n, int nv, const double* __restrict__ z, double* __restrict__ p, double* __restrict__ pv,
+                         const int* __restrict__ p2v, const hdk_pcg* st, int count, int* any,
+                         cudaGraphConditionalHandle handle, int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int c = blockIdx.y;
+  if (blockIdx.x == 0 && c == 0) {
+    int on = 0;
+    for (int s = threadIdx.x; s < count; s += blockDim.x) on |= (st[s].cond != 0 && st[s].err == 0) ? 1 : 0;
+    const int a = __syncthreads_or(on);
+    if (threadIdx.x == 0) {
+      *any = a;
+      if (use_handle) cudaGraphSetConditional(handle, a);
+    }
+  }
+  if (st[c].cond == 0) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n3 = 3 * n;
+  if (i >= n3) return;
+  const double b = st[c].beta;
+  const size_t k = (size_t)c * n3 + i;
+  const double v = z[k] + b * p[k];
+  p[k] = v;
+  const int row = i / 3;
+  pv[(size_t)c * 3 * nv + 3 * (size_t)__ldg(p2v + row) + (i - 3 * row)] = v;
+}
+
+// x_c + z_c by vertex into each column's vertex-order vector (fixed rows untouched).
+__global__ void k_cpcg_final(int n, int nv, const double* __restrict__ x, const double* __restrict__ z,
+                             double* __restrict__ xv, const int* __restrict__ p2v) {
+  const int c = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * n) return;
+  const size_t k = (size_t)c * 3 * n + i;
+  const int row = i / 3;
+  xv[(size_t)c * 3 * nv + 3 * (size_t)__ldg(p2v + row) + (i - 3 * row)] = x[k] + z[k];
+}
+
+}  // namespace
+
+extern "C" {
+
+HDK_API int hdk_cpcg_spmv(const hdk_csr* a, int columns, const double* p, double* y, const hdk_pcg* st,
+                          void* stream) {
+  hdk::launch(k_cpcg_spmv, dim3(nb(a->rows), columns), dim3(256), 0, S(stream), *a, 3 * a->rows, p, y, st);
+  return last();
+}
+HDK_API int hdk_cpcg_apply(const hdk_vtx* x, const hdk_csr* a, int columns, const double* ef_sorted,
+                           size_t ef_stride, const double* p, double* q, double* partial, unsigned int* tickets,
+                           hdk_pcg* st, void* stream) {
+  if (!x->pinc_off) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_cpcg_apply, dim3(kSRB, columns), dim3(kT), 0, S(stream), *x, *a, 3 * x->n, ef_sorted, ef_stride, p, q,
+              partial, tickets, st);
+  return last();
+}
+HDK_API int hdk_cpcg_rz(const hdk_factor* f, int columns, const double* r, double* z, const double* x,
+                        double* partial, unsigned int* tickets, hdk_pcg* st, void* stream) {
+  if (!f->tile_cta2) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_cpcg_rz, dim3(kSRB, columns), dim3(kT), 0, S(stream), *f, hdk_factor_part2_stride(f), r, z, x, partial,
+              tickets, st);
+  return last();
+}
+HDK_API int hdk_cpcg_p(int n, int nv, int columns, const double* z, double* p, double* pv, const int* p2v,
+                       const hdk_pcg* st, int* any, unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_cpcg_p, dim3(nb(3LL * n), columns), dim3(256), 0, S(stream), n, nv, z, p, pv, p2v, st, columns, any,
+              static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle ? 1 : 0);
+  return last();
+}
+HDK_API int hdk_cpcg_final(int n, int nv, int columns, const double* x, const double* z, double* xv, const int* p2v,
+                           void* stream) {
+  hdk::launch(k_cpcg_final, dim3(nb(3LL * n), columns), dim3(256), 0, S(stream), n, nv, x, z, xv, p2v);
+  return last();
+}
+
+}  // extern "C"
