@@ -548,9 +548,11 @@ def main():
         one_step()
     q_start = sim.positions()
     v_start = sim.velocities()
+    t_start = lib.lib.hd_sim_time(sim.h)
 
     # ---- device-resident throughput (value) ---------------------------------
     solves0 = sim.solve_count
+    streams0 = sim.factor_streams
     launches0 = sim.kernel_launches
     fwd_its, bwd_its = [], []
     if world > 1:
@@ -573,6 +575,7 @@ def main():
     bwd_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in split]))
     launches = sim.kernel_launches - launches0
     solves = sim.solve_count - solves0
+    streams = sim.factor_streams - streams0  # a multi-column solve of 8 contact columns streams the factor once
     from paper_2605_14526_b200.dist import max_over_ranks, replica_value
     ms = max_over_ranks(ms)
     if world > 1:
@@ -595,10 +598,14 @@ def main():
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
     e2.record(stream)
+    t_h = t_start  # the e2e steps replay the timed region's steps (same states, same times)
+    contacts_e2e = []
     for _ in range(args.steps):
-        lib.check(lib.lib.hd_sim_set_state(sim.h, ptr(q_h), ptr(v_h), 0.0))
+        lib.check(lib.lib.hd_sim_set_state(sim.h, ptr(q_h), ptr(v_h), t_h))
         lib.check(lib.lib.hd_sim_record(sim.h, 1))
         lib.check(lib.lib.hd_sim_step(sim.h))
+        t_h = lib.lib.hd_sim_time(sim.h)
+        contacts_e2e.append(sim.last_contact_count)
         lib.check(lib.lib.hd_sim_backward_canonical(sim.h, ptr(outs["dq0"]), ptr(outs["dv0"]), ptr(outs["df"]),
                                                     ptr(de_h), None, 0))
         lib.check(lib.lib.hd_sim_positions(sim.h, ptr(outs["q"]), n))
@@ -629,21 +636,27 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
 
     if rank == 0:
-        step_share = ms_solve * solves / args.steps / (ms / args.steps)
+        # factor streams timed as single solves (a multi-column stream costs more: a lower bound)
+        step_share = ms_solve * streams / args.steps / (ms / args.steps)
         # whole-step algorithmic bytes (SURVEY.md §8(d) with this layout: S' read
-        # twice per solve at 8 B per value, no indices): solves x solve bytes +
-        # per adjoint iteration a B apply (320 B/element) and the Anderson
-        # vectors with their R-space twin (2 x (2m + 4) x 24 B per vertex, m = 8)
-        # + per forward iteration a local sweep (100 B/element) and its vectors
-        # (20 x 24 B per vertex) + the cache / energy sweeps (3 x 100 B/element)
+        # twice per factor stream at 8 B per value, no indices; a multi-column
+        # stream reads it once for all its columns): streams x 16 nnz(S') +
+        # solves x 96 n (rhs / partials / z per column) + per adjoint iteration
+        # a B apply (320 B/element) and the backbone's vectors — CG: 24 x 24 B
+        # per vertex (A p with its CSR row, q, x / r, the z fold, p); Anderson:
+        # 2 x (2m + 4) x 24 B, m = 8 — + per forward iteration a local sweep
+        # (100 B/element) and its vectors (20 x 24 B per vertex) + the cache /
+        # energy sweeps (3 x 100 B/element)
         n_fwd, n_bwd = float(np.mean(fwd_its)), float(np.mean(bwd_its))
         nv = sc.vertex_count
-        step_bytes = (solves / args.steps * bytes_solve + n_bwd * (320.0 * ne + 960.0 * nv)
-                      + n_fwd * (100.0 * ne + 480.0 * nv) + 300.0 * ne)
+        factor_bytes = 16.0 * nnz
+        vec_b = 960.0 if os.environ.get("HETERODYN_ADJOINT", "pcg") == "aa" else 576.0
+        step_bytes = (streams / args.steps * factor_bytes + solves / args.steps * (bytes_solve - factor_bytes)
+                      + n_bwd * (320.0 * ne + vec_b * nv) + n_fwd * (100.0 * ne + 480.0 * nv) + 300.0 * ne)
         step_gbs = step_bytes / (ms / args.steps / 1e3) / 1e9
         step_roofline = {"bytes_per_step": step_bytes, "achieved_gbs": step_gbs, "frac": step_gbs / peak,
-                         "formula": "solves*(16 nnz(S')+96 n) + N_bwd*(320 n_e + 960 n_v) + N_fwd*(100 n_e + 480 n_v)"
-                                    " + 300 n_e"}
+                         "formula": "streams*16 nnz(S') + solves*96 n + N_bwd*(320 n_e + %d n_v) + N_fwd*(100 n_e + "
+                                    "480 n_v) + 300 n_e" % vec_b}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -657,8 +670,11 @@ def main():
                        "mean_forward_iterations": float(np.mean(fwd_its)),
                        "mean_adjoint_iterations": float(np.mean(bwd_its)),
                        "forward_ms": fwd_ms, "backward_ms": bwd_ms,
+                       "step_ms": [round(e[0].elapsed_time(e[2]), 3) for e in split],
                        "solves_per_step": solves / args.steps,
+                       "factor_streams_per_step": streams / args.steps,
                        "mean_contacts": float(np.mean(contacts[-args.steps:])),
+                       "mean_contacts_e2e": float(np.mean(contacts_e2e)),
                        "solve_share_of_step_est": step_share,
                        "step_roofline": step_roofline},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

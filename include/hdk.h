@@ -582,11 +582,14 @@ HDK_API int hdk_spcg_p(int n3s, int n3, const double* z, double* p, double* pv, 
  * partials. */
 HDK_API int hdk_cpcg_spmv(const hdk_csr* a, int columns, const double* p, double* y, const hdk_pcg* st,
                           void* stream);
+/* Per-column partials of hdk_cpcg_apply / hdk_cpcg_rz: column c's at
+ * partial + c pstride, pstride = hdk_cpcg_partial_stride(n) doubles. */
+HDK_API size_t hdk_cpcg_partial_stride(int n);
 HDK_API int hdk_cpcg_apply(const hdk_vtx* x, const hdk_csr* a, int columns, const double* ef_sorted,
-                           size_t ef_stride, const double* p, double* q, double* partial, unsigned int* tickets,
-                           hdk_pcg* st, void* stream);
+                           size_t ef_stride, const double* p, double* q, double* partial, size_t pstride,
+                           unsigned int* tickets, hdk_pcg* st, void* stream);
 HDK_API int hdk_cpcg_rz(const hdk_factor* f, int columns, const double* r, double* z, const double* x,
-                        double* partial, unsigned int* tickets, hdk_pcg* st, void* stream);
+                        double* partial, size_t pstride, unsigned int* tickets, hdk_pcg* st, void* stream);
 HDK_API int hdk_cpcg_p(int n, int nv, int columns, const double* z, double* p, double* pv, const int* p2v,
                        const hdk_pcg* st, int* any, unsigned long long cond_handle, void* stream);
 HDK_API int hdk_cpcg_final(int n, int nv, int columns, const double* x, const double* z, double* xv, const int* p2v,

@@ -183,6 +183,10 @@ HD_API hd_status hd_sim_set_young(hd_sim* sim, const double* young, size_t count
 HD_API long long hd_sim_factor_nnz(const hd_sim* sim);
 HD_API int hd_sim_free_count(const hd_sim* sim);
 HD_API long long hd_sim_solve_count(const hd_sim* sim);
+/* Passes over the factor that carried those solves: a multi-column solve of
+ * several contact-adjoint columns streams the factor once (B200 extension;
+ * equals hd_sim_solve_count where every solve is single). */
+HD_API long long hd_sim_factor_streams(const hd_sim* sim);
 HD_API long long hd_sim_a_spmv_count(const hd_sim* sim);
 HD_API long long hd_sim_refactor_count(const hd_sim* sim);
 

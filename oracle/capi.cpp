@@ -470,6 +470,7 @@ int hd_sim_free_count(const hd_sim* sim) { return sim ? sim->system.free_count()
 long long hd_sim_solve_count(const hd_sim* sim) {
   return sim ? static_cast<long long>(sim->system.factor().apply_inverse_count / 3) : 0;
 }
+long long hd_sim_factor_streams(const hd_sim* sim) { return hd_sim_solve_count(sim); }
 long long hd_sim_a_spmv_count(const hd_sim* sim) { return sim ? static_cast<long long>(sim->system.a_spmv_count) : 0; }
 long long hd_sim_refactor_count(const hd_sim* sim) { return sim ? static_cast<long long>(sim->system.refactor_count()) : 0; }
 

@@ -458,6 +458,7 @@ hd_status hd_sim_trace_loop(hd_sim* sim, double* out, size_t capacity, int* iter
 long long hd_sim_factor_nnz(const hd_sim* sim) { return sim ? sim->eng->factor().row_off.back() : 0; }
 int hd_sim_free_count(const hd_sim* sim) { return sim ? sim->eng->factor().n : 0; }
 long long hd_sim_solve_count(const hd_sim* sim) { return sim ? sim->eng->solve_count : 0; }
+long long hd_sim_factor_streams(const hd_sim* sim) { return sim ? sim->eng->factor_streams() : 0; }
 long long hd_sim_a_spmv_count(const hd_sim* sim) { return sim ? sim->eng->a_spmv_count : 0; }
 long long hd_sim_refactor_count(const hd_sim* sim) { return sim ? sim->eng->refactor_count : 0; }
 

@@ -241,6 +241,10 @@ class Engine {
   std::vector<double> seg_tau;       // segmented batch: tau of the last backward frame, per sample
   long long seg_sample_iterations = 0;  // sum over samples of their own iteration counts (fwd solves + adjoint)
   long long solve_count = 0, a_spmv_count = 0, refactor_count = 0, kernel_launches = 0;
+  // Contact-adjoint column solves (inside solve_count) and the multi-column
+  // factor streams that carried them (kColumns columns per stream).
+  long long column_solves = 0, column_streams = 0;
+  long long factor_streams() const { return solve_count - column_solves + column_streams; }
   const HostFactor& factor() const { return hf_; }
   const Mesh& mesh() const { return scene_.mesh; }
   const Material& material() const { return mat_; }

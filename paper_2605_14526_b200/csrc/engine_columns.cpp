@@ -252,6 +252,8 @@ int Engine::solve_all_columns(const ContactFrame& c) {
   }
   kernel_launches += static_cast<long long>(S.rgraph.counts[1]) * (iters / kColumns + rounds);
   ph_.col_batches += rounds;
+  column_solves += iters;
+  column_streams += iters / kColumns + rounds;
   return iters;
 }
 
@@ -347,7 +349,8 @@ void Engine::build_columns_pcg() {
   for (double** v : {&S.cz, &S.cp, &S.cq, &S.cax}) *v = A.alloc<double>(K * n3p);
   S.cpv = A.alloc<double>(K * n3);
   cuda_check(cudaMemset(S.cpv, 0, K * n3 * sizeof(double)), "zero pv");  // fixed vertices stay 0
-  S.cpart = A.alloc<double>(static_cast<size_t>(HDK_SEG_PSTRIDE) * K);
+  const size_t pst = hdk_cpcg_partial_stride(n);
+  S.cpart = A.alloc<double>(pst * K);
   S.cst = A.alloc<hdk_pcg>(K);
   S.ctickets = A.alloc<unsigned int>(K);
   cuda_check(cudaMemset(S.ctickets, 0, sizeof(unsigned int) * K), "zero tickets");
@@ -366,19 +369,19 @@ void Engine::build_columns_pcg() {
     hdk_ok(hdk_cpcg_spmv(&a_ff_, K, S.xp_all, S.cax, S.cst, s), "A x0");
     hdk_ok(hdk_pcg_r0(static_cast<int>(K * n3p), S.seedp_all, S.cax, S.rx_all, S.rhs, s), "r0");
     hdk_ok(hdk_apply_inverse3_multi(&S.f, S.rhs, K, s), "z0 = A^-1 r0");
-    hdk_ok(hdk_cpcg_rz(&S.f, K, S.rhs, S.cz, S.xp_all, S.cpart, S.ctickets, S.cst, s), "rz");
+    hdk_ok(hdk_cpcg_rz(&S.f, K, S.rhs, S.cz, S.xp_all, S.cpart, pst, S.ctickets, S.cst, s), "rz");
     hdk_ok(hdk_cpcg_p(n, nv, K, S.cz, S.cp, S.cpv, df_.p2v, S.cst, S.any, 0ULL, s), "p");
   };
   auto body = [&](unsigned long long handle) {
     hdk_ok(hdk_bapply_cols_sorted(&dm_, dcomp_, S.cpv, n3, S.ef_all, 12 * ne, corner_pos_, &S.cst->cond, cstride, K,
                                   s),
            "B p (columns)");
-    hdk_ok(hdk_cpcg_apply(&dv_, &a_ff_, K, S.ef_all, 12 * ne, S.cp, S.cq, S.cpart, S.ctickets, S.cst, s),
+    hdk_ok(hdk_cpcg_apply(&dv_, &a_ff_, K, S.ef_all, 12 * ne, S.cp, S.cq, S.cpart, pst, S.ctickets, S.cst, s),
            "q = (A - B) p (columns)");
     hdk_ok(hdk_spcg_xr(static_cast<int>(n3p), static_cast<int>(K * n3p), S.xp_all, S.rhs, S.cp, S.cq, S.cst, s),
            "x, r (columns)");
     hdk_ok(hdk_apply_inverse3_multi(&S.f, S.rhs, K, s), "z = A^-1 r (columns)");
-    hdk_ok(hdk_cpcg_rz(&S.f, K, S.rhs, S.cz, S.xp_all, S.cpart, S.ctickets, S.cst, s), "rz (columns)");
+    hdk_ok(hdk_cpcg_rz(&S.f, K, S.rhs, S.cz, S.xp_all, S.cpart, pst, S.ctickets, S.cst, s), "rz (columns)");
     hdk_ok(hdk_cpcg_p(n, nv, K, S.cz, S.cp, S.cpv, df_.p2v, S.cst, S.any, handle, s), "p + any (columns)");
   };
   build_loop_graph(st_, use_cond_, pre, body, [] {}, S.pgraph);
@@ -435,6 +438,8 @@ bool Engine::solve_columns_pcg(const ContactFrame& c, int r0, int& iterations) {
   ph_.col_batches += 1;
   ph_.col_iters += 1 + most;
   ph_.col_real_iters += iters;
+  column_solves += iters;
+  column_streams += 1 + most;
   iterations = iters;
   return true;
 }
@@ -488,6 +493,8 @@ int Engine::solve_columns(const ContactFrame& c, int r0) {
   kernel_launches += S.graph.counts[0] + static_cast<long long>(S.graph.counts[1]) * ((most + unroll_ - 1) / unroll_);
   ph_.col_batches += 1;
   ph_.col_iters += most;
+  column_solves += iters;
+  column_streams += most;
   ph_.col_real_iters += iters;
   return iters;
 }

@@ -228,10 +228,11 @@ void Engine::backward_frame(int t, GradOut& out) {
   ContactFrame* c = f.has_contacts && f.contacts->k > 0 ? f.contacts.get() : nullptr;
   if (c) {
     const int k = c->k;
-    if (cX_cols_ < static_cast<size_t>(k)) {
+    if (cX_cols_ < static_cast<size_t>(k)) {  // sized to the contact block's row capacity (grown geometrically)
+      const size_t cols = std::max(static_cast<size_t>(k), static_cast<size_t>(c->view.cap_k));
       if (cX_) cudaFree(cX_);
-      cuda_check(cudaMalloc(&cX_, sizeof(double) * n3 * k), "contact columns");
-      cX_cols_ = k;
+      cuda_check(cudaMalloc(&cX_, sizeof(double) * n3 * cols), "contact columns");
+      cX_cols_ = cols;
     }
     if (!cz0_) cuda_check(cudaMalloc(&cz0_, sizeof(double) * n3), "z0");
     cuda_check(cudaMemcpyAsync(cz0_, x_, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st_), "z0");

@@ -343,6 +343,8 @@ __global__ void __launch_bounds__(128) k_differential(hdk_mesh m, hdk_material m
   }
 }
 
+__device__ __forceinline__ M3 bforce(const ElemGeom& g, const double (&d)[30], const double* __restrict__ x);
+
 // Element force of B x: P = U (D o (U^T F(x) V)) V^T, f_i = P g_i.
 // Latency-bound (dependent index -> vertex gathers).  The block shape is a
 // template for A/B runs (HETERODYN_BAPPLY): the unbounded 128-thread form
@@ -366,6 +368,42 @@ __device__ __forceinline__ void bapply_body(const hdk_mesh& m, const double* __r
   HDK_TRACED_WAIT(hdk::kTrBapply);
   if (run_flag && *run_flag == 0) return;
   if (!live) return;
+  const M3 pm = bforce(g, d, x);
+  if (corner_pos) write_force_sorted(g, pm, ef, corner_pos, e);
+  else write_force(g, pm, ef, e);
+}
+
+// The contact-adjoint columns' B p, all columns per thread: the element's
+// geometry and differential are loaded once for the kColumns directions
+// (column c at x + c x_stride, its sorted forces at ef + c ef_stride; a
+// column whose CG has ended, cond0[c cond_stride] == 0, is skipped).
+template <int K>
+__global__ void __launch_bounds__(128) k_bapply_cols_fused(hdk_mesh m, const double* __restrict__ dcomp,
+                                                           const double* __restrict__ x, size_t x_stride,
+                                                           double* __restrict__ ef, size_t ef_stride,
+                                                           const int* __restrict__ corner_pos, const int* cond0,
+                                                           int cond_stride) {
+  hdk::pdl_trigger();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = e < m.ne;
+  const size_t n = m.ne;
+  const int ee = live ? e : 0;
+  const ElemGeom g = load_geom(m, ee);
+  double d[30];
+#pragma unroll
+  for (int i = 0; i < 30; ++i) d[i] = __ldg(dcomp + i * n + ee);
+  hdk::pdl_wait();
+  if (!live) return;
+#pragma unroll 1
+  for (int c = 0; c < K; ++c) {
+    if (cond0[(size_t)c * cond_stride] == 0) continue;
+    const M3 pm = bforce(g, d, x + c * x_stride);
+    write_force_sorted(g, pm, ef + c * ef_stride, corner_pos, e);
+  }
+}
+
+// The element force of B x from the element's geometry and differential.
+__device__ __forceinline__ M3 bforce(const ElemGeom& g, const double (&d)[30], const double* __restrict__ x) {
   const M3 df = def_grad(g, x);
   M3 u, v;
 #pragma unroll
@@ -386,9 +424,7 @@ __device__ __forceinline__ void bapply_body(const hdk_mesh& m, const double* __r
     o(i, j) = a * hat(i, j) + b * hat(j, i);
     o(j, i) = b * hat(i, j) + a * hat(j, i);
   }
-  const M3 pm = mul_nt(mul(u, o), v);
-  if (corner_pos) write_force_sorted(g, pm, ef, corner_pos, e);
-  else write_force(g, pm, ef, e);
+  return mul_nt(mul(u, o), v);
 }
 
 template <int T, int MINB>
@@ -528,6 +564,15 @@ HDK_API int hdk_bapply_flag(const hdk_mesh* m, const double* dcomp, const double
 HDK_API int hdk_bapply_cols_sorted(const hdk_mesh* m, const double* dcomp, const double* x, size_t x_stride,
                                    double* ef, size_t ef_stride, const int* corner_pos, const int* cond0,
                                    int cond_stride, int columns, void* stream) {
+  static const bool fused = [] {
+    const char* e = std::getenv("HETERODYN_BCOLS");  // "0": one column per blockIdx.y (A/B)
+    return !(e && e[0] == '0');
+  }();
+  if (fused && columns == 8) {
+    hdk::launch(k_bapply_cols_fused<8>, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m,
+                dcomp, x, x_stride, ef, ef_stride, corner_pos, cond0, cond_stride);
+    return static_cast<int>(cudaGetLastError());
+  }
   hdk::launch(k_bapply_cols_sorted, dim3(blocks(m->ne, 128), columns), dim3(128), 0, static_cast<cudaStream_t>(stream),
               *m, dcomp, x, x_stride, ef, ef_stride, corner_pos, cond0, cond_stride);
   return static_cast<int>(cudaGetLastError());

@@ -613,10 +613,40 @@ __global__ void k_cpcg_spmv(hdk_csr A, int n3, const double* __restrict__ p, dou
   yc[2] = y2;
 }
 
+// Column reductions over a grid that covers the rows once (no grid-stride
+// loop: at one block per SM-slot the columns' CG stages are latency-bound):
+// block b of column c stores quantity q at partial[c pstride + q nb + b];
+// the column's last block folds its nb partials in fixed order.
+__device__ __forceinline__ double fold_nb(const double* partial, int nb) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int b = lane; b < nb; b += 32) s += partial[b];
+  return warp_sum(s);
+}
+
+template <int NQ>
+__device__ __forceinline__ void block_store_nb(const double (&v)[NQ], double* partial, int nb) {
+  __shared__ double sm[kT / 32][NQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const double s = warp_sum(v[q]);
+    if (lane == 0) sm[warp][q] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < NQ) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) s += sm[w][threadIdx.x];
+    partial[threadIdx.x * nb + blockIdx.x] = s;
+  }
+}
+
+// q = A p - gather(B p) per column and p.q; 8 lanes per row, 32 rows per block.
 __global__ void __launch_bounds__(kT) k_cpcg_apply(hdk_vtx x, hdk_csr A, int n3, const double* __restrict__ ef,
                                                    size_t ef_stride, const double* __restrict__ p,
-                                                   double* __restrict__ q, double* partial, unsigned int* tickets,
-                                                   hdk_pcg* sts) {
+                                                   double* __restrict__ q, double* partial, size_t pstride,
+                                                   unsigned int* tickets, hdk_pcg* sts) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
   const int c = blockIdx.y;
@@ -625,51 +655,50 @@ __global__ void __launch_bounds__(kT) k_cpcg_apply(hdk_vtx x, hdk_csr A, int n3,
   const double* efc = ef + c * ef_stride;
   const double* pc = p + (size_t)c * n3;
   double* qc = q + (size_t)c * n3;
-  const int sub = threadIdx.x & 7, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double acc[1] = {0.0};
-  for (int rb = blockIdx.x * (kT / 8) + 4 * warp; rb < x.n; rb += kSRB * (kT / 8)) {
-    const int row = rb + (lane >> 3);
-    const bool live = row < x.n;
-    double c0 = 0.0, c1 = 0.0, c2 = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    const int e = live ? __ldg(x.pinc_off + row + 1) : 0;
-    for (int j = (live ? __ldg(x.pinc_off + row) : 0) + sub; j < e; j += 8) {
-      const double* f = efc + 3 * (size_t)j;
-      c0 += __ldg(f);
-      c1 += __ldg(f + 1);
-      c2 += __ldg(f + 2);
-    }
-    const int ke = live ? __ldg(A.off + row + 1) : 0;
-    for (int k = (live ? __ldg(A.off + row) : 0) + sub; k < ke; k += 8) {
-      const double w = __ldg(A.val + k);
-      const double* v = pc + 3 * (size_t)__ldg(A.col + k);
-      a0 += w * v[0];
-      a1 += w * v[1];
-      a2 += w * v[2];
-    }
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-      c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-      c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-    }
-    if (sub == 0 && live) {
-      const double q0 = a0 - c0, q1 = a1 - c1, q2 = a2 - c2;
-      double* qr = qc + 3 * (size_t)row;
-      qr[0] = q0;
-      qr[1] = q1;
-      qr[2] = q2;
-      const double* pr = pc + 3 * (size_t)row;
-      acc[0] += (pr[0] * q0 + pr[1] * q1) + pr[2] * q2;
-    }
+  const int sub = threadIdx.x & 7;
+  const int row = blockIdx.x * (kT / 8) + (threadIdx.x >> 3);
+  const bool live = row < x.n;
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  const int e = live ? __ldg(x.pinc_off + row + 1) : 0;
+  for (int j = (live ? __ldg(x.pinc_off + row) : 0) + sub; j < e; j += 8) {
+    const double* f = efc + 3 * (size_t)j;
+    c0 += __ldg(f);
+    c1 += __ldg(f + 1);
+    c2 += __ldg(f + 2);
   }
-  double* part = partial + (size_t)c * HDK_SEG_PSTRIDE;
-  block_store_rb<1>(acc, part);
+  const int ke = live ? __ldg(A.off + row + 1) : 0;
+  for (int k = (live ? __ldg(A.off + row) : 0) + sub; k < ke; k += 8) {
+    const double w = __ldg(A.val + k);
+    const double* v = pc + 3 * (size_t)__ldg(A.col + k);
+    a0 += w * v[0];
+    a1 += w * v[1];
+    a2 += w * v[2];
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+    c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+    c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+  }
+  double acc[1] = {0.0};
+  if (sub == 0 && live) {
+    const double q0 = a0 - c0, q1 = a1 - c1, q2 = a2 - c2;
+    double* qr = qc + 3 * (size_t)row;
+    qr[0] = q0;
+    qr[1] = q1;
+    qr[2] = q2;
+    const double* pr = pc + 3 * (size_t)row;
+    acc[0] = (pr[0] * q0 + pr[1] * q1) + pr[2] * q2;
+  }
+  double* part = partial + (size_t)c * pstride;
+  const int nb = gridDim.x;
+  block_store_nb<1>(acc, part, nb);
   if (!last_block(tickets + c)) return;
   if (threadIdx.x >= 32) return;
-  const double pq = fold_rb(part, 0);
+  const double pq = fold_nb(part, nb);
   if (threadIdx.x != 0) return;
   st->pq = pq;
   if (!(pq > 0.0)) {
@@ -681,10 +710,11 @@ __global__ void __launch_bounds__(kT) k_cpcg_apply(hdk_vtx x, hdk_csr A, int n3,
 }
 
 // z = A^{-1} r folded per column from the multi-column solve's tile partials
-// (the fold of hdk_bb_dots), then r.z, the stopping test and beta.
+// (the fold of hdk_bb_dots), then r.z, the stopping test and beta.  One
+// element per thread.
 __global__ void __launch_bounds__(kT) k_cpcg_rz(hdk_factor f, size_t part2_stride, const double* __restrict__ r,
                                                 double* __restrict__ z, const double* __restrict__ x, double* partial,
-                                                unsigned int* tickets, hdk_pcg* sts) {
+                                                size_t pstride, unsigned int* tickets, hdk_pcg* sts) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
   const int c = blockIdx.y;
@@ -692,11 +722,12 @@ __global__ void __launch_bounds__(kT) k_cpcg_rz(hdk_factor f, size_t part2_strid
   if (st->cond == 0) return;
   const size_t n3 = 3 * (size_t)f.n;
   const double* p2 = f.part2 + c * part2_stride;
-  const double* rc = r + c * n3;
-  const double* xc = x + c * n3;
-  double* zc = z + c * n3;
   double acc[3] = {0.0, 0.0, 0.0};
-  for (size_t i = blockIdx.x * kT + threadIdx.x; i < n3; i += (size_t)kSRB * kT) {
+  const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
+  if (i < n3) {
+    const double* rc = r + c * n3;
+    const double* xc = x + c * n3;
+    double* zc = z + c * n3;
     const int col = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)col);
     const int tile = col >> 8;
     const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
@@ -705,15 +736,16 @@ __global__ void __launch_bounds__(kT) k_cpcg_rz(hdk_factor f, size_t part2_strid
     for (int b = 0; b <= tb1 - tb0; ++b) zi += __ldg(p2 + 3 * (base + 256 * (size_t)b) + a);
     zc[i] = zi;
     const double t = xc[i] + zi;
-    acc[0] += rc[i] * zi;
-    acc[1] += zi * zi;
-    acc[2] += t * t;
+    acc[0] = rc[i] * zi;
+    acc[1] = zi * zi;
+    acc[2] = t * t;
   }
-  double* part = partial + (size_t)c * HDK_SEG_PSTRIDE;
-  block_store_rb<3>(acc, part);
+  double* part = partial + (size_t)c * pstride;
+  const int nb = gridDim.x;
+  block_store_nb<3>(acc, part, nb);
   if (!last_block(tickets + c)) return;
   if (threadIdx.x >= 32) return;
-  const double rz = fold_rb(part, 0), zz = fold_rb(part, 1), tt = fold_rb(part, 2);
+  const double rz = fold_nb(part, nb), zz = fold_nb(part + nb, nb), tt = fold_nb(part + 2 * nb, nb);
   if (threadIdx.x != 0) return;
   const int it = st->iter + 1;
   st->iter = it;
@@ -775,19 +807,25 @@ HDK_API int hdk_cpcg_spmv(const hdk_csr* a, int columns, const double* p, double
   hdk::launch(k_cpcg_spmv, dim3(nb(a->rows), columns), dim3(256), 0, S(stream), *a, 3 * a->rows, p, y, st);
   return last();
 }
+HDK_API size_t hdk_cpcg_partial_stride(int n) {
+  const size_t apply_blocks = (static_cast<size_t>(n) + kT / 8 - 1) / (kT / 8);
+  const size_t rz_blocks = (3 * static_cast<size_t>(n) + kT - 1) / kT;
+  return 3 * (apply_blocks > rz_blocks ? apply_blocks : rz_blocks);
+}
 HDK_API int hdk_cpcg_apply(const hdk_vtx* x, const hdk_csr* a, int columns, const double* ef_sorted,
-                           size_t ef_stride, const double* p, double* q, double* partial, unsigned int* tickets,
-                           hdk_pcg* st, void* stream) {
+                           size_t ef_stride, const double* p, double* q, double* partial, size_t pstride,
+                           unsigned int* tickets, hdk_pcg* st, void* stream) {
   if (!x->pinc_off) return static_cast<int>(cudaErrorInvalidValue);
-  hdk::launch(k_cpcg_apply, dim3(kSRB, columns), dim3(kT), 0, S(stream), *x, *a, 3 * x->n, ef_sorted, ef_stride, p, q,
-              partial, tickets, st);
+  const int nbx = (x->n + kT / 8 - 1) / (kT / 8);
+  hdk::launch(k_cpcg_apply, dim3(nbx > 0 ? nbx : 1, columns), dim3(kT), 0, S(stream), *x, *a, 3 * x->n, ef_sorted,
+              ef_stride, p, q, partial, pstride, tickets, st);
   return last();
 }
 HDK_API int hdk_cpcg_rz(const hdk_factor* f, int columns, const double* r, double* z, const double* x,
-                        double* partial, unsigned int* tickets, hdk_pcg* st, void* stream) {
+                        double* partial, size_t pstride, unsigned int* tickets, hdk_pcg* st, void* stream) {
   if (!f->tile_cta2) return static_cast<int>(cudaErrorInvalidValue);
-  hdk::launch(k_cpcg_rz, dim3(kSRB, columns), dim3(kT), 0, S(stream), *f, hdk_factor_part2_stride(f), r, z, x, partial,
-              tickets, st);
+  hdk::launch(k_cpcg_rz, dim3(nb(3LL * f->n), columns), dim3(kT), 0, S(stream), *f, hdk_factor_part2_stride(f), r, z,
+              x, partial, pstride, tickets, st);
   return last();
 }
 HDK_API int hdk_cpcg_p(int n, int nv, int columns, const double* z, double* p, double* pv, const int* p2v,

@@ -78,6 +78,7 @@ SIGNATURES = {
     "hd_sim_factor_nnz": (C.c_longlong, [_VP]),
     "hd_sim_free_count": (C.c_int, [_VP]),
     "hd_sim_solve_count": (C.c_longlong, [_VP]),
+    "hd_sim_factor_streams": (C.c_longlong, [_VP]),
     "hd_sim_a_spmv_count": (C.c_longlong, [_VP]),
     "hd_sim_refactor_count": (C.c_longlong, [_VP]),
     "hd_sim_backward_canonical": (C.c_int, [_VP, _D, _D, _D, _D, _D, C.c_size_t]),
@@ -458,6 +459,10 @@ class Sim:
     @property
     def solve_count(self):
         return self.L.lib.hd_sim_solve_count(self.h)
+
+    @property
+    def factor_streams(self):
+        return self.L.lib.hd_sim_factor_streams(self.h)
 
     @property
     def a_spmv_count(self):
