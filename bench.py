@@ -671,6 +671,8 @@ def main():
                        "mean_adjoint_iterations": float(np.mean(bwd_its)),
                        "forward_ms": fwd_ms, "backward_ms": bwd_ms,
                        "step_ms": [round(e[0].elapsed_time(e[2]), 3) for e in split],
+                       "contacts_per_step": [int(x) for x in contacts[-args.steps:]],
+                       "adjoint_iterations_per_step": [int(x) for x in bwd_its],
                        "solves_per_step": solves / args.steps,
                        "factor_streams_per_step": streams / args.steps,
                        "mean_contacts": float(np.mean(contacts[-args.steps:])),

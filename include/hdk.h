@@ -58,7 +58,7 @@ typedef struct hdk_material {
  * persistent CTA an equal contiguous range of chunks, streamed into shared
  * memory with bulk asynchronous copies (factor.cpp:106-109). */
 #define HDK_CHUNK_VALS 3072
-#define HDK_CHUNK_SEGS 256
+#define HDK_CHUNK_SEGS 64 /* caps the per-stage segment (and pass-2 z-row) staging */
 
 typedef struct hdk_seg {   /* 16 bytes */
   int row;                 /* S' row */
@@ -585,6 +585,9 @@ HDK_API int hdk_cpcg_spmv(const hdk_csr* a, int columns, const double* p, double
 /* Per-column partials of hdk_cpcg_apply / hdk_cpcg_rz: column c's at
  * partial + c pstride, pstride = hdk_cpcg_partial_stride(n) doubles. */
 HDK_API size_t hdk_cpcg_partial_stride(int n);
+/* Profiling: per-chunk ring timestamps of the multi-column passes (4 int64 per
+ * chunk, solve.cu g_chunk_trace); NULL turns the trace off. */
+HDK_API int hdk_set_chunk_trace(long long* const* trace, void* stream);
 HDK_API int hdk_cpcg_apply(const hdk_vtx* x, const hdk_csr* a, int columns, const double* ef_sorted,
                            size_t ef_stride, const double* p, double* q, double* partial, size_t pstride,
                            unsigned int* tickets, hdk_pcg* st, void* stream);

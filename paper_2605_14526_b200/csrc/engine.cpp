@@ -22,10 +22,15 @@ static void hdk_check(int e, const char* what) { cuda_check(static_cast<cudaErro
 DevArena::~DevArena() {
   for (void* p : ptrs) cudaFree(p);
 }
+void cuda_zero(void* p, size_t bytes, const char* what) {
+  cuda_check(cudaMemsetAsync(p, 0, bytes, cudaStreamLegacy), what);
+  cuda_check(cudaStreamSynchronize(cudaStreamLegacy), what);
+}
+
 void* DevArena::raw(size_t bytes) {
   void* p = nullptr;
   cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
-  cuda_check(cudaMemset(p, 0, bytes), "cudaMemset");
+  cuda_zero(p, bytes, "cudaMemset");
   ptrs.push_back(p);
   return p;
 }
@@ -215,6 +220,7 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared
   cuda_check(cudaMallocHost(&h_ctl_, sizeof(hdk_ctl) * segs_), "pinned ctl");
   if (const char* pe = std::getenv("HETERODYN_PHASES"); pe && std::atoi(pe) != 0) {
     ph_.on = true;
+    ph_.per_frame = std::atoi(pe) == 2;
     for (cudaEvent_t& e : ph_.ev) cuda_check(cudaEventCreate(&e), "phase event");
   }
   fgraph_ = std::make_unique<LoopGraph>();
@@ -277,6 +283,7 @@ Engine::~Engine() {
       std::fprintf(stderr, "  contact columns: %lld batches of %d, %.3f ms total, %lld batched iterations "
                    "(%.1f us each), %lld column iterations\n", ph_.col_batches, kColumns, ph_.col_ms,
                    ph_.col_iters, 1e3 * ph_.col_ms / std::max(1LL, ph_.col_iters), ph_.col_real_iters);
+    std::fprintf(stderr, "  CG backbone fallbacks to Anderson (p.q <= 0): %lld\n", pcg_fallbacks);
   }
   for (cudaEvent_t e : ph_.ev)
     if (e) cudaEventDestroy(e);
@@ -353,10 +360,10 @@ void Engine::build_static() {
   snap_ = A.alloc<hdk_ctl>(segs_);
   if (segs_ > 1) {
     part18_ = A.alloc<double>(static_cast<size_t>(HDK_SEG_PSTRIDE) * segs_);
-    cuda_check(cudaMemset(part18_, 0, sizeof(double) * HDK_SEG_PSTRIDE * segs_), "zero partials");
+    cuda_zero(part18_, sizeof(double) * HDK_SEG_PSTRIDE * segs_, "zero partials");
     any_ = A.alloc<int>(1);
     gate_ticket_ = A.alloc<unsigned int>(1);
-    cuda_check(cudaMemset(gate_ticket_, 0, sizeof(unsigned int)), "zero ticket");
+    cuda_zero(gate_ticket_, sizeof(unsigned int), "zero ticket");
     seg_windows_ = A.alloc<int>(2 * static_cast<size_t>(segs_));
     seg_means_dev_ = A.alloc<double>(3 * static_cast<size_t>(segs_));
   }
@@ -390,7 +397,7 @@ void Engine::build_static() {
   dmat_.w2 = A.alloc<double>(ne);
   dmat_.mu_e = A.alloc<double>(ne);
   dmat_.lambda_e = A.alloc<double>(ne);
-  cuda_check(cudaMemset(ticket_, 0, sizeof(unsigned int) * segs_), "zero tickets");
+  cuda_zero(ticket_, sizeof(unsigned int) * segs_, "zero tickets");
   dmat_.beta_vh = mat_.beta0 > 0 ? A.alloc<double>(ne) : nullptr;
   dmat_.vol = A.upload(m.vol);
   upload_material();

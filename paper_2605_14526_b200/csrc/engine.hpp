@@ -35,6 +35,12 @@ struct DevArena {
 };
 
 void cuda_check(cudaError_t e, const char* what);
+// Zero device memory and wait for it: a plain cudaMemset runs on the legacy
+// stream, which does not order against the engines' non-blocking streams, so
+// a buffer zeroed after the engine started (lazily built graphs) could be
+// cleared while its first kernels already run (seen as nondeterminism with
+// several engines per process, HETERODYN_BATCH=streams).
+void cuda_zero(void* p, size_t bytes, const char* what);
 
 struct LoopGraph {
   cudaGraphExec_t exec = nullptr, pre = nullptr, body = nullptr, post = nullptr;
@@ -177,6 +183,8 @@ class Engine {
     long long n = 0;
     double col_ms = 0;  // contact columns: time, batches, batched and per-column iterations
     long long col_batches = 0, col_iters = 0, col_real_iters = 0;
+    bool per_frame = false;  // HETERODYN_PHASES=2: one stderr line per backward frame
+    double last_col_ms = 0;
   } ph_;
   void phase_mark(int i);
   void phase_collect(int first, int last);

@@ -11,7 +11,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
+#include <vector>
 
 namespace hdb {
 
@@ -53,7 +55,26 @@ struct Engine::ColumnSet {
   hdk_pcg* h_cst = nullptr;
   unsigned int* ctickets = nullptr;
   LoopGraph pgraph;
+  long long* trace = nullptr;  // profiling (HETERODYN_CHUNK_TRACE)
+  long long** h_trace_ptr = nullptr;
+  const char* trace_path = nullptr;
+  int trace_grid = 0, trace_chunks = 0;
+  std::vector<int> h_first2;
   ~ColumnSet() {
+    if (trace) {
+      std::vector<long long> h(4 * static_cast<size_t>(trace_chunks));
+      if (cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess) {
+        if (FILE* fp = std::fopen(trace_path, "wb")) {
+          std::fwrite(&trace_grid, sizeof(int), 1, fp);
+          std::fwrite(h_first2.data(), sizeof(int), h_first2.size(), fp);
+          std::fwrite(h.data(), sizeof(long long), h.size(), fp);
+          std::fclose(fp);
+        }
+      }
+      cudaFree(trace);
+      cudaFreeHost(h_trace_ptr);
+    }
+    pgraph.destroy();
     pgraph.destroy();
     if (h_cst) cudaFreeHost(h_cst);
     graph.destroy();
@@ -348,12 +369,12 @@ void Engine::build_columns_pcg() {
   const int n = hf_.n, nv = scene_.mesh.nv, K = kColumns;
   for (double** v : {&S.cz, &S.cp, &S.cq, &S.cax}) *v = A.alloc<double>(K * n3p);
   S.cpv = A.alloc<double>(K * n3);
-  cuda_check(cudaMemset(S.cpv, 0, K * n3 * sizeof(double)), "zero pv");  // fixed vertices stay 0
+  cuda_zero(S.cpv, K * n3 * sizeof(double), "zero pv");  // fixed vertices stay 0
   const size_t pst = hdk_cpcg_partial_stride(n);
   S.cpart = A.alloc<double>(pst * K);
   S.cst = A.alloc<hdk_pcg>(K);
   S.ctickets = A.alloc<unsigned int>(K);
-  cuda_check(cudaMemset(S.ctickets, 0, sizeof(unsigned int) * K), "zero tickets");
+  cuda_zero(S.ctickets, sizeof(unsigned int) * K, "zero tickets");
   cuda_check(cudaMallocHost(&S.h_cst, sizeof(hdk_pcg) * K), "pinned pcg");
   void* s = st_;
   const int cstride = static_cast<int>(sizeof(hdk_pcg) / sizeof(int));
@@ -397,6 +418,25 @@ bool Engine::solve_columns_pcg(const ContactFrame& c, int r0, int& iterations) {
     hdk_ok(hdk_contact_column_init(&c.view, row, nv, df_.v2p, S.col[j].seed, S.col[j].x, st_), "column init");
   }
   kernel_launches += K;
+  // profiling: per-chunk ring timestamps of this batch's multi-column passes
+  // (HETERODYN_CHUNK_TRACE=path: the last traced batch is written at exit)
+  static const char* trace_path = std::getenv("HETERODYN_CHUNK_TRACE");
+  if (trace_path && !S.trace) {
+    cuda_check(cudaMalloc(&S.trace, 4 * sizeof(long long) * df_.n_chunks), "chunk trace");
+    cuda_check(cudaMallocHost(&S.h_trace_ptr, 2 * sizeof(long long*)), "chunk trace");
+    S.h_trace_ptr[0] = S.trace;
+    S.h_trace_ptr[1] = nullptr;
+    S.trace_path = trace_path;
+    S.trace_grid = df_.grid2;
+    S.h_first2.resize(df_.grid2 + 1);
+    cuda_check(cudaMemcpy(S.h_first2.data(), df_.first2, sizeof(int) * (df_.grid2 + 1), cudaMemcpyDeviceToHost),
+               "first2");
+    S.trace_chunks = df_.n_chunks;
+  }
+  if (S.trace) {
+    cuda_check(cudaMemsetAsync(S.trace, 0, 4 * sizeof(long long) * df_.n_chunks, st_), "chunk trace");
+    hdk_ok(hdk_set_chunk_trace(S.h_trace_ptr, st_), "chunk trace");
+  }
   if (ph_.on) cuda_check(cudaEventRecord(ph_.ev[6], st_), "phase event");
   LoopGraph& g = S.pgraph;
   if (g.exec) {
@@ -410,6 +450,7 @@ bool Engine::solve_columns_pcg(const ContactFrame& c, int r0, int& iterations) {
       cuda_check(cudaGraphLaunch(g.body, st_), "columns (CG)");
     }
   }
+  if (S.trace) hdk_ok(hdk_set_chunk_trace(S.h_trace_ptr + 1, st_), "chunk trace off");
   cuda_check(cudaMemcpyAsync(S.h_cst, S.cst, sizeof(hdk_pcg) * K, cudaMemcpyDeviceToHost, st_), "pcg state");
   cuda_check(cudaStreamSynchronize(st_), "columns (CG) sync");
   const int real = std::min(K, c.k - r0);

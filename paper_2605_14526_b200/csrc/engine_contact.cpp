@@ -21,6 +21,7 @@
 // backbone per contact row (engine_columns.cpp), the reduced multiplier
 // system (LDL^T on the device) and the friction pushback.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 
@@ -52,7 +53,7 @@ void ContactFrame::allocate(int cap_c, int cap_k, int cap_u, int n) {
   base = nullptr;
   bytes = hdk_contact_block_bytes(cap_c, cap_k, cap_u, n);
   cuda_check(cudaMalloc(&base, bytes), "contact block");
-  cuda_check(cudaMemset(base, 0, bytes), "contact block");
+  cuda_zero(base, bytes, "contact block");
   hdk_contact_block_layout(base, cap_c, cap_k, cap_u, n, &view);
 }
 
@@ -147,7 +148,11 @@ void Engine::build_contact_graph() {
 // One forward step of a scene with obstacles; false when the contact set
 // overflowed the capacities (grown here; the caller re-runs the step).
 bool Engine::run_contact_step() {
-  if (!cw_.base) ensure_contact_capacity(32, 96, 32);
+  // first capacity: 128 contacts and a 224-row system (the shared-memory
+  // factorization's limit), so a growing contact set (C4 reaches ~70 contacts,
+  // 200 rows in five steps) does not re-capture the forward graph and re-run
+  // steps mid-trajectory
+  if (!cw_.base) ensure_contact_capacity(std::min(64, scene_.mesh.nv), hdk_contact_smem_rows() / 2, 64);
   if (cgraph_.exec) {
     cuda_check(cudaGraphLaunch(cgraph_.exec, st_), "contact forward graph");
   } else {
@@ -270,6 +275,15 @@ void Engine::backward_frame(int t, GradOut& out) {
   out.adjoint_iterations += iters;
   sync_ctl();
   phase_collect(3, 6);
+  if (ph_.per_frame) {
+    float pre = 0.f, loop = 0.f, post = 0.f;
+    cudaEventElapsedTime(&pre, ph_.ev[3], ph_.ev[4]);
+    cudaEventElapsedTime(&loop, ph_.ev[4], ph_.ev[5]);
+    cudaEventElapsedTime(&post, ph_.ev[5], ph_.ev[6]);
+    std::fprintf(stderr, "[frame %d] pre %.3f backbone %.3f post %.3f ms (columns %.3f ms), K %d, iterations %d\n", t,
+                 pre, loop, post, ph_.col_ms - ph_.last_col_ms, c ? c->k : 0, iters);
+    ph_.last_col_ms = ph_.col_ms;
+  }
   check_ctl("backward step");
 }
 

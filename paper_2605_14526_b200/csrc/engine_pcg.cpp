@@ -23,10 +23,10 @@ void Engine::build_pcg_graph() {
     pcg_ = A.alloc<hdk_pcg>(segs_);
     pcg_part_ = A.alloc<double>(segs_ > 1 ? static_cast<size_t>(HDK_SEG_PSTRIDE) * segs_ : 4 * HDK_RED_BLOCKS);
     pcg_ticket_ = A.alloc<unsigned int>(segs_);
-    cuda_check(cudaMemset(pcg_ticket_, 0, sizeof(unsigned int) * segs_), "zero ticket");
+    cuda_zero(pcg_ticket_, sizeof(unsigned int) * segs_, "zero ticket");
     for (double** v : {&pr_, &pz_, &pp_, &pq_, &pap_, &prp_}) *v = A.alloc<double>(n3p);
     ppv_ = A.alloc<double>(n3);
-    cuda_check(cudaMemset(ppv_, 0, n3 * sizeof(double)), "zero pv");  // fixed vertices stay 0
+    cuda_zero(ppv_, n3 * sizeof(double), "zero pv");  // fixed vertices stay 0
     cuda_check(cudaMallocHost(&h_pcg_, sizeof(hdk_pcg) * segs_), "pinned pcg");
   }
   if (!pgraph_) pgraph_ = std::make_unique<LoopGraph>();

@@ -41,7 +41,7 @@ namespace hdb {
 
 namespace {
 constexpr int HDK_VALS = 3072;  // == HDK_CHUNK_VALS (include/hdk.h)
-constexpr int HDK_SEGS = 256;   // == HDK_CHUNK_SEGS
+constexpr int HDK_SEGS = 64;    // == HDK_CHUNK_SEGS
 
 int hw_threads() {
   int n = static_cast<int>(std::thread::hardware_concurrency());

@@ -110,6 +110,14 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarps) : "memory"); }
 
+// Per-chunk ring trace of the multi-column passes (profiling; set by
+// hdk_set_chunk_trace, null otherwise): for chunk c, [4c] the producer's
+// clock when it could issue (before its empty wait), [4c + 1] when it
+// issued, [4c + 2] when the consumers saw it land, [4c + 3] when its last
+// worker finished (SM-local clock64).
+__device__ long long* g_chunk_trace = nullptr;
+__device__ __forceinline__ long long sm_clock() { return clock64(); }
+
 // Per-CTA timing trace, compiled only into microbenchmarks that define
 // HDK_SOLVE_TRACE: [2 b] = start, [2 b + 1] = end (globaltimer, ns) of CTA b.
 #ifdef HDK_SOLVE_TRACE
@@ -256,7 +264,13 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
     const int st = k % S;
     const hdk_chunk ch = nxt;
     if (k + 1 < n) nxt = f.chunk[chunk_at(k + 1)];  // descriptor prefetch, off the critical path
+    long long* tr = g_chunk_trace;
+    const long long t_ready = tr ? sm_clock() : 0;
     if (k >= S) mbar_wait(&r.empty[st], ((k / S) - 1) & 1);
+    if (tr && k >= S) {  // (the prefilled chunks are not traced: they are issued before the run flag is read)
+      tr[4 * (size_t)chunk_at(k)] = t_ready;
+      tr[4 * (size_t)chunk_at(k) + 1] = sm_clock();
+    }
     fence_proxy_async();
     r.info[st] = ChunkInfo{ch.nseg, ch.tile, ch.seg0, 0};
     const uint32_t vb = static_cast<uint32_t>(ch.len) * 8u, sb = static_cast<uint32_t>(ch.nseg) * 16u;
@@ -624,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rowdot_c2(hdk_factor f, const d
 constexpr int kWarpsMma = 16;
 template <int R>
 struct MmaPass1Smem {
-  static constexpr int S = R >= 8 ? 5 : 6;  // ring depth (the B tile grows with R)
+  static constexpr int S = 6;  // ring depth (229.6 KB with the R = 8 B tile)
   // row pitch 8 NB + 4: the 16 lanes of a half-warp (4 t x 4 g) hit 16 distinct 8-byte banks
   static constexpr int NQ = 3 * R, NB = (NQ + 7) / 8, LD = 8 * NB + 4;
   Ring<S> ring;
@@ -664,6 +678,11 @@ __global__ void __launch_bounds__(32 * (kWarpsMma + 1), 1) k_rowdot_mma(hdk_fact
   for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
     const int st = k % S;
     mbar_wait(&ring.full[st], (k / S) & 1);
+    long long* tr = g_chunk_trace;
+    if (tr && warp == 0 && lane == 0) {
+      tr[4 * (size_t)c + 2] = sm_clock();
+      tr[4 * (size_t)c + 3] = ((ring.info[st].nseg + 7) >> 3);  // groups
+    }
     const ChunkInfo ch = ring.info[st];
     if (ch.tile != tile) {  // every consumer warp reaches the new tile at this chunk
       mma_consumers_sync();
@@ -739,6 +758,108 @@ __global__ void __launch_bounds__(32 * (kWarpsMma + 1), 1) k_rowdot_mma(hdk_fact
   }
 }
 
+// The same pass with the work of a staged chunk split finer: an item is one
+// group of eight segments x one n-block of eight right-hand sides, so a chunk
+// of g groups gives g NB items for the consumer warps (not g).  A stage is
+// released only when every consumer warp has finished it, so with ~2 groups
+// per chunk the group-per-warp form kept most warps waiting behind the few
+// long groups; here each warp's share of a chunk is a third as long and the
+// ring turns over faster.  Each item runs kAccN independent DMMA chains.
+template <int R>
+__global__ void __launch_bounds__(32 * (kWarpsMma + 1), 1) k_rowdot_mma_nb(hdk_factor f, const double* __restrict__ rhs) {
+  using Sm = MmaPass1Smem<R>;
+  constexpr int NQ = Sm::NQ, NB = Sm::NB, LD = Sm::LD, S = Sm::S, W = kWarpsMma;
+  constexpr int kAccN = 4;
+  hdk::pdl_trigger();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
+  Ring<S>& ring = sm.ring;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  ring_init(ring, W);
+  const int c_beg = f.first1 ? f.first1[blockIdx.x] : range_first(blockIdx.x, gridDim.x, f.n_chunks);
+  const int c_end = f.first1 ? f.first1[blockIdx.x + 1] : range_first(blockIdx.x + 1LL, gridDim.x, f.n_chunks);
+  if (warp == W) {
+    produce(f, ring, c_beg, c_end, false);
+    return;
+  }
+  HDK_TRACED_WAIT(hdk::kTrRowdot);
+  if (f.run_flag && *f.run_flag == 0) return;
+  const int g = lane >> 2, t = lane & 3;
+  const size_t ps = 3 * (size_t)f.n_pslot;
+  int tile = -1;
+  for (int c = c_beg, k = 0; c < c_end; ++c, ++k) {
+    const int st = k % S;
+    mbar_wait(&ring.full[st], (k / S) & 1);
+    const ChunkInfo ch = ring.info[st];
+    if (ch.tile != tile) {  // every consumer warp reaches the new tile at this chunk
+      mma_consumers_sync();
+      tile = ch.tile;
+      for (int e = threadIdx.x; e < kW * 8 * NB; e += 32 * W) {
+        const int col = e / (8 * NB), q = e - col * (8 * NB);
+        const int gc = tile * kW + col;
+        double v = 0.0;
+        if (q < NQ && gc < f.n) v = __ldg(rhs + (size_t)(q / 3) * 3 * (size_t)f.n + 3 * (size_t)gc + (q % 3));
+        sm.bt[col * LD + q] = v;
+      }
+      mma_consumers_sync();
+    }
+    const double* vals = ring.vals[st];
+    const int items = ((ch.nseg + 7) >> 3) * NB;
+    for (int it = (warp - (ch.seg0 >> 3) * NB) & (W - 1); it < items; it += W) {
+      const int grp = it / NB, nb = it - grp * NB;
+      const int i = 8 * grp + g;
+      const bool live = i < ch.nseg;
+      const hdk_seg sg = ring.segs[st][live ? i : 0];
+      const int lo = live ? (sg.clo_len & 0xffff) : kW;
+      const int hi = live ? lo + (sg.clo_len >> 16) : 0;
+      int ulo = lo, uhi = hi;
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        ulo = min(ulo, __shfl_xor_sync(0xffffffffu, ulo, o));
+        uhi = max(uhi, __shfl_xor_sync(0xffffffffu, uhi, o));
+      }
+      const double* v = vals + sg.coff - lo;
+      const double* bcol = sm.bt + 8 * nb + g;
+      double d[kAccN][2];
+#pragma unroll
+      for (int u = 0; u < kAccN; ++u) d[u][0] = d[u][1] = 0.0;
+      int kc = ulo & ~3;
+      for (; kc + 4 * (kAccN - 1) < uhi; kc += 4 * kAccN) {
+        double a[kAccN], b[kAccN];
+#pragma unroll
+        for (int u = 0; u < kAccN; ++u) {
+          const int col = kc + 4 * u + t;
+          a[u] = (col >= lo && col < hi) ? v[col] : 0.0;
+          b[u] = bcol[col * LD];
+        }
+#pragma unroll
+        for (int u = 0; u < kAccN; ++u) dmma_m8n8k4(d[u], a[u], b[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kAccN - 1; ++u) {  // remainder: at most kAccN - 1 k-steps (warp-uniform bound)
+        if (kc + 4 * u >= uhi) break;
+        const int col = kc + 4 * u + t;
+        const double a = (col >= lo && col < hi) ? v[col] : 0.0;
+        dmma_m8n8k4(d[u], a, bcol[col * LD]);
+      }
+      if (live) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int q = 8 * nb + 2 * t + j;
+          if (q < NQ) {
+            double sum = d[0][j];
+#pragma unroll
+            for (int u = 1; u < kAccN; ++u) sum = sum + d[u][j];  // fixed order
+            f.part1[(size_t)(q / 3) * ps + 3 * (size_t)sg.pslot + (q % 3)] = sum;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[st]);
+  }
+}
+
 // z-fold: one warp per task.  (Folding z in the row-dot kernel's epilogue
 // behind a grid barrier measured 1-2 us slower than this separate launch.)
 __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
@@ -754,7 +875,7 @@ __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
 // with each chunk; 227 KB of shared memory per CTA).
 template <int R>
 struct Stages2 {
-  static constexpr int value = R == 1 ? kStages2 : R == 2 ? 4 : R == 4 ? 3 : 2;
+  static constexpr int value = R == 1 ? kStages2 : R == 2 ? 6 : R == 4 ? 6 : 5;
 };
 
 template <int R>
@@ -1167,6 +1288,12 @@ const Grids& grids() {
                          static_cast<int>(sizeof(MmaPass1Smem<4>)));
     cudaFuncSetAttribute(k_rowdot_mma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(MmaPass1Smem<8>)));
+    cudaFuncSetAttribute(k_rowdot_mma_nb<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(MmaPass1Smem<2>)));
+    cudaFuncSetAttribute(k_rowdot_mma_nb<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(MmaPass1Smem<4>)));
+    cudaFuncSetAttribute(k_rowdot_mma_nb<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(MmaPass1Smem<8>)));
     cudaFuncSetAttribute(k_coltile_c2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(Pass2Smem<8>)));
     cudaFuncSetAttribute(k_rowdot_c2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc2);
@@ -1219,7 +1346,9 @@ int launch_multi(const hdk_factor* f, const double* rhs, cudaStream_t st) {
     const char* c = std::getenv("HETERODYN_ROWDOT_C2");
     return (c && c[0] == '0') ? 0 : 2;
   }();
-  if (mode1 == 2)
+  if (mode1 == 3)
+    hdk::launch(k_rowdot_mma_nb<R>, dim3(g2), dim3(32 * (kWarpsMma + 1)), sizeof(MmaPass1Smem<R>), st, f1, rhs);
+  else if (mode1 == 2)
     hdk::launch(k_rowdot_mma<R>, dim3(g2), dim3(32 * (kWarpsMma + 1)), sizeof(MmaPass1Smem<R>), st, f1, rhs);
   else if (mode1 == 1) hdk::launch(k_rowdot_c2<R>, dim3(g2), dim3(kThreads), sizeof(Ring<kStagesC2>), st, f1, rhs);
   else hdk::launch(k_rowdot<false, R, 16>, dim3(g2), dim3(Pass1<16>::threads), sizeof(Ring<Pass1<16>::stages>), st, f1, rhs);
@@ -1297,6 +1426,11 @@ HDK_API int hdk_apply_inverse3_multi(const hdk_factor* f, const double* rhs_perm
 }
 
 HDK_API size_t hdk_factor_part2_stride(const hdk_factor* f) { return part2_stride(*f); }
+
+HDK_API int hdk_set_chunk_trace(long long* const* trace, void* stream) {  // trace: pinned host cell
+  return static_cast<int>(cudaMemcpyToSymbolAsync(g_chunk_trace, trace, sizeof(long long*), 0,
+                                                  cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)));
+}
 
 HDK_API int hdk_apply_inverse3_perm(const hdk_factor* f, const double* rhs_perm, double* out_perm, void* stream) {
   return launch(f, rhs_perm, out_perm, false, static_cast<cudaStream_t>(stream));
