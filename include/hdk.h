@@ -588,6 +588,8 @@ HDK_API size_t hdk_cpcg_partial_stride(int n);
 /* Profiling: per-chunk ring timestamps of the multi-column passes (4 int64 per
  * chunk, solve.cu g_chunk_trace); NULL turns the trace off. */
 HDK_API int hdk_set_chunk_trace(long long* const* trace, void* stream);
+/* Profiling: (alpha, beta) of each column's CG, [column][512][2] doubles. */
+HDK_API int hdk_set_cpcg_trace(double* const* trace, void* stream);
 HDK_API int hdk_cpcg_apply(const hdk_vtx* x, const hdk_csr* a, int columns, const double* ef_sorted,
                            size_t ef_stride, const double* p, double* q, double* partial, size_t pstride,
                            unsigned int* tickets, hdk_pcg* st, void* stream);

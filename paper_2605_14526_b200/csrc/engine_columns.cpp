@@ -55,12 +55,25 @@ struct Engine::ColumnSet {
   hdk_pcg* h_cst = nullptr;
   unsigned int* ctickets = nullptr;
   LoopGraph pgraph;
+  double* cg_trace = nullptr;  // profiling (HETERODYN_CG_TRACE)
+  double** h_cg_trace_ptr = nullptr;
+  const char* cg_trace_path = nullptr;
   long long* trace = nullptr;  // profiling (HETERODYN_CHUNK_TRACE)
   long long** h_trace_ptr = nullptr;
   const char* trace_path = nullptr;
   int trace_grid = 0, trace_chunks = 0;
   std::vector<int> h_first2;
   ~ColumnSet() {
+    if (cg_trace) {
+      std::vector<double> h(static_cast<size_t>(kColumns) * 512 * 2);
+      if (cudaMemcpy(h.data(), cg_trace, h.size() * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess)
+        if (FILE* fp = std::fopen(cg_trace_path, "wb")) {
+          std::fwrite(h.data(), sizeof(double), h.size(), fp);
+          std::fclose(fp);
+        }
+      cudaFree(cg_trace);
+      cudaFreeHost(h_cg_trace_ptr);
+    }
     if (trace) {
       std::vector<long long> h(4 * static_cast<size_t>(trace_chunks));
       if (cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess) {
@@ -432,6 +445,18 @@ bool Engine::solve_columns_pcg(const ContactFrame& c, int r0, int& iterations) {
     cuda_check(cudaMemcpy(S.h_first2.data(), df_.first2, sizeof(int) * (df_.grid2 + 1), cudaMemcpyDeviceToHost),
                "first2");
     S.trace_chunks = df_.n_chunks;
+  }
+  static const char* cg_trace_path = std::getenv("HETERODYN_CG_TRACE");
+  if (cg_trace_path && !S.cg_trace) {
+    cuda_check(cudaMalloc(&S.cg_trace, sizeof(double) * K * 512 * 2), "cg trace");
+    cuda_check(cudaMallocHost(&S.h_cg_trace_ptr, 2 * sizeof(double*)), "cg trace");
+    S.h_cg_trace_ptr[0] = S.cg_trace;
+    S.h_cg_trace_ptr[1] = nullptr;
+    S.cg_trace_path = cg_trace_path;
+  }
+  if (S.cg_trace) {
+    cuda_check(cudaMemsetAsync(S.cg_trace, 0, sizeof(double) * K * 512 * 2, st_), "cg trace");
+    hdk_ok(hdk_set_cpcg_trace(S.h_cg_trace_ptr, st_), "cg trace");
   }
   if (S.trace) {
     cuda_check(cudaMemsetAsync(S.trace, 0, 4 * sizeof(long long) * df_.n_chunks, st_), "chunk trace");

@@ -394,8 +394,9 @@ __global__ void __launch_bounds__(128) k_bapply_cols_fused(hdk_mesh m, const dou
   for (int i = 0; i < 30; ++i) d[i] = __ldg(dcomp + i * n + ee);
   hdk::pdl_wait();
   if (!live) return;
+  const int c0 = K * blockIdx.y;  // column group of this block row
 #pragma unroll 1
-  for (int c = 0; c < K; ++c) {
+  for (int c = c0; c < c0 + K; ++c) {
     if (cond0[(size_t)c * cond_stride] == 0) continue;
     const M3 pm = bforce(g, d, x + c * x_stride);
     write_force_sorted(g, pm, ef + c * ef_stride, corner_pos, e);
@@ -568,9 +569,21 @@ HDK_API int hdk_bapply_cols_sorted(const hdk_mesh* m, const double* dcomp, const
     const char* e = std::getenv("HETERODYN_BCOLS");  // "0": one column per blockIdx.y (A/B)
     return !(e && e[0] == '0');
   }();
+  static const int per_thread = [] {  // columns per thread (HETERODYN_BCOLS_K: 8, 4 or 2)
+    const char* e = std::getenv("HETERODYN_BCOLS_K");
+    return e ? std::atoi(e) : 8;
+  }();
   if (fused && columns == 8) {
-    hdk::launch(k_bapply_cols_fused<8>, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m,
-                dcomp, x, x_stride, ef, ef_stride, corner_pos, cond0, cond_stride);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (per_thread == 4)
+      hdk::launch(k_bapply_cols_fused<4>, dim3(blocks(m->ne, 128), 2), dim3(128), 0, st, *m, dcomp, x, x_stride, ef,
+                  ef_stride, corner_pos, cond0, cond_stride);
+    else if (per_thread == 2)
+      hdk::launch(k_bapply_cols_fused<2>, dim3(blocks(m->ne, 128), 4), dim3(128), 0, st, *m, dcomp, x, x_stride, ef,
+                  ef_stride, corner_pos, cond0, cond_stride);
+    else
+      hdk::launch(k_bapply_cols_fused<8>, dim3(blocks(m->ne, 128)), dim3(128), 0, st, *m, dcomp, x, x_stride, ef,
+                  ef_stride, corner_pos, cond0, cond_stride);
     return static_cast<int>(cudaGetLastError());
   }
   hdk::launch(k_bapply_cols_sorted, dim3(blocks(m->ne, 128), columns), dim3(128), 0, static_cast<cudaStream_t>(stream),

@@ -709,6 +709,11 @@ __global__ void __launch_bounds__(kT) k_cpcg_apply(hdk_vtx x, hdk_csr A, int n3,
   }
 }
 
+// Profiling: per-column CG coefficients (alpha_k, beta_k) of the columns' CG
+// (the Lanczos matrix of A^{-1}(A - B), HETERODYN_CG_TRACE); null = off.
+__device__ double* g_cpcg_trace = nullptr;
+constexpr int kCgTraceIters = 512;
+
 // z = A^{-1} r folded per column from the multi-column solve's tile partials
 // (the fold of hdk_bb_dots), then r.z, the stopping test and beta.  One
 // element per thread.
@@ -751,6 +756,10 @@ __global__ void __launch_bounds__(kT) k_cpcg_rz(hdk_factor f, size_t part2_strid
   st->iter = it;
   const bool done = sqrt(zz) <= st->tol * fmax(sqrt(tt), 1e-30);
   st->beta = st->rz > 0.0 && it > 1 ? rz / st->rz : 0.0;
+  if (double* tr = g_cpcg_trace; tr && it > 1 && it - 2 < kCgTraceIters) {
+    tr[2 * ((size_t)c * kCgTraceIters + it - 2)] = st->alpha;
+    tr[2 * ((size_t)c * kCgTraceIters + it - 2) + 1] = st->beta;
+  }
   st->rz = rz;
   st->done = done ? 1 : 0;
   if (!done && it >= st->k_max) st->err = 10;
@@ -806,6 +815,10 @@ HDK_API int hdk_cpcg_spmv(const hdk_csr* a, int columns, const double* p, double
                           void* stream) {
   hdk::launch(k_cpcg_spmv, dim3(nb(a->rows), columns), dim3(256), 0, S(stream), *a, 3 * a->rows, p, y, st);
   return last();
+}
+HDK_API int hdk_set_cpcg_trace(double* const* trace, void* stream) {  // trace: pinned host cell
+  return static_cast<int>(cudaMemcpyToSymbolAsync(g_cpcg_trace, trace, sizeof(double*), 0, cudaMemcpyHostToDevice,
+                                                  static_cast<cudaStream_t>(stream)));
 }
 HDK_API size_t hdk_cpcg_partial_stride(int n) {
   const size_t apply_blocks = (static_cast<size_t>(n) + kT / 8 - 1) / (kT / 8);

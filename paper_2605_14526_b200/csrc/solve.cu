@@ -1353,12 +1353,15 @@ int launch_multi(const hdk_factor* f, const double* rhs, cudaStream_t st) {
   else if (mode1 == 1) hdk::launch(k_rowdot_c2<R>, dim3(g2), dim3(kThreads), sizeof(Ring<kStagesC2>), st, f1, rhs);
   else hdk::launch(k_rowdot<false, R, 16>, dim3(g2), dim3(Pass1<16>::threads), sizeof(Ring<Pass1<16>::stages>), st, f1, rhs);
   hdk::launch(k_zreduce, dim3((f->n_ztask + 7) / 8, R), dim3(256), 0, st, *f);
-  static const int mode2 = [] {  // pass 2: 1 = two columns per warp (default), 2 = FP64 tensor cores, 0 = one
+  // pass 2: 2 = FP64 tensor cores (default at R = 8: 67.8 vs 85.9 us at C4),
+  // 1 = two columns per warp (default at R <= 4: 50.8 vs 59.5 us), 0 = one
+  static const int mode2_env = [] {
     const char* e = std::getenv("HETERODYN_COLTILE");
     if (e) return std::atoi(e);
     const char* c = std::getenv("HETERODYN_COLTILE_C2");
-    return (c && c[0] == '0') ? 0 : 1;
+    return (c && c[0] == '0') ? 0 : -1;
   }();
+  const int mode2 = mode2_env >= 0 ? mode2_env : (R >= 8 ? 2 : 1);
   if (mode2 == 2)
     hdk::launch(k_coltile_mma<R>, dim3(g2), dim3(32 * (kWarpsMma2 + 2)), sizeof(MmaPass2Smem<R>), st, *f);
   else if (mode2 == 1) hdk::launch(k_coltile_c2<R>, dim3(g2), dim3(kThreads2), sizeof(Pass2Smem<R>), st, *f);
