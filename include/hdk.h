@@ -582,6 +582,28 @@ HDK_API int hdk_spcg_p(int n3s, int n3, const double* z, double* p, double* pv, 
  * partials. */
 HDK_API int hdk_cpcg_spmv(const hdk_csr* a, int columns, const double* p, double* y, const hdk_pcg* st,
                           void* stream);
+/* Block CG over a batch of m <= 8 contact-adjoint columns (pcg.cu): one
+ * block Krylov space for the batch's right-hand sides (O'Leary's block PCG:
+ * alpha = (P^T Q)^{-1} (Z^T R), beta = (Z^T R)_old^{-1} (Z^T R)), the
+ * columns' vectors as for hdk_cpcg_*.  err = -1: a Gram matrix lost
+ * definiteness (the caller solves the batch column by column). */
+typedef struct hdk_bcg {
+  double rz[64], rz_old[64], g[64], alpha[64], beta[64];
+  double tol;
+  int m, iter, k_max, err, cond, done;
+} hdk_bcg;
+HDK_API size_t hdk_bcg_partial_doubles(int n);
+HDK_API int hdk_bcg_init(hdk_bcg* st, const int* m, double tol, int k_max, int* any, hdk_pcg* cst, int cst_count,
+                         void* stream);
+HDK_API int hdk_bcg_gram_pq(int n3, const double* p, const double* q, double* partial, unsigned int* ticket,
+                            hdk_bcg* st, void* stream);
+HDK_API int hdk_bcg_xr(int n3, double* x, double* r, const double* p, const double* q, const hdk_bcg* st,
+                       void* stream);
+HDK_API int hdk_bcg_zfold(const hdk_factor* f, const double* r, double* z, const double* x, double* partial,
+                          unsigned int* ticket, hdk_bcg* st, void* stream);
+HDK_API int hdk_bcg_p(int n, int nv, const double* z, double* p, double* pv, const int* p2v, hdk_bcg* st, int* any,
+                      unsigned long long cond_handle, void* stream);
+
 /* Per-column partials of hdk_cpcg_apply / hdk_cpcg_rz: column c's at
  * partial + c pstride, pstride = hdk_cpcg_partial_stride(n) doubles. */
 HDK_API size_t hdk_cpcg_partial_stride(int n);
@@ -593,6 +615,9 @@ HDK_API int hdk_set_cpcg_trace(double* const* trace, void* stream);
 HDK_API int hdk_cpcg_apply(const hdk_vtx* x, const hdk_csr* a, int columns, const double* ef_sorted,
                            size_t ef_stride, const double* p, double* q, double* partial, size_t pstride,
                            unsigned int* tickets, hdk_pcg* st, void* stream);
+/* q only (no p.q / alpha): the block CG's Gram matrices are formed separately. */
+HDK_API int hdk_cpcg_apply_q(const hdk_vtx* x, const hdk_csr* a, int columns, const double* ef_sorted,
+                             size_t ef_stride, const double* p, double* q, hdk_pcg* st, void* stream);
 HDK_API int hdk_cpcg_rz(const hdk_factor* f, int columns, const double* r, double* z, const double* x,
                         double* partial, size_t pstride, unsigned int* tickets, hdk_pcg* st, void* stream);
 HDK_API int hdk_cpcg_p(int n, int nv, int columns, const double* z, double* p, double* pv, const int* p2v,

@@ -283,7 +283,8 @@ Engine::~Engine() {
       std::fprintf(stderr, "  contact columns: %lld batches of %d, %.3f ms total, %lld batched iterations "
                    "(%.1f us each), %lld column iterations\n", ph_.col_batches, kColumns, ph_.col_ms,
                    ph_.col_iters, 1e3 * ph_.col_ms / std::max(1LL, ph_.col_iters), ph_.col_real_iters);
-    std::fprintf(stderr, "  CG backbone fallbacks to Anderson (p.q <= 0): %lld\n", pcg_fallbacks);
+    std::fprintf(stderr, "  CG backbone fallbacks to Anderson (p.q <= 0): %lld; block-CG batches solved column by column: %lld\n",
+                 pcg_fallbacks, bcg_fallbacks);
   }
   for (cudaEvent_t e : ph_.ev)
     if (e) cudaEventDestroy(e);

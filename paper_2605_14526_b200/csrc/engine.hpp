@@ -207,6 +207,10 @@ class Engine {
   // when a column's p.q <= 0 (the caller runs the Anderson columns).
   bool solve_columns_pcg(const ContactFrame& c, int r0, int& iterations);
   void build_columns_pcg();
+  // The same rows by block CG over the batch (the default; a batch of one row
+  // and a lost-definiteness / cap failure go to solve_columns_pcg).
+  bool solve_columns_bcg(const ContactFrame& c, int r0, int& iterations);
+  void build_columns_bcg();
   // All K columns of contact frame c through the kColumns slots, a finished
   // slot refilled with the next row (the loop exits when a column finishes);
   // returns the columns' iterations.  Opt-in (HETERODYN_COLUMN_REFILL=1): the
@@ -286,7 +290,7 @@ class Engine {
   double *pcg_part_ = nullptr, *pr_ = nullptr, *pz_ = nullptr, *pp_ = nullptr, *pq_ = nullptr, *pap_ = nullptr,
          *prp_ = nullptr, *ppv_ = nullptr;
   unsigned int* pcg_ticket_ = nullptr;
-  long long pcg_fallbacks = 0;
+  long long pcg_fallbacks = 0, bcg_fallbacks = 0;
   void build_pcg_graph();
   void build_pcg_graph_seg();
   bool run_pcg(int& iterations);  // false: fall back to the Anderson backbone

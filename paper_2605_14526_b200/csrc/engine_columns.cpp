@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <string>
 #include <vector>
 
 namespace hdb {
@@ -55,6 +56,14 @@ struct Engine::ColumnSet {
   hdk_pcg* h_cst = nullptr;
   unsigned int* ctickets = nullptr;
   LoopGraph pgraph;
+  // block CG (default): the batch's columns in one block Krylov space
+  hdk_bcg* bst = nullptr;
+  hdk_bcg* h_bst = nullptr;
+  int* bm = nullptr;
+  int* h_bm = nullptr;
+  double* bpart = nullptr;
+  unsigned int* bticket = nullptr;
+  LoopGraph bgraph;
   double* cg_trace = nullptr;  // profiling (HETERODYN_CG_TRACE)
   double** h_cg_trace_ptr = nullptr;
   const char* cg_trace_path = nullptr;
@@ -89,6 +98,9 @@ struct Engine::ColumnSet {
     }
     pgraph.destroy();
     pgraph.destroy();
+    bgraph.destroy();
+    if (h_bst) cudaFreeHost(h_bst);
+    if (h_bm) cudaFreeHost(h_bm);
     if (h_cst) cudaFreeHost(h_cst);
     graph.destroy();
     rgraph.destroy();
@@ -421,6 +433,107 @@ void Engine::build_columns_pcg() {
   build_loop_graph(st_, use_cond_, pre, body, [] {}, S.pgraph);
 }
 
+// The batch's columns by block CG (pcg.cu hdk_bcg_*): B p and q = (A - B) p
+// per column as in the column CG, then the block's Gram matrices, X / R,
+// the multi-column solve, Z^T R with the per-column stopping tests, P.
+void Engine::build_columns_bcg() {
+  ColumnSet& S = *cols_;
+  if (!S.cst) build_columns_pcg();
+  DevArena& A = *S.mem;
+  const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), n3p = 3 * static_cast<size_t>(hf_.n),
+               ne = scene_.mesh.ne;
+  const int n = hf_.n, nv = scene_.mesh.nv, K = kColumns;
+  S.bst = A.alloc<hdk_bcg>(1);
+  S.bm = A.alloc<int>(1);
+  S.bpart = A.alloc<double>(hdk_bcg_partial_doubles(n));
+  S.bticket = A.alloc<unsigned int>(1);
+  cuda_check(cudaMallocHost(&S.h_bst, sizeof(hdk_bcg)), "pinned bcg");
+  cuda_check(cudaMallocHost(&S.h_bm, sizeof(int)), "pinned bcg");
+  void* s = st_;
+  auto pre = [&] {
+    hdk_ok(hdk_bcg_init(S.bst, S.bm, 1e-10, 500, S.any, S.cst, K, s), "block CG init");
+    for (int c = 0; c < K; ++c) {
+      ColumnSet::Col& C = S.col[c];
+      hdk_ok(hdk_gather_perm(&dv_, C.seed, nullptr, C.seedp, s), "seed in elimination order");
+      hdk_ok(hdk_gather_perm(&dv_, C.x, nullptr, C.xp, s), "x0 in elimination order");
+      hdk_ok(hdk_bapply(&dm_, dcomp_, C.x, C.ef, s), "B x0");
+      hdk_ok(hdk_gather_pp(&dv_, nullptr, C.ef, C.rx, nullptr, s), "R(x0)");
+    }
+    hdk_ok(hdk_cpcg_spmv(&a_ff_, K, S.xp_all, S.cax, S.cst, s), "A x0");
+    hdk_ok(hdk_pcg_r0(static_cast<int>(K * n3p), S.seedp_all, S.cax, S.rx_all, S.rhs, s), "r0");
+    hdk_ok(hdk_apply_inverse3_multi(&S.f, S.rhs, K, s), "Z0 = A^-1 R0");
+    hdk_ok(hdk_bcg_zfold(&S.f, S.rhs, S.cz, S.xp_all, S.bpart, S.bticket, S.bst, s), "Z^T R");
+    hdk_ok(hdk_bcg_p(n, nv, S.cz, S.cp, S.cpv, df_.p2v, S.bst, S.any, 0ULL, s), "P");
+  };
+  const int cstride = static_cast<int>(sizeof(hdk_pcg) / sizeof(int));
+  auto body = [&](unsigned long long handle) {
+    hdk_ok(hdk_bapply_cols_sorted(&dm_, dcomp_, S.cpv, n3, S.ef_all, 12 * ne, corner_pos_, &S.cst->cond, cstride, K,
+                                  s),
+           "B P (block)");
+    hdk_ok(hdk_cpcg_apply_q(&dv_, &a_ff_, K, S.ef_all, 12 * ne, S.cp, S.cq, S.cst, s), "Q = (A - B) P");
+    hdk_ok(hdk_bcg_gram_pq(static_cast<int>(n3p), S.cp, S.cq, S.bpart, S.bticket, S.bst, s), "P^T Q, alpha");
+    hdk_ok(hdk_bcg_xr(static_cast<int>(n3p), S.xp_all, S.rhs, S.cp, S.cq, S.bst, s), "X, R");
+    hdk_ok(hdk_apply_inverse3_multi(&S.f, S.rhs, K, s), "Z = A^-1 R (block)");
+    hdk_ok(hdk_bcg_zfold(&S.f, S.rhs, S.cz, S.xp_all, S.bpart, S.bticket, S.bst, s), "Z^T R, beta");
+    hdk_ok(hdk_bcg_p(n, nv, S.cz, S.cp, S.cpv, df_.p2v, S.bst, S.any, handle, s), "P + cond");
+  };
+  build_loop_graph(st_, use_cond_, pre, body, [] {}, S.bgraph);
+}
+
+bool Engine::solve_columns_bcg(const ContactFrame& c, int r0, int& iterations) {
+  ColumnSet& S = *cols_;
+  if (!S.bst) build_columns_bcg();
+  const int nv = scene_.mesh.nv, K = kColumns;
+  const size_t n3 = 3 * static_cast<size_t>(nv);
+  const int real = std::min(K, c.k - r0);
+  for (int j = 0; j < K; ++j) {
+    const int row = std::min(r0 + j, c.k - 1);
+    hdk_ok(hdk_contact_column_init(&c.view, row, nv, df_.v2p, S.col[j].seed, S.col[j].x, st_), "column init");
+  }
+  *S.h_bm = real;
+  cuda_check(cudaMemcpyAsync(S.bm, S.h_bm, sizeof(int), cudaMemcpyHostToDevice, st_), "block size");
+  kernel_launches += K;
+  if (ph_.on) cuda_check(cudaEventRecord(ph_.ev[6], st_), "phase event");
+  LoopGraph& g = S.bgraph;
+  if (g.exec) {
+    cuda_check(cudaGraphLaunch(g.exec, st_), "columns (block CG)");
+  } else {  // host-driven loop (profiling fallback)
+    if (g.pre) cuda_check(cudaGraphLaunch(g.pre, st_), "columns (block CG)");
+    for (;;) {
+      cuda_check(cudaMemcpyAsync(S.h_any, S.any, sizeof(int), cudaMemcpyDeviceToHost, st_), "flag");
+      cuda_check(cudaStreamSynchronize(st_), "sync");
+      if (!*S.h_any) break;
+      cuda_check(cudaGraphLaunch(g.body, st_), "columns (block CG)");
+    }
+  }
+  cuda_check(cudaMemcpyAsync(S.h_bst, S.bst, sizeof(hdk_bcg), cudaMemcpyDeviceToHost, st_), "block CG state");
+  cuda_check(cudaStreamSynchronize(st_), "columns (block CG) sync");
+  const hdk_bcg& h = *S.h_bst;
+  if (h.err == -1 || h.err == 10) {  // Gram matrix lost definiteness or the cap: column by column
+    ++bcg_fallbacks;
+    return false;
+  }
+  if (h.err != 0) raise(Code::AdjointDiverged, "backward step: contact column block CG failed");
+  hdk_ok(hdk_cpcg_final(hf_.n, nv, K, S.xp_all, S.cz, S.x_all, df_.p2v, st_), "x = x + z (block)");
+  cuda_check(cudaMemcpyAsync(cX_ + n3 * r0, S.x_all, n3 * real * sizeof(double), cudaMemcpyDeviceToDevice, st_),
+             "columns");
+  if (ph_.on) {
+    cuda_check(cudaEventRecord(ph_.ev[7], st_), "phase event");
+    cuda_check(cudaEventSynchronize(ph_.ev[7]), "phase event");
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ph_.ev[6], ph_.ev[7]) == cudaSuccess) ph_.col_ms += ms;
+  }
+  kernel_launches += g.counts[0] + static_cast<long long>(g.counts[1]) * h.iter + 1;
+  const int per_col = 1 + h.iter;  // solves per column, as the column CG counts them
+  ph_.col_batches += 1;
+  ph_.col_iters += per_col;
+  ph_.col_real_iters += static_cast<long long>(per_col) * real;
+  column_solves += static_cast<long long>(per_col) * real;
+  column_streams += per_col;
+  iterations = per_col * real;
+  return true;
+}
+
 bool Engine::solve_columns_pcg(const ContactFrame& c, int r0, int& iterations) {
   ColumnSet& S = *cols_;
   if (!S.cst) build_columns_pcg();
@@ -513,7 +626,12 @@ bool Engine::solve_columns_pcg(const ContactFrame& c, int r0, int& iterations) {
 int Engine::solve_columns(const ContactFrame& c, int r0) {
   if (!cols_) build_columns();
   if (use_pcg_) {
+    static const bool block = [] {  // HETERODYN_COLUMN_CG=column: one CG per column (A/B)
+      const char* e = std::getenv("HETERODYN_COLUMN_CG");
+      return !(e && std::string(e) == "column");
+    }();
     int it = 0;
+    if (block && c.k - r0 > 1 && solve_columns_bcg(c, r0, it)) return it;
     if (solve_columns_pcg(c, r0, it)) return it;
   }
   ColumnSet& S = *cols_;

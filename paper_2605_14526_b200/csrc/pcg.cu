@@ -643,6 +643,7 @@ __device__ __forceinline__ void block_store_nb(const double (&v)[NQ], double* pa
 }
 
 // q = A p - gather(B p) per column and p.q; 8 lanes per row, 32 rows per block.
+template <bool kReduce>
 __global__ void __launch_bounds__(kT) k_cpcg_apply(hdk_vtx x, hdk_csr A, int n3, const double* __restrict__ ef,
                                                    size_t ef_stride, const double* __restrict__ p,
                                                    double* __restrict__ q, double* partial, size_t pstride,
@@ -693,6 +694,7 @@ __global__ void __launch_bounds__(kT) k_cpcg_apply(hdk_vtx x, hdk_csr A, int n3,
     const double* pr = pc + 3 * (size_t)row;
     acc[0] = (pr[0] * q0 + pr[1] * q1) + pr[2] * q2;
   }
+  if (!kReduce) return;
   double* part = partial + (size_t)c * pstride;
   const int nb = gridDim.x;
   block_store_nb<1>(acc, part, nb);
@@ -830,8 +832,17 @@ HDK_API int hdk_cpcg_apply(const hdk_vtx* x, const hdk_csr* a, int columns, cons
                            unsigned int* tickets, hdk_pcg* st, void* stream) {
   if (!x->pinc_off) return static_cast<int>(cudaErrorInvalidValue);
   const int nbx = (x->n + kT / 8 - 1) / (kT / 8);
-  hdk::launch(k_cpcg_apply, dim3(nbx > 0 ? nbx : 1, columns), dim3(kT), 0, S(stream), *x, *a, 3 * x->n, ef_sorted,
-              ef_stride, p, q, partial, pstride, tickets, st);
+  hdk::launch(k_cpcg_apply<true>, dim3(nbx > 0 ? nbx : 1, columns), dim3(kT), 0, S(stream), *x, *a, 3 * x->n,
+              ef_sorted, ef_stride, p, q, partial, pstride, tickets, st);
+  return last();
+}
+HDK_API int hdk_cpcg_apply_q(const hdk_vtx* x, const hdk_csr* a, int columns, const double* ef_sorted,
+                             size_t ef_stride, const double* p, double* q, hdk_pcg* st, void* stream) {
+  if (!x->pinc_off) return static_cast<int>(cudaErrorInvalidValue);
+  const int nbx = (x->n + kT / 8 - 1) / (kT / 8);
+  hdk::launch(k_cpcg_apply<false>, dim3(nbx > 0 ? nbx : 1, columns), dim3(kT), 0, S(stream), *x, *a, 3 * x->n,
+              ef_sorted, ef_stride, p, q, static_cast<double*>(nullptr), size_t{0}, static_cast<unsigned int*>(nullptr),
+              st);
   return last();
 }
 HDK_API int hdk_cpcg_rz(const hdk_factor* f, int columns, const double* r, double* z, const double* x,
@@ -850,6 +861,376 @@ HDK_API int hdk_cpcg_p(int n, int nv, int columns, const double* z, double* p, d
 HDK_API int hdk_cpcg_final(int n, int nv, int columns, const double* x, const double* z, double* xv, const int* p2v,
                            void* stream) {
   hdk::launch(k_cpcg_final, dim3(nb(3LL * n), columns), dim3(256), 0, S(stream), n, nv, x, z, xv, p2v);
+  return last();
+}
+
+}  // extern "C"
+
+// ---- block CG over a batch of contact-adjoint columns -------------------------
+// O'Leary's block PCG on (A - B) X = J with the preconditioner A (the
+// multi-column solve): the batch's m columns share one block Krylov space,
+// so the slow modes of A^{-1}(A - B) that every column meets (the columns'
+// Lanczos spectra coincide) are resolved once for the batch.
+//   Q = (A - B) P;  alpha = (P^T Q)^{-1} (Z^T R);  X += P alpha;  R -= Q alpha
+//   Z = A^{-1} R;   beta = (Z^T R)_old^{-1} (Z^T R);  P = Z + P beta
+// The stopping test is the reference's per column (||z_c|| <= tol ||x_c +
+// z_c||, backward.cpp:170-204), required of all m columns at the same
+// iteration; the columns return x_c + z_c.  The m x m algebra (Cholesky of
+// the two Gram matrices) runs in the last block of the reductions; a pivot
+// that is not positive ends the block with err = -1.
+namespace {
+
+constexpr int kBC = 8;                    // columns per batch (HDK_BB_COLUMNS)
+constexpr int kGram = kBC * (kBC + 1) / 2;  // 36: the upper triangle of a symmetric 8 x 8
+constexpr int kZq = kGram + 2 * kBC;      // Z^T R triangle + ||z_c||^2 + ||x_c + z_c||^2
+
+__device__ __forceinline__ int tri(int j, int c) { return c * (c + 1) / 2 + j; }  // j <= c
+
+// out = A^{-1} B for m x m symmetric positive definite A, by the whole block
+// in shared memory (row r, column c at [r * 8 + c]; entries outside m x m
+// ignored): Cholesky column by column (threads over the trailing entries),
+// then the m right-hand sides' triangular solves one per thread.  Returns
+// false (in every thread) if a pivot is not positive relative to the
+// largest diagonal.  A and B are overwritten.
+__device__ bool spd_solve8_block(double* a, double* b, int m, double* out) {
+  __shared__ int ok;
+  __shared__ double dmax;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    double d = 0.0;
+    for (int i = 0; i < m; ++i) d = fmax(d, a[i * 8 + i]);
+    dmax = d;
+    ok = 1;
+  }
+  __syncthreads();
+  for (int k = 0; k < m; ++k) {  // L overwrites the lower triangle of a
+    if (t == 0) {
+      const double d = a[k * 8 + k];
+      if (!(d > 1e-14 * dmax)) ok = 0;
+      a[k * 8 + k] = sqrt(fmax(d, 0.0));
+    }
+    __syncthreads();
+    if (!ok) return false;
+    const double lkk = a[k * 8 + k];
+    if (t > k && t < m) a[t * 8 + k] /= lkk;
+    __syncthreads();
+    const int i = k + 1 + t / 8, j = k + 1 + t % 8;  // trailing update a[i][j] -= l_ik l_jk, j <= i
+    if (t < 64 && i < m && j <= i) a[i * 8 + j] -= a[i * 8 + k] * a[j * 8 + k];
+    __syncthreads();
+  }
+  if (t < m) {  // column t of B: L y = b, L^T x = y
+    double y[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r < m) {
+        double v = b[r * 8 + t];
+        for (int q = 0; q < r; ++q) v -= a[r * 8 + q] * y[q];
+        y[r] = v / a[r * 8 + r];
+      }
+    }
+#pragma unroll
+    for (int r = 7; r >= 0; --r) {
+      if (r < m) {
+        double v = y[r];
+        for (int q = r + 1; q < m; ++q) v -= a[q * 8 + r] * y[q];
+        y[r] = v / a[r * 8 + r];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) out[r * 8 + t] = r < m ? y[r] : 0.0;
+  } else if (t < 8) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) out[r * 8 + t] = 0.0;
+  }
+  __syncthreads();
+  return true;
+}
+
+template <int NQ>
+__device__ __forceinline__ void block_store_many(const double (&v)[NQ], double* partial, int nb) {
+  __shared__ double sm[kT / 32][NQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const double s = warp_sum(v[q]);
+    if (lane == 0) sm[warp][q] = s;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < NQ; q += kT) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) s += sm[w][q];
+    partial[(size_t)q * nb + blockIdx.x] = s;
+  }
+}
+
+// Fixed-order fold of NQ quantities' nb block partials into red[] by the
+// whole (last) block: warp w folds quantities w, w + 8, ... with all of its
+// loads issued before the shuffle trees (a serial per-quantity fold by one
+// warp paid one L2 round trip per quantity: ~50 us for the 52 of k_bcg_zfold).
+template <int NQ>
+__device__ __forceinline__ void fold_many(const double* partial, int nb, double* red) {
+  constexpr int W = kT / 32, PER = (NQ + W - 1) / W;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double s[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int q = warp + W * k;
+    s[k] = 0.0;
+    if (q < NQ)
+      for (int b = lane; b < nb; b += 32) s[k] += partial[(size_t)q * nb + b];
+  }
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const double v = warp_sum(s[k]);
+    const int q = warp + W * k;
+    if (lane == 0 && q < NQ) red[q] = v;
+  }
+  __syncthreads();
+}
+
+__global__ void k_bcg_init(hdk_bcg* st, const int* m, double tol, int k_max, int* any, hdk_pcg* cst, int cst_count) {
+  const int mm = *m;
+  if (threadIdx.x == 0) {
+    st->m = mm;
+    st->tol = tol;
+    st->iter = 0;
+    st->k_max = k_max;
+    st->err = 0;
+    st->cond = 1;
+    st->done = 0;
+    *any = 1;
+  }
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) st->rz[i] = st->rz_old[i] = st->g[i] = st->alpha[i] = st->beta[i] = 0.0;
+  for (int c = threadIdx.x; c < cst_count; c += blockDim.x) {  // the per-column run flags of B p and q
+    cst[c].cond = c < mm ? 1 : 0;
+    cst[c].err = 0;
+  }
+}
+
+// G = P^T Q (upper triangle), then alpha = G^{-1} (Z^T R) in the last block.
+__global__ void __launch_bounds__(kT) k_bcg_gram_pq(int n3, const double* __restrict__ p, const double* __restrict__ q,
+                                                    double* partial, unsigned int* ticket, hdk_bcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (st->cond == 0) return;
+  const int m = st->m;
+  const int i = blockIdx.x * kT + threadIdx.x;
+  double acc[kGram];
+#pragma unroll
+  for (int k = 0; k < kGram; ++k) acc[k] = 0.0;
+  if (i < n3) {
+    double pv[kBC], qv[kBC];
+#pragma unroll
+    for (int c = 0; c < kBC; ++c) {
+      pv[c] = c < m ? p[(size_t)c * n3 + i] : 0.0;
+      qv[c] = c < m ? q[(size_t)c * n3 + i] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < kBC; ++c)
+#pragma unroll
+      for (int j = 0; j <= c; ++j) acc[tri(j, c)] = pv[j] * qv[c];
+  }
+  const int nb = gridDim.x;
+  block_store_many<kGram>(acc, partial, nb);
+  if (!last_block(ticket)) return;
+  __shared__ double red[kGram];
+  fold_many<kGram>(partial, nb, red);
+  __shared__ double g[64], rz[64];
+  if (threadIdx.x < 64) {
+    const int j = threadIdx.x >> 3, c = threadIdx.x & 7;
+    const bool in = j < m && c < m;
+    g[threadIdx.x] = in ? red[j <= c ? tri(j, c) : tri(c, j)] : 0.0;
+    st->g[threadIdx.x] = g[threadIdx.x];
+    rz[threadIdx.x] = st->rz[threadIdx.x];
+  }
+  __syncthreads();
+  if (!spd_solve8_block(g, rz, m, st->alpha) && threadIdx.x == 0) {
+    st->err = -1;
+    st->cond = 0;
+  }
+}
+
+// X += P alpha, R -= Q alpha (column c: sum over j of column j times alpha[j][c]).
+__global__ void k_bcg_xr(int n3, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                         const double* __restrict__ q, const hdk_bcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (st->cond == 0) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  const int m = st->m;
+  double pv[kBC], qv[kBC];
+#pragma unroll
+  for (int j = 0; j < kBC; ++j) {
+    pv[j] = j < m ? p[(size_t)j * n3 + i] : 0.0;
+    qv[j] = j < m ? q[(size_t)j * n3 + i] : 0.0;
+  }
+#pragma unroll
+  for (int c = 0; c < kBC; ++c) {
+    if (c >= m) break;
+    double dx = 0.0, dr = 0.0;
+#pragma unroll
+    for (int j = 0; j < kBC; ++j) {
+      const double a = st->alpha[j * 8 + c];
+      dx += pv[j] * a;
+      dr += qv[j] * a;
+    }
+    x[(size_t)c * n3 + i] += dx;
+    r[(size_t)c * n3 + i] -= dr;
+  }
+}
+
+// Z = A^{-1} R folded from the multi-column solve's tile partials; Z^T R,
+// ||z_c||^2, ||x_c + z_c||^2; in the last block the per-column stopping
+// tests and beta = (Z^T R)_old^{-1} (Z^T R).
+__global__ void __launch_bounds__(kT) k_bcg_zfold(hdk_factor f, size_t part2_stride, const double* __restrict__ r,
+                                                  double* __restrict__ z, const double* __restrict__ x, double* partial,
+                                                  unsigned int* ticket, hdk_bcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (st->cond == 0) return;
+  const int m = st->m;
+  const size_t n3 = 3 * (size_t)f.n;
+  const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
+  double acc[kZq];
+#pragma unroll
+  for (int k = 0; k < kZq; ++k) acc[k] = 0.0;
+  if (i < n3) {
+    const int col = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)col);
+    const int tile = col >> 8;
+    const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
+    const size_t base = (size_t)(tile + tb0) * 256 + (col & 255);
+    double zv[kBC], rv[kBC];
+#pragma unroll
+    for (int c = 0; c < kBC; ++c) {
+      zv[c] = 0.0;
+      rv[c] = 0.0;
+      if (c < m) {
+        const double* p2 = f.part2 + c * part2_stride;
+        double zi = 0.0;
+        for (int b = 0; b <= tb1 - tb0; ++b) zi += __ldg(p2 + 3 * (base + 256 * (size_t)b) + a);
+        zv[c] = zi;
+        rv[c] = r[c * n3 + i];
+        z[c * n3 + i] = zi;
+        const double t = x[c * n3 + i] + zi;
+        acc[kGram + c] = zi * zi;
+        acc[kGram + kBC + c] = t * t;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kBC; ++c)
+#pragma unroll
+      for (int j = 0; j <= c; ++j) acc[tri(j, c)] = zv[j] * rv[c];
+  }
+  const int nb = gridDim.x;
+  block_store_many<kZq>(acc, partial, nb);
+  if (!last_block(ticket)) return;
+  __shared__ double red[kZq];
+  fold_many<kZq>(partial, nb, red);
+  const int it = st->iter + 1;
+  bool all = true, finite = true;
+  for (int c = 0; c < m; ++c) {
+    const double zz = red[kGram + c], tt = red[kGram + kBC + c];
+    all = all && sqrt(zz) <= st->tol * fmax(sqrt(tt), 1e-30);
+    finite = finite && isfinite(zz) && isfinite(tt);
+  }
+  __shared__ double rz_new[64], a_old[64], rz_rhs[64];
+  if (threadIdx.x < 64) {
+    const int j = threadIdx.x >> 3, c = threadIdx.x & 7;
+    rz_new[threadIdx.x] = (j < m && c < m) ? red[j <= c ? tri(j, c) : tri(c, j)] : 0.0;
+    rz_rhs[threadIdx.x] = rz_new[threadIdx.x];
+    a_old[threadIdx.x] = st->rz[threadIdx.x];
+  }
+  __syncthreads();
+  bool ok = true;
+  if (it > 1 && !all) ok = spd_solve8_block(a_old, rz_rhs, m, st->beta);  // beta = RZ_old^{-1} RZ
+  if (threadIdx.x < 64) {
+    st->rz_old[threadIdx.x] = st->rz[threadIdx.x];
+    st->rz[threadIdx.x] = rz_new[threadIdx.x];
+  }
+  if (threadIdx.x != 0) return;
+  st->iter = it;
+  if (!ok) {
+    st->err = -1;
+    st->cond = 0;
+    return;
+  }
+  st->done = all ? 1 : 0;
+  if (!finite || (!all && it >= st->k_max)) st->err = 10;
+  st->cond = (!all && st->err == 0) ? 1 : 0;
+}
+
+// P = Z + P beta (P = Z after the first solve) and P by vertex; block 0
+// publishes the run flag / WHILE condition.
+__global__ void k_bcg_p(int n, int nv, const double* __restrict__ z, double* __restrict__ p, double* __restrict__ pv,
+                        const int* __restrict__ p2v, const hdk_bcg* st, int* any, cudaGraphConditionalHandle handle,
+                        int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int on = st->cond != 0 && st->err == 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *any = on;
+    if (use_handle) cudaGraphSetConditional(handle, on);
+  }
+  if (!on) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t n3 = 3 * (size_t)n;
+  if (i >= (int)n3) return;
+  const int m = st->m;
+  const bool first = st->iter == 1;
+  double old[kBC];
+#pragma unroll
+  for (int j = 0; j < kBC; ++j) old[j] = (!first && j < m) ? p[j * n3 + i] : 0.0;
+  const int row = i / 3;
+  const size_t vtx = 3 * (size_t)__ldg(p2v + row) + (i - 3 * row);
+#pragma unroll
+  for (int c = 0; c < kBC; ++c) {
+    if (c >= m) break;
+    double v = z[c * n3 + i];
+    if (!first) {
+#pragma unroll
+      for (int j = 0; j < kBC; ++j) v += old[j] * st->beta[j * 8 + c];
+    }
+    p[c * n3 + i] = v;
+    pv[(size_t)c * 3 * nv + vtx] = v;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+HDK_API size_t hdk_bcg_partial_doubles(int n) {
+  const size_t nb = (3 * static_cast<size_t>(n) + kT - 1) / kT;
+  return static_cast<size_t>(kZq) * nb;
+}
+HDK_API int hdk_bcg_init(hdk_bcg* st, const int* m, double tol, int k_max, int* any, hdk_pcg* cst, int cst_count,
+                         void* stream) {
+  hdk::launch(k_bcg_init, dim3(1), dim3(64), 0, S(stream), st, m, tol, k_max, any, cst, cst_count);
+  return last();
+}
+HDK_API int hdk_bcg_gram_pq(int n3, const double* p, const double* q, double* partial, unsigned int* ticket,
+                            hdk_bcg* st, void* stream) {
+  hdk::launch(k_bcg_gram_pq, dim3(nb(n3)), dim3(kT), 0, S(stream), n3, p, q, partial, ticket, st);
+  return last();
+}
+HDK_API int hdk_bcg_xr(int n3, double* x, double* r, const double* p, const double* q, const hdk_bcg* st,
+                       void* stream) {
+  hdk::launch(k_bcg_xr, dim3(nb(n3)), dim3(256), 0, S(stream), n3, x, r, p, q, st);
+  return last();
+}
+HDK_API int hdk_bcg_zfold(const hdk_factor* f, const double* r, double* z, const double* x, double* partial,
+                          unsigned int* ticket, hdk_bcg* st, void* stream) {
+  if (!f->tile_cta2) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_bcg_zfold, dim3(nb(3LL * f->n)), dim3(kT), 0, S(stream), *f, hdk_factor_part2_stride(f), r, z, x,
+              partial, ticket, st);
+  return last();
+}
+HDK_API int hdk_bcg_p(int n, int nv, const double* z, double* p, double* pv, const int* p2v, hdk_bcg* st, int* any,
+                      unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_bcg_p, dim3(nb(3LL * n)), dim3(256), 0, S(stream), n, nv, z, p, pv, p2v, st, any,
+              static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle ? 1 : 0);
   return last();
 }
 
