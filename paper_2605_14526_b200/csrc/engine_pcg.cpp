@@ -21,7 +21,8 @@ void Engine::build_pcg_graph() {
   if (!pcg_) {
     DevArena& A = *mem_;
     pcg_ = A.alloc<hdk_pcg>(segs_);
-    pcg_part_ = A.alloc<double>(segs_ > 1 ? static_cast<size_t>(HDK_SEG_PSTRIDE) * segs_ : 4 * HDK_RED_BLOCKS);
+    pcg_part_ = A.alloc<double>(segs_ > 1 ? static_cast<size_t>(HDK_SEG_PSTRIDE) * segs_
+                                          : std::max<size_t>(4 * HDK_RED_BLOCKS, hdk_cpcg_partial_stride(hf_.n)));
     pcg_ticket_ = A.alloc<unsigned int>(segs_);
     cuda_zero(pcg_ticket_, sizeof(unsigned int) * segs_, "zero ticket");
     for (double** v : {&pr_, &pz_, &pp_, &pq_, &pap_, &prp_}) *v = A.alloc<double>(n3p);
@@ -38,6 +39,39 @@ void Engine::build_pcg_graph() {
   const int n = hf_.n;
   hdk_factor fs = df_;
   fs.run_flag = &pcg_->cond;
+  // fused stages (default): q = (A - B) p over a grid covering the rows once,
+  // and z folded from the solve's tile partials in the r.z kernel (no
+  // separate x-fold launch); HETERODYN_PCG_FUSED=0: the first form
+  static const bool fused = [] {
+    const char* e = std::getenv("HETERODYN_PCG_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  if (fused && df_.tile_cta2) {
+    const size_t pst = hdk_cpcg_partial_stride(n);
+    auto pre_f = [&] {
+      hdk_check_p(hdk_pcg_init(pcg_, 1e-10, 500, s), "pcg init");
+      hdk_check_p(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
+      hdk_check_p(hdk_gather_perm(&dv_, x_, nullptr, xp_, s), "x0 in elimination order");
+      hdk_check_p(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B x0");
+      hdk_check_p(hdk_gather_pp(&dv_, nullptr, ef_, rx_, nullptr, s), "R(x0)");
+      hdk_check_p(hdk_pcg_spmv(&a_ff_, xp_, pap_, pcg_, s), "A x0");
+      hdk_check_p(hdk_pcg_r0(static_cast<int>(n3p), seedp_, pap_, rx_, pr_, s), "r0");
+      hdk_check_p(hdk_apply_inverse3_partial(&fs, pr_, s), "A^-1 r0 (tile partials)");
+      hdk_check_p(hdk_cpcg_rz(&fs, 1, pr_, pz_, xp_, pcg_part_, pst, pcg_ticket_, pcg_, s), "z0, rz");
+      hdk_check_p(hdk_pcg_p(n, pz_, pp_, ppv_, df_.p2v, pcg_, 0ULL, s), "p");
+    };
+    auto body_f = [&](unsigned long long handle) {
+      hdk_check_p(hdk_bapply_sorted(&dm_, dcomp_, ppv_, ef_, corner_pos_, &pcg_->cond, s), "B p");
+      hdk_check_p(hdk_cpcg_apply(&dv_, &a_ff_, 1, ef_, 0, pp_, pq_, pcg_part_, pst, pcg_ticket_, pcg_, s),
+                  "q = (A - B) p");
+      hdk_check_p(hdk_pcg_xr(static_cast<int>(n3p), xp_, pr_, pp_, pq_, pcg_, s), "x, r");
+      hdk_check_p(hdk_apply_inverse3_partial(&fs, pr_, s), "A^-1 r (tile partials)");
+      hdk_check_p(hdk_cpcg_rz(&fs, 1, pr_, pz_, xp_, pcg_part_, pst, pcg_ticket_, pcg_, s), "z, rz");
+      hdk_check_p(hdk_pcg_p(n, pz_, pp_, ppv_, df_.p2v, pcg_, handle, s), "p + cond");
+    };
+    build_loop_graph(st_, use_cond_, pre_f, body_f, [] {}, *pgraph_);
+    return;
+  }
   auto pre = [&] {
     hdk_check_p(hdk_pcg_init(pcg_, 1e-10, 500, s), "pcg init");
     hdk_check_p(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
