@@ -604,6 +604,32 @@ HDK_API int hdk_bcg_zfold(const hdk_factor* f, const double* r, double* z, const
 HDK_API int hdk_bcg_p(int n, int nv, const double* z, double* p, double* pv, const int* p2v, hdk_bcg* st, int* any,
                       unsigned long long cond_handle, void* stream);
 
+/* Deflated CG for the single backbone (pcg.cu, Saad et al.'s deflated PCG):
+ * k <= 8 approximate slow eigenvectors W of A^{-1}(A - B) (Ritz vectors of an
+ * earlier backbone CG, recycled across time steps) are projected out: the
+ * first iterate is Galerkin-corrected on span W and every search direction
+ * is made (A - B)-orthogonal to W.  Same system, same stopping test; only the
+ * iteration count changes.  W and AW = (A - B) W are [8][3n] in elimination
+ * order; hist records (alpha, beta, r.z) and the z's of a recording solve. */
+typedef struct hdk_defl {
+  double l[64];          /* Cholesky factor of E = W^T (A - B) W, row r col c at [r * 8 + c] */
+  double mu[8], c[8];    /* per-iteration projection / first-iterate coefficients */
+  int k, use, active, rec, hcap, pad;
+} hdk_defl;
+HDK_API size_t hdk_defl_partial_doubles(int n);
+HDK_API int hdk_defl_gram(int n3, const double* w, const double* aw, double* partial, unsigned int* ticket,
+                          hdk_defl* d, void* stream);
+HDK_API int hdk_defl_galerkin(int n3, double* x, double* r, const double* w, const double* aw, double* partial,
+                              unsigned int* ticket, hdk_defl* d, void* stream);
+HDK_API int hdk_dpcg_rz(const hdk_factor* f, const double* r, double* z, const double* x, const double* aw,
+                        double* partial, unsigned int* ticket, hdk_pcg* st, hdk_defl* d, double* zhist,
+                        double* hist, void* stream);
+HDK_API int hdk_dpcg_p(int n, const double* z, double* p, double* pv, const int* p2v, const hdk_pcg* st,
+                       const hdk_defl* d, const double* w, unsigned long long cond_handle, void* stream);
+HDK_API int hdk_ritz_combine(int n3, const double* zhist, const double* coef, int j, int k, double* w, void* stream);
+HDK_API int hdk_scatter_cols(int n, int nv, int k, const double* w, double* wv, const int* p2v, const hdk_defl* d,
+                             void* stream);
+
 /* Per-column partials of hdk_cpcg_apply / hdk_cpcg_rz: column c's at
  * partial + c pstride, pstride = hdk_cpcg_partial_stride(n) doubles. */
 HDK_API size_t hdk_cpcg_partial_stride(int n);

@@ -176,6 +176,14 @@ HD_API hd_status hd_sim_solve_free(hd_sim* sim, const double* rhs_full, const do
  * at their current values when freeze_means is nonzero (freeze_means,
  * material.cpp:82-86, the gradcheck/identify convention). */
 HD_API hd_status hd_sim_set_young(hd_sim* sim, const double* young, size_t count, int freeze_means);
+/* B200 extension: recycled-subspace deflation of the adjoint backbone CG
+ * (on by default; HETERODYN_DEFLATION=0 at creation turns it off).  The
+ * backbone solves reuse Ritz vectors of an earlier solve, so a repeated
+ * backward of the same frame agrees with the first to the CG stopping
+ * tolerance rather than bitwise; off, every solve is a pure function of its
+ * inputs.  Toggling drops the recycled subspace.  (The reference CPU library
+ * accepts and ignores it.) */
+HD_API hd_status hd_sim_set_deflation(hd_sim* sim, int on);
 
 /* Counters for roofline accounting (factor.hpp:39,119-121; forward.hpp:100;
  * backward.hpp:26): factor nnz, free vertex count, cumulative 3-axis solves,

@@ -422,6 +422,11 @@ hd_status hd_sim_solve_free(hd_sim* sim, const double* rhs, const double* fixed_
   });
 }
 
+hd_status hd_sim_set_deflation(hd_sim* sim, int) {  // the CPU restatement has no recycled subspace
+  if (!sim) return null_arg("hd_sim_set_deflation");
+  return HD_OK;
+}
+
 hd_status hd_sim_set_young(hd_sim* sim, const double* young, size_t count, int freeze) {
   if (!sim || !young) return null_arg("hd_sim_set_young");
   return guarded([&] {

@@ -401,6 +401,11 @@ hd_status hd_sim_set_young(hd_sim* sim, const double* young, size_t count, int f
   return guarded([&] { sim->eng->set_young(Vec(young, young + count), freeze != 0); });
 }
 
+hd_status hd_sim_set_deflation(hd_sim* sim, int on) {
+  if (!sim) return bad_arg("hd_sim_set_deflation: sim is NULL");
+  return guarded([&] { sim->eng->set_deflation(on != 0); });
+}
+
 hd_status hd_sim_backward_canonical(hd_sim* sim, double* dl_dq0, double* dl_dv0, double* dl_df_ext, double* dl_de,
                                     double* dl_dw, size_t dl_dw_capacity) {
   if (!sim) return bad_arg("hd_sim_backward_canonical: sim is NULL");

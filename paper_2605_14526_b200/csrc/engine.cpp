@@ -206,6 +206,10 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared
   // HETERODYN_ADJOINT=aa keeps the reference's Anderson fixed point
   use_pcg_ = true;
   if (const char* ad = std::getenv("HETERODYN_ADJOINT")) use_pcg_ = std::string(ad) != "aa";
+  {  // recycled-subspace deflation of the backbone CG (HETERODYN_DEFLATION=0: off; hd_sim_set_deflation)
+    const char* e = std::getenv("HETERODYN_DEFLATION");
+    defl_.on = !(e && e[0] == '0');
+  }
   const char* nc = std::getenv("HETERODYN_NO_COND_GRAPH");
   use_cond_ = !(nc && std::atoi(nc) != 0);
   int dev_count = 0;

@@ -113,6 +113,9 @@ struct GradOut {
 
 class Engine {
  public:
+  // Turns recycled-subspace deflation of the backbone CG on or off for the
+  // following solves and drops the recycled subspace (engine_pcg.cpp).
+  void set_deflation(bool on);
   // young: optional per-element Young's moduli replacing the scene's (a
   // parameter sample of a batch); the factor is built once for them.
   // solve_ctas: cap on the CTAs of each solve pass (0 = one resident wave).
@@ -290,6 +293,24 @@ class Engine {
   double *pcg_part_ = nullptr, *pr_ = nullptr, *pz_ = nullptr, *pp_ = nullptr, *pq_ = nullptr, *pap_ = nullptr,
          *prp_ = nullptr, *ppv_ = nullptr;
   unsigned int* pcg_ticket_ = nullptr;
+  // Deflated backbone CG (engine_pcg.cpp, pcg.cu hdk_defl): Ritz vectors of a
+  // recorded backbone CG, recycled across steps.
+  struct Deflation {
+    bool on = false;        // HETERODYN_DEFLATION != 0 and a single (non-segmented) engine
+    bool valid = false;     // W holds Ritz vectors
+    int k = 0, hcap = 0, plain_iters = 0;
+    hdk_defl* d = nullptr;  // device state
+    hdk_defl* h = nullptr;  // pinned mirror (the int fields are uploaded per solve)
+    hdk_pcg* ones = nullptr;  // run flags of the 8-column B apply / q kernels
+    hdk_pcg* h_ones = nullptr;
+    double *w = nullptr, *aw = nullptr, *wv = nullptr, *ef8 = nullptr, *zhist = nullptr, *hist = nullptr,
+           *coef = nullptr, *part = nullptr, *h_hist = nullptr, *h_coef = nullptr;
+    unsigned int* ticket = nullptr;
+    long long refreshes = 0, deflated_solves = 0;
+  } defl_;
+  void defl_alloc();
+
+  void defl_after_solve(int iterations, bool converged);
   long long pcg_fallbacks = 0, bcg_fallbacks = 0;
   void build_pcg_graph();
   void build_pcg_graph_seg();

@@ -1,12 +1,15 @@
+#include <cmath>
 // The adjoint backbone by preconditioned conjugate gradients (pcg.cu): the
 // same linear system and the same stopping test as the reference's Anderson
 // fixed point (backward.cpp:170-204), a Krylov method instead of the
 // window-8 mixing.  One iteration: B p (matrix-free, engine layout), A p
 // (A_ff SpMV), q = A p - B p, the CG updates, one global solve z = A^{-1} r.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "engine.hpp"
 
@@ -48,7 +51,33 @@ void Engine::build_pcg_graph() {
   }();
   if (fused && df_.tile_cta2) {
     const size_t pst = hdk_cpcg_partial_stride(n);
+    if (defl_.on) defl_alloc();
+    Deflation& D = defl_;
+    const size_t n3 = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
+    const int cstride = static_cast<int>(sizeof(hdk_pcg) / sizeof(int));
     auto pre_f = [&] {
+      if (D.on) {
+        hdk_check_p(hdk_pcg_init(pcg_, 1e-10, 500, s), "pcg init");
+        hdk_check_p(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
+        hdk_check_p(hdk_gather_perm(&dv_, x_, nullptr, xp_, s), "x0 in elimination order");
+        hdk_check_p(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B x0");
+        hdk_check_p(hdk_gather_pp(&dv_, nullptr, ef_, rx_, nullptr, s), "R(x0)");
+        hdk_check_p(hdk_pcg_spmv(&a_ff_, xp_, pap_, pcg_, s), "A x0");
+        hdk_check_p(hdk_pcg_r0(static_cast<int>(n3p), seedp_, pap_, rx_, pr_, s), "r0");
+        // this step's (A - B) W, E = W^T (A - B) W, and the Galerkin first iterate
+        hdk_check_p(hdk_scatter_cols(n, scene_.mesh.nv, 8, D.w, D.wv, df_.p2v, D.d, s), "W by vertex");
+        hdk_check_p(hdk_bapply_cols_sorted(&dm_, dcomp_, D.wv, n3, D.ef8, 12 * ne, corner_pos_, &D.ones->cond, cstride,
+                                           8, s),
+                    "B W");
+        hdk_check_p(hdk_cpcg_apply_q(&dv_, &a_ff_, 8, D.ef8, 12 * ne, D.w, D.aw, D.ones, s), "(A - B) W");
+        hdk_check_p(hdk_defl_gram(static_cast<int>(n3p), D.w, D.aw, D.part, D.ticket, D.d, s), "E = W^T A' W");
+        hdk_check_p(hdk_defl_galerkin(static_cast<int>(n3p), xp_, pr_, D.w, D.aw, D.part, D.ticket, D.d, s),
+                    "Galerkin first iterate");
+        hdk_check_p(hdk_apply_inverse3_partial(&fs, pr_, s), "A^-1 r0 (tile partials)");
+        hdk_check_p(hdk_dpcg_rz(&fs, pr_, pz_, xp_, D.aw, D.part, D.ticket, pcg_, D.d, D.zhist, D.hist, s), "z0, rz");
+        hdk_check_p(hdk_dpcg_p(n, pz_, pp_, ppv_, df_.p2v, pcg_, D.d, D.w, 0ULL, s), "p");
+        return;
+      }
       hdk_check_p(hdk_pcg_init(pcg_, 1e-10, 500, s), "pcg init");
       hdk_check_p(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
       hdk_check_p(hdk_gather_perm(&dv_, x_, nullptr, xp_, s), "x0 in elimination order");
@@ -66,6 +95,11 @@ void Engine::build_pcg_graph() {
                   "q = (A - B) p");
       hdk_check_p(hdk_pcg_xr(static_cast<int>(n3p), xp_, pr_, pp_, pq_, pcg_, s), "x, r");
       hdk_check_p(hdk_apply_inverse3_partial(&fs, pr_, s), "A^-1 r (tile partials)");
+      if (D.on) {
+        hdk_check_p(hdk_dpcg_rz(&fs, pr_, pz_, xp_, D.aw, D.part, D.ticket, pcg_, D.d, D.zhist, D.hist, s), "z, rz");
+        hdk_check_p(hdk_dpcg_p(n, pz_, pp_, ppv_, df_.p2v, pcg_, D.d, D.w, handle, s), "p + cond");
+        return;
+      }
       hdk_check_p(hdk_cpcg_rz(&fs, 1, pr_, pz_, xp_, pcg_part_, pst, pcg_ticket_, pcg_, s), "z, rz");
       hdk_check_p(hdk_pcg_p(n, pz_, pp_, ppv_, df_.p2v, pcg_, handle, s), "p + cond");
     };
@@ -130,6 +164,32 @@ void Engine::build_pcg_graph_seg() {
 bool Engine::run_pcg(int& iterations) {
   if (!pgraph_ || (!pgraph_->exec && !pgraph_->body)) build_pcg_graph();
   LoopGraph& g = *pgraph_;
+  // profiling: HETERODYN_CG_TRACE1=path writes the (alpha, beta) of the last
+  // backbone CG (the fused path's r.z kernel records them)
+  static const char* trace1 = std::getenv("HETERODYN_CG_TRACE1");
+  static double* d_tr = nullptr;
+  static double** h_tr = nullptr;
+  if (trace1 && !d_tr) {
+    cuda_check(cudaMalloc(&d_tr, sizeof(double) * 8 * 512 * 2), "cg trace");
+    cuda_check(cudaMallocHost(&h_tr, 2 * sizeof(double*)), "cg trace");
+    h_tr[0] = d_tr;
+    h_tr[1] = nullptr;
+  }
+  if (d_tr) {
+    cuda_check(cudaMemsetAsync(d_tr, 0, sizeof(double) * 8 * 512 * 2, st_), "cg trace");
+    hdk_check_p(hdk_set_cpcg_trace(h_tr, st_), "cg trace");
+  }
+  if (defl_.on && defl_.d) {  // this solve: deflate with W, or record the Ritz data for W
+    Deflation& D = defl_;
+    D.h->use = D.valid ? 1 : 0;
+    D.h->k = D.valid ? D.k : 0;
+    D.h->rec = D.valid ? 0 : 1;
+    D.h->hcap = D.hcap;
+    D.h->active = 0;
+    cuda_check(cudaMemcpyAsync(&D.d->k, &D.h->k, 6 * sizeof(int), cudaMemcpyHostToDevice, st_), "deflation flags");
+    for (int c = 0; c < 8; ++c) D.h_ones[c].cond = (D.valid && c < D.k) ? 1 : 0;
+    cuda_check(cudaMemcpyAsync(D.ones, D.h_ones, 8 * sizeof(hdk_pcg), cudaMemcpyHostToDevice, st_), "deflation flags");
+  }
   if (g.exec) {
     cuda_check(cudaGraphLaunch(g.exec, st_), "pcg");
   } else {  // host-driven loop (profiling fallback)
@@ -145,6 +205,15 @@ bool Engine::run_pcg(int& iterations) {
   }
   cuda_check(cudaMemcpyAsync(h_pcg_, pcg_, sizeof(hdk_pcg) * segs_, cudaMemcpyDeviceToHost, st_), "pcg state");
   cuda_check(cudaStreamSynchronize(st_), "pcg");
+  if (d_tr) {
+    hdk_check_p(hdk_set_cpcg_trace(h_tr + 1, st_), "cg trace off");
+    std::vector<double> h(8 * 512 * 2);
+    cuda_check(cudaMemcpy(h.data(), d_tr, h.size() * sizeof(double), cudaMemcpyDeviceToHost), "cg trace");
+    if (FILE* fp = std::fopen(trace1, "wb")) {
+      std::fwrite(h.data(), sizeof(double), h.size(), fp);
+      std::fclose(fp);
+    }
+  }
   int most = 0;
   for (int k = 0; k < segs_; ++k) {
     const hdk_pcg& h = h_pcg_[k];
@@ -158,10 +227,134 @@ bool Engine::run_pcg(int& iterations) {
     most = std::max(most, h.iter);
     if (segs_ > 1) seg_sample_iterations += 1 + h.iter;
   }
+  if (defl_.on && defl_.d && segs_ == 1) defl_after_solve(h_pcg_[0].iter, h_pcg_[0].done != 0);
   hdk_check_p(hdk_pcg_final(hf_.n, xp_, pz_, x_, df_.p2v, st_), "x = x + z");
   iterations = 1 + most;  // the first solve x0 = A^{-1} s and one solve per CG step (the slowest sample)
   kernel_launches += g.counts[0] + static_cast<long long>(g.counts[1]) * most + 2;
   return true;
+}
+
+}  // namespace hdb
+
+namespace hdb {
+
+void Engine::set_deflation(bool on) {
+  defl_.valid = false;
+  if (on == defl_.on) return;
+  defl_.on = on;
+  if (pgraph_) {  // the captured graph has or lacks the deflation stages: re-capture
+    pgraph_->destroy();
+    pgraph_.reset();
+  }
+}
+
+void Engine::defl_alloc() {
+  Deflation& D = defl_;
+  if (D.d) return;
+  DevArena& A = *mem_;
+  const size_t n3p = 3 * static_cast<size_t>(hf_.n), n3 = 3 * static_cast<size_t>(scene_.mesh.nv),
+               ne = scene_.mesh.ne;
+  D.hcap = 200;
+  D.d = A.alloc<hdk_defl>(1);
+  D.ones = A.alloc<hdk_pcg>(8);
+  D.w = A.alloc<double>(8 * n3p);
+  D.aw = A.alloc<double>(8 * n3p);
+  D.wv = A.alloc<double>(8 * n3);
+  D.ef8 = A.alloc<double>(8 * 12 * ne);
+  D.zhist = A.alloc<double>(static_cast<size_t>(D.hcap) * n3p);
+  D.hist = A.alloc<double>(3 * static_cast<size_t>(D.hcap));
+  D.coef = A.alloc<double>(8 * static_cast<size_t>(D.hcap));
+  D.part = A.alloc<double>(std::max(hdk_defl_partial_doubles(hf_.n), hdk_bcg_partial_doubles(hf_.n)));
+  D.ticket = A.alloc<unsigned int>(1);
+  cuda_check(cudaMallocHost(&D.h, sizeof(hdk_defl)), "pinned deflation");
+  cuda_check(cudaMallocHost(&D.h_ones, 8 * sizeof(hdk_pcg)), "pinned deflation");
+  cuda_check(cudaMallocHost(&D.h_hist, 3 * sizeof(double) * D.hcap), "pinned deflation");
+  cuda_check(cudaMallocHost(&D.h_coef, 8 * sizeof(double) * D.hcap), "pinned deflation");
+  std::memset(D.h, 0, sizeof(hdk_defl));
+  std::memset(D.h_ones, 0, 8 * sizeof(hdk_pcg));
+}
+
+namespace {
+// Eigen-decomposition of a symmetric m x m matrix (cyclic Jacobi): a is
+// destroyed, eigenvalues into ev, eigenvectors into the columns of v.
+void jacobi_eigen(std::vector<double>& a, int m, std::vector<double>& ev, std::vector<double>& v) {
+  v.assign(static_cast<size_t>(m) * m, 0.0);
+  for (int i = 0; i < m; ++i) v[i * m + i] = 1.0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) off += a[p * m + q] * a[p * m + q];
+    if (off < 1e-30) break;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        const double apq = a[p * m + q];
+        if (std::fabs(apq) < 1e-300) continue;
+        const double theta = (a[q * m + q] - a[p * m + p]) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < m; ++k) {  // rotate columns p, q
+          const double akp = a[k * m + p], akq = a[k * m + q];
+          a[k * m + p] = c * akp - s * akq;
+          a[k * m + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < m; ++k) {  // rotate rows p, q
+          const double apk = a[p * m + k], aqk = a[q * m + k];
+          a[p * m + k] = c * apk - s * aqk;
+          a[q * m + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < m; ++k) {
+          const double vkp = v[k * m + p], vkq = v[k * m + q];
+          v[k * m + p] = c * vkp - s * vkq;
+          v[k * m + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  ev.resize(m);
+  for (int i = 0; i < m; ++i) ev[i] = a[i * m + i];
+}
+}  // namespace
+
+// After a backbone CG: a recording solve yields W (the Ritz vectors of the
+// k smallest Ritz values of its Lanczos matrix, from its z's); a deflated
+// solve that needed more than 85 % of the recorded solve's iterations (the
+// state has drifted) or whose E lost definiteness drops W, so the next
+// solve records again.
+void Engine::defl_after_solve(int iterations, bool converged) {
+  Deflation& D = defl_;
+  if (D.valid) {
+    ++D.deflated_solves;
+    cuda_check(cudaMemcpy(&D.h->active, &D.d->active, sizeof(int), cudaMemcpyDeviceToHost), "deflation state");
+    if (!D.h->active || iterations > (85 * D.plain_iters) / 100) D.valid = false;
+    return;
+  }
+  const int J = iterations;  // z_1 .. z_J recorded (rz calls)
+  if (!converged || J < 6 || J > D.hcap) return;
+  cuda_check(cudaMemcpy(D.h_hist, D.hist, 3 * sizeof(double) * J, cudaMemcpyDeviceToHost), "Ritz history");
+  const int m = J - 1;  // Lanczos matrix from (alpha_j, beta_j), j = 1 .. J - 1
+  std::vector<double> T(static_cast<size_t>(m) * m, 0.0), ev, Y;
+  for (int j = 0; j < m; ++j) {
+    const double a = D.h_hist[3 * (j + 1)], b = D.h_hist[3 * (j + 1) + 1];
+    const double ap = j > 0 ? D.h_hist[3 * j] : 0.0, bp = j > 0 ? D.h_hist[3 * j + 1] : 0.0;
+    if (!(a > 0.0) || !(b >= 0.0)) return;
+    T[j * m + j] = 1.0 / a + (j > 0 ? bp / ap : 0.0);
+    if (j + 1 < m) T[j * m + j + 1] = T[(j + 1) * m + j] = std::sqrt(b) / a;
+  }
+  jacobi_eigen(T, m, ev, Y);
+  std::vector<int> order(m);
+  for (int i = 0; i < m; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int x, int y) { return ev[x] < ev[y]; });
+  const int k = std::min(8, m / 2);
+  for (int c = 0; c < k; ++c)
+    for (int j = 0; j < m; ++j) {  // v_j = (-1)^j z_{j+1} / sqrt(r_{j+1}.z_{j+1})
+      const double rz = D.h_hist[3 * j + 2];
+      D.h_coef[c * m + j] = Y[j * m + order[c]] * ((j & 1) ? -1.0 : 1.0) / std::sqrt(rz);
+    }
+  cuda_check(cudaMemcpyAsync(D.coef, D.h_coef, sizeof(double) * k * m, cudaMemcpyHostToDevice, st_), "Ritz coefficients");
+  hdk_check_p(hdk_ritz_combine(3 * hf_.n, D.zhist, D.coef, m, k, D.w, st_), "Ritz vectors");
+  D.k = k;
+  D.valid = true;
+  D.plain_iters = J;
+  ++D.refreshes;
 }
 
 }  // namespace hdb

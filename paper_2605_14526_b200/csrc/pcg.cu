@@ -1235,3 +1235,288 @@ HDK_API int hdk_bcg_p(int n, int nv, const double* z, double* p, double* pv, con
 }
 
 }  // extern "C"
+
+// ---- deflated CG for the single backbone ---------------------------------------
+// (hdk.h hdk_defl).  Per iteration the r.z kernel also forms d = (AW)^T z
+// and mu = E^{-1} d (E = W^T A' W, A' = A - B, Cholesky factor precomputed),
+// and the p kernel subtracts W mu: p = z + beta p - W mu.  A recording solve
+// (no deflation) keeps its z's and (alpha, beta, r.z) for the host's Ritz
+// extraction.
+namespace {
+
+constexpr int kDq = 3 + 8;  // r.z, |z|^2, |x + z|^2, (AW_k)^T z
+
+__device__ void chol_solve_l(const double* l, int k, const double* b, double* x) {  // L L^T x = b
+  double y[8];
+  for (int i = 0; i < k; ++i) {
+    double v = b[i];
+    for (int t = 0; t < i; ++t) v -= l[i * 8 + t] * y[t];
+    y[i] = v / l[i * 8 + i];
+  }
+  for (int i = k - 1; i >= 0; --i) {
+    double v = y[i];
+    for (int t = i + 1; t < k; ++t) v -= l[t * 8 + i] * y[t];
+    y[i] = v / l[i * 8 + i];
+  }
+  for (int i = 0; i < k; ++i) x[i] = y[i];
+}
+
+// E = W^T A' W (upper triangle) and its Cholesky factor; active = factor ok.
+__global__ void __launch_bounds__(kT) k_defl_gram(int n3, const double* __restrict__ w, const double* __restrict__ aw,
+                                                  double* partial, unsigned int* ticket, hdk_defl* d) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (!d->use) return;
+  const int k = d->k;
+  const int i = blockIdx.x * kT + threadIdx.x;
+  double acc[kGram];
+#pragma unroll
+  for (int q = 0; q < kGram; ++q) acc[q] = 0.0;
+  if (i < n3) {
+    double wv[kBC], av[kBC];
+#pragma unroll
+    for (int c = 0; c < kBC; ++c) {
+      wv[c] = c < k ? w[(size_t)c * n3 + i] : 0.0;
+      av[c] = c < k ? aw[(size_t)c * n3 + i] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < kBC; ++c)
+#pragma unroll
+      for (int j = 0; j <= c; ++j) acc[tri(j, c)] = 0.5 * (wv[j] * av[c] + wv[c] * av[j]);  // symmetrised
+  }
+  const int nb = gridDim.x;
+  block_store_many<kGram>(acc, partial, nb);
+  if (!last_block(ticket)) return;
+  __shared__ double red[kGram];
+  fold_many<kGram>(partial, nb, red);
+  if (threadIdx.x != 0) return;
+  double l[64];
+  for (int q = 0; q < 64; ++q) l[q] = 0.0;
+  for (int r = 0; r < k; ++r)
+    for (int c = 0; c <= r; ++c) l[r * 8 + c] = red[tri(c, r)];
+  double dmax = 0.0;
+  for (int r = 0; r < k; ++r) dmax = fmax(dmax, l[r * 8 + r]);
+  bool ok = k > 0;
+  for (int j = 0; j < k && ok; ++j) {
+    double dj = l[j * 8 + j];
+    for (int t = 0; t < j; ++t) dj -= l[j * 8 + t] * l[j * 8 + t];
+    if (!(dj > 1e-12 * dmax)) {
+      ok = false;
+      break;
+    }
+    dj = sqrt(dj);
+    l[j * 8 + j] = dj;
+    for (int r = j + 1; r < k; ++r) {
+      double v = l[r * 8 + j];
+      for (int t = 0; t < j; ++t) v -= l[r * 8 + t] * l[j * 8 + t];
+      l[r * 8 + j] = v / dj;
+    }
+  }
+  for (int q = 0; q < 64; ++q) d->l[q] = l[q];
+  d->active = ok ? 1 : 0;
+}
+
+// First iterate: c = E^{-1} W^T r (last block), then (k_defl_correct) x += W c, r -= AW c.
+__global__ void __launch_bounds__(kT) k_defl_dots(int n3, const double* __restrict__ r, const double* __restrict__ w,
+                                                  double* partial, unsigned int* ticket, hdk_defl* d) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (!d->use || !d->active) return;
+  const int k = d->k;
+  const int i = blockIdx.x * kT + threadIdx.x;
+  double acc[kBC];
+#pragma unroll
+  for (int c = 0; c < kBC; ++c) acc[c] = (i < n3 && c < k) ? w[(size_t)c * n3 + i] * r[i] : 0.0;
+  const int nb = gridDim.x;
+  block_store_many<kBC>(acc, partial, nb);
+  if (!last_block(ticket)) return;
+  __shared__ double red[kBC];
+  fold_many<kBC>(partial, nb, red);
+  if (threadIdx.x != 0) return;
+  double cc[8];
+  chol_solve_l(d->l, k, red, cc);
+  for (int c = 0; c < 8; ++c) d->c[c] = c < k ? cc[c] : 0.0;
+}
+
+__global__ void k_defl_correct(int n3, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ w,
+                               const double* __restrict__ aw, const hdk_defl* d) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (!d->use || !d->active) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  const int k = d->k;
+  double dx = 0.0, dr = 0.0;
+#pragma unroll
+  for (int c = 0; c < kBC; ++c)
+    if (c < k) {
+      dx += w[(size_t)c * n3 + i] * d->c[c];
+      dr += aw[(size_t)c * n3 + i] * d->c[c];
+    }
+  x[i] += dx;
+  r[i] -= dr;
+}
+
+// z from the solve's tile partials, r.z / |z|^2 / |x + z|^2, d = (AW)^T z;
+// last block: stopping test, beta, mu = E^{-1} d; recording: z and the
+// coefficients into the history.
+__global__ void __launch_bounds__(kT) k_dpcg_rz(hdk_factor f, const double* __restrict__ r, double* __restrict__ z,
+                                                const double* __restrict__ x, const double* __restrict__ aw,
+                                                double* partial, unsigned int* ticket, hdk_pcg* st, hdk_defl* d,
+                                                double* __restrict__ zhist, double* hist) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (st->cond == 0) return;
+  const size_t n3 = 3 * (size_t)f.n;
+  const bool defl = d->use && d->active;
+  const int k = defl ? d->k : 0;
+  const int it = st->iter + 1;
+  const bool rec = d->rec && it <= d->hcap;
+  double acc[kDq];
+#pragma unroll
+  for (int q = 0; q < kDq; ++q) acc[q] = 0.0;
+  const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
+  if (i < n3) {
+    const int col = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)col);
+    const int tile = col >> 8;
+    const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
+    const size_t base = (size_t)(tile + tb0) * 256 + (col & 255);
+    double zi = 0.0;
+    for (int b = 0; b <= tb1 - tb0; ++b) zi += __ldg(f.part2 + 3 * (base + 256 * (size_t)b) + a);
+    z[i] = zi;
+    if (rec) zhist[(size_t)(it - 1) * n3 + i] = zi;
+    const double t = x[i] + zi;
+    acc[0] = r[i] * zi;
+    acc[1] = zi * zi;
+    acc[2] = t * t;
+#pragma unroll
+    for (int c = 0; c < kBC; ++c) acc[3 + c] = c < k ? aw[(size_t)c * n3 + i] * zi : 0.0;
+  }
+  const int nb = gridDim.x;
+  block_store_many<kDq>(acc, partial, nb);
+  if (!last_block(ticket)) return;
+  __shared__ double red[kDq];
+  fold_many<kDq>(partial, nb, red);
+  if (threadIdx.x != 0) return;
+  const double rz = red[0], zz = red[1], tt = red[2];
+  st->iter = it;
+  const bool done = sqrt(zz) <= st->tol * fmax(sqrt(tt), 1e-30);
+  st->beta = st->rz > 0.0 && it > 1 ? rz / st->rz : 0.0;
+  if (rec) {
+    hist[3 * (it - 1)] = it > 1 ? st->alpha : 0.0;
+    hist[3 * (it - 1) + 1] = st->beta;
+    hist[3 * (it - 1) + 2] = rz;
+  }
+  st->rz = rz;
+  st->done = done ? 1 : 0;
+  if (!done && it >= st->k_max) st->err = 10;
+  if (!isfinite(rz)) st->err = 10;
+  st->cond = (!done && st->err == 0) ? 1 : 0;
+  if (defl) {
+    double mu[8];
+    chol_solve_l(d->l, k, red + 3, mu);
+    for (int c = 0; c < 8; ++c) d->mu[c] = c < k ? mu[c] : 0.0;
+  }
+}
+
+// p = z + beta p - W mu, and p by vertex; the WHILE condition.
+__global__ void k_dpcg_p(int n, const double* __restrict__ z, double* __restrict__ p, double* __restrict__ pv,
+                         const int* __restrict__ p2v, const hdk_pcg* st, const hdk_defl* d,
+                         const double* __restrict__ w, cudaGraphConditionalHandle handle, int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (use_handle && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, st->cond);
+  if (st->cond == 0) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t n3 = 3 * (size_t)n;
+  if (i >= (int)n3) return;
+  double v = z[i] + st->beta * p[i];
+  if (d->use && d->active) {
+    const int k = d->k;
+#pragma unroll
+    for (int c = 0; c < kBC; ++c)
+      if (c < k) v -= w[(size_t)c * n3 + i] * d->mu[c];
+  }
+  p[i] = v;
+  const int row = i / 3;
+  pv[3 * (size_t)__ldg(p2v + row) + (i - 3 * row)] = v;
+}
+
+// w_c = sum_j coef[c J + j] zhist_j (the Ritz vectors of a recorded solve).
+__global__ void k_ritz_combine(int n3, const double* __restrict__ zhist, const double* __restrict__ coef, int nj,
+                               int k, double* __restrict__ w) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  double acc[kBC];
+#pragma unroll
+  for (int c = 0; c < kBC; ++c) acc[c] = 0.0;
+  for (int j = 0; j < nj; ++j) {
+    const double zj = zhist[(size_t)j * n3 + i];
+#pragma unroll
+    for (int c = 0; c < kBC; ++c)
+      if (c < k) acc[c] += __ldg(coef + c * nj + j) * zj;
+  }
+#pragma unroll
+  for (int c = 0; c < kBC; ++c)
+    if (c < k) w[(size_t)c * n3 + i] = acc[c];
+}
+
+// W by vertex (the B apply's layout; fixed vertices stay 0).
+__global__ void k_scatter_cols(int n, int nv, int kmax, const double* __restrict__ w, double* __restrict__ wv,
+                               const int* __restrict__ p2v, const hdk_defl* d) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (!d->use) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t n3 = 3 * (size_t)n;
+  if (i >= (int)n3) return;
+  const int row = i / 3;
+  const size_t vtx = 3 * (size_t)__ldg(p2v + row) + (i - 3 * row);
+  for (int c = 0; c < kmax; ++c) wv[(size_t)c * 3 * nv + vtx] = c < d->k ? w[(size_t)c * n3 + i] : 0.0;
+}
+
+}  // namespace
+
+extern "C" {
+
+HDK_API size_t hdk_defl_partial_doubles(int n) {
+  const size_t nb = (3 * static_cast<size_t>(n) + kT - 1) / kT;
+  return static_cast<size_t>(kGram) * nb;
+}
+HDK_API int hdk_defl_gram(int n3, const double* w, const double* aw, double* partial, unsigned int* ticket,
+                          hdk_defl* d, void* stream) {
+  hdk::launch(k_defl_gram, dim3(nb(n3)), dim3(kT), 0, S(stream), n3, w, aw, partial, ticket, d);
+  return last();
+}
+HDK_API int hdk_defl_galerkin(int n3, double* x, double* r, const double* w, const double* aw, double* partial,
+                              unsigned int* ticket, hdk_defl* d, void* stream) {
+  hdk::launch(k_defl_dots, dim3(nb(n3)), dim3(kT), 0, S(stream), n3, static_cast<const double*>(r), w, partial, ticket,
+              d);
+  hdk::launch(k_defl_correct, dim3(nb(n3)), dim3(256), 0, S(stream), n3, x, r, w, aw, static_cast<const hdk_defl*>(d));
+  return last();
+}
+HDK_API int hdk_dpcg_rz(const hdk_factor* f, const double* r, double* z, const double* x, const double* aw,
+                        double* partial, unsigned int* ticket, hdk_pcg* st, hdk_defl* d, double* zhist,
+                        double* hist, void* stream) {
+  if (!f->tile_cta2) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_dpcg_rz, dim3(nb(3LL * f->n)), dim3(kT), 0, S(stream), *f, r, z, x, aw, partial, ticket, st, d, zhist,
+              hist);
+  return last();
+}
+HDK_API int hdk_dpcg_p(int n, const double* z, double* p, double* pv, const int* p2v, const hdk_pcg* st,
+                       const hdk_defl* d, const double* w, unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_dpcg_p, dim3(nb(3LL * n)), dim3(256), 0, S(stream), n, z, p, pv, p2v, st, d, w,
+              static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle ? 1 : 0);
+  return last();
+}
+HDK_API int hdk_ritz_combine(int n3, const double* zhist, const double* coef, int j, int k, double* w, void* stream) {
+  k_ritz_combine<<<nb(n3), 256, 0, S(stream)>>>(n3, zhist, coef, j, k, w);
+  return last();
+}
+HDK_API int hdk_scatter_cols(int n, int nv, int k, const double* w, double* wv, const int* p2v, const hdk_defl* d,
+                             void* stream) {
+  hdk::launch(k_scatter_cols, dim3(nb(3LL * n)), dim3(256), 0, S(stream), n, nv, k, w, wv, p2v, d);
+  return last();
+}
+
+}  // extern "C"

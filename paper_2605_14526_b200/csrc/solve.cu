@@ -39,14 +39,20 @@ constexpr int kWarps = 8;     // consumer warps
 constexpr int kThreads = 32 * (kWarps + 1);  // + one producer warp
 constexpr int kVals = HDK_CHUNK_VALS;
 constexpr int kSegs = HDK_CHUNK_SEGS;
-constexpr int kStages1 = 3;   // pass 1 ring depth (2 CTAs / SM)
+#ifndef HDK_STAGES1
+#define HDK_STAGES1 3
+#endif
+#ifndef HDK_STAGES2
+#define HDK_STAGES2 5
+#endif
+constexpr int kStages1 = HDK_STAGES1;   // pass 1 ring depth (2 CTAs / SM)
 // Pass 1 with W consumer warps: W = 8 runs 2 CTAs per SM with a 3-stage ring;
 // W = 16 (multi-column passes, which are compute-bound) 1 CTA per SM, 6 stages.
 template <int W>
 struct Pass1 {
   static constexpr int threads = 32 * (W + 1), min_blocks = W == 8 ? 2 : 1, stages = W == 8 ? kStages1 : 6;
 };
-constexpr int kStages2 = 5;   // pass 2 ring depth (1 CTA / SM)
+constexpr int kStages2 = HDK_STAGES2;   // pass 2 ring depth (1 CTA / SM)
 constexpr int kThreads2 = 32 * (kWarps + 2);  // pass 2: + copy warp + z-gather warp
 
 static_assert(kW == 256, "tile width is fixed by the factor layout");

@@ -75,6 +75,7 @@ SIGNATURES = {
     "hd_sim_backward_iterations": (C.c_int, [_VP]),
     "hd_sim_solve_free": (C.c_int, [_VP, _D, _D, _D]),
     "hd_sim_set_young": (C.c_int, [_VP, _D, C.c_size_t, C.c_int]),
+    "hd_sim_set_deflation": (C.c_int, [_VP, C.c_int]),
     "hd_sim_factor_nnz": (C.c_longlong, [_VP]),
     "hd_sim_free_count": (C.c_int, [_VP]),
     "hd_sim_solve_count": (C.c_longlong, [_VP]),
@@ -447,6 +448,9 @@ class Sim:
     def set_young(self, young, freeze_means: bool = False):
         y = _f64(young)
         self.L.check(self.L.lib.hd_sim_set_young(self.h, _ptr(y), y.size, 1 if freeze_means else 0))
+
+    def set_deflation(self, on: bool):
+        self.L.check(self.L.lib.hd_sim_set_deflation(self.h, 1 if on else 0))
 
     @property
     def factor_nnz(self):

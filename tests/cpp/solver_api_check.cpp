@@ -281,7 +281,11 @@ static void device_checks() {
     CHECK(sys.refactor_count() == 2);
     const GradientBundle g1 = backward_step(b.s.mesh, b.s.material, sys, c0, AdjointSeed{c0.q_star, c0.v_star},
                                             nullptr, 0.1);
-    CHECK((g1.dl_dq_t - g0.dl_dq_t).norm() == 0.0 && (g1.dl_de - g0.dl_de).norm() == 0.0);
+    // the same frame's adjoint again: equal to the CG stopping tolerance (the
+    // second solve is deflated with the first one's recycled Ritz vectors;
+    // HETERODYN_DEFLATION=0 makes repeated solves bitwise equal)
+    CHECK((g1.dl_dq_t - g0.dl_dq_t).norm() <= 1e-8 * g0.dl_dq_t.norm() &&
+          (g1.dl_de - g0.dl_de).norm() <= 1e-8 * g0.dl_de.norm());
   }
   {  // errors cross as heterodyn::Error with the reference's codes
     Block b({2, 2, 2}, -2.0, false, false, false, 0.0);
