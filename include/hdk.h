@@ -605,15 +605,16 @@ HDK_API int hdk_bcg_p(int n, int nv, const double* z, double* p, double* pv, con
                       unsigned long long cond_handle, void* stream);
 
 /* Deflated CG for the single backbone (pcg.cu, Saad et al.'s deflated PCG):
- * k <= 8 approximate slow eigenvectors W of A^{-1}(A - B) (Ritz vectors of an
+ * k <= HDK_DEFL_MAX approximate slow eigenvectors W of A^{-1}(A - B) (Ritz vectors of an
  * earlier backbone CG, recycled across time steps) are projected out: the
  * first iterate is Galerkin-corrected on span W and every search direction
  * is made (A - B)-orthogonal to W.  Same system, same stopping test; only the
- * iteration count changes.  W and AW = (A - B) W are [8][3n] in elimination
+ * iteration count changes.  W and AW = (A - B) W are [MAX][3n] in elimination
  * order; hist records (alpha, beta, r.z) and the z's of a recording solve. */
+#define HDK_DEFL_MAX 8
 typedef struct hdk_defl {
-  double l[64];          /* Cholesky factor of E = W^T (A - B) W, row r col c at [r * 8 + c] */
-  double mu[8], c[8];    /* per-iteration projection / first-iterate coefficients */
+  double l[HDK_DEFL_MAX * HDK_DEFL_MAX]; /* Cholesky factor of E = W^T (A - B) W, [r * MAX + c] */
+  double mu[HDK_DEFL_MAX], c[HDK_DEFL_MAX]; /* per-iteration projection / first-iterate coefficients */
   int k, use, active, rec, hcap, pad;
 } hdk_defl;
 HDK_API size_t hdk_defl_partial_doubles(int n);

@@ -65,11 +65,12 @@ void Engine::build_pcg_graph() {
         hdk_check_p(hdk_pcg_spmv(&a_ff_, xp_, pap_, pcg_, s), "A x0");
         hdk_check_p(hdk_pcg_r0(static_cast<int>(n3p), seedp_, pap_, rx_, pr_, s), "r0");
         // this step's (A - B) W, E = W^T (A - B) W, and the Galerkin first iterate
-        hdk_check_p(hdk_scatter_cols(n, scene_.mesh.nv, 8, D.w, D.wv, df_.p2v, D.d, s), "W by vertex");
-        hdk_check_p(hdk_bapply_cols_sorted(&dm_, dcomp_, D.wv, n3, D.ef8, 12 * ne, corner_pos_, &D.ones->cond, cstride,
-                                           8, s),
-                    "B W");
-        hdk_check_p(hdk_cpcg_apply_q(&dv_, &a_ff_, 8, D.ef8, 12 * ne, D.w, D.aw, D.ones, s), "(A - B) W");
+        hdk_check_p(hdk_scatter_cols(n, scene_.mesh.nv, HDK_DEFL_MAX, D.w, D.wv, df_.p2v, D.d, s), "W by vertex");
+        for (int g = 0; g < HDK_DEFL_MAX; g += 8)  // B W, eight columns per launch
+          hdk_check_p(hdk_bapply_cols_sorted(&dm_, dcomp_, D.wv + g * n3, n3, D.ef8 + g * 12 * ne, 12 * ne, corner_pos_,
+                                             &D.ones[g].cond, cstride, 8, s),
+                      "B W");
+        hdk_check_p(hdk_cpcg_apply_q(&dv_, &a_ff_, HDK_DEFL_MAX, D.ef8, 12 * ne, D.w, D.aw, D.ones, s), "(A - B) W");
         hdk_check_p(hdk_defl_gram(static_cast<int>(n3p), D.w, D.aw, D.part, D.ticket, D.d, s), "E = W^T A' W");
         hdk_check_p(hdk_defl_galerkin(static_cast<int>(n3p), xp_, pr_, D.w, D.aw, D.part, D.ticket, D.d, s),
                     "Galerkin first iterate");
@@ -187,8 +188,9 @@ bool Engine::run_pcg(int& iterations) {
     D.h->hcap = D.hcap;
     D.h->active = 0;
     cuda_check(cudaMemcpyAsync(&D.d->k, &D.h->k, 6 * sizeof(int), cudaMemcpyHostToDevice, st_), "deflation flags");
-    for (int c = 0; c < 8; ++c) D.h_ones[c].cond = (D.valid && c < D.k) ? 1 : 0;
-    cuda_check(cudaMemcpyAsync(D.ones, D.h_ones, 8 * sizeof(hdk_pcg), cudaMemcpyHostToDevice, st_), "deflation flags");
+    for (int c = 0; c < HDK_DEFL_MAX; ++c) D.h_ones[c].cond = (D.valid && c < D.k) ? 1 : 0;
+    cuda_check(cudaMemcpyAsync(D.ones, D.h_ones, HDK_DEFL_MAX * sizeof(hdk_pcg), cudaMemcpyHostToDevice, st_),
+               "deflation flags");
   }
   if (g.exec) {
     cuda_check(cudaGraphLaunch(g.exec, st_), "pcg");
@@ -256,22 +258,23 @@ void Engine::defl_alloc() {
                ne = scene_.mesh.ne;
   D.hcap = 200;
   D.d = A.alloc<hdk_defl>(1);
-  D.ones = A.alloc<hdk_pcg>(8);
-  D.w = A.alloc<double>(8 * n3p);
-  D.aw = A.alloc<double>(8 * n3p);
-  D.wv = A.alloc<double>(8 * n3);
-  D.ef8 = A.alloc<double>(8 * 12 * ne);
+  constexpr int K = HDK_DEFL_MAX;
+  D.ones = A.alloc<hdk_pcg>(K);
+  D.w = A.alloc<double>(K * n3p);
+  D.aw = A.alloc<double>(K * n3p);
+  D.wv = A.alloc<double>(K * n3);
+  D.ef8 = A.alloc<double>(K * 12 * ne);
   D.zhist = A.alloc<double>(static_cast<size_t>(D.hcap) * n3p);
   D.hist = A.alloc<double>(3 * static_cast<size_t>(D.hcap));
-  D.coef = A.alloc<double>(8 * static_cast<size_t>(D.hcap));
+  D.coef = A.alloc<double>(K * static_cast<size_t>(D.hcap));
   D.part = A.alloc<double>(std::max(hdk_defl_partial_doubles(hf_.n), hdk_bcg_partial_doubles(hf_.n)));
   D.ticket = A.alloc<unsigned int>(1);
   cuda_check(cudaMallocHost(&D.h, sizeof(hdk_defl)), "pinned deflation");
-  cuda_check(cudaMallocHost(&D.h_ones, 8 * sizeof(hdk_pcg)), "pinned deflation");
+  cuda_check(cudaMallocHost(&D.h_ones, K * sizeof(hdk_pcg)), "pinned deflation");
   cuda_check(cudaMallocHost(&D.h_hist, 3 * sizeof(double) * D.hcap), "pinned deflation");
-  cuda_check(cudaMallocHost(&D.h_coef, 8 * sizeof(double) * D.hcap), "pinned deflation");
+  cuda_check(cudaMallocHost(&D.h_coef, K * sizeof(double) * D.hcap), "pinned deflation");
   std::memset(D.h, 0, sizeof(hdk_defl));
-  std::memset(D.h_ones, 0, 8 * sizeof(hdk_pcg));
+  std::memset(D.h_ones, 0, K * sizeof(hdk_pcg));
 }
 
 namespace {
@@ -343,7 +346,12 @@ void Engine::defl_after_solve(int iterations, bool converged) {
   std::vector<int> order(m);
   for (int i = 0; i < m; ++i) order[i] = i;
   std::sort(order.begin(), order.end(), [&](int x, int y) { return ev[x] < ev[y]; });
-  const int k = std::min(8, m / 2);
+  static const int kmax = [] {  // HETERODYN_DEFLATION_K: recycled vectors (default and cap HDK_DEFL_MAX)
+    const char* e = std::getenv("HETERODYN_DEFLATION_K");
+    const int v = e ? std::atoi(e) : HDK_DEFL_MAX;
+    return std::max(1, std::min(v, HDK_DEFL_MAX));
+  }();
+  const int k = std::min(kmax, m / 2);
   for (int c = 0; c < k; ++c)
     for (int j = 0; j < m; ++j) {  // v_j = (-1)^j z_{j+1} / sqrt(r_{j+1}.z_{j+1})
       const double rz = D.h_hist[3 * j + 2];

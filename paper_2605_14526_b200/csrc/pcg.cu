@@ -1241,78 +1241,85 @@ HDK_API int hdk_bcg_p(int n, int nv, const double* z, double* p, double* pv, con
 // and mu = E^{-1} d (E = W^T A' W, A' = A - B, Cholesky factor precomputed),
 // and the p kernel subtracts W mu: p = z + beta p - W mu.  A recording solve
 // (no deflation) keeps its z's and (alpha, beta, r.z) for the host's Ritz
-// extraction.
+// extraction.  Up to kDK = HDK_DEFL_MAX vectors.
 namespace {
 
-constexpr int kDq = 3 + 8;  // r.z, |z|^2, |x + z|^2, (AW_k)^T z
+constexpr int kDK = HDK_DEFL_MAX;
+constexpr int kDq = 3 + kDK;  // r.z, |z|^2, |x + z|^2, (AW_k)^T z
 
 __device__ void chol_solve_l(const double* l, int k, const double* b, double* x) {  // L L^T x = b
-  double y[8];
+  double y[kDK];
   for (int i = 0; i < k; ++i) {
     double v = b[i];
-    for (int t = 0; t < i; ++t) v -= l[i * 8 + t] * y[t];
-    y[i] = v / l[i * 8 + i];
+    for (int t = 0; t < i; ++t) v -= l[i * kDK + t] * y[t];
+    y[i] = v / l[i * kDK + i];
   }
   for (int i = k - 1; i >= 0; --i) {
     double v = y[i];
-    for (int t = i + 1; t < k; ++t) v -= l[t * 8 + i] * y[t];
-    y[i] = v / l[i * 8 + i];
+    for (int t = i + 1; t < k; ++t) v -= l[t * kDK + i] * y[t];
+    y[i] = v / l[i * kDK + i];
   }
   for (int i = 0; i < k; ++i) x[i] = y[i];
 }
 
-// E = W^T A' W (upper triangle) and its Cholesky factor; active = factor ok.
+// E[j][c] = (w_j . aw_c + w_c . aw_j) / 2: one block per (j <= c) pair, fixed-order sums.
 __global__ void __launch_bounds__(kT) k_defl_gram(int n3, const double* __restrict__ w, const double* __restrict__ aw,
-                                                  double* partial, unsigned int* ticket, hdk_defl* d) {
+                                                  double* e, const hdk_defl* d) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
   if (!d->use) return;
   const int k = d->k;
-  const int i = blockIdx.x * kT + threadIdx.x;
-  double acc[kGram];
-#pragma unroll
-  for (int q = 0; q < kGram; ++q) acc[q] = 0.0;
-  if (i < n3) {
-    double wv[kBC], av[kBC];
-#pragma unroll
-    for (int c = 0; c < kBC; ++c) {
-      wv[c] = c < k ? w[(size_t)c * n3 + i] : 0.0;
-      av[c] = c < k ? aw[(size_t)c * n3 + i] : 0.0;
-    }
-#pragma unroll
-    for (int c = 0; c < kBC; ++c)
-#pragma unroll
-      for (int j = 0; j <= c; ++j) acc[tri(j, c)] = 0.5 * (wv[j] * av[c] + wv[c] * av[j]);  // symmetrised
+  int j = 0, idx = blockIdx.x;  // pair index -> (j, c), j <= c: ordered by j, then c = j .. kDK - 1
+  while (idx >= kDK - j) {
+    idx -= kDK - j;
+    ++j;
   }
-  const int nb = gridDim.x;
-  block_store_many<kGram>(acc, partial, nb);
-  if (!last_block(ticket)) return;
-  __shared__ double red[kGram];
-  fold_many<kGram>(partial, nb, red);
-  if (threadIdx.x != 0) return;
-  double l[64];
-  for (int q = 0; q < 64; ++q) l[q] = 0.0;
+  const int c = j + idx;
+  if (j >= k || c >= k) return;
+  double acc[1] = {0.0};
+  for (int i = threadIdx.x; i < n3; i += kT)
+    acc[0] += 0.5 * (w[(size_t)j * n3 + i] * aw[(size_t)c * n3 + i] + w[(size_t)c * n3 + i] * aw[(size_t)j * n3 + i]);
+  __shared__ double sm[kT / 32];
+  const double v = warp_sum(acc[0]);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < kT / 32; ++q) t += sm[q];
+    e[j * kDK + c] = t;
+    e[c * kDK + j] = t;
+  }
+}
+
+// Cholesky of E (one thread; once per step); active = factor ok.
+__global__ void k_defl_chol(const double* __restrict__ e, hdk_defl* d) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (!d->use || threadIdx.x != 0) return;
+  const int k = d->k;
+  double* l = d->l;
+  for (int q = 0; q < kDK * kDK; ++q) l[q] = 0.0;
   for (int r = 0; r < k; ++r)
-    for (int c = 0; c <= r; ++c) l[r * 8 + c] = red[tri(c, r)];
+    for (int c = 0; c <= r; ++c) l[r * kDK + c] = e[r * kDK + c];
   double dmax = 0.0;
-  for (int r = 0; r < k; ++r) dmax = fmax(dmax, l[r * 8 + r]);
+  for (int r = 0; r < k; ++r) dmax = fmax(dmax, l[r * kDK + r]);
   bool ok = k > 0;
   for (int j = 0; j < k && ok; ++j) {
-    double dj = l[j * 8 + j];
-    for (int t = 0; t < j; ++t) dj -= l[j * 8 + t] * l[j * 8 + t];
+    double dj = l[j * kDK + j];
+    for (int t = 0; t < j; ++t) dj -= l[j * kDK + t] * l[j * kDK + t];
     if (!(dj > 1e-12 * dmax)) {
       ok = false;
       break;
     }
     dj = sqrt(dj);
-    l[j * 8 + j] = dj;
+    l[j * kDK + j] = dj;
     for (int r = j + 1; r < k; ++r) {
-      double v = l[r * 8 + j];
-      for (int t = 0; t < j; ++t) v -= l[r * 8 + t] * l[j * 8 + t];
-      l[r * 8 + j] = v / dj;
+      double v = l[r * kDK + j];
+      for (int t = 0; t < j; ++t) v -= l[r * kDK + t] * l[j * kDK + t];
+      l[r * kDK + j] = v / dj;
     }
   }
-  for (int q = 0; q < 64; ++q) d->l[q] = l[q];
   d->active = ok ? 1 : 0;
 }
 
@@ -1324,18 +1331,18 @@ __global__ void __launch_bounds__(kT) k_defl_dots(int n3, const double* __restri
   if (!d->use || !d->active) return;
   const int k = d->k;
   const int i = blockIdx.x * kT + threadIdx.x;
-  double acc[kBC];
+  double acc[kDK];
 #pragma unroll
-  for (int c = 0; c < kBC; ++c) acc[c] = (i < n3 && c < k) ? w[(size_t)c * n3 + i] * r[i] : 0.0;
+  for (int c = 0; c < kDK; ++c) acc[c] = (i < n3 && c < k) ? w[(size_t)c * n3 + i] * r[i] : 0.0;
   const int nb = gridDim.x;
-  block_store_many<kBC>(acc, partial, nb);
+  block_store_many<kDK>(acc, partial, nb);
   if (!last_block(ticket)) return;
-  __shared__ double red[kBC];
-  fold_many<kBC>(partial, nb, red);
+  __shared__ double red[kDK];
+  fold_many<kDK>(partial, nb, red);
   if (threadIdx.x != 0) return;
-  double cc[8];
+  double cc[kDK];
   chol_solve_l(d->l, k, red, cc);
-  for (int c = 0; c < 8; ++c) d->c[c] = c < k ? cc[c] : 0.0;
+  for (int c = 0; c < kDK; ++c) d->c[c] = c < k ? cc[c] : 0.0;
 }
 
 __global__ void k_defl_correct(int n3, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ w,
@@ -1348,7 +1355,7 @@ __global__ void k_defl_correct(int n3, double* __restrict__ x, double* __restric
   const int k = d->k;
   double dx = 0.0, dr = 0.0;
 #pragma unroll
-  for (int c = 0; c < kBC; ++c)
+  for (int c = 0; c < kDK; ++c)
     if (c < k) {
       dx += w[(size_t)c * n3 + i] * d->c[c];
       dr += aw[(size_t)c * n3 + i] * d->c[c];
@@ -1390,7 +1397,7 @@ __global__ void __launch_bounds__(kT) k_dpcg_rz(hdk_factor f, const double* __re
     acc[1] = zi * zi;
     acc[2] = t * t;
 #pragma unroll
-    for (int c = 0; c < kBC; ++c) acc[3 + c] = c < k ? aw[(size_t)c * n3 + i] * zi : 0.0;
+    for (int c = 0; c < kDK; ++c) acc[3 + c] = c < k ? aw[(size_t)c * n3 + i] * zi : 0.0;
   }
   const int nb = gridDim.x;
   block_store_many<kDq>(acc, partial, nb);
@@ -1413,9 +1420,9 @@ __global__ void __launch_bounds__(kT) k_dpcg_rz(hdk_factor f, const double* __re
   if (!isfinite(rz)) st->err = 10;
   st->cond = (!done && st->err == 0) ? 1 : 0;
   if (defl) {
-    double mu[8];
+    double mu[kDK];
     chol_solve_l(d->l, k, red + 3, mu);
-    for (int c = 0; c < 8; ++c) d->mu[c] = c < k ? mu[c] : 0.0;
+    for (int c = 0; c < kDK; ++c) d->mu[c] = c < k ? mu[c] : 0.0;
   }
 }
 
@@ -1434,7 +1441,7 @@ __global__ void k_dpcg_p(int n, const double* __restrict__ z, double* __restrict
   if (d->use && d->active) {
     const int k = d->k;
 #pragma unroll
-    for (int c = 0; c < kBC; ++c)
+    for (int c = 0; c < kDK; ++c)
       if (c < k) v -= w[(size_t)c * n3 + i] * d->mu[c];
   }
   p[i] = v;
@@ -1447,17 +1454,17 @@ __global__ void k_ritz_combine(int n3, const double* __restrict__ zhist, const d
                                int k, double* __restrict__ w) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n3) return;
-  double acc[kBC];
+  double acc[kDK];
 #pragma unroll
-  for (int c = 0; c < kBC; ++c) acc[c] = 0.0;
+  for (int c = 0; c < kDK; ++c) acc[c] = 0.0;
   for (int j = 0; j < nj; ++j) {
     const double zj = zhist[(size_t)j * n3 + i];
 #pragma unroll
-    for (int c = 0; c < kBC; ++c)
+    for (int c = 0; c < kDK; ++c)
       if (c < k) acc[c] += __ldg(coef + c * nj + j) * zj;
   }
 #pragma unroll
-  for (int c = 0; c < kBC; ++c)
+  for (int c = 0; c < kDK; ++c)
     if (c < k) w[(size_t)c * n3 + i] = acc[c];
 }
 
@@ -1481,11 +1488,15 @@ extern "C" {
 
 HDK_API size_t hdk_defl_partial_doubles(int n) {
   const size_t nb = (3 * static_cast<size_t>(n) + kT - 1) / kT;
-  return static_cast<size_t>(kGram) * nb;
+  return static_cast<size_t>(kDq) * nb + static_cast<size_t>(kDK) * kDK;
 }
 HDK_API int hdk_defl_gram(int n3, const double* w, const double* aw, double* partial, unsigned int* ticket,
                           hdk_defl* d, void* stream) {
-  hdk::launch(k_defl_gram, dim3(nb(n3)), dim3(kT), 0, S(stream), n3, w, aw, partial, ticket, d);
+  (void)ticket;
+  double* e = partial;  // kDK x kDK
+  hdk::launch(k_defl_gram, dim3(kDK * (kDK + 1) / 2), dim3(kT), 0, S(stream), n3, w, aw, e,
+              static_cast<const hdk_defl*>(d));
+  hdk::launch(k_defl_chol, dim3(1), dim3(32), 0, S(stream), static_cast<const double*>(e), d);
   return last();
 }
 HDK_API int hdk_defl_galerkin(int n3, double* x, double* r, const double* w, const double* aw, double* partial,
