@@ -14,6 +14,8 @@
 // bitwise reproducible.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "../../include/hdk.h"
 #include "launch.cuh"
 
@@ -1262,7 +1264,9 @@ __device__ void chol_solve_l(const double* l, int k, const double* b, double* x)
   for (int i = 0; i < k; ++i) x[i] = y[i];
 }
 
-// E[j][c] = (w_j . aw_c + w_c . aw_j) / 2: one block per (j <= c) pair, fixed-order sums.
+// E[j][c] = (w_j . aw_c + w_c . aw_j) / 2: kGramSlices blocks per (j <= c)
+// pair, the slices folded in fixed order by k_defl_chol.
+constexpr int kGramSlices = 16;
 __global__ void __launch_bounds__(kT) k_defl_gram(int n3, const double* __restrict__ w, const double* __restrict__ aw,
                                                   double* e, const hdk_defl* d) {
   hdk::pdl_wait();
@@ -1276,8 +1280,8 @@ __global__ void __launch_bounds__(kT) k_defl_gram(int n3, const double* __restri
   }
   const int c = j + idx;
   if (j >= k || c >= k) return;
-  double acc[1] = {0.0};
-  for (int i = threadIdx.x; i < n3; i += kT)
+  double acc[1] = {0.0};  // slice blockIdx.y of the pair's dot product
+  for (int i = blockIdx.y * kT + threadIdx.x; i < n3; i += kGramSlices * kT)
     acc[0] += 0.5 * (w[(size_t)j * n3 + i] * aw[(size_t)c * n3 + i] + w[(size_t)c * n3 + i] * aw[(size_t)j * n3 + i]);
   __shared__ double sm[kT / 32];
   const double v = warp_sum(acc[0]);
@@ -1287,8 +1291,7 @@ __global__ void __launch_bounds__(kT) k_defl_gram(int n3, const double* __restri
     double t = 0.0;
 #pragma unroll
     for (int q = 0; q < kT / 32; ++q) t += sm[q];
-    e[j * kDK + c] = t;
-    e[c * kDK + j] = t;
+    e[kDK * kDK + (size_t)blockIdx.x * kGramSlices + blockIdx.y] = t;  // slice partials after the matrix
   }
 }
 
@@ -1300,8 +1303,13 @@ __global__ void k_defl_chol(const double* __restrict__ e, hdk_defl* d) {
   const int k = d->k;
   double* l = d->l;
   for (int q = 0; q < kDK * kDK; ++q) l[q] = 0.0;
-  for (int r = 0; r < k; ++r)
-    for (int c = 0; c <= r; ++c) l[r * kDK + c] = e[r * kDK + c];
+  for (int pj = 0, pair = 0; pj < kDK; ++pj)
+    for (int pc = pj; pc < kDK; ++pc, ++pair) {
+      if (pj >= k || pc >= k) continue;
+      double t = 0.0;
+      for (int q = 0; q < kGramSlices; ++q) t += e[kDK * kDK + (size_t)pair * kGramSlices + q];
+      l[pc * kDK + pj] = t;  // lower triangle (row pc >= column pj)
+    }
   double dmax = 0.0;
   for (int r = 0; r < k; ++r) dmax = fmax(dmax, l[r * kDK + r]);
   bool ok = k > 0;
@@ -1488,13 +1496,13 @@ extern "C" {
 
 HDK_API size_t hdk_defl_partial_doubles(int n) {
   const size_t nb = (3 * static_cast<size_t>(n) + kT - 1) / kT;
-  return static_cast<size_t>(kDq) * nb + static_cast<size_t>(kDK) * kDK;
+  return std::max(static_cast<size_t>(kDq) * nb, static_cast<size_t>(kDK) * kDK + kDK * (kDK + 1) / 2 * kGramSlices);
 }
 HDK_API int hdk_defl_gram(int n3, const double* w, const double* aw, double* partial, unsigned int* ticket,
                           hdk_defl* d, void* stream) {
   (void)ticket;
   double* e = partial;  // kDK x kDK
-  hdk::launch(k_defl_gram, dim3(kDK * (kDK + 1) / 2), dim3(kT), 0, S(stream), n3, w, aw, e,
+  hdk::launch(k_defl_gram, dim3(kDK * (kDK + 1) / 2, kGramSlices), dim3(kT), 0, S(stream), n3, w, aw, e,
               static_cast<const hdk_defl*>(d));
   hdk::launch(k_defl_chol, dim3(1), dim3(32), 0, S(stream), static_cast<const double*>(e), d);
   return last();

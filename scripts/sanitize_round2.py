@@ -1,7 +1,8 @@
 """compute-sanitizer target for the round-2 paths: the lockstep batch
-(hdk_seg_* kernels) with a device refactorization (refactor.cu) and a
-contact scene whose adjoint columns run eight per factor stream through the
-tensor-core row-dot pass."""
+(hdk_seg_* kernels) with a device refactorization (refactor.cu), a contact
+scene whose adjoint columns run by block CG eight per factor stream through
+the tensor-core passes, and a three-frame backward whose backbone solves
+record and then deflate with the recycled Ritz vectors (hdk_defl_*)."""
 import sys
 
 import numpy as np
@@ -25,4 +26,9 @@ sim.step(2)
 q = sim.positions()
 g = sim.backward(dl_dq_final=q, dl_dv_final=sim.velocities())
 print("contacts", sim.last_contact_count, "adjoint iterations", g["adjoint_iterations"])
+sim = lib.scene(scenes.block_scene(dims=(6, 4, 3), frames=3, contrast=10.0, alpha=0.02, gravity_z=-9.81)).sim()
+sim.record(True)
+sim.step(3)
+g = sim.backward(dl_dq_final=sim.positions(), dl_dv_final=sim.velocities())
+print("deflated backward, adjoint iterations", g["adjoint_iterations"])
 print("ok")
