@@ -587,6 +587,7 @@ HDK_API int hdk_cpcg_spmv(const hdk_csr* a, int columns, const double* p, double
  * alpha = (P^T Q)^{-1} (Z^T R), beta = (Z^T R)_old^{-1} (Z^T R)), the
  * columns' vectors as for hdk_cpcg_*.  err = -1: a Gram matrix lost
  * definiteness (the caller solves the batch column by column). */
+typedef struct hdk_defl hdk_defl; /* below */
 typedef struct hdk_bcg {
   double rz[64], rz_old[64], g[64], alpha[64], beta[64];
   double tol;
@@ -602,7 +603,7 @@ HDK_API int hdk_bcg_xr(int n3, double* x, double* r, const double* p, const doub
 HDK_API int hdk_bcg_zfold(const hdk_factor* f, const double* r, double* z, const double* x, double* partial,
                           unsigned int* ticket, hdk_bcg* st, void* stream);
 HDK_API int hdk_bcg_p(int n, int nv, const double* z, double* p, double* pv, const int* p2v, hdk_bcg* st, int* any,
-                      unsigned long long cond_handle, void* stream);
+                      const hdk_defl* d, const double* w, unsigned long long cond_handle, void* stream);
 
 /* Deflated CG for the single backbone (pcg.cu, Saad et al.'s deflated PCG):
  * k <= HDK_DEFL_MAX approximate slow eigenvectors W of A^{-1}(A - B) (Ritz vectors of an
@@ -612,11 +613,20 @@ HDK_API int hdk_bcg_p(int n, int nv, const double* z, double* p, double* pv, con
  * iteration count changes.  W and AW = (A - B) W are [MAX][3n] in elimination
  * order; hist records (alpha, beta, r.z) and the z's of a recording solve. */
 #define HDK_DEFL_MAX 8
-typedef struct hdk_defl {
+struct hdk_defl {
   double l[HDK_DEFL_MAX * HDK_DEFL_MAX]; /* Cholesky factor of E = W^T (A - B) W, [r * MAX + c] */
   double mu[HDK_DEFL_MAX], c[HDK_DEFL_MAX]; /* per-iteration projection / first-iterate coefficients */
-  int k, use, active, rec, hcap, pad;
-} hdk_defl;
+  double cm[HDK_DEFL_MAX * 8];           /* block CG columns: E^{-1} W^T V per column, [i * 8 + c] */
+  int k, use, active, rec, hcap, cols;   /* cols: deflate the contact columns' block CG too */
+};
+/* Block CG columns deflated by the frame's W: cm = E^{-1} Wsrc^T V for the
+ * batch's m columns (Wsrc = W for the first iterate's Galerkin correction,
+ * AW for the projection of Z); then X += W cm, R -= AW cm. */
+HDK_API size_t hdk_bdefl_partial_doubles(int n);
+HDK_API int hdk_bdefl_dots(int n3, const double* v, const double* wsrc, hdk_defl* d, const hdk_bcg* st,
+                           double* partial, unsigned int* tickets, void* stream);
+HDK_API int hdk_bdefl_correct(int n3, double* x, double* r, const double* w, const double* aw, const hdk_defl* d,
+                              const hdk_bcg* st, void* stream);
 HDK_API size_t hdk_defl_partial_doubles(int n);
 HDK_API int hdk_defl_gram(int n3, const double* w, const double* aw, double* partial, unsigned int* ticket,
                           hdk_defl* d, void* stream);

@@ -213,6 +213,7 @@ class Engine {
   // The same rows by block CG over the batch (the default; a batch of one row
   // and a lost-definiteness / cap failure go to solve_columns_pcg).
   bool solve_columns_bcg(const ContactFrame& c, int r0, int& iterations);
+  void column_deflation_setup();
   void build_columns_bcg();
   // All K columns of contact frame c through the kColumns slots, a finished
   // slot refilled with the next row (the loop exits when a column finishes);

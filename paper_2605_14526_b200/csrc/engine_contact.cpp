@@ -247,9 +247,12 @@ void Engine::backward_frame(int t, GradOut& out) {
       const char* e = std::getenv("HETERODYN_COLUMN_REFILL");
       return e && e[0] == '1';
     }();
-    if (refill) iters += solve_all_columns(*c);
-    else
+    if (refill) {
+      iters += solve_all_columns(*c);
+    } else {
+      if (use_pcg_) column_deflation_setup();
       for (int r = 0; r < k; r += kColumns) iters += solve_columns(*c, r);
+    }
     const size_t ms = hdk_contact_scratch_doubles(c->view.cap_k);
     if (ms > cM_len_) {
       if (cM_) cudaFree(cM_);

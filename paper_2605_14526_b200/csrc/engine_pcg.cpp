@@ -187,6 +187,7 @@ bool Engine::run_pcg(int& iterations) {
     D.h->rec = D.valid ? 0 : 1;
     D.h->hcap = D.hcap;
     D.h->active = 0;
+    D.h->cols = 0;
     cuda_check(cudaMemcpyAsync(&D.d->k, &D.h->k, 6 * sizeof(int), cudaMemcpyHostToDevice, st_), "deflation flags");
     for (int c = 0; c < HDK_DEFL_MAX; ++c) D.h_ones[c].cond = (D.valid && c < D.k) ? 1 : 0;
     cuda_check(cudaMemcpyAsync(D.ones, D.h_ones, HDK_DEFL_MAX * sizeof(hdk_pcg), cudaMemcpyHostToDevice, st_),

@@ -1166,8 +1166,8 @@ __global__ void __launch_bounds__(kT) k_bcg_zfold(hdk_factor f, size_t part2_str
 // P = Z + P beta (P = Z after the first solve) and P by vertex; block 0
 // publishes the run flag / WHILE condition.
 __global__ void k_bcg_p(int n, int nv, const double* __restrict__ z, double* __restrict__ p, double* __restrict__ pv,
-                        const int* __restrict__ p2v, const hdk_bcg* st, int* any, cudaGraphConditionalHandle handle,
-                        int use_handle) {
+                        const int* __restrict__ p2v, const hdk_bcg* st, int* any, const hdk_defl* d,
+                        const double* __restrict__ w, cudaGraphConditionalHandle handle, int use_handle) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
   const int on = st->cond != 0 && st->err == 0;
@@ -1186,6 +1186,11 @@ __global__ void k_bcg_p(int n, int nv, const double* __restrict__ z, double* __r
   for (int j = 0; j < kBC; ++j) old[j] = (!first && j < m) ? p[j * n3 + i] : 0.0;
   const int row = i / 3;
   const size_t vtx = 3 * (size_t)__ldg(p2v + row) + (i - 3 * row);
+  const bool defl = d && d->cols && d->use && d->active;  // P -= W E^{-1} (AW)^T Z
+  const int kd = defl ? d->k : 0;
+  double wv[kBC];
+#pragma unroll
+  for (int q = 0; q < kBC; ++q) wv[q] = q < kd ? w[(size_t)q * n3 + i] : 0.0;
 #pragma unroll
   for (int c = 0; c < kBC; ++c) {
     if (c >= m) break;
@@ -1194,6 +1199,9 @@ __global__ void k_bcg_p(int n, int nv, const double* __restrict__ z, double* __r
 #pragma unroll
       for (int j = 0; j < kBC; ++j) v += old[j] * st->beta[j * 8 + c];
     }
+#pragma unroll
+    for (int q = 0; q < kBC; ++q)
+      if (q < kd) v -= wv[q] * d->cm[q * 8 + c];
     p[c * n3 + i] = v;
     pv[(size_t)c * 3 * nv + vtx] = v;
   }
@@ -1230,8 +1238,9 @@ HDK_API int hdk_bcg_zfold(const hdk_factor* f, const double* r, double* z, const
   return last();
 }
 HDK_API int hdk_bcg_p(int n, int nv, const double* z, double* p, double* pv, const int* p2v, hdk_bcg* st, int* any,
-                      unsigned long long cond_handle, void* stream) {
-  hdk::launch(k_bcg_p, dim3(nb(3LL * n)), dim3(256), 0, S(stream), n, nv, z, p, pv, p2v, st, any,
+                      const hdk_defl* d, const double* w, unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_bcg_p, dim3(nb(3LL * n)), dim3(256), 0, S(stream), n, nv, z, p, pv, p2v,
+              static_cast<const hdk_bcg*>(st), any, d, w,
               static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle ? 1 : 0);
   return last();
 }
@@ -1476,6 +1485,61 @@ __global__ void k_ritz_combine(int n3, const double* __restrict__ zhist, const d
     if (c < k) w[(size_t)c * n3 + i] = acc[c];
 }
 
+// Block CG columns: cm[:, c] = E^{-1} Wsrc^T v_c for the batch's columns
+// (blockIdx.y = column, its own partials and ticket).
+__global__ void __launch_bounds__(kT) k_bdefl_dots(int n3, const double* __restrict__ v,
+                                                   const double* __restrict__ wsrc, hdk_defl* d, const hdk_bcg* st,
+                                                   double* partial, unsigned int* tickets) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  const int c = blockIdx.y;
+  if (!d->cols || !d->use || !d->active || c >= st->m || st->cond == 0) return;
+  const int k = d->k;
+  const int i = blockIdx.x * kT + threadIdx.x;
+  double acc[kDK];
+  const double vi = i < n3 ? v[(size_t)c * n3 + i] : 0.0;
+#pragma unroll
+  for (int q = 0; q < kDK; ++q) acc[q] = (i < n3 && q < k) ? wsrc[(size_t)q * n3 + i] * vi : 0.0;
+  const int nb = gridDim.x;
+  double* part = partial + (size_t)c * kDK * nb;
+  block_store_many<kDK>(acc, part, nb);
+  if (!last_block(tickets + c)) return;
+  __shared__ double red[kDK];
+  fold_many<kDK>(part, nb, red);
+  if (threadIdx.x != 0) return;
+  double out[kDK];
+  chol_solve_l(d->l, k, red, out);
+  for (int q = 0; q < kDK; ++q) d->cm[q * 8 + c] = q < k ? out[q] : 0.0;
+}
+
+// X_c += W cm[:, c], R_c -= AW cm[:, c].
+__global__ void k_bdefl_correct(int n3, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ w,
+                                const double* __restrict__ aw, const hdk_defl* d, const hdk_bcg* st) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  if (!d->cols || !d->use || !d->active || st->cond == 0) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  const int k = d->k, m = st->m;
+  double wv[kDK], av[kDK];
+#pragma unroll
+  for (int q = 0; q < kDK; ++q) {
+    wv[q] = q < k ? w[(size_t)q * n3 + i] : 0.0;
+    av[q] = q < k ? aw[(size_t)q * n3 + i] : 0.0;
+  }
+  for (int c = 0; c < m; ++c) {
+    double dx = 0.0, dr = 0.0;
+#pragma unroll
+    for (int q = 0; q < kDK; ++q) {
+      const double cq = d->cm[q * 8 + c];
+      dx += wv[q] * cq;
+      dr += av[q] * cq;
+    }
+    x[(size_t)c * n3 + i] += dx;
+    r[(size_t)c * n3 + i] -= dr;
+  }
+}
+
 // W by vertex (the B apply's layout; fixed vertices stay 0).
 __global__ void k_scatter_cols(int n, int nv, int kmax, const double* __restrict__ w, double* __restrict__ wv,
                                const int* __restrict__ p2v, const hdk_defl* d) {
@@ -1526,6 +1590,20 @@ HDK_API int hdk_dpcg_p(int n, const double* z, double* p, double* pv, const int*
                        const hdk_defl* d, const double* w, unsigned long long cond_handle, void* stream) {
   hdk::launch(k_dpcg_p, dim3(nb(3LL * n)), dim3(256), 0, S(stream), n, z, p, pv, p2v, st, d, w,
               static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle ? 1 : 0);
+  return last();
+}
+HDK_API size_t hdk_bdefl_partial_doubles(int n) {
+  const size_t nb = (3 * static_cast<size_t>(n) + kT - 1) / kT;
+  return static_cast<size_t>(8) * kDK * nb;
+}
+HDK_API int hdk_bdefl_dots(int n3, const double* v, const double* wsrc, hdk_defl* d, const hdk_bcg* st,
+                           double* partial, unsigned int* tickets, void* stream) {
+  hdk::launch(k_bdefl_dots, dim3(nb(n3), 8), dim3(kT), 0, S(stream), n3, v, wsrc, d, st, partial, tickets);
+  return last();
+}
+HDK_API int hdk_bdefl_correct(int n3, double* x, double* r, const double* w, const double* aw, const hdk_defl* d,
+                              const hdk_bcg* st, void* stream) {
+  hdk::launch(k_bdefl_correct, dim3(nb(n3)), dim3(256), 0, S(stream), n3, x, r, w, aw, d, st);
   return last();
 }
 HDK_API int hdk_ritz_combine(int n3, const double* zhist, const double* coef, int j, int k, double* w, void* stream) {
