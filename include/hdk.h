@@ -619,6 +619,29 @@ struct hdk_defl {
   double cm[HDK_DEFL_MAX * 8];           /* block CG columns: E^{-1} W^T V per column, [i * 8 + c] */
   int k, use, active, rec, hcap, cols;   /* cols: deflate the contact columns' block CG too */
 };
+/* Lockstep batch (segmented engine): the same deflation per sample.  W and
+ * AW are [MAX][n3] over the concatenated index space (sample s's vectors in
+ * its own range, the block-diagonal operator keeps them apart); per-sample
+ * E factors, coefficients and flags in hdk_sdefl; the global flags (k, use,
+ * rec, hcap) in the engine's hdk_defl. */
+typedef struct hdk_sdefl {
+  double l[HDK_DEFL_MAX * HDK_DEFL_MAX];
+  double mu[HDK_DEFL_MAX], c[HDK_DEFL_MAX];
+  int active, pad;
+} hdk_sdefl;
+HDK_API int hdk_sdefl_gram(int n3s, int count, const double* w, const double* aw, const hdk_defl* d,
+                           hdk_sdefl* ds, double* e, void* stream);
+HDK_API int hdk_sdefl_galerkin(int n3s, int count, double* x, double* r, const double* w, const double* aw,
+                               const hdk_defl* d, hdk_sdefl* ds, double* partial, unsigned int* tickets, void* stream);
+HDK_API int hdk_sdpcg_rz(int n3s, int count, const double* r, const double* z, const double* x, const double* aw,
+                         double* partial, unsigned int* tickets, hdk_pcg* st, const hdk_defl* d, hdk_sdefl* ds,
+                         double* zhist, double* hist, void* stream);
+HDK_API int hdk_sdpcg_p(int n3s, int n3, const double* z, double* p, double* pv, const int* p2v, const hdk_pcg* st,
+                        int count, int* any, const hdk_defl* d, const hdk_sdefl* ds, const double* w,
+                        unsigned long long cond_handle, void* stream);
+HDK_API int hdk_sritz_combine(int n3s, int n3, const double* zhist, const double* coef, int jmax, int k, double* w,
+                              void* stream);
+
 /* Block CG columns deflated by the frame's W: cm = E^{-1} Wsrc^T V for the
  * batch's m columns (Wsrc = W for the first iterate's Galerkin correction,
  * AW for the projection of Z); then X += W cm, R -= AW cm. */

@@ -206,9 +206,11 @@ Engine::Engine(const Scene& scene, const Vec* young, int solve_ctas, bool shared
   // HETERODYN_ADJOINT=aa keeps the reference's Anderson fixed point
   use_pcg_ = true;
   if (const char* ad = std::getenv("HETERODYN_ADJOINT")) use_pcg_ = std::string(ad) != "aa";
-  {  // recycled-subspace deflation of the backbone CG (HETERODYN_DEFLATION=0: off; hd_sim_set_deflation)
+  {  // recycled-subspace deflation of the backbone CG (HETERODYN_DEFLATION=0: off; hd_sim_set_deflation).
+     // Segmented (lockstep) engines: opt-in (=1) — C2-sized samples have few isolated slow modes
+     // (40-41 vs 41-43 solves) and the per-sample (A - B)W costs more than it saves
     const char* e = std::getenv("HETERODYN_DEFLATION");
-    defl_.on = !(e && e[0] == '0');
+    defl_.on = segs_ > 1 ? (e && e[0] == '1') : !(e && e[0] == '0');
   }
   const char* nc = std::getenv("HETERODYN_NO_COND_GRAPH");
   use_cond_ = !(nc && std::atoi(nc) != 0);
@@ -289,6 +291,8 @@ Engine::~Engine() {
                    ph_.col_iters, 1e3 * ph_.col_ms / std::max(1LL, ph_.col_iters), ph_.col_real_iters);
     std::fprintf(stderr, "  CG backbone fallbacks to Anderson (p.q <= 0): %lld; block-CG batches solved column by column: %lld\n",
                  pcg_fallbacks, bcg_fallbacks);
+    std::fprintf(stderr, "  deflation: %lld recorded subspaces, %lld deflated solves (k = %d, recorded solve %d iterations)\n",
+                 defl_.refreshes, defl_.deflated_solves, defl_.k, defl_.plain_iters);
   }
   for (cudaEvent_t e : ph_.ev)
     if (e) cudaEventDestroy(e);

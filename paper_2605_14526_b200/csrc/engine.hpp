@@ -300,6 +300,7 @@ class Engine {
     bool on = false;        // HETERODYN_DEFLATION != 0 and a single (non-segmented) engine
     bool valid = false;     // W holds Ritz vectors
     int k = 0, hcap = 0, plain_iters = 0;
+    int misses = 0, cooldown = 0;  // deflated solves that did not pay; plain solves left before retrying
     hdk_defl* d = nullptr;  // device state
     hdk_defl* h = nullptr;  // pinned mirror (the int fields are uploaded per solve)
     hdk_pcg* ones = nullptr;  // run flags of the 8-column B apply / q kernels
@@ -308,7 +309,12 @@ class Engine {
            *coef = nullptr, *part = nullptr, *h_hist = nullptr, *h_coef = nullptr;
     unsigned int* ticket = nullptr;
     long long refreshes = 0, deflated_solves = 0;
+    // lockstep batch (per sample): E factors / coefficients, E scratch, per-sample tickets
+    hdk_sdefl* ds = nullptr;
+    double* e = nullptr;
+    unsigned int* tickets = nullptr;
   } defl_;
+  void defl_after_solve_seg();
   void defl_alloc();
 
   void defl_after_solve(int iterations, bool converged);

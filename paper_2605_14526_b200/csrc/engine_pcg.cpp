@@ -139,6 +139,45 @@ void Engine::build_pcg_graph_seg() {
   const int S = segs_, ns = dseg_.n, n3s = 3 * dseg_.n, n3 = static_cast<int>(n3p);
   hdk_factor fs = df_;
   fs.run_flag = any_;
+  if (defl_.on) {  // per-sample recycled deflation (the single engine's scheme, sample by sample)
+    defl_alloc();
+    Deflation& D = defl_;
+    const size_t nvv = 3 * static_cast<size_t>(scene_.mesh.nv), ne = scene_.mesh.ne;
+    const int cstride = static_cast<int>(sizeof(hdk_pcg) / sizeof(int));
+    auto pre_d = [&] {
+      hdk_check_p(hdk_spcg_init(pcg_, S, 1e-10, 500, any_, s), "pcg init");
+      hdk_check_p(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
+      hdk_check_p(hdk_gather_perm(&dv_, x_, nullptr, xp_, s), "x0 in elimination order");
+      hdk_check_p(hdk_bapply(&dm_, dcomp_, x_, ef_, s), "B x0");
+      hdk_check_p(hdk_gather_pp(&dv_, nullptr, ef_, rx_, nullptr, s), "R(x0)");
+      hdk_check_p(hdk_spcg_spmv(&a_ff_, ns, xp_, pap_, pcg_, s), "A x0");
+      hdk_check_p(hdk_pcg_r0(n3, seedp_, pap_, rx_, pr_, s), "r0");
+      hdk_check_p(hdk_scatter_cols(hf_.n, scene_.mesh.nv, HDK_DEFL_MAX, D.w, D.wv, df_.p2v, D.d, s), "W by vertex");
+      for (int g = 0; g < HDK_DEFL_MAX; g += 8)
+        hdk_check_p(hdk_bapply_cols_sorted(&dm_, dcomp_, D.wv + g * nvv, nvv, D.ef8 + g * 12 * ne, 12 * ne,
+                                           corner_pos_, &D.ones[g].cond, cstride, 8, s),
+                    "B W");
+      hdk_check_p(hdk_cpcg_apply_q(&dv_, &a_ff_, HDK_DEFL_MAX, D.ef8, 12 * ne, D.w, D.aw, D.ones, s), "(A - B) W");
+      hdk_check_p(hdk_sdefl_gram(n3s, S, D.w, D.aw, D.d, D.ds, D.e, s), "E per sample");
+      hdk_check_p(hdk_sdefl_galerkin(n3s, S, xp_, pr_, D.w, D.aw, D.d, D.ds, pcg_part_, D.tickets, s),
+                  "Galerkin first iterates");
+      hdk_check_p(hdk_apply_inverse3_perm(&fs, pr_, pz_, s), "z0 = A^-1 r0");
+      hdk_check_p(hdk_sdpcg_rz(n3s, S, pr_, pz_, xp_, D.aw, pcg_part_, pcg_ticket_, pcg_, D.d, D.ds, D.zhist, D.hist, s),
+                  "rz");
+      hdk_check_p(hdk_sdpcg_p(n3s, n3, pz_, pp_, ppv_, df_.p2v, pcg_, S, any_, D.d, D.ds, D.w, 0ULL, s), "p");
+    };
+    auto body_d = [&](unsigned long long handle) {
+      hdk_check_p(hdk_bapply_sorted(&dm_, dcomp_, ppv_, ef_, corner_pos_, any_, s), "B p");
+      hdk_check_p(hdk_spcg_apply(&dv_, &a_ff_, ns, S, ef_, pp_, pq_, pcg_part_, pcg_ticket_, pcg_, s), "q = (A - B) p");
+      hdk_check_p(hdk_spcg_xr(n3s, n3, xp_, pr_, pp_, pq_, pcg_, s), "x, r");
+      hdk_check_p(hdk_apply_inverse3_perm(&fs, pr_, pz_, s), "z = A^-1 r");
+      hdk_check_p(hdk_sdpcg_rz(n3s, S, pr_, pz_, xp_, D.aw, pcg_part_, pcg_ticket_, pcg_, D.d, D.ds, D.zhist, D.hist, s),
+                  "rz");
+      hdk_check_p(hdk_sdpcg_p(n3s, n3, pz_, pp_, ppv_, df_.p2v, pcg_, S, any_, D.d, D.ds, D.w, handle, s), "p + any");
+    };
+    build_loop_graph(st_, use_cond_, pre_d, body_d, [] {}, *pgraph_);
+    return;
+  }
   auto pre = [&] {
     hdk_check_p(hdk_spcg_init(pcg_, S, 1e-10, 500, any_, s), "pcg init");
     hdk_check_p(hdk_gather_perm(&dv_, seed_, nullptr, seedp_, s), "seed in elimination order");
@@ -182,9 +221,11 @@ bool Engine::run_pcg(int& iterations) {
   }
   if (defl_.on && defl_.d) {  // this solve: deflate with W, or record the Ritz data for W
     Deflation& D = defl_;
+    const bool pause = !D.valid && D.cooldown > 0;
+    if (pause) --D.cooldown;
     D.h->use = D.valid ? 1 : 0;
     D.h->k = D.valid ? D.k : 0;
-    D.h->rec = D.valid ? 0 : 1;
+    D.h->rec = (D.valid || pause) ? 0 : 1;
     D.h->hcap = D.hcap;
     D.h->active = 0;
     D.h->cols = 0;
@@ -231,6 +272,7 @@ bool Engine::run_pcg(int& iterations) {
     if (segs_ > 1) seg_sample_iterations += 1 + h.iter;
   }
   if (defl_.on && defl_.d && segs_ == 1) defl_after_solve(h_pcg_[0].iter, h_pcg_[0].done != 0);
+  if (defl_.on && defl_.d && segs_ > 1) defl_after_solve_seg();
   hdk_check_p(hdk_pcg_final(hf_.n, xp_, pz_, x_, df_.p2v, st_), "x = x + z");
   iterations = 1 + most;  // the first solve x0 = A^{-1} s and one solve per CG step (the slowest sample)
   kernel_launches += g.counts[0] + static_cast<long long>(g.counts[1]) * most + 2;
@@ -257,8 +299,13 @@ void Engine::defl_alloc() {
   DevArena& A = *mem_;
   const size_t n3p = 3 * static_cast<size_t>(hf_.n), n3 = 3 * static_cast<size_t>(scene_.mesh.nv),
                ne = scene_.mesh.ne;
-  D.hcap = 200;
+  D.hcap = segs_ > 1 ? 160 : 200;
   D.d = A.alloc<hdk_defl>(1);
+  if (segs_ > 1) {
+    D.ds = A.alloc<hdk_sdefl>(segs_);
+    D.e = A.alloc<double>(static_cast<size_t>(segs_) * HDK_DEFL_MAX * HDK_DEFL_MAX);
+    D.tickets = A.alloc<unsigned int>(segs_);
+  }
   constexpr int K = HDK_DEFL_MAX;
   D.ones = A.alloc<hdk_pcg>(K);
   D.w = A.alloc<double>(K * n3p);
@@ -266,14 +313,14 @@ void Engine::defl_alloc() {
   D.wv = A.alloc<double>(K * n3);
   D.ef8 = A.alloc<double>(K * 12 * ne);
   D.zhist = A.alloc<double>(static_cast<size_t>(D.hcap) * n3p);
-  D.hist = A.alloc<double>(3 * static_cast<size_t>(D.hcap));
-  D.coef = A.alloc<double>(K * static_cast<size_t>(D.hcap));
+  D.hist = A.alloc<double>(3 * static_cast<size_t>(D.hcap) * segs_);
+  D.coef = A.alloc<double>(K * static_cast<size_t>(D.hcap) * segs_);
   D.part = A.alloc<double>(std::max(hdk_defl_partial_doubles(hf_.n), hdk_bcg_partial_doubles(hf_.n)));
   D.ticket = A.alloc<unsigned int>(1);
   cuda_check(cudaMallocHost(&D.h, sizeof(hdk_defl)), "pinned deflation");
   cuda_check(cudaMallocHost(&D.h_ones, K * sizeof(hdk_pcg)), "pinned deflation");
-  cuda_check(cudaMallocHost(&D.h_hist, 3 * sizeof(double) * D.hcap), "pinned deflation");
-  cuda_check(cudaMallocHost(&D.h_coef, K * sizeof(double) * D.hcap), "pinned deflation");
+  cuda_check(cudaMallocHost(&D.h_hist, 3 * sizeof(double) * D.hcap * segs_), "pinned deflation");
+  cuda_check(cudaMallocHost(&D.h_coef, K * sizeof(double) * D.hcap * segs_), "pinned deflation");
   std::memset(D.h, 0, sizeof(hdk_defl));
   std::memset(D.h_ones, 0, K * sizeof(hdk_pcg));
 }
@@ -328,9 +375,23 @@ void Engine::defl_after_solve(int iterations, bool converged) {
   if (D.valid) {
     ++D.deflated_solves;
     cuda_check(cudaMemcpy(&D.h->active, &D.d->active, sizeof(int), cudaMemcpyDeviceToHost), "deflation state");
-    if (!D.h->active || iterations > (85 * D.plain_iters) / 100) D.valid = false;
+    // Keep W while it pays: a deflated solve costs (A - B)W and E up front and
+    // 8 more dots / axpys per iteration, so it must save >= 15 % of the
+    // recorded solve's iterations (C3: 34 of 53; C1, 5k tets: 22 of 24 does
+    // not pay).  A miss drops W (the next solve records afresh, in case the
+    // state drifted); two misses in a row pause deflation for 64 solves.
+    if (!D.h->active || iterations > (85 * D.plain_iters) / 100) {
+      D.valid = false;
+      if (++D.misses >= 2) {
+        D.cooldown = 64;
+        D.misses = 0;
+      }
+    } else {
+      D.misses = 0;
+    }
     return;
   }
+  if (D.cooldown > 0) return;  // a plain solve during the pause: nothing recorded
   const int J = iterations;  // z_1 .. z_J recorded (rz calls)
   if (!converged || J < 6 || J > D.hcap) return;
   cuda_check(cudaMemcpy(D.h_hist, D.hist, 3 * sizeof(double) * J, cudaMemcpyDeviceToHost), "Ritz history");
@@ -363,6 +424,64 @@ void Engine::defl_after_solve(int iterations, bool converged) {
   D.k = k;
   D.valid = true;
   D.plain_iters = J;
+  ++D.refreshes;
+}
+
+// The lockstep batch's version: every sample records together and gets its
+// own Ritz vectors (in its range of W); k is the smallest over the samples.
+void Engine::defl_after_solve_seg() {
+  Deflation& D = defl_;
+  const int S = segs_;
+  int most = 0;
+  bool all_conv = true;
+  for (int s = 0; s < S; ++s) {
+    most = std::max(most, h_pcg_[s].iter);
+    all_conv = all_conv && h_pcg_[s].done != 0;
+  }
+  if (D.valid) {
+    ++D.deflated_solves;
+    static const bool verbose = std::getenv("HETERODYN_DEFLATION_LOG") != nullptr;
+    if (verbose) std::fprintf(stderr, "[deflation] lockstep solve: %d iterations (recorded %d)\n", most, D.plain_iters);
+    if (most > (95 * D.plain_iters) / 100) D.valid = false;
+    return;
+  }
+  if (!all_conv || most < 6 || most > D.hcap) return;
+  cuda_check(cudaMemcpy(D.h_hist, D.hist, 3 * sizeof(double) * D.hcap * S, cudaMemcpyDeviceToHost), "Ritz history");
+  int kmin = HDK_DEFL_MAX, jmax = 0;
+  for (int s = 0; s < S; ++s) {
+    jmax = std::max(jmax, h_pcg_[s].iter - 1);
+    kmin = std::min(kmin, (h_pcg_[s].iter - 1) / 2);
+  }
+  if (kmin < 1) return;
+  std::fill(D.h_coef, D.h_coef + static_cast<size_t>(S) * HDK_DEFL_MAX * jmax, 0.0);
+  std::vector<double> T, ev, Y;
+  std::vector<int> order;
+  for (int s = 0; s < S; ++s) {
+    const double* h = D.h_hist + static_cast<size_t>(s) * 3 * D.hcap;
+    const int m = h_pcg_[s].iter - 1;
+    T.assign(static_cast<size_t>(m) * m, 0.0);
+    for (int j = 0; j < m; ++j) {
+      const double a = h[3 * (j + 1)], b = h[3 * (j + 1) + 1];
+      const double ap = j > 0 ? h[3 * j] : 0.0, bp = j > 0 ? h[3 * j + 1] : 0.0;
+      if (!(a > 0.0) || !(b >= 0.0)) return;
+      T[j * m + j] = 1.0 / a + (j > 0 ? bp / ap : 0.0);
+      if (j + 1 < m) T[j * m + j + 1] = T[(j + 1) * m + j] = std::sqrt(b) / a;
+    }
+    jacobi_eigen(T, m, ev, Y);
+    order.resize(m);
+    for (int i = 0; i < m; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int x, int y) { return ev[x] < ev[y]; });
+    double* cs = D.h_coef + static_cast<size_t>(s) * HDK_DEFL_MAX * jmax;
+    for (int c = 0; c < kmin; ++c)
+      for (int j = 0; j < m; ++j)
+        cs[c * jmax + j] = Y[j * m + order[c]] * ((j & 1) ? -1.0 : 1.0) / std::sqrt(h[3 * j + 2]);
+  }
+  cuda_check(cudaMemcpyAsync(D.coef, D.h_coef, sizeof(double) * S * HDK_DEFL_MAX * jmax, cudaMemcpyHostToDevice, st_),
+             "Ritz coefficients");
+  hdk_check_p(hdk_sritz_combine(3 * dseg_.n, 3 * hf_.n, D.zhist, D.coef, jmax, kmin, D.w, st_), "Ritz vectors");
+  D.k = kmin;
+  D.valid = true;
+  D.plain_iters = most;
   ++D.refreshes;
 }
 

@@ -1617,3 +1617,312 @@ HDK_API int hdk_scatter_cols(int n, int nv, int k, const double* w, double* wv, 
 }
 
 }  // extern "C"
+
+// ---- deflated CG for the lockstep batch (per sample) ----------------------------
+namespace {
+
+constexpr int kSDq = 3 + HDK_DEFL_MAX;
+
+__device__ void chol_solve_s(const double* l, int k, const double* b, double* x) {  // L L^T x = b
+  constexpr int K = HDK_DEFL_MAX;
+  double y[K];
+  for (int i = 0; i < k; ++i) {
+    double v = b[i];
+    for (int t = 0; t < i; ++t) v -= l[i * K + t] * y[t];
+    y[i] = v / l[i * K + i];
+  }
+  for (int i = k - 1; i >= 0; --i) {
+    double v = y[i];
+    for (int t = i + 1; t < k; ++t) v -= l[t * K + i] * y[t];
+    y[i] = v / l[i * K + i];
+  }
+  for (int i = 0; i < k; ++i) x[i] = y[i];
+}
+
+// E_s[j][c] for every sample: block (pair, sample), fixed-order sums over the sample's range.
+__global__ void __launch_bounds__(kT) k_sdefl_gram(int n3s, const double* __restrict__ w, const double* __restrict__ aw,
+                                                   const hdk_defl* d, double* e) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  constexpr int K = HDK_DEFL_MAX;
+  if (!d->use) return;
+  const int k = d->k, smp = blockIdx.y;
+  int j = 0, idx = blockIdx.x;
+  while (idx >= K - j) {
+    idx -= K - j;
+    ++j;
+  }
+  const int c = j + idx;
+  if (j >= k || c >= k) return;
+  const size_t n3 = (size_t)n3s * gridDim.y, i0 = (size_t)smp * n3s;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n3s; i += kT) {
+    const size_t g = i0 + i;
+    acc += 0.5 * (w[j * n3 + g] * aw[c * n3 + g] + w[c * n3 + g] * aw[j * n3 + g]);
+  }
+  __shared__ double sm[kT / 32];
+  const double v = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < kT / 32; ++q) t += sm[q];
+    e[(size_t)smp * K * K + j * K + c] = t;
+    e[(size_t)smp * K * K + c * K + j] = t;
+  }
+}
+
+// One thread per sample: Cholesky of E_s, active_s.
+__global__ void k_sdefl_chol(int count, const double* __restrict__ e, const hdk_defl* d, hdk_sdefl* ds) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  constexpr int K = HDK_DEFL_MAX;
+  const int smp = blockIdx.x * blockDim.x + threadIdx.x;
+  if (smp >= count) return;
+  hdk_sdefl* o = ds + smp;
+  if (!d->use) {
+    o->active = 0;
+    return;
+  }
+  const int k = d->k;
+  double* l = o->l;
+  const double* es = e + (size_t)smp * K * K;
+  for (int q = 0; q < K * K; ++q) l[q] = 0.0;
+  for (int r = 0; r < k; ++r)
+    for (int c = 0; c <= r; ++c) l[r * K + c] = es[r * K + c];
+  double dmax = 0.0;
+  for (int r = 0; r < k; ++r) dmax = fmax(dmax, l[r * K + r]);
+  bool ok = k > 0;
+  for (int j = 0; j < k && ok; ++j) {
+    double dj = l[j * K + j];
+    for (int t = 0; t < j; ++t) dj -= l[j * K + t] * l[j * K + t];
+    if (!(dj > 1e-12 * dmax)) {
+      ok = false;
+      break;
+    }
+    dj = sqrt(dj);
+    l[j * K + j] = dj;
+    for (int r = j + 1; r < k; ++r) {
+      double v = l[r * K + j];
+      for (int t = 0; t < j; ++t) v -= l[r * K + t] * l[j * K + t];
+      l[r * K + j] = v / dj;
+    }
+  }
+  o->active = ok ? 1 : 0;
+}
+
+// Galerkin first iterate per sample: c_s = E_s^{-1} W_s^T r_s (grid (kSRB, S)).
+__global__ void __launch_bounds__(kT) k_sdefl_dots(int n3s, const double* __restrict__ r, const double* __restrict__ w,
+                                                   const hdk_defl* d, hdk_sdefl* ds, double* partial,
+                                                   unsigned int* tickets) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  constexpr int K = HDK_DEFL_MAX;
+  const int smp = blockIdx.y;
+  if (!d->use || !ds[smp].active) return;
+  const int k = d->k;
+  const size_t n3 = (size_t)n3s * gridDim.y;
+  double acc[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) acc[q] = 0.0;
+  const size_t i0 = (size_t)smp * n3s, i1 = i0 + n3s;
+  for (size_t i = i0 + blockIdx.x * kT + threadIdx.x; i < i1; i += (size_t)kSRB * kT) {
+    const double ri = r[i];
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      if (q < k) acc[q] += w[q * n3 + i] * ri;
+  }
+  double* part = partial + (size_t)smp * HDK_SEG_PSTRIDE;
+  block_store_rb<K>(acc, part);
+  if (!last_block(tickets + smp)) return;
+  if (threadIdx.x >= 32) return;
+  double red[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) red[q] = fold_rb(part, q);
+  if (threadIdx.x != 0) return;
+  double cc[K];
+  chol_solve_s(ds[smp].l, k, red, cc);
+  for (int q = 0; q < K; ++q) ds[smp].c[q] = q < k ? cc[q] : 0.0;
+}
+
+__global__ void k_sdefl_correct(int n3s, int n3, double* __restrict__ x, double* __restrict__ r,
+                                const double* __restrict__ w, const double* __restrict__ aw, const hdk_defl* d,
+                                const hdk_sdefl* ds) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  constexpr int K = HDK_DEFL_MAX;
+  if (!d->use) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  const hdk_sdefl& o = ds[i / n3s];
+  if (!o.active) return;
+  const int k = d->k;
+  double dx = 0.0, dr = 0.0;
+#pragma unroll
+  for (int q = 0; q < K; ++q)
+    if (q < k) {
+      dx += w[(size_t)q * n3 + i] * o.c[q];
+      dr += aw[(size_t)q * n3 + i] * o.c[q];
+    }
+  x[i] += dx;
+  r[i] -= dr;
+}
+
+// k_spcg_rz plus d_s = (AW_s)^T z_s, mu_s = E_s^{-1} d_s, and the recording.
+__global__ void __launch_bounds__(kT) k_sdpcg_rz(int n3s, const double* __restrict__ r, const double* __restrict__ z,
+                                                 const double* __restrict__ x, const double* __restrict__ aw,
+                                                 double* partial, unsigned int* tickets, hdk_pcg* sts,
+                                                 const hdk_defl* d, hdk_sdefl* ds, double* __restrict__ zhist,
+                                                 double* hist) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  constexpr int K = HDK_DEFL_MAX;
+  const int smp = blockIdx.y;
+  hdk_pcg* st = sts + smp;
+  if (st->cond == 0) return;
+  const bool defl = d->use && ds[smp].active;
+  const int k = defl ? d->k : 0;
+  const int it = st->iter + 1;
+  const bool rec = d->rec && it <= d->hcap;
+  const size_t n3 = (size_t)n3s * gridDim.y;
+  double acc[kSDq];
+#pragma unroll
+  for (int q = 0; q < kSDq; ++q) acc[q] = 0.0;
+  const size_t i0 = (size_t)smp * n3s, i1 = i0 + n3s;
+  for (size_t i = i0 + blockIdx.x * kT + threadIdx.x; i < i1; i += (size_t)kSRB * kT) {
+    const double zi = z[i], t = x[i] + zi;
+    if (rec) zhist[(size_t)(it - 1) * n3 + i] = zi;
+    acc[0] += r[i] * zi;
+    acc[1] += zi * zi;
+    acc[2] += t * t;
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      if (q < k) acc[3 + q] += aw[q * n3 + i] * zi;
+  }
+  double* part = partial + (size_t)smp * HDK_SEG_PSTRIDE;
+  block_store_rb<kSDq>(acc, part);
+  if (!last_block(tickets + smp)) return;
+  if (threadIdx.x >= 32) return;
+  double red[kSDq];
+#pragma unroll
+  for (int q = 0; q < kSDq; ++q) red[q] = fold_rb(part, q);
+  if (threadIdx.x != 0) return;
+  const double rz = red[0], zz = red[1], tt = red[2];
+  st->iter = it;
+  const bool done = sqrt(zz) <= st->tol * fmax(sqrt(tt), 1e-30);
+  st->beta = st->rz > 0.0 && it > 1 ? rz / st->rz : 0.0;
+  if (rec) {
+    double* h = hist + (size_t)smp * 3 * d->hcap;
+    h[3 * (it - 1)] = it > 1 ? st->alpha : 0.0;
+    h[3 * (it - 1) + 1] = st->beta;
+    h[3 * (it - 1) + 2] = rz;
+  }
+  st->rz = rz;
+  st->done = done ? 1 : 0;
+  if (!done && it >= st->k_max) st->err = 10;
+  if (!isfinite(rz)) st->err = 10;
+  st->cond = (!done && st->err == 0) ? 1 : 0;
+  if (defl) {
+    double mu[K];
+    chol_solve_s(ds[smp].l, k, red + 3, mu);
+    for (int q = 0; q < K; ++q) ds[smp].mu[q] = q < k ? mu[q] : 0.0;
+  }
+}
+
+// k_spcg_p minus W_s mu_s.
+__global__ void k_sdpcg_p(int n3s, int n3, const double* __restrict__ z, double* __restrict__ p,
+                          double* __restrict__ pv, const int* __restrict__ p2v, const hdk_pcg* st, int count, int* any,
+                          const hdk_defl* d, const hdk_sdefl* ds, const double* __restrict__ w,
+                          cudaGraphConditionalHandle handle, int use_handle) {
+  hdk::pdl_wait();
+  hdk::pdl_trigger();
+  constexpr int K = HDK_DEFL_MAX;
+  if (blockIdx.x == 0) {
+    int on = 0;
+    for (int s = threadIdx.x; s < count; s += blockDim.x) on |= (st[s].cond != 0 && st[s].err == 0) ? 1 : 0;
+    const int a = __syncthreads_or(on);
+    if (threadIdx.x == 0) {
+      *any = a;
+      if (use_handle) cudaGraphSetConditional(handle, a);
+    }
+  }
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  const int smp = i / n3s;
+  const hdk_pcg& c = st[smp];
+  if (c.cond == 0) return;
+  double v = z[i] + c.beta * p[i];
+  if (d->use && ds[smp].active) {
+    const int k = d->k;
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      if (q < k) v -= w[(size_t)q * n3 + i] * ds[smp].mu[q];
+  }
+  p[i] = v;
+  const int row = i / 3;
+  pv[3 * (size_t)__ldg(p2v + row) + (i - 3 * row)] = v;
+}
+
+// w_c[i] = sum_j coef[s][c][j] zhist_j[i], s = sample of i (coefficients zero past a sample's own count).
+__global__ void k_sritz_combine(int n3s, int n3, const double* __restrict__ zhist, const double* __restrict__ coef,
+                                int jmax, int k, double* __restrict__ w) {
+  constexpr int K = HDK_DEFL_MAX;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  const double* cs = coef + (size_t)(i / n3s) * K * jmax;
+  double acc[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) acc[q] = 0.0;
+  for (int j = 0; j < jmax; ++j) {
+    const double zj = zhist[(size_t)j * n3 + i];
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      if (q < k) acc[q] += __ldg(cs + q * jmax + j) * zj;
+  }
+#pragma unroll
+  for (int q = 0; q < K; ++q)
+    if (q < k) w[(size_t)q * n3 + i] = acc[q];
+}
+
+}  // namespace
+
+extern "C" {
+
+HDK_API int hdk_sdefl_gram(int n3s, int count, const double* w, const double* aw, const hdk_defl* d, hdk_sdefl* ds,
+                           double* e, void* stream) {
+  constexpr int K = HDK_DEFL_MAX;
+  hdk::launch(k_sdefl_gram, dim3(K * (K + 1) / 2, count), dim3(kT), 0, S(stream), n3s, w, aw, d, e);
+  hdk::launch(k_sdefl_chol, dim3((count + 63) / 64), dim3(64), 0, S(stream), count, static_cast<const double*>(e), d,
+              ds);
+  return last();
+}
+HDK_API int hdk_sdefl_galerkin(int n3s, int count, double* x, double* r, const double* w, const double* aw,
+                               const hdk_defl* d, hdk_sdefl* ds, double* partial, unsigned int* tickets, void* stream) {
+  hdk::launch(k_sdefl_dots, dim3(kSRB, count), dim3(kT), 0, S(stream), n3s, static_cast<const double*>(r), w, d, ds,
+              partial, tickets);
+  hdk::launch(k_sdefl_correct, dim3(nb(static_cast<long long>(n3s) * count)), dim3(256), 0, S(stream), n3s,
+              n3s * count, x, r, w, aw, d, static_cast<const hdk_sdefl*>(ds));
+  return last();
+}
+HDK_API int hdk_sdpcg_rz(int n3s, int count, const double* r, const double* z, const double* x, const double* aw,
+                         double* partial, unsigned int* tickets, hdk_pcg* st, const hdk_defl* d, hdk_sdefl* ds,
+                         double* zhist, double* hist, void* stream) {
+  hdk::launch(k_sdpcg_rz, dim3(kSRB, count), dim3(kT), 0, S(stream), n3s, r, z, x, aw, partial, tickets, st, d, ds,
+              zhist, hist);
+  return last();
+}
+HDK_API int hdk_sdpcg_p(int n3s, int n3, const double* z, double* p, double* pv, const int* p2v, const hdk_pcg* st,
+                        int count, int* any, const hdk_defl* d, const hdk_sdefl* ds, const double* w,
+                        unsigned long long cond_handle, void* stream) {
+  hdk::launch(k_sdpcg_p, dim3(nb(n3)), dim3(256), 0, S(stream), n3s, n3, z, p, pv, p2v, st, count, any, d, ds, w,
+              static_cast<cudaGraphConditionalHandle>(cond_handle), cond_handle ? 1 : 0);
+  return last();
+}
+HDK_API int hdk_sritz_combine(int n3s, int n3, const double* zhist, const double* coef, int jmax, int k, double* w,
+                              void* stream) {
+  k_sritz_combine<<<nb(n3), 256, 0, S(stream)>>>(n3s, n3, zhist, coef, jmax, k, w);
+  return last();
+}
+
+}  // extern "C"
