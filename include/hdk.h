@@ -617,6 +617,7 @@ struct hdk_defl {
   double l[HDK_DEFL_MAX * HDK_DEFL_MAX]; /* Cholesky factor of E = W^T (A - B) W, [r * MAX + c] */
   double mu[HDK_DEFL_MAX], c[HDK_DEFL_MAX]; /* per-iteration projection / first-iterate coefficients */
   double cm[HDK_DEFL_MAX * 8];           /* block CG columns: E^{-1} W^T V per column, [i * 8 + c] */
+  double einv[HDK_DEFL_MAX * HDK_DEFL_MAX]; /* E^{-1} (the per-iteration projection is a mat-vec) */
   int k, use, active, rec, hcap, cols;   /* cols: deflate the contact columns' block CG too */
 };
 /* Lockstep batch (segmented engine): the same deflation per sample.  W and

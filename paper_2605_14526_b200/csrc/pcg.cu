@@ -1337,6 +1337,14 @@ __global__ void k_defl_chol(const double* __restrict__ e, hdk_defl* d) {
       l[r * kDK + j] = v / dj;
     }
   }
+  if (ok) {  // E^{-1} column by column (the per-iteration mu = E^{-1} d becomes a mat-vec)
+    double col[kDK];
+    for (int c = 0; c < kDK; ++c) {
+      for (int r = 0; r < kDK; ++r) col[r] = (r == c) ? 1.0 : 0.0;
+      if (c < k) chol_solve_l(l, k, col, col);
+      for (int r = 0; r < kDK; ++r) d->einv[r * kDK + c] = (r < k && c < k) ? col[r] : 0.0;
+    }
+  }
   d->active = ok ? 1 : 0;
 }
 
@@ -1421,6 +1429,12 @@ __global__ void __launch_bounds__(kT) k_dpcg_rz(hdk_factor f, const double* __re
   if (!last_block(ticket)) return;
   __shared__ double red[kDq];
   fold_many<kDq>(partial, nb, red);
+  if (defl && threadIdx.x < kDK) {  // mu = E^{-1} d, one row per thread
+    double m = 0.0;
+#pragma unroll
+    for (int j = 0; j < kDK; ++j) m += d->einv[threadIdx.x * kDK + j] * red[3 + j];
+    d->mu[threadIdx.x] = threadIdx.x < k ? m : 0.0;
+  }
   if (threadIdx.x != 0) return;
   const double rz = red[0], zz = red[1], tt = red[2];
   st->iter = it;
@@ -1436,11 +1450,6 @@ __global__ void __launch_bounds__(kT) k_dpcg_rz(hdk_factor f, const double* __re
   if (!done && it >= st->k_max) st->err = 10;
   if (!isfinite(rz)) st->err = 10;
   st->cond = (!done && st->err == 0) ? 1 : 0;
-  if (defl) {
-    double mu[kDK];
-    chol_solve_l(d->l, k, red + 3, mu);
-    for (int c = 0; c < kDK; ++c) d->mu[c] = c < k ? mu[c] : 0.0;
-  }
 }
 
 // p = z + beta p - W mu, and p by vertex; the WHILE condition.
