@@ -104,7 +104,17 @@ typedef struct hdk_factor {
   const int* first2;      /* grid2+1: first chunk of pass-2 CTA b */
   const int* tile_cta2;   /* 2*n_tiles: first and last pass-2 CTA touching tile t */
   const int2* vfold;      /* nv: (first tile-partial slot of the vertex's column, slot count; 0 if fixed) */
+  /* fp32 copy of the value stream for preconditioner-only solves (the
+   * adjoint CG: an approximate SPD preconditioner leaves CG's answer and
+   * its residuals exact).  chunk32: the chunks with offsets into sval32
+   * (each chunk padded to a multiple of 4 values for 16-byte bulk copies);
+   * use32 != 0 makes hdk_apply_inverse3_* stream sval32. */
+  const float* sval32;
+  const hdk_chunk* chunk32;
+  int use32;
 } hdk_factor;
+/* sval32[chunk32[c].off + i] = (float) sval[chunk[c].off + i], padding 0. */
+HDK_API int hdk_factor_to_fp32(const hdk_factor* f, float* sval32, const hdk_chunk* chunk32, void* stream);
 
 /* Scalar CSR in elimination order (a_free / a_free_fixed, factor.hpp:98-99). */
 typedef struct hdk_csr {

@@ -508,6 +508,11 @@ void Engine::fill_factor_values(double* sv) {
   cuda_check(cudaStreamSynchronize(st_), "device factor values");
 }
 
+void Engine::refresh_fp32() {
+  if (!df_.sval32) return;
+  hdk_check(hdk_factor_to_fp32(&df_, const_cast<float*>(df_.sval32), df_.chunk32, st_), "fp32 factor values");
+}
+
 void Engine::build_factor_device() {
   fmem_ = std::make_unique<DevArena>();
   DevArena& A = *fmem_;
@@ -535,6 +540,23 @@ void Engine::build_factor_device() {
   hdk_chunk* ch = A.alloc<hdk_chunk>(F.chunks.size());
   DevArena::copy_h2d(ch, F.chunks.data(), sizeof(ChunkDesc) * F.chunks.size());
   df_.chunk = ch;
+  if (const char* e32 = std::getenv("HETERODYN_PCG_FP32"); e32 && e32[0] == '1') {
+    // fp32 copy of the stream for the adjoint CG's preconditioner solves
+    // (opt-in, engine_pcg.cpp); chunks padded to 4 values
+    std::vector<ChunkDesc> c32(F.chunks.begin(), F.chunks.end());
+    long long off = 0;
+    for (ChunkDesc& c : c32) {
+      c.off = off;
+      c.len = (c.len + 3) & ~3;
+      off += c.len;
+    }
+    hdk_chunk* ch32 = A.alloc<hdk_chunk>(c32.size());
+    DevArena::copy_h2d(ch32, c32.data(), sizeof(ChunkDesc) * c32.size());
+    df_.chunk32 = ch32;
+    df_.sval32 = A.alloc<float>(static_cast<size_t>(std::max(off, 4LL)));
+    df_.use32 = 0;  // exact solves by default; the CG's factor view sets it
+    refresh_fp32();
+  }
   df_.tile_chunk = A.upload(F.tile_chunk);
   df_.row_pslot = A.upload(F.row_pslot);
   df_.n_pslot = F.row_pslot.back();
@@ -1367,6 +1389,7 @@ void Engine::set_young(const Vec& young, bool freeze) {
     hf_ = std::move(nf);
     upload_material();
     fill_factor_values(const_cast<double*>(df_.sval));
+    refresh_fp32();
     DevArena::copy_h2d(const_cast<double*>(a_ff_.val), hf_.a_ff.val.data(), hf_.a_ff.val.size() * sizeof(double));
     if (!hf_.a_fd.val.empty()) {
       DevArena::copy_h2d(const_cast<double*>(a_fd_.val), hf_.a_fd.val.data(), hf_.a_fd.val.size() * sizeof(double));

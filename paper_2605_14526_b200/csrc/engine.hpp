@@ -116,6 +116,8 @@ class Engine {
   // Turns recycled-subspace deflation of the backbone CG on or off for the
   // following solves and drops the recycled subspace (engine_pcg.cpp).
   void set_deflation(bool on);
+  // The fp32 copy of the factor values (the adjoint CG's preconditioner), re-made after every S' build.
+  void refresh_fp32();
   // young: optional per-element Young's moduli replacing the scene's (a
   // parameter sample of a batch); the factor is built once for them.
   // solve_ctas: cap on the CTAs of each solve pass (0 = one resident wave).

@@ -17,6 +17,22 @@ namespace hdb {
 
 namespace {
 void hdk_check_p(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
+
+// The CG's preconditioner solves z = A^{-1} r may stream the fp32 copy of S'
+// (hdk_factor::use32): CG converges to the solution of (A - B) x = s for any
+// fixed SPD preconditioner, and M = S~^T S~ with S~ the fp32-rounded factor is
+// one; its residuals r and the operator applies stay fp64, so x is exact to
+// the stopping test and x + z differs from x + A^{-1} r by (M - A^{-1}) r,
+// ~1e-7 of a quantity the test has already made 1e-10 of x.  The forward
+// solves, the first backbone solve and the contact columns' warm starts keep
+// the fp64 factor.  Opt-in (HETERODYN_PCG_FP32=1): the passes are not
+// bandwidth-bound at these sizes (C3: 35.9 / 28.4 us with half the bytes vs
+// 36.5 / 31.5 us), and the rounded preconditioner costs iterations (C3 36.9 vs
+// 34.0 solves per step: 221 vs 230 steps/s; C5 1383 vs 1330 sample-steps/s).
+bool pcg_fp32_preconditioner() {
+  const char* e = std::getenv("HETERODYN_PCG_FP32");
+  return e && e[0] == '1';
+}
 }  // namespace
 
 void Engine::build_pcg_graph() {
@@ -42,6 +58,7 @@ void Engine::build_pcg_graph() {
   const int n = hf_.n;
   hdk_factor fs = df_;
   fs.run_flag = &pcg_->cond;
+  fs.use32 = pcg_fp32_preconditioner() ? 1 : 0;
   // fused stages (default): q = (A - B) p over a grid covering the rows once,
   // and z folded from the solve's tile partials in the r.z kernel (no
   // separate x-fold launch); HETERODYN_PCG_FUSED=0: the first form
@@ -139,6 +156,7 @@ void Engine::build_pcg_graph_seg() {
   const int S = segs_, ns = dseg_.n, n3s = 3 * dseg_.n, n3 = static_cast<int>(n3p);
   hdk_factor fs = df_;
   fs.run_flag = any_;
+  fs.use32 = pcg_fp32_preconditioner() ? 1 : 0;
   if (defl_.on) {  // per-sample recycled deflation (the single engine's scheme, sample by sample)
     defl_alloc();
     Deflation& D = defl_;

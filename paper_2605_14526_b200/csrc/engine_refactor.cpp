@@ -142,6 +142,7 @@ void Engine::refactor_device_values() {
   hdk_check_r(hdk_mf_factor(&R.mf, a_ff_.val, R.lx, R.d, R.dis, R.err, s), "multifrontal LDL^T");
   if (trace) cuda_check(cudaEventRecord(ev[1], st_), "event");
   hdk_check_r(hdk_inverse_values(&R.build, const_cast<double*>(df_.sval), s), "S' values");
+  refresh_fp32();
   if (trace) {
     cuda_check(cudaEventRecord(ev[2], st_), "event");
     cuda_check(cudaEventSynchronize(ev[2]), "event");

@@ -218,17 +218,17 @@ struct ChunkInfo {
   int nseg, tile, seg0, pad;
 };
 
-template <int S>
+template <int S, typename V = double>
 struct Ring {
-  double vals[S][kVals];
+  V vals[S][kVals];
   hdk_seg segs[S][kSegs];
   ChunkInfo info[S];  // written by the producer before its arrive (release)
   uint64_t full[S];
   uint64_t empty[S];
 };
 
-template <int S>
-__device__ __forceinline__ void ring_init(Ring<S>& r, int consumers = kWarps) {
+template <int S, typename V>
+__device__ __forceinline__ void ring_init(Ring<S, V>& r, int consumers = kWarps) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&r.full[s], 1);
@@ -256,12 +256,27 @@ __device__ __forceinline__ bool after_prefill(const hdk_factor& f, FullBars& ful
   return true;
 }
 
-template <int S>
-__device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_beg, int c_end, bool reverse) {
+// The value stream a pass reads: fp64 (exact solves) or the fp32 copy
+// (preconditioner-only solves, hdk_factor::use32), with its chunk table.
+template <typename V>
+__device__ __forceinline__ const V* value_stream(const hdk_factor& f);
+template <>
+__device__ __forceinline__ const double* value_stream<double>(const hdk_factor& f) { return f.sval; }
+template <>
+__device__ __forceinline__ const float* value_stream<float>(const hdk_factor& f) { return f.sval32; }
+template <typename V>
+__device__ __forceinline__ const hdk_chunk* chunk_table(const hdk_factor& f) {
+  return sizeof(V) == 8 ? f.chunk : f.chunk32;
+}
+
+template <int S, typename V>
+__device__ __forceinline__ void produce(const hdk_factor& f, Ring<S, V>& r, int c_beg, int c_end, bool reverse) {
   if ((threadIdx.x & 31) != 0) return;
   const int n = c_end - c_beg;
   auto chunk_at = [&](int k) { return reverse ? c_end - 1 - k : c_beg + k; };
-  hdk_chunk nxt = n > 0 ? f.chunk[chunk_at(0)] : hdk_chunk{};
+  const hdk_chunk* ctab = chunk_table<V>(f);
+  const V* vsrc = value_stream<V>(f);
+  hdk_chunk nxt = n > 0 ? ctab[chunk_at(0)] : hdk_chunk{};
   const uint64_t pol = policy_evict_first();
   const int pre = n < S ? n : S;
   if (pre == 0 && !after_prefill<S>(f, r.full, 0)) return;
@@ -269,7 +284,7 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
     if (k == pre && !after_prefill<S>(f, r.full, pre)) return;
     const int st = k % S;
     const hdk_chunk ch = nxt;
-    if (k + 1 < n) nxt = f.chunk[chunk_at(k + 1)];  // descriptor prefetch, off the critical path
+    if (k + 1 < n) nxt = ctab[chunk_at(k + 1)];  // descriptor prefetch, off the critical path
     long long* tr = g_chunk_trace;
     const long long t_ready = tr ? sm_clock() : 0;
     if (k >= S) mbar_wait(&r.empty[st], ((k / S) - 1) & 1);
@@ -279,11 +294,11 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
     }
     fence_proxy_async();
     r.info[st] = ChunkInfo{ch.nseg, ch.tile, ch.seg0, 0};
-    const uint32_t vb = static_cast<uint32_t>(ch.len) * 8u, sb = static_cast<uint32_t>(ch.nseg) * 16u;
+    const uint32_t vb = static_cast<uint32_t>(ch.len) * static_cast<uint32_t>(sizeof(V)), sb = static_cast<uint32_t>(ch.nseg) * 16u;
     mbar_expect_tx(&r.full[st], vb + sb);
     if (vb) {
-      if (f.l2_hint) bulk_g2s_hint(r.vals[st], f.sval + ch.off, vb, &r.full[st], pol);
-      else bulk_g2s(r.vals[st], f.sval + ch.off, vb, &r.full[st]);
+      if (f.l2_hint) bulk_g2s_hint(r.vals[st], vsrc + ch.off, vb, &r.full[st], pol);
+      else bulk_g2s(r.vals[st], vsrc + ch.off, vb, &r.full[st]);
     }
     bulk_g2s(r.segs[st], f.seg + ch.seg0, sb, &r.full[st]);
   }
@@ -293,9 +308,9 @@ __device__ __forceinline__ void produce(const hdk_factor& f, Ring<S>& r, int c_b
 // Pass 2 ring: as Ring, plus the z rows of each staged chunk's segments,
 // gathered into shared memory by the producer warp (zfull) so the consumers
 // never wait on a global load.
-template <int S, int R>
+template <int S, int R, typename V = double>
 struct Ring2 {
-  double vals[S][kVals];
+  V vals[S][kVals];
   hdk_seg segs[S][kSegs];
   double zs[S][kSegs][3 * R];
   ChunkInfo info[S];
@@ -304,8 +319,8 @@ struct Ring2 {
   uint64_t empty[S];
 };
 
-template <int S, int R>
-__device__ __forceinline__ void ring2_init(Ring2<S, R>& r) {
+template <int S, int R, typename V>
+__device__ __forceinline__ void ring2_init(Ring2<S, R, V>& r) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&r.full[s], 1);
@@ -322,8 +337,8 @@ __device__ __forceinline__ void ring2_init(Ring2<S, R>& r) {
 // gathers the z rows of its segments into zs with asynchronous 8-byte copies
 // that complete on zfull, so neither the stream nor the consumers wait on a
 // dependent global load.
-template <int S, int R>
-__device__ __forceinline__ void gather_z(const hdk_factor& f, Ring2<S, R>& r, int n) {
+template <int S, int R, typename V>
+__device__ __forceinline__ void gather_z(const hdk_factor& f, Ring2<S, R, V>& r, int n) {
   const int lane = threadIdx.x & 31;
   for (int j = 0; j < n; ++j) {
     const int st = j % S;
@@ -343,11 +358,13 @@ __device__ __forceinline__ void gather_z(const hdk_factor& f, Ring2<S, R>& r, in
   }
 }
 
-template <int S, int R>
-__device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S, R>& r, int c_beg, int c_end) {
+template <int S, int R, typename V>
+__device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S, R, V>& r, int c_beg, int c_end) {
   if ((threadIdx.x & 31) != 0) return;
   const int n = c_end - c_beg;
-  hdk_chunk nxt = n > 0 ? f.chunk[c_end - 1] : hdk_chunk{};
+  const hdk_chunk* ctab = chunk_table<V>(f);
+  const V* vsrc = value_stream<V>(f);
+  hdk_chunk nxt = n > 0 ? ctab[c_end - 1] : hdk_chunk{};
   const uint64_t pol = policy_evict_first();
   const int pre = n < S ? n : S;
   if (pre == 0 && !after_prefill<S>(f, r.full, 0)) return;
@@ -355,15 +372,15 @@ __device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S, R>& r, int
     if (k == pre && !after_prefill<S>(f, r.full, pre)) return;
     const int st = k % S;
     const hdk_chunk ch = nxt;
-    if (k + 1 < n) nxt = f.chunk[c_end - 2 - k];
+    if (k + 1 < n) nxt = ctab[c_end - 2 - k];
     if (k >= S) mbar_wait(&r.empty[st], ((k / S) - 1) & 1);
     fence_proxy_async();
     r.info[st] = ChunkInfo{ch.nseg, ch.tile, ch.seg0, 0};
-    const uint32_t vb = static_cast<uint32_t>(ch.len) * 8u, sb = static_cast<uint32_t>(ch.nseg) * 16u;
+    const uint32_t vb = static_cast<uint32_t>(ch.len) * static_cast<uint32_t>(sizeof(V)), sb = static_cast<uint32_t>(ch.nseg) * 16u;
     mbar_expect_tx(&r.full[st], vb + sb);
     if (vb) {
-      if (f.l2_hint) bulk_g2s_hint(r.vals[st], f.sval + ch.off, vb, &r.full[st], pol);
-      else bulk_g2s(r.vals[st], f.sval + ch.off, vb, &r.full[st]);
+      if (f.l2_hint) bulk_g2s_hint(r.vals[st], vsrc + ch.off, vb, &r.full[st], pol);
+      else bulk_g2s(r.vals[st], vsrc + ch.off, vb, &r.full[st]);
     }
     bulk_g2s(r.segs[st], f.seg + ch.seg0, sb, &r.full[st]);
   }
@@ -371,20 +388,20 @@ __device__ __forceinline__ void stream2(const hdk_factor& f, Ring2<S, R>& r, int
 }
 
 // ---- pass 1 ------------------------------------------------------------------
-template <bool kDry, int R, int W>
-__device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<Pass1<W>::stages>& ring,
+template <bool kDry, int R, int W, typename V>
+__device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<Pass1<W>::stages, V>& ring,
                                                const double* __restrict__ rhs, int c_beg, int c_end);
 
 // R columns: consumer warp w serves column w / (W / R) and every (W / R)-th
 // segment pair of each staged chunk, so the chunk is streamed once for all R
 // columns and a warp still holds one column's right-hand side tile.
-template <bool kDry = false, int R = 1, int W = kWarps>  // kDry: stream only (microbenchmarks)
+template <bool kDry = false, int R = 1, int W = kWarps, typename V = double>  // kDry: stream only (microbenchmarks)
 __global__ void __launch_bounds__(Pass1<W>::threads, Pass1<W>::min_blocks) k_rowdot(hdk_factor f,
                                                                                    const double* __restrict__ rhs) {
   constexpr int S = Pass1<W>::stages;
   hdk::pdl_trigger();  // the producer prefills before the PDL wait; consumers wait below
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Ring<S>& ring = *reinterpret_cast<Ring<S>*>(smem_raw);
+  Ring<S, V>& ring = *reinterpret_cast<Ring<S, V>*>(smem_raw);
   const int warp = threadIdx.x >> 5;
   unsigned long long* trace = HDK_TRACE_PTR;
   if (trace && threadIdx.x == 0) trace[2 * blockIdx.x] = globaltimer();
@@ -397,15 +414,15 @@ __global__ void __launch_bounds__(Pass1<W>::threads, Pass1<W>::min_blocks) k_row
   }
   HDK_TRACED_WAIT(hdk::kTrRowdot);
   if (f.run_flag && *f.run_flag == 0) return;
-  rowdot_consume<kDry, R, W>(f, ring, rhs, c_beg, c_end);
+  rowdot_consume<kDry, R, W, V>(f, ring, rhs, c_beg, c_end);
   if (trace) {
     asm volatile("bar.sync 1, %0;" ::"r"(32 * W) : "memory");
     if (threadIdx.x == 0) trace[2 * blockIdx.x + 1] = globaltimer();
   }
 }
 
-template <bool kDry, int R, int W>
-__device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<Pass1<W>::stages>& ring,
+template <bool kDry, int R, int W, typename V>
+__device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<Pass1<W>::stages, V>& ring,
                                                const double* __restrict__ rhs, int c_beg, int c_end) {
   constexpr int S = Pass1<W>::stages;
   constexpr int WPC = W / R;  // consumer warps per column
@@ -431,7 +448,7 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<Pass1<W
         b2[m] = ok ? __ldg(rhs + 3 * (size_t)col + 2) : 0.0;
       }
     }
-    const double* vals = ring.vals[st];
+    const V* vals = ring.vals[st];
     // segment pair p = {2p, 2p+1} of the chunk goes to warp (seg0/2 + p) mod 8
     // (balanced over chunks); the two dot products share one shuffle tree.
     // The stage is released as soon as the warp's last pair sits in
@@ -445,14 +462,14 @@ __device__ __forceinline__ void rowdot_consume(const hdk_factor& f, Ring<Pass1<W
       const hdk_seg sb = hasb ? ring.segs[st][ib] : sa;
       const int la = sa.clo_len & 0xffff, ha = la + (sa.clo_len >> 16);
       const int lb = sb.clo_len & 0xffff, hb = hasb ? lb + (sb.clo_len >> 16) : lb;
-      const double* va = vals + sa.coff - la;
-      const double* vb = vals + sb.coff - lb;
+      const V* va = vals + sa.coff - la;
+      const V* vb = vals + sb.coff - lb;
       double wa[kM], wb[kM];
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
-        wa[m] = (cl >= la && cl < ha) ? va[cl] : 0.0;
-        wb[m] = (cl >= lb && cl < hb) ? vb[cl] : 0.0;
+        wa[m] = (cl >= la && cl < ha) ? static_cast<double>(va[cl]) : 0.0;
+        wb[m] = (cl >= lb && cl < hb) ? static_cast<double>(vb[cl]) : 0.0;
       }
       if (pi + WPC >= npair) {
         __syncwarp();
@@ -866,6 +883,14 @@ __global__ void __launch_bounds__(32 * (kWarpsMma + 1), 1) k_rowdot_mma_nb(hdk_f
   }
 }
 
+// fp32 copy of the value stream, chunk by chunk (one block per chunk).
+__global__ void k_to_fp32(const double* __restrict__ sval, const hdk_chunk* __restrict__ chunk,
+                          float* __restrict__ sval32, const hdk_chunk* __restrict__ chunk32) {
+  const hdk_chunk c = chunk[blockIdx.x], c32 = chunk32[blockIdx.x];
+  for (int i = threadIdx.x; i < c32.len; i += blockDim.x)
+    sval32[c32.off + i] = i < c.len ? static_cast<float>(sval[c.off + i]) : 0.0f;
+}
+
 // z-fold: one warp per task.  (Folding z in the row-dot kernel's epilogue
 // behind a grid barrier measured 1-2 us slower than this separate launch.)
 __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
@@ -884,17 +909,17 @@ struct Stages2 {
   static constexpr int value = R == 1 ? kStages2 : R == 2 ? 6 : R == 4 ? 6 : 5;
 };
 
-template <int R>
+template <int R, typename V = double>
 struct Pass2Smem {
-  Ring2<Stages2<R>::value, R> ring;
+  Ring2<Stages2<R>::value, R, V> ring;
   double fold[kWarps / 2][3][kW];
 };
 
 // Fixed-order fold of the consumer warps' accumulators (4..7 into 0..3, 2..3
 // into 0..1, 1 into 0; with R columns within each column's 8 / R warps) and
 // write of the tile partial; consumer warps only.
-template <int R>
-__device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem<R>& sm, int slot, double (&x0)[kM],
+template <int R, typename V>
+__device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem<R, V>& sm, int slot, double (&x0)[kM],
                                                double (&x1)[kM], double (&x2)[kM]) {
   constexpr int WPC = kWarps / R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -938,13 +963,13 @@ __device__ __forceinline__ void fold_and_write(const hdk_factor& f, Pass2Smem<R>
   for (int m = 0; m < kM; ++m) x0[m] = x1[m] = x2[m] = 0.0;
 }
 
-template <bool kDry = false, int R = 1>
+template <bool kDry = false, int R = 1, typename V = double>
 __global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
   constexpr int S = Stages2<R>::value, WPC = kWarps / R;
   hdk::pdl_trigger();  // the producer prefills before the PDL wait; the others wait below
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Pass2Smem<R>& sm = *reinterpret_cast<Pass2Smem<R>*>(smem_raw);
-  Ring2<S, R>& ring = sm.ring;
+  Pass2Smem<R, V>& sm = *reinterpret_cast<Pass2Smem<R, V>*>(smem_raw);
+  Ring2<S, R, V>& ring = sm.ring;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long* trace = HDK_TRACE_PTR;
   if (trace && threadIdx.x == 0) trace[2 * blockIdx.x] = globaltimer();
@@ -975,19 +1000,19 @@ __global__ void __launch_bounds__(kThreads2) k_coltile(hdk_factor f) {
       if (tile >= 0) fold_and_write(f, sm, tile + blockIdx.x, x0, x1, x2);
       tile = ch.tile;
     }
-    const double* vals = ring.vals[st];
+    const V* vals = ring.vals[st];
     const int i0 = (warp % WPC - ch.seg0) & (WPC - 1);
     const int zc = 3 * (warp / WPC);
     for (int i = i0; i < (kDry ? 0 : ch.nseg); i += WPC) {
       const hdk_seg sg = ring.segs[st][i];
       const int lo = sg.clo_len & 0xffff, hi = lo + (sg.clo_len >> 16);
-      const double* v = vals + sg.coff - lo;
+      const V* v = vals + sg.coff - lo;
       const double z0 = ring.zs[st][i][zc], z1 = ring.zs[st][i][zc + 1], z2 = ring.zs[st][i][zc + 2];
 #pragma unroll
       for (int m = 0; m < kM; ++m) {
         const int cl = lane + 32 * m;
         if (cl >= lo && cl < hi) {
-          const double w = v[cl];
+          const double w = static_cast<double>(v[cl]);
           x0[m] += w * z0;
           x1[m] += w * z1;
           x2[m] += w * z2;
@@ -1278,6 +1303,10 @@ const Grids& grids() {
     const size_t s1 = sizeof(Ring<kStages1>), s2 = sizeof(Pass2Smem<1>);
     cudaFuncSetAttribute(k_rowdot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
     cudaFuncSetAttribute(k_coltile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s2));
+    cudaFuncSetAttribute(k_rowdot<false, 1, kWarps, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(Ring<kStages1, float>)));
+    cudaFuncSetAttribute(k_coltile<false, 1, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(Pass2Smem<1, float>)));
     const int s16 = static_cast<int>(sizeof(Ring<Pass1<16>::stages>));
     cudaFuncSetAttribute(k_rowdot<false, 2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, s16);
     cudaFuncSetAttribute(k_rowdot<false, 4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, s16);
@@ -1388,9 +1417,21 @@ int launch(const hdk_factor* f, const double* rhs_perm, double* out, bool scatte
     fl.first2 = nullptr;
     fl.tile_cta2 = nullptr;
   }
-  if (!(skip & 1u)) hdk::launch(k_rowdot<false>, dim3(g1), dim3(kThreads), s1, st, fl, rhs_perm);
+  const bool fp32 = f->use32 && f->sval32 && f->chunk32;  // preconditioner-only solve
+  if (!(skip & 1u)) {
+    if (fp32)
+      hdk::launch(k_rowdot<false, 1, kWarps, float>, dim3(g1), dim3(kThreads), sizeof(Ring<kStages1, float>), st, fl,
+                  rhs_perm);
+    else
+      hdk::launch(k_rowdot<false>, dim3(g1), dim3(kThreads), s1, st, fl, rhs_perm);
+  }
   if (!(skip & 2u)) hdk::launch(k_zreduce, dim3((f->n_ztask + 7) / 8), dim3(256), 0, st, fl);
-  if (!(skip & 4u)) hdk::launch(k_coltile<false>, dim3(g2), dim3(kThreads2), s2, st, fl);
+  if (!(skip & 4u)) {
+    if (fp32)
+      hdk::launch(k_coltile<false, 1, float>, dim3(g2), dim3(kThreads2), sizeof(Pass2Smem<1, float>), st, fl);
+    else
+      hdk::launch(k_coltile<false>, dim3(g2), dim3(kThreads2), s2, st, fl);
+  }
   if (!fold) return static_cast<int>(cudaGetLastError());
   if (scatter)
     hdk::launch(k_xreduce<true>, dim3((f->n + 255) / 256), dim3(256), 0, st, fl, g2, out);
@@ -1435,6 +1476,12 @@ HDK_API int hdk_apply_inverse3_multi(const hdk_factor* f, const double* rhs_perm
 }
 
 HDK_API size_t hdk_factor_part2_stride(const hdk_factor* f) { return part2_stride(*f); }
+
+HDK_API int hdk_factor_to_fp32(const hdk_factor* f, float* sval32, const hdk_chunk* chunk32, void* stream) {
+  if (f->n_chunks <= 0) return 0;
+  k_to_fp32<<<f->n_chunks, 256, 0, static_cast<cudaStream_t>(stream)>>>(f->sval, f->chunk, sval32, chunk32);
+  return static_cast<int>(cudaGetLastError());
+}
 
 HDK_API int hdk_set_chunk_trace(long long* const* trace, void* stream) {  // trace: pinned host cell
   return static_cast<int>(cudaMemcpyToSymbolAsync(g_chunk_trace, trace, sizeof(long long*), 0,
