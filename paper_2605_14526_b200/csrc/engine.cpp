@@ -310,6 +310,7 @@ Engine::~Engine() {
   fmem_.reset();
   mem_.reset();
   if (h_ctl_) cudaFreeHost(h_ctl_);
+  if (h_stage_) cudaFreeHost(h_stage_);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
   if (st2_) cudaStreamDestroy(st2_);
@@ -433,51 +434,74 @@ void Engine::build_static() {
 void Engine::upload_material() {
   const Mesh& m = scene_.mesh;
   const size_t ne = m.ne;
-  Vec w1(ne), w2(ne), bvh(ne);
   const double h = scene_.solver.h;
-  for (size_t e = 0; e < ne; ++e) {
-    const double V = m.vol[e];
-    if (mat_.kind == Kind::NeoHookean) {
-      w1[e] = mat_.weight(static_cast<int>(e)) * V;
-      w2[e] = 0.0;
-    } else {
-      w1[e] = 2.0 * mat_.mu[e] * V;
-      w2[e] = mat_.lambda[e] * V;
+  // pinned staging (w1, w2, mu, lambda, beta V / h, beta), filled by host
+  // threads and copied asynchronously on st_ (a lockstep batch holds ~2 M
+  // elements: pageable copies and one-thread loops cost ~30 ms per update)
+  if (!h_stage_) cuda_check(cudaMallocHost(&h_stage_, 6 * ne * sizeof(double)), "pinned material stage");
+  double *w1 = h_stage_, *w2 = w1 + ne, *mu = w2 + ne, *la = mu + ne, *bvh = la + ne, *beta = bvh + ne;
+  const bool nh = mat_.kind == Kind::NeoHookean;
+  parallel_ranges(static_cast<long long>(ne), [&](long long lo, long long hi) {
+    for (long long e = lo; e < hi; ++e) {
+      const double V = m.vol[e];
+      if (nh) {
+        w1[e] = mat_.weight(static_cast<int>(e)) * V;
+        w2[e] = 0.0;
+      } else {
+        w1[e] = 2.0 * mat_.mu[e] * V;
+        w2[e] = mat_.lambda[e] * V;
+      }
+      bvh[e] = mat_.beta[e] * V / h;
+      mu[e] = mat_.mu[e];
+      la[e] = mat_.lambda[e];
+      beta[e] = mat_.beta[e];
     }
-    bvh[e] = mat_.beta[e] * V / h;
-  }
-  dmat_.kind = mat_.kind == Kind::NeoHookean ? 1 : 0;
+  }, 0, 1 << 15);
+  dmat_.kind = nh ? 1 : 0;
   dmat_.barrier = mat_.barrier ? 1 : 0;
   dmat_.mu_bar = mat_.mu_bar;
   dmat_.lambda_bar = mat_.lambda_bar;
   dmat_.k_bar = mat_.k_bar;
-  const auto put = [&](const double* d, const Vec& v) {
-    DevArena::copy_h2d(const_cast<double*>(d), v.data(), v.size() * sizeof(double));
+  const auto put = [&](const double* d, const double* v) {
+    cuda_check(cudaMemcpyAsync(const_cast<double*>(d), v, ne * sizeof(double), cudaMemcpyHostToDevice, st_),
+               "upload material");
   };
   put(dmat_.w1, w1);
   put(dmat_.w2, w2);
-  put(dmat_.mu_e, mat_.mu);
-  put(dmat_.lambda_e, mat_.lambda);
+  put(dmat_.mu_e, mu);
+  put(dmat_.lambda_e, la);
   if (dmat_.beta_vh) put(dmat_.beta_vh, bvh);
-  aa_window_ = scene_.solver.aa_window > 0 ? scene_.solver.aa_window : (mat_.contrast() > 10.0 ? 1 : 5);
+  // weight range per sample (the whole mesh when not segmented): Anderson windows
+  const int segs = segs_ > 1 ? segs_ : 1;
+  const size_t sne = segs_ > 1 ? static_cast<size_t>(dseg_.ne) : ne;
+  std::vector<double> lo(segs), hi(segs);
+  parallel_ranges(segs, [&](long long k0, long long k1) {
+    for (long long k = k0; k < k1; ++k) {
+      double l = mat_.weight(static_cast<int>(k * sne)), u = l;
+      for (size_t e = k * sne; e < (k + 1) * sne; ++e) {
+        l = std::min(l, mat_.weight(static_cast<int>(e)));
+        u = std::max(u, mat_.weight(static_cast<int>(e)));
+      }
+      lo[k] = l;
+      hi[k] = u;
+    }
+  }, 0, 1);
+  const double contrast = *std::max_element(hi.begin(), hi.end()) / *std::min_element(lo.begin(), lo.end());
+  aa_window_ = scene_.solver.aa_window > 0 ? scene_.solver.aa_window : (contrast > 10.0 ? 1 : 5);
   aa_window_ = std::min(aa_window_, HDK_AA_MAX);
   if (segs_ > 1) {  // per-sample prox means and Anderson windows (each copy's own weight contrast)
-    put(seg_means_dev_, mat_.seg_means);
+    DevArena::copy_h2d(seg_means_dev_, mat_.seg_means.data(), mat_.seg_means.size() * sizeof(double));
     dmat_.seg_means = seg_means_dev_;
     dmat_.seg_ne = dseg_.ne;
     dmat_.tau_stride = static_cast<int>(sizeof(hdk_ctl) / sizeof(double));
     std::vector<int> win(2 * static_cast<size_t>(segs_), HDK_AA_MAX);
     for (int k = 0; k < segs_; ++k) {
-      double lo = mat_.weight(k * dseg_.ne), hi = lo;
-      for (int e = k * dseg_.ne; e < (k + 1) * dseg_.ne; ++e) {
-        lo = std::min(lo, mat_.weight(e));
-        hi = std::max(hi, mat_.weight(e));
-      }
-      const int w = scene_.solver.aa_window > 0 ? scene_.solver.aa_window : (hi / lo > 10.0 ? 1 : 5);
+      const int w = scene_.solver.aa_window > 0 ? scene_.solver.aa_window : (hi[k] / lo[k] > 10.0 ? 1 : 5);
       win[k] = std::min(w, HDK_AA_MAX);
     }
     DevArena::copy_h2d(seg_windows_, win.data(), win.size() * sizeof(int));
   }
+  cuda_check(cudaStreamSynchronize(st_), "upload material");  // the stage is reused by the next update
 }
 
 // S' values of hf_ into the existing stream buffer (device build when the

@@ -372,6 +372,7 @@ class Engine {
   double* tv_ = nullptr;     // t by vertex (input of B t)
   void* aares_ = nullptr;    // coefficient-solve result (hdk_bb_solve -> hdk_bb_mix)  // last-block ticket of hdk_aa_dots_fused
   hdk_ctl* h_ctl_ = nullptr;  // pinned mirror
+  double* h_stage_ = nullptr;  // pinned material staging (upload_material), 6 n_e doubles
   double* hook_ = nullptr;    // 5 doubles device
 
   // backward work

@@ -123,7 +123,9 @@ void Engine::refactor_device_values() {
   const Mesh& m = scene_.mesh;
   const double h = scene_.solver.h;
   void* s = st_;
-  DevArena::copy_h2d(R.beta, mat_.beta.data(), mat_.beta.size() * sizeof(double));
+  // beta as upload_material staged it (pinned; set_young calls that first)
+  cuda_check(cudaMemcpyAsync(R.beta, h_stage_ + 5 * static_cast<size_t>(m.ne), m.ne * sizeof(double),
+                             cudaMemcpyHostToDevice, st_), "beta");
   cuda_check(cudaMemsetAsync(R.err, 0, sizeof(int), st_), "zero");
   hdk_check_r(hdk_asm_weights(m.ne, dmat_.mu_e, dmat_.lambda_e, R.beta, dmat_.vol, h, R.w, s), "A weights");
   const double inertia = (1.0 + mat_.alpha * h) / (h * h);

@@ -83,30 +83,38 @@ void segmented_set_young(Material& mat, const Vec& young, const Vec& vol, int sa
   if (young.size() != mat.young.size() || ne * samples != young.size())
     raise(Code::Validation, "set_young: element count mismatch");
   const Vec vol1(vol.begin(), vol.begin() + ne);
-  for (int k = 0; k < samples; ++k) {
-    Material mk;  // the copy's scalars and its slices (not the whole concatenation)
-    mk.kind = mat.kind;
-    mk.barrier = mat.barrier;
-    mk.poisson = mat.poisson;
-    mk.alpha = mat.alpha;
-    mk.beta0 = mat.beta0;
-    mk.frozen = mat.frozen;
-    mk.young.assign(mat.young.begin() + k * ne, mat.young.begin() + (k + 1) * ne);
-    if (mat.frozen) {
-      mk.mu_bar = mat.seg_means[3 * k];
-      mk.lambda_bar = mat.seg_means[3 * k + 1];
-      mk.k_bar = mat.seg_means[3 * k + 2];
-    }
-    mk.set_young(Vec(young.begin() + k * ne, young.begin() + (k + 1) * ne), vol1);
-    std::copy(mk.young.begin(), mk.young.end(), mat.young.begin() + k * ne);
-    std::copy(mk.mu.begin(), mk.mu.end(), mat.mu.begin() + k * ne);
-    std::copy(mk.lambda.begin(), mk.lambda.end(), mat.lambda.begin() + k * ne);
-    std::copy(mk.beta.begin(), mk.beta.end(), mat.beta.begin() + k * ne);
-    mat.seg_means[3 * k] = mk.mu_bar;
-    mat.seg_means[3 * k + 1] = mk.lambda_bar;
-    mat.seg_means[3 * k + 2] = mk.k_bar;
-    mat.version = mk.version;
-  }
+  std::vector<std::uint64_t> versions(samples);
+  // samples are independent slices: one host thread per group of samples
+  parallel_ranges(
+      samples,
+      [&](long long k0, long long k1) {
+        for (long long k = k0; k < k1; ++k) {
+          Material mk;  // the copy's scalars and its slices (not the whole concatenation)
+          mk.kind = mat.kind;
+          mk.barrier = mat.barrier;
+          mk.poisson = mat.poisson;
+          mk.alpha = mat.alpha;
+          mk.beta0 = mat.beta0;
+          mk.frozen = mat.frozen;
+          mk.young.assign(mat.young.begin() + k * ne, mat.young.begin() + (k + 1) * ne);
+          if (mat.frozen) {
+            mk.mu_bar = mat.seg_means[3 * k];
+            mk.lambda_bar = mat.seg_means[3 * k + 1];
+            mk.k_bar = mat.seg_means[3 * k + 2];
+          }
+          mk.set_young(Vec(young.begin() + k * ne, young.begin() + (k + 1) * ne), vol1);
+          std::copy(mk.young.begin(), mk.young.end(), mat.young.begin() + k * ne);
+          std::copy(mk.mu.begin(), mk.mu.end(), mat.mu.begin() + k * ne);
+          std::copy(mk.lambda.begin(), mk.lambda.end(), mat.lambda.begin() + k * ne);
+          std::copy(mk.beta.begin(), mk.beta.end(), mat.beta.begin() + k * ne);
+          mat.seg_means[3 * k] = mk.mu_bar;
+          mat.seg_means[3 * k + 1] = mk.lambda_bar;
+          mat.seg_means[3 * k + 2] = mk.k_bar;
+          versions[k] = mk.version;
+        }
+      },
+      0, 1);
+  mat.version = *std::max_element(versions.begin(), versions.end());
 }
 
 // Host OR of the samples' loop conditions after sync_ctl (host-driven loops).

@@ -5,10 +5,13 @@
 // path runs on sm_100a through the hdk_* launchers (include/hdk.h).
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
+#include <exception>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace hdb {
@@ -26,6 +29,31 @@ struct Error : std::runtime_error {
 [[noreturn]] inline void raise(Code c, const std::string& m) { throw Error(c, m); }
 
 using Vec = std::vector<double>;
+
+// fn(lo, hi) over [0, n) split into contiguous ranges on up to `workers`
+// host threads (0 = hardware threads); the first exception is rethrown.
+template <class F>
+void parallel_ranges(long long n, F&& fn, int workers = 0, long long grain = 4096) {
+  int w = workers > 0 ? workers : static_cast<int>(std::thread::hardware_concurrency());
+  w = static_cast<int>(std::max<long long>(1, std::min<long long>({static_cast<long long>(w), 64LL, n / grain})));
+  if (w <= 1) {
+    fn(0LL, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::vector<std::exception_ptr> errs(w);
+  for (int t = 0; t < w; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        fn(n * t / w, n * (t + 1) / w);
+      } catch (...) {
+        errs[t] = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
 struct P3 { double x = 0, y = 0, z = 0; };
 
 // Tetrahedral mesh (mesh.hpp:16-60).  bm holds Dm^{-1} row-major per element.
