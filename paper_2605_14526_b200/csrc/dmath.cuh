@@ -325,15 +325,25 @@ __device__ __forceinline__ V3 vmax_floor(const V3& s) { return v3(fmax(s[0], kSi
 // hdk_set_newton_eigen from HETERODYN_NEWTON_EIGEN).
 __device__ int g_newton_eigen = 0;
 
+// The accepted candidate's gradient, residual norm and objective are those
+// of the next iterate, so they carry over instead of being re-evaluated
+// (same expressions on the same values: bitwise the re-evaluated ones; the
+// log and six divisions of a gradient dominate an iteration).
 template <class D>
 __device__ __forceinline__ bool newton_stretch(const V3& sf, double k, const D& den, V3& s_out, int& iters) {
   V3 s = vmax_floor(sf);
   const double tol = 1e-10 * k;
+  V3 r;
+  double r0, f0;
+  {
+    const V3 g = den.gradient(s);
+    r = v3(k * (s[0] - sf[0]) + g[0], k * (s[1] - sf[1]) + g[1], k * (s[2] - sf[2]) + g[2]);
+    r0 = norm3(r);
+    const V3 d0 = v3(s[0] - sf[0], s[1] - sf[1], s[2] - sf[2]);
+    f0 = 0.5 * k * dot3(d0, d0) + den.value(s);
+  }
   int it = 0;
   for (; it < kNewtonCap; ++it) {
-    const V3 g = den.gradient(s);
-    const V3 r = v3(k * (s[0] - sf[0]) + g[0], k * (s[1] - sf[1]) + g[1], k * (s[2] - sf[2]) + g[2]);
-    const double r0 = norm3(r);
     if (r0 <= tol) break;
     const double lo = 1e-8 * k;
     V3 dir;
@@ -362,31 +372,32 @@ __device__ __forceinline__ bool newton_stretch(const V3& sf, double k, const D& 
 #pragma unroll
       for (int i = 0; i < 3; ++i) dir[i] = -(ev(i, 0) * pr[0] + ev(i, 1) * pr[1] + ev(i, 2) * pr[2]);
     }
-    const V3 d0 = v3(s[0] - sf[0], s[1] - sf[1], s[2] - sf[2]);
-    const double f0 = 0.5 * k * dot3(d0, d0) + den.value(s);
     const double slope = dot3(r, dir);
     double t = 1.0;
     bool accepted = false;
     for (int bt = 0; bt < kBacktrackCap; ++bt, t *= 0.5) {
       const V3 cand = vmax_floor(v3(s[0] + t * dir[0], s[1] + t * dir[1], s[2] + t * dir[2]));
       const V3 dc = v3(cand[0] - sf[0], cand[1] - sf[1], cand[2] - sf[2]);
-      const bool obj_ok = 0.5 * k * dot3(dc, dc) + den.value(cand) <= f0 + 1e-4 * t * slope;
+      const double fc = 0.5 * k * dot3(dc, dc) + den.value(cand);
+      const bool obj_ok = fc <= f0 + 1e-4 * t * slope;
       const V3 gc = den.gradient(cand);
       const V3 rc = v3(k * dc[0] + gc[0], k * dc[1] + gc[1], k * dc[2] + gc[2]);
-      const bool res_ok = norm3(rc) <= (1.0 - 1e-4 * t) * r0;
+      const double nc = norm3(rc);
+      const bool res_ok = nc <= (1.0 - 1e-4 * t) * r0;
       if (obj_ok || res_ok) {
         s = cand;
+        r = rc;
+        r0 = nc;
+        f0 = fc;
         accepted = true;
         break;
       }
     }
     if (!accepted) break;
   }
-  const V3 g = den.gradient(s);
-  const V3 r = v3(k * (s[0] - sf[0]) + g[0], k * (s[1] - sf[1]) + g[1], k * (s[2] - sf[2]) + g[2]);
   s_out = s;
   iters = it;
-  return norm3(r) <= tol;
+  return r0 <= tol;
 }
 
 // Complete-pivoting 4x4 solve (FullPivLU, localstep.cpp:215,395); a is
