@@ -198,6 +198,10 @@ HDK_API int hdk_bapply(const hdk_mesh* m, const double* dcomp, const double* x, 
  * plain layout.  Does nothing while *run_flag == 0. */
 HDK_API int hdk_bapply_sorted(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
                               const int* corner_pos, const int* run_flag, void* stream);
+/* B x for a segmented batch's per-sample CG: samples whose CG has ended
+ * (cond0[sample * cond_stride] == 0) are skipped. */
+HDK_API int hdk_bapply_sorted_seg(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
+                                  const int* corner_pos, const int* cond0, int cond_stride, int seg_ne, void* stream);
 /* hdk_bapply that does nothing while *run_flag == 0 (unrolled backbone). */
 HDK_API int hdk_bapply_flag(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
                             const int* run_flag, void* stream);
@@ -226,6 +230,10 @@ typedef struct hdk_ctl {
   double red[HDK_RED_Q];
   double tau, rho, model, eps_tr;
 } hdk_ctl;
+/* The segmented batch's forward sweep: elements of samples whose loop has
+ * ended (ctl[sample].cond == 0) are skipped; no projection cache. */
+HDK_API int hdk_local_step_seg(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
+                               int* err, const hdk_ctl* ctl, void* stream);
 
 /* Vector kernels (vec.cu).  Vectors are full xyz-interleaved (3 nv) unless
  * named *_perm ([n][3] in elimination order). */

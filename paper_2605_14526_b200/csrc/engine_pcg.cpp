@@ -185,7 +185,8 @@ void Engine::build_pcg_graph_seg() {
       hdk_check_p(hdk_sdpcg_p(n3s, n3, pz_, pp_, ppv_, df_.p2v, pcg_, S, any_, D.d, D.ds, D.w, 0ULL, s), "p");
     };
     auto body_d = [&](unsigned long long handle) {
-      hdk_check_p(hdk_bapply_sorted(&dm_, dcomp_, ppv_, ef_, corner_pos_, any_, s), "B p");
+      hdk_check_p(hdk_bapply_sorted_seg(&dm_, dcomp_, ppv_, ef_, corner_pos_, &pcg_->cond,
+                                        static_cast<int>(sizeof(hdk_pcg) / sizeof(int)), dseg_.ne, s), "B p");
       hdk_check_p(hdk_spcg_apply(&dv_, &a_ff_, ns, S, ef_, pp_, pq_, pcg_part_, pcg_ticket_, pcg_, s), "q = (A - B) p");
       hdk_check_p(hdk_spcg_xr(n3s, n3, xp_, pr_, pp_, pq_, pcg_, s), "x, r");
       hdk_check_p(hdk_apply_inverse3_perm(&fs, pr_, pz_, s), "z = A^-1 r");
@@ -209,7 +210,8 @@ void Engine::build_pcg_graph_seg() {
     hdk_check_p(hdk_spcg_p(n3s, n3, pz_, pp_, ppv_, df_.p2v, pcg_, S, any_, 0ULL, s), "p");
   };
   auto body = [&](unsigned long long handle) {
-    hdk_check_p(hdk_bapply_sorted(&dm_, dcomp_, ppv_, ef_, corner_pos_, any_, s), "B p");
+    hdk_check_p(hdk_bapply_sorted_seg(&dm_, dcomp_, ppv_, ef_, corner_pos_, &pcg_->cond,
+                                        static_cast<int>(sizeof(hdk_pcg) / sizeof(int)), dseg_.ne, s), "B p");
     hdk_check_p(hdk_spcg_apply(&dv_, &a_ff_, ns, S, ef_, pp_, pq_, pcg_part_, pcg_ticket_, pcg_, s), "q = (A - B) p");
     hdk_check_p(hdk_spcg_xr(n3s, n3, xp_, pr_, pp_, pq_, pcg_, s), "x, r");
     hdk_check_p(hdk_apply_inverse3_perm(&fs, pr_, pz_, s), "z = A^-1 r");

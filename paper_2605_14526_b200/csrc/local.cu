@@ -133,12 +133,17 @@ __device__ __forceinline__ bool project(const hdk_material& mat, int e, const V3
   return volume_stretch(sf, s);
 }
 
+// ctl (a segmented batch's per-sample control blocks, or NULL): an element
+// of a sample whose loop has ended is skipped — its iterate no longer
+// changes, so its projection and forces would be rewritten unchanged.
 __global__ void __launch_bounds__(128) k_local(hdk_mesh m, hdk_material mat, const double* __restrict__ q,
-                                                double* __restrict__ ef, double* __restrict__ cache, int* err) {
+                                                double* __restrict__ ef, double* __restrict__ cache, int* err,
+                                                const hdk_ctl* ctl) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m.ne) return;
+  if (ctl && ctl[e / mat.seg_ne].cond == 0) return;
   const ElemGeom g = load_geom(m, e);
   const M3 f = def_grad(g, q);
   M3 u, v;
@@ -435,6 +440,27 @@ __global__ void __launch_bounds__(T, MINB) k_bapply(hdk_mesh m, const double* __
   bapply_body(m, dcomp, x, ef, run_flag, corner_pos);
 }
 
+// B p of a segmented batch's CG: elements of samples whose CG has ended
+// (cond0[sample cond_stride] == 0) do nothing — no loads either, so the
+// flag is read after the PDL wait and the element data after it.
+__global__ void __launch_bounds__(128) k_bapply_seg(hdk_mesh m, const double* __restrict__ dcomp,
+                                                    const double* __restrict__ x, double* __restrict__ ef,
+                                                    const int* __restrict__ corner_pos, const int* cond0,
+                                                    int cond_stride, int seg_ne) {
+  hdk::pdl_trigger();
+  hdk::pdl_wait();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m.ne) return;
+  if (cond0[(size_t)(e / seg_ne) * cond_stride] == 0) return;
+  const size_t n = m.ne;
+  const ElemGeom g = load_geom(m, e);
+  double d[30];
+#pragma unroll
+  for (int i = 0; i < 30; ++i) d[i] = __ldg(dcomp + i * n + e);
+  const M3 pm = bforce(g, d, x);
+  write_force_sorted(g, pm, ef, corner_pos, e);
+}
+
 // B p of the contact-adjoint columns' CG (blockIdx.y = column): each column's
 // direction by vertex at x + c x_stride, its sorted element forces at
 // ef + c ef_stride; a column whose CG has ended (run flag at
@@ -529,7 +555,15 @@ HDK_API int hdk_set_newton_eigen(int on) {
 
 HDK_API int hdk_local_step(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
                            double* cache, int* err, void* stream) {
-  hdk::launch(k_local, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q, elem_force, cache, err);
+  hdk::launch(k_local, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q, elem_force, cache, err,
+              static_cast<const hdk_ctl*>(nullptr));
+  return static_cast<int>(cudaGetLastError());
+}
+HDK_API int hdk_local_step_seg(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
+                               int* err, const hdk_ctl* ctl, void* stream) {
+  if (!mat->seg_means || mat->seg_ne <= 0 || !ctl) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_local, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q, elem_force,
+              static_cast<double*>(nullptr), err, ctl);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -591,6 +625,13 @@ HDK_API int hdk_bapply_cols_sorted(const hdk_mesh* m, const double* dcomp, const
   return static_cast<int>(cudaGetLastError());
 }
 
+HDK_API int hdk_bapply_sorted_seg(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
+                                  const int* corner_pos, const int* cond0, int cond_stride, int seg_ne, void* stream) {
+  if (!corner_pos || !cond0 || seg_ne <= 0) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_bapply_seg, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, dcomp, x,
+              elem_force, corner_pos, cond0, cond_stride, seg_ne);
+  return static_cast<int>(cudaGetLastError());
+}
 HDK_API int hdk_bapply_sorted(const hdk_mesh* m, const double* dcomp, const double* x, double* elem_force,
                               const int* corner_pos, const int* run_flag, void* stream) {
   static const int variant = [] {
