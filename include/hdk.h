@@ -230,10 +230,15 @@ typedef struct hdk_ctl {
   double red[HDK_RED_Q];
   double tau, rho, model, eps_tr;
 } hdk_ctl;
-/* The segmented batch's forward sweep: elements of samples whose loop has
- * ended (ctl[sample].cond == 0) are skipped; no projection cache. */
+/* Forward sweeps whose forces feed the sorted rhs gathers: corner k of
+ * element e writes its force at slot corner_vpos[4 e + k] of the
+ * vertex-ordered incidence list (3 doubles per slot); no projection cache.
+ * _seg: elements of samples whose loop has ended (ctl[sample].cond == 0)
+ * are skipped (corner_vpos may be NULL there: element order). */
 HDK_API int hdk_local_step_seg(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
-                               int* err, const hdk_ctl* ctl, void* stream);
+                               int* err, const hdk_ctl* ctl, const int* corner_vpos, void* stream);
+HDK_API int hdk_local_step_sorted(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
+                                  int* err, const int* corner_vpos, void* stream);
 
 /* Vector kernels (vec.cu).  Vectors are full xyz-interleaved (3 nv) unless
  * named *_perm ([n][3] in elimination order). */
@@ -261,6 +266,10 @@ HDK_API int hdk_gather(const hdk_vtx* x, const double* ef, double cm, const doub
  * b_prev <- b. */
 HDK_API int hdk_gather_rhs(const hdk_vtx* x, const double* ef, double inv_h2, const double* q_tilde, const double* damp,
                            const double* fixcoup, double* b_prev, double* rhs_perm, double* partial, void* stream);
+/* The same from forces stored by incidence slot (hdk_local_step_sorted). */
+HDK_API int hdk_gather_rhs_sorted(const hdk_vtx* x, const double* efs, double inv_h2, const double* q_tilde,
+                                  const double* damp, const double* fixcoup, double* b_prev, double* rhs_perm,
+                                  double* partial, void* stream);
 /* rhs_perm[p] = base[p2v[p]] (+ element forces when ef != NULL). */
 HDK_API int hdk_gather_perm(const hdk_vtx* x, const double* base, const double* ef, double* rhs_perm, void* stream);
 /* rhs_perm[p] = base_perm[p] (0 if base_perm is NULL) + element forces,
@@ -732,6 +741,9 @@ HDK_API int hdk_seg_aa_reset(hdk_ctl* ctl, const hdk_segs* g, int window, double
 HDK_API int hdk_seg_gather_rhs(const hdk_vtx* x, const hdk_segs* g, const hdk_ctl* ctl, const double* ef,
                                double inv_h2, const double* q_tilde, const double* damp, double* b_prev,
                                double* rhs_perm, double* partial, void* stream);
+HDK_API int hdk_seg_gather_rhs_sorted(const hdk_vtx* x, const hdk_segs* g, const hdk_ctl* ctl, const double* efs,
+                                      double inv_h2, const double* q_tilde, const double* damp, double* b_prev,
+                                      double* rhs_perm, double* partial, void* stream);
 HDK_API int hdk_seg_aa_dots_fused(const hdk_vtx* x, const hdk_factor* f, const hdk_segs* g, hdk_ctl* ctl,
                                   double* qhat, const double* qcur, double* last_q, double* last_g, double* dq,
                                   double* dg, double* partial18, unsigned int* tickets, void* stream);

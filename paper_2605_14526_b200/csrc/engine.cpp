@@ -345,6 +345,11 @@ void Engine::build_static() {
   dm_.mass = A.upload(m.mass);
   dm_.inc_off = A.upload(inc_off);
   dm_.inc = A.upload(inc);
+  {  // corner -> its slot in the vertex-ordered incidence list (sorted forward forces)
+    std::vector<int> cv(4 * ne);
+    for (size_t j = 0; j < inc.size(); ++j) cv[inc[j]] = static_cast<int>(j);
+    corner_vpos_ = A.upload(cv);
+  }
   q_ = A.upload(scene_.q0);
   rest_ = A.upload(m.rest);
   v_ = A.upload(scene_.v0);
@@ -743,8 +748,8 @@ void Engine::build_forward_graph() {
     cuda_check(cudaMemcpyAsync(qhat_, q_, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st_), "qhat init");
   };
   auto body = [&](unsigned long long handle) {
-    hdk_check(hdk_local_step(&dm_, &dmat_, qcur_, ef_, nullptr, &ctl_->err, s), "local step");
-    hdk_check(hdk_gather_rhs(&dv_, ef_, 1.0 / (h * h), qtil_, damp_, hf_.fixed.empty() ? nullptr : fixc_, bprev_, rhs_,
+    hdk_check(hdk_local_step_sorted(&dm_, &dmat_, qcur_, ef_, &ctl_->err, corner_vpos_, s), "local step");
+    hdk_check(hdk_gather_rhs_sorted(&dv_, ef_, 1.0 / (h * h), qtil_, damp_, hf_.fixed.empty() ? nullptr : fixc_, bprev_, rhs_,
                              part_a_, s), "rhs");
     hdk_check(hdk_apply_inverse3_partial(&df_, rhs_, s), "solve");
     hdk_check(hdk_aa_dots_fused(&dv_, &df_, ctl_, qhat_, qcur_, lastq_, lastg_, dq_, dg_, part_b_, ticket_, 0, 0ULL, s),

@@ -367,6 +367,7 @@ class Engine {
   double* seedp_ = nullptr;  // adjoint seed in elimination order (3 n)
   double* xp_ = nullptr;     // backbone iterate in elimination order (3 n); x_ holds it by vertex
   int* corner_pos_ = nullptr;  // element corner -> slot in the elimination-order incidence list
+  int* corner_vpos_ = nullptr;  // element corner -> slot in the vertex-ordered incidence list
   // R = gather o B in elimination order: R(t), tracked R(x), last R(x) and R(g), R(dq_j + dg_j) ring
   double *rt_ = nullptr, *rx_ = nullptr, *lrx_ = nullptr, *lrg_ = nullptr, *rsq_ = nullptr;
   double* tv_ = nullptr;     // t by vertex (input of B t)

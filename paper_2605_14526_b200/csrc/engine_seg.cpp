@@ -138,8 +138,8 @@ void Engine::build_forward_graph_seg() {
     cuda_check(cudaMemcpyAsync(qhat_, q_, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st_), "qhat init");
   };
   auto body = [&](unsigned long long handle) {
-    hdk_check_s(hdk_local_step_seg(&dm_, &dmat_, qcur_, ef_, &ctl_->err, ctl_, s), "local step");
-    hdk_check_s(hdk_seg_gather_rhs(&dv_, &dseg_, ctl_, ef_, 1.0 / (h * h), qtil_, damp_, bprev_, rhs_, part_a_, s), "rhs");
+    hdk_check_s(hdk_local_step_seg(&dm_, &dmat_, qcur_, ef_, &ctl_->err, ctl_, corner_vpos_, s), "local step");
+    hdk_check_s(hdk_seg_gather_rhs_sorted(&dv_, &dseg_, ctl_, ef_, 1.0 / (h * h), qtil_, damp_, bprev_, rhs_, part_a_, s), "rhs");
     hdk_check_s(hdk_apply_inverse3_partial(&df_, rhs_, s), "solve");
     hdk_check_s(hdk_seg_aa_dots_fused(&dv_, &df_, &dseg_, ctl_, qhat_, qcur_, lastq_, lastg_, dq_, dg_, part18_, ticket_,
                                       s), "aa dots + solve");

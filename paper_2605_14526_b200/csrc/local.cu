@@ -138,7 +138,7 @@ __device__ __forceinline__ bool project(const hdk_material& mat, int e, const V3
 // changes, so its projection and forces would be rewritten unchanged.
 __global__ void __launch_bounds__(128) k_local(hdk_mesh m, hdk_material mat, const double* __restrict__ q,
                                                 double* __restrict__ ef, double* __restrict__ cache, int* err,
-                                                const hdk_ctl* ctl) {
+                                                const hdk_ctl* ctl, const int* __restrict__ corner_vpos) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -159,7 +159,10 @@ __global__ void __launch_bounds__(128) k_local(hdk_mesh m, hdk_material mat, con
     const double wr = mat.w1[e], wv = mat.w2[e];
     p = recompose(u, v3(wr + wv * s[0], wr + wv * s[1], wr + wv * s[2]), v);
   }
-  write_force(g, p, ef, e);
+  // corner_vpos: each corner's force at its slot of the vertex-ordered
+  // incidence list (the gather then reads contiguous ranges)
+  if (corner_vpos) write_force_sorted(g, p, ef, corner_vpos, e);
+  else write_force(g, p, ef, e);
   if (cache) {
     const size_t ne = m.ne;
 #pragma unroll
@@ -556,14 +559,21 @@ HDK_API int hdk_set_newton_eigen(int on) {
 HDK_API int hdk_local_step(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
                            double* cache, int* err, void* stream) {
   hdk::launch(k_local, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q, elem_force, cache, err,
-              static_cast<const hdk_ctl*>(nullptr));
+              static_cast<const hdk_ctl*>(nullptr), static_cast<const int*>(nullptr));
   return static_cast<int>(cudaGetLastError());
 }
 HDK_API int hdk_local_step_seg(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
-                               int* err, const hdk_ctl* ctl, void* stream) {
+                               int* err, const hdk_ctl* ctl, const int* corner_vpos, void* stream) {
   if (!mat->seg_means || mat->seg_ne <= 0 || !ctl) return static_cast<int>(cudaErrorInvalidValue);
   hdk::launch(k_local, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q, elem_force,
-              static_cast<double*>(nullptr), err, ctl);
+              static_cast<double*>(nullptr), err, ctl, corner_vpos);
+  return static_cast<int>(cudaGetLastError());
+}
+HDK_API int hdk_local_step_sorted(const hdk_mesh* m, const hdk_material* mat, const double* q, double* elem_force,
+                                  int* err, const int* corner_vpos, void* stream) {
+  if (!corner_vpos) return static_cast<int>(cudaErrorInvalidValue);
+  hdk::launch(k_local, dim3(blocks(m->ne, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream), *m, *mat, q, elem_force,
+              static_cast<double*>(nullptr), err, static_cast<const hdk_ctl*>(nullptr), corner_vpos);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -100,6 +100,21 @@ __device__ __forceinline__ void gather_vtx(const hdk_vtx& x, const double* __res
   }
 }
 
+// The same sums from forces stored by incidence slot (k_local with
+// corner_vpos): contiguous reads, the same order, so bitwise gather_vtx.
+__device__ __forceinline__ void gather_vtx_sorted(const hdk_vtx& x, const double* __restrict__ efs, int v, double& s0,
+                                                  double& s1, double& s2) {
+  s0 = s1 = s2 = 0.0;
+  const int e = x.inc_off[v + 1];
+#pragma unroll 4
+  for (int j = x.inc_off[v]; j < e; ++j) {
+    const double* p = efs + 3 * (size_t)j;
+    s0 += __ldg(p);
+    s1 += __ldg(p + 1);
+    s2 += __ldg(p + 2);
+  }
+}
+
 __global__ void k_free_fall(hdk_vtx x, const double* q, const double* v, const double* f, double h, int hv,
                             double ax, double ay, double az, double hk, double hd, double* qt, double* qc) {
   hdk::pdl_wait();
@@ -132,6 +147,7 @@ __global__ void k_gather(hdk_vtx x, const double* ef, double cm, const double* b
   }
 }
 
+template <bool kSorted>
 __global__ void __launch_bounds__(kT) k_gather_rhs(hdk_vtx x, const double* __restrict__ ef, double inv_h2,
                                                    const double* __restrict__ qt, const double* __restrict__ damp,
                                                    const double* __restrict__ fixc, double* bprev, double* rhs,
@@ -143,7 +159,8 @@ __global__ void __launch_bounds__(kT) k_gather_rhs(hdk_vtx x, const double* __re
     const int p = x.v2p[v];
     const double m = x.mass[v];
     double g[3];
-    gather_vtx(x, ef, v, g[0], g[1], g[2]);
+    if (kSorted) gather_vtx_sorted(x, ef, v, g[0], g[1], g[2]);
+    else gather_vtx(x, ef, v, g[0], g[1], g[2]);
     for (int a = 0; a < 3; ++a) {
       const size_t i = 3 * (size_t)v + a;
       double b = m * qt[i] * inv_h2;  // M q~ / h^2 (forward.cpp:99)
@@ -1205,7 +1222,13 @@ HDK_API int hdk_gather(const hdk_vtx* x, const double* ef, double cm, const doub
 
 HDK_API int hdk_gather_rhs(const hdk_vtx* x, const double* ef, double inv_h2, const double* q_tilde, const double* damp,
                            const double* fixcoup, double* b_prev, double* rhs_perm, double* partial, void* stream) {
-  hdk::launch(k_gather_rhs, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), *x, ef, inv_h2, q_tilde, damp, fixcoup, b_prev, rhs_perm, partial);
+  hdk::launch(k_gather_rhs<false>, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), *x, ef, inv_h2, q_tilde, damp, fixcoup, b_prev, rhs_perm, partial);
+  return last();
+}
+HDK_API int hdk_gather_rhs_sorted(const hdk_vtx* x, const double* efs, double inv_h2, const double* q_tilde,
+                                  const double* damp, const double* fixcoup, double* b_prev, double* rhs_perm,
+                                  double* partial, void* stream) {
+  hdk::launch(k_gather_rhs<true>, dim3(HDK_RED_BLOCKS), dim3(kT), 0, S(stream), *x, efs, inv_h2, q_tilde, damp, fixcoup, b_prev, rhs_perm, partial);
   return last();
 }
 
@@ -1452,6 +1475,7 @@ __global__ void k_seg_aa_reset(hdk_ctl* ctl, hdk_segs g, int window, double guar
   if (threadIdx.x == 0) *any = 1;
 }
 
+template <bool kSorted>
 __global__ void __launch_bounds__(kT) k_seg_gather_rhs(hdk_vtx x, hdk_segs g, const double* __restrict__ ef,
                                                        double inv_h2, const double* __restrict__ qt,
                                                        const double* __restrict__ damp, double* bprev, double* rhs,
@@ -1466,7 +1490,8 @@ __global__ void __launch_bounds__(kT) k_seg_gather_rhs(hdk_vtx x, hdk_segs g, co
     const int p = x.v2p[v];
     const double m = x.mass[v];
     double gg[3];
-    gather_vtx(x, ef, v, gg[0], gg[1], gg[2]);
+    if (kSorted) gather_vtx_sorted(x, ef, v, gg[0], gg[1], gg[2]);
+    else gather_vtx(x, ef, v, gg[0], gg[1], gg[2]);
     for (int a = 0; a < 3; ++a) {
       const size_t i = 3 * (size_t)v + a;
       double b = m * qt[i] * inv_h2;
@@ -1819,8 +1844,15 @@ HDK_API int hdk_seg_aa_reset(hdk_ctl* ctl, const hdk_segs* g, int window, double
 HDK_API int hdk_seg_gather_rhs(const hdk_vtx* x, const hdk_segs* g, const hdk_ctl* ctl, const double* ef,
                                double inv_h2, const double* q_tilde, const double* damp, double* b_prev,
                                double* rhs_perm, double* partial, void* stream) {
-  hdk::launch(k_seg_gather_rhs, dim3(kRB, g->count), dim3(kT), 0, S(stream), *x, *g, ef, inv_h2, q_tilde, damp, b_prev,
-              rhs_perm, partial, ctl);
+  hdk::launch(k_seg_gather_rhs<false>, dim3(kRB, g->count), dim3(kT), 0, S(stream), *x, *g, ef, inv_h2, q_tilde, damp,
+              b_prev, rhs_perm, partial, ctl);
+  return last();
+}
+HDK_API int hdk_seg_gather_rhs_sorted(const hdk_vtx* x, const hdk_segs* g, const hdk_ctl* ctl, const double* efs,
+                                      double inv_h2, const double* q_tilde, const double* damp, double* b_prev,
+                                      double* rhs_perm, double* partial, void* stream) {
+  hdk::launch(k_seg_gather_rhs<true>, dim3(kRB, g->count), dim3(kT), 0, S(stream), *x, *g, efs, inv_h2, q_tilde, damp,
+              b_prev, rhs_perm, partial, ctl);
   return last();
 }
 HDK_API int hdk_seg_aa_dots_fused(const hdk_vtx* x, const hdk_factor* f, const hdk_segs* g, hdk_ctl* ctl,
