@@ -119,7 +119,7 @@ __device__ __forceinline__ void svd_pair(M3& w, M3& u, M3& v, int p, int q, doub
     const double tt = tau > 0 ? 1.0 / (tau + w2) : 1.0 / (tau - w2);
     const double sgn = tt > 0 ? 1.0 : -1.0;
     const double n = 1.0 / sqrt(tt * tt + 1.0);
-    sr = -sgn * (n01 / fabs(n01)) * fabs(tt) * n;
+    sr = -sgn * copysign(1.0, n01) * fabs(tt) * n;  // n01 / |n01|, exactly
     cr = n;
   }
   // j_left = rot1 * j_right^T
@@ -165,7 +165,8 @@ __device__ __forceinline__ void signed_svd(const M3& f, M3& u, V3& sig, M3& v) {
     sig[i] = fabs(d) * scale;
     if (d < 0) { u(0, i) = -u(0, i); u(1, i) = -u(1, i); u(2, i) = -u(2, i); }
   }
-  // descending sort with Eigen's first-max swaps
+  // descending sort with Eigen's first-max swaps (swap partners are compile-
+  // time indices, so sig, u and v stay in registers)
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     int pos = i;
@@ -173,14 +174,16 @@ __device__ __forceinline__ void signed_svd(const M3& f, M3& u, V3& sig, M3& v) {
 #pragma unroll
     for (int k = i + 1; k < 3; ++k)
       if (sig[k] > best) { best = sig[k]; pos = k; }
-    if (pos != i) {
-      const double ts = sig[i]; sig[i] = sig[pos]; sig[pos] = ts;
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        double t = u(r, i); u(r, i) = u(r, pos); u(r, pos) = t;
-        t = v(r, i); v(r, i) = v(r, pos); v(r, pos) = t;
+    for (int k = i + 1; k < 3; ++k)
+      if (pos == k) {
+        const double ts = sig[i]; sig[i] = sig[k]; sig[k] = ts;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          double t = u(r, i); u(r, i) = u(r, k); u(r, k) = t;
+          t = v(r, i); v(r, i) = v(r, k); v(r, k) = t;
+        }
       }
-    }
   }
   if (det3(u) < 0) { u(0, 2) = -u(0, 2); u(1, 2) = -u(1, 2); u(2, 2) = -u(2, 2); sig[2] = -sig[2]; }
   if (det3(v) < 0) { v(0, 2) = -v(0, 2); v(1, 2) = -v(1, 2); v(2, 2) = -v(2, 2); sig[2] = -sig[2]; }
