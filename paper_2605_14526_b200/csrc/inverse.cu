@@ -185,7 +185,7 @@ HDK_API int hdk_inverse_values(const hdk_inverse_build* b, double* stream, void*
   const int blocks = (b->n + per_block - 1) / per_block;
   // columns resident per SM (shared memory bound): few -> run-ahead walk
   const int per_sm = per_block * static_cast<int>((227 * 1024) / smem);
-  const auto kern = per_sm < 16 ? k_inverse_values : k_inverse_values_plain;
+  const auto kern = per_sm < 24 ? k_inverse_values : k_inverse_values_plain;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   kern<<<blocks, 32 * per_block, smem, static_cast<cudaStream_t>(stream_handle)>>>(*b, per_block, stream);
   return static_cast<int>(cudaGetLastError());
