@@ -1103,23 +1103,34 @@ __global__ void __launch_bounds__(kT) k_bcg_zfold(hdk_factor f, size_t part2_str
     const int tile = col >> 8;
     const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
     const size_t base = (size_t)(tile + tb0) * 256 + (col & 255);
-    double zv[kBC], rv[kBC];
+    // every column's loads before any store: the z stores may alias the
+    // solve's partials as far as the compiler knows, so a store between
+    // two columns' folds serialised eight L2 round trips (51.7 us)
+    double zv[kBC], rv[kBC], xv[kBC];
+    const int nt = tb1 - tb0;
 #pragma unroll
     for (int c = 0; c < kBC; ++c) {
       zv[c] = 0.0;
       rv[c] = 0.0;
+      xv[c] = 0.0;
       if (c < m) {
-        const double* p2 = f.part2 + c * part2_stride;
-        double zi = 0.0;
-        for (int b = 0; b <= tb1 - tb0; ++b) zi += __ldg(p2 + 3 * (base + 256 * (size_t)b) + a);
+        const double* p2 = f.part2 + c * part2_stride + 3 * base + a;
+        double zi = __ldg(p2);
+        if (nt >= 1) zi += __ldg(p2 + 3 * 256);
+        for (int b = 2; b <= nt; ++b) zi += __ldg(p2 + 3 * 256 * (size_t)b);
         zv[c] = zi;
         rv[c] = r[c * n3 + i];
-        z[c * n3 + i] = zi;
-        const double t = x[c * n3 + i] + zi;
-        acc[kGram + c] = zi * zi;
-        acc[kGram + kBC + c] = t * t;
+        xv[c] = x[c * n3 + i];
       }
     }
+#pragma unroll
+    for (int c = 0; c < kBC; ++c)
+      if (c < m) {
+        z[c * n3 + i] = zv[c];
+        const double t = xv[c] + zv[c];
+        acc[kGram + c] = zv[c] * zv[c];
+        acc[kGram + kBC + c] = t * t;
+      }
 #pragma unroll
     for (int c = 0; c < kBC; ++c)
 #pragma unroll
@@ -1409,6 +1420,11 @@ __global__ void __launch_bounds__(kT) k_dpcg_rz(hdk_factor f, const double* __re
   for (int q = 0; q < kDq; ++q) acc[q] = 0.0;
   const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
   if (i < n3) {
+    // the loads that do not depend on the fold first, all before the stores
+    const double ri = r[i], xi = x[i];
+    double awi[kDK];
+#pragma unroll
+    for (int c = 0; c < kDK; ++c) awi[c] = c < k ? aw[(size_t)c * n3 + i] : 0.0;
     const int col = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)col);
     const int tile = col >> 8;
     const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
@@ -1417,12 +1433,12 @@ __global__ void __launch_bounds__(kT) k_dpcg_rz(hdk_factor f, const double* __re
     for (int b = 0; b <= tb1 - tb0; ++b) zi += __ldg(f.part2 + 3 * (base + 256 * (size_t)b) + a);
     z[i] = zi;
     if (rec) zhist[(size_t)(it - 1) * n3 + i] = zi;
-    const double t = x[i] + zi;
-    acc[0] = r[i] * zi;
+    const double t = xi + zi;
+    acc[0] = ri * zi;
     acc[1] = zi * zi;
     acc[2] = t * t;
 #pragma unroll
-    for (int c = 0; c < kDK; ++c) acc[3 + c] = c < k ? aw[(size_t)c * n3 + i] * zi : 0.0;
+    for (int c = 0; c < kDK; ++c) acc[3 + c] = awi[c] * zi;
   }
   const int nb = gridDim.x;
   block_store_many<kDq>(acc, partial, nb);
