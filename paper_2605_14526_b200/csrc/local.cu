@@ -76,6 +76,25 @@ __device__ __forceinline__ void write_force(const ElemGeom& g, const M3& p, doub
   }
 }
 
+__device__ __forceinline__ void write_force_at(const ElemGeom& g, const M3& p, double* __restrict__ efs, const int4 pos) {
+  double f[4][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) f[k + 1][r] = p(r, 0) * g.b[3 * k] + p(r, 1) * g.b[3 * k + 1] + p(r, 2) * g.b[3 * k + 2];
+    f[0][r] = -(f[1][r] + f[2][r] + f[3][r]);
+  }
+  const int ps[4] = {pos.x, pos.y, pos.z, pos.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (ps[k] >= 0) {
+      double* o = efs + 3 * (size_t)ps[k];
+      o[0] = f[k][0];
+      o[1] = f[k][1];
+      o[2] = f[k][2];
+    }
+}
+
 // Same forces, each corner's three components stored at its slot of the
 // elimination-order incidence list (corner_pos[4 e + k], -1 for fixed
 // vertices), so the per-vertex gather reads one contiguous range.
@@ -373,11 +392,13 @@ __device__ __forceinline__ void bapply_body(const hdk_mesh& m, const double* __r
   double d[30];
 #pragma unroll
   for (int i = 0; i < 30; ++i) d[i] = __ldg(dcomp + i * n + ee);
+  // the corners' slots are static too: no dependent load after the arithmetic
+  const int4 pos = corner_pos ? __ldg(reinterpret_cast<const int4*>(corner_pos) + ee) : make_int4(0, 0, 0, 0);
   HDK_TRACED_WAIT(hdk::kTrBapply);
   if (run_flag && *run_flag == 0) return;
   if (!live) return;
   const M3 pm = bforce(g, d, x);
-  if (corner_pos) write_force_sorted(g, pm, ef, corner_pos, e);
+  if (corner_pos) write_force_at(g, pm, ef, pos);
   else write_force(g, pm, ef, e);
 }
 
@@ -400,6 +421,7 @@ __global__ void __launch_bounds__(128) k_bapply_cols_fused(hdk_mesh m, const dou
   double d[30];
 #pragma unroll
   for (int i = 0; i < 30; ++i) d[i] = __ldg(dcomp + i * n + ee);
+  const int4 pos = __ldg(reinterpret_cast<const int4*>(corner_pos) + ee);
   hdk::pdl_wait();
   if (!live) return;
   const int c0 = K * blockIdx.y;  // column group of this block row
@@ -407,7 +429,7 @@ __global__ void __launch_bounds__(128) k_bapply_cols_fused(hdk_mesh m, const dou
   for (int c = c0; c < c0 + K; ++c) {
     if (cond0[(size_t)c * cond_stride] == 0) continue;
     const M3 pm = bforce(g, d, x + c * x_stride);
-    write_force_sorted(g, pm, ef + c * ef_stride, corner_pos, e);
+    write_force_at(g, pm, ef + c * ef_stride, pos);
   }
 }
 
@@ -461,11 +483,12 @@ __global__ void __launch_bounds__(128) k_bapply_seg(hdk_mesh m, const double* __
   double d[30];
 #pragma unroll
   for (int i = 0; i < 30; ++i) d[i] = __ldg(dcomp + i * n + ee);
+  const int4 pos = __ldg(reinterpret_cast<const int4*>(corner_pos) + ee);
   hdk::pdl_wait();
   if (!live) return;
   if (cond0[(size_t)(e / seg_ne) * cond_stride] == 0) return;
   const M3 pm = bforce(g, d, x);
-  write_force_sorted(g, pm, ef, corner_pos, e);
+  write_force_at(g, pm, ef, pos);
 }
 
 // B p of the contact-adjoint columns' CG (blockIdx.y = column): each column's

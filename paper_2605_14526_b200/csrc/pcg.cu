@@ -650,27 +650,38 @@ __global__ void __launch_bounds__(kT) k_cpcg_apply(hdk_vtx x, hdk_csr A, int n3,
                                                    size_t ef_stride, const double* __restrict__ p,
                                                    double* __restrict__ q, double* partial, size_t pstride,
                                                    unsigned int* tickets, hdk_pcg* sts) {
-  hdk::pdl_wait();
+  // the row's static index ranges and its first entry of A before the PDL
+  // wait (they do not depend on the previous kernel)
   hdk::pdl_trigger();
   const int c = blockIdx.y;
+  const int sub = threadIdx.x & 7;
+  const int row = blockIdx.x * (kT / 8) + (threadIdx.x >> 3);
+  const bool live = row < x.n;
+  const int jb = live ? __ldg(x.pinc_off + row) : 0, e = live ? __ldg(x.pinc_off + row + 1) : 0;
+  const int kb = live ? __ldg(A.off + row) : 0, ke = live ? __ldg(A.off + row + 1) : 0;
+  const bool has0 = kb + sub < ke;
+  const double w0 = has0 ? __ldg(A.val + kb + sub) : 0.0;
+  const int col0 = has0 ? __ldg(A.col + kb + sub) : 0;
+  hdk::pdl_wait();
   hdk_pcg* st = sts + c;
   if (st->cond == 0) return;
   const double* efc = ef + c * ef_stride;
   const double* pc = p + (size_t)c * n3;
   double* qc = q + (size_t)c * n3;
-  const int sub = threadIdx.x & 7;
-  const int row = blockIdx.x * (kT / 8) + (threadIdx.x >> 3);
-  const bool live = row < x.n;
   double c0 = 0.0, c1 = 0.0, c2 = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  const int e = live ? __ldg(x.pinc_off + row + 1) : 0;
-  for (int j = (live ? __ldg(x.pinc_off + row) : 0) + sub; j < e; j += 8) {
+  for (int j = jb + sub; j < e; j += 8) {
     const double* f = efc + 3 * (size_t)j;
     c0 += __ldg(f);
     c1 += __ldg(f + 1);
     c2 += __ldg(f + 2);
   }
-  const int ke = live ? __ldg(A.off + row + 1) : 0;
-  for (int k = (live ? __ldg(A.off + row) : 0) + sub; k < ke; k += 8) {
+  if (has0) {
+    const double* v = pc + 3 * (size_t)col0;
+    a0 += w0 * v[0];
+    a1 += w0 * v[1];
+    a2 += w0 * v[2];
+  }
+  for (int k = kb + sub + 8; k < ke; k += 8) {
     const double w = __ldg(A.val + k);
     const double* v = pc + 3 * (size_t)__ldg(A.col + k);
     a0 += w * v[0];
