@@ -1326,48 +1326,67 @@ __global__ void __launch_bounds__(kT) k_defl_gram(int n3, const double* __restri
   }
 }
 
-// Cholesky of E (one thread; once per step); active = factor ok.
+// Cholesky of E once per step; active = factor ok.  One warp: lanes fold the
+// pairs' slice partials, lane 0 factors in shared memory, lanes 0..k-1 form
+// E^{-1} column by column (the per-iteration mu = E^{-1} d becomes a
+// mat-vec).  The factor used to live in global memory with one thread
+// (52 us a step: every access a dependent global round trip).
 __global__ void k_defl_chol(const double* __restrict__ e, hdk_defl* d) {
   hdk::pdl_wait();
   hdk::pdl_trigger();
-  if (!d->use || threadIdx.x != 0) return;
-  const int k = d->k;
-  double* l = d->l;
-  for (int q = 0; q < kDK * kDK; ++q) l[q] = 0.0;
-  for (int pj = 0, pair = 0; pj < kDK; ++pj)
-    for (int pc = pj; pc < kDK; ++pc, ++pair) {
-      if (pj >= k || pc >= k) continue;
-      double t = 0.0;
-      for (int q = 0; q < kGramSlices; ++q) t += e[kDK * kDK + (size_t)pair * kGramSlices + q];
-      l[pc * kDK + pj] = t;  // lower triangle (row pc >= column pj)
+  if (!d->use) return;
+  const int k = d->k, lane = threadIdx.x;
+  __shared__ double l[kDK * kDK];
+  __shared__ int ok_s;
+  for (int q = lane; q < kDK * kDK; q += 32) l[q] = 0.0;
+  __syncwarp();
+  constexpr int kPairs = kDK * (kDK + 1) / 2;
+  for (int pair = lane; pair < kPairs; pair += 32) {
+    int pj = 0, idx = pair;  // pair -> (pj, pc), pj <= pc, ordered by pj then pc
+    while (idx >= kDK - pj) {
+      idx -= kDK - pj;
+      ++pj;
     }
-  double dmax = 0.0;
-  for (int r = 0; r < k; ++r) dmax = fmax(dmax, l[r * kDK + r]);
-  bool ok = k > 0;
-  for (int j = 0; j < k && ok; ++j) {
-    double dj = l[j * kDK + j];
-    for (int t = 0; t < j; ++t) dj -= l[j * kDK + t] * l[j * kDK + t];
-    if (!(dj > 1e-12 * dmax)) {
-      ok = false;
-      break;
-    }
-    dj = sqrt(dj);
-    l[j * kDK + j] = dj;
-    for (int r = j + 1; r < k; ++r) {
-      double v = l[r * kDK + j];
-      for (int t = 0; t < j; ++t) v -= l[r * kDK + t] * l[j * kDK + t];
-      l[r * kDK + j] = v / dj;
-    }
+    const int pc = pj + idx;
+    if (pj >= k || pc >= k) continue;
+    double t = 0.0;
+    for (int q = 0; q < kGramSlices; ++q) t += e[kDK * kDK + (size_t)pair * kGramSlices + q];
+    l[pc * kDK + pj] = t;  // lower triangle (row pc >= column pj)
   }
-  if (ok) {  // E^{-1} column by column (the per-iteration mu = E^{-1} d becomes a mat-vec)
+  __syncwarp();
+  if (lane == 0) {
+    double dmax = 0.0;
+    for (int r = 0; r < k; ++r) dmax = fmax(dmax, l[r * kDK + r]);
+    bool ok = k > 0;
+    for (int j = 0; j < k && ok; ++j) {
+      double dj = l[j * kDK + j];
+      for (int t = 0; t < j; ++t) dj -= l[j * kDK + t] * l[j * kDK + t];
+      if (!(dj > 1e-12 * dmax)) {
+        ok = false;
+        break;
+      }
+      dj = sqrt(dj);
+      l[j * kDK + j] = dj;
+      for (int r = j + 1; r < k; ++r) {
+        double v = l[r * kDK + j];
+        for (int t = 0; t < j; ++t) v -= l[r * kDK + t] * l[j * kDK + t];
+        l[r * kDK + j] = v / dj;
+      }
+    }
+    ok_s = ok ? 1 : 0;
+  }
+  __syncwarp();
+  const bool ok = ok_s != 0;
+  for (int q = lane; q < kDK * kDK; q += 32) d->l[q] = l[q];
+  if (ok && lane < kDK) {  // column lane of E^{-1}
     double col[kDK];
-    for (int c = 0; c < kDK; ++c) {
-      for (int r = 0; r < kDK; ++r) col[r] = (r == c) ? 1.0 : 0.0;
-      if (c < k) chol_solve_l(l, k, col, col);
-      for (int r = 0; r < kDK; ++r) d->einv[r * kDK + c] = (r < k && c < k) ? col[r] : 0.0;
-    }
+#pragma unroll
+    for (int r = 0; r < kDK; ++r) col[r] = (r == lane) ? 1.0 : 0.0;
+    if (lane < k) chol_solve_l(l, k, col, col);
+#pragma unroll
+    for (int r = 0; r < kDK; ++r) d->einv[r * kDK + lane] = (r < k && lane < k) ? col[r] : 0.0;
   }
-  d->active = ok ? 1 : 0;
+  if (lane == 0) d->active = ok ? 1 : 0;
 }
 
 // First iterate: c = E^{-1} W^T r (last block), then (k_defl_correct) x += W c, r -= AW c.
