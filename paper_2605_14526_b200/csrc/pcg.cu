@@ -1437,10 +1437,16 @@ __global__ void __launch_bounds__(kT) k_dpcg_rz(hdk_factor f, const double* __re
                                                 const double* __restrict__ x, const double* __restrict__ aw,
                                                 double* partial, unsigned int* ticket, hdk_pcg* st, hdk_defl* d,
                                                 double* __restrict__ zhist, double* hist) {
-  hdk::pdl_wait();
+  // the element's tile-partial range is static: read before the wait
   hdk::pdl_trigger();
-  if (st->cond == 0) return;
   const size_t n3 = 3 * (size_t)f.n;
+  const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
+  const size_t ii = i < n3 ? i : 0;
+  const int col = static_cast<int>(ii / 3), a = static_cast<int>(ii - 3 * (size_t)col);
+  const int tile = col >> 8;
+  const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
+  hdk::pdl_wait();
+  if (st->cond == 0) return;
   const bool defl = d->use && d->active;
   const int k = defl ? d->k : 0;
   const int it = st->iter + 1;
@@ -1448,16 +1454,12 @@ __global__ void __launch_bounds__(kT) k_dpcg_rz(hdk_factor f, const double* __re
   double acc[kDq];
 #pragma unroll
   for (int q = 0; q < kDq; ++q) acc[q] = 0.0;
-  const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
   if (i < n3) {
     // the loads that do not depend on the fold first, all before the stores
     const double ri = r[i], xi = x[i];
     double awi[kDK];
 #pragma unroll
     for (int c = 0; c < kDK; ++c) awi[c] = c < k ? aw[(size_t)c * n3 + i] : 0.0;
-    const int col = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)col);
-    const int tile = col >> 8;
-    const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
     const size_t base = (size_t)(tile + tb0) * 256 + (col & 255);
     double zi = 0.0;
     for (int b = 0; b <= tb1 - tb0; ++b) zi += __ldg(f.part2 + 3 * (base + 256 * (size_t)b) + a);

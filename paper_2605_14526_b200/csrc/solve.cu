@@ -147,25 +147,37 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // the few long rows as a 4x longer tail).  Fixed lane split and shuffle
 // tree: bitwise reproducible.
 constexpr int kZLong = 3;  // partials per lane held in flight (long rows up to 96 partials per round)
-__device__ __forceinline__ void zfold_task(const hdk_factor& f, int2 task, int column) {
+// A z-fold warp task's rows and partial-slot ranges: static (the factor's
+// layout), so k_zreduce reads them before its PDL wait.
+struct ZRows {
+  int r, stride, s0, s1;
+  bool writer;
+};
+__device__ __forceinline__ ZRows zfold_rows(const hdk_factor& f, int2 task) {
+  const int lane = threadIdx.x & 31;
+  ZRows z;
+  if (task.y < 0) {  // long row: 32 lanes
+    z.r = task.x;
+    z.stride = 32;
+    z.writer = lane == 0;
+  } else {  // short rows: 8 lanes per row
+    z.r = task.x + (lane >> 3);
+    z.stride = 8;
+    z.writer = (lane & 7) == 0 && (lane >> 3) < task.y;
+  }
+  const bool live = task.y < 0 || (lane >> 3) < task.y;
+  z.s0 = live ? __ldg(f.row_pslot + z.r) : 0;
+  z.s1 = live ? __ldg(f.row_pslot + z.r + 1) : 0;
+  return z;
+}
+
+__device__ __forceinline__ void zfold_task(const hdk_factor& f, const ZRows& zr, int column) {
   const int lane = threadIdx.x & 31;
   const double* part1 = f.part1 + (size_t)column * 3 * (size_t)f.n_pslot;
   double* zc = f.z + (size_t)column * 3 * (size_t)f.n;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  int r, stride, s0, s1;
-  bool writer;
-  if (task.y < 0) {  // long row: 32 lanes
-    r = task.x;
-    stride = 32;
-    writer = lane == 0;
-  } else {  // short rows: 8 lanes per row
-    r = task.x + (lane >> 3);
-    stride = 8;
-    writer = (lane & 7) == 0 && (lane >> 3) < task.y;
-  }
-  const bool live = task.y < 0 || (lane >> 3) < task.y;
-  s0 = live ? __ldg(f.row_pslot + r) : 0;
-  s1 = live ? __ldg(f.row_pslot + r + 1) : 0;
+  const int r = zr.r, stride = zr.stride, s0 = zr.s0, s1 = zr.s1;
+  const bool writer = zr.writer;
   const int sub = lane & (stride - 1);
   for (int s = s0 + sub; s < s1; s += kZLong * stride) {
     double v[kZLong][3];
@@ -894,11 +906,13 @@ __global__ void k_to_fp32(const double* __restrict__ sval, const hdk_chunk* __re
 // z-fold: one warp per task.  (Folding z in the row-dot kernel's epilogue
 // behind a grid barrier measured 1-2 us slower than this separate launch.)
 __global__ void __launch_bounds__(256) k_zreduce(hdk_factor f) {
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);  // one task per warp
+  const bool has = t < f.n_ztask;
+  const ZRows zr = zfold_rows(f, has ? __ldg(f.ztask + t) : make_int2(0, 0));
   HDK_TRACED_WAIT(hdk::kTrZfold);
   hdk::pdl_trigger();
   if (f.run_flag && *f.run_flag == 0) return;
-  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (t < f.n_ztask) zfold_task(f, __ldg(f.ztask + t), blockIdx.y);
+  if (has) zfold_task(f, zr, blockIdx.y);
 }
 
 // ---- pass 2 ------------------------------------------------------------------
@@ -1273,13 +1287,17 @@ __global__ void __launch_bounds__(32 * (kWarpsMma2 + 2), 1) k_coltile_mma(hdk_fa
 // column's tile (CTA order), scattered to the full vector.
 template <bool kScatter>
 __global__ void k_xreduce(hdk_factor f, int G, double* __restrict__ out) {
-  hdk::pdl_wait();
+  // the tile's CTA range and the output slot are static: read before the wait
   hdk::pdl_trigger();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= f.n) return;
-  const int t = c / kW, cl = c - t * kW;
-  const int b0 = f.tile_cta2 ? f.tile_cta2[2 * t] : cta_of(f.tile_chunk[t], G, f.n_chunks);
-  const int b1 = f.tile_cta2 ? f.tile_cta2[2 * t + 1] : cta_of(f.tile_chunk[t + 1] - 1, G, f.n_chunks);
+  const bool live = c < f.n;
+  const int cc = live ? c : 0;
+  const int t = cc / kW, cl = cc - t * kW;
+  const int b0 = f.tile_cta2 ? __ldg(f.tile_cta2 + 2 * t) : cta_of(__ldg(f.tile_chunk + t), G, f.n_chunks);
+  const int b1 = f.tile_cta2 ? __ldg(f.tile_cta2 + 2 * t + 1) : cta_of(__ldg(f.tile_chunk + t + 1) - 1, G, f.n_chunks);
+  const int slot = kScatter ? __ldg(f.p2v + cc) : cc;
+  hdk::pdl_wait();
+  if (!live) return;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (int b = b0; b <= b1; ++b) {
     const double* p = f.part2 + 3 * ((size_t)(t + b) * kW + cl);
@@ -1287,7 +1305,7 @@ __global__ void k_xreduce(hdk_factor f, int G, double* __restrict__ out) {
     a1 += p[1];
     a2 += p[2];
   }
-  double* o = kScatter ? out + 3 * (size_t)f.p2v[c] : out + 3 * (size_t)c;
+  double* o = out + 3 * (size_t)slot;
   o[0] = a0;
   o[1] = a1;
   o[2] = a2;
