@@ -352,7 +352,11 @@ HDK_API int hdk_pcg_final(int n, const double* x, const double* z, double* x_ful
 // condition) is the OR over the samples.
 namespace {
 
-constexpr int kSRB = HDK_SEG_RB;
+// blocks per sample of the per-sample CG kernels (<= 32: one lane per block
+// partial in fold_rb): twice the other segmented kernels' HDK_SEG_RB, so a
+// C5 sample's 5,950 rows take ~6 passes per thread instead of ~12
+constexpr int kSRB = 2 * HDK_SEG_RB;
+static_assert(kSRB <= 32, "fold_rb folds one partial per lane");
 
 template <int NQ>
 __device__ __forceinline__ void block_store_rb(const double (&v)[NQ], double* partial) {
