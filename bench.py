@@ -90,13 +90,19 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        """Starts the poller and waits for its first row, so the timed region
+        (as short as ~80 ms for C3) is sampled from its first millisecond."""
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", "0", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                          "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.i0 = len(self.rows)  # rows from here on fall in the timed region
 
     def _read(self):
         for line in self.proc.stdout:
@@ -107,13 +113,16 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        n_in = len(self.rows) - self.i0
+        t0 = time.time()  # a region shorter than the poll interval: the first row at its end
+        while len(self.rows) - self.i0 < 1 and time.time() - t0 < 0.5:
+            time.sleep(0.005)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
-        rows = self.rows
+        rows = self.rows[self.i0:self.i0 + max(n_in, 1)]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
