@@ -1508,12 +1508,14 @@ __global__ void __launch_bounds__(kT) k_dpcg_rz(hdk_factor f, const double* __re
 __global__ void k_dpcg_p(int n, const double* __restrict__ z, double* __restrict__ p, double* __restrict__ pv,
                          const int* __restrict__ p2v, const hdk_pcg* st, const hdk_defl* d,
                          const double* __restrict__ w, cudaGraphConditionalHandle handle, int use_handle) {
-  hdk::pdl_wait();
   hdk::pdl_trigger();
-  if (use_handle && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, st->cond);
-  if (st->cond == 0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const size_t n3 = 3 * (size_t)n;
+  const int row = i / 3;
+  const int vrow = i < (int)n3 ? __ldg(p2v + row) : 0;  // static: before the wait
+  hdk::pdl_wait();
+  if (use_handle && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, st->cond);
+  if (st->cond == 0) return;
   if (i >= (int)n3) return;
   double v = z[i] + st->beta * p[i];
   if (d->use && d->active) {
@@ -1523,8 +1525,7 @@ __global__ void k_dpcg_p(int n, const double* __restrict__ z, double* __restrict
       if (c < k) v -= w[(size_t)c * n3 + i] * d->mu[c];
   }
   p[i] = v;
-  const int row = i / 3;
-  pv[3 * (size_t)__ldg(p2v + row) + (i - 3 * row)] = v;
+  pv[3 * (size_t)vrow + (i - 3 * row)] = v;
 }
 
 // w_c = sum_j coef[c J + j] zhist_j (the Ritz vectors of a recorded solve).
