@@ -11,6 +11,8 @@
 // tile-major stream the solve passes read.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "../../include/hdk.h"
 #include "launch.cuh"
 
@@ -178,13 +180,22 @@ extern "C" {
 HDK_API int hdk_inverse_values(const hdk_inverse_build* b, double* stream, void* stream_handle) {
   if (b->n <= 0) return 0;
   const size_t slot = sizeof(double) * static_cast<size_t>(b->max_depth + 1);
-  int per_block = 8;
-  while (per_block > 1 && per_block * slot > 200 * 1024) per_block /= 2;
-  if (per_block * slot > 220 * 1024) return static_cast<int>(cudaErrorInvalidValue);  // elimination tree too deep
+  if (slot > 220 * 1024) return static_cast<int>(cudaErrorInvalidValue);  // elimination tree too deep
+  // columns per block: the most resident columns per SM (shared memory
+  // bound, at most 32 blocks per SM), ties to the larger block
+  constexpr size_t kSmem = 227 * 1024;
+  int per_block = 1, per_sm = 0;
+  for (int pb = 8; pb >= 1; pb /= 2) {
+    if (pb * slot > 200 * 1024) continue;
+    const int blocks_sm = static_cast<int>(std::min<size_t>(32, kSmem / (pb * slot)));
+    if (pb * blocks_sm > per_sm) {
+      per_sm = pb * blocks_sm;
+      per_block = pb;
+    }
+  }
   const size_t smem = per_block * slot;
   const int blocks = (b->n + per_block - 1) / per_block;
-  // columns resident per SM (shared memory bound): few -> run-ahead walk
-  const int per_sm = per_block * static_cast<int>((227 * 1024) / smem);
+  // few resident columns per SM -> run-ahead walk
   const auto kern = per_sm < 24 ? k_inverse_values : k_inverse_values_plain;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   kern<<<blocks, 32 * per_block, smem, static_cast<cudaStream_t>(stream_handle)>>>(*b, per_block, stream);
