@@ -529,8 +529,11 @@ __global__ void __launch_bounds__(kT) k_spcg_rz(int n3s, const double* __restric
 __global__ void k_spcg_p(int n3s, int n3, const double* __restrict__ z, double* __restrict__ p,
                          double* __restrict__ pv, const int* __restrict__ p2v, const hdk_pcg* st, int count, int* any,
                          cudaGraphConditionalHandle handle, int use_handle) {
-  hdk::pdl_wait();
   hdk::pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = i / 3;
+  const int vrow = i < n3 ? __ldg(p2v + row) : 0;  // static: before the wait
+  hdk::pdl_wait();
   if (blockIdx.x == 0) {
     int on = 0;
     for (int s = threadIdx.x; s < count; s += blockDim.x) on |= (st[s].cond != 0 && st[s].err == 0) ? 1 : 0;
@@ -540,14 +543,12 @@ __global__ void k_spcg_p(int n3s, int n3, const double* __restrict__ z, double* 
       if (use_handle) cudaGraphSetConditional(handle, a);
     }
   }
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n3) return;
   const hdk_pcg& c = st[i / n3s];
   if (c.cond == 0) return;
   const double v = z[i] + c.beta * p[i];
   p[i] = v;
-  const int row = i / 3;
-  pv[3 * (size_t)__ldg(p2v + row) + (i - 3 * row)] = v;
+  pv[3 * (size_t)vrow + (i - 3 * row)] = v;
 }
 
 }  // namespace
@@ -1104,19 +1105,20 @@ __global__ void k_bcg_xr(int n3, double* __restrict__ x, double* __restrict__ r,
 __global__ void __launch_bounds__(kT) k_bcg_zfold(hdk_factor f, size_t part2_stride, const double* __restrict__ r,
                                                   double* __restrict__ z, const double* __restrict__ x, double* partial,
                                                   unsigned int* ticket, hdk_bcg* st) {
-  hdk::pdl_wait();
   hdk::pdl_trigger();
-  if (st->cond == 0) return;
-  const int m = st->m;
   const size_t n3 = 3 * (size_t)f.n;
   const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
+  const size_t ii = i < n3 ? i : 0;  // the tile-partial range is static: before the wait
+  const int col = static_cast<int>(ii / 3), a = static_cast<int>(ii - 3 * (size_t)col);
+  const int tile = col >> 8;
+  const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
+  hdk::pdl_wait();
+  if (st->cond == 0) return;
+  const int m = st->m;
   double acc[kZq];
 #pragma unroll
   for (int k = 0; k < kZq; ++k) acc[k] = 0.0;
   if (i < n3) {
-    const int col = static_cast<int>(i / 3), a = static_cast<int>(i - 3 * (size_t)col);
-    const int tile = col >> 8;
-    const int tb0 = __ldg(f.tile_cta2 + 2 * tile), tb1 = __ldg(f.tile_cta2 + 2 * tile + 1);
     const size_t base = (size_t)(tile + tb0) * 256 + (col & 255);
     // every column's loads before any store: the z stores may alias the
     // solve's partials as far as the compiler knows, so a store between
@@ -1194,8 +1196,10 @@ __global__ void __launch_bounds__(kT) k_bcg_zfold(hdk_factor f, size_t part2_str
 __global__ void k_bcg_p(int n, int nv, const double* __restrict__ z, double* __restrict__ p, double* __restrict__ pv,
                         const int* __restrict__ p2v, const hdk_bcg* st, int* any, const hdk_defl* d,
                         const double* __restrict__ w, cudaGraphConditionalHandle handle, int use_handle) {
-  hdk::pdl_wait();
   hdk::pdl_trigger();
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int vrow0 = i0 < 3 * n ? __ldg(p2v + i0 / 3) : 0;  // static: before the wait
+  hdk::pdl_wait();
   const int on = st->cond != 0 && st->err == 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *any = on;
@@ -1211,7 +1215,7 @@ __global__ void k_bcg_p(int n, int nv, const double* __restrict__ z, double* __r
 #pragma unroll
   for (int j = 0; j < kBC; ++j) old[j] = (!first && j < m) ? p[j * n3 + i] : 0.0;
   const int row = i / 3;
-  const size_t vtx = 3 * (size_t)__ldg(p2v + row) + (i - 3 * row);
+  const size_t vtx = 3 * (size_t)vrow0 + (i - 3 * row);
   const bool defl = d && d->cols && d->use && d->active;  // P -= W E^{-1} (AW)^T Z
   const int kd = defl ? d->k : 0;
   double wv[kBC];
